@@ -1,0 +1,196 @@
+/*
+ * dbx.h — C-ABI of the B200-native anti-reflective (AR) deblurring hot path.
+ *
+ * The reference (`deblur`, a header-only C++20 library under
+ * /root/reference/proj/include/deblur) exposes this path as value-semantics
+ * C++ functions over Eigen row-major double matrices.  This C-ABI is the
+ * drop-in boundary for that path: plain pointers and sizes, opaque plan
+ * handles, status codes instead of exceptions.  include/deblur_b200.hpp
+ * re-creates the reference's C++ names on top of it.
+ *
+ * Conventions (all entry points):
+ *   - arrays are FP64, row-major, ld = n2 (reference core.hpp:17-19: vec(X)
+ *     is the row-major buffer); batched arrays are image-major with stride
+ *     n1*n2;
+ *   - every array pointer may be HOST or DEVICE memory (detected with
+ *     cudaPointerGetAttributes); host arrays are staged through the plan's
+ *     device buffers, device arrays are used in place;
+ *   - status: DBX_OK = 0, DBX_EINVAL = 1 (reference std::invalid_argument,
+ *     core.hpp:26-28), DBX_EDIVERGED = 2 (reference SolverDivergence,
+ *     solver.hpp:42-44), DBX_ECUDA = 3 (device/driver error or missing
+ *     sm_100a device: there is no CPU fallback);
+ *   - dbx_last_error() returns the thread-local message of the last failure
+ *     (the reference exception's what()).
+ *   - one plan per stream; plans are independent and there is no global lock
+ *     (replaces the reference's process-wide FFTW mutex, transforms.hpp:21-26).
+ */
+#ifndef DBX_H_
+#define DBX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DBX_OK 0
+#define DBX_EINVAL 1
+#define DBX_EDIVERGED 2
+#define DBX_ECUDA 3
+
+/* boundary.hpp:9 BoundaryCondition order {Zero, Periodic, Reflective, AntiReflective};
+ * this path implements AntiReflective only. */
+#define DBX_BC_ANTIREFLECTIVE 3
+
+/* transforms.hpp:17 TransformKind order {Dft, CosineIII, SineI, AntiReflective,
+ * AntiReflectiveInverse}; the AR path needs the last three. */
+#define DBX_KIND_SINEI 2
+#define DBX_KIND_AR 3
+#define DBX_KIND_ARINV 4
+
+/* solver.hpp:17-32 StoppingRule::Kind order {FixedIterations, MinRre,
+ * RelativeResidualBelow}. */
+#define DBX_STOP_FIXED 0
+#define DBX_STOP_MINRRE 1
+#define DBX_STOP_RESIDUAL 2
+
+/* Blur-apply engine selection (dbx_plan_set_conv). AUTO mirrors the
+ * reference's direct/FFT cutover at q = 7 (blur.hpp:70, 79-81). */
+#define DBX_CONV_AUTO 0
+#define DBX_CONV_DIRECT 1
+#define DBX_CONV_FFT 2
+
+typedef struct dbx_plan dbx_plan;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* dbx_last_error(void);
+
+/* Library version string, e.g. "dbx 0.1 sm_100a". */
+const char* dbx_version(void);
+
+/* Number of usable sm_100 devices (0 when none: every compute call then fails
+ * with DBX_ECUDA — there is no CPU fallback). */
+int dbx_device_count(void);
+
+/*
+ * Creates a plan for `batch` images of n1 x n2 pixels blurred by the
+ * (2q1+1) x (2q2+1) mask `taps` (row-major, centre (q1,q2), host memory).
+ * Replaces the construction of BlurOperator(Psf(taps), bc, n1, n2)
+ * (reference blur.hpp:17-34) including Psf validation (psf.hpp:15-25: odd
+ * dims, finite, >= 0, |sum-1| <= 1e-12) and check_support (boundary.hpp:66-81:
+ * q <= n-2 on every axis with q > 0).  `device` selects the CUDA device.
+ */
+int dbx_plan_create(int n1, int n2, int batch, const double* taps, int q1, int q2, int bc,
+                    int device, dbx_plan** out);
+void dbx_plan_destroy(dbx_plan* plan);
+
+/* cudaStream_t of the plan (as void*), for callers that time with CUDA events. */
+void* dbx_plan_stream(dbx_plan* plan);
+
+/* Blur engine override (DBX_CONV_*); default DBX_CONV_AUTO. */
+int dbx_plan_set_conv(dbx_plan* plan, int conv);
+
+/*
+ * y = A x (adjoint = 0) or y = A' x (adjoint = 1), for every image of the
+ * batch.  Replaces apply (blur.hpp:75-83) and apply_reblur_adjoint
+ * (blur.hpp:87-90): AR extension computed on the fly, no padded image.
+ */
+int dbx_blur_apply(dbx_plan* plan, const double* x, double* y, int adjoint);
+
+/*
+ * Builds D = T diag(d) T~ with d = 1/(lambda^2 + alpha), lambda the AR
+ * eigenvalue grid of the SYMMETRISED mask.  Replaces build_tikhonov with
+ * PreconditionerSpec{AntiReflective, alpha} (preconditioner.hpp:62-85) =
+ * symmetrize (psf.hpp:71-85) + eig_antireflective (spectral.hpp:120-133) +
+ * tikhonov_filter (preconditioner.hpp:37-57).  Errors like the reference:
+ * alpha < 0, or alpha == 0 with a zero eigenvalue -> DBX_EINVAL.
+ */
+int dbx_precond_build(dbx_plan* plan, double alpha);
+
+/* Copies the filter grid d (n1 x n2) to `d_out` (FilteredOperator::sop.eigs). */
+int dbx_precond_eigs(dbx_plan* plan, double* d_out);
+
+/* Replaces the filter grid with a caller-supplied one (SpectralOperator with
+ * explicit eigs, spectral.hpp:32-39) — used for identity / constant filters. */
+int dbx_precond_set_eigs(dbx_plan* plan, const double* d);
+
+/* y = D r = T (d o (T~ r)) for every image.  Replaces precondition_apply
+ * (preconditioner.hpp:88-90) -> filter_apply AR branch (spectral.hpp:161-165). */
+int dbx_precond_apply(dbx_plan* plan, const double* r, double* y);
+
+/* 2D separable transform (columns then rows, transforms.hpp:179-192) of
+ * kind DBX_KIND_{SINEI,AR,ARINV}; replaces tensor_apply (transforms.hpp:198-226). */
+int dbx_tensor_apply(dbx_plan* plan, int kind, const double* x, double* y);
+
+/*
+ * Runs (preconditioned) Landweber for every image of the batch:
+ *   x_0 = 0, x_k = x_{k-1} + tau * [D] A'(g - A x_{k-1}),
+ * with the reference's bookkeeping (solver.hpp:63-132): residual_history[k-1]
+ * = ||g - A x_k||, rre_history[k-1] = ||x_k - f||/||f|| (when f_true != NULL),
+ * best_iteration by strict '<' (first minimum, 1-based), divergence guard
+ * ||x_k|| > 1e8 ||g|| (-> DBX_EDIVERGED; the first diverging image index is
+ * reported by dbx_last_error), RelativeResidualBelow breaking after recording,
+ * restored = best iterate under MinRre with tracking, else the last iterate.
+ * Replaces landweber (use_precond = 0) and d_landweber (use_precond = 1,
+ * after dbx_precond_build) (solver.hpp:139-148).
+ *
+ *   g, f_true        [batch][n1][n2]   (f_true nullable: no RRE tracking)
+ *   restored         [batch][n1][n2]
+ *   rre_hist         [batch][H] with H = total iterations (nullable)
+ *   res_hist         [batch][H]        (nullable)
+ *   best_iter, iters_done  [batch]     (nullable, host memory)
+ *   x_hist           [batch][H][n1][n2] every iterate (nullable; parity tests)
+ *
+ * H = fixed_iters for DBX_STOP_FIXED, else max_iters.
+ */
+int dbx_landweber_run(dbx_plan* plan, const double* g, const double* f_true, double tau,
+                      int max_iters, int stop_kind, int fixed_iters, double resid_eps,
+                      int use_precond, double* restored, double* rre_hist, double* res_hist,
+                      int* best_iter, int* iters_done, double* x_hist);
+
+/*
+ * Per-kernel-class device time (ms) and launch counts of the most recent
+ * dbx_landweber_run made with timing enabled (dbx_plan_set_timing(plan, 1)):
+ * classes 0 = blur A' (+fused epilogue), 1 = blur A (+residual), 2 = AR
+ * transform passes, 3 = finalize/reductions.  Returns the number of classes.
+ */
+int dbx_plan_set_timing(dbx_plan* plan, int enable);
+int dbx_plan_kernel_times(dbx_plan* plan, double* ms, int* launches, int max_classes);
+
+/* Total kernels launched by this plan since creation (launch accounting). */
+int64_t dbx_plan_launch_count(dbx_plan* plan);
+
+/* ---- input generation (host side, shared by the GPU harness and the oracle
+ * tests) ---- */
+
+/* Seeded scene: `nshapes` random ellipses / rectangles with U[0,1] intensities
+ * on 0 (+ amp * smooth sinusoid when amp != 0), rows x cols, row-major. */
+int dbx_gen_scene(int rows, int cols, int nshapes, double sinus_amp, uint64_t seed, double* out);
+
+/* Gaussian mask: sigma (row, col), rotated by theta_deg (counter-clockwise,
+ * columns to the right, rows down), centre offset (o1 rows, o2 cols),
+ * normalised to sum 1 (generalises gaussian_portion_psf, psf.hpp:126-138). */
+int dbx_gen_psf_gaussian(int q1, int q2, double sigma1, double sigma2, double theta_deg,
+                         double off1, double off2, double* taps);
+
+/* Motion mask: line of `length` px at `angle_deg` plus a one-sided exponential
+ * tail of decay length `tail` px, rasterised by bilinear splatting, sum 1. */
+int dbx_gen_psf_motion(int q1, int q2, double length, double angle_deg, double tail,
+                       double* taps);
+
+/* Honest data generation (experiment.hpp:71-99): centred crop offsets, direct
+ * correlation of the scene (canvas rows x cols) with the mask, crop to
+ * n1 x n2, then add_noise (image.hpp:72-82: mt19937_64 + Box-Muller, rescaled
+ * to ||eta|| = level ||g|| exactly).  Threads: host threads used (0 = all). */
+int dbx_gen_honest(const double* scene, int rows, int cols, const double* taps, int q1, int q2,
+                   int n1, int n2, double noise_level, uint64_t noise_seed, int threads,
+                   double* f_true, double* g);
+
+/* add_noise alone (image.hpp:72-82). */
+int dbx_add_noise(const double* g, int n1, int n2, double level, uint64_t seed, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DBX_H_ */

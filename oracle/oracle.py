@@ -1,0 +1,215 @@
+"""CPU ORACLE wrapper (TEST INFRASTRUCTURE ONLY).
+
+ctypes bindings over ``oracle/build/liborc.so`` (built from
+``oracle/deblur_oracle.cpp`` by ``oracle/Makefile``), the scalar C++
+restatement of the reference ``deblur`` library's anti-reflective
+preconditioned-Landweber path.  Only ``tests/``, ``__graft_entry__.smoke()``
+and ``bench.py``'s cpu_baseline / ``--impl reference`` legs may import this
+module — it is the checker, never the product.
+
+Function names mirror the reference API (file:line in the C++ source).
+Errors map like the reference: invalid arguments raise ``ValueError``
+(std::invalid_argument), divergence raises ``OracleDivergence``
+(SolverDivergence, solver.hpp:42-44).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "build", "liborc.so")
+_lib = None
+
+STOP_FIXED, STOP_MINRRE, STOP_RESID = 0, 1, 2
+KIND_SINEI, KIND_AR, KIND_ARINV = 2, 3, 4
+
+
+class OracleDivergence(RuntimeError):
+    pass
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        _lib = C.CDLL(_LIB_PATH)
+        _lib.orc_last_error.restype = C.c_char_p
+        _lib.orc_rre.restype = C.c_double
+        _lib.orc_rre.argtypes = [C.c_void_p, C.c_void_p, C.c_long]
+        _lib.orc_add_noise.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_void_p]
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _check(st: int):
+    if st == 0:
+        return
+    msg = lib().orc_last_error().decode()
+    if st == 1:
+        raise ValueError(msg)
+    raise OracleDivergence(msg)
+
+
+def _q(taps):
+    taps = _f64(taps)
+    if taps.ndim != 2 or taps.shape[0] % 2 == 0 or taps.shape[1] % 2 == 0:
+        raise ValueError("Psf: taps must have odd dimensions")
+    return taps, (taps.shape[0] - 1) // 2, (taps.shape[1] - 1) // 2
+
+
+def fft(x, sign=-1):
+    z = np.ascontiguousarray(x, dtype=np.complex128).copy()
+    _check(lib().orc_fft(_p(z), C.c_int(z.size), C.c_int(sign)))
+    return z
+
+
+def symmetrize(taps):
+    taps, q1, q2 = _q(taps)
+    out = np.empty_like(taps)
+    _check(lib().orc_symmetrize(_p(taps), q1, q2, _p(out)))
+    return out
+
+
+def rotate180(taps):
+    return np.ascontiguousarray(_f64(taps)[::-1, ::-1])
+
+
+def pad_ar(f, q1, q2):
+    f = _f64(f)
+    out = np.empty((f.shape[0] + 2 * q1, f.shape[1] + 2 * q2))
+    _check(lib().orc_pad_ar(_p(f), f.shape[0], f.shape[1], q1, q2, _p(out)))
+    return out
+
+
+def apply(taps, f, adjoint=False, path=0):
+    """blur.hpp:75-83 (adjoint=True: apply_reblur_adjoint, blur.hpp:87-90)."""
+    taps, q1, q2 = _q(taps)
+    f = _f64(f)
+    out = np.empty_like(f)
+    _check(lib().orc_apply(_p(taps), q1, q2, _p(f), f.shape[0], f.shape[1], int(adjoint), int(path), _p(out)))
+    return out
+
+
+def sine1_forward(v):
+    v = _f64(v)
+    y = np.empty_like(v)
+    _check(lib().orc_sine1(_p(v), v.size, _p(y)))
+    return y
+
+
+def ar_forward(v):
+    v = _f64(v)
+    y = np.empty_like(v)
+    _check(lib().orc_ar_1d(0, _p(v), v.size, _p(y)))
+    return y
+
+
+def ar_inverse(v):
+    v = _f64(v)
+    y = np.empty_like(v)
+    _check(lib().orc_ar_1d(1, _p(v), v.size, _p(y)))
+    return y
+
+
+def make_ar_transform(m):
+    alpha = C.c_double()
+    p = np.empty(max(m - 2, 0))
+    _check(lib().orc_ar_alpha(m, C.byref(alpha), _p(p)))
+    return alpha.value, p
+
+
+def tensor_apply(kind, x):
+    x = _f64(x)
+    y = np.empty_like(x)
+    _check(lib().orc_tensor_apply(kind, _p(x), x.shape[0], x.shape[1], _p(y)))
+    return y
+
+
+def eig_antireflective(taps, n1, n2):
+    taps, q1, q2 = _q(taps)
+    e = np.empty((n1, n2))
+    _check(lib().orc_eig_antireflective(_p(taps), q1, q2, n1, n2, _p(e)))
+    return e
+
+
+def tikhonov_filter(eigs, alpha):
+    eigs = _f64(eigs)
+    d = np.empty_like(eigs)
+    _check(lib().orc_tikhonov_filter(_p(eigs), eigs.shape[0], eigs.shape[1], C.c_double(alpha), _p(d)))
+    return d
+
+
+def build_tikhonov(taps, alpha, n1, n2):
+    taps, q1, q2 = _q(taps)
+    d = np.empty((n1, n2))
+    _check(lib().orc_build_tikhonov(_p(taps), q1, q2, n1, n2, C.c_double(alpha), _p(d)))
+    return d
+
+
+def precondition_apply(d, r):
+    d, r = _f64(d), _f64(r)
+    y = np.empty_like(r)
+    _check(lib().orc_precondition_apply(_p(d), _p(r), r.shape[0], r.shape[1], _p(y)))
+    return y
+
+
+def add_noise(g, level, seed):
+    g = _f64(g)
+    out = np.empty_like(g)
+    _check(lib().orc_add_noise(_p(g), g.shape[0], g.shape[1], level, seed, _p(out)))
+    return out
+
+
+def rre(x, f):
+    x, f = _f64(x), _f64(f)
+    return lib().orc_rre(_p(x), _p(f), x.size)
+
+
+def landweber(taps, g, d=None, f_true=None, tau=1.0, max_iters=100, stop=STOP_MINRRE,
+              fixed_iters=0, resid_eps=0.0, conv_path=0, keep_iterates=False):
+    """solver.hpp:63-148.  Returns a dict shaped like RestorationRun."""
+    taps, q1, q2 = _q(taps)
+    g = _f64(g)
+    n1, n2 = g.shape
+    total = fixed_iters if stop == STOP_FIXED else max_iters
+    hist = max(total, 1)
+    restored = np.empty_like(g)
+    rre_h = np.zeros(hist)
+    res_h = np.zeros(hist)
+    best = C.c_int()
+    done = C.c_int()
+    xh = np.empty((hist, n1, n2)) if keep_iterates else None
+    dd = _f64(d) if d is not None else None
+    ft = _f64(f_true) if f_true is not None else None
+    st = lib().orc_landweber(
+        _p(taps), q1, q2, n1, n2, _p(dd) if dd is not None else None, _p(g),
+        _p(ft) if ft is not None else None, C.c_double(tau), max_iters, stop, fixed_iters,
+        C.c_double(resid_eps), conv_path, _p(restored), _p(rre_h), _p(res_h), C.byref(best),
+        C.byref(done), _p(xh) if xh is not None else None)
+    _check(st)
+    k = done.value
+    return {
+        "restored": restored,
+        "iterations_executed": k,
+        "best_iteration": best.value,
+        "rre_history": rre_h[:k].copy() if ft is not None else np.zeros(0),
+        "residual_history": res_h[:k].copy(),
+        "iterates": xh[:k] if xh is not None else None,
+    }

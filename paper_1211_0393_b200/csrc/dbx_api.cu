@@ -1,0 +1,741 @@
+// dbx_api.cu — host side of the C-ABI (include/dbx.h): plan lifetime, argument
+// validation with the reference's error semantics, host/device staging, the
+// dense AR transform matrices, and the Landweber driver (captured as one CUDA
+// graph per run shape).  No CPU compute path exists: every numerical result is
+// produced by the sm_100a kernels in blur.cu / gemm.cu / solver_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dbx.h"
+#include "dbx_internal.h"
+
+using namespace dbx;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct InvalidArg : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Diverged : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// core.hpp:26-28 detail::require
+inline void require(bool c, const std::string& what) {
+  if (!c) throw InvalidArg(what);
+}
+
+inline void ck(cudaError_t e, const char* where) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw CudaErr(std::string(where) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return DBX_OK;
+  } catch (const InvalidArg& e) {
+    g_err = e.what();
+    return DBX_EINVAL;
+  } catch (const Diverged& e) {
+    g_err = e.what();
+    return DBX_EDIVERGED;
+  } catch (const CudaErr& e) {
+    g_err = e.what();
+    return DBX_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DBX_ECUDA;
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+struct DevBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)), "cudaMalloc");
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// Dense T~_n, T_n, Q_n with integer-reduced sine arguments:
+// Q_m(s,t) = sqrt(2/(m+1)) sin(pi ((s t) mod 2(m+1)) / (m+1)), long double.
+std::vector<long double> sine_table(long m) {
+  const long N2 = 2 * (m + 1);
+  std::vector<long double> tab((size_t)N2);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (long e = 0; e < N2; ++e) tab[(size_t)e] = sinl(pi * (long double)e / (long double)(m + 1));
+  return tab;
+}
+
+// Q_m as an m x m matrix (1-based s,t), long double entries.
+void fill_q(long m, std::vector<long double>& q) {
+  const auto tab = sine_table(m);
+  const long N2 = 2 * (m + 1);
+  const long double sc = sqrtl(2.0L / (long double)(m + 1));
+  q.assign((size_t)(m * m), 0.0L);
+  for (long s = 1; s <= m; ++s)
+    for (long t = 1; t <= m; ++t) q[(size_t)((s - 1) * m + (t - 1))] = sc * tab[(size_t)((s * t) % N2)];
+}
+
+// transforms.hpp:135-144 (p and alpha exactly as the reference computes them)
+void ar_params(long n, std::vector<double>& p, double& alpha) {
+  p.assign((size_t)(n - 2), 0.0);
+  double sq = 0.0;
+  for (long j = 1; j <= n - 2; ++j) p[(size_t)(j - 1)] = 1.0 - (double)j / (double)(n - 1);
+  for (double v : p) sq += v * v;
+  alpha = std::sqrt(1.0 + sq);
+}
+
+// kind: DBX_KIND_SINEI -> Q_n ; DBX_KIND_AR -> T_n ; DBX_KIND_ARINV -> T~_n
+std::vector<double> dense_transform(int kind, long n) {
+  std::vector<double> M((size_t)(n * n), 0.0);
+  if (kind == DBX_KIND_SINEI) {
+    std::vector<long double> q;
+    fill_q(n, q);
+    for (size_t i = 0; i < q.size(); ++i) M[i] = (double)q[i];
+    return M;
+  }
+  const long m = n - 2;
+  std::vector<long double> q;
+  fill_q(m, q);
+  std::vector<double> p;
+  double alpha;
+  ar_params(n, p, alpha);
+  for (long s = 0; s < m; ++s)
+    for (long t = 0; t < m; ++t) M[(size_t)((s + 1) * n + (t + 1))] = (double)q[(size_t)(s * m + t)];
+  if (kind == DBX_KIND_AR) {
+    // dense_ar_forward block form: first/last columns = normalised ramps
+    const double inv_a = 1.0 / alpha;
+    M[0] = inv_a;
+    M[(size_t)(n * n - 1)] = inv_a;
+    for (long j = 0; j < m; ++j) {
+      M[(size_t)((1 + j) * n)] = inv_a * p[(size_t)j];
+      M[(size_t)((1 + j) * n + (n - 1))] = inv_a * p[(size_t)(m - 1 - j)];
+    }
+  } else {
+    // dense_ar_inverse block form: [alpha 0 0; -Qp Q -QJp; 0 0 alpha]
+    M[0] = alpha;
+    M[(size_t)(n * n - 1)] = alpha;
+    for (long s = 0; s < m; ++s) {
+      long double qp = 0.0L, qjp = 0.0L;
+      for (long t = 0; t < m; ++t) {
+        qp += q[(size_t)(s * m + t)] * (long double)p[(size_t)t];
+        qjp += q[(size_t)(s * m + t)] * (long double)p[(size_t)(m - 1 - t)];
+      }
+      M[(size_t)((1 + s) * n)] = -(double)qp;
+      M[(size_t)((1 + s) * n + (n - 1))] = -(double)qjp;
+    }
+  }
+  return M;
+}
+
+std::vector<double> transpose(const std::vector<double>& a, long n) {
+  std::vector<double> t(a.size());
+  for (long i = 0; i < n; ++i)
+    for (long j = 0; j < n; ++j) t[(size_t)(j * n + i)] = a[(size_t)(i * n + j)];
+  return t;
+}
+
+enum KClass { KC_BLUR_ADJ = 0, KC_BLUR = 1, KC_TRANSFORM = 2, KC_FINALIZE = 3, KC_NUM = 4 };
+
+}  // namespace
+
+struct dbx_plan {
+  int n1 = 0, n2 = 0, batch = 0, q1 = 0, q2 = 0, device = 0;
+  size_t N = 0;
+  std::vector<double> taps;
+  cudaStream_t stream = nullptr;
+  double* w_A = nullptr;   // weights of A (rotate180 of taps)
+  double* w_At = nullptr;  // weights of A' (taps)
+  double* sym = nullptr;   // symmetrised taps (psf.hpp:71-85)
+  double* d = nullptr;     // filter grid
+  bool have_d = false;
+  int conv = DBX_CONV_AUTO;
+  // dense transform matrices [kind][0 col-matrix (n1), 1 row-matrix^T (n2)]
+  double* mats[5][2] = {};
+  DevBuf g, f, r, s, u, X3, in, out, part, rre, res, xh;
+  ImgState* st = nullptr;
+  int part_cap = 0;
+  int64_t launches = 0;
+  bool timing = false;
+  double kms[KC_NUM] = {};
+  int kcount[KC_NUM] = {};
+  std::vector<cudaEvent_t> evpool;
+  size_t evused = 0;
+  std::vector<std::pair<int, size_t>> evrecs;
+  // graph cache
+  cudaGraphExec_t gexec = nullptr;
+  std::string gkey;
+
+  ~dbx_plan() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    for (auto e : evpool) cudaEventDestroy(e);
+    for (auto& km : mats)
+      for (auto p : km)
+        if (p) cudaFree(p);
+    for (double* p : {w_A, w_At, sym, d})
+      if (p) cudaFree(p);
+    if (st) cudaFree(st);
+    for (DevBuf* b : {&g, &f, &r, &s, &u, &X3, &in, &out, &part, &rre, &res, &xh}) b->release();
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void set_dev() const { ck(cudaSetDevice(device), "cudaSetDevice"); }
+
+  double* upload(const std::vector<double>& h) {
+    double* p = nullptr;
+    ck(cudaMalloc(&p, h.size() * sizeof(double)), "cudaMalloc");
+    ck(cudaMemcpy(p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice), "upload");
+    return p;
+  }
+
+  double* matrix(int kind, int which) {
+    if (!mats[kind][which]) {
+      const long n = which == 0 ? n1 : n2;
+      auto M = dense_transform(kind, n);
+      if (which == 1) M = transpose(M, n);
+      mats[kind][which] = upload(M);
+    }
+    return mats[kind][which];
+  }
+
+  // ---- launch bookkeeping (optional per-class CUDA-event timing) ----
+  void ev_begin(int cls) {
+    ++launches;
+    if (!timing) return;
+    if (evused + 2 > evpool.size()) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        evpool.push_back(e);
+      }
+    }
+    ck(cudaEventRecord(evpool[evused], stream), "cudaEventRecord");
+    evrecs.push_back({cls, evused});
+    evused += 2;
+  }
+  void ev_end() {
+    if (!timing) return;
+    ck(cudaEventRecord(evpool[evrecs.back().second + 1], stream), "cudaEventRecord");
+  }
+  void ev_collect() {
+    if (!timing) return;
+    ck(cudaStreamSynchronize(stream), "sync");
+    for (int i = 0; i < KC_NUM; ++i) kms[i] = 0.0, kcount[i] = 0;
+    for (auto& rc : evrecs) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, evpool[rc.second], evpool[rc.second + 1]), "elapsed");
+      kms[rc.first] += ms;
+      kcount[rc.first] += 1;
+    }
+    evrecs.clear();
+    evused = 0;
+  }
+
+  void check_launch() { ck(cudaGetLastError(), "kernel launch"); }
+
+  int blur(const double* x, int xsel, double* y, int ysel, bool adjoint, int mode,
+           const double* gg, const double* xold, int xoldsel, const double* ff, double tau,
+           const ImgState* stp, Partials pt, int cls) {
+    BlurArgs a{};
+    a.x = x; a.xsel = xsel; a.y = y; a.ysel = ysel;
+    a.w = adjoint ? w_At : w_A;
+    a.n1 = n1; a.n2 = n2; a.q1 = q1; a.q2 = q2; a.batch = batch;
+    a.mode = mode; a.g = gg; a.xold = xold; a.xoldsel = xoldsel; a.f = ff; a.tau = tau;
+    a.st = stp; a.part = pt;
+    int ctas = 0;
+    ev_begin(cls);
+    launch_blur(a, stream, &ctas);
+    ev_end();
+    check_launch();
+    return ctas;
+  }
+
+  // one tensor_map half-pass: col (C = M1 X) or row (C = X M2^T)
+  int pass(int kind, bool col, const double* X, int xsel, double* C, int csel, int epi,
+           const double* xold, int xoldsel, const double* ff, double tau, const ImgState* stp,
+           Partials pt) {
+    GemmArgs a{};
+    const long long NN = (long long)N;
+    if (col) {
+      a.A = matrix(kind, 0); a.sA = 0; a.asel = SEL_EXPLICIT;
+      a.B = X; a.sB = NN; a.bsel = xsel;
+      a.M = n1; a.K = n1; a.N = n2;
+    } else {
+      a.A = X; a.sA = NN; a.asel = xsel;
+      a.B = matrix(kind, 1); a.sB = 0; a.bsel = SEL_EXPLICIT;
+      a.M = n1; a.K = n2; a.N = n2;
+    }
+    a.C = C; a.sC = NN; a.csel = csel;
+    a.batch = batch; a.epi = epi; a.d = d; a.xold = xold; a.xoldsel = xoldsel; a.f = ff;
+    a.tau = tau; a.st = stp; a.part = pt; a.img_elems = N;
+    int ctas = 0;
+    ev_begin(KC_TRANSFORM);
+    launch_gemm(a, stream, &ctas);
+    ev_end();
+    check_launch();
+    return ctas;
+  }
+};
+
+namespace {
+
+void validate_taps(const double* taps, int q1, int q2) {
+  require(taps != nullptr, "Psf: null taps");
+  require(q1 >= 0 && q2 >= 0, "Psf: taps must have odd dimensions");
+  const size_t n = (size_t)(2 * q1 + 1) * (2 * q2 + 1);
+  double s = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    require(std::isfinite(taps[i]), "Psf: taps must be finite");
+    require(taps[i] >= 0.0, "Psf: taps must be nonnegative");
+    s += taps[i];
+  }
+  require(std::abs(s - 1.0) <= 1e-12, "Psf: taps must sum to 1 (within 1e-12)");
+}
+
+// Stage a caller array into the plan (device pointers are used in place).
+const double* stage_in(dbx_plan* P, const double* x, DevBuf& buf, size_t count) {
+  if (is_device_ptr(x)) return x;
+  buf.ensure(count);
+  ck(cudaMemcpyAsync(buf.p, x, count * sizeof(double), cudaMemcpyHostToDevice, P->stream), "H2D");
+  return buf.p;
+}
+
+void stage_out(dbx_plan* P, double* dst, const double* src, size_t count) {
+  if (dst == src) return;
+  ck(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDefault, P->stream), "D2H");
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+const char* dbx_last_error(void) { return g_err.c_str(); }
+
+const char* dbx_version(void) { return "dbx 0.1 sm_100a (FP64 AR stencil + dense AR transform)"; }
+
+int dbx_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int ok = 0;
+  for (int i = 0; i < n; ++i) {
+    cudaDeviceProp pr;
+    if (cudaGetDeviceProperties(&pr, i) == cudaSuccess && pr.major == 10) ++ok;
+  }
+  return ok;
+}
+
+int dbx_plan_create(int n1, int n2, int batch, const double* taps, int q1, int q2, int bc,
+                    int device, dbx_plan** out) {
+  return guarded([&] {
+    require(out != nullptr, "dbx_plan_create: null out");
+    *out = nullptr;
+    require(bc == DBX_BC_ANTIREFLECTIVE, "dbx_plan_create: only AntiReflective BCs are implemented");
+    validate_taps(taps, q1, q2);
+    // blur.hpp:26-29 + boundary.hpp:66-81 (AR branch)
+    require(n1 >= 1 && n2 >= 1, "BlurOperator: empty field of view");
+    require((q1 == 0 || q1 <= n1 - 2) && (q2 == 0 || q2 <= n2 - 2),
+            "anti-reflective support condition violated (q > n-2)");
+    require(batch >= 1, "dbx_plan_create: batch must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw CudaErr("no CUDA device: the B200 path has no CPU fallback");
+    }
+    require(device >= 0 && device < ndev, "dbx_plan_create: bad device index");
+    cudaDeviceProp pr;
+    ck(cudaGetDeviceProperties(&pr, device), "cudaGetDeviceProperties");
+    if (pr.major != 10) throw CudaErr("device is not sm_100 (Blackwell B200)");
+    auto P = std::make_unique<dbx_plan>();
+    P->n1 = n1; P->n2 = n2; P->batch = batch; P->q1 = q1; P->q2 = q2; P->device = device;
+    P->N = (size_t)n1 * n2;
+    const size_t nt = (size_t)(2 * q1 + 1) * (2 * q2 + 1);
+    P->taps.assign(taps, taps + nt);
+    P->set_dev();
+    ck(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    // weights for the correlation form y = sum_t,u w(t,u) P(r-q1+t, c-q2+u):
+    // A uses the 180-rotated taps, A' (rotate180 mask, psf.hpp:88-91) the taps.
+    std::vector<double> rot(P->taps.rbegin(), P->taps.rend());
+    P->w_A = P->upload(rot);
+    P->w_At = P->upload(P->taps);
+    // symmetrize (psf.hpp:71-85): one orbit average written to four cells
+    std::vector<double> s(nt);
+    const int W = 2 * q2 + 1;
+    auto tp = [&](int i1, int i2) { return P->taps[(size_t)((q1 + i1) * W + (q2 + i2))]; };
+    for (int i1 = 0; i1 <= q1; ++i1)
+      for (int i2 = 0; i2 <= q2; ++i2) {
+        const double avg = (tp(-i1, -i2) + tp(-i1, i2) + tp(i1, -i2) + tp(i1, i2)) / 4.0;
+        s[(size_t)((q1 + i1) * W + q2 + i2)] = avg;
+        s[(size_t)((q1 - i1) * W + q2 + i2)] = avg;
+        s[(size_t)((q1 + i1) * W + q2 - i2)] = avg;
+        s[(size_t)((q1 - i1) * W + q2 - i2)] = avg;
+      }
+    P->sym = P->upload(s);
+    ck(cudaMalloc(&P->st, sizeof(ImgState) * (size_t)batch), "cudaMalloc");
+    // partial-sum capacity = CTAs per image of the finest launch grid (blur)
+    P->part_cap = ((n2 + 63) / 64) * ((n1 + 31) / 32);
+    *out = P.release();
+  });
+}
+
+void dbx_plan_destroy(dbx_plan* plan) {
+  if (!plan) return;
+  cudaSetDevice(plan->device);
+  cudaStreamSynchronize(plan->stream);
+  delete plan;
+}
+
+void* dbx_plan_stream(dbx_plan* plan) { return plan ? (void*)plan->stream : nullptr; }
+
+int dbx_plan_set_conv(dbx_plan* plan, int conv) {
+  return guarded([&] {
+    require(plan != nullptr, "null plan");
+    require(conv == DBX_CONV_AUTO || conv == DBX_CONV_DIRECT || conv == DBX_CONV_FFT,
+            "dbx_plan_set_conv: unknown engine");
+    plan->conv = conv;
+  });
+}
+
+int dbx_plan_set_timing(dbx_plan* plan, int enable) {
+  return guarded([&] {
+    require(plan != nullptr, "null plan");
+    plan->timing = enable != 0;
+  });
+}
+
+int dbx_plan_kernel_times(dbx_plan* plan, double* ms, int* launches, int max_classes) {
+  if (!plan) return 0;
+  const int n = std::min(max_classes, (int)KC_NUM);
+  for (int i = 0; i < n; ++i) {
+    if (ms) ms[i] = plan->kms[i];
+    if (launches) launches[i] = plan->kcount[i];
+  }
+  return KC_NUM;
+}
+
+int64_t dbx_plan_launch_count(dbx_plan* plan) { return plan ? plan->launches : 0; }
+
+int dbx_blur_apply(dbx_plan* P, const double* x, double* y, int adjoint) {
+  return guarded([&] {
+    require(P && x && y, "apply: null argument");
+    P->set_dev();
+    const size_t cnt = P->N * P->batch;
+    const double* xin = stage_in(P, x, P->in, cnt);
+    double* yout = y;
+    if (!is_device_ptr(y)) {
+      P->out.ensure(cnt);
+      yout = P->out.p;
+    }
+    P->blur(xin, SEL_EXPLICIT, yout, SEL_EXPLICIT, adjoint != 0, BLUR_STORE, nullptr, nullptr,
+            SEL_EXPLICIT, nullptr, 0.0, nullptr, Partials{nullptr, 0}, adjoint ? KC_BLUR_ADJ : KC_BLUR);
+    stage_out(P, y, yout, cnt);
+    ck(cudaStreamSynchronize(P->stream), "sync");
+  });
+}
+
+int dbx_precond_build(dbx_plan* P, double alpha) {
+  return guarded([&] {
+    require(P != nullptr, "null plan");
+    require(alpha >= 0.0, "tikhonov_filter: alpha must be nonnegative");
+    // eig_antireflective preconditions (spectral.hpp:122-126)
+    require(P->n1 >= 3 && P->n2 >= 3, "eig_antireflective: sizes must be >= 3");
+    require(P->q1 <= P->n1 - 2 && P->q2 <= P->n2 - 2, "eig_antireflective: support condition violated");
+    P->set_dev();
+    if (!P->d) ck(cudaMalloc(&P->d, P->N * sizeof(double)), "cudaMalloc");
+    int* flag = nullptr;
+    ck(cudaMalloc(&flag, sizeof(int)), "cudaMalloc");
+    ck(cudaMemsetAsync(flag, 0, sizeof(int), P->stream), "memset");
+    launch_build_filter(P->sym, P->q1, P->q2, P->n1, P->n2, alpha, P->d, flag, P->stream);
+    P->launches += 3;
+    P->check_launch();
+    int hflag = 0;
+    ck(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, P->stream), "D2H");
+    ck(cudaStreamSynchronize(P->stream), "sync");
+    cudaFree(flag);
+    P->have_d = false;
+    require(alpha > 0.0 || hflag == 0, "tikhonov_filter: alpha = 0 with a zero eigenvalue");
+    P->have_d = true;
+  });
+}
+
+int dbx_precond_eigs(dbx_plan* P, double* d_out) {
+  return guarded([&] {
+    require(P && d_out, "null argument");
+    require(P->have_d, "precondition: filter not built");
+    P->set_dev();
+    stage_out(P, d_out, P->d, P->N);
+    ck(cudaStreamSynchronize(P->stream), "sync");
+  });
+}
+
+int dbx_precond_set_eigs(dbx_plan* P, const double* dd) {
+  return guarded([&] {
+    require(P && dd, "null argument");
+    P->set_dev();
+    if (!P->d) ck(cudaMalloc(&P->d, P->N * sizeof(double)), "cudaMalloc");
+    ck(cudaMemcpyAsync(P->d, dd, P->N * sizeof(double), cudaMemcpyDefault, P->stream), "copy");
+    ck(cudaStreamSynchronize(P->stream), "sync");
+    P->have_d = true;
+  });
+}
+
+int dbx_precond_apply(dbx_plan* P, const double* r, double* y) {
+  return guarded([&] {
+    require(P && r && y, "null argument");
+    require(P->have_d, "precondition_apply: filter not built");
+    require(P->n1 >= 3 && P->n2 >= 3, "tensor_apply: anti-reflective transform needs sizes >= 3");
+    P->set_dev();
+    const size_t cnt = P->N * P->batch;
+    const double* rin = stage_in(P, r, P->in, cnt);
+    P->u.ensure(cnt);
+    P->s.ensure(cnt);
+    double* yout = y;
+    if (!is_device_ptr(y)) {
+      P->out.ensure(cnt);
+      yout = P->out.p;
+    }
+    Partials none{nullptr, 0};
+    // T~ (columns, rows) with the Hadamard by d fused, then T (columns, rows)
+    P->pass(DBX_KIND_ARINV, true, rin, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
+    P->pass(DBX_KIND_ARINV, false, P->u.p, SEL_EXPLICIT, P->s.p, SEL_EXPLICIT, EPI_HADAMARD, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
+    P->pass(DBX_KIND_AR, true, P->s.p, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
+    P->pass(DBX_KIND_AR, false, P->u.p, SEL_EXPLICIT, yout, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
+    stage_out(P, y, yout, cnt);
+    ck(cudaStreamSynchronize(P->stream), "sync");
+  });
+}
+
+int dbx_tensor_apply(dbx_plan* P, int kind, const double* x, double* y) {
+  return guarded([&] {
+    require(P && x && y, "null argument");
+    require(kind == DBX_KIND_SINEI || kind == DBX_KIND_AR || kind == DBX_KIND_ARINV,
+            "tensor_apply: unsupported kind");
+    if (kind != DBX_KIND_SINEI)
+      require(P->n1 >= 3 && P->n2 >= 3, "tensor_apply: anti-reflective transform needs sizes >= 3");
+    P->set_dev();
+    const size_t cnt = P->N * P->batch;
+    const double* xin = stage_in(P, x, P->in, cnt);
+    P->u.ensure(cnt);
+    double* yout = y;
+    if (!is_device_ptr(y)) {
+      P->out.ensure(cnt);
+      yout = P->out.p;
+    }
+    Partials none{nullptr, 0};
+    P->pass(kind, true, xin, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
+    P->pass(kind, false, P->u.p, SEL_EXPLICIT, yout, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
+    stage_out(P, y, yout, cnt);
+    ck(cudaStreamSynchronize(P->stream), "sync");
+  });
+}
+
+int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double tau,
+                      int max_iters, int stop_kind, int fixed_iters, double resid_eps,
+                      int use_precond, double* restored, double* rre_hist, double* res_hist,
+                      int* best_iter, int* iters_done, double* x_hist) {
+  return guarded([&] {
+    require(P && g && restored, "landweber: null argument");
+    // solver.hpp:66-72, 17-32
+    require(tau > 0.0, "landweber: tau must be positive");
+    require(max_iters >= 1, "landweber: max_iters must be at least 1");
+    require(stop_kind >= 0 && stop_kind <= 2, "landweber: unknown stopping rule");
+    require(stop_kind != DBX_STOP_FIXED || fixed_iters >= 0, "StoppingRule: negative iteration count");
+    require(stop_kind != DBX_STOP_RESIDUAL || resid_eps > 0.0, "StoppingRule: threshold must be positive");
+    if (use_precond) {
+      require(P->have_d, "d_landweber: preconditioner not built");
+      require(P->n1 >= 3 && P->n2 >= 3, "tensor_apply: anti-reflective transform needs sizes >= 3");
+    }
+    P->set_dev();
+    const int B = P->batch;
+    const size_t N = P->N, cnt = N * B;
+    const int total = stop_kind == DBX_STOP_FIXED ? fixed_iters : max_iters;
+    const bool track = f_true != nullptr;
+    cudaStream_t s = P->stream;
+
+    // ---- stage inputs (H2D for host arrays) ----
+    const double* gd = stage_in(P, g, P->g, cnt);
+    const double* fd = track ? stage_in(P, f_true, P->f, cnt) : nullptr;
+    P->r.ensure(cnt);
+    P->s.ensure(cnt);
+    if (use_precond) P->u.ensure(cnt);
+    P->X3.ensure(3 * cnt);
+    P->part.ensure((size_t)B * NUM_SLOTS * P->part_cap);
+    const int H = std::max(total, 1);
+    P->rre.ensure((size_t)B * H);
+    P->res.ensure((size_t)B * H);
+    const bool want_xh = x_hist != nullptr;
+    if (want_xh) P->xh.ensure((size_t)H * cnt);
+    Partials pt{P->part.p, P->part_cap};
+
+    launch_state_init(P->st, B, s);
+    launch_norms_init(gd, fd, B, N, P->st, nullptr, s);
+    P->launches += 2;
+    // x_0 = 0 in buffer 0, r_0 = g
+    ck(cudaMemsetAsync(P->X3.p, 0, cnt * sizeof(double), s), "memset");
+    ck(cudaMemcpyAsync(P->r.p, gd, cnt * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
+    P->check_launch();
+
+    auto enqueue = [&](int k) {
+      int cnt_x = 0;
+      if (use_precond) {
+        P->blur(P->r.p, SEL_EXPLICIT, P->s.p, SEL_EXPLICIT, true, BLUR_STORE, nullptr, nullptr,
+                SEL_EXPLICIT, nullptr, 0.0, P->st, pt, KC_BLUR_ADJ);
+        P->pass(DBX_KIND_ARINV, true, P->s.p, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, P->st, pt);
+        P->pass(DBX_KIND_ARINV, false, P->u.p, SEL_EXPLICIT, P->s.p, SEL_EXPLICIT, EPI_HADAMARD, nullptr, SEL_EXPLICIT, nullptr, 0, P->st, pt);
+        P->pass(DBX_KIND_AR, true, P->s.p, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, P->st, pt);
+        cnt_x = P->pass(DBX_KIND_AR, false, P->u.p, SEL_EXPLICIT, P->X3.p, SEL_NXT, EPI_AXPY,
+                        P->X3.p, SEL_CUR, fd, tau, P->st, pt);
+      } else {
+        cnt_x = P->blur(P->r.p, SEL_EXPLICIT, P->X3.p, SEL_NXT, true, BLUR_AXPY, nullptr, P->X3.p,
+                        SEL_CUR, fd, tau, P->st, pt, KC_BLUR_ADJ);
+      }
+      const int cnt_r = P->blur(P->X3.p, SEL_NXT, P->r.p, SEL_EXPLICIT, false, BLUR_RESID, gd,
+                                nullptr, SEL_EXPLICIT, nullptr, 0.0, P->st, pt, KC_BLUR);
+      FinalizeArgs fa{};
+      fa.st = P->st; fa.part = pt; fa.cnt_x = cnt_x; fa.cnt_r = cnt_r; fa.k = k;
+      fa.hist_len = H; fa.rre_hist = P->rre.p; fa.res_hist = P->res.p;
+      fa.track = track ? 1 : 0; fa.stop_kind = stop_kind; fa.resid_eps = resid_eps; fa.batch = B;
+      P->ev_begin(KC_FINALIZE);
+      launch_finalize(fa, s);
+      P->ev_end();
+      P->check_launch();
+      if (want_xh) {
+        launch_select_copy(P->X3.p, P->st, 0, B, N, P->xh.p + (size_t)(k - 1) * cnt, s);
+        ++P->launches;
+      }
+    };
+
+    if (use_precond) {
+      // dense matrices are uploaded before capture (no allocation inside a graph)
+      P->matrix(DBX_KIND_ARINV, 0); P->matrix(DBX_KIND_ARINV, 1);
+      P->matrix(DBX_KIND_AR, 0); P->matrix(DBX_KIND_AR, 1);
+    }
+    if (total > 0) {
+      // Graph path: one graph per run shape, replayed; kernels read the run's
+      // buffers through stable plan-owned pointers.
+      char key[512];
+      snprintf(key, sizeof key, "%d|%d|%d|%.17g|%.17g|%d|%d|%p|%p|%d", total, use_precond,
+               stop_kind, resid_eps, tau, (int)track, (int)want_xh, (const void*)gd,
+               (const void*)fd, P->conv);
+      const bool use_graph = !P->timing;
+      if (use_graph) {
+        if (!P->gexec || P->gkey != key) {
+          if (P->gexec) {
+            cudaGraphExecDestroy(P->gexec);
+            P->gexec = nullptr;
+          }
+          cudaGraph_t graph;
+          const int64_t before = P->launches;
+          ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+          for (int k = 1; k <= total; ++k) enqueue(k);
+          ck(cudaStreamEndCapture(s, &graph), "end capture");
+          ck(cudaGraphInstantiate(&P->gexec, graph, 0), "instantiate");
+          cudaGraphDestroy(graph);
+          P->launches = before;  // counted at replay
+          P->gkey = key;
+        }
+        ck(cudaGraphLaunch(P->gexec, s), "graph launch");
+        // launch accounting: kernels per iteration
+        P->launches += (int64_t)total * ((use_precond ? 5 : 1) + 2 + (want_xh ? 1 : 0));
+      } else {
+        for (int k = 1; k <= total; ++k) enqueue(k);
+      }
+    }
+
+    // ---- outputs ----
+    double* rd = is_device_ptr(restored) ? restored : nullptr;
+    if (!rd) {
+      P->out.ensure(cnt);
+      rd = P->out.p;
+    }
+    if (total > 0) {
+      launch_select_copy(P->X3.p, P->st, (stop_kind == DBX_STOP_MINRRE && track) ? 1 : 0, B, N, rd, s);
+      ++P->launches;
+    } else {
+      ck(cudaMemsetAsync(rd, 0, cnt * sizeof(double), s), "memset");
+    }
+    P->check_launch();
+    stage_out(P, restored, rd, cnt);
+    std::vector<ImgState> hs((size_t)B);
+    ck(cudaMemcpyAsync(hs.data(), P->st, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s), "D2H");
+    if (total > 0) {
+      if (res_hist) stage_out(P, res_hist, P->res.p, (size_t)B * H);
+      if (rre_hist && track) stage_out(P, rre_hist, P->rre.p, (size_t)B * H);
+    }
+    if (want_xh && total > 0) {
+      if (is_device_ptr(x_hist)) {
+        for (int b = 0; b < B; ++b)
+          for (int k = 0; k < total; ++k)
+            ck(cudaMemcpyAsync(x_hist + ((size_t)b * H + k) * N, P->xh.p + ((size_t)k * B + b) * N,
+                               N * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
+      } else {
+        for (int b = 0; b < B; ++b)
+          for (int k = 0; k < total; ++k)
+            ck(cudaMemcpyAsync(x_hist + ((size_t)b * H + k) * N, P->xh.p + ((size_t)k * B + b) * N,
+                               N * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+      }
+    }
+    ck(cudaStreamSynchronize(s), "sync");
+    P->ev_collect();
+    int div_img = -1, div_k = 0;
+    for (int b = 0; b < B; ++b) {
+      // the minimum-RRE buffer only matters under MinRre; a run without any
+      // iteration keeps x_0 = 0 (handled above)
+      const ImgState& h = hs[(size_t)b];
+      if (best_iter) best_iter[b] = total > 0 ? h.best_iter : 0;
+      if (iters_done) iters_done[b] = total > 0 ? h.iters : 0;
+      if (total > 0 && h.done == 2 && div_img < 0) {
+        div_img = b;
+        div_k = h.diverged_at;
+      }
+    }
+    if (div_img >= 0) {
+      char msg[160];
+      snprintf(msg, sizeof msg, "landweber: iterate exceeded 1e8 * ||g|| (image %d, iteration %d)",
+               div_img, div_k);
+      throw Diverged(msg);
+    }
+  });
+}
+
+}  // extern "C"

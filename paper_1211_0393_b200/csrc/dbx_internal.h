@@ -1,0 +1,112 @@
+// dbx_internal.h — device-side data structures and kernel launchers of the
+// B200 AR-deblurring path (see DESIGN.md for the data layout in HBM).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace dbx {
+
+// Per-image iteration state, resident in HBM for the whole run.  The three
+// iterate buffers X[0..2] are used round-robin so that tracking the best
+// iterate (solver.hpp:111-119) never copies x: `best` pins a buffer, `cur`
+// holds x_{k-1}, `nxt` receives x_k.
+struct ImgState {
+  int cur, best, nxt;
+  int done;         // 0 running, 1 residual rule hit, 2 diverged
+  int iters;        // iterations executed (solver.hpp:120)
+  int best_iter;    // 1-based, 0 = none
+  int diverged_at;  // first iteration whose ||x|| > guard
+  int pad_;
+  double best_rre;
+  double g_norm, f_norm;
+};
+
+enum BufSel { SEL_EXPLICIT = -1, SEL_CUR = 0, SEL_NXT = 2 };
+
+// Partial-sum slots written by the fused epilogues and reduced (fixed order,
+// deterministic) by the finalize kernel.
+enum Slot { SLOT_X2 = 0, SLOT_XF2 = 1, SLOT_R2 = 2, NUM_SLOTS = 3 };
+
+struct Partials {
+  double* p;      // [batch][NUM_SLOTS][cap]
+  int cap;        // entries per (image, slot)
+};
+
+__host__ __device__ inline const double* resolve_ptr(const double* base, const ImgState* st,
+                                                     int sel, int b, int batch, size_t N) {
+#ifdef __CUDA_ARCH__
+  if (sel == SEL_EXPLICIT) return base + (size_t)b * N;
+  const int idx = sel == SEL_CUR ? st[b].cur : st[b].nxt;
+  return base + ((size_t)idx * batch + b) * N;
+#else
+  (void)st; (void)sel;
+  return base + (size_t)b * N;
+#endif
+}
+
+// ---- blur (AR stencil) --------------------------------------------------
+enum BlurMode { BLUR_STORE = 0, BLUR_RESID = 1, BLUR_AXPY = 2 };
+
+struct BlurArgs {
+  const double* x; int xsel;          // input image(s)
+  double* y; int ysel;                // output (STORE/RESID: explicit; AXPY: x_nxt)
+  const double* w;                    // correlation weights (2q1+1)(2q2+1), oriented
+  int n1, n2, q1, q2, batch;
+  int mode;
+  const double* g;                    // RESID: data
+  const double* xold; int xoldsel;    // AXPY: x_{k-1}
+  const double* f;                    // AXPY: true image (nullable)
+  double tau;
+  const ImgState* st;                 // nullable outside the solver
+  Partials part;
+};
+void launch_blur(const BlurArgs& a, cudaStream_t s, int* ctas_per_image);
+
+// ---- dense-form AR transform passes (FP64 GEMM with fused epilogues) ----
+enum GemmEpi { EPI_STORE = 0, EPI_HADAMARD = 1, EPI_AXPY = 2 };
+
+struct GemmArgs {
+  // C[b] (M x N) = A[b] (M x K) * B[b] (K x N), row-major.
+  const double* A; long long sA; int asel;
+  const double* B; long long sB; int bsel;
+  double* C; long long sC; int csel;
+  int M, N, K, batch;
+  int epi;
+  const double* d;                    // HADAMARD: M x N filter grid (shared)
+  const double* xold; int xoldsel;    // AXPY
+  const double* f;                    // AXPY (nullable)
+  double tau;
+  const ImgState* st;
+  Partials part;
+  size_t img_elems;                   // n1*n2 (for buffer resolution)
+};
+void launch_gemm(const GemmArgs& a, cudaStream_t s, int* ctas_per_image);
+
+// ---- spectrum, norms, finalize -----------------------------------------
+void launch_build_filter(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha,
+                         double* d, int* zero_flag, cudaStream_t s);
+void launch_norms_init(const double* g, const double* f, int batch, size_t N, ImgState* st,
+                       double* scratch, cudaStream_t s);
+struct FinalizeArgs {
+  ImgState* st;
+  Partials part;
+  int cnt_x, cnt_r;       // partial counts per image for the x- and r-norm slots
+  int k;                  // 1-based iteration index
+  int hist_len;
+  double* rre_hist;       // [batch][hist_len] (device)
+  double* res_hist;
+  int track, stop_kind;
+  double resid_eps;
+  int batch;
+};
+void launch_finalize(const FinalizeArgs& a, cudaStream_t s);
+void launch_state_init(ImgState* st, int batch, cudaStream_t s);
+void launch_select_copy(const double* X3, const ImgState* st, int which_best, int batch,
+                        size_t N, double* out, cudaStream_t s);
+void launch_zero(double* p, size_t n, cudaStream_t s);
+
+}  // namespace dbx

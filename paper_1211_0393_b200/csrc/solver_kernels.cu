@@ -1,0 +1,213 @@
+// solver_kernels.cu — K5 (Tikhonov filter grid) and K6 (deterministic norm
+// reductions, history recording, best-iterate tracking, stopping rules).
+//
+// Replaces (reference):
+//   symbol_real                  psf.hpp:98-109
+//   antireflective_grid / eig_antireflective   spectral.hpp:63-69, 120-133
+//   tikhonov_filter              preconditioner.hpp:37-57
+//   landweber_loop bookkeeping   solver.hpp:86-130 (guard, histories, strict-'<'
+//                                best, residual rule), rre image.hpp:85-91
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "dbx_internal.h"
+
+namespace dbx {
+
+namespace {
+
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+// cos(s * x_r) tables on the AR grid x_0 = 0, x_r = r*pi/(n-1), x_{n-1} = 0
+// (spectral.hpp:63-69); argument formed exactly like the reference
+// (double(r)*kPi/double(n-1), then s*x) so both sides see the same angle.
+__global__ void cos_table_kernel(int n, int q, double* tab) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * (q + 1)) return;
+  const int r = idx / (q + 1), s = idx - r * (q + 1);
+  double x = 0.0;
+  if (r >= 1 && r <= n - 2) x = (double)r * kPi / (double)(n - 1);
+  tab[idx] = cos((double)s * x);
+}
+
+// d(a,b) = 1 / (lambda^2 + alpha), lambda = symbol_real(h_sym, x_a, x_b) with
+// the reference accumulation order: h00, axis-1 terms, axis-2 terms, cross.
+__global__ void filter_kernel(const double* __restrict__ h, int q1, int q2, int n1, int n2,
+                              const double* __restrict__ c1, const double* __restrict__ c2,
+                              double alpha, double* __restrict__ d, int* zero_flag) {
+  extern __shared__ double hs[];
+  const int wq = 2 * q2 + 1;
+  for (int i = threadIdx.x; i < (2 * q1 + 1) * wq; i += blockDim.x) hs[i] = h[i];
+  __syncthreads();
+  const int bcol = blockIdx.x * blockDim.x + threadIdx.x;
+  const int arow = blockIdx.y;
+  if (bcol >= n2) return;
+  const double* C1 = c1 + (size_t)arow * (q1 + 1);
+  const double* C2 = c2 + (size_t)bcol * (q2 + 1);
+  auto tap = [&](int s1, int s2) { return hs[(q1 + s1) * wq + (q2 + s2)]; };
+  double acc = tap(0, 0);
+  for (int s1 = 1; s1 <= q1; ++s1) acc += 2.0 * tap(s1, 0) * C1[s1];
+  for (int s2 = 1; s2 <= q2; ++s2) acc += 2.0 * tap(0, s2) * C2[s2];
+  for (int s1 = 1; s1 <= q1; ++s1) {
+    const double a1 = C1[s1];
+    for (int s2 = 1; s2 <= q2; ++s2) acc += 4.0 * tap(s1, s2) * a1 * C2[s2];
+  }
+  const double m2 = acc * acc;
+  if (!(m2 > 0.0)) atomicOr(zero_flag, 1);
+  d[(size_t)arow * n2 + bcol] = 1.0 / (m2 + alpha);
+}
+
+// Fixed-order block reduction (deterministic).
+__device__ double block_reduce(double v) {
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+  return s;
+}
+
+__device__ double strided_sumsq(const double* p, size_t n) {
+  double s = 0.0;
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) s += p[i] * p[i];
+  return block_reduce(s);
+}
+
+__global__ void norms_init_kernel(const double* g, const double* f, size_t N, ImgState* st) {
+  const int b = blockIdx.x;
+  const double gs = strided_sumsq(g + (size_t)b * N, N);
+  double fs = 0.0;
+  if (f) fs = strided_sumsq(f + (size_t)b * N, N);
+  if (threadIdx.x == 0) {
+    st[b].g_norm = sqrt(gs);
+    st[b].f_norm = f ? sqrt(fs) : 0.0;
+  }
+}
+
+__global__ void state_init_kernel(ImgState* st, int batch) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  ImgState s = st[b];
+  s.cur = 0;
+  s.best = 0;
+  s.nxt = 1;
+  s.done = 0;
+  s.iters = 0;
+  s.best_iter = 0;
+  s.diverged_at = 0;
+  s.best_rre = INFINITY;
+  st[b] = s;
+}
+
+__device__ double partial_sum(const double* p, int cnt) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) s += p[i];
+  return block_reduce(s);
+}
+
+// One CTA per image: reduce the fused-epilogue partials of iteration k and
+// apply the reference loop bookkeeping (solver.hpp:107-124).
+__global__ void finalize_kernel(FinalizeArgs a) {
+  const int b = blockIdx.x;
+  ImgState* st = a.st + b;
+  if (st->done) return;
+  const double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
+  const double x2 = partial_sum(P + SLOT_X2 * a.part.cap, a.cnt_x);
+  const double xf2 = a.track ? partial_sum(P + SLOT_XF2 * a.part.cap, a.cnt_x) : 0.0;
+  const double r2 = partial_sum(P + SLOT_R2 * a.part.cap, a.cnt_r);
+  if (threadIdx.x != 0) return;
+  ImgState s = *st;
+  const int k = a.k;
+  const double xn = sqrt(x2);
+  // divergence guard before recording (solver.hpp:107-108)
+  if (xn > 1e8 * s.g_norm && s.g_norm > 0.0) {
+    s.done = 2;
+    s.diverged_at = k;
+    s.cur = s.nxt;
+    *st = s;
+    return;
+  }
+  const double rn = sqrt(r2);
+  if (a.res_hist) a.res_hist[(size_t)b * a.hist_len + (k - 1)] = rn;
+  if (a.track) {
+    const double e = sqrt(xf2) / s.f_norm;
+    if (a.rre_hist) a.rre_hist[(size_t)b * a.hist_len + (k - 1)] = e;
+    if (e < s.best_rre) {  // strict '<': first minimum wins (solver.hpp:114)
+      s.best_rre = e;
+      s.best_iter = k;
+      s.best = s.nxt;
+    }
+  }
+  s.iters = k;
+  // rotate buffers: x_k becomes current; next target avoids cur and best
+  s.cur = s.nxt;
+  int n = 0;
+  while (n == s.cur || n == s.best) ++n;
+  s.nxt = n;
+  if (a.stop_kind == 2 && s.g_norm > 0.0 && rn / s.g_norm < a.resid_eps) s.done = 1;
+  *st = s;
+}
+
+__global__ void select_copy_kernel(const double* X3, const ImgState* st, int which_best,
+                                   int batch, size_t N, double* out) {
+  const int b = blockIdx.y;
+  const int idx = (which_best && st[b].best_iter > 0) ? st[b].best : st[b].cur;
+  const double* src = X3 + ((size_t)idx * batch + b) * N;
+  double* dst = out + (size_t)b * N;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+__global__ void zero_kernel(double* p, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    p[i] = 0.0;
+}
+
+}  // namespace
+
+void launch_build_filter(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha,
+                         double* d, int* zero_flag, cudaStream_t s) {
+  double *c1 = nullptr, *c2 = nullptr;
+  cudaMallocAsync(&c1, sizeof(double) * (size_t)n1 * (q1 + 1), s);
+  cudaMallocAsync(&c2, sizeof(double) * (size_t)n2 * (q2 + 1), s);
+  cos_table_kernel<<<(n1 * (q1 + 1) + 255) / 256, 256, 0, s>>>(n1, q1, c1);
+  cos_table_kernel<<<(n2 * (q2 + 1) + 255) / 256, 256, 0, s>>>(n2, q2, c2);
+  const size_t sm = sizeof(double) * (2 * q1 + 1) * (2 * q2 + 1);
+  if (sm > 48 * 1024)
+    cudaFuncSetAttribute(filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  dim3 grid((n2 + 127) / 128, n1);
+  filter_kernel<<<grid, 128, sm, s>>>(sym_taps, q1, q2, n1, n2, c1, c2, alpha, d, zero_flag);
+  cudaFreeAsync(c1, s);
+  cudaFreeAsync(c2, s);
+}
+
+void launch_norms_init(const double* g, const double* f, int batch, size_t N, ImgState* st,
+                       double* /*scratch*/, cudaStream_t s) {
+  norms_init_kernel<<<batch, 1024, 0, s>>>(g, f, N, st);
+}
+
+void launch_finalize(const FinalizeArgs& a, cudaStream_t s) {
+  finalize_kernel<<<a.batch, 256, 0, s>>>(a);
+}
+
+void launch_state_init(ImgState* st, int batch, cudaStream_t s) {
+  state_init_kernel<<<(batch + 127) / 128, 128, 0, s>>>(st, batch);
+}
+
+void launch_select_copy(const double* X3, const ImgState* st, int which_best, int batch,
+                        size_t N, double* out, cudaStream_t s) {
+  dim3 grid((unsigned)((N + 255) / 256 < 1024 ? (N + 255) / 256 : 1024), batch);
+  select_copy_kernel<<<grid, 256, 0, s>>>(X3, st, which_best, batch, N, out);
+}
+
+void launch_zero(double* p, size_t n, cudaStream_t s) {
+  zero_kernel<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(p, n);
+}
+
+}  // namespace dbx
