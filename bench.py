@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Benchmark: Mpixel-iterations/s of preconditioned AR-BC Landweber on B200.
+
+Workload (default): BASELINE config C3 — a batch of 64 FP64 1024x1024 images
+(seed per image), 31x31 Gaussian mask sigma=(4,4.5) offset (+1,0), 1% noise,
+40 preconditioned (D-)Landweber iterations under anti-reflective BCs.  One
+"step" is one complete 40-iteration restoration of the rank's 64-image batch
+(histories, best-iterate tracking and all per-iteration norms included).
+Weak scaling: every rank restores its own 64-image batch (images
+rank*64 .. rank*64+63), no data-path collective.
+
+  value  : device-resident inputs, CUDA events on the plan's stream, max over ranks
+  e2e    : same solve through the public C-ABI with pinned HOST buffers, i.e.
+           H2D of g and f_true + D2H of the restored images inside the timed region
+  roofline: dominant kernel class (per-launch CUDA events over the timed region)
+  cpu_baseline: the CPU oracle port (oracle/), rank 0 at N=1, bounded sample
+
+`--impl reference` times the reference algorithm's CPU restatement (the oracle
+port; the reference itself cannot be built: Eigen3/FFTW3 are absent) with all
+host threads on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mpixel-iterations/s of preconditioned AR-BC iteration"
+UNIT = "Mpixel-iterations/s"
+PEAKS_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--images", type=int, default=0, help="override images per rank")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def cpu_sample(cfg, threads: int, iters: int):
+    """Oracle (CPU restatement of the reference) on `threads` concurrent images,
+    each `iters` D-Landweber iterations; returns (Mpx-it/s, seconds, sample str)."""
+    from oracle import oracle as O
+    from paper_1211_0393_b200 import configs as cf
+    O.build()
+    probs = [cf.make_problem(cfg, image=i) for i in range(threads)]
+    taps = probs[0][2]
+    d = O.build_tikhonov(taps, cfg.alpha, cfg.n, cfg.n)
+    errs = []
+
+    def work(i):
+        try:
+            f, g, _ = probs[i]
+            O.landweber(taps, g, d=d, f_true=f, max_iters=iters)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    t0 = time.perf_counter()
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    dt = time.perf_counter() - t0
+    if errs:
+        raise errs[0]
+    px_it = threads * cfg.n * cfg.n * iters
+    sample = (f"{threads} image(s) x {iters} D-Landweber iteration(s) of {cfg.name} ({cfg.n}^2, q={cfg.q}), "
+              f"oracle port: reference algorithm (FFT correlation for q>7, FFT DST-I), {threads} thread(s)")
+    return px_it / dt / 1e6, dt, sample
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1211_0393_b200 import configs as cf
+    cfg = cf.CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    vals = []
+    for s in range(args.warmup + args.steps):
+        v, dt, sample = cpu_sample(cfg, threads, 1)
+        if s >= args.warmup:
+            vals.append((v, dt))
+    v = float(np.median([x[0] for x in vals]))
+    ms = float(np.median([x[1] for x in vals])) * 1e3
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, host-generated)",
+            "config": {"workload": f"{cfg.name} (bounded CPU sample)", "n": cfg.n, "q": cfg.q},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference (Eigen3/FFTW3 header library) is unbuildable here; timed its CPU restatement "
+                    "oracle/deblur_oracle.cpp (own FFT in place of FFTW), one image per host thread"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1211_0393_b200 as dbx
+    from paper_1211_0393_b200 import configs as cf
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    L = dbx.lib()
+    cfg = cf.CONFIGS[args.config]
+    B = args.images or cfg.batch
+    n, q = cfg.n, cfg.q
+    N = n * n
+
+    # ---- synthetic inputs (host, seeded per image; not timed) ----
+    F, G, taps = cf.make_batch(cfg, B, first=rank * B)
+    dev = torch.device("cuda", local)
+    g_d = torch.from_numpy(G).to(dev)
+    f_d = torch.from_numpy(F).to(dev)
+    out_d = torch.empty_like(g_d)
+    del F, G
+
+    plan = C.c_void_p()
+    dbx._check(L.dbx_plan_create(n, n, B, dbx._ptr(taps), q, q, 3, local, C.byref(plan)))
+    dbx._check(L.dbx_precond_build(plan, float(cfg.alpha)))
+    stream = torch.cuda.ExternalStream(L.dbx_plan_stream(plan), device=dev)
+    H = cfg.iters
+    rre_h = np.zeros((B, H))
+    res_h = np.zeros((B, H))
+    best = (C.c_int * B)()
+    done = (C.c_int * B)()
+
+    def solve(g, f, out):
+        dbx._check(L.dbx_landweber_run(plan, dbx._ptr(g), dbx._ptr(f), 1.0, H, 1, 0, 0.0, 1, dbx._ptr(out),
+                                       dbx._ptr(rre_h), dbx._ptr(res_h), best, done, None))
+
+    for _ in range(args.warmup):
+        solve(g_d, f_d, out_d)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs ----
+    L.dbx_plan_set_timing(plan, 1)
+    clocks = Clocks(local)
+    kms_tot = np.zeros(4)
+    kcnt_tot = np.zeros(4, dtype=np.int64)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = L.dbx_plan_launch_count(plan)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for s in range(args.steps):
+        with torch.cuda.stream(stream):
+            ev[s][0].record(stream)
+        solve(g_d, f_d, out_d)
+        with torch.cuda.stream(stream):
+            ev[s][1].record(stream)
+        ms = (C.c_double * 8)()
+        cnt = (C.c_int * 8)()
+        L.dbx_plan_kernel_times(plan, ms, cnt, 8)
+        kms_tot += np.array(ms[:4])
+        kcnt_tot += np.array(cnt[:4])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = int(L.dbx_plan_launch_count(plan) - launches0)
+    L.dbx_plan_set_timing(plan, 0)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_ms = float(np.sum(step_ms))
+    t_local = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    t_max = float(t_local.item())
+    px_it = world * B * N * H * args.steps
+    value = px_it / (t_max * 1e-3) / 1e6
+
+    # ---- e2e: public C-ABI with pinned host buffers (H2D + D2H inside) ----
+    e2e = None
+    if not args.no_e2e:
+        gh = g_d.cpu().pin_memory()
+        fh = f_d.cpu().pin_memory()
+        oh = torch.empty_like(gh).pin_memory()
+        solve(gh, fh, oh)  # warm (host-staging buffers)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        for _ in range(args.steps):
+            solve(gh, fh, oh)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": px_it / (float(te.item()) * 1e-3) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(2 * B * N * 8), "d2h_bytes_per_step": int(B * N * 8 + 2 * B * H * 8)}
+
+    # ---- roofline of the dominant kernel class ----
+    names = ["blur_adjoint(A')", "blur(A)+residual", "ar_transform_pass", "finalize"]
+    dom = int(np.argmax(kms_tot))
+    avg_ms = kms_tot[dom] / max(kcnt_tot[dom], 1)
+    peaks = {}
+    if os.path.exists(PEAKS_FILE):
+        peaks = json.load(open(PEAKS_FILE))
+    stencil_flops = 2.0 * (2 * q + 1) ** 2 * N * B          # one blur launch, dense count
+    if dom == 2:
+        flops = 2.0 * n * n * n * B                       # one dense transform pass (GEMM form, 2 n^3 / image)
+        peak = peaks.get("dmma_tflops_sustained", 37.0)
+        psrc = "measured DMMA FP64 (profiles/r01_fp64_peak.json, sustained)"
+    else:
+        flops = stencil_flops
+        peak = peaks.get("dfma_tflops_sustained", 34.0)
+        psrc = "measured DFMA FP64 (profiles/r01_fp64_peak.json, sustained)"
+    achieved = flops / (avg_ms * 1e-3) / 1e12
+    roof = {"bound": "tensor" if dom == 2 else "fp64", "kernel": names[dom], "achieved": achieved,
+            "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+            "peak_source": psrc, "avg_launch_ms": avg_ms,
+            "share_of_step": float(kms_tot[dom] / max(kms_tot.sum(), 1e-9)),
+            "class_ms_per_step": {names[i]: float(kms_tot[i] / args.steps) for i in range(4)}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, sample = cpu_sample(cfg, 1, 2)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded scenes/masks/noise, host-generated; stands in for Cameraman/Bridge)",
+                "config": {"workload": f"{cfg.name}: {B} x {n}x{n} FP64 images per GPU, q={q} mask, "
+                                       f"{H} D-Landweber iterations, AR BCs, alpha={cfg.alpha}",
+                           "images_per_gpu": B, "global_images": B * world, "n": n, "q": q, "iters": H,
+                           "parallelism": f"batch-sharded x{world} (no data-path collective)",
+                           "l2": "inputs larger than L2 (each 64x1024^2 FP64 array = 512 MiB)"},
+                "clocks": clk, "gpu_launches": launches, "roofline": roof, "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    L.dbx_plan_destroy(plan)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
