@@ -60,6 +60,14 @@ extern "C" {
 #define DBX_CONV_DIRECT 1
 #define DBX_CONV_FFT 2
 
+/* AR-transform engine selection (dbx_plan_set_dst).  FFT = Bluestein DST-I in
+ * shared memory (power-of-two M >= 2N-1 up to 8192); DENSE = FP64 GEMM with the
+ * dense T~/T matrices (reference dense_ar_forward / dense_ar_inverse block
+ * forms).  AUTO picks FFT whenever the length is compiled. */
+#define DBX_DST_AUTO 0
+#define DBX_DST_DENSE 1
+#define DBX_DST_FFT 2
+
 typedef struct dbx_plan dbx_plan;
 
 /* Message of the last failing call on this thread ("" if none). */
@@ -89,6 +97,13 @@ void* dbx_plan_stream(dbx_plan* plan);
 
 /* Blur engine override (DBX_CONV_*); default DBX_CONV_AUTO. */
 int dbx_plan_set_conv(dbx_plan* plan, int conv);
+
+/* AR-transform engine override (DBX_DST_*); default DBX_DST_AUTO. */
+int dbx_plan_set_dst(dbx_plan* plan, int engine);
+
+/* Engines the plan will use: *conv in {DBX_CONV_DIRECT, DBX_CONV_FFT},
+ * *dst in {DBX_DST_DENSE, DBX_DST_FFT}. */
+int dbx_plan_engines(dbx_plan* plan, int* conv, int* dst);
 
 /*
  * y = A x (adjoint = 0) or y = A' x (adjoint = 1), for every image of the

@@ -63,6 +63,8 @@ def lib():
         L.dbx_plan_stream.argtypes = [vp]
         L.dbx_plan_stream.restype = vp
         L.dbx_plan_set_conv.argtypes = [vp, i]
+        L.dbx_plan_set_dst.argtypes = [vp, i]
+        L.dbx_plan_engines.argtypes = [vp, C.POINTER(i), C.POINTER(i)]
         L.dbx_blur_apply.argtypes = [vp, vp, vp, i]
         L.dbx_precond_build.argtypes = [vp, d]
         L.dbx_precond_eigs.argtypes = [vp, vp]
@@ -146,6 +148,12 @@ class Algebra(enum.IntEnum):  # spectral.hpp:12
 class ConvEngine(enum.IntEnum):
     Auto = 0
     Direct = 1
+    Fft = 2
+
+
+class DstEngine(enum.IntEnum):
+    Auto = 0
+    Dense = 1
     Fft = 2
 
 
@@ -239,6 +247,16 @@ class BlurOperator:
 
     def set_conv(self, engine: ConvEngine):
         _check(lib().dbx_plan_set_conv(self.handle, int(engine)))
+        return self
+
+    def set_dst(self, engine: DstEngine):
+        _check(lib().dbx_plan_set_dst(self.handle, int(engine)))
+        return self
+
+    def engines(self):
+        c, d = C.c_int(), C.c_int()
+        _check(lib().dbx_plan_engines(self.handle, C.byref(c), C.byref(d)))
+        return ConvEngine(c.value), DstEngine(d.value)
 
     def stream(self):
         return lib().dbx_plan_stream(self.handle)
@@ -279,7 +297,7 @@ def apply_reblur_adjoint(op: BlurOperator, r):
     return y
 
 
-def tensor_apply(kind: TransformKind, x, op: Optional[BlurOperator] = None):
+def tensor_apply(kind: TransformKind, x, op: Optional[BlurOperator] = None, engine: DstEngine = DstEngine.Auto):
     """2D separable transform, columns then rows (transforms.hpp:198-226)."""
     x = _f64(x)
     if kind == TransformKind.Dft:
@@ -291,6 +309,7 @@ def tensor_apply(kind: TransformKind, x, op: Optional[BlurOperator] = None):
         raise ValueError("tensor_apply: anti-reflective transform needs sizes >= 3")
     if op is None:
         op = _transform_op(n1, n2, 1 if x.ndim == 2 else x.shape[0])
+    op.set_dst(engine)
     y = _empty_like(x)
     _check(lib().dbx_tensor_apply(op.handle, int(kind), _ptr(x), _ptr(y)))
     return y
@@ -350,7 +369,7 @@ def filter_from_eigs(eigs, n1=None, n2=None, batch: int = 1) -> FilteredOperator
     return FilteredOperator(eigs, None, 0.0, op)
 
 
-def precondition_apply(d: FilteredOperator, r):
+def precondition_apply(d: FilteredOperator, r, engine: DstEngine = DstEngine.Auto):
     """D r = T (d o T~ r) (preconditioner.hpp:88-90, spectral.hpp:161-165)."""
     r = _f64(r)
     if (r.shape[-2], r.shape[-1]) != (d.n1, d.n2):
@@ -359,6 +378,7 @@ def precondition_apply(d: FilteredOperator, r):
         op = filter_from_eigs(d.eigs, batch=r.shape[0])._op
     else:
         op = d._op
+    op.set_dst(engine)
     y = _empty_like(r)
     _check(lib().dbx_precond_apply(op.handle, _ptr(r), _ptr(y)))
     return y

@@ -16,6 +16,8 @@
 
 #include "../../include/dbx.h"
 #include "dbx_internal.h"
+#include "spectral.h"
+#include "tables.h"
 
 using namespace dbx;
 
@@ -172,6 +174,13 @@ std::vector<double> transpose(const std::vector<double>& a, long n) {
   return t;
 }
 
+// Launcher result check: a negative CTA count means the size is not compiled
+// or its shared-memory plan does not fit this device.
+inline int lc(int rc, const char* what) {
+  if (rc < 0) throw CudaErr(std::string(what) + ": launch configuration unsupported on this device");
+  return rc;
+}
+
 enum KClass { KC_BLUR_ADJ = 0, KC_BLUR = 1, KC_TRANSFORM = 2, KC_FINALIZE = 3, KC_NUM = 4 };
 
 }  // namespace
@@ -202,6 +211,18 @@ struct dbx_plan {
   // graph cache
   cudaGraphExec_t gexec = nullptr;
   std::string gkey;
+  // ---- FFT-form state ----
+  int dst = DBX_DST_AUTO;
+  bool conv_ready = false;
+  int L1 = 0, L2 = 0, Lh = 0;
+  double *tw1 = nullptr, *tw2 = nullptr, *HA = nullptr, *HAt = nullptr;
+  DevBuf zb, yb;
+  struct Blue {
+    bool ready = false;
+    double *tw = nullptr, *chirp = nullptr, *bhat = nullptr, *p = nullptr;
+    BlueTables t;
+  } blue[2][2];  // [axis 0 = columns (n1), 1 = rows (n2)][0 = AR kinds, 1 = SineI]
+  std::vector<double*> owned;
 
   ~dbx_plan() {
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -211,17 +232,115 @@ struct dbx_plan {
         if (p) cudaFree(p);
     for (double* p : {w_A, w_At, sym, d})
       if (p) cudaFree(p);
+    for (double* p : owned) cudaFree(p);
     if (st) cudaFree(st);
-    for (DevBuf* b : {&g, &f, &r, &s, &u, &X3, &in, &out, &part, &rre, &res, &xh}) b->release();
+    for (DevBuf* b : {&g, &f, &r, &s, &u, &X3, &in, &out, &part, &rre, &res, &xh, &zb, &yb}) b->release();
     if (stream) cudaStreamDestroy(stream);
+  }
+
+  double* upload_owned(const std::vector<double>& h) {
+    double* p = upload(h);
+    owned.push_back(p);
+    return p;
+  }
+
+  // ---- engine selection ----
+  // Conv: the reference switches to FFT correlation for q > 7 (blur.hpp:70,
+  // 79-82); AUTO follows that cutover whenever a compiled FFT length fits.
+  int conv_len(int n, int q) const { return conv_supported_len(n + 2 * q + (n + 2 * q) % 2); }
+  bool use_fft_conv() const {
+    if (conv == DBX_CONV_DIRECT) return false;
+    const bool fits = conv_len(n1, q1) > 0 && conv_len(n2, q2) > 0;
+    if (conv == DBX_CONV_FFT) return fits;
+    return fits && (q1 > 7 || q2 > 7);
+  }
+  // DST line length: the direct odd-length DFT when N is compiled (prime
+  // factors <= 31: 255, 1023, ...), else a power-of-two Bluestein M >= 2N-1.
+  static int blue_len(int N) {
+    if (direct_supported_len(N)) return N;
+    return blue_supported_len(2 * N - 1 < 16 ? 16 : 2 * N - 1);
+  }
+  // The packed Bluestein DST-I reads the odd outputs from the (-1)^j-modulated
+  // DFT, which needs N = m+1 odd (every BASELINE config: N = n-1, n even);
+  // even N runs the dense engine.
+  bool use_fft_dst(bool sine) const {
+    if (dst == DBX_DST_DENSE) return false;
+    const int N1 = sine ? n1 + 1 : n1 - 1, N2 = sine ? n2 + 1 : n2 - 1;
+    return (N1 & 1) && (N2 & 1) && blue_len(N1) > 0 && blue_len(N2) > 0;
+  }
+
+  void ensure_conv() {
+    if (conv_ready) return;
+    L1 = conv_len(n1, q1);
+    L2 = conv_len(n2, q2);
+    Lh = L2 / 2 + 1;
+    tw1 = upload_owned(twiddles(L1));
+    tw2 = upload_owned(twiddles(L2));
+    const size_t nt = taps.size();
+    std::vector<double> rot(taps.rbegin(), taps.rend());
+    HA = upload_owned(conv_spectrum(rot.data(), q1, q2, L1, L2));
+    HAt = upload_owned(conv_spectrum(taps.data(), q1, q2, L1, L2));
+    (void)nt;
+    zb.ensure((size_t)batch * n1 * Lh * 2);
+    yb.ensure((size_t)batch * n1 * Lh * 2);
+    conv_ready = true;
+  }
+
+  const BlueTables& blue_tables(int axis, bool sine) {
+    Blue& B = blue[axis][sine ? 1 : 0];
+    if (!B.ready) {
+      const int n = axis == 0 ? n1 : n2;
+      const int N = sine ? n + 1 : n - 1;
+      const BlueHost h = bluestein(n, sine, blue_len(N));
+      B.tw = upload_owned(h.tw);
+      B.chirp = upload_owned(h.chirp);
+      B.bhat = upload_owned(h.bhat);
+      B.p = upload_owned(h.p);
+      B.t.tw = reinterpret_cast<const double2*>(B.tw);
+      B.t.chirp = reinterpret_cast<const double2*>(B.chirp);
+      B.t.bhat = reinterpret_cast<const double2*>(B.bhat);
+      B.t.p = B.p;
+      B.t.alpha = h.alpha;
+      B.t.scale = h.scale;
+      B.t.n = h.n;
+      B.t.N = h.N;
+      B.t.M = h.M;
+      B.ready = true;
+    }
+    return B.t;
+  }
+
+  // prepare everything a run needs before graph capture (no allocation inside)
+  void prepare(bool precond) {
+    if (use_fft_conv()) ensure_conv();
+    if (precond) {
+      if (use_fft_dst(false)) {
+        blue_tables(0, false);
+        blue_tables(1, false);
+      } else {
+        matrix(DBX_KIND_ARINV, 0); matrix(DBX_KIND_ARINV, 1);
+        matrix(DBX_KIND_AR, 0); matrix(DBX_KIND_AR, 1);
+      }
+    }
+  }
+
+  SpecArgs spec_base(const ImgState* stp, Partials pt) const {
+    SpecArgs a;
+    a.n1 = n1; a.n2 = n2; a.q1 = q1; a.q2 = q2; a.batch = batch;
+    a.st = stp; a.part = pt;
+    return a;
   }
 
   void set_dev() const { ck(cudaSetDevice(device), "cudaSetDevice"); }
 
+  // Ordered on the plan's (non-blocking) stream: a plain cudaMemcpy from
+  // pageable memory may return before its DMA lands, which would race the
+  // next kernel on this stream.
   double* upload(const std::vector<double>& h) {
     double* p = nullptr;
     ck(cudaMalloc(&p, h.size() * sizeof(double)), "cudaMalloc");
-    ck(cudaMemcpy(p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice), "upload");
+    ck(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, stream), "upload");
+    ck(cudaStreamSynchronize(stream), "upload sync");
     return p;
   }
 
@@ -273,6 +392,28 @@ struct dbx_plan {
   int blur(const double* x, int xsel, double* y, int ysel, bool adjoint, int mode,
            const double* gg, const double* xold, int xoldsel, const double* ff, double tau,
            const ImgState* stp, Partials pt, int cls) {
+    if (use_fft_conv()) {
+      ensure_conv();
+      SpecArgs a = spec_base(stp, pt);
+      a.conv.tw1 = reinterpret_cast<const double2*>(tw1);
+      a.conv.tw2 = reinterpret_cast<const double2*>(tw2);
+      a.conv.H = reinterpret_cast<const double2*>(adjoint ? HAt : HA);
+      a.conv.L1 = L1; a.conv.L2 = L2; a.conv.Lh = Lh;
+      a.zbuf = reinterpret_cast<double2*>(zb.p);
+      a.ybuf = reinterpret_cast<double2*>(yb.p);
+      a.in = x; a.insel = xsel;
+      ev_begin(cls);
+      lc(launch_conv_row_fwd(a, stream), "launch_conv_row_fwd");
+      lc(launch_conv_col(a, stream), "launch_conv_col");
+      a.out = y; a.outsel = ysel;
+      a.epi = mode == BLUR_STORE ? SPEC_STORE : mode == BLUR_RESID ? SPEC_RESID : SPEC_AXPY;
+      a.g = gg; a.xold = xold; a.xoldsel = xoldsel; a.f = ff; a.tau = tau;
+      const int ctas = lc(launch_conv_row_inv(a, stream), "launch_conv_row_inv");
+      ev_end();
+      launches += 2;
+      check_launch();
+      return ctas;
+    }
     BlurArgs a{};
     a.x = x; a.xsel = xsel; a.y = y; a.ysel = ysel;
     a.w = adjoint ? w_At : w_A;
@@ -312,6 +453,41 @@ struct dbx_plan {
     check_launch();
     return ctas;
   }
+
+  // D x = T (d o (T~ x)) (or its first/last halves).  FFT form: T~ rows,
+  // [T~ -> d -> T] columns, T rows with the caller's epilogue; dense form: the
+  // four GEMM half-passes.  Returns the CTA count of the epilogue launch.
+  int apply_D(const double* X, int xsel, double* Y, int ysel, int epi_spec, const double* xold,
+              int xoldsel, const double* ff, double tau, const ImgState* stp, Partials pt) {
+    if (use_fft_dst(false)) {
+      SpecArgs a = spec_base(stp, pt);
+      a.blue1 = blue_tables(0, false);
+      a.blue2 = blue_tables(1, false);
+      a.d = d;
+      // T~ along rows
+      a.in = X; a.insel = xsel; a.out = u.p; a.outsel = SEL_EXPLICIT; a.kind1 = DBX_KIND_ARINV;
+      a.epi = SPEC_STORE;
+      ev_begin(KC_TRANSFORM); lc(launch_dst_rows(a, stream), "launch_dst_rows"); ev_end();
+      // T~ -> d -> T along columns
+      a.in = u.p; a.insel = SEL_EXPLICIT; a.out = s.p; a.outsel = SEL_EXPLICIT;
+      a.kind1 = DBX_KIND_ARINV; a.kind2 = DBX_KIND_AR;
+      ev_begin(KC_TRANSFORM); lc(launch_dst_cols(a, stream), "launch_dst_cols"); ev_end();
+      // T along rows + epilogue
+      a.in = s.p; a.insel = SEL_EXPLICIT; a.out = Y; a.outsel = ysel; a.kind1 = DBX_KIND_AR; a.kind2 = -1;
+      a.epi = epi_spec; a.xold = xold; a.xoldsel = xoldsel; a.f = ff; a.tau = tau;
+      ev_begin(KC_TRANSFORM);
+      const int ctas = lc(launch_dst_rows(a, stream), "launch_dst_rows");
+      ev_end();
+      check_launch();
+      return ctas;
+    }
+    Partials none{nullptr, 0};
+    const int gemm_epi = epi_spec == SPEC_AXPY ? EPI_AXPY : EPI_STORE;
+    pass(DBX_KIND_ARINV, true, X, xsel, u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, stp, none);
+    pass(DBX_KIND_ARINV, false, u.p, SEL_EXPLICIT, s.p, SEL_EXPLICIT, EPI_HADAMARD, nullptr, SEL_EXPLICIT, nullptr, 0, stp, none);
+    pass(DBX_KIND_AR, true, s.p, SEL_EXPLICIT, u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, stp, none);
+    return pass(DBX_KIND_AR, false, u.p, SEL_EXPLICIT, Y, ysel, gemm_epi, xold, xoldsel, ff, tau, stp, pt);
+  }
 };
 
 namespace {
@@ -349,7 +525,7 @@ extern "C" {
 
 const char* dbx_last_error(void) { return g_err.c_str(); }
 
-const char* dbx_version(void) { return "dbx 0.1 sm_100a (FP64 AR stencil + dense AR transform)"; }
+const char* dbx_version(void) { return "dbx 0.2 sm_100a (FP64 AR stencil / FFT correlation + Bluestein DST-I AR transform)"; }
 
 int dbx_device_count(void) {
   int n = 0;
@@ -413,7 +589,7 @@ int dbx_plan_create(int n1, int n2, int batch, const double* taps, int q1, int q
     P->sym = P->upload(s);
     ck(cudaMalloc(&P->st, sizeof(ImgState) * (size_t)batch), "cudaMalloc");
     // partial-sum capacity = CTAs per image of the finest launch grid (blur)
-    P->part_cap = ((n2 + 63) / 64) * ((n1 + 31) / 32);
+    P->part_cap = std::max(((n2 + 63) / 64) * ((n1 + 31) / 32), n1);
     *out = P.release();
   });
 }
@@ -433,6 +609,23 @@ int dbx_plan_set_conv(dbx_plan* plan, int conv) {
     require(conv == DBX_CONV_AUTO || conv == DBX_CONV_DIRECT || conv == DBX_CONV_FFT,
             "dbx_plan_set_conv: unknown engine");
     plan->conv = conv;
+  });
+}
+
+int dbx_plan_set_dst(dbx_plan* plan, int engine) {
+  return guarded([&] {
+    require(plan != nullptr, "null plan");
+    require(engine == DBX_DST_AUTO || engine == DBX_DST_DENSE || engine == DBX_DST_FFT,
+            "dbx_plan_set_dst: unknown engine");
+    plan->dst = engine;
+  });
+}
+
+int dbx_plan_engines(dbx_plan* plan, int* conv, int* dst) {
+  return guarded([&] {
+    require(plan != nullptr, "null plan");
+    if (conv) *conv = plan->use_fft_conv() ? DBX_CONV_FFT : DBX_CONV_DIRECT;
+    if (dst) *dst = plan->use_fft_dst(false) ? DBX_DST_FFT : DBX_DST_DENSE;
   });
 }
 
@@ -534,12 +727,8 @@ int dbx_precond_apply(dbx_plan* P, const double* r, double* y) {
       P->out.ensure(cnt);
       yout = P->out.p;
     }
-    Partials none{nullptr, 0};
-    // T~ (columns, rows) with the Hadamard by d fused, then T (columns, rows)
-    P->pass(DBX_KIND_ARINV, true, rin, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
-    P->pass(DBX_KIND_ARINV, false, P->u.p, SEL_EXPLICIT, P->s.p, SEL_EXPLICIT, EPI_HADAMARD, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
-    P->pass(DBX_KIND_AR, true, P->s.p, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
-    P->pass(DBX_KIND_AR, false, P->u.p, SEL_EXPLICIT, yout, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
+    P->apply_D(rin, SEL_EXPLICIT, yout, SEL_EXPLICIT, SPEC_STORE, nullptr, SEL_EXPLICIT, nullptr, 0.0,
+               nullptr, Partials{nullptr, 0});
     stage_out(P, y, yout, cnt);
     ck(cudaStreamSynchronize(P->stream), "sync");
   });
@@ -562,8 +751,22 @@ int dbx_tensor_apply(dbx_plan* P, int kind, const double* x, double* y) {
       yout = P->out.p;
     }
     Partials none{nullptr, 0};
-    P->pass(kind, true, xin, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
-    P->pass(kind, false, P->u.p, SEL_EXPLICIT, yout, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
+    const bool sine = kind == DBX_KIND_SINEI;
+    if (P->use_fft_dst(sine)) {
+      // rows then columns (Kronecker order is immaterial; the reference runs
+      // columns first, transforms.hpp:183-190)
+      SpecArgs a = P->spec_base(nullptr, none);
+      a.blue1 = P->blue_tables(0, sine);
+      a.blue2 = P->blue_tables(1, sine);
+      a.in = xin; a.out = P->u.p; a.kind1 = kind; a.kind2 = -1; a.epi = SPEC_STORE;
+      P->ev_begin(KC_TRANSFORM); lc(launch_dst_rows(a, P->stream), "launch_dst_rows"); P->ev_end();
+      a.in = P->u.p; a.out = yout;
+      P->ev_begin(KC_TRANSFORM); lc(launch_dst_cols(a, P->stream), "launch_dst_cols"); P->ev_end();
+      P->check_launch();
+    } else {
+      P->pass(kind, true, xin, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
+      P->pass(kind, false, P->u.p, SEL_EXPLICIT, yout, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, nullptr, none);
+    }
     stage_out(P, y, yout, cnt);
     ck(cudaStreamSynchronize(P->stream), "sync");
   });
@@ -620,11 +823,8 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
       if (use_precond) {
         P->blur(P->r.p, SEL_EXPLICIT, P->s.p, SEL_EXPLICIT, true, BLUR_STORE, nullptr, nullptr,
                 SEL_EXPLICIT, nullptr, 0.0, P->st, pt, KC_BLUR_ADJ);
-        P->pass(DBX_KIND_ARINV, true, P->s.p, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, P->st, pt);
-        P->pass(DBX_KIND_ARINV, false, P->u.p, SEL_EXPLICIT, P->s.p, SEL_EXPLICIT, EPI_HADAMARD, nullptr, SEL_EXPLICIT, nullptr, 0, P->st, pt);
-        P->pass(DBX_KIND_AR, true, P->s.p, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, P->st, pt);
-        cnt_x = P->pass(DBX_KIND_AR, false, P->u.p, SEL_EXPLICIT, P->X3.p, SEL_NXT, EPI_AXPY,
-                        P->X3.p, SEL_CUR, fd, tau, P->st, pt);
+        cnt_x = P->apply_D(P->s.p, SEL_EXPLICIT, P->X3.p, SEL_NXT, SPEC_AXPY, P->X3.p, SEL_CUR, fd, tau,
+                           P->st, pt);
       } else {
         cnt_x = P->blur(P->r.p, SEL_EXPLICIT, P->X3.p, SEL_NXT, true, BLUR_AXPY, nullptr, P->X3.p,
                         SEL_CUR, fd, tau, P->st, pt, KC_BLUR_ADJ);
@@ -645,18 +845,15 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
       }
     };
 
-    if (use_precond) {
-      // dense matrices are uploaded before capture (no allocation inside a graph)
-      P->matrix(DBX_KIND_ARINV, 0); P->matrix(DBX_KIND_ARINV, 1);
-      P->matrix(DBX_KIND_AR, 0); P->matrix(DBX_KIND_AR, 1);
-    }
+    // tables / matrices are uploaded before capture (no allocation inside a graph)
+    P->prepare(use_precond != 0);
     if (total > 0) {
       // Graph path: one graph per run shape, replayed; kernels read the run's
       // buffers through stable plan-owned pointers.
       char key[512];
-      snprintf(key, sizeof key, "%d|%d|%d|%.17g|%.17g|%d|%d|%p|%p|%d", total, use_precond,
+      snprintf(key, sizeof key, "%d|%d|%d|%.17g|%.17g|%d|%d|%p|%p|%d|%d", total, use_precond,
                stop_kind, resid_eps, tau, (int)track, (int)want_xh, (const void*)gd,
-               (const void*)fd, P->conv);
+               (const void*)fd, P->conv, P->dst);
       const bool use_graph = !P->timing;
       if (use_graph) {
         if (!P->gexec || P->gkey != key) {

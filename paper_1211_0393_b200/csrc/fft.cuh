@@ -1,0 +1,495 @@
+// fft.cuh — batched FP64 complex FFT of compile-time length L in shared memory.
+//
+// Stockham autosort, mixed radix {8, 4, 2, 3, 5}: every stage loads the
+// thread's butterflies into registers, synchronises, applies the stage
+// twiddles W_{Ns R}^{r k} (from a forward twiddle table W_L^e, e < L, built on
+// the host in long double with exact integer argument reduction), runs the
+// radix-R DFT in registers and stores in place.  Each line owns a padded smem
+// buffer (index i -> i + i/8) so that the stride-R stores of the first stage
+// do not serialise on one bank group.  T threads cooperate on one line; a CTA
+// runs several lines in lock-step (every thread calls every stage, so the
+// __syncthreads() inside are CTA-uniform).
+//
+// This engine stands in for FFTW (reference transforms.hpp:39-82, blur.hpp:56-68):
+// it carries the FFT-correlation blur and the Bluestein DST-I of the AR
+// transform on the GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "dft_consts.h"
+
+namespace dbx {
+namespace fft {
+
+// Even lengths (power-of-two radices) pad one element per 8 so stride-8
+// accesses spread over the banks; odd lengths (odd strides) are conflict-free
+// unpadded, which keeps a butterfly's addresses base + immediate.
+template <int L>
+__host__ __device__ constexpr int pad(int i) { return (L & 1) ? i : i + (i >> 3); }
+__host__ __device__ constexpr int padded_len(int L) { return (L & 1) ? L + 1 : L + (L >> 3) + 1; }
+
+// threads per line: one radix-8 butterfly per thread, rounded to a warp
+__host__ __device__ constexpr int threads_for(int L) {
+  int t = (L / 8 + 31) / 32 * 32;
+  return t < 32 ? 32 : (t > 512 ? 512 : t);
+}
+
+// Power-of-two factors first (8, 4, 2), then the LARGEST odd prime <= 31: the
+// first stage (Ns = 1) needs no twiddles, so it takes the most expensive radix.
+__host__ __device__ constexpr int next_radix(int rem) {
+  if (rem % 8 == 0) return 8;
+  if (rem % 4 == 0) return 4;
+  if (rem % 2 == 0) return 2;
+  constexpr int primes[10] = {31, 29, 23, 19, 17, 13, 11, 7, 5, 3};
+  for (int i = 0; i < 10; ++i)
+    if (rem % primes[i] == 0) return primes[i];
+  return 0;
+}
+
+__host__ __device__ constexpr bool supported(int L) {
+  if (L < 2) return false;
+  while (L > 1) {
+    const int r = next_radix(L);
+    if (r == 0) return false;
+    L /= r;
+  }
+  return true;
+}
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// v * (S*i)
+template <int S>
+__device__ __forceinline__ double2 mul_si(double2 v) {
+  return S < 0 ? make_double2(v.y, -v.x) : make_double2(-v.y, v.x);
+}
+
+template <int S>
+__device__ __forceinline__ void dft2(double2* v) {
+  const double2 a = v[0];
+  v[0] = cadd(a, v[1]);
+  v[1] = csub(a, v[1]);
+}
+
+template <int S>
+__device__ __forceinline__ void dft4(double2& x0, double2& x1, double2& x2, double2& x3) {
+  const double2 t0 = cadd(x0, x2), t1 = csub(x0, x2), t2 = cadd(x1, x3);
+  const double2 t3 = mul_si<S>(csub(x1, x3));
+  x0 = cadd(t0, t2);
+  x2 = csub(t0, t2);
+  x1 = cadd(t1, t3);
+  x3 = csub(t1, t3);
+}
+
+template <int S>
+__device__ __forceinline__ void dft8(double2* v) {
+  constexpr double h = 0.70710678118654752440084436210484904;
+  double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  dft4<S>(e0, e1, e2, e3);
+  dft4<S>(o0, o1, o2, o3);
+  // W8^1 = h(1 + S i), W8^2 = S i, W8^3 = h(-1 + S i)
+  const double2 w1 = make_double2(h * (o1.x - S * o1.y), h * (o1.y + S * o1.x));
+  const double2 w2 = mul_si<S>(o2);
+  const double2 w3 = make_double2(h * (-o3.x - S * o3.y), h * (-o3.y + S * o3.x));
+  v[0] = cadd(e0, o0);
+  v[4] = csub(e0, o0);
+  v[1] = cadd(e1, w1);
+  v[5] = csub(e1, w1);
+  v[2] = cadd(e2, w2);
+  v[6] = csub(e2, w2);
+  v[3] = cadd(e3, w3);
+  v[7] = csub(e3, w3);
+}
+
+template <int S>
+__device__ __forceinline__ void dft3(double2* v) {
+  constexpr double c = 0.86602540378443864676372317075293618;  // sqrt(3)/2
+  const double2 t = cadd(v[1], v[2]);
+  const double2 u = mul_si<S>(cscale(csub(v[1], v[2]), c));
+  const double2 m = make_double2(v[0].x - 0.5 * t.x, v[0].y - 0.5 * t.y);
+  v[0] = cadd(v[0], t);
+  v[1] = cadd(m, u);
+  v[2] = csub(m, u);
+}
+
+template <int S>
+__device__ __forceinline__ void dft5(double2* v) {
+  constexpr double c1 = 0.30901699437494742410229341718281906;    // cos(2pi/5)
+  constexpr double c2 = -0.80901699437494742410229341718281906;   // cos(4pi/5)
+  constexpr double s1 = 0.95105651629515357211643933337938214;    // sin(2pi/5)
+  constexpr double s2 = 0.58778525229247312916870595463907277;    // sin(4pi/5)
+  const double2 a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
+  const double2 a2 = cadd(v[2], v[3]), b2 = csub(v[2], v[3]);
+  const double2 x0 = v[0];
+  const double2 m1 = make_double2(x0.x + c1 * a1.x + c2 * a2.x, x0.y + c1 * a1.y + c2 * a2.y);
+  const double2 m2 = make_double2(x0.x + c2 * a1.x + c1 * a2.x, x0.y + c2 * a1.y + c1 * a2.y);
+  const double2 n1 = mul_si<S>(make_double2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y));
+  const double2 n2 = mul_si<S>(make_double2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y));
+  v[0] = cadd(x0, cadd(a1, a2));
+  v[1] = cadd(m1, n1);
+  v[4] = csub(m1, n1);
+  v[2] = cadd(m2, n2);
+  v[3] = csub(m2, n2);
+}
+
+// Odd prime P >= 7 via the (P-1)/2 symmetric pairs:
+//   X_k = x0 + sum_j c_jk a_j + S i sum_j s_jk b_j,  X_{P-k} = same with -S i,
+//   a_j = x_j + x_{P-j}, b_j = x_j - x_{P-j}; ~2P real FMAs per element instead
+//   of 4P for the plain matrix form.  Constants are compile-time (dft_consts.h).
+template <int P, int S>
+__device__ __forceinline__ void dft_odd(double2* v) {
+  constexpr int H = (P - 1) / 2;
+  using K = OddConst<P>;
+  double2 a[H], b[H];
+  const double2 x0 = v[0];
+  double2 sum = x0;
+#pragma unroll
+  for (int j = 1; j <= H; ++j) {
+    a[j - 1] = cadd(v[j], v[P - j]);
+    b[j - 1] = csub(v[j], v[P - j]);
+    sum = cadd(sum, a[j - 1]);
+  }
+  v[0] = sum;
+#pragma unroll
+  for (int k = 1; k <= H; ++k) {
+    double2 A = x0, B = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 1; j <= H; ++j) {
+      const int e = (j * k) % P;
+      A.x = fma(K::c(e), a[j - 1].x, A.x);
+      A.y = fma(K::c(e), a[j - 1].y, A.y);
+      B.x = fma(K::s(e), b[j - 1].x, B.x);
+      B.y = fma(K::s(e), b[j - 1].y, B.y);
+    }
+    const double2 sb = mul_si<S>(B);
+    v[k] = cadd(A, sb);
+    v[P - k] = csub(A, sb);
+  }
+}
+
+// Same transform, register-lean: the symmetric pairs overwrite the inputs in
+// place (v[j] <- a_j, v[P-j] <- b_j) and every output pair is stored to the
+// padded smem line as soon as it is formed (2P + 6 live doubles, not 4P).
+template <int P, int S, int L>
+__device__ __forceinline__ void dft_odd_store(double2* v, double2* buf, int base, int Ns) {
+  constexpr int H = (P - 1) / 2;
+  using K = OddConst<P>;
+  const double2 x0 = v[0];
+  double2 sum = x0;
+#pragma unroll
+  for (int j = 1; j <= H; ++j) {
+    const double2 a = cadd(v[j], v[P - j]);
+    const double2 b = csub(v[j], v[P - j]);
+    v[j] = a;
+    v[P - j] = b;
+    sum = cadd(sum, a);
+  }
+  buf[pad<L>(base)] = sum;
+#pragma unroll
+  for (int k = 1; k <= H; ++k) {
+    double2 A = x0, B = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 1; j <= H; ++j) {
+      const int e = (j * k) % P;
+      A.x = fma(K::c(e), v[j].x, A.x);
+      A.y = fma(K::c(e), v[j].y, A.y);
+      B.x = fma(K::s(e), v[P - j].x, B.x);
+      B.y = fma(K::s(e), v[P - j].y, B.y);
+    }
+    const double2 sb = mul_si<S>(B);
+    buf[pad<L>(base + k * Ns)] = cadd(A, sb);
+    buf[pad<L>(base + (P - k) * Ns)] = csub(A, sb);
+  }
+}
+
+template <int R, int S>
+__device__ __forceinline__ void dft(double2* v) {
+  if constexpr (R == 2) dft2<S>(v);
+  else if constexpr (R == 4) dft4<S>(v[0], v[1], v[2], v[3]);
+  else if constexpr (R == 8) dft8<S>(v);
+  else if constexpr (R == 3) dft3<S>(v);
+  else if constexpr (R == 5) dft5<S>(v);
+  else dft_odd<R, S>(v);
+}
+
+// One Stockham stage on a padded in-smem line.
+template <int L, int Ns, int R, int S, int T>
+__device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ tw, int t) {
+  constexpr int NB = L / R;
+  constexpr int PER = (NB + T - 1) / T;
+  constexpr int NW = Ns > 1 ? R - 1 : 1;
+  double2 v[PER][R];
+  double2 w[PER][NW];
+  // twiddles first: their (L1/L2) latency overlaps the smem loads and barrier
+  if constexpr (Ns > 1) {
+    constexpr int step = L / (Ns * R);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int b = t + i * T;
+      if (NB % T == 0 || b < NB) {
+        const int k = b % Ns;
+#pragma unroll
+        for (int r = 1; r < R; ++r) w[i][r - 1] = tw[r * k * step];  // smem- or global-resident table
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int b = t + i * T;
+    if (NB % T == 0 || b < NB) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[i][r] = buf[pad<L>(b + r * NB)];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int b = t + i * T;
+    if (NB % T == 0 || b < NB) {
+      const int k = b % Ns;
+      if constexpr (Ns > 1) {
+#pragma unroll
+        for (int r = 1; r < R; ++r)
+          v[i][r] = S < 0 ? cmul(v[i][r], w[i][r - 1]) : cmulc(v[i][r], w[i][r - 1]);
+      }
+      const int base = (b / Ns) * Ns * R + k;
+      if constexpr (R >= 7 && (R & 1)) {
+        dft_odd_store<R, S, L>(v[i], buf, base, Ns);
+      } else {
+        dft<R, S>(v[i]);
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[pad<L>(base + r * Ns)] = v[i][r];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Output pairs k = H0+1 .. H1 of an odd-prime butterfly whose symmetric pairs
+// are already in v (v[j] = a_j, v[P-j] = b_j); H0/H1 compile-time so every
+// constant is a fixed c[bank][offset] operand.
+template <int P, int S, int H0, int H1, int L>
+__device__ __forceinline__ void odd_part(const double2* v, double2 x0, double2* buf, int base, int Ns) {
+  using K = OddConst<P>;
+  constexpr int H = (P - 1) / 2;
+#pragma unroll
+  for (int k = H0 + 1; k <= H1; ++k) {
+    double2 A = x0, B = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 1; j <= H; ++j) {
+      const int e = (j * k) % P;
+      A.x = fma(K::c(e), v[j].x, A.x);
+      A.y = fma(K::c(e), v[j].y, A.y);
+      B.x = fma(K::s(e), v[P - j].x, B.x);
+      B.y = fma(K::s(e), v[P - j].y, B.y);
+    }
+    const double2 sb = mul_si<S>(B);
+    buf[pad<L>(base + k * Ns)] = cadd(A, sb);
+    buf[pad<L>(base + (P - k) * Ns)] = csub(A, sb);
+  }
+}
+
+// Stockham stage for a large odd prime R (>= 17): every butterfly is shared by
+// two warp-uniform halves (slot = half * NBp + b, NBp = NB rounded to warps),
+// each computing half of the (R-1)/2 output pairs.  This halves the live
+// accumulators (the full butterfly needs ~234 registers) and doubles the
+// number of busy threads in the stage (NB = L/R is small).
+template <int L, int Ns, int R, int S, int T>
+__device__ __forceinline__ void stage_split(double2* buf, const double2* __restrict__ tw, int t) {
+  constexpr int NB = L / R;
+  constexpr int NBp = (NB + 31) / 32 * 32;
+  constexpr int SLOTS = 2 * NBp;
+  constexpr int PER = (SLOTS + T - 1) / T;
+  constexpr int H = (R - 1) / 2;
+  static_assert(PER == 1, "split stage expects one slot per thread");
+  const int half = t / NBp;           // warp-uniform
+  const int b = t - half * NBp;
+  const bool act = t < SLOTS && b < NB;
+  double2 v[R];
+  double2 w[Ns > 1 ? R - 1 : 1];
+  const int k = act ? b % Ns : 0;
+  if constexpr (Ns > 1) {
+    constexpr int step = L / (Ns * R);
+    if (act) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) w[r - 1] = tw[r * k * step];  // smem- or global-resident table
+    }
+  }
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = buf[pad<L>(b + r * NB)];
+  }
+  __syncthreads();
+  if (act) {
+    if constexpr (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = S < 0 ? cmul(v[r], w[r - 1]) : cmulc(v[r], w[r - 1]);
+    }
+    const double2 x0 = v[0];
+    double2 sum = x0;
+#pragma unroll
+    for (int j = 1; j <= H; ++j) {
+      const double2 a = cadd(v[j], v[R - j]);
+      const double2 c = csub(v[j], v[R - j]);
+      v[j] = a;
+      v[R - j] = c;
+      sum = cadd(sum, a);
+    }
+    const int base = (b / Ns) * Ns * R + k;
+    if (half == 0) buf[pad<L>(base)] = sum;
+    // rolled loop over this half's output pairs: the pair index kk is
+    // warp-uniform, so the constant-table reads go through the uniform
+    // datapath (ULDC -> DFMA UR operand) and only one pair's accumulators live
+    const int k0 = half == 0 ? 1 : H / 2 + 1, k1 = half == 0 ? H / 2 : H;
+    using K = OddConst<R>;
+#pragma unroll 1
+    for (int kk = k0; kk <= k1; ++kk) {
+      double2 A = x0, B = make_double2(0.0, 0.0);
+      int e = 0;
+#pragma unroll
+      for (int j = 1; j <= H; ++j) {
+        e += kk;
+        if (e >= R) e -= R;
+        const double c = K::c(e), s = K::s(e);
+        A.x = fma(c, v[j].x, A.x);
+        A.y = fma(c, v[j].y, A.y);
+        B.x = fma(s, v[R - j].x, B.x);
+        B.y = fma(s, v[R - j].y, B.y);
+      }
+      const double2 sb = mul_si<S>(B);
+      buf[pad<L>(base + kk * Ns)] = cadd(A, sb);
+      buf[pad<L>(base + (R - kk) * Ns)] = csub(A, sb);
+    }
+  }
+  __syncthreads();
+}
+
+// CTA-wide stage for a large odd prime R (>= 17) on G lines at once: the
+// G * NB butterflies (NB = L/R is small, e.g. 33 for 1023 = 31*33) are packed
+// densely over the CTA's threads (slot -> line, butterfly), so few warps are
+// busy and those are full.  The output-pair loop is rolled with a CTA-uniform
+// counter: the cos/sin table reads become uniform-datapath loads feeding DFMA
+// directly, and only one pair of accumulators is live (~70 registers instead
+// of ~230 for the fully unrolled butterfly).
+template <int L, int Ns, int R, int S, int G, int PL>
+__device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __restrict__ tw, int tid, int nthreads) {
+  constexpr int NB = L / R;
+  constexpr int H = (R - 1) / 2;
+  using K = OddConst<R>;
+  const bool act = tid < G * NB;
+  const int line = act ? tid / NB : 0;
+  const int b = act ? tid - line * NB : 0;
+  double2* buf = sm + line * PL;
+  double2 v[R];
+  double2 w[Ns > 1 ? R - 1 : 1];
+  const int k = b % Ns;
+  if constexpr (Ns > 1) {
+    constexpr int step = L / (Ns * R);
+    if (act) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) w[r - 1] = tw[r * k * step];  // smem- or global-resident table
+    }
+  }
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = buf[pad<L>(b + r * NB)];
+  }
+  __syncthreads();
+  if (act) {
+    if constexpr (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = S < 0 ? cmul(v[r], w[r - 1]) : cmulc(v[r], w[r - 1]);
+    }
+    const double2 x0 = v[0];
+    double2 sum = x0;
+#pragma unroll
+    for (int j = 1; j <= H; ++j) {
+      const double2 a = cadd(v[j], v[R - j]);
+      const double2 c = csub(v[j], v[R - j]);
+      v[j] = a;
+      v[R - j] = c;
+      sum = cadd(sum, a);
+    }
+    const int base = (b / Ns) * Ns * R + k;
+    buf[pad<L>(base)] = sum;
+#pragma unroll 1
+    for (int kk = 1; kk <= H; ++kk) {
+      double2 A = x0, B = make_double2(0.0, 0.0);
+      int e = 0;
+#pragma unroll
+      for (int j = 1; j <= H; ++j) {
+        e += kk;
+        if (e >= R) e -= R;
+        const double c = K::c(e), s = K::s(e);
+        A.x = fma(c, v[j].x, A.x);
+        A.y = fma(c, v[j].y, A.y);
+        B.x = fma(s, v[R - j].x, B.x);
+        B.y = fma(s, v[R - j].y, B.y);
+      }
+      const double2 sb = mul_si<S>(B);
+      buf[pad<L>(base + kk * Ns)] = cadd(A, sb);
+      buf[pad<L>(base + (R - kk) * Ns)] = csub(A, sb);
+    }
+  }
+  (void)nthreads;
+  __syncthreads();
+}
+
+template <int L, int Ns, int S, int T>
+__device__ __forceinline__ void run_stages(double2* buf, const double2* __restrict__ tw, int t) {
+  if constexpr (Ns < L) {
+    constexpr int R = next_radix(L / Ns);
+    static_assert(R != 0, "FFT length must factor into {2,3,4,5,8} and odd primes <= 31");
+    constexpr int NBp = (L / R + 31) / 32 * 32;
+    if constexpr (R >= 17 && (R & 1) && 2 * NBp <= T)
+      stage_split<L, Ns, R, S, T>(buf, tw, t);
+    else
+      stage<L, Ns, R, S, T>(buf, tw, t);
+    run_stages<L, Ns * R, S, T>(buf, tw, t);
+  }
+}
+
+// CTA-wide variant: G lines of PL (padded) elements starting at sm, T threads
+// per line; thread tid = g*T + t.  Large odd-prime stages run packed across
+// the lines (stage_odd_cta), the rest per line.
+template <int L, int Ns, int S, int T, int G, int PL>
+__device__ __forceinline__ void run_stages_cta(double2* sm, const double2* __restrict__ tw, int tid) {
+  if constexpr (Ns < L) {
+    constexpr int R = next_radix(L / Ns);
+    static_assert(R != 0, "FFT length must factor into {2,3,4,5,8} and odd primes <= 31");
+    if constexpr (R >= 17 && (R & 1) && G * (L / R) <= G * T) {
+      stage_odd_cta<L, Ns, R, S, G, PL>(sm, tw, tid, G * T);
+    } else {
+      const int g = tid / T;
+      stage<L, Ns, R, S, T>(sm + g * PL, tw, tid - g * T);
+    }
+    run_stages_cta<L, Ns * R, S, T, G, PL>(sm, tw, tid);
+  }
+}
+
+template <int L, int S, int T, int G>
+__device__ __forceinline__ void fft_cta(double2* sm, const double2* __restrict__ tw, int tid) {
+  static_assert(supported(L), "unsupported FFT length");
+  run_stages_cta<L, 1, S, T, G, padded_len(L)>(sm, tw, tid);
+}
+
+// In-place unnormalised FFT of one padded line; S = -1 forward, +1 inverse.
+// Every thread of the CTA must call it (contains __syncthreads()).
+template <int L, int S, int T>
+__device__ __forceinline__ void fft(double2* buf, const double2* __restrict__ tw, int t) {
+  static_assert(supported(L), "unsupported FFT length");
+  run_stages<L, 1, S, T>(buf, tw, t);
+}
+
+}  // namespace fft
+}  // namespace dbx

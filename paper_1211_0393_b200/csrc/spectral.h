@@ -1,0 +1,71 @@
+// spectral.h — argument blocks and launchers of the FFT-form kernels
+// (spectral.cu): FFT-correlation blur and Bluestein DST-I / AR transforms.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../../include/dbx.h"
+#include "dbx_internal.h"
+
+namespace dbx {
+
+enum SpecEpi { SPEC_STORE = 0, SPEC_HADAMARD = 1, SPEC_RESID = 2, SPEC_AXPY = 3 };
+
+// FFT-correlation tables (device): twiddles W_L^e for L1/L2 and the kernel
+// spectrum H[k2][k1] = conj(FFT2(w))[k1][k2] / (L1 L2), k2 < Lh = L2/2 + 1.
+struct ConvTables {
+  const double2* tw1 = nullptr;
+  const double2* tw2 = nullptr;
+  const double2* H = nullptr;
+  int L1 = 0, L2 = 0, Lh = 0;
+};
+
+// Bluestein DST-I tables for one line length n (device): M-point twiddles,
+// chirp w_j = exp(-i pi j^2 / N) (j < N), kernel spectrum FFT_M(conj chirp)/M,
+// the AR ramp p_j = 1 - j/(n-1) and alpha_n (transforms.hpp:135-144).
+struct BlueTables {
+  const double2* tw = nullptr;
+  const double2* chirp = nullptr;
+  const double2* bhat = nullptr;
+  const double* p = nullptr;
+  double alpha = 1.0;
+  double scale = 1.0;  // sqrt(2/N)
+  int n = 0, N = 0, M = 0;
+};
+
+struct SpecArgs {
+  const double* in = nullptr; int insel = SEL_EXPLICIT;
+  double* out = nullptr; int outsel = SEL_EXPLICIT;
+  int n1 = 0, n2 = 0, q1 = 0, q2 = 0, batch = 0;
+  int epi = SPEC_STORE;
+  const double* g = nullptr;                     // RESID
+  const double* xold = nullptr; int xoldsel = SEL_EXPLICIT;  // AXPY
+  const double* f = nullptr;                     // AXPY (nullable)
+  const double* d = nullptr;                     // HADAMARD / dst_cols middle
+  double tau = 0.0;
+  const ImgState* st = nullptr;
+  Partials part{nullptr, 0};
+  // FFT correlation
+  ConvTables conv;
+  double2* zbuf = nullptr;                       // [batch][n1][Lh]
+  double2* ybuf = nullptr;                       // [batch][n1][Lh]
+  // DST
+  int kind1 = DBX_KIND_ARINV, kind2 = -1;
+  BlueTables blue1;                              // columns (length n1)
+  BlueTables blue2;                              // rows (length n2)
+};
+
+int conv_supported_len(int need);   // smallest compiled L >= need, 0 if none
+int blue_supported_len(int need);   // smallest compiled power of two M >= need, 0 if none
+int conv_rows_per_cta(int L2);
+int direct_supported_len(int N);  // N if the direct odd-length DFT is compiled, else 0
+
+// Each returns the number of CTAs per image (for the partial-sum count), -1 if
+// the size is not compiled.
+int launch_conv_row_fwd(const SpecArgs& a, cudaStream_t s);
+int launch_conv_col(const SpecArgs& a, cudaStream_t s);
+int launch_conv_row_inv(const SpecArgs& a, cudaStream_t s);
+int launch_dst_rows(const SpecArgs& a, cudaStream_t s);
+int launch_dst_cols(const SpecArgs& a, cudaStream_t s);
+
+}  // namespace dbx

@@ -1,0 +1,148 @@
+// tables.cpp — host-side precomputation for the FFT-form kernels (plan setup,
+// not on the timed path).  All angles use exact integer argument reduction and
+// long double evaluation, so every table entry is the correctly rounded double
+// (naive sin(s t pi/(m+1)) arguments would burn ~1e-13 of the
+// parity budget at the config lengths).
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <thread>
+#include <vector>
+
+#include "tables.h"
+
+namespace dbx {
+namespace {
+constexpr long double kPiL = 3.141592653589793238462643383279502884L;
+
+inline void put(double* out, long i, long double re, long double im) {
+  out[2 * i] = (double)re;
+  out[2 * i + 1] = (double)im;
+}
+
+template <typename F>
+void parallel_for(long n, F f) {
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt == 0) nt = 1;
+  if (nt > 32) nt = 32;
+  if (n < 64 || nt == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t) th.emplace_back(f, n * t / nt, n * (t + 1) / nt);
+  for (auto& x : th) x.join();
+}
+}  // namespace
+
+std::vector<double> twiddles(int L) {
+  std::vector<double> tw(2 * (size_t)L);
+  for (long e = 0; e < L; ++e) {
+    const long double a = 2.0L * kPiL * (long double)e / (long double)L;
+    put(tw.data(), e, cosl(a), -sinl(a));
+  }
+  return tw;
+}
+
+// H[k2][k1] = conj(sum_{t,u} w(t,u) exp(-2 pi i (k1 t / L1 + k2 u / L2))) / (L1 L2)
+// (stored k2-major so a column pass reads its spectrum column contiguously)
+std::vector<double> conv_spectrum(const double* w, int q1, int q2, int L1, int L2) {
+  const int Lh = L2 / 2 + 1, H1 = 2 * q1 + 1, W2 = 2 * q2 + 1;
+  std::vector<std::complex<long double>> e1((size_t)L1), e2((size_t)L2);
+  for (long e = 0; e < L1; ++e) {
+    const long double a = 2.0L * kPiL * (long double)e / (long double)L1;
+    e1[(size_t)e] = {cosl(a), -sinl(a)};
+  }
+  for (long e = 0; e < L2; ++e) {
+    const long double a = 2.0L * kPiL * (long double)e / (long double)L2;
+    e2[(size_t)e] = {cosl(a), -sinl(a)};
+  }
+  // V(t, k2) = sum_u w(t,u) e2[k2 u]
+  std::vector<std::complex<long double>> V((size_t)H1 * Lh);
+  for (int t = 0; t < H1; ++t)
+    for (int k2 = 0; k2 < Lh; ++k2) {
+      std::complex<long double> acc = 0;
+      for (int u = 0; u < W2; ++u) acc += (long double)w[t * W2 + u] * e2[(size_t)(((long)k2 * u) % L2)];
+      V[(size_t)t * Lh + k2] = acc;
+    }
+  std::vector<double> H(2 * (size_t)L1 * Lh);
+  const long double s = 1.0L / ((long double)L1 * (long double)L2);
+  parallel_for(L1, [&](long b, long e) {
+    for (long k1 = b; k1 < e; ++k1)
+      for (int k2 = 0; k2 < Lh; ++k2) {
+        std::complex<long double> acc = 0;
+        for (int t = 0; t < H1; ++t) acc += e1[(size_t)((k1 * t) % L1)] * V[(size_t)t * Lh + k2];
+        put(H.data(), (long)k2 * L1 + k1, acc.real() * s, -acc.imag() * s);  // [k2][k1]
+      }
+  });
+  return H;
+}
+
+void blue_chirp(BlueHost& b, long N, int M);
+void ar_ramp(BlueHost& b, int n, bool sine_i);
+
+BlueHost bluestein(int n, bool sine_i, int M) {
+  BlueHost b;
+  b.n = n;
+  b.N = sine_i ? n + 1 : n - 1;
+  b.M = M;
+  const long N = b.N;
+  b.scale = (double)sqrtl(2.0L / (long double)N);
+  b.tw = twiddles(M);
+  if (M == N) {  // direct odd-length DFT: no chirp / kernel spectrum
+    b.chirp.assign(2, 0.0);
+    b.bhat.assign(2, 0.0);
+  } else {
+    blue_chirp(b, N, M);
+  }
+  ar_ramp(b, n, sine_i);
+  return b;
+}
+
+void blue_chirp(BlueHost& b, long N, int M) {
+  b.chirp.assign(2 * (size_t)(N + 1), 0.0);
+  std::vector<std::complex<long double>> w((size_t)N + 1);
+  for (long j = 0; j <= N; ++j) {
+    const long e = (j * j) % (2 * N);  // exact reduction of pi j^2 / N
+    const long double a = kPiL * (long double)e / (long double)N;
+    w[(size_t)j] = {cosl(a), -sinl(a)};
+    put(b.chirp.data(), j, w[(size_t)j].real(), w[(size_t)j].imag());
+  }
+  // kernel c_t = conj(w_|t|) on t in (-N, N), wrapped mod M; bhat = FFT_M(c) / M
+  std::vector<std::complex<long double>> c((size_t)M, 0);
+  for (long t = 0; t < N; ++t) {
+    c[(size_t)t] = std::conj(w[(size_t)t]);
+    if (t) c[(size_t)(M - t)] = std::conj(w[(size_t)t]);
+  }
+  std::vector<std::complex<long double>> eM((size_t)M);
+  for (long e = 0; e < M; ++e) {
+    const long double a = 2.0L * kPiL * (long double)e / (long double)M;
+    eM[(size_t)e] = {cosl(a), -sinl(a)};
+  }
+  b.bhat.assign(2 * (size_t)M, 0.0);
+  parallel_for(M, [&](long kb, long ke) {
+    for (long k = kb; k < ke; ++k) {
+      std::complex<long double> acc = 0;
+      for (long t = 0; t < M; ++t)
+        if (c[(size_t)t] != std::complex<long double>(0)) acc += c[(size_t)t] * eM[(size_t)((k * t) % M)];
+      acc /= (long double)M;
+      put(b.bhat.data(), k, acc.real(), acc.imag());
+    }
+  });
+}
+
+// AR ramp (transforms.hpp:135-144), computed exactly as the reference does
+void ar_ramp(BlueHost& b, int n, bool sine_i) {
+  if (!sine_i) {
+    b.p.assign((size_t)(n - 2), 0.0);
+    double sq = 0.0;
+    for (long j = 1; j <= n - 2; ++j) b.p[(size_t)(j - 1)] = 1.0 - (double)j / (double)(n - 1);
+    for (double v : b.p) sq += v * v;
+    b.alpha = std::sqrt(1.0 + sq);
+  } else {
+    b.p.assign(1, 0.0);
+    b.alpha = 1.0;
+  }
+}
+
+}  // namespace dbx

@@ -1,0 +1,25 @@
+// tables.h — host-side precomputation for the FFT-form kernels.
+#pragma once
+
+#include <vector>
+
+namespace dbx {
+
+// W_L^e = exp(-2 pi i e / L), e < L, interleaved (re, im).
+std::vector<double> twiddles(int L);
+
+// Kernel spectrum of the correlation weights w ((2q1+1) x (2q2+1), row-major):
+// H[k2][k1] = conj(FFT2(w))[k1][k2] / (L1 L2), k1 < L1, k2 < L2/2 + 1 (k2-major).
+std::vector<double> conv_spectrum(const double* w, int q1, int q2, int L1, int L2);
+
+struct BlueHost {
+  int n = 0, N = 0, M = 0;
+  double alpha = 1.0, scale = 1.0;
+  std::vector<double> tw, chirp, bhat, p;
+};
+
+// Bluestein tables of the DST-I of one line: AR kinds (sine_i = false) use the
+// interior of length n-2 (N = n-1); the plain SineI kind uses N = n+1.
+BlueHost bluestein(int n, bool sine_i, int M);
+
+}  // namespace dbx

@@ -228,3 +228,54 @@ def test_full_size_properties(dev, name):
     assert rel(dev.apply(op, 2.0 * x - y), 2.0 * dev.apply(op, x) - dev.apply(op, y)) <= 1e-13
     ident = dev.filter_from_eigs(np.ones((n, n)))
     assert rel(dev.precondition_apply(ident, x), x) <= 1e-11
+
+
+# ---------------------------------------------------------------------------
+# engine coverage: FFT correlation vs direct stencil, Bluestein vs dense DST
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n1,n2,q1,q2", [(24, 30, 1, 9), (64, 64, 7, 7), (100, 70, 8, 3), (130, 67, 15, 2),
+                                         (200, 200, 31, 31), (37, 53, 3, 5), (5, 9, 1, 3)])
+def test_fft_conv_engine_matches_oracle(dev, oracle, n1, n2, q1, q2):
+    rng = np.random.default_rng(7 * n1 + n2 + q1)
+    t = rand_psf(rng, q1, q2)
+    f = rng.uniform(0, 1, (n1, n2))
+    op = dev.BlurOperator(dev.Psf(t), dev.BoundaryCondition.AntiReflective, n1, n2).set_conv(dev.ConvEngine.Fft)
+    assert op.engines()[0] == dev.ConvEngine.Fft
+    for adj in (False, True):
+        got = dev.apply_reblur_adjoint(op, f) if adj else dev.apply(op, f)
+        assert rel(got, oracle.apply(t, f, adjoint=adj, path=2)) <= OP_TOL
+        assert rel(got, oracle.apply(t, f, adjoint=adj, path=1)) <= OP_TOL
+
+
+@pytest.mark.parametrize("n1,n2", [(3, 3), (6, 7), (16, 16), (33, 20), (256, 256), (512, 300), (1024, 1024)])
+@pytest.mark.parametrize("engine", ["Fft", "Dense"])
+def test_dst_engines_match_oracle(dev, oracle, n1, n2, engine):
+    rng = np.random.default_rng(n1 + 3 * n2)
+    x = rng.uniform(-1, 1, (n1, n2))
+    eng = getattr(dev.DstEngine, engine)
+    for kind in (dev.TransformKind.SineI, dev.TransformKind.AntiReflective,
+                 dev.TransformKind.AntiReflectiveInverse):
+        got = dev.tensor_apply(kind, x, engine=eng)
+        assert rel(got, oracle.tensor_apply(int(kind), x)) <= OP_TOL, (kind, engine)
+    t = rand_psf(rng, 2, 1)
+    d = dev.build_tikhonov(dev.Psf(t), dev.PreconditionerSpec(dev.Algebra.AntiReflective, 0.02), n1, n2) \
+        if min(n1, n2) >= 5 else None
+    if d is not None:
+        r = rng.uniform(-1, 1, (n1, n2))
+        ref = oracle.precondition_apply(oracle.build_tikhonov(t, 0.02, n1, n2), r)
+        assert rel(dev.precondition_apply(d, r, engine=eng), ref) <= OP_TOL
+
+
+@pytest.mark.parametrize("conv,dst", [("Direct", "Dense"), ("Fft", "Fft"), ("Direct", "Fft"), ("Fft", "Dense")])
+def test_engine_combinations_same_trajectory(dev, oracle, conv, dst):
+    from paper_1211_0393_b200 import configs as cf
+    c = cf.CONFIGS["C3"]
+    n, iters = 96, 12
+    f, g, taps = cf.make_problem(c, n=n)
+    op = dev.BlurOperator(dev.Psf(taps), dev.BoundaryCondition.AntiReflective, n, n)
+    op.set_conv(getattr(dev.ConvEngine, conv)).set_dst(getattr(dev.DstEngine, dst))
+    d = dev.build_tikhonov(dev.Psf(taps), dev.PreconditionerSpec(dev.Algebra.AntiReflective, c.alpha), n, n)
+    run = dev.d_landweber(op, d, g, dev.SolverConfig(max_iters=iters, track_rre_against=f), keep_iterates=True)
+    ref = oracle.landweber(taps, g, d=oracle.build_tikhonov(taps, c.alpha, n, n), f_true=f, max_iters=iters,
+                           keep_iterates=True)
+    _trajectory_check(run, ref)
