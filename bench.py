@@ -269,27 +269,39 @@ def main():
                "h2d_bytes_per_step": int(2 * B * N * 8), "d2h_bytes_per_step": int(B * N * 8 + 2 * B * H * 8)}
 
     # ---- roofline of the dominant kernel class ----
+    from paper_1211_0393_b200 import workmodel as wm
     names = ["blur_adjoint(A')", "blur(A)+residual", "ar_transform_pass", "finalize"]
     dom = int(np.argmax(kms_tot))
     avg_ms = kms_tot[dom] / max(kcnt_tot[dom], 1)
     peaks = {}
     if os.path.exists(PEAKS_FILE):
         peaks = json.load(open(PEAKS_FILE))
-    stencil_flops = 2.0 * (2 * q + 1) ** 2 * N * B          # one blur launch, dense count
+    conv_e, dst_e = C.c_int(), C.c_int()
+    L.dbx_plan_engines(plan, C.byref(conv_e), C.byref(dst_e))
+    fft_conv, fft_dst = conv_e.value == 2, dst_e.value == 2
+    p_fp64 = peaks.get("dfma_tflops_sustained", 34.0)
+    per_launch_blur = (wm.conv_apply_flops(n, n, q, q) if fft_conv else wm.direct_apply_flops(n, n, q, q)) * B
     if dom == 2:
-        flops = 2.0 * n * n * n * B                       # one dense transform pass (GEMM form, 2 n^3 / image)
-        peak = peaks.get("dmma_tflops_sustained", 37.0)
-        psrc = "measured DMMA FP64 (profiles/r01_fp64_peak.json, sustained)"
+        # 4 transform passes per iteration spread over the class's launches
+        launches_per_it = 3 if fft_dst else 4
+        flops = (wm.transform_iteration_flops(n, n) if fft_dst else 8.0 * n * n * n) * B / launches_per_it
+        peak, psrc = (p_fp64, "measured DFMA FP64 sustained (profiles/r01_fp64_peak.json)") if fft_dst else \
+            (peaks.get("dmma_tflops_sustained", 37.0), "measured DMMA FP64 sustained (profiles/r01_fp64_peak.json)")
+        form = "FFT-form AR transform (direct odd-N DFT / Bluestein)" if fft_dst else "dense GEMM-form AR transform"
     else:
-        flops = stencil_flops
-        peak = peaks.get("dfma_tflops_sustained", 34.0)
-        psrc = "measured DFMA FP64 (profiles/r01_fp64_peak.json, sustained)"
+        flops = per_launch_blur
+        peak, psrc = p_fp64, "measured DFMA FP64 sustained (profiles/r01_fp64_peak.json)"
+        form = "FFT correlation (3 launches per apply)" if fft_conv else "direct AR stencil"
     achieved = flops / (avg_ms * 1e-3) / 1e12
-    roof = {"bound": "tensor" if dom == 2 else "fp64", "kernel": names[dom], "achieved": achieved,
-            "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-            "peak_source": psrc, "avg_launch_ms": avg_ms,
+    step_s = t_max * 1e-3 / args.steps
+    roof = {"bound": "tensor", "pipe": "FP64 (no tcgen05 FP64 kind on sm_100a; DFMA/DMMA)",
+            "kernel": names[dom], "form": form, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": None, "peak_source": psrc, "avg_launch_ms": avg_ms,
+            "algorithmic_flops_per_launch": flops,
             "share_of_step": float(kms_tot[dom] / max(kms_tot.sum(), 1e-9)),
-            "class_ms_per_step": {names[i]: float(kms_tot[i] / args.steps) for i in range(4)}}
+            "class_ms_per_step": {names[i]: float(kms_tot[i] / args.steps) for i in range(4)},
+            "canonical_step": wm.canonical(q, float(world * B * N * H) / world, step_s,
+                                           6544.7, p_fp64)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -237,14 +237,25 @@ conv_row_fwd(SpecArgs a) {
   const double* x = resolve_ptr(a.in, a.st, a.insel, b, a.batch, N);
   const int ra = (blockIdx.x * G + g) * 2, rb = ra + 1;
   const int wext = n2 + 2 * q2;
-  for (int p = t; p < L2; p += T) {
-    double va = 0.0, vb = 0.0;
+  // all of this thread's loads are issued before any smem store (one DRAM
+  // round trip per kernel instead of one per element)
+  constexpr int PF = (L2 + T - 1) / T;
+  double va[PF], vb[PF];
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int p = t + i * T;
+    va[i] = 0.0;
+    vb[i] = 0.0;
     if (p < wext) {
       const int j = p - q2;
-      if (ra < n1) va = hext(x, ra, j, n2);
-      if (rb < n1) vb = hext(x, rb, j, n2);
+      if (ra < n1) va[i] = hext(x, ra, j, n2);
+      if (rb < n1) vb[i] = hext(x, rb, j, n2);
     }
-    buf[pad<L2>(p)] = make_double2(va, vb);
+  }
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int p = t + i * T;
+    if (p < L2) buf[pad<L2>(p)] = make_double2(va[i], vb[i]);
   }
   cp_async_wait_all();
   __syncthreads();
@@ -282,22 +293,32 @@ conv_col(SpecArgs a) {
   const double2* Z = a.zbuf + (size_t)b * n1 * Lh;
   const int hext_rows = n1 + 2 * q1;
   // load the G columns with the vertical AR extension synthesised spectrally
-  for (int idx = threadIdx.x; idx < L1 * G; idx += NT) {
+  // (loads batched in registers first, then stored)
+  constexpr int PF = (L1 * G + NT - 1) / NT;
+  double2 v[PF];
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int idx = threadIdx.x + i * NT;
     const int p = idx / G, gg = idx - p * G, k = k0 + gg;
-    double2 v = make_double2(0.0, 0.0);
-    if (k < Lh && p < hext_rows) {
+    v[i] = make_double2(0.0, 0.0);
+    if (idx < L1 * G && k < Lh && p < hext_rows) {
       const int rho = p - q1;
       if (rho < 0) {
         const double2 z0 = Z[k], zi = Z[(size_t)(-rho) * Lh + k];
-        v = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
+        v[i] = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
       } else if (rho >= n1) {
         const double2 z0 = Z[(size_t)(n1 - 1) * Lh + k], zi = Z[(size_t)(2 * (n1 - 1) - rho) * Lh + k];
-        v = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
+        v[i] = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
       } else {
-        v = Z[(size_t)rho * Lh + k];
+        v[i] = Z[(size_t)rho * Lh + k];
       }
     }
-    sm[gg * padded_len(L1) + pad<L1>(p)] = v;
+  }
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int idx = threadIdx.x + i * NT;
+    const int p = idx / G, gg = idx - p * G;
+    if (idx < L1 * G) sm[gg * padded_len(L1) + pad<L1>(p)] = v[i];
   }
   cp_async_wait_group<1>();  // twiddles landed (H may still be in flight)
   __syncthreads();
@@ -349,17 +370,28 @@ conv_row_inv(SpecArgs a) {
     }
   }
   const double2* Y = a.ybuf + (size_t)b * n1 * Lh;
-  for (int k = t; k < L2; k += T) {
-    double2 A = make_double2(0.0, 0.0), B = A;
-    const bool lo = k < Lh;
-    const int kk = lo ? k : L2 - k;
-    if (ra < n1) A = Y[(size_t)ra * Lh + kk];
-    if (rb < n1) B = Y[(size_t)rb * Lh + kk];
-    if (!lo) {
-      A.y = -A.y;
-      B.y = -B.y;
+  // only the Lh stored spectra are read (the upper half is their conjugate);
+  // loads batched in registers before the smem stores
+  constexpr int PF = (L2 / 2 + 1 + T - 1) / T;
+  double2 A[PF], Bv[PF];
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int k = t + i * T;
+    A[i] = make_double2(0.0, 0.0);
+    Bv[i] = A[i];
+    if (k < Lh) {
+      if (ra < n1) A[i] = Y[(size_t)ra * Lh + k];
+      if (rb < n1) Bv[i] = Y[(size_t)rb * Lh + k];
     }
-    buf[pad<L2>(k)] = make_double2(A.x - B.y, A.y + B.x);
+  }
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int k = t + i * T;
+    if (k < Lh) {
+      // Z_k = A_k + i B_k and Z_{L2-k} = conj(A_k) + i conj(B_k)
+      buf[pad<L2>(k)] = make_double2(A[i].x - Bv[i].y, A[i].y + Bv[i].x);
+      if (k > 0 && k < L2 - k) buf[pad<L2>(L2 - k)] = make_double2(A[i].x + Bv[i].y, Bv[i].x - A[i].y);
+    }
   }
   cp_async_wait_all();
   __syncthreads();
@@ -389,13 +421,22 @@ __device__ __forceinline__ double2 pre(double2 z, const BlueTables& bt, int j) {
 template <int M, int T, bool BLUE, typename F>
 __device__ __forceinline__ void blue_fill(double2* buf, const BlueTables& bt, int t, F val) {
   const int N = bt.N;
-  for (int j = t; j < M; j += T) {
-    double2 v = make_double2(0.0, 0.0);
+  // every load of the thread (line values, chirp) is issued before any store
+  constexpr int PF = (M + T - 1) / T;
+  double2 v[PF];
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int j = t + i * T;
+    v[i] = make_double2(0.0, 0.0);
     if (j >= 1 && j < N) {
       const double z = val(j);
-      v = pre<BLUE>(make_double2(z, (j & 1) ? -z : z), bt, j);
+      v[i] = pre<BLUE>(make_double2(z, (j & 1) ? -z : z), bt, j);
     }
-    buf[pad<M>(j)] = v;
+  }
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int j = t + i * T;
+    if (j < M) buf[pad<M>(j)] = v[i];
   }
 }
 
@@ -565,18 +606,29 @@ dst_cols(SpecArgs a) {
   }
   __syncthreads();
   const int kind1 = a.kind1, kind2 = a.kind2;
-  for (int idx = threadIdx.x; idx < M * G; idx += NT) {
-    const int j = idx / G, gg = idx - j * G, cc = c0 + gg;
-    double2 v = make_double2(0.0, 0.0);
-    if (j >= 1 && j < NL && cc < n2) {
-      double z;
-      if (kind1 == DBX_KIND_SINEI) z = in[(size_t)(j - 1) * n2 + cc];
-      else if (kind1 == DBX_KIND_ARINV)
-        z = (in[(size_t)j * n2 + cc] - vb0[gg] * __ldg(p + j - 1)) - vbe[gg] * __ldg(p + n - 2 - j);
-      else z = in[(size_t)j * n2 + cc];
-      v = pre<BLUE>(make_double2(z, (j & 1) ? -z : z), bt, j);
+  {
+    constexpr int PF = (M * G + NT - 1) / NT;
+    double2 v[PF];
+#pragma unroll
+    for (int i = 0; i < PF; ++i) {
+      const int idx = threadIdx.x + i * NT;
+      const int j = idx / G, gg = idx - j * G, cc = c0 + gg;
+      v[i] = make_double2(0.0, 0.0);
+      if (idx < M * G && j >= 1 && j < NL && cc < n2) {
+        double z;
+        if (kind1 == DBX_KIND_SINEI) z = in[(size_t)(j - 1) * n2 + cc];
+        else if (kind1 == DBX_KIND_ARINV)
+          z = (in[(size_t)j * n2 + cc] - vb0[gg] * __ldg(p + j - 1)) - vbe[gg] * __ldg(p + n - 2 - j);
+        else z = in[(size_t)j * n2 + cc];
+        v[i] = pre<BLUE>(make_double2(z, (j & 1) ? -z : z), bt, j);
+      }
     }
-    sm[gg * padded_len(M) + pad<M>(j)] = v;
+#pragma unroll
+    for (int i = 0; i < PF; ++i) {
+      const int idx = threadIdx.x + i * NT;
+      const int j = idx / G, gg = idx - j * G;
+      if (idx < M * G) sm[gg * padded_len(M) + pad<M>(j)] = v[i];
+    }
   }
   blue_core<M, T, G, BLUE>(sm, buf, bt, tw, t);
 

@@ -1,0 +1,82 @@
+"""Algorithmic work model of the AR path (bytes / flops per kernel launch and
+per pixel-iteration), used by bench.py for the roofline fields and by
+DESIGN.md §4.
+
+Two accountings are reported:
+
+* per kernel class, the ALGORITHMIC work of the form actually executed
+  (nominal 5 N log2 N flops per complex N-point FFT, 8 flops per complex
+  multiply-add, 2(2q+1)^2 flops per direct-stencil pixel; bytes = the arrays a
+  launch must read and write once);
+* the SURVEY §8d canonical step model: B = 72 B / px-it (D-Landweber fused
+  dataflow) and F = 4(2q+1)^2 (two dense stencils, as the reference's
+  correlate_valid_direct computes them) + 250 (nominal FFT-form DST-I), with
+  T_min = max(B W / BW_HBM, F W / P_FP64).
+"""
+from __future__ import annotations
+
+import math
+
+CONV_LENGTHS = [64, 72, 80, 96, 128, 144, 160, 192, 256, 270, 288, 320, 384, 512, 540, 576, 640, 768,
+                1024, 1080, 1152, 1280, 1536, 2048, 2160, 2304, 2560, 3072, 4096, 4320, 4608, 5120,
+                6144, 8192, 8640]
+DIRECT_DFT = [15, 31, 63, 255, 1023, 4095]
+BLUE_LENGTHS = [16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192]
+
+
+def conv_len(n: int, q: int) -> int:
+    need = n + 2 * q
+    need += need % 2
+    for L in CONV_LENGTHS:
+        if L >= need:
+            return L
+    return 0
+
+
+def dst_line_flops(n: int) -> float:
+    """Nominal flops of one AR transform line (length n): the packed N-point
+    DFT (N = n-1) directly, or Bluestein (2 FFTs of M + 3 pointwise passes)."""
+    N = n - 1
+    if N in DIRECT_DFT:
+        return 5.0 * N * math.log2(N) + 16.0 * N
+    M = next((m for m in BLUE_LENGTHS if m >= 2 * N - 1), 0)
+    if not M:
+        return 2.0 * (n - 2) * (n - 2)  # dense form
+    return 2 * 5.0 * M * math.log2(M) + 3 * 6.0 * M + 16.0 * N
+
+
+def conv_apply_flops(n1: int, n2: int, q1: int, q2: int) -> float:
+    L1, L2 = conv_len(n1, q1), conv_len(n2, q2)
+    Lh = L2 // 2 + 1
+    rows = (n1 + 1) // 2 * 2 * 5.0 * L2 * math.log2(L2)          # fwd + inv row FFTs (packed pairs)
+    cols = Lh * (2 * 5.0 * L1 * math.log2(L1) + 6.0 * L1)       # fwd, multiply, inv
+    return rows + cols
+
+
+def conv_apply_bytes(n1: int, n2: int, q1: int, q2: int, epi_arrays: int) -> float:
+    L2 = conv_len(n2, q2)
+    Lh = L2 // 2 + 1
+    z = 16.0 * n1 * Lh
+    return 8.0 * n1 * n2 + z + 2 * z + z + 8.0 * n1 * n2 * epi_arrays
+
+
+def direct_apply_flops(n1: int, n2: int, q1: int, q2: int) -> float:
+    return 2.0 * (2 * q1 + 1) * (2 * q2 + 1) * n1 * n2
+
+
+def transform_iteration_flops(n1: int, n2: int) -> float:
+    """Four AR transform passes (T~ rows/cols, T cols/rows) per iteration."""
+    return 2 * n1 * dst_line_flops(n2) + 2 * n2 * dst_line_flops(n1)
+
+
+def transform_iteration_bytes(n1: int, n2: int) -> float:
+    # rows T~: r+w 16; cols (T~, d, T): r+w + d = 24; rows T + axpy: r v, x, f, w x = 32
+    return (16 + 24 + 32) * float(n1 * n2)
+
+
+def canonical(q: int, px_it: float, seconds: float, bw_gbs: float, p_fp64_tflops: float):
+    B, F = 72.0, 4.0 * (2 * q + 1) ** 2 + 250.0
+    t_min = max(B * px_it / (bw_gbs * 1e9), F * px_it / (p_fp64_tflops * 1e12))
+    return {"bytes_per_px_it": B, "flops_per_px_it": F, "t_min_s": t_min, "t_meas_s": seconds,
+            "frac": t_min / seconds if seconds > 0 else None,
+            "bound": "fp64" if F * bw_gbs * 1e9 > B * p_fp64_tflops * 1e12 else "hbm"}
