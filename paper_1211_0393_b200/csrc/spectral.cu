@@ -61,7 +61,9 @@ __host__ __device__ constexpr int lines_for(int L, int budget_bytes, int per) {
   g = g < 1 ? 1 : (g > 4 ? 4 : g);
   // odd lengths carry radix <= 31 butterflies in registers: cap the CTA at 256
   // threads so each thread may use up to 255 registers without spilling
-  const int cap = 384;  // odd: radix <= 31 butterflies in registers; even: 2 CTAs/SM
+  // odd lengths: radix <= 31 butterflies (~170 registers) -> at most 192
+  // threads so two CTAs share an SM; even lengths: 384 (2 CTAs/SM at <= 85 regs)
+  const int cap = (L & 1) ? 192 : 384;
   while (g > 1 && g * line_threads(L, per) > cap) --g;
   return g;
 }
@@ -485,7 +487,7 @@ __device__ __forceinline__ double blue_out(const double2* buf, const BlueTables&
 
 // Row pass: one AR (or SineI) transform per row, fused epilogue.
 template <int M, bool BLUE>
-__global__ void __launch_bounds__(lines_for(M, kDstBudget, dst_per(M)) * line_threads(M, dst_per(M)))
+__global__ void __launch_bounds__(lines_for(M, kDstBudget, dst_per(M)) * line_threads(M, dst_per(M)), (M & 1) ? 2 : 1)
 dst_rows(SpecArgs a) {
   constexpr int T = line_threads(M, dst_per(M)), G = lines_for(M, kDstBudget, dst_per(M));
   constexpr int NT = T * G;
@@ -562,7 +564,7 @@ dst_rows(SpecArgs a) {
 // Column pass: CW adjacent columns per CTA; kind1, then optional Hadamard by
 // the d column, then optional kind2 (-1 = none).  Output with STORE epilogue.
 template <int M, bool BLUE>
-__global__ void __launch_bounds__(lines_for(M, kDstBudget, dst_per(M)) * line_threads(M, dst_per(M)))
+__global__ void __launch_bounds__(lines_for(M, kDstBudget, dst_per(M)) * line_threads(M, dst_per(M)), (M & 1) ? 2 : 1)
 dst_cols(SpecArgs a) {
   constexpr int T = line_threads(M, dst_per(M)), G = lines_for(M, kDstBudget, dst_per(M));
   constexpr int NT = T * G;
