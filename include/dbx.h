@@ -101,6 +101,10 @@ int dbx_plan_set_conv(dbx_plan* plan, int conv);
 /* AR-transform engine override (DBX_DST_*); default DBX_DST_AUTO. */
 int dbx_plan_set_dst(dbx_plan* plan, int engine);
 
+/* Fused row pipelines for the preconditioned FFT-form iteration (default 1):
+ * 6 launches + finalize per iteration instead of 9 + finalize. */
+int dbx_plan_set_fusion(dbx_plan* plan, int enable);
+
 /* Engines the plan will use: *conv in {DBX_CONV_DIRECT, DBX_CONV_FFT},
  * *dst in {DBX_DST_DENSE, DBX_DST_FFT}. */
 int dbx_plan_engines(dbx_plan* plan, int* conv, int* dst);

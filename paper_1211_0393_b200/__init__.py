@@ -65,6 +65,7 @@ def lib():
         L.dbx_plan_set_conv.argtypes = [vp, i]
         L.dbx_plan_set_dst.argtypes = [vp, i]
         L.dbx_plan_engines.argtypes = [vp, C.POINTER(i), C.POINTER(i)]
+        L.dbx_plan_set_fusion.argtypes = [vp, i]
         L.dbx_blur_apply.argtypes = [vp, vp, vp, i]
         L.dbx_precond_build.argtypes = [vp, d]
         L.dbx_precond_eigs.argtypes = [vp, vp]
@@ -251,6 +252,10 @@ class BlurOperator:
 
     def set_dst(self, engine: DstEngine):
         _check(lib().dbx_plan_set_dst(self.handle, int(engine)))
+        return self
+
+    def set_fusion(self, on: bool):
+        _check(lib().dbx_plan_set_fusion(self.handle, int(bool(on))))
         return self
 
     def engines(self):

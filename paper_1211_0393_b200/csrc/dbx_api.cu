@@ -211,6 +211,8 @@ struct dbx_plan {
   // graph cache
   cudaGraphExec_t gexec = nullptr;
   std::string gkey;
+  int64_t glaunches = 0;
+  bool fusion = true;  // fused row pipelines when compiled for the sizes
   // ---- FFT-form state ----
   int dst = DBX_DST_AUTO;
   bool conv_ready = false;
@@ -621,6 +623,13 @@ int dbx_plan_set_dst(dbx_plan* plan, int engine) {
   });
 }
 
+int dbx_plan_set_fusion(dbx_plan* plan, int enable) {
+  return guarded([&] {
+    require(plan != nullptr, "null plan");
+    plan->fusion = enable != 0;
+  });
+}
+
 int dbx_plan_engines(dbx_plan* plan, int* conv, int* dst) {
   return guarded([&] {
     require(plan != nullptr, "null plan");
@@ -818,8 +827,79 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
     ck(cudaMemcpyAsync(P->r.p, gd, cnt * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
     P->check_launch();
 
+    // Fused FFT-form pipeline (fused.cu): 6 launches + finalize per iteration.
+    P->prepare(use_precond != 0);
+    const bool fused = use_precond && P->use_fft_conv() && P->use_fft_dst(false) && P->fusion &&
+                       fused_supported(P->L2, P->blue_tables(1, false).M,
+                                       P->blue_tables(1, false).M != P->blue_tables(1, false).N);
+    SpecArgs fa0 = P->spec_base(P->st, pt);
+    if (fused) {
+      fa0.conv.tw1 = reinterpret_cast<const double2*>(P->tw1);
+      fa0.conv.tw2 = reinterpret_cast<const double2*>(P->tw2);
+      fa0.conv.L1 = P->L1; fa0.conv.L2 = P->L2; fa0.conv.Lh = P->Lh;
+      fa0.zbuf = reinterpret_cast<double2*>(P->zb.p);
+      fa0.ybuf = reinterpret_cast<double2*>(P->yb.p);
+      fa0.blue1 = P->blue_tables(0, false);
+      fa0.blue2 = P->blue_tables(1, false);
+      fa0.d = P->d;
+      fa0.g = gd;
+      fa0.f = fd;
+      fa0.tau = tau;
+    }
+    auto enqueue_pre = [&]() {
+      if (!fused) return;
+      // spectrum of the AR-extended r_0 = g for the first A' apply
+      SpecArgs a = fa0;
+      a.in = gd; a.insel = SEL_EXPLICIT;
+      P->ev_begin(KC_BLUR_ADJ);
+      lc(launch_conv_row_fwd(a, s), "launch_conv_row_fwd");
+      P->ev_end();
+    };
+    auto enqueue_fused = [&](int k) {
+      SpecArgs a = fa0;
+      // K1: column pass of A' (spectral AR extension, kernel spectrum of the rotated mask)
+      a.conv.H = reinterpret_cast<const double2*>(P->HAt);
+      P->ev_begin(KC_BLUR_ADJ); lc(launch_conv_col(a, s), "launch_conv_col"); P->ev_end();
+      // K2: inverse row FFT -> A'r rows -> T~ along rows -> u
+      a.out = P->u.p; a.outsel = SEL_EXPLICIT;
+      P->ev_begin(KC_TRANSFORM); lc(launch_fused(FUSED_AINV_TT, a, s), "rows_ainv_tt"); P->ev_end();
+      // K3: columns: T~ -> d -> T
+      a.in = P->u.p; a.insel = SEL_EXPLICIT; a.out = P->s.p; a.outsel = SEL_EXPLICIT;
+      a.kind1 = DBX_KIND_ARINV; a.kind2 = DBX_KIND_AR; a.epi = SPEC_STORE;
+      P->ev_begin(KC_TRANSFORM); lc(launch_dst_cols(a, s), "launch_dst_cols"); P->ev_end();
+      // K4: T along rows -> x_k = x_{k-1} + tau (.) + norms -> forward row FFT for A x_k
+      a.in = P->s.p; a.out = P->X3.p; a.outsel = SEL_NXT; a.xold = P->X3.p; a.xoldsel = SEL_CUR;
+      P->ev_begin(KC_TRANSFORM);
+      const int cnt_x = lc(launch_fused(FUSED_T_AXPY_AFWD, a, s), "rows_t_axpy_afwd");
+      P->ev_end();
+      // K5: column pass of A
+      a.conv.H = reinterpret_cast<const double2*>(P->HA);
+      P->ev_begin(KC_BLUR); lc(launch_conv_col(a, s), "launch_conv_col"); P->ev_end();
+      // K6: inverse row FFT -> r_k = g - A x_k + ||r||^2 -> forward row FFT for the next A'
+      P->ev_begin(KC_BLUR);
+      const int cnt_r = lc(launch_fused(FUSED_AINV_RESID, a, s), "rows_ainv_resid");
+      P->ev_end();
+      return std::make_pair(cnt_x, cnt_r);
+    };
+
     auto enqueue = [&](int k) {
       int cnt_x = 0;
+      if (fused) {
+        const auto cr = enqueue_fused(k);
+        FinalizeArgs fa{};
+        fa.st = P->st; fa.part = pt; fa.cnt_x = cr.first; fa.cnt_r = cr.second; fa.k = k;
+        fa.hist_len = H; fa.rre_hist = P->rre.p; fa.res_hist = P->res.p;
+        fa.track = track ? 1 : 0; fa.stop_kind = stop_kind; fa.resid_eps = resid_eps; fa.batch = B;
+        P->ev_begin(KC_FINALIZE);
+        launch_finalize(fa, s);
+        P->ev_end();
+        P->check_launch();
+        if (want_xh) {
+          launch_select_copy(P->X3.p, P->st, 0, B, N, P->xh.p + (size_t)(k - 1) * cnt, s);
+          ++P->launches;
+        }
+        return;
+      }
       if (use_precond) {
         P->blur(P->r.p, SEL_EXPLICIT, P->s.p, SEL_EXPLICIT, true, BLUR_STORE, nullptr, nullptr,
                 SEL_EXPLICIT, nullptr, 0.0, P->st, pt, KC_BLUR_ADJ);
@@ -845,15 +925,13 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
       }
     };
 
-    // tables / matrices are uploaded before capture (no allocation inside a graph)
-    P->prepare(use_precond != 0);
     if (total > 0) {
       // Graph path: one graph per run shape, replayed; kernels read the run's
       // buffers through stable plan-owned pointers.
       char key[512];
-      snprintf(key, sizeof key, "%d|%d|%d|%.17g|%.17g|%d|%d|%p|%p|%d|%d", total, use_precond,
+      snprintf(key, sizeof key, "%d|%d|%d|%.17g|%.17g|%d|%d|%p|%p|%d|%d|%d", total, use_precond,
                stop_kind, resid_eps, tau, (int)track, (int)want_xh, (const void*)gd,
-               (const void*)fd, P->conv, P->dst);
+               (const void*)fd, P->conv, P->dst, (int)fused);
       const bool use_graph = !P->timing;
       if (use_graph) {
         if (!P->gexec || P->gkey != key) {
@@ -864,17 +942,28 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
           cudaGraph_t graph;
           const int64_t before = P->launches;
           ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
-          for (int k = 1; k <= total; ++k) enqueue(k);
+          try {
+            enqueue_pre();
+            for (int k = 1; k <= total; ++k) enqueue(k);
+          } catch (...) {
+            // never leave the plan's stream in capture mode
+            cudaGraph_t broken = nullptr;
+            cudaStreamEndCapture(s, &broken);
+            if (broken) cudaGraphDestroy(broken);
+            cudaGetLastError();
+            throw;
+          }
           ck(cudaStreamEndCapture(s, &graph), "end capture");
           ck(cudaGraphInstantiate(&P->gexec, graph, 0), "instantiate");
           cudaGraphDestroy(graph);
-          P->launches = before;  // counted at replay
+          P->glaunches = P->launches - before;  // kernels per replay
+          P->launches = before;
           P->gkey = key;
         }
         ck(cudaGraphLaunch(P->gexec, s), "graph launch");
-        // launch accounting: kernels per iteration
-        P->launches += (int64_t)total * ((use_precond ? 5 : 1) + 2 + (want_xh ? 1 : 0));
+        P->launches += P->glaunches;
       } else {
+        enqueue_pre();
         for (int k = 1; k <= total; ++k) enqueue(k);
       }
     }

@@ -1,0 +1,313 @@
+// fused.cu — fused row pipelines of the preconditioned iteration (FFT-form
+// blur + FFT-form AR transform).  One CTA owns one PAIR of image rows (the
+// two rows share one packed real-FFT line of length L2 and own two DST lines
+// of length M); every stage stays in shared memory between the passes that
+// used to be separate launches:
+//
+//   rows_ainv_tt      : Y (A' r spectrum) -> inverse row FFT -> s = A'r rows
+//                       -> T~ (AR inverse transform, DST-I) along the rows -> u
+//   rows_t_axpy_afwd  : v -> T along the rows -> x_k = x_{k-1} + tau*(.) with
+//                       ||x||^2, ||x - f||^2 partials -> AR-extend x_k rows ->
+//                       forward row FFT -> Z (spectrum for A x_k)
+//   rows_ainv_resid   : Y (A x_k spectrum) -> inverse row FFT -> r = g - A x_k
+//                       with ||r||^2 partials -> AR-extend r rows -> forward
+//                       row FFT -> Z' (spectrum for A' r of the next iteration)
+//
+// Together with conv_col (twice) and dst_cols the iteration takes 6 launches
+// + finalize instead of 9 + finalize, and x, r, s never make an extra HBM
+// round trip.  Reference: the loop body of landweber_loop (solver.hpp:101-125)
+// with apply (blur.hpp:75-83), precondition_apply (preconditioner.hpp:88-90).
+#include <cuda_runtime.h>
+
+#include "spectral_common.cuh"
+
+namespace dbx {
+
+namespace {
+
+template <int L2, int M, bool BLUE>
+struct Fused {
+  static constexpr int TD = line_threads(M, dst_per(M));   // threads per DST line
+  static constexpr int NT = 2 * TD;                         // CTA = two DST lines
+  static constexpr int LC = padded_len(L2);                 // conv line (double2)
+  static constexpr int LD = padded_len(M);                  // DST line (double2)
+  static constexpr int WORK = (LC > 2 * LD ? LC : 2 * LD);  // shared work region
+  static constexpr int RROW = L2;                           // real staging row (doubles)
+  // double2 offsets
+  static constexpr int off_real = WORK;                       // 2 rows x RROW doubles
+  static constexpr int off_epi = off_real + RROW;             // 2 ops x 2 rows x RROW doubles
+  static constexpr int off_twd = off_epi + 2 * RROW;          // DST twiddles (M)
+  static constexpr int off_twc = off_twd + M;                 // conv twiddles (L2), if they fit
+  static constexpr bool TWC = (size_t)(off_twc + L2) * 16 <= 110 * 1024;
+  static constexpr size_t bytes = (size_t)(off_twc + (TWC ? L2 : 0)) * 16;
+};
+
+// Inverse packed real FFT of rows (ra, rb) from the half spectra Y -> buf.
+template <int L2, int NT>
+__device__ __forceinline__ void conv_inv_load(double2* buf, const double2* __restrict__ Y, int ra, int rb,
+                                              int n1, int Lh) {
+  const int t = threadIdx.x;
+  constexpr int PF = (L2 / 2 + 1 + NT - 1) / NT;
+  double2 A[PF], Bv[PF];
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int k = t + i * NT;
+    A[i] = make_double2(0.0, 0.0);
+    Bv[i] = A[i];
+    if (k < Lh) {
+      if (ra < n1) A[i] = Y[(size_t)ra * Lh + k];
+      if (rb < n1) Bv[i] = Y[(size_t)rb * Lh + k];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int k = t + i * NT;
+    if (k < Lh) {
+      buf[pad<L2>(k)] = make_double2(A[i].x - Bv[i].y, A[i].y + Bv[i].x);
+      if (k > 0 && k < L2 - k) buf[pad<L2>(L2 - k)] = make_double2(A[i].x + Bv[i].y, Bv[i].x - A[i].y);
+    }
+  }
+}
+
+// Forward packed real FFT of two real rows held in shared memory (AR-extended
+// horizontally on the fly, boundary.hpp:56-62) -> half spectra into Z.
+template <int L2, int NT>
+__device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, const double* rowb, bool has_b,
+                                              int n2, int q2, const double2* tw, double2* Z, int ra, int rb,
+                                              int n1, int Lh) {
+  const int t = threadIdx.x;
+  const int wext = n2 + 2 * q2;
+  auto ext = [&](const double* row, int j) -> double {
+    if (j < 0) return 2.0 * row[0] - row[-j];
+    if (j >= n2) return 2.0 * row[n2 - 1] - row[2 * (n2 - 1) - j];
+    return row[j];
+  };
+  for (int p = t; p < L2; p += NT) {
+    double va = 0.0, vb = 0.0;
+    if (p < wext) {
+      va = ext(rowa, p - q2);
+      if (has_b) vb = ext(rowb, p - q2);
+    }
+    buf[pad<L2>(p)] = make_double2(va, vb);
+  }
+  __syncthreads();
+  fft::fft<L2, -1, NT>(buf, tw, t);
+  for (int k = t; k < Lh; k += NT) {
+    const double2 zk = buf[pad<L2>(k)], zm = buf[pad<L2>(k == 0 ? 0 : L2 - k)];
+    if (ra < n1) Z[(size_t)ra * Lh + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    if (rb < n1) Z[(size_t)rb * Lh + k] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int L2, int M, bool BLUE>
+__global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecArgs a) {
+  using F = Fused<L2, M, BLUE>;
+  constexpr int NT = F::NT, TD = F::TD;
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 sm[];
+  double* rowS = reinterpret_cast<double*>(sm + F::off_real);  // 2 x RROW doubles
+  const BlueTables& bt = a.blue2;
+  const double2* twd = stage_twiddles<M, true>(sm + F::off_twd, bt.tw);
+  const double2* twc = stage_twiddles<L2, F::TWC>(sm + F::off_twc, a.conv.tw2);
+  const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
+  const size_t N = (size_t)n1 * n2;
+  const int ra = 2 * blockIdx.x, rb = ra + 1;
+  // A' r rows: inverse packed row FFT
+  conv_inv_load<L2, NT>(sm, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh);
+  cp_async_wait_all();
+  __syncthreads();
+  fft::fft<L2, +1, NT>(sm, twc, threadIdx.x);
+  for (int c = threadIdx.x; c < n2; c += NT) {
+    const double2 v = sm[pad<L2>(c)];
+    rowS[c] = v.x;
+    rowS[F::RROW + c] = v.y;
+  }
+  __syncthreads();
+  // T~ along each of the two rows (ar_inverse, transforms.hpp:163-173)
+  const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
+  const int r = ra + g;
+  const bool live = r < n1;
+  const double* s = rowS + g * F::RROW;
+  const double v0 = s[0], ve = s[n2 - 1];
+  const double* p = bt.p;
+  double2* buf = sm + g * F::LD;
+  blue_fill<M, TD, BLUE>(buf, bt, t, [&](int j) {
+    return live ? (s[j] - v0 * __ldg(p + j - 1)) - ve * __ldg(p + n2 - 2 - j) : 0.0;
+  });
+  blue_core<M, TD, 2, BLUE>(sm, buf, bt, twd, t);
+  if (live) {
+    double* u = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + (size_t)r * n2;
+    const double al = bt.alpha;
+    for (int k = t; k < n2; k += TD)
+      u[k] = (k == 0) ? al * v0 : (k == n2 - 1) ? al * ve : blue_out<M, BLUE>(buf, bt, k);
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int L2, int M, bool BLUE>
+__global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(SpecArgs a) {
+  using F = Fused<L2, M, BLUE>;
+  constexpr int NT = F::NT, TD = F::TD;
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 sm[];
+  __shared__ double red[32];
+  double* rowS = reinterpret_cast<double*>(sm + F::off_real);
+  double* stX = reinterpret_cast<double*>(sm + F::off_epi);        // x_{k-1}: 2 rows
+  double* stF = stX + 2 * F::RROW;                                  // f: 2 rows
+  const BlueTables& bt = a.blue2;
+  const double2* twd = stage_twiddles<M, true>(sm + F::off_twd, bt.tw);
+  const double2* twc = stage_twiddles<L2, F::TWC>(sm + F::off_twc, a.conv.tw2);
+  const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
+  const size_t N = (size_t)n1 * n2;
+  const int ra = 2 * blockIdx.x, rb = ra + 1;
+  const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
+  const int r = ra + g;
+  const bool live = r < n1;
+  const double* xo = resolve_ptr(a.xold, a.st, a.xoldsel, b, a.batch, N);
+  const double* fimg = a.f ? a.f + (size_t)b * N : nullptr;
+  // stage x_{k-1} and f rows (cp.async group 2) behind the transform
+  if (live) {
+    for (int k = t; k < n2; k += TD) {
+      cp_async8(stX + g * F::RROW + k, xo + (size_t)r * n2 + k);
+      if (fimg) cp_async8(stF + g * F::RROW + k, fimg + (size_t)r * n2 + k);
+    }
+  }
+  cp_async_commit();
+  // T along each row (ar_forward, transforms.hpp:148-160)
+  const double* v = a.in + (size_t)b * N + (size_t)(live ? r : 0) * n2;
+  const double v0 = v[0], ve = v[n2 - 1];
+  const double* p = bt.p;
+  double2* buf = sm + g * F::LD;
+  blue_fill<M, TD, BLUE>(buf, bt, t, [&](int j) { return live ? v[j] : 0.0; });
+  blue_core<M, TD, 2, BLUE>(sm, buf, bt, twd, t);
+  cp_async_wait_all();
+  double p0 = 0.0, p1 = 0.0;
+  double* xn = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N));
+  if (live) {
+    const double ia = 1.0 / bt.alpha, a0 = ia * v0, a1 = ia * ve;
+    for (int k = t; k < n2; k += TD) {
+      double w;
+      if (k == 0) w = a0;
+      else if (k == n2 - 1) w = a1;
+      else {
+        w = blue_out<M, BLUE>(buf, bt, k);
+        w += a0 * __ldg(p + k - 1);
+        w += a1 * __ldg(p + n2 - 2 - k);
+      }
+      const double xv = stX[g * F::RROW + k] + a.tau * w;
+      xn[(size_t)r * n2 + k] = xv;
+      rowS[g * F::RROW + k] = xv;
+      p0 += xv * xv;
+      if (fimg) {
+        const double e = xv - stF[g * F::RROW + k];
+        p1 += e * e;
+      }
+    }
+  }
+  __syncthreads();  // x rows staged; DST buffers free for the conv line
+  conv_fwd_rows<L2, NT>(sm, rowS, rowS + F::RROW, rb < n1, n2, a.q2, twc, a.zbuf + (size_t)b * n1 * Lh, ra, rb,
+                        n1, Lh);
+  if (a.part.p) {
+    double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
+    const double s0 = block_sum<NT>(p0, red);
+    if (threadIdx.x == 0) P[SLOT_X2 * a.part.cap + blockIdx.x] = s0;
+    const double s1 = block_sum<NT>(p1, red);
+    if (threadIdx.x == 0) P[SLOT_XF2 * a.part.cap + blockIdx.x] = s1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int L2, int M, bool BLUE>
+__global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_resid(SpecArgs a) {
+  using F = Fused<L2, M, BLUE>;
+  constexpr int NT = F::NT;
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 sm[];
+  __shared__ double red[32];
+  double* rowS = reinterpret_cast<double*>(sm + F::off_real);
+  double* stG = reinterpret_cast<double*>(sm + F::off_epi);
+  const double2* twc = stage_twiddles<L2, F::TWC>(sm + F::off_twc, a.conv.tw2);
+  const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
+  const size_t N = (size_t)n1 * n2;
+  const int ra = 2 * blockIdx.x, rb = ra + 1;
+  const double* gimg = a.g + (size_t)b * N;
+  for (int c = threadIdx.x; c < n2; c += NT) {
+    if (ra < n1) cp_async8(stG + c, gimg + (size_t)ra * n2 + c);
+    if (rb < n1) cp_async8(stG + F::RROW + c, gimg + (size_t)rb * n2 + c);
+  }
+  cp_async_commit();
+  conv_inv_load<L2, NT>(sm, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh);
+  cp_async_wait_group<1>();
+  __syncthreads();
+  fft::fft<L2, +1, NT>(sm, twc, threadIdx.x);
+  cp_async_wait_all();
+  double p0 = 0.0;
+  for (int c = threadIdx.x; c < n2; c += NT) {
+    const double2 ax = sm[pad<L2>(c)];
+    if (ra < n1) {
+      const double rv = stG[c] - ax.x;  // r = g - A x (solver.hpp:105)
+      rowS[c] = rv;
+      p0 += rv * rv;
+    }
+    if (rb < n1) {
+      const double rv = stG[F::RROW + c] - ax.y;
+      rowS[F::RROW + c] = rv;
+      p0 += rv * rv;
+    }
+  }
+  __syncthreads();
+  conv_fwd_rows<L2, NT>(sm, rowS, rowS + F::RROW, rb < n1, n2, a.q2, twc, a.zbuf + (size_t)b * n1 * Lh, ra, rb,
+                        n1, Lh);
+  if (a.part.p) {
+    double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
+    const double s0 = block_sum<NT>(p0, red);
+    if (threadIdx.x == 0) P[SLOT_R2 * a.part.cap + blockIdx.x] = s0;
+  }
+}
+
+// WHICH makes the attribute flag per kernel (the three kernels share one
+// function-pointer type).
+template <int L2, int M, bool BLUE, int WHICH, typename K>
+int fused_launch(K kernel, const SpecArgs& a, cudaStream_t s) {
+  using F = Fused<L2, M, BLUE>;
+  static bool init = false;
+  if (!init) {
+    if (!set_smem(kernel, F::bytes)) return -1;
+    init = true;
+  }
+  dim3 grid((a.n1 + 1) / 2, a.batch);
+  kernel<<<grid, F::NT, F::bytes, s>>>(a);
+  return (int)grid.x;
+}
+
+}  // namespace
+
+// (conv L2, DST M, Bluestein?) combinations compiled for the fused pipeline.
+#define DBX_FUSED_LIST(X) X(1080, 1023, false) X(540, 1024, true) X(270, 255, false) X(2160, 4096, true)
+
+bool fused_supported(int L2, int M, bool blue) {
+#define X(L, MM, BL) if (L2 == (L) && M == (MM) && blue == (BL)) return Fused<L, MM, BL>::bytes <= 200 * 1024;
+  DBX_FUSED_LIST(X)
+#undef X
+  return false;
+}
+
+int launch_fused(int which, const SpecArgs& a, cudaStream_t s) {
+  const int L2 = a.conv.L2, M = a.blue2.M;
+  const bool blue = a.blue2.M != a.blue2.N;
+#define X(L, MM, BL)                                                                          \
+  if (L2 == (L) && M == (MM) && blue == (BL)) {                                               \
+    if (which == FUSED_AINV_TT) return fused_launch<L, MM, BL, 0>(rows_ainv_tt<L, MM, BL>, a, s); \
+    if (which == FUSED_T_AXPY_AFWD) return fused_launch<L, MM, BL, 1>(rows_t_axpy_afwd<L, MM, BL>, a, s); \
+    if (which == FUSED_AINV_RESID) return fused_launch<L, MM, BL, 2>(rows_ainv_resid<L, MM, BL>, a, s); \
+  }
+  DBX_FUSED_LIST(X)
+#undef X
+  return -1;
+}
+
+}  // namespace dbx

@@ -24,204 +24,12 @@
 //                  half of D = T diag(d) T~ in one pass.
 #include <cuda_runtime.h>
 
-#include "dbx_internal.h"
-#include "fft.cuh"
-#include "spectral.h"
+#include "spectral_common.cuh"
 
 namespace dbx {
 
-using fft::cadd;
-using fft::cmul;
-using fft::csub;
-using fft::pad;
-using fft::padded_len;
 
 namespace {
-
-// threads per FFT line: conv lines get one radix-8 butterfly per thread, DST
-// lines (power-of-two M) two; both capped at 256 so a CTA of <= 512 threads
-// keeps >= 128 registers per thread for the in-register radix stages.
-__host__ __device__ constexpr int line_threads(int L, int per) {
-  if (L & 1) {
-    // direct odd length: the first (largest-prime) stage runs packed across
-    // the CTA's lines, so size the line for the second stage's butterflies
-    // (1023 = 31*11*3 -> 93 radix-11 butterflies -> 96 threads)
-    const int r1 = fft::next_radix(L);
-    const int r2 = fft::next_radix(L / r1);
-    int t = ((r2 ? L / r2 : L) + 31) / 32 * 32;
-    return t < 32 ? 32 : (t > 256 ? 256 : t);
-  }
-  int t = (L / per + 31) / 32 * 32;
-  return t < 32 ? 32 : (t > 256 ? 256 : t);
-}
-// lines (rows / columns / row pairs) per CTA for a line length L
-__host__ __device__ constexpr int lines_for(int L, int budget_bytes, int per) {
-  const int bytes = padded_len(L) * 16;
-  int g = budget_bytes / bytes;
-  g = g < 1 ? 1 : (g > 4 ? 4 : g);
-  // odd lengths carry radix <= 31 butterflies in registers: cap the CTA at 256
-  // threads so each thread may use up to 255 registers without spilling
-  // odd lengths: radix <= 31 butterflies (~170 registers) -> at most 192
-  // threads so two CTAs share an SM; even lengths: 384 (2 CTAs/SM at <= 85 regs)
-  const int cap = (L & 1) ? 192 : 384;
-  while (g > 1 && g * line_threads(L, per) > cap) --g;
-  return g;
-}
-// DST lines: direct odd-length DFTs (radix up to 31) get one butterfly-sized
-// share per thread (L/8), power-of-two Bluestein lines two radix-8 butterflies.
-__host__ __device__ constexpr int dst_per(int L) { return (L & 1) ? 8 : 16; }
-constexpr int kConvBudget = 100 * 1024;
-constexpr int kDstBudget = 160 * 1024;
-
-// Asynchronous global -> shared copies (LDGSTS): operands needed only after a
-// transform are staged at kernel start without holding registers.
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-// Bulk L2 prefetch of a contiguous row (TMA unit; no registers, no smem).
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-  const unsigned long long a = (unsigned long long)p;
-  if ((a & 15) || (bytes & 15) || bytes == 0) return;
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// Twiddle table of an FFT length L staged into shared memory (cp.async group
-// committed here) when `smem_ok`, else read from global (L1/L2).
-template <int L, bool SMEM>
-__device__ __forceinline__ const double2* stage_twiddles(double2* dst, const double2* src) {
-  if constexpr (SMEM) {
-    for (int i = threadIdx.x; i < L; i += blockDim.x) cp_async16(dst + i, src + i);
-    cp_async_commit();
-    return dst;
-  } else {
-    cp_async_commit();  // keep group numbering uniform
-    return src;
-  }
-}
-constexpr int kSmemCap = 200 * 1024;
-
-__device__ __forceinline__ double hext(const double* __restrict__ x, int i, int j, int n2) {
-  const double* row = x + (size_t)i * n2;
-  if (j < 0) return 2.0 * row[0] - row[-j];
-  if (j >= n2) return 2.0 * row[n2 - 1] - row[2 * (n2 - 1) - j];
-  return row[j];
-}
-
-template <int NT>
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x == 0)
-    for (int i = 0; i < NT / 32; ++i) s += red[i];
-  return s;
-}
-
-// Shared epilogue of the passes that produce final image values.
-struct Epi {
-  int mode;  // EPI_STORE / EPI_RESID / EPI_AXPY / EPI_HADAMARD
-  double* y;
-  const double* g;
-  const double* xo;
-  const double* f;
-  const double* d;
-  double tau;
-  double p0 = 0.0, p1 = 0.0;
-  __device__ __forceinline__ void put(size_t o, double v) {
-    if (mode == SPEC_STORE) {
-      y[o] = v;
-    } else if (mode == SPEC_HADAMARD) {
-      y[o] = v * d[o];
-    } else if (mode == SPEC_RESID) {
-      const double rv = g[o] - v;
-      y[o] = rv;
-      p0 += rv * rv;
-    } else {
-      const double xv = xo[o] + tau * v;
-      y[o] = xv;
-      p0 += xv * xv;
-      if (f) {
-        const double e = xv - f[o];
-        p1 += e * e;
-      }
-    }
-  }
-  // Same with the operands already in registers: pa = x_{k-1} / g / d, pb = f.
-  __device__ __forceinline__ void put_pre(size_t o, double v, double pa, double pb) {
-    if (mode == SPEC_STORE) {
-      y[o] = v;
-    } else if (mode == SPEC_HADAMARD) {
-      y[o] = v * pa;
-    } else if (mode == SPEC_RESID) {
-      const double rv = pa - v;
-      y[o] = rv;
-      p0 += rv * rv;
-    } else {
-      const double xv = pa + tau * v;
-      y[o] = xv;
-      p0 += xv * xv;
-      if (f) {
-        const double e = xv - pb;
-        p1 += e * e;
-      }
-    }
-  }
-};
-
-template <int NT>
-__device__ __forceinline__ void write_partials(const SpecArgs& a, Epi& e, double* red, int b) {
-  if (!(a.epi == SPEC_RESID || a.epi == SPEC_AXPY) || !a.part.p) return;
-  const int cta = blockIdx.x;
-  double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
-  const double s0 = block_sum<NT>(e.p0, red);
-  if (a.epi == SPEC_RESID) {
-    if (threadIdx.x == 0) P[SLOT_R2 * a.part.cap + cta] = s0;
-  } else {
-    if (threadIdx.x == 0) P[SLOT_X2 * a.part.cap + cta] = s0;
-    const double s1 = block_sum<NT>(e.p1, red);
-    if (threadIdx.x == 0) P[SLOT_XF2 * a.part.cap + cta] = s1;
-  }
-}
-
-__device__ __forceinline__ Epi make_epi(const SpecArgs& a, int b, size_t N) {
-  Epi e;
-  e.mode = a.epi;
-  e.y = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N));
-  e.g = a.g ? a.g + (size_t)b * N : nullptr;
-  e.xo = a.epi == SPEC_AXPY ? resolve_ptr(a.xold, a.st, a.xoldsel, b, a.batch, N) : nullptr;
-  e.f = (a.epi == SPEC_AXPY && a.f) ? a.f + (size_t)b * N : nullptr;
-  e.d = a.d;
-  e.tau = a.tau;
-  return e;
-}
-
-// ---------------------------------------------------------------------------
-// FFT correlation
-// ---------------------------------------------------------------------------
-// Shared-memory plan of a conv kernel: G line buffers, optionally the twiddle
-// table (TW) and, for conv_col, the G kernel-spectrum columns (HS).
-template <int L, int G>
-struct ConvSmem {
-  static constexpr int lines = G * padded_len(L);
-  static constexpr bool HS = (2 * lines) * 16 <= kSmemCap;          // conv_col H staging
-  static constexpr bool TW = (lines + (HS ? lines : 0) + L) * 16 <= kSmemCap;
-  static constexpr bool TW_ROW = (lines + L) * 16 <= kSmemCap;      // row kernels
-  static constexpr size_t col_bytes = (size_t)(lines + (HS ? lines : 0) + (TW ? L : 0)) * 16;
-  static constexpr size_t row_bytes = (size_t)(lines + (TW_ROW ? L : 0)) * 16;
-};
 
 template <int L2>
 __global__ void __launch_bounds__(lines_for(L2, kConvBudget, 8) * line_threads(L2, 8))
@@ -404,85 +212,6 @@ conv_row_inv(SpecArgs a) {
     if (rb < n1) e.put((size_t)rb * n2 + c, v.y);
   }
   write_partials<NT>(a, e, red, b);
-}
-
-// ---------------------------------------------------------------------------
-// Bluestein DST-I / AR transforms
-// ---------------------------------------------------------------------------
-// Fill one padded line with a_j = z_j w_j, z_j = v_j (1 + i(-1)^j), j in [1, N).
-// `val(j)` returns v_j (1-based interior index).
-// Two forms of the N-point DFT of z: BLUE = Bluestein chirp-z over a power of
-// two L = M >= 2N-1 (any N); !BLUE = direct mixed-radix FFT of length L = N
-// (N with prime factors <= 31, e.g. 255 = 3.5.17, 1023 = 3.11.31).
-template <bool BLUE>
-__device__ __forceinline__ double2 pre(double2 z, const BlueTables& bt, int j) {
-  if constexpr (BLUE) return cmul(z, __ldg(bt.chirp + j));
-  else return z;
-}
-
-template <int M, int T, bool BLUE, typename F>
-__device__ __forceinline__ void blue_fill(double2* buf, const BlueTables& bt, int t, F val) {
-  const int N = bt.N;
-  // every load of the thread (line values, chirp) is issued before any store
-  constexpr int PF = (M + T - 1) / T;
-  double2 v[PF];
-#pragma unroll
-  for (int i = 0; i < PF; ++i) {
-    const int j = t + i * T;
-    v[i] = make_double2(0.0, 0.0);
-    if (j >= 1 && j < N) {
-      const double z = val(j);
-      v[i] = pre<BLUE>(make_double2(z, (j & 1) ? -z : z), bt, j);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < PF; ++i) {
-    const int j = t + i * T;
-    if (j < M) buf[pad<M>(j)] = v[i];
-  }
-}
-
-// BLUE: FFT, multiply by the kernel spectrum, inverse FFT.  Direct: one FFT.
-// Shared-memory plan of a DST kernel: G line buffers, G x 2 real staging rows
-// (epilogue operands / d column and T~ output), then the twiddle table if it
-// fits.
-template <int L, int G, bool BLUE>
-struct DstSmem {
-  static constexpr int LMAX = BLUE ? L / 2 + 1 : L + 1;
-  static constexpr size_t base = (size_t)G * padded_len(L) * 16 + (size_t)G * 2 * LMAX * 8;
-  static constexpr size_t tw_off = (base + 15) / 16 * 16;
-  static constexpr bool TW = tw_off + (size_t)L * 16 <= kSmemCap;
-  static constexpr size_t bytes = TW ? tw_off + (size_t)L * 16 : base;
-};
-
-template <int M, int T, int G, bool BLUE>
-__device__ __forceinline__ void blue_core(double2* sm, double2* buf, const BlueTables& bt, const double2* tw,
-                                          int t) {
-  cp_async_wait_group<1>();  // the twiddle group (committed first) has landed
-  __syncthreads();
-  if constexpr (!BLUE) {
-    // direct odd length: large-prime stages packed across the CTA's G lines
-    fft::fft_cta<M, -1, T, G>(sm, tw, threadIdx.x);
-    return;
-  }
-  fft::fft<M, -1, T>(buf, tw, t);
-  if constexpr (BLUE) {
-    for (int j = t; j < M; j += T) buf[pad<M>(j)] = cmul(buf[pad<M>(j)], __ldg(bt.bhat + j));
-    __syncthreads();
-    fft::fft<M, +1, T>(buf, tw, t);
-  }
-}
-
-// DST-I output y_k (k in [1, N)) from Z = DFT_N(z) (post-chirp applied here
-// for BLUE), scaled by sqrt(2/N): Q v = sqrt(2/N) sum_j v_j sin(pi j k / N).
-// Even k = 2l: -Im DFT(v)_l; odd k: -Im DFT((-1)^j v)_{(k+N)/2} (N odd).
-template <int M, bool BLUE>
-__device__ __forceinline__ double blue_out(const double2* buf, const BlueTables& bt, int k) {
-  const int N = bt.N;
-  const int l = (k & 1) == 0 ? (k >> 1) : ((k + N) >> 1);
-  const double2 zl = pre<BLUE>(buf[pad<M>(l)], bt, l);
-  const double2 zm = pre<BLUE>(buf[pad<M>(N - l)], bt, N - l);
-  return (k & 1) == 0 ? 0.5 * bt.scale * (zm.y - zl.y) : 0.5 * bt.scale * (zl.x - zm.x);
 }
 
 // Row pass: one AR (or SineI) transform per row, fused epilogue.
@@ -710,14 +439,6 @@ dst_cols(SpecArgs a) {
     }
     out[(size_t)k * n2 + cc] = v;
   }
-}
-
-template <typename K>
-bool set_smem(K kernel, size_t bytes) {
-  if (bytes > 227 * 1024) return false;
-  if (bytes > 48 * 1024)
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess;
-  return true;
 }
 
 }  // namespace

@@ -68,4 +68,9 @@ int launch_conv_row_inv(const SpecArgs& a, cudaStream_t s);
 int launch_dst_rows(const SpecArgs& a, cudaStream_t s);
 int launch_dst_cols(const SpecArgs& a, cudaStream_t s);
 
+// Fused row pipelines of the preconditioned iteration (fused.cu).
+enum FusedKind { FUSED_AINV_TT = 0, FUSED_T_AXPY_AFWD = 1, FUSED_AINV_RESID = 2 };
+bool fused_supported(int L2, int M, bool bluestein);
+int launch_fused(int which, const SpecArgs& a, cudaStream_t s);
+
 }  // namespace dbx

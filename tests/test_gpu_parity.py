@@ -266,6 +266,24 @@ def test_dst_engines_match_oracle(dev, oracle, n1, n2, engine):
         assert rel(dev.precondition_apply(d, r, engine=eng), ref) <= OP_TOL
 
 
+@pytest.mark.parametrize("name,n,iters,conv", [("C1", 256, 8, "Fft"), ("C2", 512, 5, "Auto"), ("C3", 1024, 3, "Auto")])
+@pytest.mark.parametrize("fusion", [True, False])
+def test_fused_pipeline_full_size(dev, oracle, name, n, iters, conv, fusion):
+    """The fused row pipelines (fused.cu) at the compiled full-size shapes:
+    C1 (conv 270, direct DST 255), C2 (conv 540, Bluestein 1024), C3 (conv
+    1080, direct DST 1023); fused and unfused must both match the oracle."""
+    from paper_1211_0393_b200 import configs as cf
+    c = cf.CONFIGS[name]
+    f, g, taps = cf.make_problem(c, n=n)
+    op = dev.BlurOperator(dev.Psf(taps), dev.BoundaryCondition.AntiReflective, n, n)
+    op.set_conv(getattr(dev.ConvEngine, conv)).set_fusion(fusion)
+    d = dev.build_tikhonov(dev.Psf(taps), dev.PreconditionerSpec(dev.Algebra.AntiReflective, c.alpha), n, n)
+    run = dev.d_landweber(op, d, g, dev.SolverConfig(max_iters=iters, track_rre_against=f), keep_iterates=True)
+    ref = oracle.landweber(taps, g, d=oracle.build_tikhonov(taps, c.alpha, n, n), f_true=f, max_iters=iters,
+                           keep_iterates=True)
+    _trajectory_check(run, ref)
+
+
 @pytest.mark.parametrize("conv,dst", [("Direct", "Dense"), ("Fft", "Fft"), ("Direct", "Fft"), ("Fft", "Dense")])
 def test_engine_combinations_same_trajectory(dev, oracle, conv, dst):
     from paper_1211_0393_b200 import configs as cf
