@@ -30,7 +30,7 @@ from typing import List, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdbx.so")
+LIB_PATH = os.environ.get("DBX_LIB", os.path.join(_HERE, "libdbx.so"))  # DBX_LIB: A/B builds
 
 DBX_OK, DBX_EINVAL, DBX_EDIVERGED, DBX_ECUDA = 0, 1, 2, 3
 

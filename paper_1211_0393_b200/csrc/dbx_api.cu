@@ -218,7 +218,7 @@ struct dbx_plan {
   bool conv_ready = false;
   int L1 = 0, L2 = 0, Lh = 0;
   double *tw1 = nullptr, *tw2 = nullptr, *HA = nullptr, *HAt = nullptr;
-  DevBuf zb, yb;
+  DevBuf zb, yb, dT;  // dT: filter grid transposed (fused column pass)
   struct Blue {
     bool ready = false;
     double *tw = nullptr, *chirp = nullptr, *bhat = nullptr, *p = nullptr;
@@ -236,7 +236,7 @@ struct dbx_plan {
       if (p) cudaFree(p);
     for (double* p : owned) cudaFree(p);
     if (st) cudaFree(st);
-    for (DevBuf* b : {&g, &f, &r, &s, &u, &X3, &in, &out, &part, &rre, &res, &xh, &zb, &yb}) b->release();
+    for (DevBuf* b : {&g, &f, &r, &s, &u, &X3, &in, &out, &part, &rre, &res, &xh, &zb, &yb, &dT}) b->release();
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -697,6 +697,9 @@ int dbx_precond_build(dbx_plan* P, double alpha) {
     P->have_d = false;
     require(alpha > 0.0 || hflag == 0, "tikhonov_filter: alpha = 0 with a zero eigenvalue");
     P->have_d = true;
+    P->dT.ensure(P->N);
+    launch_transpose(P->d, P->dT.p, P->n1, P->n2, P->stream);
+    ck(cudaStreamSynchronize(P->stream), "transpose");
   });
 }
 
@@ -718,6 +721,9 @@ int dbx_precond_set_eigs(dbx_plan* P, const double* dd) {
     ck(cudaMemcpyAsync(P->d, dd, P->N * sizeof(double), cudaMemcpyDefault, P->stream), "copy");
     ck(cudaStreamSynchronize(P->stream), "sync");
     P->have_d = true;
+    P->dT.ensure(P->N);
+    launch_transpose(P->d, P->dT.p, P->n1, P->n2, P->stream);
+    ck(cudaStreamSynchronize(P->stream), "transpose");
   });
 }
 
@@ -829,7 +835,7 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
 
     // Fused FFT-form pipeline (fused.cu): 6 launches + finalize per iteration.
     P->prepare(use_precond != 0);
-    const bool fused = use_precond && P->use_fft_conv() && P->use_fft_dst(false) && P->fusion &&
+    const bool fused = use_precond && P->n1 == P->n2 && P->use_fft_conv() && P->use_fft_dst(false) && P->fusion &&
                        fused_supported(P->L2, P->blue_tables(1, false).M,
                                        P->blue_tables(1, false).M != P->blue_tables(1, false).N);
     SpecArgs fa0 = P->spec_base(P->st, pt);
@@ -845,6 +851,8 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
       fa0.g = gd;
       fa0.f = fd;
       fa0.tau = tau;
+      fa0.ztrans = 1;
+      fa0.dT = P->dT.p;
     }
     auto enqueue_pre = [&]() {
       if (!fused) return;
@@ -863,10 +871,10 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
       // K2: inverse row FFT -> A'r rows -> T~ along rows -> u
       a.out = P->u.p; a.outsel = SEL_EXPLICIT;
       P->ev_begin(KC_TRANSFORM); lc(launch_fused(FUSED_AINV_TT, a, s), "rows_ainv_tt"); P->ev_end();
-      // K3: columns: T~ -> d -> T
+      // K3: columns of u (= rows of u^T, contiguous): T~ -> d -> T, into row-major s
       a.in = P->u.p; a.insel = SEL_EXPLICIT; a.out = P->s.p; a.outsel = SEL_EXPLICIT;
       a.kind1 = DBX_KIND_ARINV; a.kind2 = DBX_KIND_AR; a.epi = SPEC_STORE;
-      P->ev_begin(KC_TRANSFORM); lc(launch_dst_cols(a, s), "launch_dst_cols"); P->ev_end();
+      P->ev_begin(KC_TRANSFORM); lc(launch_fused(FUSED_DST_TCOLS, a, s), "dst_tcols"); P->ev_end();
       // K4: T along rows -> x_k = x_{k-1} + tau (.) + norms -> forward row FFT for A x_k
       a.in = P->s.p; a.out = P->X3.p; a.outsel = SEL_NXT; a.xold = P->X3.p; a.xoldsel = SEL_CUR;
       P->ev_begin(KC_TRANSFORM);

@@ -108,5 +108,6 @@ void launch_state_init(ImgState* st, int batch, cudaStream_t s);
 void launch_select_copy(const double* X3, const ImgState* st, int which_best, int batch,
                         size_t N, double* out, cudaStream_t s);
 void launch_zero(double* p, size_t n, cudaStream_t s);
+void launch_transpose(const double* in, double* out, int rows, int cols, cudaStream_t s);
 
 }  // namespace dbx

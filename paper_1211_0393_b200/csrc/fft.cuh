@@ -19,6 +19,10 @@
 
 #include "dft_consts.h"
 
+#ifndef DBX_KU
+#define DBX_KU 1  // output pairs per trip of the packed large-prime stage
+#endif
+
 namespace dbx {
 namespace fft {
 
@@ -222,6 +226,20 @@ __device__ __forceinline__ void dft(double2* v) {
   else dft_odd<R, S>(v);
 }
 
+// Stage twiddles W^{r k}, r = 1..R-1, from ONE table read (W^k): the powers
+// come from a balanced product tree (w_r = w_{r/2} w_{r - r/2}, depth log2 R,
+// <= ~4 ulp), which removes (R-2)/(R-1) of the per-stage twiddle traffic on
+// the shared-memory pipe (the FFT stages are smem-bandwidth bound).
+template <int R>
+__device__ __forceinline__ void twiddle_powers(double2* w, double2 w1) {
+  w[0] = w1;
+#pragma unroll
+  for (int r = 2; r < R; ++r) {
+    const int a = r / 2;
+    w[r - 1] = cmul(w[a - 1], w[r - a - 1]);
+  }
+}
+
 // One Stockham stage on a padded in-smem line.
 template <int L, int Ns, int R, int S, int T>
 __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ tw, int t) {
@@ -239,7 +257,7 @@ __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ 
       if (NB % T == 0 || b < NB) {
         const int k = b % Ns;
 #pragma unroll
-        for (int r = 1; r < R; ++r) w[i][r - 1] = tw[r * k * step];  // smem- or global-resident table
+        twiddle_powers<R>(w[i], tw[k * step]);
       }
     }
   }
@@ -322,7 +340,7 @@ __device__ __forceinline__ void stage_split(double2* buf, const double2* __restr
     constexpr int step = L / (Ns * R);
     if (act) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) w[r - 1] = tw[r * k * step];  // smem- or global-resident table
+      twiddle_powers<R>(w, tw[k * step]);
     }
   }
   if (act) {
@@ -397,7 +415,7 @@ __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __rest
     constexpr int step = L / (Ns * R);
     if (act) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) w[r - 1] = tw[r * k * step];  // smem- or global-resident table
+      twiddle_powers<R>(w, tw[k * step]);
     }
   }
   if (act) {
@@ -422,23 +440,41 @@ __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __rest
     }
     const int base = (b / Ns) * Ns * R + k;
     buf[pad<L>(base)] = sum;
+    // KU output pairs per trip: 4*KU independent FMA chains hide the DFMA
+    // latency (one pair alone leaves 4 chains of depth H).
+    constexpr int KU = DBX_KU;
 #pragma unroll 1
-    for (int kk = 1; kk <= H; ++kk) {
-      double2 A = x0, B = make_double2(0.0, 0.0);
-      int e = 0;
+    for (int k0 = 1; k0 <= H; k0 += KU) {
+      double2 A[KU], B[KU];
+      int e[KU];
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        A[u] = x0;
+        B[u] = make_double2(0.0, 0.0);
+        e[u] = 0;
+      }
 #pragma unroll
       for (int j = 1; j <= H; ++j) {
-        e += kk;
-        if (e >= R) e -= R;
-        const double c = K::c(e), s = K::s(e);
-        A.x = fma(c, v[j].x, A.x);
-        A.y = fma(c, v[j].y, A.y);
-        B.x = fma(s, v[R - j].x, B.x);
-        B.y = fma(s, v[R - j].y, B.y);
+#pragma unroll
+        for (int u = 0; u < KU; ++u) {
+          e[u] += k0 + u;
+          if (e[u] >= R) e[u] -= R;
+          const double c = K::c(e[u]), s = K::s(e[u]);
+          A[u].x = fma(c, v[j].x, A[u].x);
+          A[u].y = fma(c, v[j].y, A[u].y);
+          B[u].x = fma(s, v[R - j].x, B[u].x);
+          B[u].y = fma(s, v[R - j].y, B[u].y);
+        }
       }
-      const double2 sb = mul_si<S>(B);
-      buf[pad<L>(base + kk * Ns)] = cadd(A, sb);
-      buf[pad<L>(base + (R - kk) * Ns)] = csub(A, sb);
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int kk = k0 + u;
+        if (kk <= H) {
+          const double2 sb = mul_si<S>(B[u]);
+          buf[pad<L>(base + kk * Ns)] = cadd(A[u], sb);
+          buf[pad<L>(base + (R - kk) * Ns)] = csub(A[u], sb);
+        }
+      }
     }
   }
   (void)nthreads;

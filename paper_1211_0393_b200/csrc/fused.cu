@@ -92,10 +92,12 @@ __device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, 
   }
   __syncthreads();
   fft::fft<L2, -1, NT>(buf, tw, t);
+  // spectra stored transposed ([k][row]): the column pass then reads each
+  // column contiguously; the pair's two rows share one 32-byte sector per k
   for (int k = t; k < Lh; k += NT) {
     const double2 zk = buf[pad<L2>(k)], zm = buf[pad<L2>(k == 0 ? 0 : L2 - k)];
-    if (ra < n1) Z[(size_t)ra * Lh + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-    if (rb < n1) Z[(size_t)rb * Lh + k] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+    if (ra < n1) Z[(size_t)k * n1 + ra] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    if (rb < n1) Z[(size_t)k * n1 + rb] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
   }
 }
 
@@ -138,10 +140,82 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
   });
   blue_core<M, TD, 2, BLUE>(sm, buf, bt, twd, t);
   if (live) {
-    double* u = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + (size_t)r * n2;
+    // u stored transposed (u^T[k][r]): the column pass reads it contiguously
+    double* uT = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + r;
     const double al = bt.alpha;
     for (int k = t; k < n2; k += TD)
-      u[k] = (k == 0) ? al * v0 : (k == n2 - 1) ? al * ve : blue_out<M, BLUE>(buf, bt, k);
+      uT[(size_t)k * n1] = (k == 0) ? al * v0 : (k == n2 - 1) ? al * ve : blue_out<M, BLUE>(buf, bt, k);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Column half of D on the transposed intermediate: line c of u^T (column c of
+// u) is contiguous.  T~ -> multiply by d^T[c][.] -> T, result written into the
+// row-major s (two adjacent columns per CTA).
+template <int M, bool BLUE>
+__global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(SpecArgs a) {
+  constexpr int TD = line_threads(M, dst_per(M));
+  using SMP = DstSmem<M, 2, BLUE>;
+  constexpr int LMAX = SMP::LMAX;
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 sm[];
+  const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
+  double2* buf = sm + g * padded_len(M);
+  const int n = a.n1, n2 = a.n2;
+  const size_t N = (size_t)n * n2;
+  const BlueTables& bt = a.blue1;
+  const double2* tw = stage_twiddles<M, SMP::TW>(
+      reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + SMP::tw_off), bt.tw);
+  double* dS = reinterpret_cast<double*>(sm + 2 * padded_len(M)) + g * 2 * LMAX;  // d^T line
+  double* midS = dS + LMAX;
+  const int c = 2 * blockIdx.x + g;
+  const bool live = c < n2;
+  // d^T row c (contiguous) staged behind the first transform
+  if (live)
+    for (int j = t; j < n; j += TD) cp_async8(dS + j, a.dT + (size_t)c * n + j);
+  cp_async_commit();
+  const double* in = a.in + (size_t)b * N + (size_t)(live ? c : 0) * n;  // u^T line
+  const double v0 = in[0], ve = in[n - 1];
+  const double* p = bt.p;
+  const int NL = bt.N;
+  blue_fill<M, TD, BLUE>(buf, bt, t, [&](int j) {
+    return live ? (in[j] - v0 * __ldg(p + j - 1)) - ve * __ldg(p + n - 2 - j) : 0.0;
+  });
+  blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
+  cp_async_wait_all();
+  __syncthreads();
+  for (int j = t; j < M; j += TD) {
+    double m = 0.0;
+    if (live && j >= 1 && j < NL) m = blue_out<M, BLUE>(buf, bt, j) * dS[j];
+    if (j < LMAX) midS[j] = m;
+  }
+  const double u0 = live ? bt.alpha * v0 * dS[0] : 0.0;
+  const double ue = live ? bt.alpha * ve * dS[n - 1] : 0.0;
+  __syncthreads();
+  for (int j = t; j < M; j += TD) {
+    double2 v = make_double2(0.0, 0.0);
+    if (j >= 1 && j < NL) {
+      const double m = midS[j];
+      v = pre<BLUE>(make_double2(m, (j & 1) ? -m : m), bt, j);
+    }
+    buf[pad<M>(j)] = v;
+  }
+  blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
+  if (live) {
+    double* s = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c;
+    const double ia = 1.0 / bt.alpha, a0 = ia * u0, a1 = ia * ue;
+    for (int k = t; k < n; k += TD) {
+      double w;
+      if (k == 0) w = a0;
+      else if (k == n - 1) w = a1;
+      else {
+        w = blue_out<M, BLUE>(buf, bt, k);
+        w += a0 * __ldg(p + k - 1);
+        w += a1 * __ldg(p + n - 2 - k);
+      }
+      s[(size_t)k * n2] = w;
+    }
   }
 }
 
@@ -284,10 +358,23 @@ int fused_launch(K kernel, const SpecArgs& a, cudaStream_t s) {
   return (int)grid.x;
 }
 
+template <int M, bool BLUE>
+int tcols_launch(const SpecArgs& a, cudaStream_t s) {
+  using SMP = DstSmem<M, 2, BLUE>;
+  static bool init = false;
+  if (!init) {
+    if (!set_smem(dst_tcols<M, BLUE>, SMP::bytes)) return -1;
+    init = true;
+  }
+  dim3 grid((a.n2 + 1) / 2, a.batch);
+  dst_tcols<M, BLUE><<<grid, 2 * line_threads(M, dst_per(M)), SMP::bytes, s>>>(a);
+  return (int)grid.x;
+}
+
 }  // namespace
 
 // (conv L2, DST M, Bluestein?) combinations compiled for the fused pipeline.
-#define DBX_FUSED_LIST(X) X(1080, 1023, false) X(540, 1024, true) X(270, 255, false) X(2160, 4096, true)
+#define DBX_FUSED_LIST(X) X(1080, 1023, false) X(540, 1024, true) X(270, 255, false)
 
 bool fused_supported(int L2, int M, bool blue) {
 #define X(L, MM, BL) if (L2 == (L) && M == (MM) && blue == (BL)) return Fused<L, MM, BL>::bytes <= 200 * 1024;
@@ -304,6 +391,7 @@ int launch_fused(int which, const SpecArgs& a, cudaStream_t s) {
     if (which == FUSED_AINV_TT) return fused_launch<L, MM, BL, 0>(rows_ainv_tt<L, MM, BL>, a, s); \
     if (which == FUSED_T_AXPY_AFWD) return fused_launch<L, MM, BL, 1>(rows_t_axpy_afwd<L, MM, BL>, a, s); \
     if (which == FUSED_AINV_RESID) return fused_launch<L, MM, BL, 2>(rows_ainv_resid<L, MM, BL>, a, s); \
+    if (which == FUSED_DST_TCOLS) return tcols_launch<MM, BL>(a, s);                             \
   }
   DBX_FUSED_LIST(X)
 #undef X

@@ -163,6 +163,21 @@ __global__ void select_copy_kernel(const double* X3, const ImgState* st, int whi
     dst[i] = src[i];
 }
 
+// out[c][r] = in[r][c] through a 32 x 33 shared tile (coalesced both ways).
+__global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out, int rows, int cols) {
+  __shared__ double tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = in[(size_t)r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[(size_t)c * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
 __global__ void zero_kernel(double* p, size_t n) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
@@ -204,6 +219,11 @@ void launch_select_copy(const double* X3, const ImgState* st, int which_best, in
                         size_t N, double* out, cudaStream_t s) {
   dim3 grid((unsigned)((N + 255) / 256 < 1024 ? (N + 255) / 256 : 1024), batch);
   select_copy_kernel<<<grid, 256, 0, s>>>(X3, st, which_best, batch, N, out);
+}
+
+void launch_transpose(const double* in, double* out, int rows, int cols, cudaStream_t s) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols);
 }
 
 void launch_zero(double* p, size_t n, cudaStream_t s) {

@@ -71,10 +71,13 @@ conv_row_fwd(SpecArgs a) {
   __syncthreads();
   fft::fft<L2, -1, T>(buf, tw, t);
   double2* Z = a.zbuf + (size_t)b * n1 * Lh;
+  // ztrans: spectra stored [k][row] so the column pass reads contiguously;
+  // the pair's two rows are adjacent (one 32-byte sector per k)
+  const size_t sr = a.ztrans ? 1 : (size_t)Lh, sk = a.ztrans ? (size_t)n1 : 1;
   for (int k = t; k < Lh; k += T) {
     const double2 zk = buf[pad<L2>(k)], zm = buf[pad<L2>(k == 0 ? 0 : L2 - k)];
-    if (ra < n1) Z[(size_t)ra * Lh + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-    if (rb < n1) Z[(size_t)rb * Lh + k] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+    if (ra < n1) Z[ra * sr + k * sk] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    if (rb < n1) Z[rb * sr + k * sk] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
   }
 }
 
@@ -106,28 +109,35 @@ conv_col(SpecArgs a) {
   // (loads batched in registers first, then stored)
   constexpr int PF = (L1 * G + NT - 1) / NT;
   double2 v[PF];
+  // element (rho, k) of the spectra: [rho][k] (default) or [k][rho] (ztrans,
+  // contiguous per column: each line's loads are fully coalesced)
+  const size_t sr = a.ztrans ? 1 : (size_t)Lh, sk = a.ztrans ? (size_t)n1 : 1;
 #pragma unroll
   for (int i = 0; i < PF; ++i) {
     const int idx = threadIdx.x + i * NT;
-    const int p = idx / G, gg = idx - p * G, k = k0 + gg;
+    // ztrans: thread-contiguous along p within one line; else along k
+    const int p = a.ztrans ? idx % L1 : idx / G;
+    const int gg = a.ztrans ? idx / L1 : idx - p * G;
+    const int k = k0 + gg;
     v[i] = make_double2(0.0, 0.0);
     if (idx < L1 * G && k < Lh && p < hext_rows) {
       const int rho = p - q1;
       if (rho < 0) {
-        const double2 z0 = Z[k], zi = Z[(size_t)(-rho) * Lh + k];
+        const double2 z0 = Z[k * sk], zi = Z[(size_t)(-rho) * sr + k * sk];
         v[i] = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
       } else if (rho >= n1) {
-        const double2 z0 = Z[(size_t)(n1 - 1) * Lh + k], zi = Z[(size_t)(2 * (n1 - 1) - rho) * Lh + k];
+        const double2 z0 = Z[(size_t)(n1 - 1) * sr + k * sk], zi = Z[(size_t)(2 * (n1 - 1) - rho) * sr + k * sk];
         v[i] = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
       } else {
-        v[i] = Z[(size_t)rho * Lh + k];
+        v[i] = Z[(size_t)rho * sr + k * sk];
       }
     }
   }
 #pragma unroll
   for (int i = 0; i < PF; ++i) {
     const int idx = threadIdx.x + i * NT;
-    const int p = idx / G, gg = idx - p * G;
+    const int p = a.ztrans ? idx % L1 : idx / G;
+    const int gg = a.ztrans ? idx / L1 : idx - p * G;
     if (idx < L1 * G) sm[gg * padded_len(L1) + pad<L1>(p)] = v[i];
   }
   cp_async_wait_group<1>();  // twiddles landed (H may still be in flight)

@@ -47,8 +47,10 @@ struct SpecArgs {
   Partials part{nullptr, 0};
   // FFT correlation
   ConvTables conv;
-  double2* zbuf = nullptr;                       // [batch][n1][Lh]
+  double2* zbuf = nullptr;                       // [batch][n1][Lh], or [batch][Lh][n1] if ztrans
   double2* ybuf = nullptr;                       // [batch][n1][Lh]
+  int ztrans = 0;                                // fused pipeline: row-FFT spectra stored transposed
+  const double* dT = nullptr;                    // d transposed [n2][n1] (fused column pass)
   // DST
   int kind1 = DBX_KIND_ARINV, kind2 = -1;
   BlueTables blue1;                              // columns (length n1)
@@ -69,7 +71,7 @@ int launch_dst_rows(const SpecArgs& a, cudaStream_t s);
 int launch_dst_cols(const SpecArgs& a, cudaStream_t s);
 
 // Fused row pipelines of the preconditioned iteration (fused.cu).
-enum FusedKind { FUSED_AINV_TT = 0, FUSED_T_AXPY_AFWD = 1, FUSED_AINV_RESID = 2 };
+enum FusedKind { FUSED_AINV_TT = 0, FUSED_T_AXPY_AFWD = 1, FUSED_AINV_RESID = 2, FUSED_DST_TCOLS = 3 };
 bool fused_supported(int L2, int M, bool bluestein);
 int launch_fused(int which, const SpecArgs& a, cudaStream_t s);
 
