@@ -221,7 +221,7 @@ struct dbx_plan {
   DevBuf zb, yb, dT;  // dT: filter grid transposed (fused column pass)
   struct Blue {
     bool ready = false;
-    double *tw = nullptr, *chirp = nullptr, *bhat = nullptr, *p = nullptr;
+    double *tw = nullptr, *chirp = nullptr, *bhat = nullptr, *p = nullptr, *sn = nullptr;
     BlueTables t;
   } blue[2][2];  // [axis 0 = columns (n1), 1 = rows (n2)][0 = AR kinds, 1 = SineI]
   std::vector<double*> owned;
@@ -298,6 +298,8 @@ struct dbx_plan {
       B.chirp = upload_owned(h.chirp);
       B.bhat = upload_owned(h.bhat);
       B.p = upload_owned(h.p);
+      B.sn = upload_owned(h.sn);
+      B.t.sn = B.sn;
       B.t.tw = reinterpret_cast<const double2*>(B.tw);
       B.t.chirp = reinterpret_cast<const double2*>(B.chirp);
       B.t.bhat = reinterpret_cast<const double2*>(B.bhat);

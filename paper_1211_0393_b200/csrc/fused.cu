@@ -151,71 +151,85 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
 // ---------------------------------------------------------------------------
 // Column half of D on the transposed intermediate: line c of u^T (column c of
 // u) is contiguous.  T~ -> multiply by d^T[c][.] -> T, result written into the
-// row-major s (two adjacent columns per CTA).
+// row-major s.  FOUR adjacent columns per CTA, two per packed complex DFT
+// (pk_fill / pk_split), so the row-major stores are full 32-byte sectors.
+template <int M, bool BLUE>
+struct TcolSmem {
+  static constexpr int TD = line_threads(M, dst_per(M));
+  static constexpr int LMAX = BLUE ? M / 2 + 1 : M + 1;         // max line length n
+  static constexpr int LS = (LMAX + 1) / 2 * 2 + 4;             // line stride (doubles): 4 lines hit distinct banks
+  static constexpr size_t off_io = (size_t)2 * padded_len(M) * 16;
+  static constexpr size_t off_d = off_io + (size_t)4 * LS * 8;
+  static constexpr size_t off_tw = off_d + (size_t)4 * LS * 8;
+  static constexpr bool TW = off_tw + (size_t)M * 16 <= 113 * 1024;  // keep 2 CTAs / SM
+  static constexpr size_t bytes = TW ? off_tw + (size_t)M * 16 : off_tw;
+};
+
 template <int M, bool BLUE>
 __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(SpecArgs a) {
-  constexpr int TD = line_threads(M, dst_per(M));
-  using SMP = DstSmem<M, 2, BLUE>;
-  constexpr int LMAX = SMP::LMAX;
+  using S = TcolSmem<M, BLUE>;
+  constexpr int TD = S::TD, NT = 2 * TD, LS = S::LS;
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 sm[];
-  const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
-  double2* buf = sm + g * padded_len(M);
+  __shared__ double e0[4], e1[4];
+  char* base = reinterpret_cast<char*>(sm);
+  double* io = reinterpret_cast<double*>(base + S::off_io);  // 4 lines: input, then DST outputs
+  double* dS = reinterpret_cast<double*>(base + S::off_d);   // 4 d^T lines
+  const BlueTables& bt = a.blue1;
+  const double2* tw = stage_twiddles<M, S::TW>(reinterpret_cast<double2*>(base + S::off_tw), bt.tw);
   const int n = a.n1, n2 = a.n2;
   const size_t N = (size_t)n * n2;
-  const BlueTables& bt = a.blue1;
-  const double2* tw = stage_twiddles<M, SMP::TW>(
-      reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + SMP::tw_off), bt.tw);
-  double* dS = reinterpret_cast<double*>(sm + 2 * padded_len(M)) + g * 2 * LMAX;  // d^T line
-  double* midS = dS + LMAX;
-  const int c = 2 * blockIdx.x + g;
-  const bool live = c < n2;
-  // d^T row c (contiguous) staged behind the first transform
-  if (live)
-    for (int j = t; j < n; j += TD) cp_async8(dS + j, a.dT + (size_t)c * n + j);
+  const int c0 = 4 * blockIdx.x;
+  const int nl = n2 - c0 < 4 ? n2 - c0 : 4;
+  stage_lines(io, LS, a.in + (size_t)b * N + (size_t)c0 * n, nl, n);  // u^T lines
   cp_async_commit();
-  const double* in = a.in + (size_t)b * N + (size_t)(live ? c : 0) * n;  // u^T line
-  const double v0 = in[0], ve = in[n - 1];
+  stage_lines(dS, LS, a.dT + (size_t)c0 * n, nl, n);                   // d^T lines
+  cp_async_commit();
+  cp_async_wait_group<1>();
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    const int h = threadIdx.x;
+    e0[h] = h < nl ? io[h * LS] : 0.0;
+    e1[h] = h < nl ? io[h * LS + n - 1] : 0.0;
+  }
+  const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
+  double2* buf = sm + g * padded_len(M);
   const double* p = bt.p;
-  const int NL = bt.N;
-  blue_fill<M, TD, BLUE>(buf, bt, t, [&](int j) {
-    return live ? (in[j] - v0 * __ldg(p + j - 1)) - ve * __ldg(p + n - 2 - j) : 0.0;
+  // T~ (ar_inverse, transforms.hpp:163-173) of lines 2g, 2g+1
+  pk_fill<M, TD, BLUE>(buf, bt, t, [&](int hh, int j) {
+    const int h = 2 * g + hh;
+    if (h >= nl) return 0.0;
+    const double* L = io + h * LS;
+    return (L[j] - L[0] * __ldg(p + j - 1)) - L[n - 1] * __ldg(p + n - 2 - j);
   });
   blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
+  pk_split<M, BLUE>(buf, bt, io + (2 * g) * LS, io + (2 * g + 1) * LS, t, TD);
+  __syncthreads();
+  odd_scans(io, LS, 4, bt);
   cp_async_wait_all();
   __syncthreads();
-  for (int j = t; j < M; j += TD) {
-    double m = 0.0;
-    if (live && j >= 1 && j < NL) m = blue_out<M, BLUE>(buf, bt, j) * dS[j];
-    if (j < LMAX) midS[j] = m;
-  }
-  const double u0 = live ? bt.alpha * v0 * dS[0] : 0.0;
-  const double ue = live ? bt.alpha * ve * dS[n - 1] : 0.0;
-  __syncthreads();
-  for (int j = t; j < M; j += TD) {
-    double2 v = make_double2(0.0, 0.0);
-    if (j >= 1 && j < NL) {
-      const double m = midS[j];
-      v = pre<BLUE>(make_double2(m, (j & 1) ? -m : m), bt, j);
-    }
-    buf[pad<M>(j)] = v;
-  }
+  // v = u o d (u_0 = alpha v_0, u_{n-1} = alpha v_{n-1}), then T (ar_forward)
+  pk_fill<M, TD, BLUE>(buf, bt, t, [&](int hh, int j) {
+    const int h = 2 * g + hh;
+    return h < nl ? io[h * LS + j] * dS[h * LS + j] : 0.0;
+  });
   blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
-  if (live) {
-    double* s = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c;
-    const double ia = 1.0 / bt.alpha, a0 = ia * u0, a1 = ia * ue;
-    for (int k = t; k < n; k += TD) {
-      double w;
-      if (k == 0) w = a0;
-      else if (k == n - 1) w = a1;
-      else {
-        w = blue_out<M, BLUE>(buf, bt, k);
-        w += a0 * __ldg(p + k - 1);
-        w += a1 * __ldg(p + n - 2 - k);
-      }
-      s[(size_t)k * n2] = w;
-    }
+  pk_split<M, BLUE>(buf, bt, io + (2 * g) * LS, io + (2 * g + 1) * LS, t, TD);
+  __syncthreads();
+  odd_scans(io, LS, 4, bt);
+  __syncthreads();
+  // T output w_0 = v_0 / alpha = e0 d_0, w_{n-1} = e1 d_{n-1}, interior DST + ramp
+  double* s = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c0;
+  for (int idx = threadIdx.x; idx < 4 * n; idx += NT) {
+    const int k = idx >> 2, h = idx & 3;
+    if (h >= nl) continue;
+    const double a0 = e0[h] * dS[h * LS], a1 = e1[h] * dS[h * LS + n - 1];
+    double w;
+    if (k == 0) w = a0;
+    else if (k == n - 1) w = a1;
+    else w = io[h * LS + k] + a0 * __ldg(p + k - 1) + a1 * __ldg(p + n - 2 - k);
+    s[(size_t)k * n2 + h] = w;
   }
 }
 
@@ -360,14 +374,14 @@ int fused_launch(K kernel, const SpecArgs& a, cudaStream_t s) {
 
 template <int M, bool BLUE>
 int tcols_launch(const SpecArgs& a, cudaStream_t s) {
-  using SMP = DstSmem<M, 2, BLUE>;
+  using SMP = TcolSmem<M, BLUE>;
   static bool init = false;
   if (!init) {
     if (!set_smem(dst_tcols<M, BLUE>, SMP::bytes)) return -1;
     init = true;
   }
-  dim3 grid((a.n2 + 1) / 2, a.batch);
-  dst_tcols<M, BLUE><<<grid, 2 * line_threads(M, dst_per(M)), SMP::bytes, s>>>(a);
+  dim3 grid((a.n2 + 3) / 4, a.batch);
+  dst_tcols<M, BLUE><<<grid, 2 * SMP::TD, SMP::bytes, s>>>(a);
   return (int)grid.x;
 }
 

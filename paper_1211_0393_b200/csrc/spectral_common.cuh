@@ -283,6 +283,115 @@ __device__ __forceinline__ double blue_out(const double2* buf, const BlueTables&
   return (k & 1) == 0 ? 0.5 * bt.scale * (zm.y - zl.y) : 0.5 * bt.scale * (zl.x - zm.x);
 }
 
+// ---------------------------------------------------------------------------
+// Packed real DST-I: TWO real lines per complex N-point DFT.
+//   y_j = sin(pi j/N) (x_j + x_{N-j}) + (x_j - x_{N-j}) / 2   (j in [1, N), y_0 = 0)
+//   Y = DFT_N(y):  X_{2l} = -Im Y_l,  X_1 = Re Y_0 / 2,  X_{2l+1} = X_{2l-1} + Re Y_l
+// (X_k = sum_j x_j sin(pi j k / N)).  Two lines a, b share one DFT of
+// z = y^a + i y^b and are separated by conjugate symmetry, so the transform
+// count is half that of one complex DFT per line; the odd outputs are a
+// prefix sum (odd_scan).  Works for any N (odd or even).
+// val(h, j): interior value x^h_j, h in {0, 1} (line a / b), j in [1, N).
+template <int M, int T, bool BLUE, typename F>
+__device__ __forceinline__ void pk_fill(double2* buf, const BlueTables& bt, int t, F val) {
+  const int N = bt.N;
+  constexpr int PF = (M + T - 1) / T;
+  double2 z[PF];
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int j = t + i * T;
+    z[i] = make_double2(0.0, 0.0);
+    if (j >= 1 && j < N) {
+      const double s = __ldg(bt.sn + j);
+      const double xa = val(0, j), xar = val(0, N - j);
+      const double xb = val(1, j), xbr = val(1, N - j);
+      z[i] = pre<BLUE>(make_double2(fma(s, xa + xar, 0.5 * (xa - xar)), fma(s, xb + xbr, 0.5 * (xb - xbr))), bt, j);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int j = t + i * T;
+    if (j < M) buf[pad<M>(j)] = z[i];
+  }
+}
+
+// Separate the two lines' spectra (A_l = (Z_l + conj Z_{N-l}) / 2,
+// B_l = (Z_l - conj Z_{N-l}) / 2i) into the DST outputs: even k final (scaled),
+// odd k the scan terms (unscaled) — odd_scan completes them.
+template <int M, bool BLUE>
+__device__ __forceinline__ void pk_split(const double2* buf, const BlueTables& bt, double* oa, double* ob, int t,
+                                         int T) {
+  const int N = bt.N;
+  const double hs = 0.5 * bt.scale;
+  for (int l = t; 2 * l <= N - 1; l += T) {
+    const int m = l == 0 ? 0 : N - l;
+    const double2 zl = pre<BLUE>(buf[pad<M>(l)], bt, l);
+    const double2 zm = pre<BLUE>(buf[pad<M>(m)], bt, m);
+    if (l >= 1) {
+      oa[2 * l] = hs * (zm.y - zl.y);
+      ob[2 * l] = hs * (zl.x - zm.x);
+    }
+    if (2 * l + 1 <= N - 1) {
+      const double f = l == 0 ? 0.25 : 0.5;
+      oa[2 * l + 1] = f * (zl.x + zm.x);
+      ob[2 * l + 1] = f * (zl.y + zm.y);
+    }
+  }
+}
+
+// One warp: inclusive prefix sums of o[1], o[3], ..., o[2 cnt - 1], scaled.
+__device__ __forceinline__ void odd_scan(double* o, int cnt, double sc, int lane) {
+  double carry = 0.0;
+  for (int base = 0; base < cnt; base += 8 * 32) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = base + i * 32 + lane;
+      v[i] = m < cnt ? o[2 * m + 1] : 0.0;
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double y = __shfl_up_sync(0xffffffffu, v[i], d);
+        if (lane >= d) v[i] += y;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double tot = __shfl_sync(0xffffffffu, v[i], 31);
+      const int m = base + i * 32 + lane;
+      if (m < cnt) o[2 * m + 1] = (v[i] + carry) * sc;
+      carry += tot;
+    }
+  }
+}
+
+// Scans of `nlines` output lines of stride LS (doubles), spread over the warps.
+__device__ __forceinline__ void odd_scans(double* o, int LS, int nlines, const BlueTables& bt) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int s = w; s < nlines; s += nw) odd_scan(o + (size_t)s * LS, bt.N / 2, bt.scale, lane);
+}
+
+// cp.async copy of `nl` contiguous lines of n doubles (src) into smem lines of
+// stride LS (dst); 16-byte copies when n and both bases allow it.
+__device__ __forceinline__ void stage_lines(double* dst, int LS, const double* src, int nl, int n) {
+  const int nt = blockDim.x;
+  const bool v16 = ((n | LS) & 1) == 0 && (((unsigned long long)src | (unsigned long long)__cvta_generic_to_shared(dst)) & 15) == 0;
+  if (v16) {
+    const int h2 = n >> 1;
+    for (int i = threadIdx.x; i < nl * h2; i += nt) {
+      const int h = i / h2, j = 2 * (i - h * h2);
+      cp_async16(dst + (size_t)h * LS + j, src + (size_t)h * n + j);
+    }
+  } else {
+    for (int i = threadIdx.x; i < nl * n; i += nt) {
+      const int h = i / n, j = i - h * n;
+      cp_async8(dst + (size_t)h * LS + j, src + i);
+    }
+  }
+}
+
 template <typename K>
 bool set_smem(K kernel, size_t bytes) {
   if (bytes > 227 * 1024) return false;

@@ -96,6 +96,9 @@ BlueHost bluestein(int n, bool sine_i, int M) {
     blue_chirp(b, N, M);
   }
   ar_ramp(b, n, sine_i);
+  // sine pre-twiddle of the packed real DST (spectral_common.cuh, pk_fill)
+  b.sn.assign((size_t)N, 0.0);
+  for (long j = 1; j < N; ++j) b.sn[(size_t)j] = (double)sinl(kPiL * (long double)j / (long double)N);
   return b;
 }
 

@@ -15,7 +15,7 @@ std::vector<double> conv_spectrum(const double* w, int q1, int q2, int L1, int L
 struct BlueHost {
   int n = 0, N = 0, M = 0;
   double alpha = 1.0, scale = 1.0;
-  std::vector<double> tw, chirp, bhat, p;
+  std::vector<double> tw, chirp, bhat, p, sn;  // sn[j] = sin(pi j / N), j < N
 };
 
 // Bluestein tables of the DST-I of one line: AR kinds (sine_i = false) use the
