@@ -247,18 +247,15 @@ __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ 
   constexpr int PER = (NB + T - 1) / T;
   constexpr int NW = Ns > 1 ? R - 1 : 1;
   double2 v[PER][R];
-  double2 w[PER][NW];
-  // twiddles first: their (L1/L2) latency overlaps the smem loads and barrier
+  double2 w1[PER];
+  // base twiddles first: their (L1/L2) latency overlaps the smem loads and
+  // the barrier; the powers are formed per butterfly after it (registers)
   if constexpr (Ns > 1) {
     constexpr int step = L / (Ns * R);
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int b = t + i * T;
-      if (NB % T == 0 || b < NB) {
-        const int k = b % Ns;
-#pragma unroll
-        twiddle_powers<R>(w[i], tw[k * step]);
-      }
+      if (NB % T == 0 || b < NB) w1[i] = tw[(b % Ns) * step];
     }
   }
 #pragma unroll
@@ -276,9 +273,11 @@ __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ 
     if (NB % T == 0 || b < NB) {
       const int k = b % Ns;
       if constexpr (Ns > 1) {
+        double2 w[NW];
+        twiddle_powers<R>(w, w1[i]);
 #pragma unroll
         for (int r = 1; r < R; ++r)
-          v[i][r] = S < 0 ? cmul(v[i][r], w[i][r - 1]) : cmulc(v[i][r], w[i][r - 1]);
+          v[i][r] = S < 0 ? cmul(v[i][r], w[r - 1]) : cmulc(v[i][r], w[r - 1]);
       }
       const int base = (b / Ns) * Ns * R + k;
       if constexpr (R >= 7 && (R & 1)) {

@@ -1,8 +1,8 @@
 // fused.cu — fused row pipelines of the preconditioned iteration (FFT-form
-// blur + FFT-form AR transform).  One CTA owns one PAIR of image rows (the
-// two rows share one packed real-FFT line of length L2 and own two DST lines
-// of length M); every stage stays in shared memory between the passes that
-// used to be separate launches:
+// blur + FFT-form AR transform).  A CTA owns four image rows (two packed
+// real-FFT conv lines of length L2 and two packed real DST lines of length M,
+// two rows per line) or, for rows_ainv_resid, one row pair; every stage stays
+// in shared memory between the passes that used to be separate launches:
 //
 //   rows_ainv_tt      : Y (A' r spectrum) -> inverse row FFT -> s = A'r rows
 //                       -> T~ (AR inverse transform, DST-I) along the rows -> u
@@ -27,31 +27,49 @@ namespace {
 
 template <int L2, int M, bool BLUE>
 struct Fused {
-  static constexpr int TD = line_threads(M, dst_per(M));   // threads per DST line
-  static constexpr int NT = 2 * TD;                         // CTA = two DST lines
+  static constexpr int TD = line_threads(M, dst_per(M));   // threads per line
+  static constexpr int NT = 2 * TD;                         // CTA = two FFT lines
   static constexpr int LC = padded_len(L2);                 // conv line (double2)
   static constexpr int LD = padded_len(M);                  // DST line (double2)
-  static constexpr int WORK = (LC > 2 * LD ? LC : 2 * LD);  // shared work region
-  static constexpr int RROW = L2;                           // real staging row (doubles)
-  // double2 offsets
-  static constexpr int off_real = WORK;                       // 2 rows x RROW doubles
-  static constexpr int off_epi = off_real + RROW;             // 2 ops x 2 rows x RROW doubles
-  static constexpr int off_twd = off_epi + 2 * RROW;          // DST twiddles (M)
-  static constexpr int off_twc = off_twd + M;                 // conv twiddles (L2), if they fit
-  static constexpr bool TWC = (size_t)(off_twc + L2) * 16 <= 110 * 1024;
-  static constexpr size_t bytes = (size_t)(off_twc + (TWC ? L2 : 0)) * 16;
+  static constexpr size_t kBudget = 113 * 1024;             // two CTAs per SM
+  // ---- 4-row kernels (rows_ainv_tt, rows_t_axpy_afwd): two conv lines of
+  // two packed rows each, then two packed DST lines of two rows each
+  static constexpr int W4 = (LC > LD ? LC : LD) * 2;        // work region (double2)
+  static constexpr int LMAX = BLUE ? M / 2 + 1 : M + 1;     // longest row n2
+  static constexpr int LS = (LMAX + 1) / 2 * 2 + 4;         // smem row stride (doubles)
+  static constexpr size_t off_rows = (size_t)W4 * 16;       // 4 rows
+  static constexpr size_t off_x = off_rows + (size_t)4 * LS * 8;  // 4 more rows (t_axpy)
+  // rows_ainv_tt: twiddles after the rows
+  static constexpr size_t tt_twd = off_x;
+  static constexpr bool TT_TWD = tt_twd + (size_t)M * 16 <= kBudget;
+  static constexpr size_t tt_twc = tt_twd + (TT_TWD ? (size_t)M * 16 : 0);
+  static constexpr bool TT_TWC = tt_twc + (size_t)L2 * 16 <= kBudget;
+  static constexpr size_t tt_bytes = tt_twc + (TT_TWC ? (size_t)L2 * 16 : 0);
+  // rows_t_axpy_afwd: v rows (then T output), x rows, twiddles if they fit
+  static constexpr size_t ax_twd = off_x + (size_t)4 * LS * 8;
+  static constexpr bool AX_TWD = ax_twd + (size_t)M * 16 <= kBudget;
+  static constexpr size_t ax_twc = ax_twd + (AX_TWD ? (size_t)M * 16 : 0);
+  static constexpr bool AX_TWC = ax_twc + (size_t)L2 * 16 <= kBudget;
+  static constexpr size_t ax_bytes = ax_twc + (AX_TWC ? (size_t)L2 * 16 : 0);
+  // ---- rows_ainv_resid (two rows, one conv line on all NT threads)
+  static constexpr int RROW = L2;
+  static constexpr size_t rs_rows = (size_t)LC * 16;                 // 2 x RROW doubles
+  static constexpr size_t rs_g = rs_rows + (size_t)RROW * 16;         // g: 2 x RROW doubles
+  static constexpr size_t rs_twc = rs_g + (size_t)RROW * 16;
+  static constexpr bool RS_TWC = rs_twc + (size_t)L2 * 16 <= kBudget;
+  static constexpr size_t rs_bytes = rs_twc + (RS_TWC ? (size_t)L2 * 16 : 0);
 };
 
-// Inverse packed real FFT of rows (ra, rb) from the half spectra Y -> buf.
-template <int L2, int NT>
+// Inverse packed real FFT of rows (ra, rb) from the half spectra Y -> buf
+// (T threads on the line, thread index t).
+template <int L2, int T>
 __device__ __forceinline__ void conv_inv_load(double2* buf, const double2* __restrict__ Y, int ra, int rb,
-                                              int n1, int Lh) {
-  const int t = threadIdx.x;
-  constexpr int PF = (L2 / 2 + 1 + NT - 1) / NT;
+                                              int n1, int Lh, int t) {
+  constexpr int PF = (L2 / 2 + 1 + T - 1) / T;
   double2 A[PF], Bv[PF];
 #pragma unroll
   for (int i = 0; i < PF; ++i) {
-    const int k = t + i * NT;
+    const int k = t + i * T;
     A[i] = make_double2(0.0, 0.0);
     Bv[i] = A[i];
     if (k < Lh) {
@@ -61,7 +79,7 @@ __device__ __forceinline__ void conv_inv_load(double2* buf, const double2* __res
   }
 #pragma unroll
   for (int i = 0; i < PF; ++i) {
-    const int k = t + i * NT;
+    const int k = t + i * T;
     if (k < Lh) {
       buf[pad<L2>(k)] = make_double2(A[i].x - Bv[i].y, A[i].y + Bv[i].x);
       if (k > 0 && k < L2 - k) buf[pad<L2>(L2 - k)] = make_double2(A[i].x + Bv[i].y, Bv[i].x - A[i].y);
@@ -70,81 +88,232 @@ __device__ __forceinline__ void conv_inv_load(double2* buf, const double2* __res
 }
 
 // Forward packed real FFT of two real rows held in shared memory (AR-extended
-// horizontally on the fly, boundary.hpp:56-62) -> half spectra into Z.
-template <int L2, int NT>
-__device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, const double* rowb, bool has_b,
-                                              int n2, int q2, const double2* tw, double2* Z, int ra, int rb,
-                                              int n1, int Lh) {
-  const int t = threadIdx.x;
+// horizontally on the fly, boundary.hpp:56-62) -> half spectra, stored
+// transposed into Z ([k][row]) so the column pass reads each column
+// contiguously.  Every thread of the CTA calls it (CTA-wide barriers).
+template <int L2, int T>
+__device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, const double* rowb, int n2,
+                                              int q2, const double2* tw, double2* Z, int ra, int rb, int n1,
+                                              int Lh, int t) {
   const int wext = n2 + 2 * q2;
+  const bool has_a = ra < n1, has_b = rb < n1;
   auto ext = [&](const double* row, int j) -> double {
     if (j < 0) return 2.0 * row[0] - row[-j];
     if (j >= n2) return 2.0 * row[n2 - 1] - row[2 * (n2 - 1) - j];
     return row[j];
   };
-  for (int p = t; p < L2; p += NT) {
+  for (int p = t; p < L2; p += T) {
     double va = 0.0, vb = 0.0;
     if (p < wext) {
-      va = ext(rowa, p - q2);
+      if (has_a) va = ext(rowa, p - q2);
       if (has_b) vb = ext(rowb, p - q2);
     }
     buf[pad<L2>(p)] = make_double2(va, vb);
   }
   __syncthreads();
-  fft::fft<L2, -1, NT>(buf, tw, t);
-  // spectra stored transposed ([k][row]): the column pass then reads each
-  // column contiguously; the pair's two rows share one 32-byte sector per k
-  for (int k = t; k < Lh; k += NT) {
+  fft::fft<L2, -1, T>(buf, tw, t);
+  for (int k = t; k < Lh; k += T) {
     const double2 zk = buf[pad<L2>(k)], zm = buf[pad<L2>(k == 0 ? 0 : L2 - k)];
-    if (ra < n1) Z[(size_t)k * n1 + ra] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-    if (rb < n1) Z[(size_t)k * n1 + rb] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+    if (has_a) Z[(size_t)k * n1 + ra] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    if (has_b) Z[(size_t)k * n1 + rb] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
   }
 }
 
 // ---------------------------------------------------------------------------
+// rows_ainv_tt: FOUR rows per CTA.  Conv line g (TD threads) inverts the
+// spectra of rows 2g, 2g+1; DST line g then carries T~ of the same two rows
+// (packed real DST).  u is written transposed (u^T[k][row], 32-byte sectors).
 template <int L2, int M, bool BLUE>
 __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecArgs a) {
   using F = Fused<L2, M, BLUE>;
-  constexpr int NT = F::NT, TD = F::TD;
+  constexpr int NT = F::NT, TD = F::TD, LS = F::LS;
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 sm[];
-  double* rowS = reinterpret_cast<double*>(sm + F::off_real);  // 2 x RROW doubles
+  __shared__ double e0[4], e1[4];
+  char* base = reinterpret_cast<char*>(sm);
+  double* rowS = reinterpret_cast<double*>(base + F::off_rows);  // 4 rows: s, then T~ output
   const BlueTables& bt = a.blue2;
-  const double2* twd = stage_twiddles<M, true>(sm + F::off_twd, bt.tw);
-  const double2* twc = stage_twiddles<L2, F::TWC>(sm + F::off_twc, a.conv.tw2);
+  const double2* twd = stage_twiddles<M, F::TT_TWD>(reinterpret_cast<double2*>(base + F::tt_twd), bt.tw);
+  const double2* twc = stage_twiddles<L2, F::TT_TWC>(reinterpret_cast<double2*>(base + F::tt_twc), a.conv.tw2);
+  const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
+  const size_t N = (size_t)n1 * n2;
+  const int r0 = 4 * blockIdx.x;
+  const int nl = n1 - r0 < 4 ? n1 - r0 : 4;
+  const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
+  const int ra = r0 + 2 * g, rb = ra + 1;
+  // A' r rows: inverse packed row FFT (conv line g = rows 2g, 2g+1)
+  double2* cbuf = sm + g * F::LC;
+  conv_inv_load<L2, TD>(cbuf, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t);
+  cp_async_wait_all();
+  __syncthreads();
+  fft::fft<L2, +1, TD>(cbuf, twc, t);
+  for (int c = t; c < n2; c += TD) {
+    const double2 v = cbuf[pad<L2>(c)];
+    rowS[(2 * g) * LS + c] = v.x;
+    rowS[(2 * g + 1) * LS + c] = v.y;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    e0[threadIdx.x] = rowS[threadIdx.x * LS];
+    e1[threadIdx.x] = rowS[threadIdx.x * LS + n2 - 1];
+  }
+  // T~ along the rows (ar_inverse, transforms.hpp:163-173)
+  const double* p = bt.p;
+  double2* dbuf = sm + g * F::LD;
+  pk_fill<M, TD, BLUE>(dbuf, bt, t, [&](int hh, int j) {
+    const int h = 2 * g + hh;
+    if (h >= nl) return 0.0;
+    const double* L = rowS + h * LS;
+    return (L[j] - L[0] * __ldg(p + j - 1)) - L[n2 - 1] * __ldg(p + n2 - 2 - j);
+  });
+  blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
+  pk_split<M, BLUE>(dbuf, bt, rowS + (2 * g) * LS, rowS + (2 * g + 1) * LS, t, TD);
+  __syncthreads();
+  odd_scans(rowS, LS, 4, bt);
+  __syncthreads();
+  double* uT = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + r0;
+  const double al = bt.alpha;
+  for (int idx = threadIdx.x; idx < 4 * n2; idx += NT) {
+    const int k = idx >> 2, h = idx & 3;
+    if (h >= nl) continue;
+    uT[(size_t)k * n1 + h] = (k == 0) ? al * e0[h] : (k == n2 - 1) ? al * e1[h] : rowS[h * LS + k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// rows_t_axpy_afwd: FOUR rows per CTA.  T (packed DST) of the rows of v ->
+// x_k = x_{k-1} + tau (.) with ||x||^2 / ||x - f||^2 partials -> forward
+// packed row FFTs of x_k (conv line g = rows 2g, 2g+1) -> Z^T.
+template <int L2, int M, bool BLUE>
+__global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(SpecArgs a) {
+  using F = Fused<L2, M, BLUE>;
+  constexpr int NT = F::NT, TD = F::TD, LS = F::LS;
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 sm[];
+  __shared__ double red[32];
+  __shared__ double e0[4], e1[4];
+  char* base = reinterpret_cast<char*>(sm);
+  double* io = reinterpret_cast<double*>(base + F::off_rows);  // v rows, then T output
+  double* stX = reinterpret_cast<double*>(base + F::off_x);    // x_{k-1} rows, then x_k
+  const BlueTables& bt = a.blue2;
+  const double2* twd = stage_twiddles<M, F::AX_TWD>(reinterpret_cast<double2*>(base + F::ax_twd), bt.tw);
+  const double2* twc = stage_twiddles<L2, F::AX_TWC>(reinterpret_cast<double2*>(base + F::ax_twc), a.conv.tw2);
+  const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
+  const size_t N = (size_t)n1 * n2;
+  const int r0 = 4 * blockIdx.x;
+  const int nl = n1 - r0 < 4 ? n1 - r0 : 4;
+  const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
+  const double* xo = resolve_ptr(a.xold, a.st, a.xoldsel, b, a.batch, N) + (size_t)r0 * n2;
+  const double* fimg = a.f ? a.f + (size_t)b * N + (size_t)r0 * n2 : nullptr;
+  stage_lines(io, LS, a.in + (size_t)b * N + (size_t)r0 * n2, nl, n2);  // v rows
+  cp_async_commit();
+  stage_lines(stX, LS, xo, nl, n2);                                       // x_{k-1} rows
+  cp_async_commit();
+  cp_async_wait_group<1>();
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    const int h = threadIdx.x;
+    e0[h] = h < nl ? io[h * LS] : 0.0;
+    e1[h] = h < nl ? io[h * LS + n2 - 1] : 0.0;
+  }
+  // T along the rows (ar_forward, transforms.hpp:148-160)
+  const double* p = bt.p;
+  double2* dbuf = sm + g * F::LD;
+  pk_fill<M, TD, BLUE>(dbuf, bt, t, [&](int hh, int j) {
+    const int h = 2 * g + hh;
+    return h < nl ? io[h * LS + j] : 0.0;
+  });
+  blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
+  pk_split<M, BLUE>(dbuf, bt, io + (2 * g) * LS, io + (2 * g + 1) * LS, t, TD);
+  __syncthreads();
+  odd_scans(io, LS, 4, bt);
+  cp_async_wait_all();
+  __syncthreads();
+  // x_k = x_{k-1} + tau * T v (solver.hpp:106), rows r0..r0+nl-1 contiguous
+  double* xn = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + (size_t)r0 * n2;
+  const double ia = 1.0 / bt.alpha, tau = a.tau;
+  double p0 = 0.0, p1 = 0.0;
+#pragma unroll 4
+  for (int idx = threadIdx.x; idx < nl * n2; idx += NT) {
+    const int h = idx / n2, k = idx - h * n2;
+    const double a0 = ia * e0[h], a1 = ia * e1[h];
+    double w;
+    if (k == 0) w = a0;
+    else if (k == n2 - 1) w = a1;
+    else w = io[h * LS + k] + a0 * __ldg(p + k - 1) + a1 * __ldg(p + n2 - 2 - k);
+    const double xv = stX[h * LS + k] + tau * w;
+    xn[idx] = xv;
+    stX[h * LS + k] = xv;
+    p0 += xv * xv;
+    if (fimg) {
+      const double e = xv - __ldg(fimg + idx);
+      p1 += e * e;
+    }
+  }
+  __syncthreads();  // x rows complete; DST buffers free for the conv lines
+  const int ra = r0 + 2 * g, rb = ra + 1;
+  conv_fwd_rows<L2, TD>(sm + g * F::LC, stX + (2 * g) * LS, stX + (2 * g + 1) * LS, n2, a.q2, twc,
+                        a.zbuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t);
+  if (a.part.p) {
+    double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
+    const double s0 = block_sum<NT>(p0, red);
+    if (threadIdx.x == 0) P[SLOT_X2 * a.part.cap + blockIdx.x] = s0;
+    const double s1 = block_sum<NT>(p1, red);
+    if (threadIdx.x == 0) P[SLOT_XF2 * a.part.cap + blockIdx.x] = s1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// rows_ainv_resid: one row PAIR per CTA (one packed conv line on NT threads).
+template <int L2, int M, bool BLUE>
+__global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_resid(SpecArgs a) {
+  using F = Fused<L2, M, BLUE>;
+  constexpr int NT = F::NT;
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 sm[];
+  __shared__ double red[32];
+  char* base = reinterpret_cast<char*>(sm);
+  double* rowS = reinterpret_cast<double*>(base + F::rs_rows);
+  double* stG = reinterpret_cast<double*>(base + F::rs_g);
+  const double2* twc = stage_twiddles<L2, F::RS_TWC>(reinterpret_cast<double2*>(base + F::rs_twc), a.conv.tw2);
   const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
   const size_t N = (size_t)n1 * n2;
   const int ra = 2 * blockIdx.x, rb = ra + 1;
-  // A' r rows: inverse packed row FFT
-  conv_inv_load<L2, NT>(sm, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh);
-  cp_async_wait_all();
+  const double* gimg = a.g + (size_t)b * N;
+  for (int c = threadIdx.x; c < n2; c += NT) {
+    if (ra < n1) cp_async8(stG + c, gimg + (size_t)ra * n2 + c);
+    if (rb < n1) cp_async8(stG + F::RROW + c, gimg + (size_t)rb * n2 + c);
+  }
+  cp_async_commit();
+  conv_inv_load<L2, NT>(sm, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, threadIdx.x);
+  cp_async_wait_group<1>();
   __syncthreads();
   fft::fft<L2, +1, NT>(sm, twc, threadIdx.x);
+  cp_async_wait_all();
+  double p0 = 0.0;
   for (int c = threadIdx.x; c < n2; c += NT) {
-    const double2 v = sm[pad<L2>(c)];
-    rowS[c] = v.x;
-    rowS[F::RROW + c] = v.y;
+    const double2 ax = sm[pad<L2>(c)];
+    if (ra < n1) {
+      const double rv = stG[c] - ax.x;  // r = g - A x (solver.hpp:105)
+      rowS[c] = rv;
+      p0 += rv * rv;
+    }
+    if (rb < n1) {
+      const double rv = stG[F::RROW + c] - ax.y;
+      rowS[F::RROW + c] = rv;
+      p0 += rv * rv;
+    }
   }
   __syncthreads();
-  // T~ along each of the two rows (ar_inverse, transforms.hpp:163-173)
-  const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
-  const int r = ra + g;
-  const bool live = r < n1;
-  const double* s = rowS + g * F::RROW;
-  const double v0 = s[0], ve = s[n2 - 1];
-  const double* p = bt.p;
-  double2* buf = sm + g * F::LD;
-  blue_fill<M, TD, BLUE>(buf, bt, t, [&](int j) {
-    return live ? (s[j] - v0 * __ldg(p + j - 1)) - ve * __ldg(p + n2 - 2 - j) : 0.0;
-  });
-  blue_core<M, TD, 2, BLUE>(sm, buf, bt, twd, t);
-  if (live) {
-    // u stored transposed (u^T[k][r]): the column pass reads it contiguously
-    double* uT = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + r;
-    const double al = bt.alpha;
-    for (int k = t; k < n2; k += TD)
-      uT[(size_t)k * n1] = (k == 0) ? al * v0 : (k == n2 - 1) ? al * ve : blue_out<M, BLUE>(buf, bt, k);
+  conv_fwd_rows<L2, NT>(sm, rowS, rowS + F::RROW, n2, a.q2, twc, a.zbuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh,
+                        threadIdx.x);
+  if (a.part.p) {
+    double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
+    const double s0 = block_sum<NT>(p0, red);
+    if (threadIdx.x == 0) P[SLOT_R2 * a.part.cap + blockIdx.x] = s0;
   }
 }
 
@@ -233,142 +402,20 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   }
 }
 
-// ---------------------------------------------------------------------------
-template <int L2, int M, bool BLUE>
-__global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(SpecArgs a) {
-  using F = Fused<L2, M, BLUE>;
-  constexpr int NT = F::NT, TD = F::TD;
-  const int b = blockIdx.y;
-  if (a.st && a.st[b].done) return;
-  extern __shared__ double2 sm[];
-  __shared__ double red[32];
-  double* rowS = reinterpret_cast<double*>(sm + F::off_real);
-  double* stX = reinterpret_cast<double*>(sm + F::off_epi);        // x_{k-1}: 2 rows
-  double* stF = stX + 2 * F::RROW;                                  // f: 2 rows
-  const BlueTables& bt = a.blue2;
-  const double2* twd = stage_twiddles<M, true>(sm + F::off_twd, bt.tw);
-  const double2* twc = stage_twiddles<L2, F::TWC>(sm + F::off_twc, a.conv.tw2);
-  const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
-  const size_t N = (size_t)n1 * n2;
-  const int ra = 2 * blockIdx.x, rb = ra + 1;
-  const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
-  const int r = ra + g;
-  const bool live = r < n1;
-  const double* xo = resolve_ptr(a.xold, a.st, a.xoldsel, b, a.batch, N);
-  const double* fimg = a.f ? a.f + (size_t)b * N : nullptr;
-  // stage x_{k-1} and f rows (cp.async group 2) behind the transform
-  if (live) {
-    for (int k = t; k < n2; k += TD) {
-      cp_async8(stX + g * F::RROW + k, xo + (size_t)r * n2 + k);
-      if (fimg) cp_async8(stF + g * F::RROW + k, fimg + (size_t)r * n2 + k);
-    }
-  }
-  cp_async_commit();
-  // T along each row (ar_forward, transforms.hpp:148-160)
-  const double* v = a.in + (size_t)b * N + (size_t)(live ? r : 0) * n2;
-  const double v0 = v[0], ve = v[n2 - 1];
-  const double* p = bt.p;
-  double2* buf = sm + g * F::LD;
-  blue_fill<M, TD, BLUE>(buf, bt, t, [&](int j) { return live ? v[j] : 0.0; });
-  blue_core<M, TD, 2, BLUE>(sm, buf, bt, twd, t);
-  cp_async_wait_all();
-  double p0 = 0.0, p1 = 0.0;
-  double* xn = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N));
-  if (live) {
-    const double ia = 1.0 / bt.alpha, a0 = ia * v0, a1 = ia * ve;
-    for (int k = t; k < n2; k += TD) {
-      double w;
-      if (k == 0) w = a0;
-      else if (k == n2 - 1) w = a1;
-      else {
-        w = blue_out<M, BLUE>(buf, bt, k);
-        w += a0 * __ldg(p + k - 1);
-        w += a1 * __ldg(p + n2 - 2 - k);
-      }
-      const double xv = stX[g * F::RROW + k] + a.tau * w;
-      xn[(size_t)r * n2 + k] = xv;
-      rowS[g * F::RROW + k] = xv;
-      p0 += xv * xv;
-      if (fimg) {
-        const double e = xv - stF[g * F::RROW + k];
-        p1 += e * e;
-      }
-    }
-  }
-  __syncthreads();  // x rows staged; DST buffers free for the conv line
-  conv_fwd_rows<L2, NT>(sm, rowS, rowS + F::RROW, rb < n1, n2, a.q2, twc, a.zbuf + (size_t)b * n1 * Lh, ra, rb,
-                        n1, Lh);
-  if (a.part.p) {
-    double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
-    const double s0 = block_sum<NT>(p0, red);
-    if (threadIdx.x == 0) P[SLOT_X2 * a.part.cap + blockIdx.x] = s0;
-    const double s1 = block_sum<NT>(p1, red);
-    if (threadIdx.x == 0) P[SLOT_XF2 * a.part.cap + blockIdx.x] = s1;
-  }
-}
-
-// ---------------------------------------------------------------------------
-template <int L2, int M, bool BLUE>
-__global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_resid(SpecArgs a) {
-  using F = Fused<L2, M, BLUE>;
-  constexpr int NT = F::NT;
-  const int b = blockIdx.y;
-  if (a.st && a.st[b].done) return;
-  extern __shared__ double2 sm[];
-  __shared__ double red[32];
-  double* rowS = reinterpret_cast<double*>(sm + F::off_real);
-  double* stG = reinterpret_cast<double*>(sm + F::off_epi);
-  const double2* twc = stage_twiddles<L2, F::TWC>(sm + F::off_twc, a.conv.tw2);
-  const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
-  const size_t N = (size_t)n1 * n2;
-  const int ra = 2 * blockIdx.x, rb = ra + 1;
-  const double* gimg = a.g + (size_t)b * N;
-  for (int c = threadIdx.x; c < n2; c += NT) {
-    if (ra < n1) cp_async8(stG + c, gimg + (size_t)ra * n2 + c);
-    if (rb < n1) cp_async8(stG + F::RROW + c, gimg + (size_t)rb * n2 + c);
-  }
-  cp_async_commit();
-  conv_inv_load<L2, NT>(sm, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh);
-  cp_async_wait_group<1>();
-  __syncthreads();
-  fft::fft<L2, +1, NT>(sm, twc, threadIdx.x);
-  cp_async_wait_all();
-  double p0 = 0.0;
-  for (int c = threadIdx.x; c < n2; c += NT) {
-    const double2 ax = sm[pad<L2>(c)];
-    if (ra < n1) {
-      const double rv = stG[c] - ax.x;  // r = g - A x (solver.hpp:105)
-      rowS[c] = rv;
-      p0 += rv * rv;
-    }
-    if (rb < n1) {
-      const double rv = stG[F::RROW + c] - ax.y;
-      rowS[F::RROW + c] = rv;
-      p0 += rv * rv;
-    }
-  }
-  __syncthreads();
-  conv_fwd_rows<L2, NT>(sm, rowS, rowS + F::RROW, rb < n1, n2, a.q2, twc, a.zbuf + (size_t)b * n1 * Lh, ra, rb,
-                        n1, Lh);
-  if (a.part.p) {
-    double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
-    const double s0 = block_sum<NT>(p0, red);
-    if (threadIdx.x == 0) P[SLOT_R2 * a.part.cap + blockIdx.x] = s0;
-  }
-}
-
 // WHICH makes the attribute flag per kernel (the three kernels share one
 // function-pointer type).
 template <int L2, int M, bool BLUE, int WHICH, typename K>
 int fused_launch(K kernel, const SpecArgs& a, cudaStream_t s) {
   using F = Fused<L2, M, BLUE>;
+  constexpr size_t bytes = WHICH == 0 ? F::tt_bytes : WHICH == 1 ? F::ax_bytes : F::rs_bytes;
+  constexpr int rows = WHICH == 2 ? 2 : 4;  // rows per CTA
   static bool init = false;
   if (!init) {
-    if (!set_smem(kernel, F::bytes)) return -1;
+    if (!set_smem(kernel, bytes)) return -1;
     init = true;
   }
-  dim3 grid((a.n1 + 1) / 2, a.batch);
-  kernel<<<grid, F::NT, F::bytes, s>>>(a);
+  dim3 grid((a.n1 + rows - 1) / rows, a.batch);
+  kernel<<<grid, F::NT, bytes, s>>>(a);
   return (int)grid.x;
 }
 
@@ -391,7 +438,7 @@ int tcols_launch(const SpecArgs& a, cudaStream_t s) {
 #define DBX_FUSED_LIST(X) X(1080, 1023, false) X(540, 1024, true) X(270, 255, false)
 
 bool fused_supported(int L2, int M, bool blue) {
-#define X(L, MM, BL) if (L2 == (L) && M == (MM) && blue == (BL)) return Fused<L, MM, BL>::bytes <= 200 * 1024;
+#define X(L, MM, BL) if (L2 == (L) && M == (MM) && blue == (BL)) return Fused<L, MM, BL>::ax_bytes <= 200 * 1024 && TcolSmem<MM, BL>::bytes <= 200 * 1024;
   DBX_FUSED_LIST(X)
 #undef X
   return false;

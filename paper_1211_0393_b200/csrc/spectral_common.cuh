@@ -296,22 +296,26 @@ template <int M, int T, bool BLUE, typename F>
 __device__ __forceinline__ void pk_fill(double2* buf, const BlueTables& bt, int t, F val) {
   const int N = bt.N;
   constexpr int PF = (M + T - 1) / T;
-  double2 z[PF];
+  constexpr int CH = 4;  // elements per load batch (bounded register use)
 #pragma unroll
-  for (int i = 0; i < PF; ++i) {
-    const int j = t + i * T;
-    z[i] = make_double2(0.0, 0.0);
-    if (j >= 1 && j < N) {
-      const double s = __ldg(bt.sn + j);
-      const double xa = val(0, j), xar = val(0, N - j);
-      const double xb = val(1, j), xbr = val(1, N - j);
-      z[i] = pre<BLUE>(make_double2(fma(s, xa + xar, 0.5 * (xa - xar)), fma(s, xb + xbr, 0.5 * (xb - xbr))), bt, j);
+  for (int i0 = 0; i0 < PF; i0 += CH) {
+    double2 z[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int j = t + (i0 + u) * T;
+      z[u] = make_double2(0.0, 0.0);
+      if (i0 + u < PF && j >= 1 && j < N) {
+        const double s = __ldg(bt.sn + j);
+        const double xa = val(0, j), xar = val(0, N - j);
+        const double xb = val(1, j), xbr = val(1, N - j);
+        z[u] = pre<BLUE>(make_double2(fma(s, xa + xar, 0.5 * (xa - xar)), fma(s, xb + xbr, 0.5 * (xb - xbr))), bt, j);
+      }
     }
-  }
 #pragma unroll
-  for (int i = 0; i < PF; ++i) {
-    const int j = t + i * T;
-    if (j < M) buf[pad<M>(j)] = z[i];
+    for (int u = 0; u < CH; ++u) {
+      const int j = t + (i0 + u) * T;
+      if (i0 + u < PF && j < M) buf[pad<M>(j)] = z[u];
+    }
   }
 }
 
