@@ -19,10 +19,6 @@
 
 #include "dft_consts.h"
 
-#ifndef DBX_KU
-#define DBX_KU 1  // output pairs per trip of the packed large-prime stage
-#endif
-
 namespace dbx {
 namespace fft {
 
@@ -391,31 +387,75 @@ __device__ __forceinline__ void stage_split(double2* buf, const double2* __restr
   __syncthreads();
 }
 
+// Output pairs k in [K0, K1] of an odd-prime butterfly (symmetric pairs in v:
+// v[j] = a_j, v[R-j] = b_j).  K0/K1 are compile-time so the rolled counter is
+// uniform: the constant-table reads go through the uniform datapath (ULDC ->
+// DFMA operand) and only one pair of accumulators is live.
+template <int R, int S, int L, int K0, int K1>
+__device__ __forceinline__ void odd_pairs(const double2* v, double2 x0, double2* buf, int base, int Ns) {
+  using K = OddConst<R>;
+  constexpr int H = (R - 1) / 2;
+#pragma unroll 1
+  for (int kk = K0; kk <= K1; ++kk) {
+    double2 A = x0, B = make_double2(0.0, 0.0);
+    int e = 0;
+#pragma unroll
+    for (int j = 1; j <= H; ++j) {
+      e += kk;
+      if (e >= R) e -= R;
+      const double c = K::c(e), s = K::s(e);
+      A.x = fma(c, v[j].x, A.x);
+      A.y = fma(c, v[j].y, A.y);
+      B.x = fma(s, v[R - j].x, B.x);
+      B.y = fma(s, v[R - j].y, B.y);
+    }
+    const double2 sb = mul_si<S>(B);
+    buf[pad<L>(base + kk * Ns)] = cadd(A, sb);
+    buf[pad<L>(base + (R - kk) * Ns)] = csub(A, sb);
+  }
+}
+
+// part -> compile-time pair range (part is warp-uniform at run time)
+template <int R, int S, int L, int H, int P, int Q>
+__device__ __forceinline__ void odd_pairs_dispatch(int part, const double2* v, double2 x0, double2* buf, int base,
+                                                   int Ns) {
+  if constexpr (Q < P) {
+    if (part == Q) {
+      odd_pairs<R, S, L, 1 + (Q * H) / P, ((Q + 1) * H) / P>(v, x0, buf, base, Ns);
+      return;
+    }
+    odd_pairs_dispatch<R, S, L, H, P, Q + 1>(part, v, x0, buf, base, Ns);
+  }
+}
+
 // CTA-wide stage for a large odd prime R (>= 17) on G lines at once: the
 // G * NB butterflies (NB = L/R is small, e.g. 33 for 1023 = 31*33) are packed
-// densely over the CTA's threads (slot -> line, butterfly), so few warps are
-// busy and those are full.  The output-pair loop is rolled with a CTA-uniform
-// counter: the cos/sin table reads become uniform-datapath loads feeding DFMA
-// directly, and only one pair of accumulators is live (~70 registers instead
-// of ~230 for the fully unrolled butterfly).
-template <int L, int Ns, int R, int S, int G, int PL>
-__device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __restrict__ tw, int tid, int nthreads) {
+// densely over a warp-aligned slot range of NBp threads, and that range is
+// replicated P times (P = CTA threads / NBp): replica `part` computes the
+// output pairs k in (part*H/P, (part+1)*H/P] of every butterfly, so all warps
+// of the CTA share the stage and each thread runs 1/P of the DFMA chains.  The
+// output-pair loop is rolled with a warp-uniform counter: the cos/sin table
+// reads become uniform-datapath loads feeding DFMA directly, and only one
+// pair of accumulators is live.
+template <int L, int Ns, int R, int S, int G, int PL, int NTH>
+__device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __restrict__ tw, int tid) {
   constexpr int NB = L / R;
   constexpr int H = (R - 1) / 2;
-  using K = OddConst<R>;
-  const bool act = tid < G * NB;
-  const int line = act ? tid / NB : 0;
-  const int b = act ? tid - line * NB : 0;
+  constexpr int NBp = (G * NB + 31) / 32 * 32;
+  constexpr int P0 = NTH / NBp;
+  constexpr int P = P0 < 1 ? 1 : (P0 > H ? H : P0);
+  const int part = tid / NBp;                 // warp-uniform
+  const int slot = tid - part * NBp;
+  const bool act = part < P && slot < G * NB;
+  const int line = act ? slot / NB : 0;
+  const int b = act ? slot - line * NB : 0;
   double2* buf = sm + line * PL;
   double2 v[R];
-  double2 w[Ns > 1 ? R - 1 : 1];
   const int k = b % Ns;
+  double2 w1 = make_double2(1.0, 0.0);
   if constexpr (Ns > 1) {
     constexpr int step = L / (Ns * R);
-    if (act) {
-#pragma unroll
-      twiddle_powers<R>(w, tw[k * step]);
-    }
+    if (act) w1 = tw[k * step];
   }
   if (act) {
 #pragma unroll
@@ -424,6 +464,8 @@ __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __rest
   __syncthreads();
   if (act) {
     if constexpr (Ns > 1) {
+      double2 w[R - 1];
+      twiddle_powers<R>(w, w1);
 #pragma unroll
       for (int r = 1; r < R; ++r) v[r] = S < 0 ? cmul(v[r], w[r - 1]) : cmulc(v[r], w[r - 1]);
     }
@@ -438,45 +480,9 @@ __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __rest
       sum = cadd(sum, a);
     }
     const int base = (b / Ns) * Ns * R + k;
-    buf[pad<L>(base)] = sum;
-    // KU output pairs per trip: 4*KU independent FMA chains hide the DFMA
-    // latency (one pair alone leaves 4 chains of depth H).
-    constexpr int KU = DBX_KU;
-#pragma unroll 1
-    for (int k0 = 1; k0 <= H; k0 += KU) {
-      double2 A[KU], B[KU];
-      int e[KU];
-#pragma unroll
-      for (int u = 0; u < KU; ++u) {
-        A[u] = x0;
-        B[u] = make_double2(0.0, 0.0);
-        e[u] = 0;
-      }
-#pragma unroll
-      for (int j = 1; j <= H; ++j) {
-#pragma unroll
-        for (int u = 0; u < KU; ++u) {
-          e[u] += k0 + u;
-          if (e[u] >= R) e[u] -= R;
-          const double c = K::c(e[u]), s = K::s(e[u]);
-          A[u].x = fma(c, v[j].x, A[u].x);
-          A[u].y = fma(c, v[j].y, A[u].y);
-          B[u].x = fma(s, v[R - j].x, B[u].x);
-          B[u].y = fma(s, v[R - j].y, B[u].y);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < KU; ++u) {
-        const int kk = k0 + u;
-        if (kk <= H) {
-          const double2 sb = mul_si<S>(B[u]);
-          buf[pad<L>(base + kk * Ns)] = cadd(A[u], sb);
-          buf[pad<L>(base + (R - kk) * Ns)] = csub(A[u], sb);
-        }
-      }
-    }
+    if (part == 0) buf[pad<L>(base)] = sum;
+    odd_pairs_dispatch<R, S, L, H, P, 0>(part, v, x0, buf, base, Ns);
   }
-  (void)nthreads;
   __syncthreads();
 }
 
@@ -503,7 +509,7 @@ __device__ __forceinline__ void run_stages_cta(double2* sm, const double2* __res
     constexpr int R = next_radix(L / Ns);
     static_assert(R != 0, "FFT length must factor into {2,3,4,5,8} and odd primes <= 31");
     if constexpr (R >= 17 && (R & 1) && G * (L / R) <= G * T) {
-      stage_odd_cta<L, Ns, R, S, G, PL>(sm, tw, tid, G * T);
+      stage_odd_cta<L, Ns, R, S, G, PL, G * T>(sm, tw, tid);
     } else {
       const int g = tid / T;
       stage<L, Ns, R, S, T>(sm + g * PL, tw, tid - g * T);
