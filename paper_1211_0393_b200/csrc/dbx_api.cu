@@ -305,6 +305,7 @@ struct dbx_plan {
       B.t.bhat = reinterpret_cast<const double2*>(B.bhat);
       B.t.p = B.p;
       B.t.alpha = h.alpha;
+      B.t.rinv = n > 1 ? 1.0 / (double)(n - 1) : 1.0;
       B.t.scale = h.scale;
       B.t.n = h.n;
       B.t.N = h.N;

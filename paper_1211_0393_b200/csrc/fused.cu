@@ -58,6 +58,7 @@ struct Fused {
   static constexpr size_t rs_twc = rs_g + (size_t)RROW * 16;
   static constexpr bool RS_TWC = rs_twc + (size_t)L2 * 16 <= kBudget;
   static constexpr size_t rs_bytes = rs_twc + (RS_TWC ? (size_t)L2 * 16 : 0);
+  static_assert((size_t)W4 * 16 >= (size_t)4 * LS * 8, "f rows are staged in the work region");
 };
 
 // Inverse packed real FFT of rows (ra, rb) from the half spectra Y -> buf
@@ -159,13 +160,14 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
     e1[threadIdx.x] = rowS[threadIdx.x * LS + n2 - 1];
   }
   // T~ along the rows (ar_inverse, transforms.hpp:163-173)
-  const double* p = bt.p;
+  const double ri = bt.rinv;
   double2* dbuf = sm + g * F::LD;
   pk_fill<M, TD, BLUE>(dbuf, bt, t, [&](int hh, int j) {
     const int h = 2 * g + hh;
     if (h >= nl) return 0.0;
     const double* L = rowS + h * LS;
-    return (L[j] - L[0] * __ldg(p + j - 1)) - L[n2 - 1] * __ldg(p + n2 - 2 - j);
+    const double t1 = (double)j * ri;  // p_j = 1 - j/(n-1), p_{n-1-j} = j/(n-1) (transforms.hpp:135-144)
+    return (L[j] - L[0] * (1.0 - t1)) - L[n2 - 1] * t1;
   });
   blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
   pk_split<M, BLUE>(dbuf, bt, rowS + (2 * g) * LS, rowS + (2 * g + 1) * LS, t, TD);
@@ -207,6 +209,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
   const double* xo = resolve_ptr(a.xold, a.st, a.xoldsel, b, a.batch, N) + (size_t)r0 * n2;
   const double* fimg = a.f ? a.f + (size_t)b * N + (size_t)r0 * n2 : nullptr;
+  if (fimg && threadIdx.x < nl) prefetch_l2(fimg + (size_t)threadIdx.x * n2, (unsigned)n2 * 8);
   stage_lines(io, LS, a.in + (size_t)b * N + (size_t)r0 * n2, nl, n2);  // v rows
   cp_async_commit();
   stage_lines(stX, LS, xo, nl, n2);                                       // x_{k-1} rows
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
     e1[h] = h < nl ? io[h * LS + n2 - 1] : 0.0;
   }
   // T along the rows (ar_forward, transforms.hpp:148-160)
-  const double* p = bt.p;
+  const double ri = bt.rinv;
   double2* dbuf = sm + g * F::LD;
   pk_fill<M, TD, BLUE>(dbuf, bt, t, [&](int hh, int j) {
     const int h = 2 * g + hh;
@@ -228,6 +231,11 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
   pk_split<M, BLUE>(dbuf, bt, io + (2 * g) * LS, io + (2 * g + 1) * LS, t, TD);
   __syncthreads();
+  // the DST lines are free now: stage the f rows there (L2-prefetched at
+  // kernel start) behind the scans
+  double* fS = reinterpret_cast<double*>(sm);
+  if (fimg) stage_lines(fS, LS, fimg, nl, n2);
+  cp_async_commit();
   odd_scans(io, LS, 4, bt);
   cp_async_wait_all();
   __syncthreads();
@@ -242,13 +250,16 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
     double w;
     if (k == 0) w = a0;
     else if (k == n2 - 1) w = a1;
-    else w = io[h * LS + k] + a0 * __ldg(p + k - 1) + a1 * __ldg(p + n2 - 2 - k);
+    else {
+      const double t1 = (double)k * ri;
+      w = io[h * LS + k] + a0 * (1.0 - t1) + a1 * t1;
+    }
     const double xv = stX[h * LS + k] + tau * w;
     xn[idx] = xv;
     stX[h * LS + k] = xv;
     p0 += xv * xv;
     if (fimg) {
-      const double e = xv - __ldg(fimg + idx);
+      const double e = xv - fS[h * LS + k];
       p1 += e * e;
     }
   }
@@ -364,13 +375,14 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   }
   const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
   double2* buf = sm + g * padded_len(M);
-  const double* p = bt.p;
+  const double ri = bt.rinv;
   // T~ (ar_inverse, transforms.hpp:163-173) of lines 2g, 2g+1
   pk_fill<M, TD, BLUE>(buf, bt, t, [&](int hh, int j) {
     const int h = 2 * g + hh;
     if (h >= nl) return 0.0;
     const double* L = io + h * LS;
-    return (L[j] - L[0] * __ldg(p + j - 1)) - L[n - 1] * __ldg(p + n - 2 - j);
+    const double t1 = (double)j * ri;
+    return (L[j] - L[0] * (1.0 - t1)) - L[n - 1] * t1;
   });
   blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
   pk_split<M, BLUE>(buf, bt, io + (2 * g) * LS, io + (2 * g + 1) * LS, t, TD);
@@ -397,7 +409,10 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
     double w;
     if (k == 0) w = a0;
     else if (k == n - 1) w = a1;
-    else w = io[h * LS + k] + a0 * __ldg(p + k - 1) + a1 * __ldg(p + n - 2 - k);
+    else {
+      const double t1 = (double)k * ri;
+      w = io[h * LS + k] + a0 * (1.0 - t1) + a1 * t1;
+    }
     s[(size_t)k * n2 + h] = w;
   }
 }

@@ -29,6 +29,7 @@ struct BlueTables {
   const double2* bhat = nullptr;
   const double* p = nullptr;
   const double* sn = nullptr;  // sin(pi j / N), j < N (packed real DST)
+  double rinv = 1.0;  // 1 / (n - 1): ramp p_j = 1 - j rinv computed in registers
   double alpha = 1.0;
   double scale = 1.0;  // sqrt(2/N)
   int n = 0, N = 0, M = 0;

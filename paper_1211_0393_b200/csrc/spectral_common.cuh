@@ -382,16 +382,13 @@ __device__ __forceinline__ void odd_scans(double* o, int LS, int nlines, const B
 __device__ __forceinline__ void stage_lines(double* dst, int LS, const double* src, int nl, int n) {
   const int nt = blockDim.x;
   const bool v16 = ((n | LS) & 1) == 0 && (((unsigned long long)src | (unsigned long long)__cvta_generic_to_shared(dst)) & 15) == 0;
-  if (v16) {
-    const int h2 = n >> 1;
-    for (int i = threadIdx.x; i < nl * h2; i += nt) {
-      const int h = i / h2, j = 2 * (i - h * h2);
-      cp_async16(dst + (size_t)h * LS + j, src + (size_t)h * n + j);
-    }
-  } else {
-    for (int i = threadIdx.x; i < nl * n; i += nt) {
-      const int h = i / n, j = i - h * n;
-      cp_async8(dst + (size_t)h * LS + j, src + i);
+  for (int h = 0; h < nl; ++h) {
+    double* d = dst + (size_t)h * LS;
+    const double* q = src + (size_t)h * n;
+    if (v16) {
+      for (int j = 2 * threadIdx.x; j < n; j += 2 * nt) cp_async16(d + j, q + j);
+    } else {
+      for (int j = threadIdx.x; j < n; j += nt) cp_async8(d + j, q + j);
     }
   }
 }
