@@ -47,6 +47,22 @@ __host__ __device__ constexpr int next_radix(int rem) {
   return 0;
 }
 
+// Twiddle entries an FFT of length L reads: stage (Ns, R) reads W_L^{k L/(Ns R)},
+// k < Ns (largest index (Ns-1) L/(Ns R)) — only that prefix of the table
+// needs staging.
+__host__ __device__ constexpr int twiddles_needed(int L) {
+  int rem = L, Ns = 1, mx = 0;
+  while (rem > 1) {
+    const int r = next_radix(rem);
+    if (r == 0) return L;
+    const int top = (Ns - 1) * (L / (Ns * r));
+    mx = top > mx ? top : mx;
+    Ns *= r;
+    rem /= r;
+  }
+  return mx + 1;
+}
+
 __host__ __device__ constexpr bool supported(int L) {
   if (L < 2) return false;
   while (L > 1) {

@@ -31,7 +31,9 @@ struct Fused {
   static constexpr int NT = 2 * TD;                         // CTA = two FFT lines
   static constexpr int LC = padded_len(L2);                 // conv line (double2)
   static constexpr int LD = padded_len(M);                  // DST line (double2)
-  static constexpr size_t kBudget = 113 * 1024;             // two CTAs per SM
+  static constexpr size_t kBudget = 115200;                 // two CTAs per SM (228 KB - reserved)
+  static constexpr size_t TWD = (size_t)fft::twiddles_needed(M) * 16;   // staged twiddle prefixes
+  static constexpr size_t TWC = (size_t)fft::twiddles_needed(L2) * 16;
   // ---- 4-row kernels (rows_ainv_tt, rows_t_axpy_afwd): two conv lines of
   // two packed rows each, then two packed DST lines of two rows each
   static constexpr int W4 = (LC > LD ? LC : LD) * 2;        // work region (double2)
@@ -41,23 +43,23 @@ struct Fused {
   static constexpr size_t off_x = off_rows + (size_t)4 * LS * 8;  // 4 more rows (t_axpy)
   // rows_ainv_tt: twiddles after the rows
   static constexpr size_t tt_twd = off_x;
-  static constexpr bool TT_TWD = tt_twd + (size_t)M * 16 <= kBudget;
-  static constexpr size_t tt_twc = tt_twd + (TT_TWD ? (size_t)M * 16 : 0);
-  static constexpr bool TT_TWC = tt_twc + (size_t)L2 * 16 <= kBudget;
-  static constexpr size_t tt_bytes = tt_twc + (TT_TWC ? (size_t)L2 * 16 : 0);
+  static constexpr bool TT_TWD = tt_twd + TWD <= kBudget;
+  static constexpr size_t tt_twc = tt_twd + (TT_TWD ? TWD : 0);
+  static constexpr bool TT_TWC = tt_twc + TWC <= kBudget;
+  static constexpr size_t tt_bytes = tt_twc + (TT_TWC ? TWC : 0);
   // rows_t_axpy_afwd: v rows (then T output), x rows, twiddles if they fit
   static constexpr size_t ax_twd = off_x + (size_t)4 * LS * 8;
-  static constexpr bool AX_TWD = ax_twd + (size_t)M * 16 <= kBudget;
-  static constexpr size_t ax_twc = ax_twd + (AX_TWD ? (size_t)M * 16 : 0);
-  static constexpr bool AX_TWC = ax_twc + (size_t)L2 * 16 <= kBudget;
-  static constexpr size_t ax_bytes = ax_twc + (AX_TWC ? (size_t)L2 * 16 : 0);
+  static constexpr bool AX_TWD = ax_twd + TWD <= kBudget;
+  static constexpr size_t ax_twc = ax_twd + (AX_TWD ? TWD : 0);
+  static constexpr bool AX_TWC = ax_twc + TWC <= kBudget;
+  static constexpr size_t ax_bytes = ax_twc + (AX_TWC ? TWC : 0);
   // ---- rows_ainv_resid (two rows, one conv line on all NT threads)
   static constexpr int RROW = L2;
   static constexpr size_t rs_rows = (size_t)LC * 16;                 // 2 x RROW doubles
   static constexpr size_t rs_g = rs_rows + (size_t)RROW * 16;         // g: 2 x RROW doubles
   static constexpr size_t rs_twc = rs_g + (size_t)RROW * 16;
-  static constexpr bool RS_TWC = rs_twc + (size_t)L2 * 16 <= kBudget;
-  static constexpr size_t rs_bytes = rs_twc + (RS_TWC ? (size_t)L2 * 16 : 0);
+  static constexpr bool RS_TWC = rs_twc + TWC <= kBudget;
+  static constexpr size_t rs_bytes = rs_twc + (RS_TWC ? TWC : 0);
   static_assert((size_t)W4 * 16 >= (size_t)4 * LS * 8, "f rows are staged in the work region");
 };
 
@@ -174,12 +176,14 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
   __syncthreads();
   odd_scans(rowS, LS, 4, bt);
   __syncthreads();
-  double* uT = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + r0;
-  const double al = bt.alpha;
-  for (int idx = threadIdx.x; idx < 4 * n2; idx += NT) {
-    const int k = idx >> 2, h = idx & 3;
-    if (h >= nl) continue;
-    uT[(size_t)k * n1 + h] = (k == 0) ? al * e0[h] : (k == n2 - 1) ? al * e1[h] : rowS[h * LS + k];
+  static_assert(NT % 4 == 0, "row-group mapping");
+  const int h = threadIdx.x & 3;
+  if (h < nl) {
+    double* uT = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + r0 + h;
+    const double* o = rowS + h * LS;
+    const double u0 = bt.alpha * e0[h], ue = bt.alpha * e1[h];
+    for (int k = threadIdx.x >> 2; k < n2; k += NT / 4)
+      uT[(size_t)k * n1] = (k == 0) ? u0 : (k == n2 - 1) ? ue : o[k];
   }
 }
 
@@ -243,24 +247,29 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   double* xn = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + (size_t)r0 * n2;
   const double ia = 1.0 / bt.alpha, tau = a.tau;
   double p0 = 0.0, p1 = 0.0;
-#pragma unroll 4
-  for (int idx = threadIdx.x; idx < nl * n2; idx += NT) {
-    const int h = idx / n2, k = idx - h * n2;
+  for (int h = 0; h < nl; ++h) {
     const double a0 = ia * e0[h], a1 = ia * e1[h];
-    double w;
-    if (k == 0) w = a0;
-    else if (k == n2 - 1) w = a1;
-    else {
-      const double t1 = (double)k * ri;
-      w = io[h * LS + k] + a0 * (1.0 - t1) + a1 * t1;
-    }
-    const double xv = stX[h * LS + k] + tau * w;
-    xn[idx] = xv;
-    stX[h * LS + k] = xv;
-    p0 += xv * xv;
-    if (fimg) {
-      const double e = xv - fS[h * LS + k];
-      p1 += e * e;
+    const double* o = io + h * LS;
+    double* xs = stX + h * LS;
+    const double* fs = fS + h * LS;
+    double* xr = xn + (size_t)h * n2;
+#pragma unroll 2
+    for (int k = threadIdx.x; k < n2; k += NT) {
+      double w;
+      if (k == 0) w = a0;
+      else if (k == n2 - 1) w = a1;
+      else {
+        const double t1 = (double)k * ri;
+        w = o[k] + a0 * (1.0 - t1) + a1 * t1;
+      }
+      const double xv = xs[k] + tau * w;
+      xr[k] = xv;
+      xs[k] = xv;
+      p0 += xv * xv;
+      if (fimg) {
+        const double e = xv - fs[k];
+        p1 += e * e;
+      }
     }
   }
   __syncthreads();  // x rows complete; DST buffers free for the conv lines
@@ -341,8 +350,9 @@ struct TcolSmem {
   static constexpr size_t off_io = (size_t)2 * padded_len(M) * 16;
   static constexpr size_t off_d = off_io + (size_t)4 * LS * 8;
   static constexpr size_t off_tw = off_d + (size_t)4 * LS * 8;
-  static constexpr bool TW = off_tw + (size_t)M * 16 <= 113 * 1024;  // keep 2 CTAs / SM
-  static constexpr size_t bytes = TW ? off_tw + (size_t)M * 16 : off_tw;
+  static constexpr size_t TWB = (size_t)fft::twiddles_needed(M) * 16;
+  static constexpr bool TW = off_tw + TWB <= 115200;  // keep 2 CTAs / SM
+  static constexpr size_t bytes = TW ? off_tw + TWB : off_tw;
 };
 
 template <int M, bool BLUE>
@@ -401,19 +411,23 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   odd_scans(io, LS, 4, bt);
   __syncthreads();
   // T output w_0 = v_0 / alpha = e0 d_0, w_{n-1} = e1 d_{n-1}, interior DST + ramp
-  double* s = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c0;
-  for (int idx = threadIdx.x; idx < 4 * n; idx += NT) {
-    const int k = idx >> 2, h = idx & 3;
-    if (h >= nl) continue;
+  // (NT % 4 == 0: each thread keeps one column h; 4 threads fill a 32-byte sector)
+  static_assert(NT % 4 == 0, "column-group mapping");
+  const int h = threadIdx.x & 3;
+  if (h < nl) {
+    double* s = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c0 + h;
+    const double* o = io + h * LS;
     const double a0 = e0[h] * dS[h * LS], a1 = e1[h] * dS[h * LS + n - 1];
-    double w;
-    if (k == 0) w = a0;
-    else if (k == n - 1) w = a1;
-    else {
-      const double t1 = (double)k * ri;
-      w = io[h * LS + k] + a0 * (1.0 - t1) + a1 * t1;
+    for (int k = threadIdx.x >> 2; k < n; k += NT / 4) {
+      double w;
+      if (k == 0) w = a0;
+      else if (k == n - 1) w = a1;
+      else {
+        const double t1 = (double)k * ri;
+        w = o[k] + a0 * (1.0 - t1) + a1 * t1;
+      }
+      s[(size_t)k * n2] = w;
     }
-    s[(size_t)k * n2 + h] = w;
   }
 }
 

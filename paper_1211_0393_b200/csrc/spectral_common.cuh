@@ -81,7 +81,8 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 template <int L, bool SMEM>
 __device__ __forceinline__ const double2* stage_twiddles(double2* dst, const double2* src) {
   if constexpr (SMEM) {
-    for (int i = threadIdx.x; i < L; i += blockDim.x) cp_async16(dst + i, src + i);
+    constexpr int NEED = fft::twiddles_needed(L);
+    for (int i = threadIdx.x; i < NEED; i += blockDim.x) cp_async16(dst + i, src + i);
     cp_async_commit();
     return dst;
   } else {
@@ -198,10 +199,11 @@ template <int L, int G>
 struct ConvSmem {
   static constexpr int lines = G * padded_len(L);
   static constexpr bool HS = (2 * lines) * 16 <= kSmemCap;          // conv_col H staging
-  static constexpr bool TW = (lines + (HS ? lines : 0) + L) * 16 <= kSmemCap;
-  static constexpr bool TW_ROW = (lines + L) * 16 <= kSmemCap;      // row kernels
-  static constexpr size_t col_bytes = (size_t)(lines + (HS ? lines : 0) + (TW ? L : 0)) * 16;
-  static constexpr size_t row_bytes = (size_t)(lines + (TW_ROW ? L : 0)) * 16;
+  static constexpr int TWN = fft::twiddles_needed(L);               // staged twiddle prefix
+  static constexpr bool TW = (lines + (HS ? lines : 0) + TWN) * 16 <= kSmemCap;
+  static constexpr bool TW_ROW = (lines + TWN) * 16 <= kSmemCap;    // row kernels
+  static constexpr size_t col_bytes = (size_t)(lines + (HS ? lines : 0) + (TW ? TWN : 0)) * 16;
+  static constexpr size_t row_bytes = (size_t)(lines + (TW_ROW ? TWN : 0)) * 16;
 };
 
 // ---------------------------------------------------------------------------
@@ -249,8 +251,8 @@ struct DstSmem {
   static constexpr int LMAX = BLUE ? L / 2 + 1 : L + 1;
   static constexpr size_t base = (size_t)G * padded_len(L) * 16 + (size_t)G * 2 * LMAX * 8;
   static constexpr size_t tw_off = (base + 15) / 16 * 16;
-  static constexpr bool TW = tw_off + (size_t)L * 16 <= kSmemCap;
-  static constexpr size_t bytes = TW ? tw_off + (size_t)L * 16 : base;
+  static constexpr bool TW = tw_off + (size_t)fft::twiddles_needed(L) * 16 <= kSmemCap;
+  static constexpr size_t bytes = TW ? tw_off + (size_t)fft::twiddles_needed(L) * 16 : base;
 };
 
 template <int M, int T, int G, bool BLUE>
