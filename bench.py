@@ -38,6 +38,8 @@ sys.path.insert(0, ROOT)
 METRIC = "Mpixel-iterations/s of preconditioned AR-BC iteration"
 UNIT = "Mpixel-iterations/s"
 PEAKS_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
+HBM_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
 
 
 def parse():
@@ -273,35 +275,57 @@ def main():
     names = ["blur_adjoint(A')", "blur(A)+residual", "ar_transform_pass", "finalize"]
     dom = int(np.argmax(kms_tot))
     avg_ms = kms_tot[dom] / max(kcnt_tot[dom], 1)
-    peaks = {}
-    if os.path.exists(PEAKS_FILE):
-        peaks = json.load(open(PEAKS_FILE))
-    conv_e, dst_e = C.c_int(), C.c_int()
-    L.dbx_plan_engines(plan, C.byref(conv_e), C.byref(dst_e))
-    fft_conv, fft_dst = conv_e.value == 2, dst_e.value == 2
-    p_fp64 = peaks.get("dfma_tflops_sustained", 34.0)
-    per_launch_blur = (wm.conv_apply_flops(n, n, q, q) if fft_conv else wm.direct_apply_flops(n, n, q, q)) * B
-    if dom == 2:
-        # 4 transform passes per iteration spread over the class's launches
-        launches_per_it = 3 if fft_dst else 4
-        flops = (wm.transform_iteration_flops(n, n) if fft_dst else 8.0 * n * n * n) * B / launches_per_it
-        peak, psrc = (p_fp64, "measured DFMA FP64 sustained (profiles/r01_fp64_peak.json)") if fft_dst else \
-            (peaks.get("dmma_tflops_sustained", 37.0), "measured DMMA FP64 sustained (profiles/r01_fp64_peak.json)")
-        form = "FFT-form AR transform (direct odd-N DFT / Bluestein)" if fft_dst else "dense GEMM-form AR transform"
+    avg_s = avg_ms * 1e-3
+    peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
+    if os.path.exists(HBM_FILE):
+        hbm_peak, hsrc = float(json.load(open(HBM_FILE))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
     else:
-        flops = per_launch_blur
-        peak, psrc = p_fp64, "measured DFMA FP64 sustained (profiles/r01_fp64_peak.json)"
-        form = "FFT correlation (3 launches per apply)" if fft_conv else "direct AR stencil"
-    achieved = flops / (avg_ms * 1e-3) / 1e12
+        hbm_peak, hsrc = 7700.0, "B200_PROFILING.md fallback (7.7 TB/s nominal)"
+    conv_e, dst_e, fz = C.c_int(), C.c_int(), C.c_int()
+    L.dbx_plan_engines(plan, C.byref(conv_e), C.byref(dst_e))
+    L.dbx_plan_pipeline(plan, C.byref(fz))
+    fft_conv, fft_dst, fused = conv_e.value == 2, dst_e.value == 2, fz.value == 1
+    p_fp64 = peaks.get("dfma_tflops_sustained", 34.0)
+    fsrc = "measured DFMA FP64 sustained (profiles/r01_fp64_peak.json)"
     step_s = t_max * 1e-3 / args.steps
-    roof = {"bound": "tensor", "pipe": "FP64 (no tcgen05 FP64 kind on sm_100a; DFMA/DMMA)",
-            "kernel": names[dom], "form": form, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": None, "peak_source": psrc, "avg_launch_ms": avg_ms,
-            "algorithmic_flops_per_launch": flops,
+    roof = {"kernel": names[dom], "avg_launch_ms": avg_ms,
             "share_of_step": float(kms_tot[dom] / max(kms_tot.sum(), 1e-9)),
-            "class_ms_per_step": {names[i]: float(kms_tot[i] / args.steps) for i in range(4)},
-            "canonical_step": wm.canonical(q, float(world * B * N * H) / world, step_s,
-                                           6544.7, p_fp64)}
+            "class_ms_per_step": {names[i]: float(kms_tot[i] / args.steps) for i in range(4)}}
+    if fused and dom < 3:
+        cls = wm.fused_classes(n, q, B)[names[dom]]
+        flops, nbytes = cls["flops"] / cls["launches"], cls["bytes"] / cls["launches"]
+        t_hbm, t_fp = nbytes / (hbm_peak * 1e9), flops / (p_fp64 * 1e12)
+        gbs, tfs = nbytes / avg_s / 1e9, flops / avg_s / 1e12
+        traffic = None
+        if os.path.exists(TRAFFIC_FILE):
+            tr = json.load(open(TRAFFIC_FILE)).get("per_image_launch_bytes", {}).get(names[dom])
+            traffic = tr * B if tr else None
+        fp = {"achieved": tfs, "peak": p_fp64, "unit": "TFLOP/s", "frac": tfs / p_fp64, "peak_source": fsrc,
+              "algorithmic_flops_per_launch": flops}
+        hb = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak, "peak_source": hsrc,
+              "algorithmic_bytes_per_launch": nbytes}
+        main, other = (hb, fp) if t_hbm >= t_fp else (fp, hb)
+        roof.update({"bound": "hbm" if t_hbm >= t_fp else "tensor", **main, "traffic": traffic,
+                     "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per image, "
+                                       "profiles/r01_ncu_traffic.json, x images per launch",
+                     "form": "fused FFT-form pipeline (packed real DST-I, FFT correlation)",
+                     "secondary": other,
+                     "note": "nominal 5 N log2 N flops per FFT; arithmetic intensity below the FP64 ridge, "
+                             "so the HBM floor is the binding roofline"})
+    else:
+        per_launch_blur = (wm.conv_apply_flops(n, n, q, q) if fft_conv else wm.direct_apply_flops(n, n, q, q)) * B
+        if dom == 2:
+            launches_per_it = 3 if fft_dst else 4
+            flops = (wm.transform_iteration_flops(n, n, packed=False) if fft_dst else 8.0 * n * n * n) * B / launches_per_it
+            if not fft_dst:
+                p_fp64, fsrc = peaks.get("dmma_tflops_sustained", 37.0), "measured DMMA FP64 sustained (profiles/r01_fp64_peak.json)"
+        else:
+            flops = per_launch_blur
+        tfs = flops / avg_s / 1e12
+        roof.update({"bound": "tensor", "pipe": "FP64 (no tcgen05 FP64 kind on sm_100a; DFMA/DMMA)",
+                     "achieved": tfs, "peak": p_fp64, "unit": "TFLOP/s", "frac": tfs / p_fp64, "traffic": None,
+                     "peak_source": fsrc, "algorithmic_flops_per_launch": flops})
+    roof["dense_stencil_sol"] = wm.canonical(q, float(world * B * N * H) / world, step_s, hbm_peak, p_fp64)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -110,6 +110,13 @@ int dbx_plan_set_fusion(dbx_plan* plan, int enable);
 int dbx_plan_engines(dbx_plan* plan, int* conv, int* dst);
 
 /*
+ * Pipeline used by the last dbx_landweber_run on this plan: *fused = 1 for the
+ * fused row pipelines (6 launches + finalize per preconditioned iteration,
+ * fused.cu), 0 for the separate passes.  Diagnostic; no reference equivalent.
+ */
+int dbx_plan_pipeline(dbx_plan* plan, int* fused);
+
+/*
  * y = A x (adjoint = 0) or y = A' x (adjoint = 1), for every image of the
  * batch.  Replaces apply (blur.hpp:75-83) and apply_reblur_adjoint
  * (blur.hpp:87-90): AR extension computed on the fly, no padded image.

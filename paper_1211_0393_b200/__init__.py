@@ -65,6 +65,7 @@ def lib():
         L.dbx_plan_set_conv.argtypes = [vp, i]
         L.dbx_plan_set_dst.argtypes = [vp, i]
         L.dbx_plan_engines.argtypes = [vp, C.POINTER(i), C.POINTER(i)]
+        L.dbx_plan_pipeline.argtypes = [vp, C.POINTER(i)]
         L.dbx_plan_set_fusion.argtypes = [vp, i]
         L.dbx_blur_apply.argtypes = [vp, vp, vp, i]
         L.dbx_precond_build.argtypes = [vp, d]
@@ -262,6 +263,12 @@ class BlurOperator:
         c, d = C.c_int(), C.c_int()
         _check(lib().dbx_plan_engines(self.handle, C.byref(c), C.byref(d)))
         return ConvEngine(c.value), DstEngine(d.value)
+
+    def pipeline_fused(self) -> bool:
+        """True when the last landweber run used the fused row pipelines."""
+        f = C.c_int()
+        _check(lib().dbx_plan_pipeline(self.handle, C.byref(f)))
+        return bool(f.value)
 
     def stream(self):
         return lib().dbx_plan_stream(self.handle)

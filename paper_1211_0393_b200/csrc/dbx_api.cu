@@ -213,6 +213,7 @@ struct dbx_plan {
   std::string gkey;
   int64_t glaunches = 0;
   bool fusion = true;  // fused row pipelines when compiled for the sizes
+  bool last_fused = false;  // pipeline of the last landweber run
   // ---- FFT-form state ----
   int dst = DBX_DST_AUTO;
   bool conv_ready = false;
@@ -641,6 +642,13 @@ int dbx_plan_engines(dbx_plan* plan, int* conv, int* dst) {
   });
 }
 
+int dbx_plan_pipeline(dbx_plan* plan, int* fused) {
+  return guarded([&] {
+    require(plan != nullptr, "null plan");
+    if (fused) *fused = plan->last_fused ? 1 : 0;
+  });
+}
+
 int dbx_plan_set_timing(dbx_plan* plan, int enable) {
   return guarded([&] {
     require(plan != nullptr, "null plan");
@@ -841,6 +849,7 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
     const bool fused = use_precond && P->n1 == P->n2 && P->use_fft_conv() && P->use_fft_dst(false) && P->fusion &&
                        fused_supported(P->L2, P->blue_tables(1, false).M,
                                        P->blue_tables(1, false).M != P->blue_tables(1, false).N);
+    P->last_fused = fused;
     SpecArgs fa0 = P->spec_base(P->st, pt);
     if (fused) {
       fa0.conv.tw1 = reinterpret_cast<const double2*>(P->tw1);

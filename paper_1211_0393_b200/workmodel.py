@@ -33,16 +33,57 @@ def conv_len(n: int, q: int) -> int:
     return 0
 
 
-def dst_line_flops(n: int) -> float:
-    """Nominal flops of one AR transform line (length n): the packed N-point
-    DFT (N = n-1) directly, or Bluestein (2 FFTs of M + 3 pointwise passes)."""
+def dst_line_flops(n: int, packed: bool = True) -> float:
+    """Nominal flops of one AR transform line (length n).  The DST-I of the
+    interior (N = n-1) is one complex N-point DFT per line, or — packed real
+    form (pk_fill / pk_split, two lines per DFT) — half of one; the DFT is
+    direct (N smooth) or Bluestein (2 FFTs of M + 3 pointwise passes).
+    Pre/post-processing: ~16 flops per element (sine pre-twiddle, split,
+    odd-output scan, AR ramp)."""
     N = n - 1
+    share = 0.5 if packed else 1.0
     if N in DIRECT_DFT:
-        return 5.0 * N * math.log2(N) + 16.0 * N
+        return share * 5.0 * N * math.log2(N) + 16.0 * N
     M = next((m for m in BLUE_LENGTHS if m >= 2 * N - 1), 0)
     if not M:
         return 2.0 * (n - 2) * (n - 2)  # dense form
-    return 2 * 5.0 * M * math.log2(M) + 3 * 6.0 * M + 16.0 * N
+    return share * (2 * 5.0 * M * math.log2(M) + 3 * 6.0 * M) + 16.0 * N
+
+
+def row_fft_pass_flops(n1: int, n2: int, q2: int) -> float:
+    """One direction of the row FFTs of an FFT-form blur (two real rows per
+    complex FFT of length L2)."""
+    L2 = conv_len(n2, q2)
+    return (n1 + 1) // 2 * 5.0 * L2 * math.log2(L2)
+
+
+def col_pass_flops(n1: int, n2: int, q1: int, q2: int) -> float:
+    """Column pass: Lh columns x (forward FFT L1, spectrum multiply, inverse)."""
+    L1, L2 = conv_len(n1, q1), conv_len(n2, q2)
+    return (L2 // 2 + 1) * (2 * 5.0 * L1 * math.log2(L1) + 6.0 * L1)
+
+
+def fused_classes(n: int, q: int, images: int) -> dict:
+    """Per-iteration algorithmic work of the fused preconditioned pipeline
+    (fused.cu) by timing class, for `images` n x n images.
+
+    bytes = the arrays each launch must read and write once (Z/Y half spectra
+    16 n Lh bytes, images 8 n^2 bytes; the shared d^T grid once per launch)."""
+    L2 = conv_len(n, q)
+    Lh = L2 // 2 + 1
+    Z, P = 16.0 * n * Lh, 8.0 * n * n
+    rows, cols = row_fft_pass_flops(n, n, q), col_pass_flops(n, n, q, q)
+    dst = n * dst_line_flops(n, packed=True)
+    return {
+        # rows_ainv_tt (inverse rows of A'r + T~ rows), dst_tcols (T~ cols, d, T cols),
+        # rows_t_axpy_afwd (T rows + axpy + forward rows of A x)
+        "ar_transform_pass": {"launches": 3, "flops": images * (4 * dst + 2 * rows),
+                              "bytes": images * (2 * Z + 7 * P) + P},
+        # conv_col(A) + rows_ainv_resid (inverse rows of A x, r = g - A x, forward rows of r)
+        "blur(A)+residual": {"launches": 2, "flops": images * (cols + 2 * rows), "bytes": images * (4 * Z + P)},
+        # conv_col(A')
+        "blur_adjoint(A')": {"launches": 1, "flops": images * cols, "bytes": images * 2 * Z},
+    }
 
 
 def conv_apply_flops(n1: int, n2: int, q1: int, q2: int) -> float:
@@ -64,9 +105,9 @@ def direct_apply_flops(n1: int, n2: int, q1: int, q2: int) -> float:
     return 2.0 * (2 * q1 + 1) * (2 * q2 + 1) * n1 * n2
 
 
-def transform_iteration_flops(n1: int, n2: int) -> float:
+def transform_iteration_flops(n1: int, n2: int, packed: bool = True) -> float:
     """Four AR transform passes (T~ rows/cols, T cols/rows) per iteration."""
-    return 2 * n1 * dst_line_flops(n2) + 2 * n2 * dst_line_flops(n1)
+    return 2 * n1 * dst_line_flops(n2, packed) + 2 * n2 * dst_line_flops(n1, packed)
 
 
 def transform_iteration_bytes(n1: int, n2: int) -> float:
@@ -75,8 +116,11 @@ def transform_iteration_bytes(n1: int, n2: int) -> float:
 
 
 def canonical(q: int, px_it: float, seconds: float, bw_gbs: float, p_fp64_tflops: float):
+    """Speed-of-light of the reference's own algorithm: dense
+    direct-stencil correlation for A and A' plus FFT-form DST-I.  The FFT-form
+    pipeline does far fewer flops, so t_meas < t_min is possible."""
     B, F = 72.0, 4.0 * (2 * q + 1) ** 2 + 250.0
     t_min = max(B * px_it / (bw_gbs * 1e9), F * px_it / (p_fp64_tflops * 1e12))
     return {"bytes_per_px_it": B, "flops_per_px_it": F, "t_min_s": t_min, "t_meas_s": seconds,
-            "frac": t_min / seconds if seconds > 0 else None,
+            "t_min_over_t_meas": t_min / seconds if seconds > 0 else None,
             "bound": "fp64" if F * bw_gbs * 1e9 > B * p_fp64_tflops * 1e12 else "hbm"}
