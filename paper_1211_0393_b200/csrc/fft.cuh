@@ -41,9 +41,15 @@ __host__ __device__ constexpr int next_radix(int rem) {
   if (rem % 8 == 0) return 8;
   if (rem % 4 == 0) return 4;
   if (rem % 2 == 0) return 2;
-  constexpr int primes[10] = {31, 29, 23, 19, 17, 13, 11, 7, 5, 3};
-  for (int i = 0; i < 10; ++i)
+  constexpr int primes[8] = {31, 29, 23, 19, 17, 13, 11, 7};
+  for (int i = 0; i < 8; ++i)
     if (rem % primes[i] == 0) return primes[i];
+  // 3^a 5^b: composite in-register radices 15 (3x5 prime factor) and 9 (3x3)
+  // halve the number of shared-memory passes against 5, 3, 3, ...
+  if (rem % 15 == 0) return 15;
+  if (rem % 9 == 0) return 9;
+  if (rem % 5 == 0) return 5;
+  if (rem % 3 == 0) return 3;
   return 0;
 }
 
@@ -158,6 +164,61 @@ __device__ __forceinline__ void dft5(double2* v) {
   v[3] = csub(m2, n2);
 }
 
+// Radix 9 = 3 x 3 (Cooley-Tukey): DFT-3 over n1 for each n2, internal twiddles
+// W9^{n2 k1}, DFT-3 over n2; output k = k1 + 3 k2 (natural order).
+template <int S>
+__device__ __forceinline__ void dft9(double2* v) {
+  constexpr double c1 = 0.76604444311897803520239265055541667;   // cos(2pi/9)
+  constexpr double s1 = 0.64278760968653932632264340990726343;   // sin(2pi/9)
+  constexpr double c2 = 0.17364817766693034885171662676931480;   // cos(4pi/9)
+  constexpr double s2 = 0.98480775301220805936674302458952301;   // sin(4pi/9)
+  constexpr double c4 = -0.93969262078590838405410927732473147;  // cos(8pi/9)
+  constexpr double s4 = 0.34202014332566873304409961468225958;   // sin(8pi/9)
+  double2 y[3][3];
+#pragma unroll
+  for (int n2 = 0; n2 < 3; ++n2) {
+    double2 t[3] = {v[n2], v[n2 + 3], v[n2 + 6]};
+    dft3<S>(t);
+    y[n2][0] = t[0];
+    y[n2][1] = t[1];
+    y[n2][2] = t[2];
+  }
+  y[1][1] = cmul(y[1][1], make_double2(c1, S * s1));
+  y[1][2] = cmul(y[1][2], make_double2(c2, S * s2));
+  y[2][1] = cmul(y[2][1], make_double2(c2, S * s2));
+  y[2][2] = cmul(y[2][2], make_double2(c4, S * s4));
+#pragma unroll
+  for (int k1 = 0; k1 < 3; ++k1) {
+    double2 t[3] = {y[0][k1], y[1][k1], y[2][k1]};
+    dft3<S>(t);
+    v[k1] = t[0];
+    v[k1 + 3] = t[1];
+    v[k1 + 6] = t[2];
+  }
+}
+
+// Radix 15 = 3 x 5 prime-factor (Good-Thomas, no internal twiddles): input
+// n = (5 n1 + 3 n2) mod 15, output k = (10 k1 + 6 k2) mod 15.
+template <int S>
+__device__ __forceinline__ void dft15(double2* v) {
+  double2 y[5][3];
+#pragma unroll
+  for (int n2 = 0; n2 < 5; ++n2) {
+    double2 t[3] = {v[(3 * n2) % 15], v[(5 + 3 * n2) % 15], v[(10 + 3 * n2) % 15]};
+    dft3<S>(t);
+    y[n2][0] = t[0];
+    y[n2][1] = t[1];
+    y[n2][2] = t[2];
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 3; ++k1) {
+    double2 u[5] = {y[0][k1], y[1][k1], y[2][k1], y[3][k1], y[4][k1]};
+    dft5<S>(u);
+#pragma unroll
+    for (int k2 = 0; k2 < 5; ++k2) v[(10 * k1 + 6 * k2) % 15] = u[k2];
+  }
+}
+
 // Odd prime P >= 7 via the (P-1)/2 symmetric pairs:
 //   X_k = x0 + sum_j c_jk a_j + S i sum_j s_jk b_j,  X_{P-k} = same with -S i,
 //   a_j = x_j + x_{P-j}, b_j = x_j - x_{P-j}; ~2P real FMAs per element instead
@@ -235,20 +296,26 @@ __device__ __forceinline__ void dft(double2* v) {
   else if constexpr (R == 8) dft8<S>(v);
   else if constexpr (R == 3) dft3<S>(v);
   else if constexpr (R == 5) dft5<S>(v);
+  else if constexpr (R == 9) dft9<S>(v);
+  else if constexpr (R == 15) dft15<S>(v);
   else dft_odd<R, S>(v);
 }
 
-// Stage twiddles W^{r k}, r = 1..R-1, from ONE table read (W^k): the powers
-// come from a balanced product tree (w_r = w_{r/2} w_{r - r/2}, depth log2 R,
-// <= ~4 ulp), which removes (R-2)/(R-1) of the per-stage twiddle traffic on
-// the shared-memory pipe (the FFT stages are smem-bandwidth bound).
-template <int R>
-__device__ __forceinline__ void twiddle_powers(double2* w, double2 w1) {
-  w[0] = w1;
+// v[r] *= W^r (S < 0) or conj(W^r) (S > 0), r = 1..R-1, with the powers formed
+// on the fly from a window of four: w_r = w_{r-4} w_4 for r > 4 (product depth
+// <= r/4 + 2, a few ulp), so at most five twiddles are live instead of R-1.
+template <int R, int S>
+__device__ __forceinline__ void apply_twiddles(double2* v, double2 w1) {
+  double2 win[4];
+  win[0] = w1;
+  win[1] = cmul(w1, w1);
+  win[2] = cmul(win[1], w1);
+  win[3] = cmul(win[1], win[1]);
+  const double2 w4 = win[3];
 #pragma unroll
-  for (int r = 2; r < R; ++r) {
-    const int a = r / 2;
-    w[r - 1] = cmul(w[a - 1], w[r - a - 1]);
+  for (int r = 1; r < R; ++r) {
+    if (r > 4) win[(r - 1) & 3] = cmul(win[(r - 1) & 3], w4);
+    v[r] = S < 0 ? cmul(v[r], win[(r - 1) & 3]) : cmulc(v[r], win[(r - 1) & 3]);
   }
 }
 
@@ -257,7 +324,6 @@ template <int L, int Ns, int R, int S, int T>
 __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ tw, int t) {
   constexpr int NB = L / R;
   constexpr int PER = (NB + T - 1) / T;
-  constexpr int NW = Ns > 1 ? R - 1 : 1;
   double2 v[PER][R];
   double2 w1[PER];
   // base twiddles first: their (L1/L2) latency overlaps the smem loads and
@@ -284,120 +350,15 @@ __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ 
     const int b = t + i * T;
     if (NB % T == 0 || b < NB) {
       const int k = b % Ns;
-      if constexpr (Ns > 1) {
-        double2 w[NW];
-        twiddle_powers<R>(w, w1[i]);
-#pragma unroll
-        for (int r = 1; r < R; ++r)
-          v[i][r] = S < 0 ? cmul(v[i][r], w[r - 1]) : cmulc(v[i][r], w[r - 1]);
-      }
+      if constexpr (Ns > 1) apply_twiddles<R, S>(v[i], w1[i]);
       const int base = (b / Ns) * Ns * R + k;
-      if constexpr (R >= 7 && (R & 1)) {
+      if constexpr (R >= 7 && (R & 1) && R != 9 && R != 15) {
         dft_odd_store<R, S, L>(v[i], buf, base, Ns);
       } else {
         dft<R, S>(v[i]);
 #pragma unroll
         for (int r = 0; r < R; ++r) buf[pad<L>(base + r * Ns)] = v[i][r];
       }
-    }
-  }
-  __syncthreads();
-}
-
-// Output pairs k = H0+1 .. H1 of an odd-prime butterfly whose symmetric pairs
-// are already in v (v[j] = a_j, v[P-j] = b_j); H0/H1 compile-time so every
-// constant is a fixed c[bank][offset] operand.
-template <int P, int S, int H0, int H1, int L>
-__device__ __forceinline__ void odd_part(const double2* v, double2 x0, double2* buf, int base, int Ns) {
-  using K = OddConst<P>;
-  constexpr int H = (P - 1) / 2;
-#pragma unroll
-  for (int k = H0 + 1; k <= H1; ++k) {
-    double2 A = x0, B = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int j = 1; j <= H; ++j) {
-      const int e = (j * k) % P;
-      A.x = fma(K::c(e), v[j].x, A.x);
-      A.y = fma(K::c(e), v[j].y, A.y);
-      B.x = fma(K::s(e), v[P - j].x, B.x);
-      B.y = fma(K::s(e), v[P - j].y, B.y);
-    }
-    const double2 sb = mul_si<S>(B);
-    buf[pad<L>(base + k * Ns)] = cadd(A, sb);
-    buf[pad<L>(base + (P - k) * Ns)] = csub(A, sb);
-  }
-}
-
-// Stockham stage for a large odd prime R (>= 17): every butterfly is shared by
-// two warp-uniform halves (slot = half * NBp + b, NBp = NB rounded to warps),
-// each computing half of the (R-1)/2 output pairs.  This halves the live
-// accumulators (the full butterfly needs ~234 registers) and doubles the
-// number of busy threads in the stage (NB = L/R is small).
-template <int L, int Ns, int R, int S, int T>
-__device__ __forceinline__ void stage_split(double2* buf, const double2* __restrict__ tw, int t) {
-  constexpr int NB = L / R;
-  constexpr int NBp = (NB + 31) / 32 * 32;
-  constexpr int SLOTS = 2 * NBp;
-  constexpr int PER = (SLOTS + T - 1) / T;
-  constexpr int H = (R - 1) / 2;
-  static_assert(PER == 1, "split stage expects one slot per thread");
-  const int half = t / NBp;           // warp-uniform
-  const int b = t - half * NBp;
-  const bool act = t < SLOTS && b < NB;
-  double2 v[R];
-  double2 w[Ns > 1 ? R - 1 : 1];
-  const int k = act ? b % Ns : 0;
-  if constexpr (Ns > 1) {
-    constexpr int step = L / (Ns * R);
-    if (act) {
-#pragma unroll
-      twiddle_powers<R>(w, tw[k * step]);
-    }
-  }
-  if (act) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = buf[pad<L>(b + r * NB)];
-  }
-  __syncthreads();
-  if (act) {
-    if constexpr (Ns > 1) {
-#pragma unroll
-      for (int r = 1; r < R; ++r) v[r] = S < 0 ? cmul(v[r], w[r - 1]) : cmulc(v[r], w[r - 1]);
-    }
-    const double2 x0 = v[0];
-    double2 sum = x0;
-#pragma unroll
-    for (int j = 1; j <= H; ++j) {
-      const double2 a = cadd(v[j], v[R - j]);
-      const double2 c = csub(v[j], v[R - j]);
-      v[j] = a;
-      v[R - j] = c;
-      sum = cadd(sum, a);
-    }
-    const int base = (b / Ns) * Ns * R + k;
-    if (half == 0) buf[pad<L>(base)] = sum;
-    // rolled loop over this half's output pairs: the pair index kk is
-    // warp-uniform, so the constant-table reads go through the uniform
-    // datapath (ULDC -> DFMA UR operand) and only one pair's accumulators live
-    const int k0 = half == 0 ? 1 : H / 2 + 1, k1 = half == 0 ? H / 2 : H;
-    using K = OddConst<R>;
-#pragma unroll 1
-    for (int kk = k0; kk <= k1; ++kk) {
-      double2 A = x0, B = make_double2(0.0, 0.0);
-      int e = 0;
-#pragma unroll
-      for (int j = 1; j <= H; ++j) {
-        e += kk;
-        if (e >= R) e -= R;
-        const double c = K::c(e), s = K::s(e);
-        A.x = fma(c, v[j].x, A.x);
-        A.y = fma(c, v[j].y, A.y);
-        B.x = fma(s, v[R - j].x, B.x);
-        B.y = fma(s, v[R - j].y, B.y);
-      }
-      const double2 sb = mul_si<S>(B);
-      buf[pad<L>(base + kk * Ns)] = cadd(A, sb);
-      buf[pad<L>(base + (R - kk) * Ns)] = csub(A, sb);
     }
   }
   __syncthreads();
@@ -479,12 +440,7 @@ __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __rest
   }
   __syncthreads();
   if (act) {
-    if constexpr (Ns > 1) {
-      double2 w[R - 1];
-      twiddle_powers<R>(w, w1);
-#pragma unroll
-      for (int r = 1; r < R; ++r) v[r] = S < 0 ? cmul(v[r], w[r - 1]) : cmulc(v[r], w[r - 1]);
-    }
+    if constexpr (Ns > 1) apply_twiddles<R, S>(v, w1);
     const double2 x0 = v[0];
     double2 sum = x0;
 #pragma unroll
@@ -507,11 +463,7 @@ __device__ __forceinline__ void run_stages(double2* buf, const double2* __restri
   if constexpr (Ns < L) {
     constexpr int R = next_radix(L / Ns);
     static_assert(R != 0, "FFT length must factor into {2,3,4,5,8} and odd primes <= 31");
-    constexpr int NBp = (L / R + 31) / 32 * 32;
-    if constexpr (R >= 17 && (R & 1) && 2 * NBp <= T)
-      stage_split<L, Ns, R, S, T>(buf, tw, t);
-    else
-      stage<L, Ns, R, S, T>(buf, tw, t);
+    stage<L, Ns, R, S, T>(buf, tw, t);
     run_stages<L, Ns * R, S, T>(buf, tw, t);
   }
 }
