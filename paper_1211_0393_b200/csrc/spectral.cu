@@ -94,55 +94,91 @@ conv_col(SpecArgs a) {
   const int n1 = a.n1, q1 = a.q1, Lh = a.conv.Lh;
   const int k0 = blockIdx.x * G;
   const int kk = k0 + g;
-  // group 0: twiddles; group 1: this CTA's kernel-spectrum columns ([k2][k1]
-  // layout, contiguous in p) -- both land while the columns are loaded / FFT'd
+  // cp.async groups: twiddles, (ztrans) this line's spectrum column, then the
+  // kernel-spectrum columns ([k2][k1] layout, contiguous in p) which may still
+  // be in flight during the forward FFT
   double2* hst = sm + SM::lines + g * padded_len(L1);
   const double2* tw = stage_twiddles<L1, SM::TW>(sm + SM::lines + (SM::HS ? SM::lines : 0), a.conv.tw1);
   const double2* Hcol = a.conv.H + (size_t)(kk < Lh ? kk : 0) * L1;
-  if constexpr (SM::HS) {
-    for (int p = t; p < L1; p += T) cp_async16(hst + p, Hcol + p);
-  }
-  cp_async_commit();
   const double2* Z = a.zbuf + (size_t)b * n1 * Lh;
   const int hext_rows = n1 + 2 * q1;
-  // load the G columns with the vertical AR extension synthesised spectrally
-  // (loads batched in registers first, then stored)
-  constexpr int PF = (L1 * G + NT - 1) / NT;
-  double2 v[PF];
-  // element (rho, k) of the spectra: [rho][k] (default) or [k][rho] (ztrans,
-  // contiguous per column: each line's loads are fully coalesced)
-  const size_t sr = a.ztrans ? 1 : (size_t)Lh, sk = a.ztrans ? (size_t)n1 : 1;
+  double2* buf = sm + g * padded_len(L1);
+  if (a.ztrans) {
+    // column kk of Z^T is contiguous: copy it straight into rows q1 .. q1+n1-1
+    // of the line (no registers, all loads in flight at once)
+    if (kk < Lh) {
+      const double2* zc = Z + (size_t)kk * n1;
+      for (int rho = t; rho < n1; rho += T) cp_async16(buf + pad<L1>(rho + q1), zc + rho);
+    }
+    cp_async_commit();
+    // bulk-prefetch into L2 the column of the CTA one resident wave ahead, so
+    // its copies hit L2 instead of waiting on HBM
+    if (t == 0) {
+      const long long ahead = (long long)blockIdx.y * gridDim.x + blockIdx.x + 2 * nsm();
+      const int bb = (int)(ahead / gridDim.x), kx = (int)(ahead % gridDim.x) * G + g;
+      if (bb < a.batch && kx < Lh)
+        prefetch_l2(a.zbuf + (size_t)bb * n1 * Lh + (size_t)kx * n1, (unsigned)n1 * 16);
+    }
+    if constexpr (SM::HS) {
+      for (int p = t; p < L1; p += T) cp_async16(hst + p, Hcol + p);
+    }
+    cp_async_commit();
+    cp_async_wait_group<1>();
+    __syncthreads();
+    // vertical AR extension synthesised spectrally (Z[-i] = 2 Z[0] - Z[i]) and
+    // the zero tail, from the rows already in shared memory
+    for (int p = t; p < L1; p += T) {
+      if (p >= q1 && p < q1 + n1) continue;
+      double2 v = make_double2(0.0, 0.0);
+      if (kk < Lh && p < hext_rows) {
+        const int rho = p - q1;
+        const int r0 = rho < 0 ? 0 : n1 - 1, ri = rho < 0 ? -rho : 2 * (n1 - 1) - rho;
+        const double2 z0 = buf[pad<L1>(r0 + q1)], zi = buf[pad<L1>(ri + q1)];
+        v = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
+      }
+      buf[pad<L1>(p)] = v;
+    }
+    if (kk >= Lh)
+      for (int p = q1 + t; p < q1 + n1; p += T) buf[pad<L1>(p)] = make_double2(0.0, 0.0);
+    __syncthreads();
+  } else {
+    if constexpr (SM::HS) {
+      for (int p = t; p < L1; p += T) cp_async16(hst + p, Hcol + p);
+    }
+    cp_async_commit();
+    cp_async_commit();  // (empty) keeps the group count of the ztrans branch
+    // load the G columns with the vertical AR extension synthesised spectrally
+    // (loads batched in registers first, then stored)
+    constexpr int PF = (L1 * G + NT - 1) / NT;
+    double2 v[PF];
 #pragma unroll
-  for (int i = 0; i < PF; ++i) {
-    const int idx = threadIdx.x + i * NT;
-    // ztrans: thread-contiguous along p within one line; else along k
-    const int p = a.ztrans ? idx % L1 : idx / G;
-    const int gg = a.ztrans ? idx / L1 : idx - p * G;
-    const int k = k0 + gg;
-    v[i] = make_double2(0.0, 0.0);
-    if (idx < L1 * G && k < Lh && p < hext_rows) {
-      const int rho = p - q1;
-      if (rho < 0) {
-        const double2 z0 = Z[k * sk], zi = Z[(size_t)(-rho) * sr + k * sk];
-        v[i] = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
-      } else if (rho >= n1) {
-        const double2 z0 = Z[(size_t)(n1 - 1) * sr + k * sk], zi = Z[(size_t)(2 * (n1 - 1) - rho) * sr + k * sk];
-        v[i] = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
-      } else {
-        v[i] = Z[(size_t)rho * sr + k * sk];
+    for (int i = 0; i < PF; ++i) {
+      const int idx = threadIdx.x + i * NT;
+      const int p = idx / G, gg = idx - p * G;
+      const int k = k0 + gg;
+      v[i] = make_double2(0.0, 0.0);
+      if (idx < L1 * G && k < Lh && p < hext_rows) {
+        const int rho = p - q1;
+        if (rho < 0) {
+          const double2 z0 = Z[k], zi = Z[(size_t)(-rho) * Lh + k];
+          v[i] = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
+        } else if (rho >= n1) {
+          const double2 z0 = Z[(size_t)(n1 - 1) * Lh + k], zi = Z[(size_t)(2 * (n1 - 1) - rho) * Lh + k];
+          v[i] = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
+        } else {
+          v[i] = Z[(size_t)rho * Lh + k];
+        }
       }
     }
-  }
 #pragma unroll
-  for (int i = 0; i < PF; ++i) {
-    const int idx = threadIdx.x + i * NT;
-    const int p = a.ztrans ? idx % L1 : idx / G;
-    const int gg = a.ztrans ? idx / L1 : idx - p * G;
-    if (idx < L1 * G) sm[gg * padded_len(L1) + pad<L1>(p)] = v[i];
+    for (int i = 0; i < PF; ++i) {
+      const int idx = threadIdx.x + i * NT;
+      const int p = idx / G, gg = idx - p * G;
+      if (idx < L1 * G) sm[gg * padded_len(L1) + pad<L1>(p)] = v[i];
+    }
+    cp_async_wait_group<2>();  // twiddles landed (H may still be in flight)
+    __syncthreads();
   }
-  cp_async_wait_group<1>();  // twiddles landed (H may still be in flight)
-  __syncthreads();
-  double2* buf = sm + g * padded_len(L1);
   fft::fft<L1, -1, T>(buf, tw, t);
   cp_async_wait_all();  // each thread multiplies only the entries it staged
   if constexpr (SM::HS) {

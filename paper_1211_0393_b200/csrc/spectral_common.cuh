@@ -76,6 +76,13 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// Number of SMs (for prefetch-ahead distances of one resident wave).
+__device__ __forceinline__ int nsm() {
+  unsigned r;
+  asm("mov.u32 %0, %%nsmid;" : "=r"(r));
+  return (int)r;
+}
+
 // Twiddle table of an FFT length L staged into shared memory (cp.async group
 // committed here) when `smem_ok`, else read from global (L1/L2).
 template <int L, bool SMEM>
