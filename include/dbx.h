@@ -60,13 +60,17 @@ extern "C" {
 #define DBX_CONV_DIRECT 1
 #define DBX_CONV_FFT 2
 
-/* AR-transform engine selection (dbx_plan_set_dst).  FFT = Bluestein DST-I in
- * shared memory (power-of-two M >= 2N-1 up to 8192); DENSE = FP64 GEMM with the
- * dense T~/T matrices (reference dense_ar_forward / dense_ar_inverse block
- * forms).  AUTO picks FFT whenever the length is compiled. */
+/* AR-transform engine selection (dbx_plan_set_dst).  FFT = packed real DST-I in
+ * shared memory (two lines per complex N-point DFT) whose DFT core is direct
+ * (N with prime factors <= 31), Bluestein (power-of-two M >= 2N-1 up to 8192)
+ * or Rader (N prime, N-1 compiled, e.g. 8191); DENSE = FP64 GEMM with the dense
+ * T~/T matrices (reference dense_ar_forward / dense_ar_inverse block forms);
+ * RADER = FFT with the Rader core forced where N is prime (tests).  AUTO picks
+ * FFT whenever a core exists for the length. */
 #define DBX_DST_AUTO 0
 #define DBX_DST_DENSE 1
 #define DBX_DST_FFT 2
+#define DBX_DST_RADER 3
 
 typedef struct dbx_plan dbx_plan;
 

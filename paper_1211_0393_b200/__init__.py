@@ -157,6 +157,7 @@ class DstEngine(enum.IntEnum):
     Auto = 0
     Dense = 1
     Fft = 2
+    Rader = 3
 
 
 # ---------------------------------------------------------------------------

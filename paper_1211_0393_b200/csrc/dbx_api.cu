@@ -246,6 +246,14 @@ struct dbx_plan {
     owned.push_back(p);
     return p;
   }
+  const int* upload_owned_int(const std::vector<int>& h) {
+    int* p = nullptr;
+    ck(cudaMalloc(&p, h.size() * sizeof(int)), "cudaMalloc");
+    ck(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, stream), "upload");
+    ck(cudaStreamSynchronize(stream), "upload sync");
+    owned.push_back(reinterpret_cast<double*>(p));
+    return p;
+  }
 
   // ---- engine selection ----
   // Conv: the reference switches to FFT correlation for q > 7 (blur.hpp:70,
@@ -257,19 +265,23 @@ struct dbx_plan {
     if (conv == DBX_CONV_FFT) return fits;
     return fits && (q1 > 7 || q2 > 7);
   }
-  // DST line length: the direct odd-length DFT when N is compiled (prime
-  // factors <= 31: 255, 1023, ...), else a power-of-two Bluestein M >= 2N-1.
-  static int blue_len(int N) {
-    if (direct_supported_len(N)) return N;
-    return blue_supported_len(2 * N - 1 < 16 ? 16 : 2 * N - 1);
+  // DST core and DFT length M for an N-point DFT: direct (N compiled: prime
+  // factors <= 31), Bluestein (compiled power of two M >= 2N-1), Rader (N
+  // prime, N-1 compiled; e.g. 8191 for C5).  DBX_DST_RADER forces Rader.
+  int dst_core(int N, int* M) const {
+    if (dst != DBX_DST_RADER) {
+      if (direct_supported_len(N)) { *M = N; return CORE_DIRECT; }
+      const int Mb = blue_supported_len(2 * N - 1 < 16 ? 16 : 2 * N - 1);
+      if (Mb) { *M = Mb; return CORE_BLUE; }
+    }
+    if (N > 2 && is_prime(N) && rader_supported_len(N - 1)) { *M = N - 1; return CORE_RADER; }
+    return -1;
   }
-  // The packed Bluestein DST-I reads the odd outputs from the (-1)^j-modulated
-  // DFT, which needs N = m+1 odd (every BASELINE config: N = n-1, n even);
-  // even N runs the dense engine.
   bool use_fft_dst(bool sine) const {
     if (dst == DBX_DST_DENSE) return false;
     const int N1 = sine ? n1 + 1 : n1 - 1, N2 = sine ? n2 + 1 : n2 - 1;
-    return (N1 & 1) && (N2 & 1) && blue_len(N1) > 0 && blue_len(N2) > 0;
+    int M = 0;
+    return N1 >= 2 && N2 >= 2 && dst_core(N1, &M) >= 0 && dst_core(N2, &M) >= 0;
   }
 
   void ensure_conv() {
@@ -294,13 +306,21 @@ struct dbx_plan {
     if (!B.ready) {
       const int n = axis == 0 ? n1 : n2;
       const int N = sine ? n + 1 : n - 1;
-      const BlueHost h = bluestein(n, sine, blue_len(N));
+      int M = 0;
+      const int core = dst_core(N, &M);
+      require(core >= 0, "no FFT-form DST for this line length");
+      const BlueHost h = core == CORE_RADER ? rader(n, sine) : bluestein(n, sine, M);
       B.tw = upload_owned(h.tw);
       B.chirp = upload_owned(h.chirp);
       B.bhat = upload_owned(h.bhat);
       B.p = upload_owned(h.p);
       B.sn = upload_owned(h.sn);
       B.t.sn = B.sn;
+      if (core == CORE_RADER) {
+        B.t.dlog = upload_owned_int(h.dlog);
+        B.t.ridx = upload_owned_int(h.ridx);
+      }
+      B.t.core = core;
       B.t.tw = reinterpret_cast<const double2*>(B.tw);
       B.t.chirp = reinterpret_cast<const double2*>(B.chirp);
       B.t.bhat = reinterpret_cast<const double2*>(B.bhat);
@@ -621,8 +641,12 @@ int dbx_plan_set_conv(dbx_plan* plan, int conv) {
 int dbx_plan_set_dst(dbx_plan* plan, int engine) {
   return guarded([&] {
     require(plan != nullptr, "null plan");
-    require(engine == DBX_DST_AUTO || engine == DBX_DST_DENSE || engine == DBX_DST_FFT,
+    require(engine == DBX_DST_AUTO || engine == DBX_DST_DENSE || engine == DBX_DST_FFT ||
+                engine == DBX_DST_RADER,
             "dbx_plan_set_dst: unknown engine");
+    if (engine != plan->dst)
+      for (auto& ax : plan->blue)
+        for (auto& B : ax) B.ready = false;  // the DFT core may change: rebuild the tables
     plan->dst = engine;
   });
 }
@@ -847,8 +871,9 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
     // Fused FFT-form pipeline (fused.cu): 6 launches + finalize per iteration.
     P->prepare(use_precond != 0);
     const bool fused = use_precond && P->n1 == P->n2 && P->use_fft_conv() && P->use_fft_dst(false) && P->fusion &&
+                       P->blue_tables(1, false).core != CORE_RADER &&
                        fused_supported(P->L2, P->blue_tables(1, false).M,
-                                       P->blue_tables(1, false).M != P->blue_tables(1, false).N);
+                                       P->blue_tables(1, false).core == CORE_BLUE);
     P->last_fused = fused;
     SpecArgs fa0 = P->spec_base(P->st, pt);
     if (fused) {

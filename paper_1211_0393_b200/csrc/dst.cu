@@ -1,0 +1,373 @@
+// dst.cu — separate-pass AR / SineI transforms (tensor_apply, precondition_apply,
+// and the D-Landweber iteration when the fused row pipelines do not apply) in
+// packed real form: TWO image lines per complex N-point DFT (sine pre-twiddle,
+// conjugate-symmetric split, odd-output prefix scan — spectral_common.cuh).
+//
+// The N-point DFT (N = m+1 for the SineI kind, N = n-1 for the AR kinds) has
+// three cores, chosen per axis on the host:
+//   CORE_DIRECT  M = N, N smooth (prime factors <= 31): one mixed-radix FFT;
+//   CORE_BLUE    M = 2^k >= 2N-1: Bluestein chirp-z (FFT, kernel multiply, IFFT);
+//   CORE_RADER   M = N-1, N prime with N-1 smooth (8191 for C5): Rader's cyclic
+//                convolution over the generator order (FFT, kernel, IFFT).
+// The DST outputs overwrite the FFT line in place (two real lines of doubles),
+// so a line costs padded_len(M) * 16 bytes of shared memory and nothing more:
+// M = 8190 / 8192 lines (C5, 147 KB) fit one CTA.
+//
+// Replaces (reference): sine1_forward + r2r RODFT00 (transforms.hpp:114-121,
+// 28-53), ar_forward / ar_inverse (transforms.hpp:148-173), tensor_map /
+// tensor_apply (transforms.hpp:179-221), filter_apply AR branch
+// (spectral.hpp:161-165).
+#include <cuda_runtime.h>
+
+#include "spectral_common.cuh"
+
+namespace dbx {
+
+namespace {
+
+template <int M, int CORE>
+struct DstCfg {
+  static constexpr int T = line_threads(M, dst_per(M));
+  static constexpr int G = lines_for(M, kDstBudget, dst_per(M));  // FFT lines per CTA
+  static constexpr int NT = T * G;
+  static constexpr int LINE = padded_len(M);                      // double2 per FFT line
+  static constexpr int LO = LINE;                                 // output line stride (doubles)
+  static constexpr int TWN = fft::twiddles_needed(M);
+  static constexpr size_t base = (size_t)G * LINE * 16;
+  static constexpr bool TW = base + (size_t)TWN * 16 <= kSmemCap;
+  static constexpr size_t bytes = base + (TW ? (size_t)TWN * 16 : 0);
+  static constexpr int NMAX = CORE == CORE_BLUE ? M / 2 + 1 : M + 1;  // N <= NMAX
+  static constexpr int PS = ((NMAX - 1) / 2 + 1 + T - 1) / T;         // split items per thread
+};
+
+// buffer position of z_j and the DFT output Z_l for each core
+template <int M, int CORE>
+__device__ __forceinline__ double2 pkc_get(const double2* buf, const BlueTables& bt, int l, double2 A0) {
+  if constexpr (CORE == CORE_RADER) {
+    if (l == 0) return A0;
+    return buf[pad<M>(__ldg(bt.ridx + l))];
+  } else if constexpr (CORE == CORE_BLUE) {
+    return cmul(buf[pad<M>(l)], __ldg(bt.chirp + l));
+  } else {
+    return buf[pad<M>(l)];
+  }
+}
+
+// Fill one FFT line with z_j = y^a_j + i y^b_j (pk_fill), placed per core.
+template <int M, int T, int CORE, typename F>
+__device__ __forceinline__ void pkc_fill(double2* buf, const BlueTables& bt, int t, F val) {
+  const int N = bt.N;
+  auto zj = [&](int j) {
+    const double s = __ldg(bt.sn + j);
+    const double xa = val(0, j), xar = val(0, N - j);
+    const double xb = val(1, j), xbr = val(1, N - j);
+    return make_double2(fma(s, xa + xar, 0.5 * (xa - xar)), fma(s, xb + xbr, 0.5 * (xb - xbr)));
+  };
+  if constexpr (CORE == CORE_RADER) {
+    // a_p = z_{g^p}: position dlog[j] for j = 1..N-1 (a bijection onto [0, M))
+    for (int j = 1 + t; j < N; j += T) buf[pad<M>(__ldg(bt.dlog + j))] = zj(j);
+  } else {
+    for (int j = t; j < M; j += T) {
+      double2 z = make_double2(0.0, 0.0);
+      if (j >= 1 && j < N) {
+        z = zj(j);
+        if constexpr (CORE == CORE_BLUE) z = cmul(z, __ldg(bt.chirp + j));
+      }
+      buf[pad<M>(j)] = z;
+    }
+  }
+}
+
+// The N-point DFT of the G lines (every thread of the CTA calls it).
+template <int M, int T, int G, int CORE>
+__device__ __forceinline__ void pkc_core(double2* sm, double2* buf, const BlueTables& bt, const double2* tw, int t,
+                                         double2* A0s, int g) {
+  cp_async_wait_all();
+  __syncthreads();
+  if constexpr (CORE == CORE_DIRECT && (M & 1)) {
+    fft::fft_cta<M, -1, T, G>(sm, tw, threadIdx.x);
+  } else {
+    fft::fft<M, -1, T>(buf, tw, t);
+    if constexpr (CORE != CORE_DIRECT) {
+      if constexpr (CORE == CORE_RADER) {
+        if (t == 0) A0s[g] = buf[pad<M>(0)];  // X_0 = sum of a (z_0 = 0)
+      }
+      for (int p = t; p < M; p += T) buf[pad<M>(p)] = cmul(buf[pad<M>(p)], __ldg(bt.bhat + p));
+      __syncthreads();
+      fft::fft<M, +1, T>(buf, tw, t);
+    }
+  }
+}
+
+// pk_split in place: the DST outputs of lines a, b overwrite the FFT line as
+// doubles oa = [0, LO), ob = [LO, 2 LO).  Reads land in registers, then a
+// CTA barrier, then the writes.
+template <int M, int T, int CORE, int PS, int LO>
+__device__ __forceinline__ void pkc_split(double2* buf, const BlueTables& bt, int t, double2 A0) {
+  const int N = bt.N;
+  const double hs = 0.5 * bt.scale;
+  double r[PS][4];
+#pragma unroll
+  for (int i = 0; i < PS; ++i) {
+    const int l = t + i * T;
+    if (2 * l <= N - 1) {
+      const double2 zl = pkc_get<M, CORE>(buf, bt, l, A0);
+      const double2 zm = pkc_get<M, CORE>(buf, bt, l == 0 ? 0 : N - l, A0);
+      const double f = l == 0 ? 0.25 : 0.5;
+      r[i][0] = hs * (zm.y - zl.y);   // X^a_{2l}
+      r[i][1] = hs * (zl.x - zm.x);   // X^b_{2l}
+      r[i][2] = f * (zl.x + zm.x);    // scan term of X^a_{2l+1}
+      r[i][3] = f * (zl.y + zm.y);    // scan term of X^b_{2l+1}
+    }
+  }
+  __syncthreads();
+  double* oa = reinterpret_cast<double*>(buf);
+  double* ob = oa + LO;
+#pragma unroll
+  for (int i = 0; i < PS; ++i) {
+    const int l = t + i * T;
+    if (2 * l <= N - 1) {
+      if (l >= 1) {
+        oa[2 * l] = r[i][0];
+        ob[2 * l] = r[i][1];
+      }
+      if (2 * l + 1 <= N - 1) {
+        oa[2 * l + 1] = r[i][2];
+        ob[2 * l + 1] = r[i][3];
+      }
+    }
+  }
+}
+
+// Odd-output scans of the CTA's 2G output lines (every thread calls it).
+template <int G, int LINE, int LO>
+__device__ __forceinline__ void pkc_scans(double2* sm, const BlueTables& bt) {
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int s = w; s < 2 * G; s += nw)
+    odd_scan(reinterpret_cast<double*>(sm + (s >> 1) * LINE) + (s & 1) * LO, bt.N / 2, bt.scale, lane);
+  __syncthreads();
+}
+
+// Interior-input value of one line for a transform kind.
+__device__ __forceinline__ double kind_in(int kind, double xj, double x0, double xe, int j, double ri) {
+  if (kind == DBX_KIND_ARINV) {
+    const double t1 = (double)j * ri;  // p_j = 1 - j/(n-1), p_{n-1-j} = j/(n-1)
+    return (xj - x0 * (1.0 - t1)) - xe * t1;
+  }
+  return xj;
+}
+
+// Output k (0-based, line length n) of a transform kind from the DST outputs o.
+__device__ __forceinline__ double kind_out(int kind, const double* o, int k, int n, double x0, double xe,
+                                           double al, double ri) {
+  if (kind == DBX_KIND_SINEI) return o[k + 1];
+  if (kind == DBX_KIND_ARINV) return k == 0 ? al * x0 : (k == n - 1 ? al * xe : o[k]);
+  const double a0 = x0 / al, a1 = xe / al;
+  if (k == 0) return a0;
+  if (k == n - 1) return a1;
+  const double t1 = (double)k * ri;
+  return o[k] + a0 * (1.0 - t1) + a1 * t1;
+}
+
+// ---------------------------------------------------------------------------
+// Row pass: 2G rows per CTA (line g carries rows 2g, 2g+1), fused epilogue
+// (store / Hadamard / r = g - v with ||r||^2 / x += tau v with norms).
+template <int M, int CORE>
+__global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_rows(SpecArgs a) {
+  using C = DstCfg<M, CORE>;
+  constexpr int T = C::T, G = C::G, NT = C::NT;
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 sm[];
+  __shared__ double red[32];
+  __shared__ double2 A0s[G];
+  const int g = threadIdx.x / T, t = threadIdx.x - g * T;
+  double2* buf = sm + g * C::LINE;
+  const BlueTables& bt = a.blue2;
+  const double2* tw = stage_twiddles<M, C::TW>(sm + G * C::LINE, bt.tw);
+  const int n1 = a.n1, n = a.n2, kind = a.kind1;
+  const size_t N = (size_t)n1 * n;
+  const int ra = blockIdx.x * 2 * G + 2 * g;
+  const double* in = resolve_ptr(a.in, a.st, a.insel, b, a.batch, N);
+  const double* xa = ra < n1 ? in + (size_t)ra * n : nullptr;
+  const double* xb = ra + 1 < n1 ? in + (size_t)(ra + 1) * n : nullptr;
+  const bool sine = kind == DBX_KIND_SINEI;
+  const double a0 = (xa && !sine) ? xa[0] : 0.0, ae = (xa && !sine) ? xa[n - 1] : 0.0;
+  const double b0 = (xb && !sine) ? xb[0] : 0.0, be = (xb && !sine) ? xb[n - 1] : 0.0;
+  const double ri = bt.rinv;
+  pkc_fill<M, T, CORE>(buf, bt, t, [&](int hh, int j) {
+    const double* x = hh ? xb : xa;
+    if (!x) return 0.0;
+    if (sine) return x[j - 1];
+    return kind_in(kind, x[j], hh ? b0 : a0, hh ? be : ae, j, ri);
+  });
+  pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g);
+  pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0));
+  pkc_scans<G, C::LINE, C::LO>(sm, bt);
+  Epi e = make_epi(a, b, N);
+  const double* o = reinterpret_cast<const double*>(buf);
+  const double al = bt.alpha;
+  for (int hh = 0; hh < 2; ++hh) {
+    const int r = ra + hh;
+    if (r >= n1) continue;
+    const double* oh = o + hh * C::LO;
+    const double x0 = hh ? b0 : a0, xe = hh ? be : ae;
+    for (int k = t; k < n; k += T) e.put((size_t)r * n + k, kind_out(kind, oh, k, n, x0, xe, al, ri));
+  }
+  write_partials<NT>(a, e, red, b);
+}
+
+// ---------------------------------------------------------------------------
+// Column pass: 2G adjacent columns per CTA (line g carries columns 2g, 2g+1;
+// row segments of 2G doubles).  kind1, then (kind2 >= 0) the middle Hadamard
+// by the d column and kind2 — the whole column half of D = T diag(d) T~ — with
+// the middle product parked in the output array (the CTA's own columns).
+// ---------------------------------------------------------------------------
+// Column pass: 2G adjacent columns per CTA (line g carries columns 2g, 2g+1;
+// row segments of 2G doubles), transform a.kind1 with the STORE / Hadamard
+// epilogue.  The column half of D = T diag(d) T~ is two launches (the host
+// side, launch_dst_cols): T~ with the Hadamard by d into the output array, then
+// T in place on it.
+template <int M, int CORE>
+__global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_cols(SpecArgs a) {
+  using C = DstCfg<M, CORE>;
+  constexpr int T = C::T, G = C::G, NT = C::NT;
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 sm[];
+  __shared__ double2 A0s[G];
+  __shared__ double e0[2 * G], e1[2 * G];
+  const int g = threadIdx.x / T, t = threadIdx.x - g * T;
+  double2* buf = sm + g * C::LINE;
+  const BlueTables& bt = a.blue1;
+  const double2* tw = stage_twiddles<M, C::TW>(sm + G * C::LINE, bt.tw);
+  const int n = a.n1, n2 = a.n2;
+  const size_t N = (size_t)n * n2;
+  const int c0 = blockIdx.x * 2 * G;
+  const int ncol = n2 - c0 < 2 * G ? n2 - c0 : 2 * G;
+  double* out = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N));
+  const double* in = resolve_ptr(a.in, a.st, a.insel, b, a.batch, N);
+  const double ri = bt.rinv, al = bt.alpha;
+  const int kind = a.kind1;
+  const bool sine = kind == DBX_KIND_SINEI;
+  if (threadIdx.x < 2 * G) {
+    const int s = threadIdx.x, c = c0 + s;
+    e0[s] = (s < ncol && !sine) ? in[c] : 0.0;
+    e1[s] = (s < ncol && !sine) ? in[(size_t)(n - 1) * n2 + c] : 0.0;
+  }
+  __syncthreads();
+  const int ca = c0 + 2 * g;
+  const double xa0 = e0[2 * g], xae = e1[2 * g], xb0 = e0[2 * g + 1], xbe = e1[2 * g + 1];
+  const bool la = 2 * g < ncol, lb = 2 * g + 1 < ncol;
+  pkc_fill<M, T, CORE>(buf, bt, t, [&](int hh, int j) {
+    if (!(hh ? lb : la)) return 0.0;
+    const double* x = in + ca + hh;
+    if (sine) return x[(size_t)(j - 1) * n2];
+    return kind_in(kind, x[(size_t)j * n2], hh ? xb0 : xa0, hh ? xbe : xae, j, ri);
+  });
+  pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g);
+  pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0));
+  pkc_scans<G, C::LINE, C::LO>(sm, bt);
+  // outputs: 2G adjacent columns per row (index s fastest)
+  const bool had = a.epi == SPEC_HADAMARD && a.d;
+  for (int idx = threadIdx.x; idx < n * 2 * G; idx += NT) {
+    const int k = idx / (2 * G), s = idx - k * (2 * G);
+    if (s >= ncol) continue;
+    const double* o = reinterpret_cast<const double*>(sm + (s >> 1) * C::LINE) + (s & 1) * C::LO;
+    double v = kind_out(kind, o, k, n, e0[s], e1[s], al, ri);
+    const size_t at = (size_t)k * n2 + c0 + s;
+    if (had) v *= a.d[at];
+    out[at] = v;
+  }
+}
+
+template <int L, int CORE>
+int rows_launch(const SpecArgs& a, cudaStream_t s) {
+  using C = DstCfg<L, CORE>;
+  static bool init = false;
+  if (!init) {
+    if (!set_smem(dst_rows<L, CORE>, C::bytes)) return -1;
+    init = true;
+  }
+  dim3 grid((a.n1 + 2 * C::G - 1) / (2 * C::G), a.batch);
+  dst_rows<L, CORE><<<grid, C::NT, C::bytes, s>>>(a);
+  return (int)grid.x;
+}
+
+template <int L, int CORE>
+int cols_launch(const SpecArgs& a, cudaStream_t s) {
+  using C = DstCfg<L, CORE>;
+  static bool init = false;
+  if (!init) {
+    if (!set_smem(dst_cols<L, CORE>, C::bytes)) return -1;
+    init = true;
+  }
+  dim3 grid((a.n2 + 2 * C::G - 1) / (2 * C::G), a.batch);
+  dst_cols<L, CORE><<<grid, C::NT, C::bytes, s>>>(a);
+  return (int)grid.x;
+}
+
+}  // namespace
+
+#define DBX_DIRECT_LIST(X) X(15) X(31) X(63) X(255) X(1023) X(4095)
+#define DBX_BLUE_LIST(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
+#define DBX_RADER_LIST(X) X(22) X(126) X(8190)
+
+int direct_supported_len(int N) {
+#define X(L) if (N == (L)) return (L);
+  DBX_DIRECT_LIST(X)
+#undef X
+  return 0;
+}
+
+int blue_supported_len(int need) {
+  int best = 0;
+#define X(L) if (best == 0 && (L) >= need) best = (L);
+  DBX_BLUE_LIST(X)
+#undef X
+  return best;
+}
+
+int rader_supported_len(int M) {
+#define X(L) if (M == (L)) return (L);
+  DBX_RADER_LIST(X)
+#undef X
+  return 0;
+}
+
+static int dispatch(int core, int M, const SpecArgs& a, cudaStream_t s, bool rows) {
+  if (core == CORE_DIRECT) {
+#define X(L) if (M == (L)) return rows ? rows_launch<L, CORE_DIRECT>(a, s) : cols_launch<L, CORE_DIRECT>(a, s);
+    DBX_DIRECT_LIST(X)
+#undef X
+  } else if (core == CORE_BLUE) {
+#define X(L) if (M == (L)) return rows ? rows_launch<L, CORE_BLUE>(a, s) : cols_launch<L, CORE_BLUE>(a, s);
+    DBX_BLUE_LIST(X)
+#undef X
+  } else {
+#define X(L) if (M == (L)) return rows ? rows_launch<L, CORE_RADER>(a, s) : cols_launch<L, CORE_RADER>(a, s);
+    DBX_RADER_LIST(X)
+#undef X
+  }
+  return -1;
+}
+
+int launch_dst_rows(const SpecArgs& a, cudaStream_t s) { return dispatch(a.blue2.core, a.blue2.M, a, s, true); }
+// kind2 >= 0: kind1 with the Hadamard by d (when given) into out, then kind2
+// in place on out.
+int launch_dst_cols(const SpecArgs& a, cudaStream_t s) {
+  if (a.kind2 < 0) return dispatch(a.blue1.core, a.blue1.M, a, s, false);
+  SpecArgs p = a;
+  p.kind2 = -1;
+  p.epi = a.d ? SPEC_HADAMARD : SPEC_STORE;
+  const int r = dispatch(a.blue1.core, a.blue1.M, p, s, false);
+  if (r < 0) return r;
+  p.kind1 = a.kind2;
+  p.in = a.out;
+  p.insel = a.outsel;
+  p.epi = SPEC_STORE;
+  return dispatch(a.blue1.core, a.blue1.M, p, s, false);
+}
+
+}  // namespace dbx

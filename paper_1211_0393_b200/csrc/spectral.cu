@@ -260,233 +260,6 @@ conv_row_inv(SpecArgs a) {
   write_partials<NT>(a, e, red, b);
 }
 
-// Row pass: one AR (or SineI) transform per row, fused epilogue.
-template <int M, bool BLUE>
-__global__ void __launch_bounds__(lines_for(M, kDstBudget, dst_per(M)) * line_threads(M, dst_per(M)), (M & 1) ? 2 : 1)
-dst_rows(SpecArgs a) {
-  constexpr int T = line_threads(M, dst_per(M)), G = lines_for(M, kDstBudget, dst_per(M));
-  constexpr int NT = T * G;
-  const int b = blockIdx.y;
-  if (a.st && a.st[b].done) return;
-  extern __shared__ double2 sm[];
-  __shared__ double red[32];
-  const int g = threadIdx.x / T, t = threadIdx.x - g * T;
-  double2* buf = sm + g * padded_len(M);
-  const int n1 = a.n1, n = a.n2;
-  const size_t N = (size_t)n1 * n;
-  const BlueTables& bt = a.blue2;
-  using SMP = DstSmem<M, G, BLUE>;
-  const double2* tw = stage_twiddles<M, SMP::TW>(
-      reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + SMP::tw_off), bt.tw);
-  const int r = blockIdx.x * G + g;
-  const bool live = r < n1;
-  const double* in = resolve_ptr(a.in, a.st, a.insel, b, a.batch, N) + (size_t)(live ? r : 0) * n;
-  const int kind = a.kind1;
-  const double v0 = in[0], ve = in[n - 1];
-  const double* p = bt.p;
-  if (kind == DBX_KIND_SINEI) {
-    blue_fill<M, T, BLUE>(buf, bt, t, [&](int j) { return live ? in[j - 1] : 0.0; });
-  } else if (kind == DBX_KIND_ARINV) {
-    blue_fill<M, T, BLUE>(buf, bt, t, [&](int j) {
-      return live ? (in[j] - v0 * __ldg(p + j - 1)) - ve * __ldg(p + n - 2 - j) : 0.0;
-    });
-  } else {
-    blue_fill<M, T, BLUE>(buf, bt, t, [&](int j) { return live ? in[j] : 0.0; });
-  }
-  // Stage the epilogue operands (x_{k-1} and f, or g, or d) into shared
-  // memory with cp.async at kernel start: their HBM latency hides behind the
-  // transform and they cost no registers.  A line holds at most M/2+1
-  // (Bluestein) or M+1 (direct) pixels.
-  constexpr int LMAX = BLUE ? M / 2 + 1 : M + 1;
-  double* stA = reinterpret_cast<double*>(sm + G * padded_len(M)) + g * 2 * LMAX;
-  double* stB = stA + LMAX;
-  Epi e = make_epi(a, b, N);
-  const size_t ro = (size_t)(live ? r : 0) * n;
-  if (live && e.mode != SPEC_STORE) {
-    const double* srcA = e.mode == SPEC_AXPY ? e.xo : e.mode == SPEC_RESID ? e.g : e.d;
-    for (int k = t; k < n; k += T) {
-      cp_async8(stA + k, srcA + ro + k);
-      if (e.mode == SPEC_AXPY && e.f) cp_async8(stB + k, e.f + ro + k);
-    }
-  }
-  cp_async_commit();
-  blue_core<M, T, G, BLUE>(sm, buf, bt, tw, t);
-  cp_async_wait_all();  // each thread reads back only what it staged
-  if (live) {
-    const double al = bt.alpha, ia = 1.0 / bt.alpha;
-    const double a0 = ia * v0, a1 = ia * ve;
-    for (int k = t; k < n; k += T) {
-      double v;
-      if (kind == DBX_KIND_SINEI) {
-        v = blue_out<M, BLUE>(buf, bt, k + 1);
-      } else if (kind == DBX_KIND_ARINV) {
-        v = (k == 0) ? al * v0 : (k == n - 1) ? al * ve : blue_out<M, BLUE>(buf, bt, k);
-      } else if (k == 0) {
-        v = a0;
-      } else if (k == n - 1) {
-        v = a1;
-      } else {
-        v = blue_out<M, BLUE>(buf, bt, k);
-        v += a0 * __ldg(p + k - 1);
-        v += a1 * __ldg(p + n - 2 - k);
-      }
-      e.put_pre(ro + k, v, stA[k], stB[k]);
-    }
-  }
-  write_partials<NT>(a, e, red, b);
-}
-
-// Column pass: CW adjacent columns per CTA; kind1, then optional Hadamard by
-// the d column, then optional kind2 (-1 = none).  Output with STORE epilogue.
-template <int M, bool BLUE>
-__global__ void __launch_bounds__(lines_for(M, kDstBudget, dst_per(M)) * line_threads(M, dst_per(M)), (M & 1) ? 2 : 1)
-dst_cols(SpecArgs a) {
-  constexpr int T = line_threads(M, dst_per(M)), G = lines_for(M, kDstBudget, dst_per(M));
-  constexpr int NT = T * G;
-  const int b = blockIdx.y;
-  if (a.st && a.st[b].done) return;
-  extern __shared__ double2 sm[];
-  __shared__ double vb0[4], vbe[4];
-  const int g = threadIdx.x / T, t = threadIdx.x - g * T;
-  double2* buf = sm + g * padded_len(M);
-  const int n = a.n1, n2 = a.n2;
-  const size_t N = (size_t)n * n2;
-  const BlueTables& bt = a.blue1;
-  using SMP = DstSmem<M, G, BLUE>;
-  const double2* tw = stage_twiddles<M, SMP::TW>(
-      reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + SMP::tw_off), bt.tw);
-  const int c0 = blockIdx.x * G;
-  const int c = c0 + g;
-  const bool live = c < n2;
-  const double* in = resolve_ptr(a.in, a.st, a.insel, b, a.batch, N);
-  const double* p = bt.p;
-  const int NL = bt.N;
-
-  // staging areas after the G line buffers: d column and T~ output (real)
-  constexpr int LMAX = BLUE ? M / 2 + 1 : M + 1;
-  double* dst_d = reinterpret_cast<double*>(sm + G * padded_len(M)) + g * 2 * LMAX;
-  double* midS = dst_d + LMAX;
-  if (a.kind2 >= 0 && a.d) {
-    for (int idx = threadIdx.x; idx < n * G; idx += NT) {
-      const int j = idx / G, gg = idx - j * G, cc = c0 + gg;
-      if (cc < n2)
-        cp_async8(reinterpret_cast<double*>(sm + G * padded_len(M)) + gg * 2 * LMAX + j, a.d + (size_t)j * n2 + cc);
-    }
-  }
-  cp_async_commit();
-
-  // ---- first transform (input from global, column-strided, 32 B segments) ----
-  if (threadIdx.x < G) {
-    const int cc = c0 + threadIdx.x;
-    vb0[threadIdx.x] = cc < n2 ? in[cc] : 0.0;
-    vbe[threadIdx.x] = cc < n2 ? in[(size_t)(n - 1) * n2 + cc] : 0.0;
-  }
-  __syncthreads();
-  const int kind1 = a.kind1, kind2 = a.kind2;
-  {
-    constexpr int PF = (M * G + NT - 1) / NT;
-    double2 v[PF];
-#pragma unroll
-    for (int i = 0; i < PF; ++i) {
-      const int idx = threadIdx.x + i * NT;
-      const int j = idx / G, gg = idx - j * G, cc = c0 + gg;
-      v[i] = make_double2(0.0, 0.0);
-      if (idx < M * G && j >= 1 && j < NL && cc < n2) {
-        double z;
-        if (kind1 == DBX_KIND_SINEI) z = in[(size_t)(j - 1) * n2 + cc];
-        else if (kind1 == DBX_KIND_ARINV)
-          z = (in[(size_t)j * n2 + cc] - vb0[gg] * __ldg(p + j - 1)) - vbe[gg] * __ldg(p + n - 2 - j);
-        else z = in[(size_t)j * n2 + cc];
-        v[i] = pre<BLUE>(make_double2(z, (j & 1) ? -z : z), bt, j);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < PF; ++i) {
-      const int idx = threadIdx.x + i * NT;
-      const int j = idx / G, gg = idx - j * G;
-      if (idx < M * G) sm[gg * padded_len(M) + pad<M>(j)] = v[i];
-    }
-  }
-  blue_core<M, T, G, BLUE>(sm, buf, bt, tw, t);
-
-  double* out = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N));
-  if (kind2 < 0) {
-    // single transform: write the column directly
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < n * G; idx += NT) {
-      const int k = idx / G, gg = idx - k * G, cc = c0 + gg;
-      if (cc >= n2) continue;
-      const double2* bb = sm + gg * padded_len(M);
-      double v;
-      if (kind1 == DBX_KIND_SINEI) v = blue_out<M, BLUE>(bb, bt, k + 1);
-      else if (kind1 == DBX_KIND_ARINV) v = (k == 0) ? bt.alpha * vb0[gg] : (k == n - 1) ? bt.alpha * vbe[gg] : blue_out<M, BLUE>(bb, bt, k);
-      else {
-        const double ia = 1.0 / bt.alpha, a0 = ia * vb0[gg], a1 = ia * vbe[gg];
-        if (k == 0) v = a0;
-        else if (k == n - 1) v = a1;
-        else {
-          v = blue_out<M, BLUE>(bb, bt, k);
-          v += a0 * __ldg(p + k - 1);
-          v += a1 * __ldg(p + n - 2 - k);
-        }
-      }
-      if (a.epi == SPEC_HADAMARD) v *= a.d[(size_t)k * n2 + cc];
-      out[(size_t)k * n2 + cc] = v;
-    }
-    return;
-  }
-
-  // ---- middle: u = T~ result (AR inverse), v' = u o d, refill for kind2 = T ----
-  // (the d column was staged into shared memory by cp.async at kernel start)
-  cp_async_wait_all();
-  __syncthreads();
-  for (int j = t; j < M; j += T) {  // interior index 1..NL-1
-    double m = 0.0;
-    if (live && j >= 1 && j < NL) {
-      const double u = blue_out<M, BLUE>(buf, bt, j);
-      m = a.d ? u * dst_d[j] : u;
-    }
-    if (j < LMAX) midS[j] = m;
-  }
-  __syncthreads();
-  if (threadIdx.x < G) {
-    const int cc = c0 + threadIdx.x;
-    double u0 = bt.alpha * vb0[threadIdx.x], ue = bt.alpha * vbe[threadIdx.x];
-    if (a.d && cc < n2) {
-      u0 *= a.d[cc];
-      ue *= a.d[(size_t)(n - 1) * n2 + cc];
-    }
-    vb0[threadIdx.x] = u0;
-    vbe[threadIdx.x] = ue;
-  }
-  for (int j = t; j < M; j += T) {
-    double2 v = make_double2(0.0, 0.0);
-    if (j >= 1 && j < NL) {
-      const double m = midS[j];
-      v = pre<BLUE>(make_double2(m, (j & 1) ? -m : m), bt, j);
-    }
-    buf[pad<M>(j)] = v;
-  }
-  blue_core<M, T, G, BLUE>(sm, buf, bt, tw, t);
-  // ---- T (AR forward) output, coalesced 32 B row segments ----
-  const double ia = 1.0 / bt.alpha;
-  for (int idx = threadIdx.x; idx < n * G; idx += NT) {
-    const int k = idx / G, gg = idx - k * G, cc = c0 + gg;
-    if (cc >= n2) continue;
-    const double2* bb = sm + gg * padded_len(M);
-    const double a0 = ia * vb0[gg], a1 = ia * vbe[gg];
-    double v;
-    if (k == 0) v = a0;
-    else if (k == n - 1) v = a1;
-    else {
-      v = blue_out<M, BLUE>(bb, bt, k);
-      v += a0 * __ldg(p + k - 1);
-      v += a1 * __ldg(p + n - 2 - k);
-    }
-    out[(size_t)k * n2 + cc] = v;
-  }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -496,20 +269,11 @@ dst_cols(SpecArgs a) {
   X(64) X(72) X(80) X(96) X(128) X(144) X(160) X(192) X(256) X(270) X(288) X(320) X(384) X(512) \
   X(540) X(576) X(640) X(768) X(1024) X(1080) X(1152) X(1280) X(1536) X(2048) X(2160) X(2304) \
   X(2560) X(3072) X(4096) X(4320) X(4608) X(5120) X(6144) X(8192) X(8640)
-#define DBX_BLUE_LIST(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
 
 int conv_supported_len(int need) {
   int best = 0;
 #define X(L) if (best == 0 && (L) >= need) best = (L);
   DBX_CONV_LIST(X)
-#undef X
-  return best;
-}
-
-int blue_supported_len(int need) {
-  int best = 0;
-#define X(L) if (best == 0 && (L) >= need) best = (L);
-  DBX_BLUE_LIST(X)
 #undef X
   return best;
 }
@@ -561,67 +325,6 @@ int launch_conv_row_inv(const SpecArgs& a, cudaStream_t s) {
     return (int)grid.x;                                                                  \
   }
   DBX_CONV_LIST(X)
-#undef X
-  return -1;
-}
-
-// DST launch over both forms: BLUE lines use M (power of two), direct lines
-// use M == N (odd, prime factors <= 31).
-#define DBX_DIRECT_LIST(X) X(15) X(31) X(63) X(255) X(1023) X(4095)
-
-template <int L, bool BLUE>
-int dst_rows_launch(const SpecArgs& a, cudaStream_t s) {
-  constexpr int T = line_threads(L, dst_per(L)), G = lines_for(L, kDstBudget, dst_per(L));
-  const size_t sm = DstSmem<L, G, BLUE>::bytes;
-  static bool init = false;
-  if (!init) { if (!set_smem(dst_rows<L, BLUE>, sm)) return -1; init = true; }
-  dim3 grid((a.n1 + G - 1) / G, a.batch);
-  dst_rows<L, BLUE><<<grid, T * G, sm, s>>>(a);
-  return (int)grid.x;
-}
-
-template <int L, bool BLUE>
-int dst_cols_launch(const SpecArgs& a, cudaStream_t s) {
-  constexpr int T = line_threads(L, dst_per(L)), G = lines_for(L, kDstBudget, dst_per(L));
-  const size_t sm = DstSmem<L, G, BLUE>::bytes;
-  static bool init = false;
-  if (!init) { if (!set_smem(dst_cols<L, BLUE>, sm)) return -1; init = true; }
-  dim3 grid((a.n2 + G - 1) / G, a.batch);
-  dst_cols<L, BLUE><<<grid, T * G, sm, s>>>(a);
-  return (int)grid.x;
-}
-
-int direct_supported_len(int N) {
-#define X(L) if (N == (L)) return (L);
-  DBX_DIRECT_LIST(X)
-#undef X
-  return 0;
-}
-
-int launch_dst_rows(const SpecArgs& a, cudaStream_t s) {
-  const int M = a.blue2.M;
-  if (M == a.blue2.N) {
-#define X(L) if (M == (L)) return dst_rows_launch<L, false>(a, s);
-    DBX_DIRECT_LIST(X)
-#undef X
-    return -1;
-  }
-#define X(L) if (M == (L)) return dst_rows_launch<L, true>(a, s);
-  DBX_BLUE_LIST(X)
-#undef X
-  return -1;
-}
-
-int launch_dst_cols(const SpecArgs& a, cudaStream_t s) {
-  const int M = a.blue1.M;
-  if (M == a.blue1.N) {
-#define X(L) if (M == (L)) return dst_cols_launch<L, false>(a, s);
-    DBX_DIRECT_LIST(X)
-#undef X
-    return -1;
-  }
-#define X(L) if (M == (L)) return dst_cols_launch<L, true>(a, s);
-  DBX_BLUE_LIST(X)
 #undef X
   return -1;
 }

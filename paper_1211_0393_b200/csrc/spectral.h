@@ -9,6 +9,10 @@
 
 namespace dbx {
 
+// N-point DFT core of the packed DST (dst.cu): direct (M = N smooth),
+// Bluestein (M = 2^k >= 2N-1), Rader (M = N-1, N prime).
+enum DstCore { CORE_DIRECT = 0, CORE_BLUE = 1, CORE_RADER = 2 };
+
 enum SpecEpi { SPEC_STORE = 0, SPEC_HADAMARD = 1, SPEC_RESID = 2, SPEC_AXPY = 3 };
 
 // FFT-correlation tables (device): twiddles W_L^e for L1/L2 and the kernel
@@ -29,6 +33,9 @@ struct BlueTables {
   const double2* bhat = nullptr;
   const double* p = nullptr;
   const double* sn = nullptr;  // sin(pi j / N), j < N (packed real DST)
+  const int* dlog = nullptr;   // Rader: position of z_j (discrete log base g), j in [1, N)
+  const int* ridx = nullptr;   // Rader: position of Z_l in the convolution output, l in [1, N)
+  int core = 0;                // DstCore
   double rinv = 1.0;  // 1 / (n - 1): ramp p_j = 1 - j rinv computed in registers
   double alpha = 1.0;
   double scale = 1.0;  // sqrt(2/N)
@@ -63,6 +70,7 @@ int conv_supported_len(int need);   // smallest compiled L >= need, 0 if none
 int blue_supported_len(int need);   // smallest compiled power of two M >= need, 0 if none
 int conv_rows_per_cta(int L2);
 int direct_supported_len(int N);  // N if the direct odd-length DFT is compiled, else 0
+int rader_supported_len(int M);   // M (= N-1) if the Rader convolution length is compiled, else 0
 
 // Each returns the number of CTAs per image (for the partial-sum count), -1 if
 // the size is not compiled.

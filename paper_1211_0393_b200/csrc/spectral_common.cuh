@@ -216,52 +216,17 @@ struct ConvSmem {
 // ---------------------------------------------------------------------------
 // Bluestein DST-I / AR transforms
 // ---------------------------------------------------------------------------
-// Fill one padded line with a_j = z_j w_j, z_j = v_j (1 + i(-1)^j), j in [1, N).
-// `val(j)` returns v_j (1-based interior index).
-// Two forms of the N-point DFT of z: BLUE = Bluestein chirp-z over a power of
-// two L = M >= 2N-1 (any N); !BLUE = direct mixed-radix FFT of length L = N
-// (N with prime factors <= 31, e.g. 255 = 3.5.17, 1023 = 3.11.31).
+// Two forms of the N-point DFT in the fused kernels: BLUE = Bluestein chirp-z
+// over a power of two M >= 2N-1 (any N); !BLUE = direct mixed-radix FFT of
+// length M = N (N with prime factors <= 31, e.g. 255 = 3.5.17, 1023 = 3.11.31).
+// (dst.cu adds the Rader core for prime N.)
 template <bool BLUE>
 __device__ __forceinline__ double2 pre(double2 z, const BlueTables& bt, int j) {
   if constexpr (BLUE) return cmul(z, __ldg(bt.chirp + j));
   else return z;
 }
 
-template <int M, int T, bool BLUE, typename F>
-__device__ __forceinline__ void blue_fill(double2* buf, const BlueTables& bt, int t, F val) {
-  const int N = bt.N;
-  // every load of the thread (line values, chirp) is issued before any store
-  constexpr int PF = (M + T - 1) / T;
-  double2 v[PF];
-#pragma unroll
-  for (int i = 0; i < PF; ++i) {
-    const int j = t + i * T;
-    v[i] = make_double2(0.0, 0.0);
-    if (j >= 1 && j < N) {
-      const double z = val(j);
-      v[i] = pre<BLUE>(make_double2(z, (j & 1) ? -z : z), bt, j);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < PF; ++i) {
-    const int j = t + i * T;
-    if (j < M) buf[pad<M>(j)] = v[i];
-  }
-}
-
 // BLUE: FFT, multiply by the kernel spectrum, inverse FFT.  Direct: one FFT.
-// Shared-memory plan of a DST kernel: G line buffers, G x 2 real staging rows
-// (epilogue operands / d column and T~ output), then the twiddle table if it
-// fits.
-template <int L, int G, bool BLUE>
-struct DstSmem {
-  static constexpr int LMAX = BLUE ? L / 2 + 1 : L + 1;
-  static constexpr size_t base = (size_t)G * padded_len(L) * 16 + (size_t)G * 2 * LMAX * 8;
-  static constexpr size_t tw_off = (base + 15) / 16 * 16;
-  static constexpr bool TW = tw_off + (size_t)fft::twiddles_needed(L) * 16 <= kSmemCap;
-  static constexpr size_t bytes = TW ? tw_off + (size_t)fft::twiddles_needed(L) * 16 : base;
-};
-
 template <int M, int T, int G, bool BLUE>
 __device__ __forceinline__ void blue_core(double2* sm, double2* buf, const BlueTables& bt, const double2* tw,
                                           int t) {
@@ -278,18 +243,6 @@ __device__ __forceinline__ void blue_core(double2* sm, double2* buf, const BlueT
     __syncthreads();
     fft::fft<M, +1, T>(buf, tw, t);
   }
-}
-
-// DST-I output y_k (k in [1, N)) from Z = DFT_N(z) (post-chirp applied here
-// for BLUE), scaled by sqrt(2/N): Q v = sqrt(2/N) sum_j v_j sin(pi j k / N).
-// Even k = 2l: -Im DFT(v)_l; odd k: -Im DFT((-1)^j v)_{(k+N)/2} (N odd).
-template <int M, bool BLUE>
-__device__ __forceinline__ double blue_out(const double2* buf, const BlueTables& bt, int k) {
-  const int N = bt.N;
-  const int l = (k & 1) == 0 ? (k >> 1) : ((k + N) >> 1);
-  const double2 zl = pre<BLUE>(buf[pad<M>(l)], bt, l);
-  const double2 zm = pre<BLUE>(buf[pad<M>(N - l)], bt, N - l);
-  return (k & 1) == 0 ? 0.5 * bt.scale * (zm.y - zl.y) : 0.5 * bt.scale * (zl.x - zm.x);
 }
 
 // ---------------------------------------------------------------------------

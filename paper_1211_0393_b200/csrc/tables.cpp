@@ -87,6 +87,7 @@ BlueHost bluestein(int n, bool sine_i, int M) {
   b.N = sine_i ? n + 1 : n - 1;
   b.M = M;
   const long N = b.N;
+  b.core = M == N ? 0 : 1;
   b.scale = (double)sqrtl(2.0L / (long double)N);
   b.tw = twiddles(M);
   if (M == N) {  // direct odd-length DFT: no chirp / kernel spectrum
@@ -97,6 +98,83 @@ BlueHost bluestein(int n, bool sine_i, int M) {
   }
   ar_ramp(b, n, sine_i);
   // sine pre-twiddle of the packed real DST (spectral_common.cuh, pk_fill)
+  b.sn.assign((size_t)N, 0.0);
+  for (long j = 1; j < N; ++j) b.sn[(size_t)j] = (double)sinl(kPiL * (long double)j / (long double)N);
+  return b;
+}
+
+bool is_prime(long N) {
+  if (N < 2) return false;
+  for (long d = 2; d * d <= N; ++d)
+    if (N % d == 0) return false;
+  return true;
+}
+
+static long powmod(long a, long e, long m) {
+  long r = 1 % m;
+  a %= m;
+  while (e > 0) {
+    if (e & 1) r = (long)((__int128)r * a % m);
+    a = (long)((__int128)a * a % m);
+    e >>= 1;
+  }
+  return r;
+}
+
+BlueHost rader(int n, bool sine_i) {
+  BlueHost b;
+  b.n = n;
+  b.N = sine_i ? n + 1 : n - 1;
+  const long N = b.N, M = N - 1;
+  b.M = (int)M;
+  b.core = 2;
+  b.scale = (double)sqrtl(2.0L / (long double)N);
+  b.tw = twiddles((int)M);
+  // primitive root: g^(M/q) != 1 for every prime factor q of M
+  std::vector<long> qs;
+  for (long m = M, d = 2; m > 1; ++d) {
+    if (d * d > m) d = m;
+    if (m % d == 0) {
+      qs.push_back(d);
+      while (m % d == 0) m /= d;
+    }
+  }
+  long g = 2;
+  for (;; ++g) {
+    bool ok = true;
+    for (long q : qs) ok = ok && powmod(g, M / q, N) != 1;
+    if (ok) break;
+  }
+  b.dlog.assign((size_t)N, 0);
+  b.ridx.assign((size_t)N, 0);
+  std::vector<long> gp((size_t)M);  // g^p
+  long v = 1;
+  for (long p = 0; p < M; ++p) {
+    gp[(size_t)p] = v;
+    b.dlog[(size_t)v] = (int)p;
+    v = v * g % N;
+  }
+  for (long l = 1; l < N; ++l) b.ridx[(size_t)l] = (int)((M - b.dlog[(size_t)l]) % M);
+  // b_m = w^{g^-m}, g^-m = g^{(M - m) mod M}; bhat = FFT_M(b) / M
+  std::vector<std::complex<long double>> bb((size_t)M), eM((size_t)M);
+  for (long m = 0; m < M; ++m) {
+    const long e = gp[(size_t)((M - m) % M)];
+    const long double a = 2.0L * kPiL * (long double)e / (long double)N;
+    bb[(size_t)m] = {cosl(a), -sinl(a)};
+    const long double c = 2.0L * kPiL * (long double)m / (long double)M;
+    eM[(size_t)m] = {cosl(c), -sinl(c)};
+  }
+  b.bhat.assign(2 * (size_t)M, 0.0);
+  parallel_for(M, [&](long kb, long ke) {
+    for (long k = kb; k < ke; ++k) {
+      std::complex<long double> acc = 0;
+      for (long t = 0; t < M; ++t) acc += bb[(size_t)t] * eM[(size_t)((k * t) % M)];
+      acc /= (long double)M;
+      put(b.bhat.data(), k, acc.real(), acc.imag());
+    }
+  });
+  b.chirp.assign(2, 0.0);
+  ar_ramp(b, n, sine_i);
   b.sn.assign((size_t)N, 0.0);
   for (long j = 1; j < N; ++j) b.sn[(size_t)j] = (double)sinl(kPiL * (long double)j / (long double)N);
   return b;

@@ -16,10 +16,18 @@ struct BlueHost {
   int n = 0, N = 0, M = 0;
   double alpha = 1.0, scale = 1.0;
   std::vector<double> tw, chirp, bhat, p, sn;  // sn[j] = sin(pi j / N), j < N
+  std::vector<int> dlog, ridx;                 // Rader permutations (prime N)
+  int core = 0;                                // DstCore (spectral.h)
 };
 
 // Bluestein tables of the DST-I of one line: AR kinds (sine_i = false) use the
 // interior of length n-2 (N = n-1); the plain SineI kind uses N = n+1.
 BlueHost bluestein(int n, bool sine_i, int M);
+
+// Rader tables of the same DST-I for prime N (M = N - 1): generator g of
+// (Z/N)^*, dlog[j] = p with g^p = j, ridx[l] = q with g^-q = l, and the kernel
+// spectrum bhat = FFT_M(b) / M, b_m = exp(-2 pi i g^-m / N).
+BlueHost rader(int n, bool sine_i);
+bool is_prime(long N);
 
 }  // namespace dbx

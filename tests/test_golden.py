@@ -50,4 +50,7 @@ def test_gpu_ar_lines_golden(dbx, m):
     got = dbx.tensor_apply(dbx.TransformKind.AntiReflectiveInverse, X)
     # column transform T~_3 applied to e_1 (middle row): T~_3 e_1 = (0, Q_1 * 1, 0) = (0, 1, 0)
     assert rel(got[1], G[f"arinv_{n}"]) <= 1e-13
-    assert np.abs(got[0]).max() == 0.0 and np.abs(got[2]).max() == 0.0
+    # rows 0 and 2 are zero up to rounding: the packed DST shares one complex
+    # DFT between two lines, so a zero line sees ~1e-16 crosstalk of its partner
+    scale = np.abs(got[1]).max()
+    assert np.abs(got[0]).max() <= 1e-14 * scale and np.abs(got[2]).max() <= 1e-14 * scale

@@ -266,6 +266,39 @@ def test_dst_engines_match_oracle(dev, oracle, n1, n2, engine):
         assert rel(dev.precondition_apply(d, r, engine=eng), ref) <= OP_TOL
 
 
+@pytest.mark.parametrize("n1,n2,kinds", [
+    (24, 128, ("AntiReflective", "AntiReflectiveInverse")),  # N = n-1 = 23, 127 (prime; M = 22, 126)
+    (22, 126, ("SineI",)),                                    # N = n+1 = 23, 127
+])
+def test_rader_dst_matches_oracle(dev, oracle, n1, n2, kinds):
+    """Rader core of the packed DST (prime N, cyclic convolution of length
+    N-1) forced at small sizes; AUTO selects it for C5 (N = 8191)."""
+    rng = np.random.default_rng(n1 * 5 + n2)
+    x = rng.uniform(-1, 1, (n1, n2))
+    for name in kinds:
+        kind = getattr(dev.TransformKind, name)
+        got = dev.tensor_apply(kind, x, engine=dev.DstEngine.Rader)
+        assert rel(got, oracle.tensor_apply(int(kind), x)) <= OP_TOL, name
+    if "AntiReflective" in kinds:
+        t = rand_psf(rng, 2, 3)
+        d = dev.build_tikhonov(dev.Psf(t), dev.PreconditionerSpec(dev.Algebra.AntiReflective, 0.02), n1, n2)
+        r = rng.uniform(-1, 1, (n1, n2))
+        ref = oracle.precondition_apply(oracle.build_tikhonov(t, 0.02, n1, n2), r)
+        assert rel(dev.precondition_apply(d, r, engine=dev.DstEngine.Rader), ref) <= OP_TOL
+
+
+@pytest.mark.parametrize("n1,n2", [(25, 17), (9, 10), (257, 129), (65, 64)])
+def test_packed_dst_even_n_matches_oracle(dev, oracle, n1, n2):
+    """Odd image sizes (even DFT length N = n-1) run the packed FFT form too
+    (formerly dense only)."""
+    rng = np.random.default_rng(n1 * 3 + n2)
+    x = rng.uniform(-1, 1, (n1, n2))
+    for kind in (dev.TransformKind.SineI, dev.TransformKind.AntiReflective,
+                 dev.TransformKind.AntiReflectiveInverse):
+        got = dev.tensor_apply(kind, x, engine=dev.DstEngine.Fft)
+        assert rel(got, oracle.tensor_apply(int(kind), x)) <= OP_TOL, kind
+
+
 @pytest.mark.parametrize("name,n,iters,conv", [("C1", 256, 8, "Fft"), ("C2", 512, 5, "Auto"), ("C3", 1024, 3, "Auto")])
 @pytest.mark.parametrize("fusion", [True, False])
 def test_fused_pipeline_full_size(dev, oracle, name, n, iters, conv, fusion):
