@@ -87,14 +87,15 @@ __device__ __forceinline__ void pkc_core(double2* sm, double2* buf, const BlueTa
   if constexpr (CORE == CORE_DIRECT && (M & 1)) {
     fft::fft_cta<M, -1, T, G>(sm, tw, threadIdx.x);
   } else {
-    fft::fft<M, -1, T>(buf, tw, t);
+    const int bar = G > 1 ? 1 + g : 0;
+    fft::fft<M, -1, T>(buf, tw, t, bar);
     if constexpr (CORE != CORE_DIRECT) {
       if constexpr (CORE == CORE_RADER) {
         if (t == 0) A0s[g] = buf[pad<M>(0)];  // X_0 = sum of a (z_0 = 0)
       }
       for (int p = t; p < M; p += T) buf[pad<M>(p)] = cmul(buf[pad<M>(p)], __ldg(bt.bhat + p));
-      __syncthreads();
-      fft::fft<M, +1, T>(buf, tw, t);
+      fft::line_sync(bar, T);
+      fft::fft<M, +1, T>(buf, tw, t, bar);
     }
   }
 }

@@ -319,9 +319,20 @@ __device__ __forceinline__ void apply_twiddles(double2* v, double2 w1) {
   }
 }
 
+// Barrier of the threads working on one line: id 0 = the whole CTA
+// (__syncthreads), id > 0 = named barrier over the line's T threads (whole
+// warps), so the lines of a CTA run their stages independently.
+__device__ __forceinline__ void line_sync(int id, int nthreads) {
+  if (id == 0) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  }
+}
+
 // One Stockham stage on a padded in-smem line.
 template <int L, int Ns, int R, int S, int T>
-__device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ tw, int t) {
+__device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ tw, int t, int bar = 0) {
   constexpr int NB = L / R;
   constexpr int PER = (NB + T - 1) / T;
   double2 v[PER][R];
@@ -344,7 +355,7 @@ __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ 
       for (int r = 0; r < R; ++r) v[i][r] = buf[pad<L>(b + r * NB)];
     }
   }
-  __syncthreads();
+  line_sync(bar, T);
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int b = t + i * T;
@@ -361,7 +372,7 @@ __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ 
       }
     }
   }
-  __syncthreads();
+  line_sync(bar, T);
 }
 
 // Output pairs k in [K0, K1] of an odd-prime butterfly (symmetric pairs in v:
@@ -459,12 +470,12 @@ __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __rest
 }
 
 template <int L, int Ns, int S, int T>
-__device__ __forceinline__ void run_stages(double2* buf, const double2* __restrict__ tw, int t) {
+__device__ __forceinline__ void run_stages(double2* buf, const double2* __restrict__ tw, int t, int bar) {
   if constexpr (Ns < L) {
     constexpr int R = next_radix(L / Ns);
     static_assert(R != 0, "FFT length must factor into {2,3,4,5,8} and odd primes <= 31");
-    stage<L, Ns, R, S, T>(buf, tw, t);
-    run_stages<L, Ns * R, S, T>(buf, tw, t);
+    stage<L, Ns, R, S, T>(buf, tw, t, bar);
+    run_stages<L, Ns * R, S, T>(buf, tw, t, bar);
   }
 }
 
@@ -477,10 +488,11 @@ __device__ __forceinline__ void run_stages_cta(double2* sm, const double2* __res
     constexpr int R = next_radix(L / Ns);
     static_assert(R != 0, "FFT length must factor into {2,3,4,5,8} and odd primes <= 31");
     if constexpr (R >= 17 && (R & 1) && G * (L / R) <= G * T) {
+      if constexpr (Ns > 1) __syncthreads();  // threads read other lines here
       stage_odd_cta<L, Ns, R, S, G, PL, G * T>(sm, tw, tid);
     } else {
       const int g = tid / T;
-      stage<L, Ns, R, S, T>(sm + g * PL, tw, tid - g * T);
+      stage<L, Ns, R, S, T>(sm + g * PL, tw, tid - g * T, G > 1 ? 1 + g : 0);
     }
     run_stages_cta<L, Ns * R, S, T, G, PL>(sm, tw, tid);
   }
@@ -493,11 +505,12 @@ __device__ __forceinline__ void fft_cta(double2* sm, const double2* __restrict__
 }
 
 // In-place unnormalised FFT of one padded line; S = -1 forward, +1 inverse.
-// Every thread of the CTA must call it (contains __syncthreads()).
+// Every thread of the line's group must call it; bar = 0 synchronises the
+// whole CTA, bar > 0 only the line's T threads (named barrier `bar`).
 template <int L, int S, int T>
-__device__ __forceinline__ void fft(double2* buf, const double2* __restrict__ tw, int t) {
+__device__ __forceinline__ void fft(double2* buf, const double2* __restrict__ tw, int t, int bar = 0) {
   static_assert(supported(L), "unsupported FFT length");
-  run_stages<L, 1, S, T>(buf, tw, t);
+  run_stages<L, 1, S, T>(buf, tw, t, bar);
 }
 
 }  // namespace fft

@@ -97,7 +97,7 @@ __device__ __forceinline__ void conv_inv_load(double2* buf, const double2* __res
 template <int L2, int T>
 __device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, const double* rowb, int n2,
                                               int q2, const double2* tw, double2* Z, int ra, int rb, int n1,
-                                              int Lh, int t) {
+                                              int Lh, int t, int bar) {
   const int wext = n2 + 2 * q2;
   const bool has_a = ra < n1, has_b = rb < n1;
   auto ext = [&](const double* row, int j) -> double {
@@ -113,8 +113,8 @@ __device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, 
     }
     buf[pad<L2>(p)] = make_double2(va, vb);
   }
-  __syncthreads();
-  fft::fft<L2, -1, T>(buf, tw, t);
+  fft::line_sync(bar, T);
+  fft::fft<L2, -1, T>(buf, tw, t, bar);
   for (int k = t; k < Lh; k += T) {
     const double2 zk = buf[pad<L2>(k)], zm = buf[pad<L2>(k == 0 ? 0 : L2 - k)];
     if (has_a) Z[(size_t)k * n1 + ra] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
   conv_inv_load<L2, TD>(cbuf, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t);
   cp_async_wait_all();
   __syncthreads();
-  fft::fft<L2, +1, TD>(cbuf, twc, t);
+  fft::fft<L2, +1, TD>(cbuf, twc, t, 1 + g);
   for (int c = t; c < n2; c += TD) {
     const double2 v = cbuf[pad<L2>(c)];
     rowS[(2 * g) * LS + c] = v.x;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   __syncthreads();  // x rows complete; DST buffers free for the conv lines
   const int ra = r0 + 2 * g, rb = ra + 1;
   conv_fwd_rows<L2, TD>(sm + g * F::LC, stX + (2 * g) * LS, stX + (2 * g + 1) * LS, n2, a.q2, twc,
-                        a.zbuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t);
+                        a.zbuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t, 1 + g);
   if (a.part.p) {
     double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
     const double s0 = block_sum<NT>(p0, red);
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_resid(Spe
   }
   __syncthreads();
   conv_fwd_rows<L2, NT>(sm, rowS, rowS + F::RROW, n2, a.q2, twc, a.zbuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh,
-                        threadIdx.x);
+                        threadIdx.x, 0);
   if (a.part.p) {
     double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
     const double s0 = block_sum<NT>(p0, red);

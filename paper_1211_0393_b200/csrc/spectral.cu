@@ -69,7 +69,7 @@ conv_row_fwd(SpecArgs a) {
   }
   cp_async_wait_all();
   __syncthreads();
-  fft::fft<L2, -1, T>(buf, tw, t);
+  fft::fft<L2, -1, T>(buf, tw, t, G > 1 ? 1 + g : 0);
   double2* Z = a.zbuf + (size_t)b * n1 * Lh;
   // ztrans: spectra stored [k][row] so the column pass reads contiguously;
   // the pair's two rows are adjacent (one 32-byte sector per k)
@@ -179,15 +179,16 @@ conv_col(SpecArgs a) {
     cp_async_wait_group<2>();  // twiddles landed (H may still be in flight)
     __syncthreads();
   }
-  fft::fft<L1, -1, T>(buf, tw, t);
+  fft::fft<L1, -1, T>(buf, tw, t, G > 1 ? 1 + g : 0);
   cp_async_wait_all();  // each thread multiplies only the entries it staged
   if constexpr (SM::HS) {
     for (int p = t; p < L1; p += T) buf[pad<L1>(p)] = cmul(buf[pad<L1>(p)], hst[p]);
   } else {
     for (int p = t; p < L1; p += T) buf[pad<L1>(p)] = cmul(buf[pad<L1>(p)], __ldg(Hcol + p));
   }
-  __syncthreads();
-  fft::fft<L1, +1, T>(buf, tw, t);
+  fft::line_sync(G > 1 ? 1 + g : 0, T);
+  fft::fft<L1, +1, T>(buf, tw, t, G > 1 ? 1 + g : 0);
+  if (G > 1) __syncthreads();  // the stores interleave the CTA's lines
   double2* Y = a.ybuf + (size_t)b * n1 * Lh;
   for (int idx = threadIdx.x; idx < n1 * G; idx += NT) {
     const int p = idx / G, gg = idx - p * G, k = k0 + gg;
@@ -251,7 +252,7 @@ conv_row_inv(SpecArgs a) {
   }
   cp_async_wait_all();
   __syncthreads();
-  fft::fft<L2, +1, T>(buf, tw, t);
+  fft::fft<L2, +1, T>(buf, tw, t, G > 1 ? 1 + g : 0);
   for (int c = t; c < n2; c += T) {
     const double2 v = buf[pad<L2>(c)];
     if (ra < n1) e.put((size_t)ra * n2 + c, v.x);

@@ -237,12 +237,14 @@ __device__ __forceinline__ void blue_core(double2* sm, double2* buf, const BlueT
     fft::fft_cta<M, -1, T, G>(sm, tw, threadIdx.x);
     return;
   }
-  fft::fft<M, -1, T>(buf, tw, t);
+  const int bar = G > 1 ? 1 + (int)threadIdx.x / T : 0;  // per-line named barrier
+  fft::fft<M, -1, T>(buf, tw, t, bar);
   if constexpr (BLUE) {
     for (int j = t; j < M; j += T) buf[pad<M>(j)] = cmul(buf[pad<M>(j)], __ldg(bt.bhat + j));
-    __syncthreads();
-    fft::fft<M, +1, T>(buf, tw, t);
+    fft::line_sync(bar, T);
+    fft::fft<M, +1, T>(buf, tw, t, bar);
   }
+  __syncthreads();  // the split reads other lines' data only after every line finished
 }
 
 // ---------------------------------------------------------------------------
