@@ -1,7 +1,7 @@
 // fused.cu — fused row pipelines of the preconditioned iteration (FFT-form
 // blur + FFT-form AR transform).  A CTA owns four image rows (two packed
-// real-FFT conv lines of length L2 and two packed real DST lines of length M,
-// two rows per line) or, for rows_ainv_resid, one row pair; every stage stays
+// real-FFT conv lines of length L2 and, where a transform follows, two packed
+// real DST lines of length M, two rows per line); every stage stays
 // in shared memory between the passes that used to be separate launches:
 //
 //   rows_ainv_tt      : Y (A' r spectrum) -> inverse row FFT -> s = A'r rows
@@ -53,13 +53,6 @@ struct Fused {
   static constexpr size_t ax_twc = ax_twd + (AX_TWD ? TWD : 0);
   static constexpr bool AX_TWC = ax_twc + TWC <= kBudget;
   static constexpr size_t ax_bytes = ax_twc + (AX_TWC ? TWC : 0);
-  // ---- rows_ainv_resid (two rows, one conv line on all NT threads)
-  static constexpr int RROW = L2;
-  static constexpr size_t rs_rows = (size_t)LC * 16;                 // 2 x RROW doubles
-  static constexpr size_t rs_g = rs_rows + (size_t)RROW * 16;         // g: 2 x RROW doubles
-  static constexpr size_t rs_twc = rs_g + (size_t)RROW * 16;
-  static constexpr bool RS_TWC = rs_twc + TWC <= kBudget;
-  static constexpr size_t rs_bytes = rs_twc + (RS_TWC ? TWC : 0);
   static_assert((size_t)W4 * 16 >= (size_t)4 * LS * 8, "f rows are staged in the work region");
 };
 
@@ -286,50 +279,95 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
 }
 
 // ---------------------------------------------------------------------------
-// rows_ainv_resid: one row PAIR per CTA (one packed conv line on NT threads).
-template <int L2, int M, bool BLUE>
-__global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_resid(SpecArgs a) {
-  using F = Fused<L2, M, BLUE>;
-  constexpr int NT = F::NT;
+// rows_ainv_resid: FOUR rows per CTA, two packed conv lines of T threads each
+// (T sized for the conv radices, not the DST).  The residual never leaves the
+// registers: g is prefetched into registers before the inverse FFT, r = g - A x
+// is written straight into the forward line at its extended position q2 + c,
+// and the horizontal AR extension is filled from the line itself.
+template <int L2>
+struct RsCfg {
+  static constexpr int T = line_threads(L2, 8), G = 2, NT = T * G;
+  static constexpr int LC = padded_len(L2);
+  static constexpr int LS = (L2 + 1) / 2 * 2 + 4;  // g row stride (doubles), n2 <= L2
+  static constexpr size_t gs = (size_t)G * LC * 16;
+  static constexpr size_t twc = gs + (size_t)4 * LS * 8;
+  static constexpr size_t bytes = twc + (size_t)fft::twiddles_needed(L2) * 16;
+};
+
+template <int L2>
+__global__ void __launch_bounds__(RsCfg<L2>::NT, 2) rows_ainv_resid(SpecArgs a) {
+  using C = RsCfg<L2>;
+  constexpr int T = C::T, NT = C::NT, LS = C::LS;
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 sm[];
   __shared__ double red[32];
-  char* base = reinterpret_cast<char*>(sm);
-  double* rowS = reinterpret_cast<double*>(base + F::rs_rows);
-  double* stG = reinterpret_cast<double*>(base + F::rs_g);
-  const double2* twc = stage_twiddles<L2, F::RS_TWC>(reinterpret_cast<double2*>(base + F::rs_twc), a.conv.tw2);
-  const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
+  const double2* twc = stage_twiddles<L2, true>(reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + C::twc),
+                                                a.conv.tw2);
+  const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh, q2 = a.q2;  // n2 <= L2 - 2 q2
   const size_t N = (size_t)n1 * n2;
-  const int ra = 2 * blockIdx.x, rb = ra + 1;
-  const double* gimg = a.g + (size_t)b * N;
-  for (int c = threadIdx.x; c < n2; c += NT) {
-    if (ra < n1) cp_async8(stG + c, gimg + (size_t)ra * n2 + c);
-    if (rb < n1) cp_async8(stG + F::RROW + c, gimg + (size_t)rb * n2 + c);
-  }
+  const int g = threadIdx.x / T, t = threadIdx.x - g * T;
+  const int ra = 4 * blockIdx.x + 2 * g, rb = ra + 1;
+  const bool has_a = ra < n1, has_b = rb < n1;
+  double2* buf = sm + g * C::LC;
+  const int bar = 1 + g;
+  // g rows staged behind the inverse FFT (cp.async, rows r0..r0+3 contiguous)
+  double* gS = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + C::gs);
+  const int r0 = 4 * blockIdx.x, nl = n1 - r0 < 4 ? n1 - r0 : 4;
+  stage_lines(gS, LS, a.g + (size_t)b * N + (size_t)r0 * n2, nl, n2);
   cp_async_commit();
-  conv_inv_load<L2, NT>(sm, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, threadIdx.x);
-  cp_async_wait_group<1>();
+  conv_inv_load<L2, T>(buf, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t);
+  cp_async_wait_group<1>();  // twiddles
   __syncthreads();
-  fft::fft<L2, +1, NT>(sm, twc, threadIdx.x);
+  fft::fft<L2, +1, T>(buf, twc, t, bar);
   cp_async_wait_all();
+  __syncthreads();  // g rows (staged by the whole CTA) visible
+  // r = g - A x (solver.hpp:105) in place of A x, shifted to its extended
+  // position q2 + c: values pass through registers around a line barrier
+  const double* gA = gS + (2 * g) * LS;
+  const double* gB = gA + LS;
   double p0 = 0.0;
-  for (int c = threadIdx.x; c < n2; c += NT) {
-    const double2 ax = sm[pad<L2>(c)];
-    if (ra < n1) {
-      const double rv = stG[c] - ax.x;  // r = g - A x (solver.hpp:105)
-      rowS[c] = rv;
-      p0 += rv * rv;
-    }
-    if (rb < n1) {
-      const double rv = stG[F::RROW + c] - ax.y;
-      rowS[F::RROW + c] = rv;
-      p0 += rv * rv;
+  constexpr int CP = (L2 + T - 1) / T;
+  double2 rv[CP];
+#pragma unroll
+  for (int i = 0; i < CP; ++i) {
+    const int c = t + i * T;
+    rv[i] = make_double2(0.0, 0.0);
+    if (c < n2) {
+      const double2 ax = buf[pad<L2>(c)];
+      rv[i] = make_double2(has_a ? gA[c] - ax.x : 0.0, has_b ? gB[c] - ax.y : 0.0);
+      p0 += rv[i].x * rv[i].x + rv[i].y * rv[i].y;
     }
   }
-  __syncthreads();
-  conv_fwd_rows<L2, NT>(sm, rowS, rowS + F::RROW, n2, a.q2, twc, a.zbuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh,
-                        threadIdx.x, 0);
+  fft::line_sync(bar, T);
+#pragma unroll
+  for (int i = 0; i < CP; ++i) {
+    const int c = t + i * T;
+    if (c < n2) buf[pad<L2>(q2 + c)] = rv[i];
+  }
+  fft::line_sync(bar, T);
+  // horizontal AR extension of r (boundary.hpp:56-62) and the zero tail
+  for (int p = t; p < L2; p += T) {
+    if (p >= q2 && p < q2 + n2) continue;
+    double2 v = make_double2(0.0, 0.0);
+    const int j = p - q2;
+    if (j < 0) {
+      const double2 r0 = buf[pad<L2>(q2)], ri = buf[pad<L2>(q2 - j)];
+      v = make_double2(2.0 * r0.x - ri.x, 2.0 * r0.y - ri.y);
+    } else if (j < n2 + q2) {
+      const double2 r0 = buf[pad<L2>(q2 + n2 - 1)], ri = buf[pad<L2>(q2 + 2 * (n2 - 1) - j)];
+      v = make_double2(2.0 * r0.x - ri.x, 2.0 * r0.y - ri.y);
+    }
+    buf[pad<L2>(p)] = v;
+  }
+  fft::line_sync(bar, T);
+  fft::fft<L2, -1, T>(buf, twc, t, bar);
+  double2* Z = a.zbuf + (size_t)b * n1 * Lh;
+  for (int k = t; k < Lh; k += T) {
+    const double2 zk = buf[pad<L2>(k)], zm = buf[pad<L2>(k == 0 ? 0 : L2 - k)];
+    if (has_a) Z[(size_t)k * n1 + ra] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    if (has_b) Z[(size_t)k * n1 + rb] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+  }
   if (a.part.p) {
     double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
     const double s0 = block_sum<NT>(p0, red);
@@ -436,15 +474,16 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
 template <int L2, int M, bool BLUE, int WHICH, typename K>
 int fused_launch(K kernel, const SpecArgs& a, cudaStream_t s) {
   using F = Fused<L2, M, BLUE>;
-  constexpr size_t bytes = WHICH == 0 ? F::tt_bytes : WHICH == 1 ? F::ax_bytes : F::rs_bytes;
-  constexpr int rows = WHICH == 2 ? 2 : 4;  // rows per CTA
+  constexpr size_t bytes = WHICH == 0 ? F::tt_bytes : WHICH == 1 ? F::ax_bytes : RsCfg<L2>::bytes;
+  constexpr int nt = WHICH == 2 ? RsCfg<L2>::NT : F::NT;
+  constexpr int rows = 4;  // rows per CTA
   static bool init = false;
   if (!init) {
     if (!set_smem(kernel, bytes)) return -1;
     init = true;
   }
   dim3 grid((a.n1 + rows - 1) / rows, a.batch);
-  kernel<<<grid, F::NT, bytes, s>>>(a);
+  kernel<<<grid, nt, bytes, s>>>(a);
   return (int)grid.x;
 }
 
@@ -480,7 +519,7 @@ int launch_fused(int which, const SpecArgs& a, cudaStream_t s) {
   if (L2 == (L) && M == (MM) && blue == (BL)) {                                               \
     if (which == FUSED_AINV_TT) return fused_launch<L, MM, BL, 0>(rows_ainv_tt<L, MM, BL>, a, s); \
     if (which == FUSED_T_AXPY_AFWD) return fused_launch<L, MM, BL, 1>(rows_t_axpy_afwd<L, MM, BL>, a, s); \
-    if (which == FUSED_AINV_RESID) return fused_launch<L, MM, BL, 2>(rows_ainv_resid<L, MM, BL>, a, s); \
+    if (which == FUSED_AINV_RESID) return fused_launch<L, MM, BL, 2>(rows_ainv_resid<L>, a, s); \
     if (which == FUSED_DST_TCOLS) return tcols_launch<MM, BL>(a, s);                             \
   }
   DBX_FUSED_LIST(X)
