@@ -13,8 +13,12 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libdbx.so")
+# Instrumented A/B variants: DBX_BUILD_TAG=phases DBX_BUILD_DEFS=-DDBX_PHASES
+# builds build_phases/ + libdbx_phases.so (select it with DBX_LIB=...).
+TAG = os.environ.get("DBX_BUILD_TAG", "")
+DEFS = os.environ.get("DBX_BUILD_DEFS", "").split()
+OBJ = os.path.join(HERE, "build" + ("_" + TAG if TAG else ""))
+LIB = os.path.join(HERE, "libdbx" + ("_" + TAG if TAG else "") + ".so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -34,9 +38,9 @@ def _compile(src: str, verbose: bool) -> str:
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj
     if src.endswith(".cu"):
-        cmd = [NVCC] + NVFLAGS + ["-c", src, "-o", obj]
+        cmd = [NVCC] + NVFLAGS + DEFS + ["-c", src, "-o", obj]
     else:
-        cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-march=x86-64-v3", "-I", INCLUDE, "-c", src, "-o", obj]
+        cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-march=x86-64-v3", "-I", INCLUDE] + DEFS + ["-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -666,6 +666,11 @@ int dbx_plan_engines(dbx_plan* plan, int* conv, int* dst) {
   });
 }
 
+#ifdef DBX_PHASES
+// Instrumented builds only: read and reset the fused kernels' phase clock sums.
+int dbx_debug_phases(unsigned long long* out, int n) { return dbx::fused_debug_phases(out, n); }
+#endif
+
 int dbx_plan_pipeline(dbx_plan* plan, int* fused) {
   return guarded([&] {
     require(plan != nullptr, "null plan");

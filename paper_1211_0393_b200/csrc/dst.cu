@@ -53,28 +53,30 @@ __device__ __forceinline__ double2 pkc_get(const double2* buf, const BlueTables&
   }
 }
 
-// Fill one FFT line with z_j = y^a_j + i y^b_j (pk_fill), placed per core.
+// Fill one FFT line with z_j = y^a_j + i y^b_j (pk_fill), placed per core;
+// sd(h, j) = (x^h_j + x^h_{N-j}, x^h_j - x^h_{N-j}), j in [1, N/2].
 template <int M, int T, int CORE, typename F>
-__device__ __forceinline__ void pkc_fill(double2* buf, const BlueTables& bt, int t, F val) {
-  const int N = bt.N;
-  auto zj = [&](int j) {
-    const double s = __ldg(bt.sn + j);
-    const double xa = val(0, j), xar = val(0, N - j);
-    const double xb = val(1, j), xbr = val(1, N - j);
-    return make_double2(fma(s, xa + xar, 0.5 * (xa - xar)), fma(s, xb + xbr, 0.5 * (xb - xbr)));
-  };
-  if constexpr (CORE == CORE_RADER) {
-    // a_p = z_{g^p}: position dlog[j] for j = 1..N-1 (a bijection onto [0, M))
-    for (int j = 1 + t; j < N; j += T) buf[pad<M>(__ldg(bt.dlog + j))] = zj(j);
-  } else {
-    for (int j = t; j < M; j += T) {
-      double2 z = make_double2(0.0, 0.0);
-      if (j >= 1 && j < N) {
-        z = zj(j);
-        if constexpr (CORE == CORE_BLUE) z = cmul(z, __ldg(bt.chirp + j));
-      }
+__device__ __forceinline__ void pkc_fill(double2* buf, const BlueTables& bt, int t, F sd) {
+  const int N = bt.N, H = N / 2;
+  auto put = [&](int j, double2 z) {
+    if constexpr (CORE == CORE_RADER) {
+      buf[pad<M>(__ldg(bt.dlog + j))] = z;  // a_p = z_{g^p}: dlog is a bijection onto [0, M)
+    } else if constexpr (CORE == CORE_BLUE) {
+      buf[pad<M>(j)] = cmul(z, __ldg(bt.chirp + j));
+    } else {
       buf[pad<M>(j)] = z;
     }
+  };
+  if constexpr (CORE != CORE_RADER) {
+    if (t == 0) buf[pad<M>(0)] = make_double2(0.0, 0.0);
+    if constexpr (CORE == CORE_BLUE)
+      for (int p = N + t; p < M; p += T) buf[pad<M>(p)] = make_double2(0.0, 0.0);
+  }
+  for (int j = 1 + t; j <= H; j += T) {
+    const double s = __ldg(bt.sn + j);
+    const double2 A = sd(0, j), B = sd(1, j);
+    put(j, make_double2(fma(s, A.x, 0.5 * A.y), fma(s, B.x, 0.5 * B.y)));
+    if (N - j != j) put(N - j, make_double2(fma(s, A.x, -0.5 * A.y), fma(s, B.x, -0.5 * B.y)));
   }
 }
 
@@ -150,13 +152,13 @@ __device__ __forceinline__ void pkc_scans(double2* sm, const BlueTables& bt) {
   __syncthreads();
 }
 
-// Interior-input value of one line for a transform kind.
-__device__ __forceinline__ double kind_in(int kind, double xj, double x0, double xe, int j, double ri) {
-  if (kind == DBX_KIND_ARINV) {
-    const double t1 = (double)j * ri;  // p_j = 1 - j/(n-1), p_{n-1-j} = j/(n-1)
-    return (xj - x0 * (1.0 - t1)) - xe * t1;
-  }
-  return xj;
+// (sum, difference) of the interior inputs at j and N-j for a transform kind
+// (xj, xm: the raw line values there; ARINV subtracts the ramp terms,
+// transforms.hpp:163-173, with p_j = 1 - j/(n-1)).
+__device__ __forceinline__ double2 kind_sd(int kind, double xj, double xm, double x0, double xe, int j, double ri) {
+  if (kind == DBX_KIND_ARINV)
+    return make_double2(xj + xm - (x0 + xe), (xj - xm) - (x0 - xe) * fma(-2.0 * ri, (double)j, 1.0));
+  return make_double2(xj + xm, xj - xm);
 }
 
 // Output k (0-based, line length n) of a transform kind from the DST outputs o.
@@ -197,11 +199,12 @@ __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_rows(SpecArgs a) {
   const double a0 = (xa && !sine) ? xa[0] : 0.0, ae = (xa && !sine) ? xa[n - 1] : 0.0;
   const double b0 = (xb && !sine) ? xb[0] : 0.0, be = (xb && !sine) ? xb[n - 1] : 0.0;
   const double ri = bt.rinv;
+  const int NL = bt.N;
   pkc_fill<M, T, CORE>(buf, bt, t, [&](int hh, int j) {
     const double* x = hh ? xb : xa;
-    if (!x) return 0.0;
-    if (sine) return x[j - 1];
-    return kind_in(kind, x[j], hh ? b0 : a0, hh ? be : ae, j, ri);
+    if (!x) return make_double2(0.0, 0.0);
+    if (sine) return kind_sd(kind, x[j - 1], x[NL - j - 1], 0.0, 0.0, j, ri);
+    return kind_sd(kind, x[j], x[NL - j], hh ? b0 : a0, hh ? be : ae, j, ri);
   });
   pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g);
   pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0));
@@ -261,11 +264,12 @@ __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_cols(SpecArgs a) {
   const int ca = c0 + 2 * g;
   const double xa0 = e0[2 * g], xae = e1[2 * g], xb0 = e0[2 * g + 1], xbe = e1[2 * g + 1];
   const bool la = 2 * g < ncol, lb = 2 * g + 1 < ncol;
+  const int NL = bt.N;
   pkc_fill<M, T, CORE>(buf, bt, t, [&](int hh, int j) {
-    if (!(hh ? lb : la)) return 0.0;
+    if (!(hh ? lb : la)) return make_double2(0.0, 0.0);
     const double* x = in + ca + hh;
-    if (sine) return x[(size_t)(j - 1) * n2];
-    return kind_in(kind, x[(size_t)j * n2], hh ? xb0 : xa0, hh ? xbe : xae, j, ri);
+    if (sine) return kind_sd(kind, x[(size_t)(j - 1) * n2], x[(size_t)(NL - j - 1) * n2], 0.0, 0.0, j, ri);
+    return kind_sd(kind, x[(size_t)j * n2], x[(size_t)(NL - j) * n2], hh ? xb0 : xa0, hh ? xbe : xae, j, ri);
   });
   pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g);
   pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0));

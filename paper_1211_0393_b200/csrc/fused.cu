@@ -157,12 +157,18 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
   // T~ along the rows (ar_inverse, transforms.hpp:163-173)
   const double ri = bt.rinv;
   double2* dbuf = sm + g * F::LD;
+  // AR-inverse interior (s_j - s_0 p_j - s_{n-1} p_{n-1-j}; p_j = 1 - j/(n-1),
+  // transforms.hpp:135-144, 163-173) as (sum, difference) of the pair j, N-j
+  const int N2 = bt.N;
+  const double xa0 = rowS[(2 * g) * LS], xae = rowS[(2 * g) * LS + n2 - 1];
+  const double xb0 = rowS[(2 * g + 1) * LS], xbe = rowS[(2 * g + 1) * LS + n2 - 1];
   pk_fill<M, TD, BLUE>(dbuf, bt, t, [&](int hh, int j) {
     const int h = 2 * g + hh;
-    if (h >= nl) return 0.0;
+    if (h >= nl) return make_double2(0.0, 0.0);
     const double* L = rowS + h * LS;
-    const double t1 = (double)j * ri;  // p_j = 1 - j/(n-1), p_{n-1-j} = j/(n-1) (transforms.hpp:135-144)
-    return (L[j] - L[0] * (1.0 - t1)) - L[n2 - 1] * t1;
+    const double x0 = hh ? xb0 : xa0, xe = hh ? xbe : xae;
+    const double lj = L[j], lm = L[N2 - j];
+    return make_double2(lj + lm - (x0 + xe), (lj - lm) - (x0 - xe) * fma(-2.0 * ri, (double)j, 1.0));
   });
   blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
   pk_split<M, BLUE>(dbuf, bt, rowS + (2 * g) * LS, rowS + (2 * g + 1) * LS, t, TD);
@@ -221,9 +227,12 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   // T along the rows (ar_forward, transforms.hpp:148-160)
   const double ri = bt.rinv;
   double2* dbuf = sm + g * F::LD;
+  const int N2 = bt.N;
   pk_fill<M, TD, BLUE>(dbuf, bt, t, [&](int hh, int j) {
     const int h = 2 * g + hh;
-    return h < nl ? io[h * LS + j] : 0.0;
+    if (h >= nl) return make_double2(0.0, 0.0);
+    const double vj = io[h * LS + j], vm = io[h * LS + N2 - j];
+    return make_double2(vj + vm, vj - vm);
   });
   blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
   pk_split<M, BLUE>(dbuf, bt, io + (2 * g) * LS, io + (2 * g + 1) * LS, t, TD);
@@ -408,6 +417,7 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   const double2* tw = stage_twiddles<M, S::TW>(reinterpret_cast<double2*>(base + S::off_tw), bt.tw);
   const int n = a.n1, n2 = a.n2;
   const size_t N = (size_t)n * n2;
+  PH_DECL
   const int c0 = 4 * blockIdx.x;
   const int nl = n2 - c0 < 4 ? n2 - c0 : 4;
   stage_lines(io, LS, a.in + (size_t)b * N + (size_t)c0 * n, nl, n);  // u^T lines
@@ -416,6 +426,7 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   cp_async_commit();
   cp_async_wait_group<1>();
   __syncthreads();
+  PH(0)
   if (threadIdx.x < 4) {
     const int h = threadIdx.x;
     e0[h] = h < nl ? io[h * LS] : 0.0;
@@ -425,29 +436,43 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   double2* buf = sm + g * padded_len(M);
   const double ri = bt.rinv;
   // T~ (ar_inverse, transforms.hpp:163-173) of lines 2g, 2g+1
+  const int NL = bt.N;
+  const double xa0 = io[(2 * g) * LS], xae = io[(2 * g) * LS + n - 1];
+  const double xb0 = io[(2 * g + 1) * LS], xbe = io[(2 * g + 1) * LS + n - 1];
   pk_fill<M, TD, BLUE>(buf, bt, t, [&](int hh, int j) {
     const int h = 2 * g + hh;
-    if (h >= nl) return 0.0;
+    if (h >= nl) return make_double2(0.0, 0.0);
     const double* L = io + h * LS;
-    const double t1 = (double)j * ri;
-    return (L[j] - L[0] * (1.0 - t1)) - L[n - 1] * t1;
+    const double x0 = hh ? xb0 : xa0, xe = hh ? xbe : xae;
+    const double lj = L[j], lm = L[NL - j];
+    return make_double2(lj + lm - (x0 + xe), (lj - lm) - (x0 - xe) * fma(-2.0 * ri, (double)j, 1.0));
   });
+  PH(1)
   blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
+  PH(2)
   pk_split<M, BLUE>(buf, bt, io + (2 * g) * LS, io + (2 * g + 1) * LS, t, TD);
   __syncthreads();
+  PH(3)
   odd_scans(io, LS, 4, bt);
   cp_async_wait_all();
   __syncthreads();
+  PH(4)
   // v = u o d (u_0 = alpha v_0, u_{n-1} = alpha v_{n-1}), then T (ar_forward)
   pk_fill<M, TD, BLUE>(buf, bt, t, [&](int hh, int j) {
     const int h = 2 * g + hh;
-    return h < nl ? io[h * LS + j] * dS[h * LS + j] : 0.0;
+    if (h >= nl) return make_double2(0.0, 0.0);
+    const double mj = io[h * LS + j] * dS[h * LS + j], mm = io[h * LS + NL - j] * dS[h * LS + NL - j];
+    return make_double2(mj + mm, mj - mm);
   });
+  PH(5)
   blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
+  PH(6)
   pk_split<M, BLUE>(buf, bt, io + (2 * g) * LS, io + (2 * g + 1) * LS, t, TD);
   __syncthreads();
+  PH(7)
   odd_scans(io, LS, 4, bt);
   __syncthreads();
+  PH(8)
   // T output w_0 = v_0 / alpha = e0 d_0, w_{n-1} = e1 d_{n-1}, interior DST + ramp
   // (NT % 4 == 0: each thread keeps one column h; 4 threads fill a 32-byte sector)
   static_assert(NT % 4 == 0, "column-group mapping");
@@ -467,6 +492,7 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
       s[(size_t)k * n2] = w;
     }
   }
+  PH(9)
 }
 
 // WHICH makes the attribute flag per kernel (the three kernels share one
@@ -501,6 +527,17 @@ int tcols_launch(const SpecArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+#ifdef DBX_PHASES
+int fused_debug_phases(unsigned long long* out, int n) {
+  if (n > 64) n = 64;
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, g_phase, n * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  static const unsigned long long zero[64] = {};
+  cudaMemcpyToSymbol(g_phase, zero, sizeof zero);
+  return n;
+}
+#endif
 
 // (conv L2, DST M, Bluestein?) combinations compiled for the fused pipeline.
 #define DBX_FUSED_LIST(X) X(1080, 1023, false) X(540, 1024, true) X(270, 255, false)

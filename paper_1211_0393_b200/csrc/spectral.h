@@ -84,5 +84,8 @@ int launch_dst_cols(const SpecArgs& a, cudaStream_t s);
 enum FusedKind { FUSED_AINV_TT = 0, FUSED_T_AXPY_AFWD = 1, FUSED_AINV_RESID = 2, FUSED_DST_TCOLS = 3 };
 bool fused_supported(int L2, int M, bool bluestein);
 int launch_fused(int which, const SpecArgs& a, cudaStream_t s);
+#ifdef DBX_PHASES
+int fused_debug_phases(unsigned long long* out, int n);  // read + reset (instrumented builds)
+#endif
 
 }  // namespace dbx

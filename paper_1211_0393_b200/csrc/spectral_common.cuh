@@ -10,6 +10,22 @@
 
 namespace dbx {
 
+// Phase timing (instrumented builds only: -DDBX_PHASES): thread 0 of every CTA
+// adds the clock64() delta since its previous mark to g_phase[i].
+#ifdef DBX_PHASES
+static __device__ unsigned long long g_phase[64];  // per translation unit (fused.cu reads its own)
+#define PH_DECL unsigned long long ph_t0 = clock64();
+#define PH(i)                                        \
+  if (threadIdx.x == 0) {                            \
+    const unsigned long long ph_t1 = clock64();      \
+    atomicAdd(&g_phase[i], ph_t1 - ph_t0);           \
+    ph_t0 = ph_t1;                                   \
+  }
+#else
+#define PH_DECL
+#define PH(i)
+#endif
+
 using fft::cadd;
 using fft::cmul;
 using fft::csub;
@@ -255,30 +271,28 @@ __device__ __forceinline__ void blue_core(double2* sm, double2* buf, const BlueT
 // z = y^a + i y^b and are separated by conjugate symmetry, so the transform
 // count is half that of one complex DFT per line; the odd outputs are a
 // prefix sum (odd_scan).  Works for any N (odd or even).
-// val(h, j): interior value x^h_j, h in {0, 1} (line a / b), j in [1, N).
+// sd(h, j) returns (x^h_j + x^h_{N-j}, x^h_j - x^h_{N-j}) for line h in {0, 1}
+// and j in [1, N/2]: each thread forms z_j and z_{N-j} from one set of loads
+// (sin(pi (N-j)/N) = sin(pi j/N)).
 template <int M, int T, bool BLUE, typename F>
-__device__ __forceinline__ void pk_fill(double2* buf, const BlueTables& bt, int t, F val) {
-  const int N = bt.N;
-  constexpr int PF = (M + T - 1) / T;
-  constexpr int CH = 4;  // elements per load batch (bounded register use)
+__device__ __forceinline__ void pk_fill(double2* buf, const BlueTables& bt, int t, F sd) {
+  const int N = bt.N, H = N / 2;
+  // positions no pair covers: 0, and the Bluestein zero padding [N, M)
+  if (t == 0) buf[pad<M>(0)] = make_double2(0.0, 0.0);
+  if constexpr (BLUE)
+    for (int p = N + t; p < M; p += T) buf[pad<M>(p)] = make_double2(0.0, 0.0);
+  constexpr int HMAX = (BLUE ? M / 2 + 1 : M) / 2;
+  constexpr int PF = (HMAX + T - 1) / T;
 #pragma unroll
-  for (int i0 = 0; i0 < PF; i0 += CH) {
-    double2 z[CH];
-#pragma unroll
-    for (int u = 0; u < CH; ++u) {
-      const int j = t + (i0 + u) * T;
-      z[u] = make_double2(0.0, 0.0);
-      if (i0 + u < PF && j >= 1 && j < N) {
-        const double s = __ldg(bt.sn + j);
-        const double xa = val(0, j), xar = val(0, N - j);
-        const double xb = val(1, j), xbr = val(1, N - j);
-        z[u] = pre<BLUE>(make_double2(fma(s, xa + xar, 0.5 * (xa - xar)), fma(s, xb + xbr, 0.5 * (xb - xbr))), bt, j);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < CH; ++u) {
-      const int j = t + (i0 + u) * T;
-      if (i0 + u < PF && j < M) buf[pad<M>(j)] = z[u];
+  for (int i = 0; i < PF; ++i) {
+    const int j = 1 + t + i * T;
+    if (j <= H) {
+      const double s = __ldg(bt.sn + j);
+      const double2 A = sd(0, j), B = sd(1, j);
+      const double2 zj = make_double2(fma(s, A.x, 0.5 * A.y), fma(s, B.x, 0.5 * B.y));
+      const double2 zm = make_double2(fma(s, A.x, -0.5 * A.y), fma(s, B.x, -0.5 * B.y));
+      buf[pad<M>(j)] = pre<BLUE>(zj, bt, j);
+      if (N - j != j) buf[pad<M>(N - j)] = pre<BLUE>(zm, bt, N - j);
     }
   }
 }
@@ -310,23 +324,24 @@ __device__ __forceinline__ void pk_split(const double2* buf, const BlueTables& b
 // One warp: inclusive prefix sums of o[1], o[3], ..., o[2 cnt - 1], scaled.
 __device__ __forceinline__ void odd_scan(double* o, int cnt, double sc, int lane) {
   double carry = 0.0;
-  for (int base = 0; base < cnt; base += 8 * 32) {
-    double v[8];
+  constexpr int RW = 16;  // rows of 32 in flight (one chunk covers 512 outputs)
+  for (int base = 0; base < cnt; base += RW * 32) {
+    double v[RW];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < RW; ++i) {
       const int m = base + i * 32 + lane;
       v[i] = m < cnt ? o[2 * m + 1] : 0.0;
     }
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < RW; ++i) {
         const double y = __shfl_up_sync(0xffffffffu, v[i], d);
         if (lane >= d) v[i] += y;
       }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < RW; ++i) {
       const double tot = __shfl_sync(0xffffffffu, v[i], 31);
       const int m = base + i * 32 + lane;
       if (m < cnt) o[2 * m + 1] = (v[i] + carry) * sc;
