@@ -39,8 +39,9 @@ struct Fused {
   static constexpr int W4 = (LC > LD ? LC : LD) * 2;        // work region (double2)
   static constexpr int LMAX = BLUE ? M / 2 + 1 : M + 1;     // longest row n2
   static constexpr int LS = (LMAX + 1) / 2 * 2 + 4;         // smem row stride (doubles)
-  static constexpr size_t off_rows = (size_t)W4 * 16;       // 4 rows
-  static constexpr size_t off_x = off_rows + (size_t)4 * LS * 8;  // 4 more rows (t_axpy)
+  static constexpr int LSO = ((LMAX > PkOut<LMAX>::OL ? LMAX : PkOut<LMAX>::OL) + 1) / 2 * 2 + 4;  // rows that receive DST outputs
+  static constexpr size_t off_rows = (size_t)W4 * 16;       // 4 rows (stride LSO)
+  static constexpr size_t off_x = off_rows + (size_t)4 * LSO * 8;  // 4 more rows (t_axpy)
   // rows_ainv_tt: twiddles after the rows
   static constexpr size_t tt_twd = off_x;
   static constexpr bool TT_TWD = tt_twd + TWD <= kBudget;
@@ -122,7 +123,7 @@ __device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, 
 template <int L2, int M, bool BLUE>
 __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecArgs a) {
   using F = Fused<L2, M, BLUE>;
-  constexpr int NT = F::NT, TD = F::TD, LS = F::LS;
+  constexpr int NT = F::NT, TD = F::TD, LS = F::LSO, LMAX = F::LMAX;
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 sm[];
@@ -171,9 +172,9 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
     return make_double2(lj + lm - (x0 + xe), (lj - lm) - (x0 - xe) * fma(-2.0 * ri, (double)j, 1.0));
   });
   blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
-  pk_split<M, BLUE>(dbuf, bt, rowS + (2 * g) * LS, rowS + (2 * g + 1) * LS, t, TD);
+  pk_split2<M, BLUE, LMAX>(dbuf, bt, rowS + (2 * g) * LS, rowS + (2 * g + 1) * LS, t, TD);
   __syncthreads();
-  odd_scans(rowS, LS, 4, bt);
+  odd_scans2<LMAX>(rowS, LS, 4, bt);
   __syncthreads();
   static_assert(NT % 4 == 0, "row-group mapping");
   const int h = threadIdx.x & 3;
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
     const double* o = rowS + h * LS;
     const double u0 = bt.alpha * e0[h], ue = bt.alpha * e1[h];
     for (int k = threadIdx.x >> 2; k < n2; k += NT / 4)
-      uT[(size_t)k * n1] = (k == 0) ? u0 : (k == n2 - 1) ? ue : o[k];
+      uT[(size_t)k * n1] = (k == 0) ? u0 : (k == n2 - 1) ? ue : pk_at<LMAX>(o, k);
   }
 }
 
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
 template <int L2, int M, bool BLUE>
 __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(SpecArgs a) {
   using F = Fused<L2, M, BLUE>;
-  constexpr int NT = F::NT, TD = F::TD, LS = F::LS;
+  constexpr int NT = F::NT, TD = F::TD, LS = F::LS, LSO = F::LSO, LMAX = F::LMAX;
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 sm[];
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   const double* xo = resolve_ptr(a.xold, a.st, a.xoldsel, b, a.batch, N) + (size_t)r0 * n2;
   const double* fimg = a.f ? a.f + (size_t)b * N + (size_t)r0 * n2 : nullptr;
   if (fimg && threadIdx.x < nl) prefetch_l2(fimg + (size_t)threadIdx.x * n2, (unsigned)n2 * 8);
-  stage_lines(io, LS, a.in + (size_t)b * N + (size_t)r0 * n2, nl, n2);  // v rows
+  stage_lines(io, LSO, a.in + (size_t)b * N + (size_t)r0 * n2, nl, n2);  // v rows
   cp_async_commit();
   stage_lines(stX, LS, xo, nl, n2);                                       // x_{k-1} rows
   cp_async_commit();
@@ -221,8 +222,8 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   __syncthreads();
   if (threadIdx.x < 4) {
     const int h = threadIdx.x;
-    e0[h] = h < nl ? io[h * LS] : 0.0;
-    e1[h] = h < nl ? io[h * LS + n2 - 1] : 0.0;
+    e0[h] = h < nl ? io[h * LSO] : 0.0;
+    e1[h] = h < nl ? io[h * LSO + n2 - 1] : 0.0;
   }
   // T along the rows (ar_forward, transforms.hpp:148-160)
   const double ri = bt.rinv;
@@ -231,18 +232,18 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   pk_fill<M, TD, BLUE>(dbuf, bt, t, [&](int hh, int j) {
     const int h = 2 * g + hh;
     if (h >= nl) return make_double2(0.0, 0.0);
-    const double vj = io[h * LS + j], vm = io[h * LS + N2 - j];
+    const double vj = io[h * LSO + j], vm = io[h * LSO + N2 - j];
     return make_double2(vj + vm, vj - vm);
   });
   blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
-  pk_split<M, BLUE>(dbuf, bt, io + (2 * g) * LS, io + (2 * g + 1) * LS, t, TD);
+  pk_split2<M, BLUE, LMAX>(dbuf, bt, io + (2 * g) * LSO, io + (2 * g + 1) * LSO, t, TD);
   __syncthreads();
   // the DST lines are free now: stage the f rows there (L2-prefetched at
   // kernel start) behind the scans
   double* fS = reinterpret_cast<double*>(sm);
   if (fimg) stage_lines(fS, LS, fimg, nl, n2);
   cp_async_commit();
-  odd_scans(io, LS, 4, bt);
+  odd_scans2<LMAX>(io, LSO, 4, bt);
   cp_async_wait_all();
   __syncthreads();
   // x_k = x_{k-1} + tau * T v (solver.hpp:106), rows r0..r0+nl-1 contiguous
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   double p0 = 0.0, p1 = 0.0;
   for (int h = 0; h < nl; ++h) {
     const double a0 = ia * e0[h], a1 = ia * e1[h];
-    const double* o = io + h * LS;
+    const double* o = io + h * LSO;
     double* xs = stX + h * LS;
     const double* fs = fS + h * LS;
     double* xr = xn + (size_t)h * n2;
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
       else if (k == n2 - 1) w = a1;
       else {
         const double t1 = (double)k * ri;
-        w = o[k] + a0 * (1.0 - t1) + a1 * t1;
+        w = pk_at<LMAX>(o, k) + a0 * (1.0 - t1) + a1 * t1;
       }
       const double xv = xs[k] + tau * w;
       xr[k] = xv;
@@ -394,8 +395,9 @@ struct TcolSmem {
   static constexpr int TD = line_threads(M, dst_per(M));
   static constexpr int LMAX = BLUE ? M / 2 + 1 : M + 1;         // max line length n
   static constexpr int LS = (LMAX + 1) / 2 * 2 + 4;             // line stride (doubles): 4 lines hit distinct banks
+  static constexpr int LSO = ((LMAX > PkOut<LMAX>::OL ? LMAX : PkOut<LMAX>::OL) + 1) / 2 * 2 + 4;  // io lines
   static constexpr size_t off_io = (size_t)2 * padded_len(M) * 16;
-  static constexpr size_t off_d = off_io + (size_t)4 * LS * 8;
+  static constexpr size_t off_d = off_io + (size_t)4 * LSO * 8;
   static constexpr size_t off_tw = off_d + (size_t)4 * LS * 8;
   static constexpr size_t TWB = (size_t)fft::twiddles_needed(M) * 16;
   static constexpr bool TW = off_tw + TWB <= 115200;  // keep 2 CTAs / SM
@@ -405,7 +407,7 @@ struct TcolSmem {
 template <int M, bool BLUE>
 __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(SpecArgs a) {
   using S = TcolSmem<M, BLUE>;
-  constexpr int TD = S::TD, NT = 2 * TD, LS = S::LS;
+  constexpr int TD = S::TD, NT = 2 * TD, LS = S::LS, LSO = S::LSO, LMAX = S::LMAX;
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 sm[];
@@ -420,7 +422,7 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   PH_DECL
   const int c0 = 4 * blockIdx.x;
   const int nl = n2 - c0 < 4 ? n2 - c0 : 4;
-  stage_lines(io, LS, a.in + (size_t)b * N + (size_t)c0 * n, nl, n);  // u^T lines
+  stage_lines(io, LSO, a.in + (size_t)b * N + (size_t)c0 * n, nl, n);  // u^T lines
   cp_async_commit();
   stage_lines(dS, LS, a.dT + (size_t)c0 * n, nl, n);                   // d^T lines
   cp_async_commit();
@@ -429,20 +431,20 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   PH(0)
   if (threadIdx.x < 4) {
     const int h = threadIdx.x;
-    e0[h] = h < nl ? io[h * LS] : 0.0;
-    e1[h] = h < nl ? io[h * LS + n - 1] : 0.0;
+    e0[h] = h < nl ? io[h * LSO] : 0.0;
+    e1[h] = h < nl ? io[h * LSO + n - 1] : 0.0;
   }
   const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
   double2* buf = sm + g * padded_len(M);
   const double ri = bt.rinv;
   // T~ (ar_inverse, transforms.hpp:163-173) of lines 2g, 2g+1
   const int NL = bt.N;
-  const double xa0 = io[(2 * g) * LS], xae = io[(2 * g) * LS + n - 1];
-  const double xb0 = io[(2 * g + 1) * LS], xbe = io[(2 * g + 1) * LS + n - 1];
+  const double xa0 = io[(2 * g) * LSO], xae = io[(2 * g) * LSO + n - 1];
+  const double xb0 = io[(2 * g + 1) * LSO], xbe = io[(2 * g + 1) * LSO + n - 1];
   pk_fill<M, TD, BLUE>(buf, bt, t, [&](int hh, int j) {
     const int h = 2 * g + hh;
     if (h >= nl) return make_double2(0.0, 0.0);
-    const double* L = io + h * LS;
+    const double* L = io + h * LSO;
     const double x0 = hh ? xb0 : xa0, xe = hh ? xbe : xae;
     const double lj = L[j], lm = L[NL - j];
     return make_double2(lj + lm - (x0 + xe), (lj - lm) - (x0 - xe) * fma(-2.0 * ri, (double)j, 1.0));
@@ -450,10 +452,10 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   PH(1)
   blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
   PH(2)
-  pk_split<M, BLUE>(buf, bt, io + (2 * g) * LS, io + (2 * g + 1) * LS, t, TD);
+  pk_split2<M, BLUE, LMAX>(buf, bt, io + (2 * g) * LSO, io + (2 * g + 1) * LSO, t, TD);
   __syncthreads();
   PH(3)
-  odd_scans(io, LS, 4, bt);
+  odd_scans2<LMAX>(io, LSO, 4, bt);
   cp_async_wait_all();
   __syncthreads();
   PH(4)
@@ -461,16 +463,17 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   pk_fill<M, TD, BLUE>(buf, bt, t, [&](int hh, int j) {
     const int h = 2 * g + hh;
     if (h >= nl) return make_double2(0.0, 0.0);
-    const double mj = io[h * LS + j] * dS[h * LS + j], mm = io[h * LS + NL - j] * dS[h * LS + NL - j];
+    const double* o = io + h * LSO;
+    const double mj = pk_at<LMAX>(o, j) * dS[h * LS + j], mm = pk_at<LMAX>(o, NL - j) * dS[h * LS + NL - j];
     return make_double2(mj + mm, mj - mm);
   });
   PH(5)
   blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
   PH(6)
-  pk_split<M, BLUE>(buf, bt, io + (2 * g) * LS, io + (2 * g + 1) * LS, t, TD);
+  pk_split2<M, BLUE, LMAX>(buf, bt, io + (2 * g) * LSO, io + (2 * g + 1) * LSO, t, TD);
   __syncthreads();
   PH(7)
-  odd_scans(io, LS, 4, bt);
+  odd_scans2<LMAX>(io, LSO, 4, bt);
   __syncthreads();
   PH(8)
   // T output w_0 = v_0 / alpha = e0 d_0, w_{n-1} = e1 d_{n-1}, interior DST + ramp
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   const int h = threadIdx.x & 3;
   if (h < nl) {
     double* s = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c0 + h;
-    const double* o = io + h * LS;
+    const double* o = io + h * LSO;
     const double a0 = e0[h] * dS[h * LS], a1 = e1[h] * dS[h * LS + n - 1];
     for (int k = threadIdx.x >> 2; k < n; k += NT / 4) {
       double w;
@@ -487,7 +490,7 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
       else if (k == n - 1) w = a1;
       else {
         const double t1 = (double)k * ri;
-        w = o[k] + a0 * (1.0 - t1) + a1 * t1;
+        w = pk_at<LMAX>(o, k) + a0 * (1.0 - t1) + a1 * t1;
       }
       s[(size_t)k * n2] = w;
     }

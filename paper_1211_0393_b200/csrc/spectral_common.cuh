@@ -356,6 +356,83 @@ __device__ __forceinline__ void odd_scans(double* o, int LS, int nlines, const B
   for (int s = w; s < nlines; s += nw) odd_scan(o + (size_t)s * LS, bt.N / 2, bt.scale, lane);
 }
 
+// ---------------------------------------------------------------------------
+// Scan-friendly output layout of the fused kernels (N <= 1025): X_{2l} at
+// o[l]; the odd terms X_{2m+1} at o[EB + (m & 15) * STR + (m >> 4)], so lane L
+// of the scanning warp owns the contiguous run m = 16L .. 16L+15 with
+// conflict-free accesses (STR odd): 16 sequential adds per lane + one warp
+// scan of the lane totals, instead of shuffle scans over every element.
+template <int LMAX>
+struct PkOut {
+  static constexpr int EB = LMAX / 2 + 1;                  // even block
+  static constexpr int CNT = LMAX / 2;                     // max odd terms
+  static constexpr int STR = ((CNT + 15) / 16) | 1;        // odd row stride >= CNT/16
+  static constexpr int STR1 = STR < (CNT + 15) / 16 + 1 ? STR + 2 : STR;
+  static constexpr int OL = EB + 16 * STR1;                // doubles per output line
+  static_assert(CNT <= 512, "one scanning warp covers 32 x 16 odd terms");
+};
+
+template <int LMAX>
+__device__ __forceinline__ double pk_at(const double* o, int k) {
+  using P = PkOut<LMAX>;
+  const int m = k >> 1;
+  const int odd_at = P::EB + (m & 15) * P::STR1 + (m >> 4);
+  return o[(k & 1) ? odd_at : m];  // select, one load (no divergent branch)
+}
+
+template <int M, bool BLUE, int LMAX>
+__device__ __forceinline__ void pk_split2(const double2* buf, const BlueTables& bt, double* oa, double* ob, int t,
+                                          int T) {
+  using P = PkOut<LMAX>;
+  const int N = bt.N;
+  const double hs = 0.5 * bt.scale;
+  for (int l = t; 2 * l <= N - 1; l += T) {
+    const int m = l == 0 ? 0 : N - l;
+    const double2 zl = pre<BLUE>(buf[pad<M>(l)], bt, l);
+    const double2 zm = pre<BLUE>(buf[pad<M>(m)], bt, m);
+    if (l >= 1) {
+      oa[l] = hs * (zm.y - zl.y);
+      ob[l] = hs * (zl.x - zm.x);
+    }
+    if (2 * l + 1 <= N - 1) {
+      const double f = l == 0 ? 0.25 : 0.5;
+      const int q = P::EB + (l & 15) * P::STR1 + (l >> 4);
+      oa[q] = f * (zl.x + zm.x);
+      ob[q] = f * (zl.y + zm.y);
+    }
+  }
+}
+
+// Odd-output scans of `nlines` output lines (stride LS), one warp per line.
+template <int LMAX>
+__device__ __forceinline__ void odd_scans2(double* o, int LS, int nlines, const BlueTables& bt) {
+  using P = PkOut<LMAX>;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int cnt = bt.N / 2;
+  const double sc = bt.scale;
+  for (int s = w; s < nlines; s += nw) {
+    double* q = o + (size_t)s * LS + P::EB + lane;
+    double v[16];
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v[i] = (16 * lane + i < cnt) ? q[i * P::STR1] : 0.0;
+      acc += v[i];
+      v[i] = acc;
+    }
+    double inc = acc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    const double off = inc - acc;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (16 * lane + i < cnt) q[i * P::STR1] = (v[i] + off) * sc;
+  }
+}
+
 // cp.async copy of `nl` contiguous lines of n doubles (src) into smem lines of
 // stride LS (dst); 16-byte copies when n and both bases allow it.
 __device__ __forceinline__ void stage_lines(double* dst, int LS, const double* src, int nl, int n) {
