@@ -375,56 +375,81 @@ __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ 
   line_sync(bar, T);
 }
 
-// Output pairs k in [K0, K1] of an odd-prime butterfly (symmetric pairs in v:
-// v[j] = a_j, v[R-j] = b_j).  K0/K1 are compile-time so the rolled counter is
-// uniform: the constant-table reads go through the uniform datapath (ULDC ->
-// DFMA operand) and only one pair of accumulators is live.
+// Output pairs K0..K1 (compile-time) of one odd-prime butterfly whose
+// symmetric pairs a_j = v_j + v_{R-j}, b_j = v_j - v_{R-j} sit in shared
+// memory at the butterfly's input slots (j, R-j): one sweep over j feeds all
+// KP pairs (4 KP independent FMA chains, constants as immediate operands).
+// The outputs stay in registers (out[2u] = X_{K0+u}, out[2u+1] = X_{R-K0-u}).
 template <int R, int S, int L, int K0, int K1>
-__device__ __forceinline__ void odd_pairs(const double2* v, double2 x0, double2* buf, int base, int Ns) {
+__device__ __forceinline__ void odd_pairs_smem(const double2* buf, int b, int NB, double2 x0, double2* out) {
   using K = OddConst<R>;
   constexpr int H = (R - 1) / 2;
-#pragma unroll 1
-  for (int kk = K0; kk <= K1; ++kk) {
-    double2 A = x0, B = make_double2(0.0, 0.0);
-    int e = 0;
+  constexpr int KP = K1 - K0 + 1;
+  double2 A[KP], B[KP];
 #pragma unroll
-    for (int j = 1; j <= H; ++j) {
-      e += kk;
-      if (e >= R) e -= R;
-      const double c = K::c(e), s = K::s(e);
-      A.x = fma(c, v[j].x, A.x);
-      A.y = fma(c, v[j].y, A.y);
-      B.x = fma(s, v[R - j].x, B.x);
-      B.y = fma(s, v[R - j].y, B.y);
+  for (int u = 0; u < KP; ++u) {
+    A[u] = x0;
+    B[u] = make_double2(0.0, 0.0);
+  }
+#pragma unroll
+  for (int j = 1; j <= H; ++j) {
+    const double2 a = buf[pad<L>(b + j * NB)], c = buf[pad<L>(b + (R - j) * NB)];
+#pragma unroll
+    for (int u = 0; u < KP; ++u) {
+      const int e = (j * (K0 + u)) % R;
+      A[u].x = fma(K::c(e), a.x, A[u].x);
+      A[u].y = fma(K::c(e), a.y, A[u].y);
+      B[u].x = fma(K::s(e), c.x, B[u].x);
+      B[u].y = fma(K::s(e), c.y, B[u].y);
     }
-    const double2 sb = mul_si<S>(B);
-    buf[pad<L>(base + kk * Ns)] = cadd(A, sb);
-    buf[pad<L>(base + (R - kk) * Ns)] = csub(A, sb);
+  }
+#pragma unroll
+  for (int u = 0; u < KP; ++u) {
+    const double2 sb = mul_si<S>(B[u]);
+    out[2 * u] = cadd(A[u], sb);
+    out[2 * u + 1] = csub(A[u], sb);
   }
 }
 
-// part -> compile-time pair range (part is warp-uniform at run time)
-template <int R, int S, int L, int H, int P, int Q>
-__device__ __forceinline__ void odd_pairs_dispatch(int part, const double2* v, double2 x0, double2* buf, int base,
-                                                   int Ns) {
+template <int R, int S, int L, int H, int P, int Q, int KPM>
+__device__ __forceinline__ void odd_pairs_smem_dispatch(int part, const double2* buf, int b, int NB, double2 x0,
+                                                        double2* out) {
   if constexpr (Q < P) {
     if (part == Q) {
-      odd_pairs<R, S, L, 1 + (Q * H) / P, ((Q + 1) * H) / P>(v, x0, buf, base, Ns);
+      odd_pairs_smem<R, S, L, 1 + (Q * H) / P, ((Q + 1) * H) / P>(buf, b, NB, x0, out);
       return;
     }
-    odd_pairs_dispatch<R, S, L, H, P, Q + 1>(part, v, x0, buf, base, Ns);
+    odd_pairs_smem_dispatch<R, S, L, H, P, Q + 1, KPM>(part, buf, b, NB, x0, out);
+  }
+}
+
+template <int R, int S, int L, int H, int P, int Q>
+__device__ __forceinline__ void odd_pairs_store_dispatch(int part, const double2* out, double2* buf, int base,
+                                                         int Ns) {
+  if constexpr (Q < P) {
+    if (part == Q) {
+      constexpr int K0 = 1 + (Q * H) / P, K1 = ((Q + 1) * H) / P;
+#pragma unroll
+      for (int u = 0; u <= K1 - K0; ++u) {
+        buf[pad<L>(base + (K0 + u) * Ns)] = out[2 * u];
+        buf[pad<L>(base + (R - K0 - u) * Ns)] = out[2 * u + 1];
+      }
+      return;
+    }
+    odd_pairs_store_dispatch<R, S, L, H, P, Q + 1>(part, out, buf, base, Ns);
   }
 }
 
 // CTA-wide stage for a large odd prime R (>= 17) on G lines at once: the
 // G * NB butterflies (NB = L/R is small, e.g. 33 for 1023 = 31*33) are packed
-// densely over a warp-aligned slot range of NBp threads, and that range is
-// replicated P times (P = CTA threads / NBp): replica `part` computes the
-// output pairs k in (part*H/P, (part+1)*H/P] of every butterfly, so all warps
-// of the CTA share the stage and each thread runs 1/P of the DFMA chains.  The
-// output-pair loop is rolled with a warp-uniform counter: the cos/sin table
-// reads become uniform-datapath loads feeding DFMA directly, and only one
-// pair of accumulators is live.
+// densely over a warp-aligned slot range of NBp threads, replicated P times
+// (P = CTA threads / NBp).  Register-lean three-phase form: (1) replica 0
+// twiddles its butterfly's inputs and folds them into the symmetric pairs in
+// place (a_j at slot j, b_j at slot R-j) and keeps X_0; (2) every replica p
+// sweeps the pairs once for its output range (pH/P, (p+1)H/P], results in
+// registers; (3) after a barrier the outputs go to the Stockham positions.
+// No thread holds the R inputs at once, so the stage needs ~4(H/P) + O(1)
+// live complex values instead of R + accumulators.
 template <int L, int Ns, int R, int S, int G, int PL, int NTH>
 __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __restrict__ tw, int tid) {
   constexpr int NB = L / R;
@@ -432,39 +457,53 @@ __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __rest
   constexpr int NBp = (G * NB + 31) / 32 * 32;
   constexpr int P0 = NTH / NBp;
   constexpr int P = P0 < 1 ? 1 : (P0 > H ? H : P0);
+  constexpr int KPM = (H + P - 1) / P;
   const int part = tid / NBp;                 // warp-uniform
   const int slot = tid - part * NBp;
   const bool act = part < P && slot < G * NB;
   const int line = act ? slot / NB : 0;
   const int b = act ? slot - line * NB : 0;
   double2* buf = sm + line * PL;
-  double2 v[R];
   const int k = b % Ns;
-  double2 w1 = make_double2(1.0, 0.0);
-  if constexpr (Ns > 1) {
-    constexpr int step = L / (Ns * R);
-    if (act) w1 = tw[k * step];
-  }
-  if (act) {
+  double2 sum = make_double2(0.0, 0.0);
+  if (act && part == 0) {
+    if constexpr (Ns > 1) {
+      // twiddle the inputs in place (r = 1..R-1), powers by the window scheme
+      constexpr int step = L / (Ns * R);
+      const double2 w1 = tw[k * step];
+      double2 win[4];
+      win[0] = w1;
+      win[1] = cmul(w1, w1);
+      win[2] = cmul(win[1], w1);
+      win[3] = cmul(win[1], win[1]);
+      const double2 w4 = win[3];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = buf[pad<L>(b + r * NB)];
-  }
-  __syncthreads();
-  if (act) {
-    if constexpr (Ns > 1) apply_twiddles<R, S>(v, w1);
-    const double2 x0 = v[0];
-    double2 sum = x0;
+      for (int r = 1; r < R; ++r) {
+        if (r > 4) win[(r - 1) & 3] = cmul(win[(r - 1) & 3], w4);
+        double2& x = buf[pad<L>(b + r * NB)];
+        x = S < 0 ? cmul(x, win[(r - 1) & 3]) : cmulc(x, win[(r - 1) & 3]);
+      }
+    }
+    sum = buf[pad<L>(b)];
 #pragma unroll
     for (int j = 1; j <= H; ++j) {
-      const double2 a = cadd(v[j], v[R - j]);
-      const double2 c = csub(v[j], v[R - j]);
-      v[j] = a;
-      v[R - j] = c;
+      double2& vj = buf[pad<L>(b + j * NB)];
+      double2& vm = buf[pad<L>(b + (R - j) * NB)];
+      const double2 x = vj, y = vm;
+      const double2 a = cadd(x, y);
+      vj = a;
+      vm = csub(x, y);
       sum = cadd(sum, a);
     }
+  }
+  __syncthreads();
+  double2 out[2 * KPM];
+  if (act) odd_pairs_smem_dispatch<R, S, L, H, P, 0, KPM>(part, buf, b, NB, buf[pad<L>(b)], out);
+  __syncthreads();
+  if (act) {
     const int base = (b / Ns) * Ns * R + k;
     if (part == 0) buf[pad<L>(base)] = sum;
-    odd_pairs_dispatch<R, S, L, H, P, 0>(part, v, x0, buf, base, Ns);
+    odd_pairs_store_dispatch<R, S, L, H, P, 0>(part, out, buf, base, Ns);
   }
   __syncthreads();
 }

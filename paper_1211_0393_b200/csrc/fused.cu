@@ -139,18 +139,22 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
   const int nl = n1 - r0 < 4 ? n1 - r0 : 4;
   const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
   const int ra = r0 + 2 * g, rb = ra + 1;
+  PH_DECL
   // A' r rows: inverse packed row FFT (conv line g = rows 2g, 2g+1)
   double2* cbuf = sm + g * F::LC;
   conv_inv_load<L2, TD>(cbuf, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t);
   cp_async_wait_all();
   __syncthreads();
+  PH(20)
   fft::fft<L2, +1, TD>(cbuf, twc, t, 1 + g);
+  PH(21)
   for (int c = t; c < n2; c += TD) {
     const double2 v = cbuf[pad<L2>(c)];
     rowS[(2 * g) * LS + c] = v.x;
     rowS[(2 * g + 1) * LS + c] = v.y;
   }
   __syncthreads();
+  PH(22)
   if (threadIdx.x < 4) {
     e0[threadIdx.x] = rowS[threadIdx.x * LS];
     e1[threadIdx.x] = rowS[threadIdx.x * LS + n2 - 1];
@@ -171,11 +175,14 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
     const double lj = L[j], lm = L[N2 - j];
     return make_double2(lj + lm - (x0 + xe), (lj - lm) - (x0 - xe) * fma(-2.0 * ri, (double)j, 1.0));
   });
+  PH(23)
   blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
+  PH(24)
   pk_split2<M, BLUE, LMAX>(dbuf, bt, rowS + (2 * g) * LS, rowS + (2 * g + 1) * LS, t, TD);
   __syncthreads();
   odd_scans2<LMAX>(rowS, LS, 4, bt);
   __syncthreads();
+  PH(25)
   static_assert(NT % 4 == 0, "row-group mapping");
   const int h = threadIdx.x & 3;
   if (h < nl) {
@@ -185,6 +192,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
     for (int k = threadIdx.x >> 2; k < n2; k += NT / 4)
       uT[(size_t)k * n1] = (k == 0) ? u0 : (k == n2 - 1) ? ue : pk_at<LMAX>(o, k);
   }
+  PH(26)
 }
 
 // ---------------------------------------------------------------------------
@@ -213,6 +221,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
   const double* xo = resolve_ptr(a.xold, a.st, a.xoldsel, b, a.batch, N) + (size_t)r0 * n2;
   const double* fimg = a.f ? a.f + (size_t)b * N + (size_t)r0 * n2 : nullptr;
+  PH_DECL
   if (fimg && threadIdx.x < nl) prefetch_l2(fimg + (size_t)threadIdx.x * n2, (unsigned)n2 * 8);
   stage_lines(io, LSO, a.in + (size_t)b * N + (size_t)r0 * n2, nl, n2);  // v rows
   cp_async_commit();
@@ -220,6 +229,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   cp_async_commit();
   cp_async_wait_group<1>();
   __syncthreads();
+  PH(10)
   if (threadIdx.x < 4) {
     const int h = threadIdx.x;
     e0[h] = h < nl ? io[h * LSO] : 0.0;
@@ -235,7 +245,9 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
     const double vj = io[h * LSO + j], vm = io[h * LSO + N2 - j];
     return make_double2(vj + vm, vj - vm);
   });
+  PH(11)
   blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
+  PH(12)
   pk_split2<M, BLUE, LMAX>(dbuf, bt, io + (2 * g) * LSO, io + (2 * g + 1) * LSO, t, TD);
   __syncthreads();
   // the DST lines are free now: stage the f rows there (L2-prefetched at
@@ -246,6 +258,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   odd_scans2<LMAX>(io, LSO, 4, bt);
   cp_async_wait_all();
   __syncthreads();
+  PH(13)
   // x_k = x_{k-1} + tau * T v (solver.hpp:106), rows r0..r0+nl-1 contiguous
   double* xn = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + (size_t)r0 * n2;
   const double ia = 1.0 / bt.alpha, tau = a.tau;
@@ -276,9 +289,11 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
     }
   }
   __syncthreads();  // x rows complete; DST buffers free for the conv lines
+  PH(14)
   const int ra = r0 + 2 * g, rb = ra + 1;
   conv_fwd_rows<L2, TD>(sm + g * F::LC, stX + (2 * g) * LS, stX + (2 * g + 1) * LS, n2, a.q2, twc,
                         a.zbuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t, 1 + g);
+  PH(15)
   if (a.part.p) {
     double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
     const double s0 = block_sum<NT>(p0, red);

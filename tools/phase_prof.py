@@ -13,7 +13,11 @@ from paper_1211_0393_b200 import configs as cf  # noqa: E402
 
 NAMES = {0: "dst_tcols:stage", 1: "dst_tcols:fill1", 2: "dst_tcols:fft1", 3: "dst_tcols:split1",
          4: "dst_tcols:scan1", 5: "dst_tcols:fill2", 6: "dst_tcols:fft2", 7: "dst_tcols:split2",
-         8: "dst_tcols:scan2", 9: "dst_tcols:store"}
+         8: "dst_tcols:scan2", 9: "dst_tcols:store",
+         10: "t_axpy:stage", 11: "t_axpy:fill", 12: "t_axpy:dft", 13: "t_axpy:split+scan",
+         14: "t_axpy:x-update", 15: "t_axpy:conv-fwd", 20: "ainv_tt:load", 21: "ainv_tt:inv-fft",
+         22: "ainv_tt:rows", 23: "ainv_tt:fill", 24: "ainv_tt:dft", 25: "ainv_tt:split+scan",
+         26: "ainv_tt:store"}
 
 
 def main():
