@@ -347,12 +347,22 @@ __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ 
       if (NB % T == 0 || b < NB) w1[i] = tw[(b % Ns) * step];
     }
   }
+  // padded addresses linear in r (base + immediate offsets) when the stride
+  // is a multiple of the padding period (or L is odd: no padding)
+  constexpr bool LIN_IN = (L & 1) || (NB % 8 == 0);
+  constexpr int SIN = (L & 1) ? NB : NB + NB / 8;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int b = t + i * T;
     if (NB % T == 0 || b < NB) {
+      if constexpr (LIN_IN) {
+        const double2* src = buf + pad<L>(b);
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[i][r] = buf[pad<L>(b + r * NB)];
+        for (int r = 0; r < R; ++r) v[i][r] = src[r * SIN];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[i][r] = buf[pad<L>(b + r * NB)];
+      }
     }
   }
   line_sync(bar, T);
@@ -367,8 +377,18 @@ __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ 
         dft_odd_store<R, S, L>(v[i], buf, base, Ns);
       } else {
         dft<R, S>(v[i]);
+        // Ns % 8 == 0: pad(base + r Ns) = pad(base) + r Ns 9/8; Ns == 1, R == 8:
+        // pad(8b + r) = 9b + r
+        constexpr bool LIN_OUT = (L & 1) || (Ns % 8 == 0) || (Ns == 1 && R == 8);
+        constexpr int SOUT = (L & 1) ? Ns : (Ns % 8 == 0 ? Ns + Ns / 8 : 1);
+        if constexpr (LIN_OUT) {
+          double2* dst = buf + pad<L>(base);
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[pad<L>(base + r * Ns)] = v[i][r];
+          for (int r = 0; r < R; ++r) dst[r * SOUT] = v[i][r];
+        } else {
+#pragma unroll
+          for (int r = 0; r < R; ++r) buf[pad<L>(base + r * Ns)] = v[i][r];
+        }
       }
     }
   }
