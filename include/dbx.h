@@ -114,6 +114,42 @@ int dbx_plan_set_fusion(dbx_plan* plan, int enable);
 int dbx_plan_engines(dbx_plan* plan, int* conv, int* dst);
 
 /*
+ * Row-slab building blocks (one very large image split into row slabs across
+ * ranks; orchestrated by paper_1211_0393_b200/slab.py with NCCL
+ * halo exchange and all-to-all transposes).  The plan is created for one slab:
+ * n1 = slab rows, n2 = full width, batch = 1.  Device pointers only.
+ *
+ * dbx_slab_blur: y = A x (adjoint = 0) or A' x on the slab's rows, from the
+ *   caller-extended slab x_ext of (n1 + 2 q1) x n2 rows (q1 halo rows from the
+ *   neighbours, or the global AR extension rows at the image's top/bottom);
+ *   the horizontal AR extension is applied here.  g != NULL: y = g - A x and
+ *   *norm2 = ||y||^2 (fixed-order sum).  Replaces apply / apply_reblur_adjoint
+ *   (blur.hpp:75-90) restricted to a slab.
+ * dbx_slab_rows: the AR transform `kind` along every row of the slab with an
+ *   epilogue: DBX_SLAB_STORE (y = T x), DBX_SLAB_HADAMARD (y = aux o T x),
+ *   DBX_SLAB_AXPY (y = aux + tau T x, norms2 = {||y||^2, ||y - f||^2}).
+ * dbx_precond_block: block [r0, r0+nr) x [c0, c0+nc) of the n1g x n2g Tikhonov
+ *   filter grid of the plan's symmetrised mask (transpose = 1: stored nc x nr).
+ * dbx_transpose: out (cols x rows) = in (rows x cols)^T.
+ * dbx_slab_extend: x_ext = [top; x; bot] ((n1 + 2 q1) x n2); top / bot = NULL
+ *   at the image's first / last slab: the global AR extension rows
+ *   (boundary.hpp:58-61) are synthesised from x instead.
+ * dbx_slab_pack: blocks[p] = x[:, p cb : (p+1) cb] (cb = n2 / parts, each block
+ *   n1 x cb contiguous) for the all-to-all transpose; unpack = 1 the inverse.
+ */
+#define DBX_SLAB_STORE 0
+#define DBX_SLAB_HADAMARD 1
+#define DBX_SLAB_AXPY 2
+int dbx_slab_blur(dbx_plan* plan, const double* x_ext, double* y, int adjoint, const double* g, double* norm2);
+int dbx_slab_rows(dbx_plan* plan, int kind, const double* x, double* y, int epi, const double* aux,
+                  const double* f, double tau, double* norms2);
+int dbx_precond_block(dbx_plan* plan, int n1g, int n2g, double alpha, int r0, int nr, int c0, int nc,
+                      int transpose, double* out);
+int dbx_transpose(dbx_plan* plan, const double* in, double* out, int rows, int cols);
+int dbx_slab_extend(dbx_plan* plan, const double* x, const double* top, const double* bot, double* x_ext);
+int dbx_slab_pack(dbx_plan* plan, const double* x, double* blocks, int parts, int unpack);
+
+/*
  * Pipeline used by the last dbx_landweber_run on this plan: *fused = 1 for the
  * fused row pipelines (6 launches + finalize per preconditioned iteration,
  * fused.cu), 0 for the separate passes.  Diagnostic; no reference equivalent.

@@ -743,6 +743,169 @@ int dbx_precond_build(dbx_plan* P, double alpha) {
   });
 }
 
+// ---------------------------------------------------------------------------
+// Row-slab building blocks (C5 multi-GPU decomposition, slab.py).  The plan is
+// created for ONE slab (n1 = slab rows, n2 = full width, batch 1); all
+// pointers are device pointers; the caller supplies halos / transposes.
+// ---------------------------------------------------------------------------
+static void sum_partials(dbx_plan* P, int slot, int cnt, double* out) {
+  std::vector<double> h((size_t)cnt);
+  ck(cudaMemcpyAsync(h.data(), P->part.p + (size_t)slot * P->part_cap, cnt * sizeof(double),
+                     cudaMemcpyDeviceToHost, P->stream), "D2H");
+  ck(cudaStreamSynchronize(P->stream), "sync");
+  double acc = 0.0;
+  for (double v : h) acc += v;  // fixed order
+  *out = acc;
+}
+
+int dbx_slab_blur(dbx_plan* P, const double* x_ext, double* y, int adjoint, const double* g, double* norm2) {
+  return guarded([&] {
+    require(P && x_ext && y, "slab_blur: null argument");
+    require(P->batch == 1, "slab_blur: one slab per plan");
+    require(is_device_ptr(x_ext) && is_device_ptr(y) && (!g || is_device_ptr(g)), "slab_blur: device pointers");
+    require(P->use_fft_conv(), "slab_blur: needs the FFT correlation engine");
+    P->set_dev();
+    P->ensure_conv();
+    P->zb.ensure((size_t)(P->n1 + 2 * P->q1) * P->Lh * 2);
+    P->part.ensure((size_t)NUM_SLOTS * P->part_cap);
+    Partials pt{P->part.p, P->part_cap};
+    SpecArgs a = P->spec_base(nullptr, pt);
+    a.conv.tw1 = reinterpret_cast<const double2*>(P->tw1);
+    a.conv.tw2 = reinterpret_cast<const double2*>(P->tw2);
+    a.conv.H = reinterpret_cast<const double2*>(adjoint ? P->HAt : P->HA);
+    a.conv.L1 = P->L1; a.conv.L2 = P->L2; a.conv.Lh = P->Lh;
+    a.zbuf = reinterpret_cast<double2*>(P->zb.p);
+    a.ybuf = reinterpret_cast<double2*>(P->yb.p);
+    // rows of the caller-extended slab (halo rows / global AR rows included)
+    a.in = x_ext;
+    a.n1 = P->n1 + 2 * P->q1;
+    lc(launch_conv_row_fwd(a, P->stream), "launch_conv_row_fwd");
+    a.n1 = P->n1;
+    a.preext = 1;
+    lc(launch_conv_col(a, P->stream), "launch_conv_col");
+    a.preext = 0;
+    a.out = y;
+    a.epi = g ? SPEC_RESID : SPEC_STORE;
+    a.g = g;
+    const int ctas = lc(launch_conv_row_inv(a, P->stream), "launch_conv_row_inv");
+    P->launches += 3;
+    P->check_launch();
+    if (g && norm2) sum_partials(P, SLOT_R2, ctas, norm2);
+    ck(cudaStreamSynchronize(P->stream), "sync");
+  });
+}
+
+int dbx_slab_rows(dbx_plan* P, int kind, const double* x, double* y, int epi, const double* aux, const double* f,
+                  double tau, double* norms2) {
+  return guarded([&] {
+    require(P && x && y, "slab_rows: null argument");
+    require(P->batch == 1, "slab_rows: one slab per plan");
+    require(kind == DBX_KIND_SINEI || kind == DBX_KIND_AR || kind == DBX_KIND_ARINV, "slab_rows: unsupported kind");
+    require(epi == DBX_SLAB_STORE || epi == DBX_SLAB_HADAMARD || epi == DBX_SLAB_AXPY, "slab_rows: unknown epilogue");
+    require(epi == DBX_SLAB_STORE || aux != nullptr, "slab_rows: missing operand");
+    require(is_device_ptr(x) && is_device_ptr(y), "slab_rows: device pointers");
+    const bool sine = kind == DBX_KIND_SINEI;
+    require(P->use_fft_dst(sine), "slab_rows: needs the FFT-form DST");
+    P->set_dev();
+    P->part.ensure((size_t)NUM_SLOTS * P->part_cap);
+    Partials pt{P->part.p, P->part_cap};
+    SpecArgs a = P->spec_base(nullptr, pt);
+    a.blue2 = P->blue_tables(1, sine);
+    a.in = x;
+    a.out = y;
+    a.kind1 = kind;
+    a.kind2 = -1;
+    a.epi = epi == DBX_SLAB_STORE ? SPEC_STORE : epi == DBX_SLAB_HADAMARD ? SPEC_HADAMARD : SPEC_AXPY;
+    a.d = epi == DBX_SLAB_HADAMARD ? aux : nullptr;
+    a.xold = epi == DBX_SLAB_AXPY ? aux : nullptr;
+    a.f = epi == DBX_SLAB_AXPY ? f : nullptr;
+    a.tau = tau;
+    const int ctas = lc(launch_dst_rows(a, P->stream), "launch_dst_rows");
+    ++P->launches;
+    P->check_launch();
+    if (epi == DBX_SLAB_AXPY && norms2) {
+      sum_partials(P, SLOT_X2, ctas, norms2);
+      if (f) sum_partials(P, SLOT_XF2, ctas, norms2 + 1);
+      else norms2[1] = 0.0;
+    }
+    ck(cudaStreamSynchronize(P->stream), "sync");
+  });
+}
+
+int dbx_precond_block(dbx_plan* P, int n1g, int n2g, double alpha, int r0, int nr, int c0, int nc, int transpose,
+                      double* out) {
+  return guarded([&] {
+    require(P && out, "precond_block: null argument");
+    require(alpha >= 0.0, "tikhonov_filter: alpha must be nonnegative");
+    require(n1g >= 3 && n2g >= 3 && P->q1 <= n1g - 2 && P->q2 <= n2g - 2, "eig_antireflective: support condition");
+    require(r0 >= 0 && nr > 0 && r0 + nr <= n1g && c0 >= 0 && nc > 0 && c0 + nc <= n2g, "precond_block: block");
+    require(is_device_ptr(out), "precond_block: device pointer");
+    P->set_dev();
+    int* flag = nullptr;
+    ck(cudaMalloc(&flag, sizeof(int)), "cudaMalloc");
+    ck(cudaMemsetAsync(flag, 0, sizeof(int), P->stream), "memset");
+    launch_build_filter_block(P->sym, P->q1, P->q2, n1g, n2g, alpha, r0, nr, c0, nc, transpose != 0, out, flag,
+                              P->stream);
+    P->launches += 3;
+    P->check_launch();
+    int hflag = 0;
+    ck(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, P->stream), "D2H");
+    ck(cudaStreamSynchronize(P->stream), "sync");
+    cudaFree(flag);
+    require(alpha > 0.0 || hflag == 0, "tikhonov_filter: alpha = 0 with a zero eigenvalue");
+  });
+}
+
+int dbx_slab_extend(dbx_plan* P, const double* x, const double* top, const double* bot, double* x_ext) {
+  return guarded([&] {
+    require(P && x && x_ext, "slab_extend: null argument");
+    require(is_device_ptr(x) && is_device_ptr(x_ext) && (!top || is_device_ptr(top)) && (!bot || is_device_ptr(bot)),
+            "slab_extend: device pointers");
+    require(P->n1 >= P->q1 + 1, "slab_extend: slab must hold at least q1 + 1 rows");
+    P->set_dev();
+    const size_t row = (size_t)P->n2 * sizeof(double), q = (size_t)P->q1;
+    cudaStream_t s = P->stream;
+    ck(cudaMemcpyAsync(x_ext + q * P->n2, x, row * P->n1, cudaMemcpyDeviceToDevice, s), "copy");
+    if (top) ck(cudaMemcpyAsync(x_ext, top, row * q, cudaMemcpyDeviceToDevice, s), "copy");
+    if (bot) ck(cudaMemcpyAsync(x_ext + (q + P->n1) * P->n2, bot, row * q, cudaMemcpyDeviceToDevice, s), "copy");
+    launch_slab_ar_rows(x, x_ext, P->n1, P->n2, P->q1, top == nullptr, bot == nullptr, s);
+    ++P->launches;
+    P->check_launch();
+    ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+int dbx_slab_pack(dbx_plan* P, const double* x, double* blocks, int parts, int unpack) {
+  return guarded([&] {
+    require(P && x && blocks && parts > 0 && P->n2 % parts == 0, "slab_pack: bad argument");
+    require(is_device_ptr(x) && is_device_ptr(blocks), "slab_pack: device pointers");
+    P->set_dev();
+    const size_t cb = (size_t)P->n2 / parts, w = cb * sizeof(double), pitch = (size_t)P->n2 * sizeof(double);
+    for (int p = 0; p < parts; ++p) {
+      double* blk = blocks + (size_t)p * P->n1 * cb;
+      const double* col = x + (size_t)p * cb;
+      if (unpack)
+        ck(cudaMemcpy2DAsync(const_cast<double*>(col), pitch, blk, w, w, P->n1, cudaMemcpyDeviceToDevice, P->stream),
+           "unpack");
+      else
+        ck(cudaMemcpy2DAsync(blk, w, col, pitch, w, P->n1, cudaMemcpyDeviceToDevice, P->stream), "pack");
+    }
+    ck(cudaStreamSynchronize(P->stream), "sync");
+  });
+}
+
+int dbx_transpose(dbx_plan* P, const double* in, double* out, int rows, int cols) {
+  return guarded([&] {
+    require(P && in && out && rows > 0 && cols > 0, "transpose: bad argument");
+    require(is_device_ptr(in) && is_device_ptr(out), "transpose: device pointers");
+    P->set_dev();
+    launch_transpose(in, out, rows, cols, P->stream);
+    ++P->launches;
+    P->check_launch();
+    ck(cudaStreamSynchronize(P->stream), "sync");
+  });
+}
+
 int dbx_precond_eigs(dbx_plan* P, double* d_out) {
   return guarded([&] {
     require(P && d_out, "null argument");

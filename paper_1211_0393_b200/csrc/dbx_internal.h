@@ -89,6 +89,8 @@ void launch_gemm(const GemmArgs& a, cudaStream_t s, int* ctas_per_image);
 // ---- spectrum, norms, finalize -----------------------------------------
 void launch_build_filter(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha,
                          double* d, int* zero_flag, cudaStream_t s);
+void launch_build_filter_block(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha, int r0,
+                               int nr, int c0, int nc, int tr, double* d, int* zero_flag, cudaStream_t s);
 void launch_norms_init(const double* g, const double* f, int batch, size_t N, ImgState* st,
                        double* scratch, cudaStream_t s);
 struct FinalizeArgs {
@@ -108,6 +110,7 @@ void launch_state_init(ImgState* st, int batch, cudaStream_t s);
 void launch_select_copy(const double* X3, const ImgState* st, int which_best, int batch,
                         size_t N, double* out, cudaStream_t s);
 void launch_zero(double* p, size_t n, cudaStream_t s);
+void launch_slab_ar_rows(const double* x, double* ext, int rows, int n2, int q, int top, int bot, cudaStream_t s);
 void launch_transpose(const double* in, double* out, int rows, int cols, cudaStream_t s);
 
 }  // namespace dbx

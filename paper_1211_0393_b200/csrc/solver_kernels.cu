@@ -32,16 +32,21 @@ __global__ void cos_table_kernel(int n, int q, double* tab) {
 
 // d(a,b) = 1 / (lambda^2 + alpha), lambda = symbol_real(h_sym, x_a, x_b) with
 // the reference accumulation order: h00, axis-1 terms, axis-2 terms, cross.
+// Block [r0, r0+nr) x [c0, c0+nc) of the n1 x n2 grid; out row-major
+// (nr x nc), or transposed (nc x nr) when tr (a rank's d^T block for the
+// column pass of a row-slab decomposition).
 __global__ void filter_kernel(const double* __restrict__ h, int q1, int q2, int n1, int n2,
                               const double* __restrict__ c1, const double* __restrict__ c2,
-                              double alpha, double* __restrict__ d, int* zero_flag) {
+                              double alpha, double* __restrict__ d, int* zero_flag,
+                              int r0, int nr, int c0, int nc, int tr) {
   extern __shared__ double hs[];
   const int wq = 2 * q2 + 1;
   for (int i = threadIdx.x; i < (2 * q1 + 1) * wq; i += blockDim.x) hs[i] = h[i];
   __syncthreads();
-  const int bcol = blockIdx.x * blockDim.x + threadIdx.x;
-  const int arow = blockIdx.y;
-  if (bcol >= n2) return;
+  const int bl = blockIdx.x * blockDim.x + threadIdx.x;
+  const int bcol = c0 + bl;
+  const int arow = r0 + blockIdx.y;
+  if (bl >= nc) return;
   const double* C1 = c1 + (size_t)arow * (q1 + 1);
   const double* C2 = c2 + (size_t)bcol * (q2 + 1);
   auto tap = [&](int s1, int s2) { return hs[(q1 + s1) * wq + (q2 + s2)]; };
@@ -54,7 +59,8 @@ __global__ void filter_kernel(const double* __restrict__ h, int q1, int q2, int 
   }
   const double m2 = acc * acc;
   if (!(m2 > 0.0)) atomicOr(zero_flag, 1);
-  d[(size_t)arow * n2 + bcol] = 1.0 / (m2 + alpha);
+  const size_t at = tr ? (size_t)bl * nr + blockIdx.y : (size_t)blockIdx.y * nc + bl;
+  d[at] = 1.0 / (m2 + alpha);
 }
 
 // Fixed-order block reduction (deterministic).
@@ -178,6 +184,18 @@ __global__ void transpose_kernel(const double* __restrict__ in, double* __restri
   }
 }
 
+// Global AR extension rows of a slab (boundary.hpp:58-61 along axis 1):
+// top: ext[i] = 2 x[0] - x[q - i] (i < q); bottom: ext[q + rows + k - 1] =
+// 2 x[rows-1] - x[rows-1-k] (k = 1..q).
+__global__ void slab_ar_rows_kernel(const double* __restrict__ x, double* __restrict__ ext, int rows, int n2,
+                                    int q, int top, int bot) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.y + 1;  // 1..q
+  if (c >= n2) return;
+  if (top) ext[(size_t)(q - k) * n2 + c] = 2.0 * x[c] - x[(size_t)k * n2 + c];
+  if (bot) ext[(size_t)(q + rows + k - 1) * n2 + c] = 2.0 * x[(size_t)(rows - 1) * n2 + c] - x[(size_t)(rows - 1 - k) * n2 + c];
+}
+
 __global__ void zero_kernel(double* p, size_t n) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
@@ -188,6 +206,11 @@ __global__ void zero_kernel(double* p, size_t n) {
 
 void launch_build_filter(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha,
                          double* d, int* zero_flag, cudaStream_t s) {
+  launch_build_filter_block(sym_taps, q1, q2, n1, n2, alpha, 0, n1, 0, n2, 0, d, zero_flag, s);
+}
+
+void launch_build_filter_block(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha, int r0,
+                               int nr, int c0, int nc, int tr, double* d, int* zero_flag, cudaStream_t s) {
   double *c1 = nullptr, *c2 = nullptr;
   cudaMallocAsync(&c1, sizeof(double) * (size_t)n1 * (q1 + 1), s);
   cudaMallocAsync(&c2, sizeof(double) * (size_t)n2 * (q2 + 1), s);
@@ -196,8 +219,8 @@ void launch_build_filter(const double* sym_taps, int q1, int q2, int n1, int n2,
   const size_t sm = sizeof(double) * (2 * q1 + 1) * (2 * q2 + 1);
   if (sm > 48 * 1024)
     cudaFuncSetAttribute(filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 grid((n2 + 127) / 128, n1);
-  filter_kernel<<<grid, 128, sm, s>>>(sym_taps, q1, q2, n1, n2, c1, c2, alpha, d, zero_flag);
+  dim3 grid((nc + 127) / 128, nr);
+  filter_kernel<<<grid, 128, sm, s>>>(sym_taps, q1, q2, n1, n2, c1, c2, alpha, d, zero_flag, r0, nr, c0, nc, tr);
   cudaFreeAsync(c1, s);
   cudaFreeAsync(c2, s);
 }
@@ -224,6 +247,12 @@ void launch_select_copy(const double* X3, const ImgState* st, int which_best, in
 void launch_transpose(const double* in, double* out, int rows, int cols, cudaStream_t s) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32);
   transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols);
+}
+
+void launch_slab_ar_rows(const double* x, double* ext, int rows, int n2, int q, int top, int bot, cudaStream_t s) {
+  if (q <= 0 || !(top || bot)) return;
+  dim3 grid((n2 + 255) / 256, q);
+  slab_ar_rows_kernel<<<grid, 256, 0, s>>>(x, ext, rows, n2, q, top, bot);
 }
 
 void launch_zero(double* p, size_t n, cudaStream_t s) {

@@ -157,7 +157,9 @@ conv_col(SpecArgs a) {
       const int p = idx / G, gg = idx - p * G;
       const int k = k0 + gg;
       v[i] = make_double2(0.0, 0.0);
-      if (idx < L1 * G && k < Lh && p < hext_rows) {
+      if (idx < L1 * G && k < Lh && p < hext_rows && a.preext) {
+        v[i] = Z[(size_t)p * Lh + k];  // row slab: halo / global AR rows supplied by the caller
+      } else if (idx < L1 * G && k < Lh && p < hext_rows) {
         const int rho = p - q1;
         if (rho < 0) {
           const double2 z0 = Z[k], zi = Z[(size_t)(-rho) * Lh + k];

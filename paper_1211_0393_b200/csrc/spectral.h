@@ -59,6 +59,7 @@ struct SpecArgs {
   double2* zbuf = nullptr;                       // [batch][n1][Lh], or [batch][Lh][n1] if ztrans
   double2* ybuf = nullptr;                       // [batch][n1][Lh]
   int ztrans = 0;                                // fused pipeline: row-FFT spectra stored transposed
+  int preext = 0;                                // conv_col: n1 + 2 q1 input rows already extended (row slabs)
   const double* dT = nullptr;                    // d transposed [n2][n1] (fused column pass)
   // DST
   int kind1 = DBX_KIND_ARINV, kind2 = -1;

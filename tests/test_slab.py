@@ -1,0 +1,118 @@
+"""Row-slab decomposition of one image: the exchange layer
+over gloo (world size 2, CPU) against the in-process LocalWorld, and — on the
+GPU — the slab D-Landweber (P simulated ranks in one process) against the
+single-image path, which tests/test_gpu_parity.py pins to the oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_1211_0393_b200.slab import LocalWorld, slab_rows_of
+
+
+def test_slab_rows_validation():
+    assert slab_rows_of(8192, 8, 15) == 1024
+    with pytest.raises(ValueError):
+        slab_rows_of(100, 3, 2)
+    with pytest.raises(ValueError):
+        slab_rows_of(64, 8, 8)  # 8 rows < q + 1
+
+
+def _local_reference(P, n, q, seed):
+    rng = np.random.default_rng(seed)
+    slabs = {p: torch.from_numpy(rng.uniform(size=(n // P, n))) for p in range(P)}
+    w = LocalWorld(P)
+    tops, bots = w.halo({p: s[:q].contiguous() for p, s in slabs.items()},
+                        {p: s[-q:].contiguous() for p, s in slabs.items()})
+    sends = {p: torch.from_numpy(rng.uniform(size=n * n // P)) for p in range(P)}
+    recvs = {p: torch.zeros(n * n // P, dtype=torch.float64) for p in range(P)}
+    w.alltoall(sends, recvs)
+    return slabs, tops, bots, sends, recvs
+
+
+def test_local_world_exchanges():
+    P, n, q = 4, 16, 2
+    slabs, tops, bots, sends, recvs = _local_reference(P, n, q, 1)
+    full = torch.cat([slabs[p] for p in range(P)])
+    R = n // P
+    for p in range(P):
+        if p > 0:
+            assert torch.equal(tops[p], full[p * R - q:p * R])
+        else:
+            assert tops[p] is None
+        if p + 1 < P:
+            assert torch.equal(bots[p], full[(p + 1) * R:(p + 1) * R + q])
+        else:
+            assert bots[p] is None
+    c = n * n // P // P
+    for p in range(P):
+        for s in range(P):
+            assert torch.equal(recvs[s][p * c:(p + 1) * c], sends[p][s * c:(s + 1) * c])
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_1211_0393_b200.slab import DistWorld
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 12
+    slabs, tops, bots, sends, recvs = _local_reference(world, n, q, 7)
+    w = DistWorld()
+    t, b = w.halo({rank: slabs[rank][:q].contiguous()}, {rank: slabs[rank][-q:].contiguous()})
+    assert (t[rank] is None) == (tops[rank] is None) and (b[rank] is None) == (bots[rank] is None)
+    if t[rank] is not None:
+        assert torch.equal(t[rank], tops[rank])
+    if b[rank] is not None:
+        assert torch.equal(b[rank], bots[rank])
+    out = {rank: torch.zeros_like(recvs[rank])}
+    w.alltoall({rank: sends[rank]}, out)
+    assert torch.equal(out[rank], recvs[rank])
+    tot = w.allreduce({rank: [float(rank + 1), 2.0]})
+    assert tot == [float(world * (world + 1) // 2), 2.0 * world]
+    dist.destroy_process_group()
+
+
+def test_dist_world_matches_local_gloo():
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), 2), nprocs=world, join=True)
+
+
+# ---------------------------------------------------------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_slab_landweber_matches_single_image(dbx, P):
+    from paper_1211_0393_b200 import configs as cf
+    from paper_1211_0393_b200.slab import SlabLandweber
+    c = cf.CONFIGS["C5"]
+    n, iters = 256, 6
+    f, g, taps = cf.make_problem(c, n=n)
+    op = dbx.BlurOperator(dbx.Psf(taps), dbx.BoundaryCondition.AntiReflective, n, n)
+    d = dbx.build_tikhonov(dbx.Psf(taps), dbx.PreconditionerSpec(dbx.Algebra.AntiReflective, c.alpha), n, n)
+    ref = dbx.d_landweber(op, d, g, dbx.SolverConfig(max_iters=iters, track_rre_against=f))
+    R = n // P
+    dev = torch.device("cuda", 0)
+    gs = {p: torch.from_numpy(np.ascontiguousarray(g[p * R:(p + 1) * R])).to(dev) for p in range(P)}
+    fs = {p: torch.from_numpy(np.ascontiguousarray(f[p * R:(p + 1) * R])).to(dev) for p in range(P)}
+    solver = SlabLandweber(LocalWorld(P), n, taps, c.q, c.alpha, device=0)
+    try:
+        run = solver.run(gs, fs, iters)
+    finally:
+        solver.close()
+    assert run["iterations_executed"] == ref.iterations_executed
+    assert run["best_iteration"] == ref.best_iteration
+    np.testing.assert_allclose(run["residual_history"], ref.residual_history, rtol=1e-10, atol=0)
+    np.testing.assert_allclose(run["rre_history"], ref.rre_history, rtol=1e-10, atol=0)
+    restored = np.concatenate([run["restored"][p].cpu().numpy() for p in range(P)])
+    assert np.linalg.norm(restored - ref.restored) / np.linalg.norm(ref.restored) <= 1e-10
