@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--images", type=int, default=0, help="override images per rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--slab", action="store_true",
+                    help="row-slab decomposition of one image (default for C5 at N > 1)")
     return ap.parse_args()
 
 
@@ -162,10 +164,79 @@ def run_reference(args):
     return 0
 
 
+def run_slab(args):
+    """One image split into row slabs across the ranks (C5):
+    NCCL halo exchange for the blur and all-to-all transposes for the column
+    DST; strong scaling (the image is fixed)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1211_0393_b200 import configs as cf
+    from paper_1211_0393_b200.slab import DistWorld, LocalWorld, SlabLandweber
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = cf.CONFIGS[args.config]
+    n, q, H = cfg.n, cfg.q, cfg.iters
+    F, G, taps = cf.make_batch(cfg, 1)
+    R = n // world
+    dev = torch.device("cuda", local)
+    g = {rank: torch.from_numpy(np.ascontiguousarray(G[0, rank * R:(rank + 1) * R])).to(dev)}
+    f = {rank: torch.from_numpy(np.ascontiguousarray(F[0, rank * R:(rank + 1) * R])).to(dev)}
+    del F, G
+    solver = SlabLandweber(DistWorld() if world > 1 else LocalWorld(1), n, taps, q, cfg.alpha, device=local)
+    for _ in range(args.warmup):
+        solver.run(g, f, H)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        solver.run(g, f, H)
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    px_it = n * n * H * args.steps
+    value = px_it / (t_max * 1e-3) / 1e6
+    solver.close()
+    if rank == 0:
+        hbm = float(json.load(open(HBM_FILE))["hbm_gbs"]) if os.path.exists(HBM_FILE) else 7700.0
+        gbs = 72.0 * px_it / (t_max * 1e-3) / 1e9 / world
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded scene/mask/noise, host-generated)",
+                "config": {"workload": f"{cfg.name}: one {n}x{n} FP64 image in {world} row slabs of {R} rows, "
+                                       f"q={q}, {H} D-Landweber iterations",
+                           "parallelism": f"row slabs x{world} (NCCL halo send/recv + all-to-all transposes)",
+                           "l2": "slab arrays exceed L2"},
+                "clocks": clk, "gpu_launches": None,
+                "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                             "traffic": None, "note": "SURVEY canonical 72 B per pixel-iteration, per GPU"},
+                "e2e": None, "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.slab or (args.config == "C5" and dist_env()[1] > 1):
+        return run_slab(args)
     import torch
     import torch.distributed as dist
 

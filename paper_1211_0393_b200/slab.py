@@ -153,11 +153,21 @@ class SlabLandweber:
             s.close()
 
     # ---- exchange helpers -------------------------------------------------
+    # The C-ABI calls run on each plan's own stream and synchronise it before
+    # returning; torch-side copies and NCCL transfers complete on torch's
+    # current stream, so that stream is synchronised before a kernel of the
+    # C-ABI reads what they produced (_fence).
+    @staticmethod
+    def _fence():
+        import torch
+        torch.cuda.current_stream().synchronize()
+
     def _extend(self, bufs: Dict[int, "object"]):
         q = self.q
         firsts = {p: bufs[p][:q].contiguous() for p in bufs}
         lasts = {p: bufs[p][-q:].contiguous() for p in bufs}
         tops, bots = self.world.halo(firsts, lasts)
+        self._fence()
         L = lib()
         for p, s in self.slabs.items():
             _check(L.dbx_slab_extend(s.plan, _ptr(bufs[p]), _ptr(tops[p]), _ptr(bots[p]), _ptr(s.ext)))
@@ -168,6 +178,7 @@ class SlabLandweber:
         for p, s in self.slabs.items():
             _check(L.dbx_slab_pack(s.plan, _ptr(src[p]), _ptr(s.send), P, 0))
         self.world.alltoall({p: s.send for p, s in self.slabs.items()}, {p: s.recv for p, s in self.slabs.items()})
+        self._fence()
         for p, s in self.slabs.items():  # recv = (n x C) rows stacked by source rank -> (C x n)
             _check(L.dbx_transpose(s.plan, _ptr(s.recv), _ptr(getattr(s, dst_attr)), self.n, s.cb))
 
@@ -176,6 +187,7 @@ class SlabLandweber:
         for p, s in self.slabs.items():
             _check(L.dbx_transpose(s.plan, _ptr(getattr(s, src_attr)), _ptr(s.send), s.cb, self.n))
         self.world.alltoall({p: s.send for p, s in self.slabs.items()}, {p: s.recv for p, s in self.slabs.items()})
+        self._fence()
         for p, s in self.slabs.items():
             _check(L.dbx_slab_pack(s.plan, _ptr(dst[p]), _ptr(s.recv), P, 1))
 
@@ -194,6 +206,7 @@ class SlabLandweber:
         for p, s in S.items():
             s.x.zero_()
             s.r.copy_(g[p])
+        self._fence()
         rre, res = [], []
         best_rre, best_iter, done = math.inf, 0, 0
         for k in range(1, iters + 1):
@@ -235,9 +248,11 @@ class SlabLandweber:
                     best_rre, best_iter = e, k
                     for s in S.values():
                         s.best.copy_(s.x)
+                    self._fence()
             done = k
             if resid_eps is not None and gnorm > 0.0 and math.sqrt(rr) / gnorm < resid_eps:
                 break
         restored = {p: (s.best if (f and best_iter > 0) else s.x).clone() for p, s in S.items()}
+        self._fence()
         return {"restored": restored, "iterations_executed": done, "best_iteration": best_iter,
                 "rre_history": rre, "residual_history": res}

@@ -91,12 +91,13 @@ def test_dist_world_matches_local_gloo():
 
 # ---------------------------------------------------------------------------
 @pytest.mark.gpu
-@pytest.mark.parametrize("P", [1, 2, 4])
-def test_slab_landweber_matches_single_image(dbx, P):
+@pytest.mark.parametrize("P,n,iters", [(1, 256, 6), (2, 256, 6), (4, 256, 6), (2, 8192, 3)])
+def test_slab_landweber_matches_single_image(dbx, P, n, iters):
+    """Scaled C5 problem (mask, shapes, noise, alpha) at 256^2 with 1/2/4
+    simulated ranks, and the full 8192^2 FOV with 2 (Rader DSTs, conv 8640)."""
     from paper_1211_0393_b200 import configs as cf
     from paper_1211_0393_b200.slab import SlabLandweber
     c = cf.CONFIGS["C5"]
-    n, iters = 256, 6
     f, g, taps = cf.make_problem(c, n=n)
     op = dbx.BlurOperator(dbx.Psf(taps), dbx.BoundaryCondition.AntiReflective, n, n)
     d = dbx.build_tikhonov(dbx.Psf(taps), dbx.PreconditionerSpec(dbx.Algebra.AntiReflective, c.alpha), n, n)
