@@ -494,12 +494,31 @@ struct dbx_plan {
       a.in = X; a.insel = xsel; a.out = u.p; a.outsel = SEL_EXPLICIT; a.kind1 = DBX_KIND_ARINV;
       a.epi = SPEC_STORE;
       ev_begin(KC_TRANSFORM); lc(launch_dst_rows(a, stream), "launch_dst_rows"); ev_end();
-      // T~ -> d -> T along columns
-      a.in = u.p; a.insel = SEL_EXPLICIT; a.out = s.p; a.outsel = SEL_EXPLICIT;
-      a.kind1 = DBX_KIND_ARINV; a.kind2 = DBX_KIND_AR;
-      ev_begin(KC_TRANSFORM); lc(launch_dst_cols(a, stream), "launch_dst_cols"); ev_end();
+      // T~ -> d -> T along columns, on the transposed images (columns become
+      // contiguous rows: coalesced lines instead of 2-4 column row segments)
+      const double* colout = s.p;
+      if (dT.p) {
+        ev_begin(KC_TRANSFORM);
+        launch_transpose(u.p, s.p, n1, n2, stream, batch);
+        SpecArgs c = a;
+        c.n1 = n2; c.n2 = n1;
+        c.blue2 = blue_tables(0, false);
+        c.in = s.p; c.out = u.p; c.kind1 = DBX_KIND_ARINV; c.epi = SPEC_HADAMARD; c.d = dT.p;
+        c.st = stp; c.part = Partials{nullptr, 0};
+        lc(launch_dst_rows(c, stream), "launch_dst_rows");
+        c.in = u.p; c.out = s.p; c.kind1 = DBX_KIND_AR; c.epi = SPEC_STORE; c.d = nullptr;
+        lc(launch_dst_rows(c, stream), "launch_dst_rows");
+        launch_transpose(s.p, u.p, n2, n1, stream, batch);
+        ev_end();
+        launches += 4;
+        colout = u.p;
+      } else {
+        a.in = u.p; a.insel = SEL_EXPLICIT; a.out = s.p; a.outsel = SEL_EXPLICIT;
+        a.kind1 = DBX_KIND_ARINV; a.kind2 = DBX_KIND_AR;
+        ev_begin(KC_TRANSFORM); lc(launch_dst_cols(a, stream), "launch_dst_cols"); ev_end();
+      }
       // T along rows + epilogue
-      a.in = s.p; a.insel = SEL_EXPLICIT; a.out = Y; a.outsel = ysel; a.kind1 = DBX_KIND_AR; a.kind2 = -1;
+      a.in = colout; a.insel = SEL_EXPLICIT; a.out = Y; a.outsel = ysel; a.kind1 = DBX_KIND_AR; a.kind2 = -1;
       a.epi = epi_spec; a.xold = xold; a.xoldsel = xoldsel; a.f = ff; a.tau = tau;
       ev_begin(KC_TRANSFORM);
       const int ctas = lc(launch_dst_rows(a, stream), "launch_dst_rows");

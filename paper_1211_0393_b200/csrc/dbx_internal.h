@@ -111,6 +111,6 @@ void launch_select_copy(const double* X3, const ImgState* st, int which_best, in
                         size_t N, double* out, cudaStream_t s);
 void launch_zero(double* p, size_t n, cudaStream_t s);
 void launch_slab_ar_rows(const double* x, double* ext, int rows, int n2, int q, int top, int bot, cudaStream_t s);
-void launch_transpose(const double* in, double* out, int rows, int cols, cudaStream_t s);
+void launch_transpose(const double* in, double* out, int rows, int cols, cudaStream_t s, int batch = 1);
 
 }  // namespace dbx

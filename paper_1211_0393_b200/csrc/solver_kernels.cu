@@ -173,6 +173,9 @@ __global__ void select_copy_kernel(const double* X3, const ImgState* st, int whi
 __global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out, int rows, int cols) {
   __shared__ double tile[32][33];
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const size_t img = (size_t)blockIdx.z * rows * cols;  // batch of matrices
+  in += img;
+  out += img;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int r = r0 + i, c = c0 + threadIdx.x;
     if (r < rows && c < cols) tile[i][threadIdx.x] = in[(size_t)r * cols + c];
@@ -244,8 +247,8 @@ void launch_select_copy(const double* X3, const ImgState* st, int which_best, in
   select_copy_kernel<<<grid, 256, 0, s>>>(X3, st, which_best, batch, N, out);
 }
 
-void launch_transpose(const double* in, double* out, int rows, int cols, cudaStream_t s) {
-  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+void launch_transpose(const double* in, double* out, int rows, int cols, cudaStream_t s, int batch) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32, batch);
   transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols);
 }
 
