@@ -109,10 +109,17 @@ __device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, 
   }
   fft::line_sync(bar, T);
   fft::fft<L2, -1, T>(buf, tw, t, bar);
+  const bool pair = has_b && ((ra | n1) & 1) == 0;  // rows ra, ra+1 adjacent and 32-byte aligned
   for (int k = t; k < Lh; k += T) {
     const double2 zk = buf[pad<L2>(k)], zm = buf[pad<L2>(k == 0 ? 0 : L2 - k)];
-    if (has_a) Z[(size_t)k * n1 + ra] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-    if (has_b) Z[(size_t)k * n1 + rb] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+    const double2 za = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    const double2 zb = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+    if (pair) {
+      st_pair(Z + (size_t)k * n1 + ra, za, zb);
+    } else {
+      if (has_a) Z[(size_t)k * n1 + ra] = za;
+      if (has_b) Z[(size_t)k * n1 + rb] = zb;
+    }
   }
 }
 
@@ -388,10 +395,17 @@ __global__ void __launch_bounds__(RsCfg<L2>::NT, 2) rows_ainv_resid(SpecArgs a) 
   fft::line_sync(bar, T);
   fft::fft<L2, -1, T>(buf, twc, t, bar);
   double2* Z = a.zbuf + (size_t)b * n1 * Lh;
+  const bool pair = has_b && ((ra | n1) & 1) == 0;
   for (int k = t; k < Lh; k += T) {
     const double2 zk = buf[pad<L2>(k)], zm = buf[pad<L2>(k == 0 ? 0 : L2 - k)];
-    if (has_a) Z[(size_t)k * n1 + ra] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-    if (has_b) Z[(size_t)k * n1 + rb] = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+    const double2 za = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    const double2 zb = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+    if (pair) {
+      st_pair(Z + (size_t)k * n1 + ra, za, zb);
+    } else {
+      if (has_a) Z[(size_t)k * n1 + ra] = za;
+      if (has_b) Z[(size_t)k * n1 + rb] = zb;
+    }
   }
   if (a.part.p) {
     double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;

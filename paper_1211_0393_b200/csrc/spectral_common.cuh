@@ -92,6 +92,13 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// One 32-byte global store of two adjacent complex values (sm_100 256-bit
+// STG): the half spectra of a packed row pair go out as one full sector.
+__device__ __forceinline__ void st_pair(double2* p, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+               : "memory");
+}
+
 // Number of SMs (for prefetch-ahead distances of one resident wave).
 __device__ __forceinline__ int nsm() {
   unsigned r;
