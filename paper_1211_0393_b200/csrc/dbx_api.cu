@@ -297,7 +297,7 @@ struct dbx_plan {
     HAt = upload_owned(conv_spectrum(taps.data(), q1, q2, L1, L2));
     (void)nt;
     zb.ensure((size_t)batch * n1 * Lh * 2);
-    yb.ensure((size_t)batch * n1 * Lh * 2);
+    yb.ensure((size_t)batch * n1 * y_stride(Lh) * 2);
     conv_ready = true;
   }
 

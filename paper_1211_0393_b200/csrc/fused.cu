@@ -70,8 +70,8 @@ __device__ __forceinline__ void conv_inv_load(double2* buf, const double2* __res
     A[i] = make_double2(0.0, 0.0);
     Bv[i] = A[i];
     if (k < Lh) {
-      if (ra < n1) A[i] = Y[(size_t)ra * Lh + k];
-      if (rb < n1) Bv[i] = Y[(size_t)rb * Lh + k];
+      if (ra < n1) A[i] = Y[(size_t)ra * y_stride(Lh) + k];
+      if (rb < n1) Bv[i] = Y[(size_t)rb * y_stride(Lh) + k];
     }
   }
 #pragma unroll
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
   PH_DECL
   // A' r rows: inverse packed row FFT (conv line g = rows 2g, 2g+1)
   double2* cbuf = sm + g * F::LC;
-  conv_inv_load<L2, TD>(cbuf, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t);
+  conv_inv_load<L2, TD>(cbuf, a.ybuf + (size_t)b * n1 * y_stride(Lh), ra, rb, n1, Lh, t);
   cp_async_wait_all();
   __syncthreads();
   PH(20)
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(RsCfg<L2>::NT, 2) rows_ainv_resid(SpecArgs a) 
   const int r0 = 4 * blockIdx.x, nl = n1 - r0 < 4 ? n1 - r0 : 4;
   stage_lines(gS, LS, a.g + (size_t)b * N + (size_t)r0 * n2, nl, n2);
   cp_async_commit();
-  conv_inv_load<L2, T>(buf, a.ybuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t);
+  conv_inv_load<L2, T>(buf, a.ybuf + (size_t)b * n1 * y_stride(Lh), ra, rb, n1, Lh, t);
   cp_async_wait_group<1>();  // twiddles
   __syncthreads();
   fft::fft<L2, +1, T>(buf, twc, t, bar);

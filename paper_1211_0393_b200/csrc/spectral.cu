@@ -191,10 +191,17 @@ conv_col(SpecArgs a) {
   fft::line_sync(G > 1 ? 1 + g : 0, T);
   fft::fft<L1, +1, T>(buf, tw, t, G > 1 ? 1 + g : 0);
   if (G > 1) __syncthreads();  // the stores interleave the CTA's lines
-  double2* Y = a.ybuf + (size_t)b * n1 * Lh;
-  for (int idx = threadIdx.x; idx < n1 * G; idx += NT) {
-    const int p = idx / G, gg = idx - p * G, k = k0 + gg;
-    if (k < Lh) Y[(size_t)p * Lh + k] = sm[gg * padded_len(L1) + pad<L1>(p)];
+  const int YS = y_stride(Lh);
+  double2* Y = a.ybuf + (size_t)b * n1 * YS;
+  if (G == 2 && k0 + 1 < Lh) {
+    // the CTA's two adjacent columns of one row: one 32-byte store
+    for (int p = threadIdx.x; p < n1; p += NT)
+      st_pair(Y + (size_t)p * YS + k0, sm[pad<L1>(p)], sm[padded_len(L1) + pad<L1>(p)]);
+  } else {
+    for (int idx = threadIdx.x; idx < n1 * G; idx += NT) {
+      const int p = idx / G, gg = idx - p * G, k = k0 + gg;
+      if (k < Lh) Y[(size_t)p * YS + k] = sm[gg * padded_len(L1) + pad<L1>(p)];
+    }
   }
 }
 
@@ -228,7 +235,7 @@ conv_row_inv(SpecArgs a) {
       }
     }
   }
-  const double2* Y = a.ybuf + (size_t)b * n1 * Lh;
+  const double2* Y = a.ybuf + (size_t)b * n1 * y_stride(Lh);
   // only the Lh stored spectra are read (the upper half is their conjugate);
   // loads batched in registers before the smem stores
   constexpr int PF = (L2 / 2 + 1 + T - 1) / T;
@@ -239,8 +246,8 @@ conv_row_inv(SpecArgs a) {
     A[i] = make_double2(0.0, 0.0);
     Bv[i] = A[i];
     if (k < Lh) {
-      if (ra < n1) A[i] = Y[(size_t)ra * Lh + k];
-      if (rb < n1) Bv[i] = Y[(size_t)rb * Lh + k];
+      if (ra < n1) A[i] = Y[(size_t)ra * y_stride(Lh) + k];
+      if (rb < n1) Bv[i] = Y[(size_t)rb * y_stride(Lh) + k];
     }
   }
 #pragma unroll

@@ -67,6 +67,10 @@ struct SpecArgs {
   BlueTables blue2;                              // rows (length n2)
 };
 
+// Row stride (complex elements) of the column-pass output Y: Lh rounded up to
+// even so a row pair of adjacent columns is one 32-byte aligned store.
+__host__ __device__ constexpr int y_stride(int Lh) { return (Lh + 1) & ~1; }
+
 int conv_supported_len(int need);   // smallest compiled L >= need, 0 if none
 int blue_supported_len(int need);   // smallest compiled power of two M >= need, 0 if none
 int conv_rows_per_cta(int L2);
