@@ -182,6 +182,16 @@ int dbx_precond_set_eigs(dbx_plan* plan, const double* d);
 
 /* y = D r = T (d o (T~ r)) for every image.  Replaces precondition_apply
  * (preconditioner.hpp:88-90) -> filter_apply AR branch (spectral.hpp:161-165). */
+/*
+ * Alpha sweep (experiment.hpp:182-265 runs one
+ * d_landweber cell per alpha): one Tikhonov filter grid per image of the
+ * batch, image b filtered with alphas[b] (host array of `batch` values), so
+ * the cells of a sweep run as one batched dbx_landweber_run.  A later
+ * dbx_precond_build / dbx_precond_set_eigs returns to one shared grid;
+ * dbx_precond_eigs reports image 0's grid.
+ */
+int dbx_precond_build_sweep(dbx_plan* plan, const double* alphas);
+
 int dbx_precond_apply(dbx_plan* plan, const double* r, double* y);
 
 /* 2D separable transform (columns then rows, transforms.hpp:179-192) of

@@ -83,6 +83,7 @@ def lib():
         L.dbx_gen_psf_motion.argtypes = [i, i, d, d, d, vp]
         L.dbx_gen_honest.argtypes = [vp, i, i, vp, i, i, i, i, d, C.c_uint64, i, vp, vp]
         L.dbx_add_noise.argtypes = [vp, i, i, d, C.c_uint64, vp]
+        L.dbx_precond_build_sweep.argtypes = [vp, vp]
         L.dbx_slab_blur.argtypes = [vp, vp, vp, i, vp, C.POINTER(d)]
         L.dbx_slab_rows.argtypes = [vp, i, vp, vp, i, vp, vp, d, C.POINTER(d)]
         L.dbx_precond_block.argtypes = [vp, i, i, d, i, i, i, i, i, vp]

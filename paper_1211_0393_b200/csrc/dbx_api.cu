@@ -193,7 +193,9 @@ struct dbx_plan {
   double* w_A = nullptr;   // weights of A (rotate180 of taps)
   double* w_At = nullptr;  // weights of A' (taps)
   double* sym = nullptr;   // symmetrised taps (psf.hpp:71-85)
-  double* d = nullptr;     // filter grid
+  double* d = nullptr;     // filter grid (one shared, or one per image for an alpha sweep)
+  size_t d_cap = 0;        // doubles allocated at d
+  size_t dstride = 0;      // 0: shared grid; N: per-image grids (dbx_precond_build_sweep)
   bool have_d = false;
   int conv = DBX_CONV_AUTO;
   // dense transform matrices [kind][0 col-matrix (n1), 1 row-matrix^T (n2)]
@@ -354,10 +356,19 @@ struct dbx_plan {
     SpecArgs a;
     a.n1 = n1; a.n2 = n2; a.q1 = q1; a.q2 = q2; a.batch = batch;
     a.st = stp; a.part = pt;
+    a.dstride = dstride;
     return a;
   }
 
   void set_dev() const { ck(cudaSetDevice(device), "cudaSetDevice"); }
+
+  void ensure_d(size_t count) {
+    if (d && d_cap >= count) return;
+    if (d) cudaFree(d);
+    d = nullptr;
+    ck(cudaMalloc(&d, count * sizeof(double)), "cudaMalloc");
+    d_cap = count;
+  }
 
   // Ordered on the plan's (non-blocking) stream: a plain cudaMemcpy from
   // pageable memory may return before its DMA lands, which would race the
@@ -470,7 +481,7 @@ struct dbx_plan {
       a.M = n1; a.K = n2; a.N = n2;
     }
     a.C = C; a.sC = NN; a.csel = csel;
-    a.batch = batch; a.epi = epi; a.d = d; a.xold = xold; a.xoldsel = xoldsel; a.f = ff;
+    a.batch = batch; a.epi = epi; a.d = d; a.dstride = dstride; a.xold = xold; a.xoldsel = xoldsel; a.f = ff;
     a.tau = tau; a.st = stp; a.part = pt; a.img_elems = N;
     int ctas = 0;
     ev_begin(KC_TRANSFORM);
@@ -742,7 +753,8 @@ int dbx_precond_build(dbx_plan* P, double alpha) {
     require(P->n1 >= 3 && P->n2 >= 3, "eig_antireflective: sizes must be >= 3");
     require(P->q1 <= P->n1 - 2 && P->q2 <= P->n2 - 2, "eig_antireflective: support condition violated");
     P->set_dev();
-    if (!P->d) ck(cudaMalloc(&P->d, P->N * sizeof(double)), "cudaMalloc");
+    P->ensure_d(P->N);
+    P->dstride = 0;
     int* flag = nullptr;
     ck(cudaMalloc(&flag, sizeof(int)), "cudaMalloc");
     ck(cudaMemsetAsync(flag, 0, sizeof(int), P->stream), "memset");
@@ -925,6 +937,37 @@ int dbx_transpose(dbx_plan* P, const double* in, double* out, int rows, int cols
   });
 }
 
+int dbx_precond_build_sweep(dbx_plan* P, const double* alphas) {
+  return guarded([&] {
+    require(P && alphas, "null argument");
+    require(P->n1 >= 3 && P->n2 >= 3, "eig_antireflective: sizes must be >= 3");
+    require(P->q1 <= P->n1 - 2 && P->q2 <= P->n2 - 2, "eig_antireflective: support condition violated");
+    for (int b = 0; b < P->batch; ++b) require(alphas[b] >= 0.0, "tikhonov_filter: alpha must be nonnegative");
+    P->set_dev();
+    const size_t B = (size_t)P->batch;
+    P->ensure_d(B * P->N);
+    int* flag = nullptr;
+    ck(cudaMalloc(&flag, B * sizeof(int)), "cudaMalloc");
+    ck(cudaMemsetAsync(flag, 0, B * sizeof(int), P->stream), "memset");
+    for (size_t b = 0; b < B; ++b)
+      launch_build_filter(P->sym, P->q1, P->q2, P->n1, P->n2, alphas[b], P->d + b * P->N, flag + b, P->stream);
+    P->launches += 3 * (int64_t)B;
+    P->check_launch();
+    std::vector<int> hflag(B);
+    ck(cudaMemcpyAsync(hflag.data(), flag, B * sizeof(int), cudaMemcpyDeviceToHost, P->stream), "D2H");
+    ck(cudaStreamSynchronize(P->stream), "sync");
+    cudaFree(flag);
+    P->have_d = false;
+    for (size_t b = 0; b < B; ++b)
+      require(alphas[b] > 0.0 || hflag[b] == 0, "tikhonov_filter: alpha = 0 with a zero eigenvalue");
+    P->have_d = true;
+    P->dstride = P->N;
+    P->dT.ensure(B * P->N);
+    launch_transpose(P->d, P->dT.p, P->n1, P->n2, P->stream, (int)B);
+    ck(cudaStreamSynchronize(P->stream), "transpose");
+  });
+}
+
 int dbx_precond_eigs(dbx_plan* P, double* d_out) {
   return guarded([&] {
     require(P && d_out, "null argument");
@@ -939,7 +982,8 @@ int dbx_precond_set_eigs(dbx_plan* P, const double* dd) {
   return guarded([&] {
     require(P && dd, "null argument");
     P->set_dev();
-    if (!P->d) ck(cudaMalloc(&P->d, P->N * sizeof(double)), "cudaMalloc");
+    P->ensure_d(P->N);
+    P->dstride = 0;
     ck(cudaMemcpyAsync(P->d, dd, P->N * sizeof(double), cudaMemcpyDefault, P->stream), "copy");
     ck(cudaStreamSynchronize(P->stream), "sync");
     P->have_d = true;

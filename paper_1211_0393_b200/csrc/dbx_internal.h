@@ -76,7 +76,8 @@ struct GemmArgs {
   double* C; long long sC; int csel;
   int M, N, K, batch;
   int epi;
-  const double* d;                    // HADAMARD: M x N filter grid (shared)
+  const double* d;                    // HADAMARD: M x N filter grid (shared, or per image: dstride)
+  size_t dstride;
   const double* xold; int xoldsel;    // AXPY
   const double* f;                    // AXPY (nullable)
   double tau;

@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_cols(SpecArgs a) {
     const double* o = reinterpret_cast<const double*>(sm + (s >> 1) * C::LINE) + (s & 1) * C::LO;
     double v = kind_out(kind, o, k, n, e0[s], e1[s], al, ri);
     const size_t at = (size_t)k * n2 + c0 + s;
-    if (had) v *= a.d[at];
+    if (had) v *= a.d[(size_t)b * a.dstride + at];
     out[at] = v;
   }
 }

@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   const int nl = n2 - c0 < 4 ? n2 - c0 : 4;
   stage_lines(io, LSO, a.in + (size_t)b * N + (size_t)c0 * n, nl, n);  // u^T lines
   cp_async_commit();
-  stage_lines(dS, LS, a.dT + (size_t)c0 * n, nl, n);                   // d^T lines
+  stage_lines(dS, LS, a.dT + (size_t)b * a.dstride + (size_t)c0 * n, nl, n);  // d^T lines
   cp_async_commit();
   cp_async_wait_group<1>();
   __syncthreads();

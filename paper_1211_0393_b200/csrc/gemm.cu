@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kThreads) gemm_kernel(GemmArgs a) {
       const long long o = (long long)gm * N + gn;
       double v = acc[i][j];
       if (a.epi == EPI_HADAMARD) {
-        v *= a.d[o];
+        v *= a.d[(size_t)b * a.dstride + o];
       } else if (a.epi == EPI_AXPY) {
         v = xo[o] + a.tau * v;
         p0 += v * v;

@@ -61,6 +61,7 @@ struct SpecArgs {
   int ztrans = 0;                                // fused pipeline: row-FFT spectra stored transposed
   int preext = 0;                                // conv_col: n1 + 2 q1 input rows already extended (row slabs)
   const double* dT = nullptr;                    // d transposed [n2][n1] (fused column pass)
+  size_t dstride = 0;                            // filter grid per image (alpha sweep) or shared (0)
   // DST
   int kind1 = DBX_KIND_ARINV, kind2 = -1;
   BlueTables blue1;                              // columns (length n1)

@@ -215,7 +215,7 @@ __device__ __forceinline__ Epi make_epi(const SpecArgs& a, int b, size_t N) {
   e.g = a.g ? a.g + (size_t)b * N : nullptr;
   e.xo = a.epi == SPEC_AXPY ? resolve_ptr(a.xold, a.st, a.xoldsel, b, a.batch, N) : nullptr;
   e.f = (a.epi == SPEC_AXPY && a.f) ? a.f + (size_t)b * N : nullptr;
-  e.d = a.d;
+  e.d = a.d ? a.d + (size_t)b * a.dstride : nullptr;
   e.tau = a.tau;
   return e;
 }
