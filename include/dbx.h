@@ -114,6 +114,18 @@ int dbx_plan_set_fusion(dbx_plan* plan, int enable);
 int dbx_plan_engines(dbx_plan* plan, int* conv, int* dst);
 
 /*
+ * Reblurred CGLS (config 2's "CGLS-type" iteration; no
+ * reference equivalent): minimises ||A x - g|| over Krylov
+ * directions with the AR preconditioner D as the SPD weight
+ * (use_precond = 1) or plain CGLS.  Arguments, stopping rules, histories,
+ * best-iterate tracking and the divergence guard as dbx_landweber_run (the
+ * residual is the recurrence's r_k = r_{k-1} - alpha q).
+ */
+int dbx_cgls_run(dbx_plan* plan, const double* g, const double* f_true, int max_iters, int stop_kind,
+                 int fixed_iters, double resid_eps, int use_precond, double* restored, double* rre_hist,
+                 double* res_hist, int* best_iter, int* iters_done, double* x_hist);
+
+/*
  * Row-slab building blocks (one very large image split into row slabs across
  * ranks; orchestrated by paper_1211_0393_b200/slab.py with NCCL
  * halo exchange and all-to-all transposes).  The plan is created for one slab:

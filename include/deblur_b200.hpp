@@ -258,7 +258,7 @@ struct RestorationRun {  // solver.hpp:46-52
 
 namespace detail {
 inline RestorationRun run(const BlurOperator& op, const FilteredOperator* d, const Matrix& g,
-                          const SolverConfig& cfg) {
+                          const SolverConfig& cfg, bool cg = false) {
   require(g.rows() == op.n1() && g.cols() == op.n2(), "landweber: data size mismatch");
   if (cfg.track_rre_against)
     require(cfg.track_rre_against->rows() == g.rows() && cfg.track_rre_against->cols() == g.cols(),
@@ -275,9 +275,14 @@ inline RestorationRun run(const BlurOperator& op, const FilteredOperator* d, con
   RestorationRun out;
   out.restored = Matrix(g.rows(), g.cols());
   const double* f = cfg.track_rre_against ? cfg.track_rre_against->data() : nullptr;
-  check(dbx_landweber_run(op.plan(), g.data(), f, cfg.tau, cfg.max_iters, static_cast<int>(cfg.stop.kind),
-                          cfg.stop.fixed_iterations, cfg.stop.residual_threshold, d ? 1 : 0,
-                          out.restored.data(), rre.data(), res.data(), &best, &done, nullptr));
+  if (cg)
+    check(dbx_cgls_run(op.plan(), g.data(), f, cfg.max_iters, static_cast<int>(cfg.stop.kind),
+                       cfg.stop.fixed_iterations, cfg.stop.residual_threshold, d ? 1 : 0, out.restored.data(),
+                       rre.data(), res.data(), &best, &done, nullptr));
+  else
+    check(dbx_landweber_run(op.plan(), g.data(), f, cfg.tau, cfg.max_iters, static_cast<int>(cfg.stop.kind),
+                            cfg.stop.fixed_iterations, cfg.stop.residual_threshold, d ? 1 : 0,
+                            out.restored.data(), rre.data(), res.data(), &best, &done, nullptr));
   out.iterations_executed = done;
   out.best_iteration = best;
   out.residual_history.assign(res.begin(), res.begin() + done);
@@ -293,6 +298,13 @@ inline RestorationRun landweber(const BlurOperator& op, const Matrix& g, const S
 inline RestorationRun d_landweber(const BlurOperator& op, const FilteredOperator& d, const Matrix& g,
                                   const SolverConfig& cfg) {
   return detail::run(op, &d, g, cfg);  // solver.hpp:145-148
+}
+
+// Reblurred CGLS, plain (d == nullptr) or preconditioned (no
+// reference equivalent).
+inline RestorationRun cgls(const BlurOperator& op, const Matrix& g, const SolverConfig& cfg,
+                           const FilteredOperator* d = nullptr) {
+  return detail::run(op, d, g, cfg, true);
 }
 
 struct NoiseSpec {  // image.hpp:31-34

@@ -182,6 +182,62 @@ def rre(x, f):
     return lib().orc_rre(_p(x), _p(f), x.size)
 
 
+def cgls(taps, g, d=None, f_true=None, max_iters=100, stop=STOP_MINRRE, fixed_iters=0, resid_eps=0.0,
+         keep_iterates=False):
+    """Reblurred (preconditioned) CGLS, SURVEY §8f f2 — NOT in the reference
+    (SPEC.md:517 lists Krylov methods as a non-goal): the standard CGLS / CGNR
+    recurrence on min ||A x - g|| with D as the SPD weight, built from the
+    reference's own primitives (apply / apply_reblur_adjoint blur.hpp:75-90,
+    precondition_apply preconditioner.hpp:88-90) and its loop bookkeeping
+    (solver.hpp:107-124: guard before recording, strict-'<' best, residual
+    rule after recording).  Parity of the recurrence itself is unpinned."""
+    g = _f64(g)
+    total = fixed_iters if stop == STOP_FIXED else max_iters
+    ft = _f64(f_true) if f_true is not None else None
+    gn = float(np.linalg.norm(g))
+    fn = float(np.linalg.norm(ft)) if ft is not None else 0.0
+    x = np.zeros_like(g)
+    r = g.copy()
+    prec = (lambda v: precondition_apply(d, v)) if d is not None else (lambda v: v)
+    s = apply(taps, r, adjoint=True)
+    z = prec(s)
+    gamma = float(np.sum(s * z))
+    p = z.copy()
+    rre_h, res_h, xs = [], [], []
+    best, best_e, k_done = 0, np.inf, 0
+    for k in range(1, total + 1):
+        q = apply(taps, p)
+        qq = float(np.sum(q * q))
+        alpha = gamma / qq if qq > 0 else 0.0
+        x = x + alpha * p
+        r = r - alpha * q
+        if gn > 0 and np.linalg.norm(x) > 1e8 * gn:
+            raise RuntimeError("landweber: iterate exceeded 1e8 * ||g||")
+        rn = float(np.linalg.norm(r))
+        res_h.append(rn)
+        if ft is not None:
+            e = float(np.linalg.norm(x - ft)) / fn
+            rre_h.append(e)
+            if e < best_e:
+                best_e, best = e, k
+                x_best = x.copy()
+        if keep_iterates:
+            xs.append(x.copy())
+        k_done = k
+        if stop == STOP_RESID and gn > 0 and rn / gn < resid_eps:
+            break
+        s = apply(taps, r, adjoint=True)
+        z = prec(s)
+        gnew = float(np.sum(s * z))
+        beta = gnew / gamma if gamma != 0 else 0.0
+        gamma = gnew
+        p = z + beta * p
+    restored = x_best if (ft is not None and stop == STOP_MINRRE and best > 0) else x
+    return {"restored": restored, "iterations_executed": k_done, "best_iteration": best,
+            "rre_history": np.array(rre_h), "residual_history": np.array(res_h),
+            "iterates": np.array(xs) if keep_iterates else None}
+
+
 def landweber(taps, g, d=None, f_true=None, tau=1.0, max_iters=100, stop=STOP_MINRRE,
               fixed_iters=0, resid_eps=0.0, conv_path=0, keep_iterates=False):
     """solver.hpp:63-148.  Returns a dict shaped like RestorationRun."""

@@ -74,6 +74,7 @@ def lib():
         L.dbx_precond_apply.argtypes = [vp, vp, vp]
         L.dbx_tensor_apply.argtypes = [vp, i, vp, vp]
         L.dbx_landweber_run.argtypes = [vp, vp, vp, d, i, i, i, d, i, vp, vp, vp, vp, vp, vp]
+        L.dbx_cgls_run.argtypes = [vp, vp, vp, i, i, i, d, i, vp, vp, vp, vp, vp, vp]
         L.dbx_plan_set_timing.argtypes = [vp, i]
         L.dbx_plan_kernel_times.argtypes = [vp, vp, vp, i]
         L.dbx_plan_launch_count.argtypes = [vp]
@@ -461,7 +462,8 @@ class SemiconvergenceReport:
     diverged_after: bool = False
 
 
-def _run(op: BlurOperator, d: Optional[FilteredOperator], g, cfg: SolverConfig, keep_iterates=False):
+def _run(op: BlurOperator, d: Optional[FilteredOperator], g, cfg: SolverConfig, keep_iterates=False,
+         method: str = "landweber"):
     g = _f64(g)
     op._shape_ok(g)
     f = cfg.track_rre_against
@@ -488,10 +490,16 @@ def _run(op: BlurOperator, d: Optional[FilteredOperator], g, cfg: SolverConfig, 
     best = (C.c_int * B)()
     done = (C.c_int * B)()
     xh = np.empty((B, H, op.n1, op.n2)) if keep_iterates else None
-    _check(lib().dbx_landweber_run(
-        op.handle, _ptr(g), _ptr(f), float(cfg.tau), int(cfg.max_iters), int(stop.kind),
-        int(stop.fixed_iterations), float(stop.residual_threshold), 1 if d is not None else 0,
-        _ptr(restored), _ptr(rre_h), _ptr(res_h), best, done, _ptr(xh)))
+    if method == "cgls":
+        _check(lib().dbx_cgls_run(
+            op.handle, _ptr(g), _ptr(f), int(cfg.max_iters), int(stop.kind),
+            int(stop.fixed_iterations), float(stop.residual_threshold), 1 if d is not None else 0,
+            _ptr(restored), _ptr(rre_h), _ptr(res_h), best, done, _ptr(xh)))
+    else:
+        _check(lib().dbx_landweber_run(
+            op.handle, _ptr(g), _ptr(f), float(cfg.tau), int(cfg.max_iters), int(stop.kind),
+            int(stop.fixed_iterations), float(stop.residual_threshold), 1 if d is not None else 0,
+            _ptr(restored), _ptr(rre_h), _ptr(res_h), best, done, _ptr(xh)))
     runs = []
     for b in range(B):
         k = done[b]
@@ -513,6 +521,12 @@ def landweber(op: BlurOperator, g, cfg: SolverConfig, keep_iterates=False):
 def d_landweber(op: BlurOperator, d: FilteredOperator, g, cfg: SolverConfig, keep_iterates=False):
     """x_{k+1} = x_k + tau D A'(g - A x_k) (solver.hpp:145-148)."""
     return _run(op, d, g, cfg, keep_iterates)
+
+
+def cgls(op: BlurOperator, g, cfg: SolverConfig, d: Optional[FilteredOperator] = None, keep_iterates=False):
+    """Reblurred CGLS on min ||A x - g||, preconditioned by D when given
+    (config 2's "CGLS-type" iteration; cfg.tau is unused)."""
+    return _run(op, d, g, cfg, keep_iterates, method="cgls")
 
 
 def semiconvergence_report(run: RestorationRun) -> SemiconvergenceReport:  # solver.hpp:152-160

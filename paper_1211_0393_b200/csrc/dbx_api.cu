@@ -222,6 +222,7 @@ struct dbx_plan {
   int L1 = 0, L2 = 0, Lh = 0;
   double *tw1 = nullptr, *tw2 = nullptr, *HA = nullptr, *HAt = nullptr;
   DevBuf zb, yb, dT;  // dT: filter grid transposed (fused column pass)
+  DevBuf cg_p, cg_q, cg_s, cg_z, cg_zero, cg_part, cg_sc;  // CGLS state (dbx_cgls_run)
   struct Blue {
     bool ready = false;
     double *tw = nullptr, *chirp = nullptr, *bhat = nullptr, *p = nullptr, *sn = nullptr;
@@ -239,7 +240,9 @@ struct dbx_plan {
       if (p) cudaFree(p);
     for (double* p : owned) cudaFree(p);
     if (st) cudaFree(st);
-    for (DevBuf* b : {&g, &f, &r, &s, &u, &X3, &in, &out, &part, &rre, &res, &xh, &zb, &yb, &dT}) b->release();
+    for (DevBuf* b : {&g, &f, &r, &s, &u, &X3, &in, &out, &part, &rre, &res, &xh, &zb, &yb, &dT, &cg_p, &cg_q,
+                      &cg_s, &cg_z, &cg_zero, &cg_part, &cg_sc})
+      b->release();
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -1053,10 +1056,28 @@ int dbx_tensor_apply(dbx_plan* P, int kind, const double* x, double* y) {
   });
 }
 
+static int run_impl(dbx_plan* P, const double* g, const double* f_true, double tau, int max_iters, int stop_kind,
+                    int fixed_iters, double resid_eps, int use_precond, double* restored, double* rre_hist,
+                    double* res_hist, int* best_iter, int* iters_done, double* x_hist, int method);
+
 int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double tau,
                       int max_iters, int stop_kind, int fixed_iters, double resid_eps,
                       int use_precond, double* restored, double* rre_hist, double* res_hist,
                       int* best_iter, int* iters_done, double* x_hist) {
+  return run_impl(P, g, f_true, tau, max_iters, stop_kind, fixed_iters, resid_eps, use_precond, restored, rre_hist,
+                  res_hist, best_iter, iters_done, x_hist, 0);
+}
+
+int dbx_cgls_run(dbx_plan* P, const double* g, const double* f_true, int max_iters, int stop_kind, int fixed_iters,
+                 double resid_eps, int use_precond, double* restored, double* rre_hist, double* res_hist,
+                 int* best_iter, int* iters_done, double* x_hist) {
+  return run_impl(P, g, f_true, 1.0, max_iters, stop_kind, fixed_iters, resid_eps, use_precond, restored, rre_hist,
+                  res_hist, best_iter, iters_done, x_hist, 1);
+}
+
+static int run_impl(dbx_plan* P, const double* g, const double* f_true, double tau, int max_iters, int stop_kind,
+                    int fixed_iters, double resid_eps, int use_precond, double* restored, double* rre_hist,
+                    double* res_hist, int* best_iter, int* iters_done, double* x_hist, int method) {
   return guarded([&] {
     require(P && g && restored, "landweber: null argument");
     // solver.hpp:66-72, 17-32
@@ -1101,7 +1122,8 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
 
     // Fused FFT-form pipeline (fused.cu): 6 launches + finalize per iteration.
     P->prepare(use_precond != 0);
-    const bool fused = use_precond && P->n1 == P->n2 && P->use_fft_conv() && P->use_fft_dst(false) && P->fusion &&
+    const bool fused = method == 0 && use_precond && P->n1 == P->n2 && P->use_fft_conv() && P->use_fft_dst(false) &&
+                       P->fusion &&
                        P->blue_tables(1, false).core != CORE_RADER &&
                        fused_supported(P->L2, P->blue_tables(1, false).M,
                                        P->blue_tables(1, false).core == CORE_BLUE);
@@ -1122,7 +1144,36 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
       fa0.ztrans = 1;
       fa0.dT = P->dT.p;
     }
+    // ---- reblurred (preconditioned) CGLS state (cg.cu) ----
+    if (method == 1) {
+      for (DevBuf* b : {&P->cg_p, &P->cg_q, &P->cg_s, &P->cg_z, &P->cg_zero}) b->ensure(cnt);
+      P->cg_part.ensure((size_t)B * P->part_cap);
+      P->cg_sc.ensure((size_t)B * 4);
+      ck(cudaMemsetAsync(P->cg_zero.p, 0, cnt * sizeof(double), s), "memset");
+    }
+    CgScalars* cgs = method == 1 ? reinterpret_cast<CgScalars*>(P->cg_sc.p) : nullptr;
+    auto cg_precond = [&](const double* in, double* out) -> const double* {
+      if (!use_precond) return in;  // plain CGLS: z = s
+      P->apply_D(in, SEL_EXPLICIT, out, SEL_EXPLICIT, SPEC_STORE, nullptr, SEL_EXPLICIT, nullptr, 0.0, P->st,
+                 Partials{nullptr, 0});
+      return out;
+    };
+    auto cg_direction = [&](int init) {  // s = A' r, z = D s, gamma = <s, z>, p = z + beta p
+      P->blur(P->r.p, SEL_EXPLICIT, P->cg_s.p, SEL_EXPLICIT, true, BLUR_STORE, nullptr, nullptr, SEL_EXPLICIT,
+              nullptr, 0.0, P->st, pt, KC_BLUR_ADJ);
+      const double* z = cg_precond(P->cg_s.p, P->cg_z.p);
+      const int cnt_d = launch_cg_dot(P->st, P->cg_s.p, z, B, N, P->cg_part.p, P->part_cap, s);
+      launch_cg_beta(P->st, cgs, P->cg_part.p, P->part_cap, cnt_d, init, B, s);
+      if (init) ck(cudaMemcpyAsync(P->cg_p.p, z, cnt * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
+      else launch_cg_xpay(P->st, cgs, z, P->cg_p.p, B, N, s);
+      P->launches += 3;
+      P->check_launch();
+    };
     auto enqueue_pre = [&]() {
+      if (method == 1) {
+        cg_direction(1);
+        return;
+      }
       if (!fused) return;
       // spectrum of the AR-extended r_0 = g for the first A' apply
       SpecArgs a = fa0;
@@ -1176,6 +1227,28 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
         }
         return;
       }
+      if (method == 1) {
+        // q' = 0 - A p (||q||^2 in the residual slot) -> alpha -> x, r updates
+        const int cnt_q = P->blur(P->cg_p.p, SEL_EXPLICIT, P->cg_q.p, SEL_EXPLICIT, false, BLUR_RESID,
+                                  P->cg_zero.p, nullptr, SEL_EXPLICIT, nullptr, 0.0, P->st, pt, KC_BLUR);
+        launch_cg_alpha(P->st, cgs, pt, cnt_q, B, s);
+        const int cnt_u = launch_cg_update(P->X3.p, P->st, cgs, P->cg_p.p, P->cg_q.p, P->r.p, fd, B, N, pt, s);
+        P->launches += 2;
+        FinalizeArgs fa{};
+        fa.st = P->st; fa.part = pt; fa.cnt_x = cnt_u; fa.cnt_r = cnt_u; fa.k = k;
+        fa.hist_len = H; fa.rre_hist = P->rre.p; fa.res_hist = P->res.p;
+        fa.track = track ? 1 : 0; fa.stop_kind = stop_kind; fa.resid_eps = resid_eps; fa.batch = B;
+        P->ev_begin(KC_FINALIZE);
+        launch_finalize(fa, s);
+        P->ev_end();
+        P->check_launch();
+        if (want_xh) {
+          launch_select_copy(P->X3.p, P->st, 0, B, N, P->xh.p + (size_t)(k - 1) * cnt, s);
+          ++P->launches;
+        }
+        if (k < total) cg_direction(0);
+        return;
+      }
       if (use_precond) {
         P->blur(P->r.p, SEL_EXPLICIT, P->s.p, SEL_EXPLICIT, true, BLUR_STORE, nullptr, nullptr,
                 SEL_EXPLICIT, nullptr, 0.0, P->st, pt, KC_BLUR_ADJ);
@@ -1205,9 +1278,9 @@ int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double
       // Graph path: one graph per run shape, replayed; kernels read the run's
       // buffers through stable plan-owned pointers.
       char key[512];
-      snprintf(key, sizeof key, "%d|%d|%d|%.17g|%.17g|%d|%d|%p|%p|%d|%d|%d", total, use_precond,
+      snprintf(key, sizeof key, "%d|%d|%d|%.17g|%.17g|%d|%d|%p|%p|%d|%d|%d|%d", total, use_precond,
                stop_kind, resid_eps, tau, (int)track, (int)want_xh, (const void*)gd,
-               (const void*)fd, P->conv, P->dst, (int)fused);
+               (const void*)fd, P->conv, P->dst, (int)fused, method);
       const bool use_graph = !P->timing;
       if (use_graph) {
         if (!P->gexec || P->gkey != key) {

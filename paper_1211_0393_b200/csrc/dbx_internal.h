@@ -111,6 +111,20 @@ void launch_state_init(ImgState* st, int batch, cudaStream_t s);
 void launch_select_copy(const double* X3, const ImgState* st, int which_best, int batch,
                         size_t N, double* out, cudaStream_t s);
 void launch_zero(double* p, size_t n, cudaStream_t s);
+
+// ---- reblurred (preconditioned) CGLS scalars and vector steps (cg.cu) ----
+struct CgScalars {
+  double gamma, alpha, beta, pad_;
+};
+void launch_cg_alpha(const ImgState* st, CgScalars* cs, Partials pt, int cnt, int batch, cudaStream_t s);
+int launch_cg_update(const double* X3, const ImgState* st, const CgScalars* cs, const double* p, const double* qn,
+                     double* r, const double* f, int batch, size_t N, Partials pt, cudaStream_t s);
+int launch_cg_dot(const ImgState* st, const double* a, const double* b, int batch, size_t N, double* part, int cap,
+                  cudaStream_t s);
+void launch_cg_beta(const ImgState* st, CgScalars* cs, const double* part, int cap, int cnt, int init, int batch,
+                    cudaStream_t s);
+void launch_cg_xpay(const ImgState* st, const CgScalars* cs, const double* z, double* p, int batch, size_t N,
+                    cudaStream_t s);
 void launch_slab_ar_rows(const double* x, double* ext, int rows, int n2, int q, int top, int bot, cudaStream_t s);
 void launch_transpose(const double* in, double* out, int rows, int cols, cudaStream_t s, int batch = 1);
 

@@ -20,6 +20,27 @@
 #include "dft_consts.h"
 
 namespace dbx {
+
+// Phase timing (instrumented builds only: -DDBX_PHASES): thread 0 of every CTA
+// adds the clock64() delta since its previous mark to g_phase[i] (one
+// namespace-scope shared timestamp per CTA, so marks may sit in any device
+// function, e.g. after every FFT stage).
+#ifdef DBX_PHASES
+static __device__ unsigned long long g_phase[64];  // per translation unit (fused.cu reads its own)
+static __shared__ unsigned long long ph_t0s;
+#define PH_DECL \
+  if (threadIdx.x == 0) ph_t0s = clock64();
+#define PH(i)                                        \
+  if (threadIdx.x == 0) {                            \
+    const unsigned long long ph_t1 = clock64();      \
+    atomicAdd(&g_phase[i], ph_t1 - ph_t0s);          \
+    ph_t0s = ph_t1;                                  \
+  }
+#else
+#define PH_DECL
+#define PH(i)
+#endif
+
 namespace fft {
 
 // Even lengths (power-of-two radices) pad one element per 8 so stride-8
@@ -553,6 +574,7 @@ __device__ __forceinline__ void run_stages_cta(double2* sm, const double2* __res
       const int g = tid / T;
       stage<L, Ns, R, S, T>(sm + g * PL, tw, tid - g * T, G > 1 ? 1 + g : 0);
     }
+    PH(40 + (Ns == 1 ? 0 : (Ns * R == L ? 2 : 1)))  // DST FFT stage (first / middle / last)
     run_stages_cta<L, Ns * R, S, T, G, PL>(sm, tw, tid);
   }
 }

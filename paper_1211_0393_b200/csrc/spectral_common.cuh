@@ -10,22 +10,6 @@
 
 namespace dbx {
 
-// Phase timing (instrumented builds only: -DDBX_PHASES): thread 0 of every CTA
-// adds the clock64() delta since its previous mark to g_phase[i].
-#ifdef DBX_PHASES
-static __device__ unsigned long long g_phase[64];  // per translation unit (fused.cu reads its own)
-#define PH_DECL unsigned long long ph_t0 = clock64();
-#define PH(i)                                        \
-  if (threadIdx.x == 0) {                            \
-    const unsigned long long ph_t1 = clock64();      \
-    atomicAdd(&g_phase[i], ph_t1 - ph_t0);           \
-    ph_t0 = ph_t1;                                   \
-  }
-#else
-#define PH_DECL
-#define PH(i)
-#endif
-
 using fft::cadd;
 using fft::cmul;
 using fft::csub;
