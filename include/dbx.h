@@ -40,10 +40,12 @@ extern "C" {
 
 /* boundary.hpp:9 BoundaryCondition order {Zero, Periodic, Reflective, AntiReflective};
  * this path implements AntiReflective only. */
+#define DBX_BC_REFLECTIVE 2     /* BoundaryCondition::Reflective (DCT-III algebra) */
 #define DBX_BC_ANTIREFLECTIVE 3
 
 /* transforms.hpp:17 TransformKind order {Dft, CosineIII, SineI, AntiReflective,
  * AntiReflectiveInverse}; the AR path needs the last three. */
+#define DBX_KIND_COSINE3 1   /* R (cosine3_forward, transforms.hpp:88-99), reflective BCs */
 #define DBX_KIND_SINEI 2
 #define DBX_KIND_AR 3
 #define DBX_KIND_ARINV 4

@@ -278,6 +278,37 @@ static void check_support_ar(long n1, long n2, long q1, long q2) {
           "anti-reflective support condition violated (q > n-2)");
 }
 
+enum Bc { kReflective = 2, kAntiReflective = 3 };  // BoundaryCondition order, boundary.hpp:9
+
+// boundary.hpp:66-81 (Reflective branch)
+static void check_support_refl(long n1, long n2, long q1, long q2) {
+  require(n1 >= 1 && n2 >= 1, "pad: empty image");
+  require(q1 <= n1 && q2 <= n2, "reflective support condition violated (q > n)");
+}
+
+// boundary.hpp:88-102 with extend_axis Reflective (49-55): f_{1-i} = f_i,
+// f_{n+i} = f_{n+1-i}; rows first, then columns of the widened image.
+static Mat pad_refl(const Mat& f, long q1, long q2) {
+  const long n1 = f.n1, n2 = f.n2;
+  check_support_refl(n1, n2, q1, q2);
+  Mat out(n1 + 2 * q1, n2 + 2 * q2);
+  for (long r = 0; r < n1; ++r)
+    for (long c = 0; c < n2; ++c) out(q1 + r, q2 + c) = f(r, c);
+  for (long r = 0; r < n1; ++r) {
+    double* b = &out(q1 + r, 0);
+    for (long i = 1; i <= q2; ++i) {
+      b[q2 - i] = b[q2 + i - 1];
+      b[q2 + n2 - 1 + i] = b[q2 + n2 - i];
+    }
+  }
+  for (long c = 0; c < n2 + 2 * q2; ++c)
+    for (long i = 1; i <= q1; ++i) {
+      out(q1 - i, c) = out(q1 + i - 1, c);
+      out(q1 + n1 - 1 + i, c) = out(q1 + n1 - i, c);
+    }
+  return out;
+}
+
 // boundary.hpp:88-102 with extend_axis AR (56-62): rows (axis 2) of the FOV
 // first, then every column (axis 1) of the widened image.
 static Mat pad_ar(const Mat& f, long q1, long q2) {
@@ -345,8 +376,8 @@ static Mat correlate_valid_fft(const Mat& P, const Psf& p, long n1, long n2) {
 constexpr long kDirectConvMaxQ = 7;  // blur.hpp:70
 
 // blur.hpp:75-83 (path: 0 auto, 1 direct, 2 fft)
-static Mat apply(const Psf& p, const Mat& f, int path = 0) {
-  const Mat P = pad_ar(f, p.q1, p.q2);
+static Mat apply(const Psf& p, const Mat& f, int path = 0, int bc = kAntiReflective) {
+  const Mat P = bc == kReflective ? pad_refl(f, p.q1, p.q2) : pad_ar(f, p.q1, p.q2);
   const bool direct = path == 1 || (path == 0 && p.q1 <= kDirectConvMaxQ && p.q2 <= kDirectConvMaxQ);
   return direct ? correlate_valid_direct(P, p, f.n1, f.n2) : correlate_valid_fft(P, p, f.n1, f.n2);
 }
@@ -426,19 +457,54 @@ static void ar_inverse(const ArT& t, const double* v, double* u) {
   for (long j = 0; j < m - 2; ++j) u[j + 1] = out[size_t(j)];
 }
 
-enum Kind { kSineI = 2, kAR = 3, kARInv = 4 };  // TransformKind order, transforms.hpp:17
+enum Kind { kCosineIII = 1, kSineI = 2, kAR = 3, kARInv = 4 };  // TransformKind order, transforms.hpp:17
+
+// transforms.hpp:88-110: R_m(s,t) = sqrt((2 - delta_{s,0})/m) cos(s (2t+1) pi / (2m))
+// (0-based), FFTW REDFT10 / REDFT01 with the orthonormal scaling; restated
+// as the dense definition with exact integer argument reduction (angle index
+// s (2t+1) mod 4m) and long-double cosines.
+static const std::vector<double>& cos4m(long m) {
+  static thread_local std::map<long, std::vector<double>> cache;
+  auto it = cache.find(m);
+  if (it != cache.end()) return it->second;
+  std::vector<double> c(size_t(4 * m));
+  for (long e = 0; e < 4 * m; ++e) c[size_t(e)] = double(cosl(kPiL * (long double)e / (long double)(2 * m)));
+  return cache.emplace(m, std::move(c)).first->second;
+}
+static void cosine3_forward(const double* v, double* y, long m) {
+  require(m >= 1, "cosine3_forward: empty input");
+  const auto& c = cos4m(m);
+  const long double w0 = sqrtl(1.0L / (long double)m), w = sqrtl(2.0L / (long double)m);
+  for (long s = 0; s < m; ++s) {
+    long double acc = 0;
+    for (long t = 0; t < m; ++t) acc += (long double)v[t] * c[size_t((s * (2 * t + 1)) % (4 * m))];
+    y[s] = double(acc * (s == 0 ? w0 : w));
+  }
+}
+static void cosine3_inverse(const double* v, double* y, long m) {
+  require(m >= 1, "cosine3_inverse: empty input");
+  const auto& c = cos4m(m);
+  const long double w0 = sqrtl(1.0L / (long double)m), w = sqrtl(2.0L / (long double)m);
+  for (long t = 0; t < m; ++t) {
+    long double acc = (long double)v[0] * w0;
+    for (long s = 1; s < m; ++s) acc += (long double)v[s] * w * c[size_t((s * (2 * t + 1)) % (4 * m))];
+    y[t] = double(acc);
+  }
+}
 
 // transforms.hpp:179-192 (columns first, then rows) + 198-226
 static Mat tensor_apply(int kind, const Mat& x) {
   const long n1 = x.n1, n2 = x.n2;
   ArT t1, t2;
-  if (kind != kSineI) {
+  if (kind == kAR || kind == kARInv) {
     require(n1 >= 3 && n2 >= 3, "tensor_apply: anti-reflective transform needs sizes >= 3");
     t1 = make_ar_transform(n1);
     t2 = make_ar_transform(n2);
   }
   auto kern = [&](const ArT& t, const double* in, double* out, long m) {
-    if (kind == kSineI) sine1_forward(in, out, m);
+    if (kind == kCosineIII) cosine3_forward(in, out, m);
+    else if (kind == -kCosineIII) cosine3_inverse(in, out, m);
+    else if (kind == kSineI) sine1_forward(in, out, m);
     else if (kind == kAR) ar_forward(t, in, out);
     else ar_inverse(t, in, out);
   };
@@ -479,6 +545,16 @@ static Mat eig_antireflective(const Psf& p, long n1, long n2) {
   return e;
 }
 
+// spectral.hpp:50-54, 73-84: x_r = r pi / m, r = 0..m-1
+static Mat eig_reflective(const Psf& p, long n1, long n2) {
+  require(max_asymmetry(p) <= 1e-12, "eig_reflective: mask is not strongly symmetric");
+  Mat e(n1, n2);
+  for (long a = 0; a < n1; ++a)
+    for (long b = 0; b < n2; ++b)
+      e(a, b) = symbol_real(p, double(a) * kPi / double(n1), double(b) * kPi / double(n2));
+  return e;
+}
+
 // preconditioner.hpp:37-57 (real algebra branch)
 static Mat tikhonov_filter(const Mat& base, double alpha) {
   require(alpha >= 0.0, "tikhonov_filter: alpha must be nonnegative");
@@ -494,6 +570,20 @@ static Mat tikhonov_filter(const Mat& base, double alpha) {
 static Mat build_tikhonov(const Psf& p, double alpha, long n1, long n2) {
   const Psf s = symmetrize(p);
   return tikhonov_filter(eig_antireflective(s, n1, n2), alpha);
+}
+
+// preconditioner.hpp:62-85 (CosineIII branch)
+static Mat build_tikhonov_cos(const Psf& p, double alpha, long n1, long n2) {
+  const Psf s = symmetrize(p);
+  return tikhonov_filter(eig_reflective(s, n1, n2), alpha);
+}
+
+// spectral.hpp:147-154: R^T diag(d) R (forward tensor, Hadamard, inverse tensor)
+static Mat filter_apply_cos(const Mat& d, const Mat& x) {
+  require(x.n1 == d.n1 && x.n2 == d.n2, "filter_apply: size mismatch");
+  Mat xhat = tensor_apply(kCosineIII, x);
+  for (size_t i = 0; i < xhat.a.size(); ++i) xhat.a[i] *= d.a[i];
+  return tensor_apply(-kCosineIII, xhat);
 }
 
 // spectral.hpp:161-165 / preconditioner.hpp:88-90
@@ -631,7 +721,8 @@ int orc_ar_alpha(int m, double* alpha, double* p) {
 
 int orc_tensor_apply(int kind, const double* x, int n1, int n2, double* y) {
   ORC_TRY({
-    require(kind == kSineI || kind == kAR || kind == kARInv, "tensor_apply: unsupported kind");
+    require(kind == kSineI || kind == kAR || kind == kARInv || kind == kCosineIII || kind == -kCosineIII,
+            "tensor_apply: unsupported kind");
     from_mat(tensor_apply(kind, to_mat(x, n1, n2)), y);
   });
 }
@@ -664,17 +755,19 @@ enum { STOP_FIXED = 0, STOP_MINRRE = 1, STOP_RESID = 2 };
 // solver.hpp:63-132 landweber_loop (+ 139-148).  d == NULL -> plain
 // Landweber.  x_hist (nullable) receives every iterate x_k, k = 1..executed.
 // conv_path: 0 auto (reference cutover), 1 direct, 2 fft.
-int orc_landweber(const double* taps, int q1, int q2, int n1, int n2, const double* d,
-                  const double* g, const double* f_true, double tau, int max_iters, int stop_kind,
-                  int fixed_iters, double resid_eps, int conv_path, double* restored,
-                  double* rre_hist, double* res_hist, int* best_iter, int* iters_done,
-                  double* x_hist) {
+int orc_landweber_bc(const double* taps, int q1, int q2, int n1, int n2, const double* d,
+                     const double* g, const double* f_true, double tau, int max_iters, int stop_kind,
+                     int fixed_iters, double resid_eps, int conv_path, int bc, double* restored,
+                     double* rre_hist, double* res_hist, int* best_iter, int* iters_done,
+                     double* x_hist) {
   *iters_done = 0;
   *best_iter = 0;
   ORC_TRY({
     Psf p = make_psf(taps, q1, q2);
     require(n1 >= 1 && n2 >= 1, "BlurOperator: empty field of view");
-    check_support_ar(n1, n2, q1, q2);
+    require(bc == kReflective || bc == kAntiReflective, "landweber: unsupported boundary condition");
+    if (bc == kReflective) check_support_refl(n1, n2, q1, q2);
+    else check_support_ar(n1, n2, q1, q2);
     require(tau > 0.0, "landweber: tau must be positive");
     require(max_iters >= 1, "landweber: max_iters must be at least 1");
     require(stop_kind != STOP_FIXED || fixed_iters >= 0, "StoppingRule: negative iteration count");
@@ -690,10 +783,10 @@ int orc_landweber(const double* taps, int q1, int q2, int n1, int n2, const doub
     Mat x(n1, n2), best(n1, n2), r = G;
     double best_rre = std::numeric_limits<double>::infinity();
     for (int k = 1; k <= total; ++k) {
-      Mat step = apply(rot, r, conv_path);
-      if (d) step = filter_apply_ar(D, step);
+      Mat step = apply(rot, r, conv_path, bc);
+      if (d) step = bc == kReflective ? filter_apply_cos(D, step) : filter_apply_ar(D, step);
       for (size_t i = 0; i < N; ++i) x.a[i] += tau * step.a[i];
-      const Mat ax = apply(p, x, conv_path);
+      const Mat ax = apply(p, x, conv_path, bc);
       for (size_t i = 0; i < N; ++i) r.a[i] = G.a[i] - ax.a[i];
       if (fro(x.a.data(), N) > guard && g_norm > 0.0)
         throw std::runtime_error("landweber: iterate exceeded 1e8 * ||g||");
@@ -715,6 +808,45 @@ int orc_landweber(const double* taps, int q1, int q2, int n1, int n2, const doub
     const Mat& out = (stop_kind == STOP_MINRRE && f_true && *best_iter > 0) ? best : x;
     from_mat(out, restored);
   });
+}
+
+int orc_landweber(const double* taps, int q1, int q2, int n1, int n2, const double* d,
+                  const double* g, const double* f_true, double tau, int max_iters, int stop_kind,
+                  int fixed_iters, double resid_eps, int conv_path, double* restored,
+                  double* rre_hist, double* res_hist, int* best_iter, int* iters_done,
+                  double* x_hist) {
+  return orc_landweber_bc(taps, q1, q2, n1, n2, d, g, f_true, tau, max_iters, stop_kind, fixed_iters, resid_eps,
+                          conv_path, kAntiReflective, restored, rre_hist, res_hist, best_iter, iters_done, x_hist);
+}
+
+// Reflective BC / CosineIII algebra (the paper's comparison path)
+int orc_apply_bc(const double* taps, int q1, int q2, const double* f, int n1, int n2, int adjoint, int path,
+                 int bc, double* out) {
+  ORC_TRY({
+    require(bc == kReflective || bc == kAntiReflective, "apply: unsupported boundary condition");
+    Psf p = make_psf(taps, q1, q2);
+    if (adjoint) p = rotate180(p);
+    from_mat(apply(p, to_mat(f, n1, n2), path, bc), out);
+  });
+}
+
+int orc_build_tikhonov_bc(const double* taps, int q1, int q2, int n1, int n2, double alpha, int bc, double* d) {
+  ORC_TRY({
+    require(bc == kReflective || bc == kAntiReflective, "build_tikhonov: unsupported boundary condition");
+    const Psf p = make_psf(taps, q1, q2);
+    from_mat(bc == kReflective ? build_tikhonov_cos(p, alpha, n1, n2) : build_tikhonov(p, alpha, n1, n2), d);
+  });
+}
+
+int orc_precondition_apply_bc(const double* d, const double* r, int n1, int n2, int bc, double* y) {
+  ORC_TRY({
+    const Mat D = to_mat(d, n1, n2), R = to_mat(r, n1, n2);
+    from_mat(bc == kReflective ? filter_apply_cos(D, R) : filter_apply_ar(D, R), y);
+  });
+}
+
+int orc_cosine3(int inverse, const double* v, int m, double* y) {
+  ORC_TRY(inverse ? cosine3_inverse(v, y, m) : cosine3_forward(v, y, m));
 }
 
 }  // extern "C"

@@ -98,13 +98,29 @@ def pad_ar(f, q1, q2):
     return out
 
 
-def apply(taps, f, adjoint=False, path=0):
+BC_REFLECTIVE, BC_ANTIREFLECTIVE = 2, 3  # BoundaryCondition order, boundary.hpp:9
+KIND_COSINE3 = 1  # TransformKind::CosineIII (forward R); -1 in tensor_apply = R^T
+
+
+def apply(taps, f, adjoint=False, path=0, bc=BC_ANTIREFLECTIVE):
     """blur.hpp:75-83 (adjoint=True: apply_reblur_adjoint, blur.hpp:87-90)."""
     taps, q1, q2 = _q(taps)
     f = _f64(f)
     out = np.empty_like(f)
-    _check(lib().orc_apply(_p(taps), q1, q2, _p(f), f.shape[0], f.shape[1], int(adjoint), int(path), _p(out)))
+    if bc == BC_ANTIREFLECTIVE:
+        _check(lib().orc_apply(_p(taps), q1, q2, _p(f), f.shape[0], f.shape[1], int(adjoint), int(path), _p(out)))
+    else:
+        _check(lib().orc_apply_bc(_p(taps), q1, q2, _p(f), f.shape[0], f.shape[1], int(adjoint), int(path), bc,
+                                  _p(out)))
     return out
+
+
+def cosine3_forward(v, inverse=False):
+    """transforms.hpp:88-110 (R_m v, or R_m^T v when inverse)."""
+    v = _f64(v)
+    y = np.empty_like(v)
+    _check(lib().orc_cosine3(int(inverse), _p(v), v.size, _p(y)))
+    return y
 
 
 def sine1_forward(v):
@@ -156,17 +172,24 @@ def tikhonov_filter(eigs, alpha):
     return d
 
 
-def build_tikhonov(taps, alpha, n1, n2):
+def build_tikhonov(taps, alpha, n1, n2, bc=BC_ANTIREFLECTIVE):
+    """preconditioner.hpp:62-85 (AntiReflective, or CosineIII for reflective BCs)."""
     taps, q1, q2 = _q(taps)
     d = np.empty((n1, n2))
-    _check(lib().orc_build_tikhonov(_p(taps), q1, q2, n1, n2, C.c_double(alpha), _p(d)))
+    if bc == BC_ANTIREFLECTIVE:
+        _check(lib().orc_build_tikhonov(_p(taps), q1, q2, n1, n2, C.c_double(alpha), _p(d)))
+    else:
+        _check(lib().orc_build_tikhonov_bc(_p(taps), q1, q2, n1, n2, C.c_double(alpha), bc, _p(d)))
     return d
 
 
-def precondition_apply(d, r):
+def precondition_apply(d, r, bc=BC_ANTIREFLECTIVE):
     d, r = _f64(d), _f64(r)
     y = np.empty_like(r)
-    _check(lib().orc_precondition_apply(_p(d), _p(r), r.shape[0], r.shape[1], _p(y)))
+    if bc == BC_ANTIREFLECTIVE:
+        _check(lib().orc_precondition_apply(_p(d), _p(r), r.shape[0], r.shape[1], _p(y)))
+    else:
+        _check(lib().orc_precondition_apply_bc(_p(d), _p(r), r.shape[0], r.shape[1], bc, _p(y)))
     return y
 
 
@@ -183,7 +206,7 @@ def rre(x, f):
 
 
 def cgls(taps, g, d=None, f_true=None, max_iters=100, stop=STOP_MINRRE, fixed_iters=0, resid_eps=0.0,
-         keep_iterates=False):
+         keep_iterates=False, bc=BC_ANTIREFLECTIVE):
     """Reblurred (preconditioned) CGLS, SURVEY §8f f2 — NOT in the reference
     (SPEC.md:517 lists Krylov methods as a non-goal): the standard CGLS / CGNR
     recurrence on min ||A x - g|| with D as the SPD weight, built from the
@@ -198,15 +221,15 @@ def cgls(taps, g, d=None, f_true=None, max_iters=100, stop=STOP_MINRRE, fixed_it
     fn = float(np.linalg.norm(ft)) if ft is not None else 0.0
     x = np.zeros_like(g)
     r = g.copy()
-    prec = (lambda v: precondition_apply(d, v)) if d is not None else (lambda v: v)
-    s = apply(taps, r, adjoint=True)
+    prec = (lambda v: precondition_apply(d, v, bc)) if d is not None else (lambda v: v)
+    s = apply(taps, r, adjoint=True, bc=bc)
     z = prec(s)
     gamma = float(np.sum(s * z))
     p = z.copy()
     rre_h, res_h, xs = [], [], []
     best, best_e, k_done = 0, np.inf, 0
     for k in range(1, total + 1):
-        q = apply(taps, p)
+        q = apply(taps, p, bc=bc)
         qq = float(np.sum(q * q))
         alpha = gamma / qq if qq > 0 else 0.0
         x = x + alpha * p
@@ -226,7 +249,7 @@ def cgls(taps, g, d=None, f_true=None, max_iters=100, stop=STOP_MINRRE, fixed_it
         k_done = k
         if stop == STOP_RESID and gn > 0 and rn / gn < resid_eps:
             break
-        s = apply(taps, r, adjoint=True)
+        s = apply(taps, r, adjoint=True, bc=bc)
         z = prec(s)
         gnew = float(np.sum(s * z))
         beta = gnew / gamma if gamma != 0 else 0.0
@@ -239,7 +262,7 @@ def cgls(taps, g, d=None, f_true=None, max_iters=100, stop=STOP_MINRRE, fixed_it
 
 
 def landweber(taps, g, d=None, f_true=None, tau=1.0, max_iters=100, stop=STOP_MINRRE,
-              fixed_iters=0, resid_eps=0.0, conv_path=0, keep_iterates=False):
+              fixed_iters=0, resid_eps=0.0, conv_path=0, keep_iterates=False, bc=BC_ANTIREFLECTIVE):
     """solver.hpp:63-148.  Returns a dict shaped like RestorationRun."""
     taps, q1, q2 = _q(taps)
     g = _f64(g)
@@ -254,10 +277,10 @@ def landweber(taps, g, d=None, f_true=None, tau=1.0, max_iters=100, stop=STOP_MI
     xh = np.empty((hist, n1, n2)) if keep_iterates else None
     dd = _f64(d) if d is not None else None
     ft = _f64(f_true) if f_true is not None else None
-    st = lib().orc_landweber(
+    st = lib().orc_landweber_bc(
         _p(taps), q1, q2, n1, n2, _p(dd) if dd is not None else None, _p(g),
         _p(ft) if ft is not None else None, C.c_double(tau), max_iters, stop, fixed_iters,
-        C.c_double(resid_eps), conv_path, _p(restored), _p(rre_h), _p(res_h), C.byref(best),
+        C.c_double(resid_eps), conv_path, bc, _p(restored), _p(rre_h), _p(res_h), C.byref(best),
         C.byref(done), _p(xh) if xh is not None else None)
     _check(st)
     k = done.value

@@ -219,10 +219,10 @@ def rotate180(p: Psf) -> Psf:  # psf.hpp:88-91
 # BlurOperator (blur.hpp:17-34) — owns one device plan
 # ---------------------------------------------------------------------------
 class _Plan:
-    def __init__(self, n1, n2, batch, taps, q1, q2, device=0):
+    def __init__(self, n1, n2, batch, taps, q1, q2, device=0, bc=None):
         self.h = C.c_void_p()
-        _check(lib().dbx_plan_create(n1, n2, batch, _ptr(taps), q1, q2, int(BoundaryCondition.AntiReflective),
-                                     device, C.byref(self.h)))
+        bc = BoundaryCondition.AntiReflective if bc is None else bc
+        _check(lib().dbx_plan_create(n1, n2, batch, _ptr(taps), q1, q2, int(bc), device, C.byref(self.h)))
 
     def __del__(self):
         try:
@@ -238,12 +238,15 @@ class BlurOperator:
     def __init__(self, psf: Psf, bc: BoundaryCondition, n1: int, n2: int, batch: int = 1, device: int = 0):
         if n1 < 1 or n2 < 1:
             raise ValueError("BlurOperator: empty field of view")
-        if bc != BoundaryCondition.AntiReflective:
-            raise ValueError("BlurOperator: this path implements AntiReflective BCs only")
-        if not ((psf.q1 == 0 or psf.q1 <= n1 - 2) and (psf.q2 == 0 or psf.q2 <= n2 - 2)):
+        if bc not in (BoundaryCondition.AntiReflective, BoundaryCondition.Reflective):
+            raise ValueError("BlurOperator: this path implements AntiReflective and Reflective BCs")
+        if bc == BoundaryCondition.Reflective:
+            if not (psf.q1 <= n1 and psf.q2 <= n2):
+                raise ValueError("reflective support condition violated (q > n)")
+        elif not ((psf.q1 == 0 or psf.q1 <= n1 - 2) and (psf.q2 == 0 or psf.q2 <= n2 - 2)):
             raise ValueError("anti-reflective support condition violated (q > n-2)")
         self._psf, self._bc, self.n1, self.n2, self.batch = psf, bc, n1, n2, batch
-        self._plan = _Plan(n1, n2, batch, psf.taps(), psf.q1, psf.q2, device)
+        self._plan = _Plan(n1, n2, batch, psf.taps(), psf.q1, psf.q2, device, bc)
         self._eigs_id = None
 
     def psf(self):
@@ -323,8 +326,6 @@ def tensor_apply(kind: TransformKind, x, op: Optional[BlurOperator] = None, engi
     x = _f64(x)
     if kind == TransformKind.Dft:
         raise ValueError("tensor_apply: Dft is complex, use dft2_forward")
-    if kind == TransformKind.CosineIII:
-        raise ValueError("tensor_apply: CosineIII (Reflective BCs) is outside the AR path")
     n1, n2 = x.shape[-2], x.shape[-1]
     if kind in (TransformKind.AntiReflective, TransformKind.AntiReflectiveInverse) and (n1 < 3 or n2 < 3):
         raise ValueError("tensor_apply: anti-reflective transform needs sizes >= 3")
@@ -356,38 +357,44 @@ class PreconditionerSpec:
 
 
 class FilteredOperator:
-    """D = T diag(d) T~ ; ``eigs`` is the d grid (sop.eigs), ``source_psf`` the
-    symmetrised mask it came from."""
+    """D = T diag(d) T~ (AntiReflective) or R^T diag(d) R (CosineIII); ``eigs``
+    is the d grid (sop.eigs), ``source_psf`` the symmetrised mask it came from."""
 
-    def __init__(self, eigs, source_psf, alpha, op):
+    def __init__(self, eigs, source_psf, alpha, op, algebra=Algebra.AntiReflective):
         self.eigs = eigs
         self.source_psf = source_psf
         self.alpha = alpha
-        self.algebra = Algebra.AntiReflective
+        self.algebra = algebra
         self.n1, self.n2 = eigs.shape
         self._op = op
 
 
+_ALGEBRA_BC = {Algebra.AntiReflective: BoundaryCondition.AntiReflective,
+               Algebra.CosineIII: BoundaryCondition.Reflective}
+
+
 def build_tikhonov(p: Psf, spec: PreconditionerSpec, n1: int, n2: int, batch: int = 1) -> FilteredOperator:
-    if spec.algebra != Algebra.AntiReflective:
-        raise ValueError("build_tikhonov: this path implements the AntiReflective algebra only")
+    """preconditioner.hpp:62-85: the symmetrised mask's AR or CosineIII (reflective) spectrum, filtered."""
+    if spec.algebra not in _ALGEBRA_BC:
+        raise ValueError("build_tikhonov: this path implements the AntiReflective and CosineIII algebras")
     if spec.alpha < 0:
         raise ValueError("tikhonov_filter: alpha must be nonnegative")
     src = symmetrize(p)
-    op = BlurOperator(p, BoundaryCondition.AntiReflective, n1, n2, batch)
+    op = BlurOperator(p, _ALGEBRA_BC[spec.algebra], n1, n2, batch)
     _check(lib().dbx_precond_build(op.handle, float(spec.alpha)))
     eigs = np.empty((n1, n2))
     _check(lib().dbx_precond_eigs(op.handle, _ptr(eigs)))
-    return FilteredOperator(eigs, src, spec.alpha, op)
+    return FilteredOperator(eigs, src, spec.alpha, op, spec.algebra)
 
 
-def filter_from_eigs(eigs, n1=None, n2=None, batch: int = 1) -> FilteredOperator:
-    """A FilteredOperator with an explicit d grid (SpectralOperator{AR, eigs})."""
+def filter_from_eigs(eigs, n1=None, n2=None, batch: int = 1,
+                     algebra: Algebra = Algebra.AntiReflective) -> FilteredOperator:
+    """A FilteredOperator with an explicit d grid (SpectralOperator{algebra, eigs})."""
     eigs = np.ascontiguousarray(eigs, dtype=np.float64)
     n1, n2 = eigs.shape
-    op = BlurOperator(delta_psf(), BoundaryCondition.AntiReflective, n1, n2, batch)
+    op = BlurOperator(delta_psf(), _ALGEBRA_BC[algebra], n1, n2, batch)
     _check(lib().dbx_precond_set_eigs(op.handle, _ptr(eigs)))
-    return FilteredOperator(eigs, None, 0.0, op)
+    return FilteredOperator(eigs, None, 0.0, op, algebra)
 
 
 def precondition_apply(d: FilteredOperator, r, engine: DstEngine = DstEngine.Auto):
@@ -396,7 +403,7 @@ def precondition_apply(d: FilteredOperator, r, engine: DstEngine = DstEngine.Aut
     if (r.shape[-2], r.shape[-1]) != (d.n1, d.n2):
         raise ValueError("filter_apply: size mismatch")
     if r.ndim == 3 and r.shape[0] != d._op.batch:
-        op = filter_from_eigs(d.eigs, batch=r.shape[0])._op
+        op = filter_from_eigs(d.eigs, batch=r.shape[0], algebra=d.algebra)._op
     else:
         op = d._op
     op.set_dst(engine)
@@ -474,7 +481,7 @@ def _run(op: BlurOperator, d: Optional[FilteredOperator], g, cfg: SolverConfig, 
     if d is not None:
         if (d.n1, d.n2) != (op.n1, op.n2):
             raise ValueError("d_landweber: preconditioner size mismatch")
-        if d.algebra != Algebra.AntiReflective:
+        if _ALGEBRA_BC.get(d.algebra) != op.bc():
             raise ValueError("d_landweber: preconditioner algebra does not match the BC")
         if op._eigs_id is not id(d):
             _check(lib().dbx_precond_set_eigs(op.handle, _ptr(d.eigs)))

@@ -14,6 +14,7 @@
 // partial, or x_k = x_{k-1} + tau*A'r with ||x||^2 and ||x-f||^2 partials.
 #include <cuda_runtime.h>
 
+#include "../../include/dbx.h"
 #include "dbx_internal.h"
 
 namespace dbx {
@@ -28,8 +29,14 @@ constexpr int kTH = kWarps * kR;  // 32
 
 // AR extension of FOV row i (0 <= i < n1) at column j in [-q2, n2+q2):
 // f_{-k} = 2 f_0 - f_k, f_{n-1+k} = 2 f_{n-1} - f_{n-1-k}  (boundary.hpp:58-61)
-__device__ __forceinline__ double hext(const double* __restrict__ x, int i, int j, int n2) {
+// Reflective (bc = 2, boundary.hpp:49-55): f_{-k} = f_{k-1}, f_{n-1+k} = f_{n-k}.
+__device__ __forceinline__ double hext(const double* __restrict__ x, int i, int j, int n2, int bc) {
   const double* row = x + (size_t)i * n2;
+  if (bc == DBX_BC_REFLECTIVE) {
+    if (j < 0) return row[-j - 1];
+    if (j >= n2) return row[2 * n2 - 1 - j];
+    return row[j];
+  }
   if (j < 0) return 2.0 * row[0] - row[-j];
   if (j >= n2) return 2.0 * row[n2 - 1] - row[2 * (n2 - 1) - j];
   return row[j];
@@ -37,10 +44,15 @@ __device__ __forceinline__ double hext(const double* __restrict__ x, int i, int 
 
 // Padded value with the reference's association: rows (axis 2) extended
 // first, then columns over the widened image (boundary.hpp:93-100).
-__device__ __forceinline__ double pext(const double* __restrict__ x, int i, int j, int n1, int n2) {
-  if (i < 0) return 2.0 * hext(x, 0, j, n2) - hext(x, -i, j, n2);
-  if (i >= n1) return 2.0 * hext(x, n1 - 1, j, n2) - hext(x, 2 * (n1 - 1) - i, j, n2);
-  return hext(x, i, j, n2);
+__device__ __forceinline__ double pext(const double* __restrict__ x, int i, int j, int n1, int n2, int bc) {
+  if (bc == DBX_BC_REFLECTIVE) {
+    if (i < 0) return hext(x, -i - 1, j, n2, bc);
+    if (i >= n1) return hext(x, 2 * n1 - 1 - i, j, n2, bc);
+    return hext(x, i, j, n2, bc);
+  }
+  if (i < 0) return 2.0 * hext(x, 0, j, n2, bc) - hext(x, -i, j, n2, bc);
+  if (i >= n1) return 2.0 * hext(x, n1 - 1, j, n2, bc) - hext(x, 2 * (n1 - 1) - i, j, n2, bc);
+  return hext(x, i, j, n2, bc);
 }
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -76,7 +88,7 @@ __global__ void __launch_bounds__(kThreads) blur_ar_kernel(BlurArgs a) {
     const int ti = idx / pitch, tj = idx - ti * pitch;
     const int i = r0 - q1 + ti, j = c0 - q2 + tj;
     double v = 0.0;
-    if (i < n1 + q1 && j < n2 + q2) v = pext(x, i, j, n1, n2);
+    if (i < n1 + q1 && j < n2 + q2) v = pext(x, i, j, n1, n2, a.bc);
     S[idx] = v;
   }
   __syncthreads();

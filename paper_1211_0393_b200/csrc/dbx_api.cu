@@ -124,9 +124,23 @@ void ar_params(long n, std::vector<double>& p, double& alpha) {
   alpha = std::sqrt(1.0 + sq);
 }
 
-// kind: DBX_KIND_SINEI -> Q_n ; DBX_KIND_AR -> T_n ; DBX_KIND_ARINV -> T~_n
+// dense matrix slots: the DBX_KIND_* values, plus slot 0 for R^T (inverse cosine)
+constexpr int MK_COSINV = 0;
+
+// kind: DBX_KIND_SINEI -> Q_n ; DBX_KIND_AR -> T_n ; DBX_KIND_ARINV -> T~_n ;
+// DBX_KIND_COSINE3 -> R_n ; MK_COSINV -> R_n^T (transforms.hpp:88-110)
 std::vector<double> dense_transform(int kind, long n) {
   std::vector<double> M((size_t)(n * n), 0.0);
+  if (kind == DBX_KIND_COSINE3 || kind == MK_COSINV) {
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (long s = 0; s < n; ++s)
+      for (long t = 0; t < n; ++t) {
+        const long e = (s * (2 * t + 1)) % (4 * n);  // exact reduction of s (2t+1) pi / 2n
+        const long double v = sqrtl((s == 0 ? 1.0L : 2.0L) / (long double)n) * cosl(pi * (long double)e / (long double)(2 * n));
+        M[(size_t)(kind == MK_COSINV ? t * n + s : s * n + t)] = (double)v;
+      }
+    return M;
+  }
   if (kind == DBX_KIND_SINEI) {
     std::vector<long double> q;
     fill_q(n, q);
@@ -215,6 +229,7 @@ struct dbx_plan {
   std::string gkey;
   int64_t glaunches = 0;
   bool fusion = true;  // fused row pipelines when compiled for the sizes
+  int bc = DBX_BC_ANTIREFLECTIVE;  // BoundaryCondition of the blur (and the preconditioner algebra)
   bool last_fused = false;  // pipeline of the last landweber run
   // ---- FFT-form state ----
   int dst = DBX_DST_AUTO;
@@ -282,6 +297,35 @@ struct dbx_plan {
     if (N > 2 && is_prime(N) && rader_supported_len(N - 1)) { *M = N - 1; return CORE_RADER; }
     return -1;
   }
+  // CosineIII transforms (reflective BCs): FFT form when both line lengths are
+  // compiled DCT lengths (dct.cu), else the dense GEMM form.
+  bool use_fft_dct() const {
+    return dst != DBX_DST_DENSE && dct_supported_len(n1) && dct_supported_len(n2);
+  }
+  struct Dct {
+    bool ready = false;
+    BlueTables t;
+  } dct[2];
+  const BlueTables& dct_tables(int axis) {
+    Dct& D = dct[axis];
+    if (!D.ready) {
+      const int m = axis == 0 ? n1 : n2;
+      std::vector<double> w(2 * (size_t)m);
+      const long double pi = 3.141592653589793238462643383279502884L;
+      for (long k = 0; k < m; ++k) {  // w_k = exp(-i pi k / 2m)
+        w[2 * k] = (double)cosl(pi * (long double)k / (long double)(2 * m));
+        w[2 * k + 1] = -(double)sinl(pi * (long double)k / (long double)(2 * m));
+      }
+      D.t.tw = reinterpret_cast<const double2*>(upload_owned(twiddles(m)));
+      D.t.chirp = reinterpret_cast<const double2*>(upload_owned(w));
+      D.t.scale = (double)sqrtl(2.0L / (long double)m);
+      D.t.c0 = (double)sqrtl(1.0L / (long double)m);
+      D.t.n = m; D.t.N = m; D.t.M = m;
+      D.ready = true;
+    }
+    return D.t;
+  }
+
   bool use_fft_dst(bool sine) const {
     if (dst == DBX_DST_DENSE) return false;
     const int N1 = sine ? n1 + 1 : n1 - 1, N2 = sine ? n2 + 1 : n2 - 1;
@@ -344,7 +388,15 @@ struct dbx_plan {
   // prepare everything a run needs before graph capture (no allocation inside)
   void prepare(bool precond) {
     if (use_fft_conv()) ensure_conv();
-    if (precond) {
+    if (precond && bc == DBX_BC_REFLECTIVE) {
+      if (use_fft_dct()) {
+        dct_tables(0);
+        dct_tables(1);
+      } else {
+        matrix(DBX_KIND_COSINE3, 0); matrix(DBX_KIND_COSINE3, 1);
+        matrix(MK_COSINV, 0); matrix(MK_COSINV, 1);
+      }
+    } else if (precond) {
       if (use_fft_dst(false)) {
         blue_tables(0, false);
         blue_tables(1, false);
@@ -360,6 +412,7 @@ struct dbx_plan {
     a.n1 = n1; a.n2 = n2; a.q1 = q1; a.q2 = q2; a.batch = batch;
     a.st = stp; a.part = pt;
     a.dstride = dstride;
+    a.bc = bc;
     return a;
   }
 
@@ -458,6 +511,7 @@ struct dbx_plan {
     a.x = x; a.xsel = xsel; a.y = y; a.ysel = ysel;
     a.w = adjoint ? w_At : w_A;
     a.n1 = n1; a.n2 = n2; a.q1 = q1; a.q2 = q2; a.batch = batch;
+    a.bc = bc;
     a.mode = mode; a.g = gg; a.xold = xold; a.xoldsel = xoldsel; a.f = ff; a.tau = tau;
     a.st = stp; a.part = pt;
     int ctas = 0;
@@ -497,8 +551,49 @@ struct dbx_plan {
   // D x = T (d o (T~ x)) (or its first/last halves).  FFT form: T~ rows,
   // [T~ -> d -> T] columns, T rows with the caller's epilogue; dense form: the
   // four GEMM half-passes.  Returns the CTA count of the epilogue launch.
+  // D = R^T diag(d) R for the CosineIII algebra (spectral.hpp:147-154):
+  // forward R along rows and columns, Hadamard by d, inverse R^T along
+  // columns and rows; columns run on transposed images.
+  int apply_D_cos(const double* X, int xsel, double* Y, int ysel, int epi_spec, const double* xold,
+                  int xoldsel, const double* ff, double tau, const ImgState* stp, Partials pt) {
+    if (use_fft_dct()) {
+      SpecArgs a = spec_base(stp, pt);
+      a.blue2 = dct_tables(1);
+      a.in = X; a.insel = xsel; a.out = u.p; a.outsel = SEL_EXPLICIT; a.kind1 = +1; a.epi = SPEC_STORE;
+      ev_begin(KC_TRANSFORM);
+      lc(launch_dct_rows(a, stream), "launch_dct_rows");
+      launch_transpose(u.p, s.p, n1, n2, stream, batch);
+      SpecArgs c = a;
+      c.n1 = n2; c.n2 = n1;
+      c.blue2 = dct_tables(0);
+      c.part = Partials{nullptr, 0};
+      c.in = s.p; c.out = u.p; c.kind1 = +1; c.epi = SPEC_HADAMARD; c.d = dT.p;
+      lc(launch_dct_rows(c, stream), "launch_dct_rows");
+      c.in = u.p; c.out = s.p; c.kind1 = -1; c.epi = SPEC_STORE; c.d = nullptr;
+      lc(launch_dct_rows(c, stream), "launch_dct_rows");
+      launch_transpose(s.p, u.p, n2, n1, stream, batch);
+      ev_end();
+      launches += 4;
+      a.in = u.p; a.insel = SEL_EXPLICIT; a.out = Y; a.outsel = ysel; a.kind1 = -1;
+      a.epi = epi_spec; a.xold = xold; a.xoldsel = xoldsel; a.f = ff; a.tau = tau; a.part = pt;
+      ev_begin(KC_TRANSFORM);
+      const int ctas = lc(launch_dct_rows(a, stream), "launch_dct_rows");
+      ev_end();
+      check_launch();
+      return ctas;
+    }
+    Partials none{nullptr, 0};
+    const int gemm_epi = epi_spec == SPEC_AXPY ? EPI_AXPY : EPI_STORE;
+    pass(DBX_KIND_COSINE3, true, X, xsel, u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, stp, none);
+    pass(DBX_KIND_COSINE3, false, u.p, SEL_EXPLICIT, s.p, SEL_EXPLICIT, EPI_HADAMARD, nullptr, SEL_EXPLICIT, nullptr, 0,
+         stp, none);
+    pass(MK_COSINV, true, s.p, SEL_EXPLICIT, u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT, nullptr, 0, stp, none);
+    return pass(MK_COSINV, false, u.p, SEL_EXPLICIT, Y, ysel, gemm_epi, xold, xoldsel, ff, tau, stp, pt);
+  }
+
   int apply_D(const double* X, int xsel, double* Y, int ysel, int epi_spec, const double* xold,
               int xoldsel, const double* ff, double tau, const ImgState* stp, Partials pt) {
+    if (bc == DBX_BC_REFLECTIVE) return apply_D_cos(X, xsel, Y, ysel, epi_spec, xold, xoldsel, ff, tau, stp, pt);
     if (use_fft_dst(false)) {
       SpecArgs a = spec_base(stp, pt);
       a.blue1 = blue_tables(0, false);
@@ -605,12 +700,16 @@ int dbx_plan_create(int n1, int n2, int batch, const double* taps, int q1, int q
   return guarded([&] {
     require(out != nullptr, "dbx_plan_create: null out");
     *out = nullptr;
-    require(bc == DBX_BC_ANTIREFLECTIVE, "dbx_plan_create: only AntiReflective BCs are implemented");
+    require(bc == DBX_BC_ANTIREFLECTIVE || bc == DBX_BC_REFLECTIVE,
+            "dbx_plan_create: implemented BCs are AntiReflective and Reflective");
     validate_taps(taps, q1, q2);
-    // blur.hpp:26-29 + boundary.hpp:66-81 (AR branch)
+    // blur.hpp:26-29 + boundary.hpp:66-81
     require(n1 >= 1 && n2 >= 1, "BlurOperator: empty field of view");
-    require((q1 == 0 || q1 <= n1 - 2) && (q2 == 0 || q2 <= n2 - 2),
-            "anti-reflective support condition violated (q > n-2)");
+    if (bc == DBX_BC_REFLECTIVE)
+      require(q1 <= n1 && q2 <= n2, "reflective support condition violated (q > n)");
+    else
+      require((q1 == 0 || q1 <= n1 - 2) && (q2 == 0 || q2 <= n2 - 2),
+              "anti-reflective support condition violated (q > n-2)");
     require(batch >= 1, "dbx_plan_create: batch must be >= 1");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -623,6 +722,7 @@ int dbx_plan_create(int n1, int n2, int batch, const double* taps, int q1, int q
     if (pr.major != 10) throw CudaErr("device is not sm_100 (Blackwell B200)");
     auto P = std::make_unique<dbx_plan>();
     P->n1 = n1; P->n2 = n2; P->batch = batch; P->q1 = q1; P->q2 = q2; P->device = device;
+    P->bc = bc;
     P->N = (size_t)n1 * n2;
     const size_t nt = (size_t)(2 * q1 + 1) * (2 * q2 + 1);
     P->taps.assign(taps, taps + nt);
@@ -752,16 +852,20 @@ int dbx_precond_build(dbx_plan* P, double alpha) {
   return guarded([&] {
     require(P != nullptr, "null plan");
     require(alpha >= 0.0, "tikhonov_filter: alpha must be nonnegative");
-    // eig_antireflective preconditions (spectral.hpp:122-126)
-    require(P->n1 >= 3 && P->n2 >= 3, "eig_antireflective: sizes must be >= 3");
-    require(P->q1 <= P->n1 - 2 && P->q2 <= P->n2 - 2, "eig_antireflective: support condition violated");
+    // eig_antireflective preconditions (spectral.hpp:122-126); eig_reflective
+    // has none beyond the (symmetrised) mask's symmetry (spectral.hpp:75-84)
+    if (P->bc == DBX_BC_ANTIREFLECTIVE) {
+      require(P->n1 >= 3 && P->n2 >= 3, "eig_antireflective: sizes must be >= 3");
+      require(P->q1 <= P->n1 - 2 && P->q2 <= P->n2 - 2, "eig_antireflective: support condition violated");
+    }
     P->set_dev();
     P->ensure_d(P->N);
     P->dstride = 0;
     int* flag = nullptr;
     ck(cudaMalloc(&flag, sizeof(int)), "cudaMalloc");
     ck(cudaMemsetAsync(flag, 0, sizeof(int), P->stream), "memset");
-    launch_build_filter(P->sym, P->q1, P->q2, P->n1, P->n2, alpha, P->d, flag, P->stream);
+    launch_build_filter(P->sym, P->q1, P->q2, P->n1, P->n2, alpha, P->d, flag, P->stream,
+                        P->bc == DBX_BC_REFLECTIVE ? 1 : 0);
     P->launches += 3;
     P->check_launch();
     int hflag = 0;
@@ -798,6 +902,7 @@ int dbx_slab_blur(dbx_plan* P, const double* x_ext, double* y, int adjoint, cons
     require(P->batch == 1, "slab_blur: one slab per plan");
     require(is_device_ptr(x_ext) && is_device_ptr(y) && (!g || is_device_ptr(g)), "slab_blur: device pointers");
     require(P->use_fft_conv(), "slab_blur: needs the FFT correlation engine");
+    require(P->bc == DBX_BC_ANTIREFLECTIVE, "slab_blur: anti-reflective slabs only");
     P->set_dev();
     P->ensure_conv();
     P->zb.ensure((size_t)(P->n1 + 2 * P->q1) * P->Lh * 2);
@@ -879,7 +984,7 @@ int dbx_precond_block(dbx_plan* P, int n1g, int n2g, double alpha, int r0, int n
     ck(cudaMalloc(&flag, sizeof(int)), "cudaMalloc");
     ck(cudaMemsetAsync(flag, 0, sizeof(int), P->stream), "memset");
     launch_build_filter_block(P->sym, P->q1, P->q2, n1g, n2g, alpha, r0, nr, c0, nc, transpose != 0, out, flag,
-                              P->stream);
+                              P->stream, P->bc == DBX_BC_REFLECTIVE ? 1 : 0);
     P->launches += 3;
     P->check_launch();
     int hflag = 0;
@@ -943,8 +1048,10 @@ int dbx_transpose(dbx_plan* P, const double* in, double* out, int rows, int cols
 int dbx_precond_build_sweep(dbx_plan* P, const double* alphas) {
   return guarded([&] {
     require(P && alphas, "null argument");
-    require(P->n1 >= 3 && P->n2 >= 3, "eig_antireflective: sizes must be >= 3");
-    require(P->q1 <= P->n1 - 2 && P->q2 <= P->n2 - 2, "eig_antireflective: support condition violated");
+    if (P->bc == DBX_BC_ANTIREFLECTIVE) {
+      require(P->n1 >= 3 && P->n2 >= 3, "eig_antireflective: sizes must be >= 3");
+      require(P->q1 <= P->n1 - 2 && P->q2 <= P->n2 - 2, "eig_antireflective: support condition violated");
+    }
     for (int b = 0; b < P->batch; ++b) require(alphas[b] >= 0.0, "tikhonov_filter: alpha must be nonnegative");
     P->set_dev();
     const size_t B = (size_t)P->batch;
@@ -953,7 +1060,8 @@ int dbx_precond_build_sweep(dbx_plan* P, const double* alphas) {
     ck(cudaMalloc(&flag, B * sizeof(int)), "cudaMalloc");
     ck(cudaMemsetAsync(flag, 0, B * sizeof(int), P->stream), "memset");
     for (size_t b = 0; b < B; ++b)
-      launch_build_filter(P->sym, P->q1, P->q2, P->n1, P->n2, alphas[b], P->d + b * P->N, flag + b, P->stream);
+      launch_build_filter(P->sym, P->q1, P->q2, P->n1, P->n2, alphas[b], P->d + b * P->N, flag + b, P->stream,
+                          P->bc == DBX_BC_REFLECTIVE ? 1 : 0);
     P->launches += 3 * (int64_t)B;
     P->check_launch();
     std::vector<int> hflag(B);
@@ -1000,7 +1108,8 @@ int dbx_precond_apply(dbx_plan* P, const double* r, double* y) {
   return guarded([&] {
     require(P && r && y, "null argument");
     require(P->have_d, "precondition_apply: filter not built");
-    require(P->n1 >= 3 && P->n2 >= 3, "tensor_apply: anti-reflective transform needs sizes >= 3");
+    require(P->bc == DBX_BC_REFLECTIVE || (P->n1 >= 3 && P->n2 >= 3),
+            "tensor_apply: anti-reflective transform needs sizes >= 3");
     P->set_dev();
     const size_t cnt = P->N * P->batch;
     const double* rin = stage_in(P, r, P->in, cnt);
@@ -1021,9 +1130,9 @@ int dbx_precond_apply(dbx_plan* P, const double* r, double* y) {
 int dbx_tensor_apply(dbx_plan* P, int kind, const double* x, double* y) {
   return guarded([&] {
     require(P && x && y, "null argument");
-    require(kind == DBX_KIND_SINEI || kind == DBX_KIND_AR || kind == DBX_KIND_ARINV,
+    require(kind == DBX_KIND_SINEI || kind == DBX_KIND_AR || kind == DBX_KIND_ARINV || kind == DBX_KIND_COSINE3,
             "tensor_apply: unsupported kind");
-    if (kind != DBX_KIND_SINEI)
+    if (kind == DBX_KIND_AR || kind == DBX_KIND_ARINV)
       require(P->n1 >= 3 && P->n2 >= 3, "tensor_apply: anti-reflective transform needs sizes >= 3");
     P->set_dev();
     const size_t cnt = P->N * P->batch;
@@ -1036,7 +1145,31 @@ int dbx_tensor_apply(dbx_plan* P, int kind, const double* x, double* y) {
     }
     Partials none{nullptr, 0};
     const bool sine = kind == DBX_KIND_SINEI;
-    if (P->use_fft_dst(sine)) {
+    if (kind == DBX_KIND_COSINE3) {
+      // R along rows, then (transposed) along columns (transforms.hpp:198-204)
+      if (P->use_fft_dct()) {
+        P->s.ensure(cnt);
+        SpecArgs a = P->spec_base(nullptr, none);
+        a.blue2 = P->dct_tables(1);
+        a.in = xin; a.out = P->u.p; a.kind1 = +1; a.epi = SPEC_STORE;
+        P->ev_begin(KC_TRANSFORM);
+        lc(launch_dct_rows(a, P->stream), "launch_dct_rows");
+        launch_transpose(P->u.p, P->s.p, P->n1, P->n2, P->stream, P->batch);
+        SpecArgs c = a;
+        c.n1 = P->n2; c.n2 = P->n1; c.blue2 = P->dct_tables(0);
+        c.in = P->s.p; c.out = P->u.p;
+        lc(launch_dct_rows(c, P->stream), "launch_dct_rows");
+        launch_transpose(P->u.p, yout, P->n2, P->n1, P->stream, P->batch);
+        P->ev_end();
+        P->launches += 3;
+        P->check_launch();
+      } else {
+        P->pass(DBX_KIND_COSINE3, true, xin, SEL_EXPLICIT, P->u.p, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT,
+                nullptr, 0, nullptr, none);
+        P->pass(DBX_KIND_COSINE3, false, P->u.p, SEL_EXPLICIT, yout, SEL_EXPLICIT, EPI_STORE, nullptr, SEL_EXPLICIT,
+                nullptr, 0, nullptr, none);
+      }
+    } else if (P->use_fft_dst(sine)) {
       // rows then columns (Kronecker order is immaterial; the reference runs
       // columns first, transforms.hpp:183-190)
       SpecArgs a = P->spec_base(nullptr, none);
@@ -1088,7 +1221,8 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
     require(stop_kind != DBX_STOP_RESIDUAL || resid_eps > 0.0, "StoppingRule: threshold must be positive");
     if (use_precond) {
       require(P->have_d, "d_landweber: preconditioner not built");
-      require(P->n1 >= 3 && P->n2 >= 3, "tensor_apply: anti-reflective transform needs sizes >= 3");
+      require(P->bc == DBX_BC_REFLECTIVE || (P->n1 >= 3 && P->n2 >= 3),
+              "tensor_apply: anti-reflective transform needs sizes >= 3");
     }
     P->set_dev();
     const int B = P->batch;
@@ -1122,7 +1256,8 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
 
     // Fused FFT-form pipeline (fused.cu): 6 launches + finalize per iteration.
     P->prepare(use_precond != 0);
-    const bool fused = method == 0 && use_precond && P->n1 == P->n2 && P->use_fft_conv() && P->use_fft_dst(false) &&
+    const bool fused = method == 0 && use_precond && P->bc == DBX_BC_ANTIREFLECTIVE && P->n1 == P->n2 &&
+                       P->use_fft_conv() && P->use_fft_dst(false) &&
                        P->fusion &&
                        P->blue_tables(1, false).core != CORE_RADER &&
                        fused_supported(P->L2, P->blue_tables(1, false).M,

@@ -57,6 +57,7 @@ struct BlurArgs {
   const double* w;                    // correlation weights (2q1+1)(2q2+1), oriented
   int n1, n2, q1, q2, batch;
   int mode;
+  int bc;                             // DBX_BC_ANTIREFLECTIVE / DBX_BC_REFLECTIVE
   const double* g;                    // RESID: data
   const double* xold; int xoldsel;    // AXPY: x_{k-1}
   const double* f;                    // AXPY: true image (nullable)
@@ -88,10 +89,12 @@ struct GemmArgs {
 void launch_gemm(const GemmArgs& a, cudaStream_t s, int* ctas_per_image);
 
 // ---- spectrum, norms, finalize -----------------------------------------
+// grid 0: anti-reflective grid, 1: reflective (DCT-III) grid
 void launch_build_filter(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha,
-                         double* d, int* zero_flag, cudaStream_t s);
+                         double* d, int* zero_flag, cudaStream_t s, int grid = 0);
 void launch_build_filter_block(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha, int r0,
-                               int nr, int c0, int nc, int tr, double* d, int* zero_flag, cudaStream_t s);
+                               int nr, int c0, int nc, int tr, double* d, int* zero_flag, cudaStream_t s,
+                               int grid = 0);
 void launch_norms_init(const double* g, const double* f, int batch, size_t N, ImgState* st,
                        double* scratch, cudaStream_t s);
 struct FinalizeArgs {

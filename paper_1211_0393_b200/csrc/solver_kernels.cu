@@ -21,12 +21,14 @@ constexpr double kPi = 3.141592653589793238462643383279502884;
 // cos(s * x_r) tables on the AR grid x_0 = 0, x_r = r*pi/(n-1), x_{n-1} = 0
 // (spectral.hpp:63-69); argument formed exactly like the reference
 // (double(r)*kPi/double(n-1), then s*x) so both sides see the same angle.
-__global__ void cos_table_kernel(int n, int q, double* tab) {
+// grid 1: the reflective (DCT-III) grid x_r = r pi / n (spectral.hpp:50-54)
+__global__ void cos_table_kernel(int n, int q, double* tab, int grid) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * (q + 1)) return;
   const int r = idx / (q + 1), s = idx - r * (q + 1);
   double x = 0.0;
-  if (r >= 1 && r <= n - 2) x = (double)r * kPi / (double)(n - 1);
+  if (grid == 1) x = (double)r * kPi / (double)n;
+  else if (r >= 1 && r <= n - 2) x = (double)r * kPi / (double)(n - 1);
   tab[idx] = cos((double)s * x);
 }
 
@@ -208,22 +210,23 @@ __global__ void zero_kernel(double* p, size_t n) {
 }  // namespace
 
 void launch_build_filter(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha,
-                         double* d, int* zero_flag, cudaStream_t s) {
-  launch_build_filter_block(sym_taps, q1, q2, n1, n2, alpha, 0, n1, 0, n2, 0, d, zero_flag, s);
+                         double* d, int* zero_flag, cudaStream_t s, int grid) {
+  launch_build_filter_block(sym_taps, q1, q2, n1, n2, alpha, 0, n1, 0, n2, 0, d, zero_flag, s, grid);
 }
 
 void launch_build_filter_block(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha, int r0,
-                               int nr, int c0, int nc, int tr, double* d, int* zero_flag, cudaStream_t s) {
+                               int nr, int c0, int nc, int tr, double* d, int* zero_flag, cudaStream_t s,
+                               int grid) {
   double *c1 = nullptr, *c2 = nullptr;
   cudaMallocAsync(&c1, sizeof(double) * (size_t)n1 * (q1 + 1), s);
   cudaMallocAsync(&c2, sizeof(double) * (size_t)n2 * (q2 + 1), s);
-  cos_table_kernel<<<(n1 * (q1 + 1) + 255) / 256, 256, 0, s>>>(n1, q1, c1);
-  cos_table_kernel<<<(n2 * (q2 + 1) + 255) / 256, 256, 0, s>>>(n2, q2, c2);
+  cos_table_kernel<<<(n1 * (q1 + 1) + 255) / 256, 256, 0, s>>>(n1, q1, c1, grid);
+  cos_table_kernel<<<(n2 * (q2 + 1) + 255) / 256, 256, 0, s>>>(n2, q2, c2, grid);
   const size_t sm = sizeof(double) * (2 * q1 + 1) * (2 * q2 + 1);
   if (sm > 48 * 1024)
     cudaFuncSetAttribute(filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 grid((nc + 127) / 128, nr);
-  filter_kernel<<<grid, 128, sm, s>>>(sym_taps, q1, q2, n1, n2, c1, c2, alpha, d, zero_flag, r0, nr, c0, nc, tr);
+  dim3 fgrid((nc + 127) / 128, nr);
+  filter_kernel<<<fgrid, 128, sm, s>>>(sym_taps, q1, q2, n1, n2, c1, c2, alpha, d, zero_flag, r0, nr, c0, nc, tr);
   cudaFreeAsync(c1, s);
   cudaFreeAsync(c2, s);
 }

@@ -58,8 +58,8 @@ conv_row_fwd(SpecArgs a) {
     vb[i] = 0.0;
     if (p < wext) {
       const int j = p - q2;
-      if (ra < n1) va[i] = hext(x, ra, j, n2);
-      if (rb < n1) vb[i] = hext(x, rb, j, n2);
+      if (ra < n1) va[i] = hext(x, ra, j, n2, a.bc);
+      if (rb < n1) vb[i] = hext(x, rb, j, n2, a.bc);
     }
   }
 #pragma unroll
@@ -132,9 +132,13 @@ conv_col(SpecArgs a) {
       double2 v = make_double2(0.0, 0.0);
       if (kk < Lh && p < hext_rows) {
         const int rho = p - q1;
-        const int r0 = rho < 0 ? 0 : n1 - 1, ri = rho < 0 ? -rho : 2 * (n1 - 1) - rho;
-        const double2 z0 = buf[pad<L1>(r0 + q1)], zi = buf[pad<L1>(ri + q1)];
-        v = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
+        if (a.bc == DBX_BC_REFLECTIVE) {
+          v = buf[pad<L1>((rho < 0 ? -rho - 1 : 2 * n1 - 1 - rho) + q1)];
+        } else {
+          const int r0 = rho < 0 ? 0 : n1 - 1, ri = rho < 0 ? -rho : 2 * (n1 - 1) - rho;
+          const double2 z0 = buf[pad<L1>(r0 + q1)], zi = buf[pad<L1>(ri + q1)];
+          v = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
+        }
       }
       buf[pad<L1>(p)] = v;
     }
@@ -161,7 +165,10 @@ conv_col(SpecArgs a) {
         v[i] = Z[(size_t)p * Lh + k];  // row slab: halo / global AR rows supplied by the caller
       } else if (idx < L1 * G && k < Lh && p < hext_rows) {
         const int rho = p - q1;
-        if (rho < 0) {
+        if (a.bc == DBX_BC_REFLECTIVE && (rho < 0 || rho >= n1)) {
+          // reflective rows are copies: Z[-i] = Z[i-1], Z[n-1+i] = Z[n-i]
+          v[i] = Z[(size_t)(rho < 0 ? -rho - 1 : 2 * n1 - 1 - rho) * Lh + k];
+        } else if (rho < 0) {
           const double2 z0 = Z[k], zi = Z[(size_t)(-rho) * Lh + k];
           v[i] = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
         } else if (rho >= n1) {

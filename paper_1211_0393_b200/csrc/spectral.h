@@ -37,6 +37,7 @@ struct BlueTables {
   const int* ridx = nullptr;   // Rader: position of Z_l in the convolution output, l in [1, N)
   int core = 0;                // DstCore
   double rinv = 1.0;  // 1 / (n - 1): ramp p_j = 1 - j rinv computed in registers
+  double c0 = 0.0;    // DCT (CosineIII): sqrt(1/m) for k = 0 (scale = sqrt(2/m) otherwise)
   double alpha = 1.0;
   double scale = 1.0;  // sqrt(2/N)
   int n = 0, N = 0, M = 0;
@@ -47,6 +48,7 @@ struct SpecArgs {
   double* out = nullptr; int outsel = SEL_EXPLICIT;
   int n1 = 0, n2 = 0, q1 = 0, q2 = 0, batch = 0;
   int epi = SPEC_STORE;
+  int bc = DBX_BC_ANTIREFLECTIVE;                // blur extension (boundary.hpp:33-64)
   const double* g = nullptr;                     // RESID
   const double* xold = nullptr; int xoldsel = SEL_EXPLICIT;  // AXPY
   const double* f = nullptr;                     // AXPY (nullable)
@@ -84,6 +86,10 @@ int launch_conv_row_fwd(const SpecArgs& a, cudaStream_t s);
 int launch_conv_col(const SpecArgs& a, cudaStream_t s);
 int launch_conv_row_inv(const SpecArgs& a, cudaStream_t s);
 int launch_dst_rows(const SpecArgs& a, cudaStream_t s);
+// CosineIII transforms along rows (dct.cu): kind1 = +1 forward R (DCT-II),
+// -1 inverse R^T (DCT-III); blue2 carries the DCT tables (chirp = e^{-i pi k / 2m}).
+int launch_dct_rows(const SpecArgs& a, cudaStream_t s);
+int dct_supported_len(int m);
 int launch_dst_cols(const SpecArgs& a, cudaStream_t s);
 
 // Fused row pipelines of the preconditioned iteration (fused.cu).

@@ -106,8 +106,14 @@ __device__ __forceinline__ const double2* stage_twiddles(double2* dst, const dou
 }
 constexpr int kSmemCap = 200 * 1024;
 
-__device__ __forceinline__ double hext(const double* __restrict__ x, int i, int j, int n2) {
+__device__ __forceinline__ double hext(const double* __restrict__ x, int i, int j, int n2,
+                                       int bc = DBX_BC_ANTIREFLECTIVE) {
   const double* row = x + (size_t)i * n2;
+  if (bc == DBX_BC_REFLECTIVE) {  // f_{-k} = f_{k-1}, f_{n-1+k} = f_{n-k} (boundary.hpp:49-55)
+    if (j < 0) return row[-j - 1];
+    if (j >= n2) return row[2 * n2 - 1 - j];
+    return row[j];
+  }
   if (j < 0) return 2.0 * row[0] - row[-j];
   if (j >= n2) return 2.0 * row[n2 - 1] - row[2 * (n2 - 1) - j];
   return row[j];

@@ -46,7 +46,10 @@ def test_plan_argument_validation(dbx):
     assert L.dbx_plan_create(8, 8, 1, dbx._ptr(bad), 1, 1, 3, 0, C.byref(h)) == dbx.DBX_EINVAL
     assert "sum to 1" in L.dbx_last_error().decode()
     ok = np.full((3, 3), 1.0 / 9)
-    assert L.dbx_plan_create(8, 8, 1, dbx._ptr(ok), 1, 1, 2, 0, C.byref(h)) == dbx.DBX_EINVAL  # Reflective
+    assert L.dbx_plan_create(8, 8, 1, dbx._ptr(ok), 1, 1, 1, 0, C.byref(h)) == dbx.DBX_EINVAL  # Periodic
+    tall = np.full((5, 3), 1.0 / 15)
+    assert L.dbx_plan_create(1, 8, 1, dbx._ptr(tall), 2, 1, 2, 0, C.byref(h)) == dbx.DBX_EINVAL  # Reflective, q > n
+    assert "reflective support condition" in L.dbx_last_error().decode()
     big = np.full((9, 9), 1.0 / 81)
     assert L.dbx_plan_create(5, 5, 1, dbx._ptr(big), 4, 4, 3, 0, C.byref(h)) == dbx.DBX_EINVAL
     assert "support condition" in L.dbx_last_error().decode()
