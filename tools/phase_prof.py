@@ -17,7 +17,7 @@ NAMES = {0: "dst_tcols:stage", 1: "dst_tcols:fill1", 2: "dst_tcols:fft1", 3: "ds
          10: "t_axpy:stage", 11: "t_axpy:fill", 12: "t_axpy:dft", 13: "t_axpy:split+scan",
          14: "t_axpy:x-update", 15: "t_axpy:conv-fwd", 20: "ainv_tt:load", 21: "ainv_tt:inv-fft",
          22: "ainv_tt:rows", 23: "ainv_tt:fill", 24: "ainv_tt:dft", 25: "ainv_tt:split+scan",
-         26: "ainv_tt:store"}
+         26: "ainv_tt:store", 40: "dst-fft:stage1(r31)", 41: "dst-fft:stage2(r11)", 42: "dst-fft:stage3(r3)"}
 
 
 def main():
@@ -42,7 +42,7 @@ def main():
     run()
     L.dbx_debug_phases(buf, 64)
     v = np.array(buf[:64], dtype=np.float64)
-    for lo, hi in ((0, 10), (10, 20), (20, 30)):
+    for lo, hi in ((0, 10), (10, 20), (20, 30), (40, 43)):
         tot = v[lo:hi].sum()
         if tot <= 0:
             continue
