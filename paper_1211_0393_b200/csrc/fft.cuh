@@ -422,7 +422,8 @@ __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ 
 // KP pairs (4 KP independent FMA chains, constants as immediate operands).
 // The outputs stay in registers (out[2u] = X_{K0+u}, out[2u+1] = X_{R-K0-u}).
 template <int R, int S, int L, int K0, int K1>
-__device__ __forceinline__ void odd_pairs_smem(const double2* buf, int b, int NB, double2 x0, double2* out) {
+__device__ __forceinline__ void odd_pairs_smem(const double2* buf, int b, int NB, double2 x0, double2* out,
+                                               double2* sum = nullptr) {
   using K = OddConst<R>;
   constexpr int H = (R - 1) / 2;
   constexpr int KP = K1 - K0 + 1;
@@ -435,6 +436,7 @@ __device__ __forceinline__ void odd_pairs_smem(const double2* buf, int b, int NB
 #pragma unroll
   for (int j = 1; j <= H; ++j) {
     const double2 a = buf[pad<L>(b + j * NB)], c = buf[pad<L>(b + (R - j) * NB)];
+    if (sum) *sum = cadd(*sum, a);
 #pragma unroll
     for (int u = 0; u < KP; ++u) {
       const int e = (j * (K0 + u)) % R;
@@ -454,13 +456,13 @@ __device__ __forceinline__ void odd_pairs_smem(const double2* buf, int b, int NB
 
 template <int R, int S, int L, int H, int P, int Q, int KPM>
 __device__ __forceinline__ void odd_pairs_smem_dispatch(int part, const double2* buf, int b, int NB, double2 x0,
-                                                        double2* out) {
+                                                        double2* out, double2* sum0 = nullptr) {
   if constexpr (Q < P) {
     if (part == Q) {
-      odd_pairs_smem<R, S, L, 1 + (Q * H) / P, ((Q + 1) * H) / P>(buf, b, NB, x0, out);
+      odd_pairs_smem<R, S, L, 1 + (Q * H) / P, ((Q + 1) * H) / P>(buf, b, NB, x0, out, Q == 0 ? sum0 : nullptr);
       return;
     }
-    odd_pairs_smem_dispatch<R, S, L, H, P, Q + 1, KPM>(part, buf, b, NB, x0, out);
+    odd_pairs_smem_dispatch<R, S, L, H, P, Q + 1, KPM>(part, buf, b, NB, x0, out, sum0);
   }
 }
 
@@ -507,8 +509,21 @@ __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __rest
   double2* buf = sm + line * PL;
   const int k = b % Ns;
   double2 sum = make_double2(0.0, 0.0);
-  if (act && part == 0) {
-    if constexpr (Ns > 1) {
+  if constexpr (Ns == 1) {
+    // no twiddles: every replica folds its own share of the pairs; replica 0
+    // accumulates X_0 while it sweeps the pairs in phase 2
+    if (act) {
+      const int j0 = 1 + (part * H) / P, j1 = ((part + 1) * H) / P;
+      for (int j = j0; j <= j1; ++j) {
+        double2& vj = buf[pad<L>(b + j * NB)];
+        double2& vm = buf[pad<L>(b + (R - j) * NB)];
+        const double2 x = vj, y = vm;
+        vj = cadd(x, y);
+        vm = csub(x, y);
+      }
+    }
+  } else if (act && part == 0) {
+    {
       // twiddle the inputs in place (r = 1..R-1), powers by the window scheme
       constexpr int step = L / (Ns * R);
       const double2 w1 = tw[k * step];
@@ -539,7 +554,14 @@ __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __rest
   }
   __syncthreads();
   double2 out[2 * KPM];
-  if (act) odd_pairs_smem_dispatch<R, S, L, H, P, 0, KPM>(part, buf, b, NB, buf[pad<L>(b)], out);
+  if constexpr (Ns == 1) {
+    if (act) {
+      sum = buf[pad<L>(b)];
+      odd_pairs_smem_dispatch<R, S, L, H, P, 0, KPM>(part, buf, b, NB, sum, out, &sum);
+    }
+  } else if (act) {
+    odd_pairs_smem_dispatch<R, S, L, H, P, 0, KPM>(part, buf, b, NB, buf[pad<L>(b)], out);
+  }
   __syncthreads();
   if (act) {
     const int base = (b / Ns) * Ns * R + k;

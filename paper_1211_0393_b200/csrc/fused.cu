@@ -94,18 +94,20 @@ __device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, 
                                               int Lh, int t, int bar) {
   const int wext = n2 + 2 * q2;
   const bool has_a = ra < n1, has_b = rb < n1;
-  auto ext = [&](const double* row, int j) -> double {
-    if (j < 0) return 2.0 * row[0] - row[-j];
-    if (j >= n2) return 2.0 * row[n2 - 1] - row[2 * (n2 - 1) - j];
-    return row[j];
-  };
+  // interior samples are plain copies; only the 2 q2 mirrored samples and
+  // the zero tail take the (warp-local) boundary branch
+#pragma unroll 4
   for (int p = t; p < L2; p += T) {
-    double va = 0.0, vb = 0.0;
-    if (p < wext) {
-      if (has_a) va = ext(rowa, p - q2);
-      if (has_b) vb = ext(rowb, p - q2);
+    const int j = p - q2;
+    int jc = j < 0 ? -j : j >= n2 ? 2 * (n2 - 1) - j : j;
+    jc = jc < 0 ? 0 : jc;
+    double va = rowa[jc], vb = rowb[jc];
+    if (j < 0 || j >= n2) {
+      const int e = j < 0 ? 0 : n2 - 1;
+      va = p < wext ? 2.0 * rowa[e] - va : 0.0;
+      vb = p < wext ? 2.0 * rowb[e] - vb : 0.0;
     }
-    buf[pad<L2>(p)] = make_double2(va, vb);
+    buf[pad<L2>(p)] = make_double2(has_a ? va : 0.0, has_b ? vb : 0.0);
   }
   fft::line_sync(bar, T);
   fft::fft<L2, -1, T>(buf, tw, t, bar);
@@ -196,8 +198,11 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
     double* uT = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + r0 + h;
     const double* o = rowS + h * LS;
     const double u0 = bt.alpha * e0[h], ue = bt.alpha * e1[h];
-    for (int k = threadIdx.x >> 2; k < n2; k += NT / 4)
-      uT[(size_t)k * n1] = (k == 0) ? u0 : (k == n2 - 1) ? ue : pk_at<LMAX>(o, k);
+#pragma unroll 4
+    for (int k = threadIdx.x >> 2; k < n2; k += NT / 4) {
+      const double v = pk_at<LMAX>(o, k);  // o[0], o[n2-1] in bounds
+      uT[(size_t)k * n1] = (k == 0) ? u0 : (k == n2 - 1) ? ue : v;
+    }
   }
   PH(26)
 }
@@ -276,15 +281,11 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
     double* xs = stX + h * LS;
     const double* fs = fS + h * LS;
     double* xr = xn + (size_t)h * n2;
-#pragma unroll 2
+#pragma unroll 4
     for (int k = threadIdx.x; k < n2; k += NT) {
-      double w;
-      if (k == 0) w = a0;
-      else if (k == n2 - 1) w = a1;
-      else {
-        const double t1 = (double)k * ri;
-        w = pk_at<LMAX>(o, k) + a0 * (1.0 - t1) + a1 * t1;
-      }
+      const double t1 = (double)k * ri;
+      double w = pk_at<LMAX>(o, k) + a0 * (1.0 - t1) + a1 * t1;  // o[0], o[n2-1] in bounds
+      w = k == 0 ? a0 : k == n2 - 1 ? a1 : w;
       const double xv = xs[k] + tau * w;
       xr[k] = xv;
       xs[k] = xv;
@@ -513,15 +514,11 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
     double* s = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c0 + h;
     const double* o = io + h * LSO;
     const double a0 = e0[h] * dS[h * LS], a1 = e1[h] * dS[h * LS + n - 1];
+#pragma unroll 4
     for (int k = threadIdx.x >> 2; k < n; k += NT / 4) {
-      double w;
-      if (k == 0) w = a0;
-      else if (k == n - 1) w = a1;
-      else {
-        const double t1 = (double)k * ri;
-        w = pk_at<LMAX>(o, k) + a0 * (1.0 - t1) + a1 * t1;
-      }
-      s[(size_t)k * n2] = w;
+      const double t1 = (double)k * ri;
+      const double w = pk_at<LMAX>(o, k) + a0 * (1.0 - t1) + a1 * t1;  // o[0], o[n-1] in bounds
+      s[(size_t)k * n2] = k == 0 ? a0 : k == n - 1 ? a1 : w;
     }
   }
   PH(9)
