@@ -17,6 +17,8 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "dft_consts.h"
 
 namespace dbx {
@@ -351,9 +353,18 @@ __device__ __forceinline__ void line_sync(int id, int nthreads) {
   }
 }
 
-// One Stockham stage on a padded in-smem line.
-template <int L, int Ns, int R, int S, int T>
-__device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ tw, int t, int bar = 0) {
+// Default input of a stage: the line itself.
+struct LineIn {};
+
+// One Stockham stage on a padded in-smem line.  With an input functor fin
+// (first stage only), v = fin(i) replaces the load of natural index i: the
+// producer of the line (pointwise spectrum product, residual, extension) is
+// folded into the stage's loads instead of a separate smem pass + barrier.
+// fin may read the line itself: every load precedes the stage's barrier.
+template <int L, int Ns, int R, int S, int T, typename F = LineIn>
+__device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ tw, int t, int bar = 0,
+                                      F fin = F()) {
+  constexpr bool FIN = !std::is_same<F, LineIn>::value;
   constexpr int NB = L / R;
   constexpr int PER = (NB + T - 1) / T;
   double2 v[PER][R];
@@ -376,7 +387,10 @@ __device__ __forceinline__ void stage(double2* buf, const double2* __restrict__ 
   for (int i = 0; i < PER; ++i) {
     const int b = t + i * T;
     if (NB % T == 0 || b < NB) {
-      if constexpr (LIN_IN) {
+      if constexpr (FIN) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[i][r] = fin(b + r * NB);
+      } else if constexpr (LIN_IN) {
         const double2* src = buf + pad<L>(b);
 #pragma unroll
         for (int r = 0; r < R; ++r) v[i][r] = src[r * SIN];
@@ -614,6 +628,16 @@ template <int L, int S, int T>
 __device__ __forceinline__ void fft(double2* buf, const double2* __restrict__ tw, int t, int bar = 0) {
   static_assert(supported(L), "unsupported FFT length");
   run_stages<L, 1, S, T>(buf, tw, t, bar);
+}
+
+// As fft, with the first stage's inputs produced by fin(natural index) (see
+// stage); the line's previous contents may be read by fin.
+template <int L, int S, int T, typename F>
+__device__ __forceinline__ void fft_in(double2* buf, const double2* __restrict__ tw, int t, int bar, F fin) {
+  static_assert(supported(L), "unsupported FFT length");
+  constexpr int R = next_radix(L);
+  stage<L, 1, R, S, T>(buf, tw, t, bar, fin);
+  run_stages<L, R, S, T>(buf, tw, t, bar);
 }
 
 }  // namespace fft

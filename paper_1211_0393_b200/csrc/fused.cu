@@ -94,10 +94,10 @@ __device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, 
                                               int Lh, int t, int bar) {
   const int wext = n2 + 2 * q2;
   const bool has_a = ra < n1, has_b = rb < n1;
-  // interior samples are plain copies; only the 2 q2 mirrored samples and
-  // the zero tail take the (warp-local) boundary branch
-#pragma unroll 4
-  for (int p = t; p < L2; p += T) {
+  // the AR-extended rows are produced inside the first FFT stage's loads:
+  // interior samples are plain copies; only the 2 q2 mirrored samples and the
+  // zero tail take the (warp-local) boundary branch
+  fft::fft_in<L2, -1, T>(buf, tw, t, bar, [&](int p) {
     const int j = p - q2;
     int jc = j < 0 ? -j : j >= n2 ? 2 * (n2 - 1) - j : j;
     jc = jc < 0 ? 0 : jc;
@@ -107,10 +107,8 @@ __device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, 
       va = p < wext ? 2.0 * rowa[e] - va : 0.0;
       vb = p < wext ? 2.0 * rowb[e] - vb : 0.0;
     }
-    buf[pad<L2>(p)] = make_double2(has_a ? va : 0.0, has_b ? vb : 0.0);
-  }
-  fft::line_sync(bar, T);
-  fft::fft<L2, -1, T>(buf, tw, t, bar);
+    return make_double2(has_a ? va : 0.0, has_b ? vb : 0.0);
+  });
   const bool pair = has_b && ((ra | n1) & 1) == 0;  // rows ra, ra+1 adjacent and 32-byte aligned
   for (int k = t; k < Lh; k += T) {
     const double2 zk = buf[pad<L2>(k)], zm = buf[pad<L2>(k == 0 ? 0 : L2 - k)];
@@ -355,46 +353,30 @@ __global__ void __launch_bounds__(RsCfg<L2>::NT, 2) rows_ainv_resid(SpecArgs a) 
   fft::fft<L2, +1, T>(buf, twc, t, bar);
   cp_async_wait_all();
   __syncthreads();  // g rows (staged by the whole CTA) visible
-  // r = g - A x (solver.hpp:105) in place of A x, shifted to its extended
-  // position q2 + c: values pass through registers around a line barrier
+  // r = g - A x (solver.hpp:105) and its horizontal AR extension
+  // (boundary.hpp:56-62) produced inside the forward FFT's first-stage loads
+  // straight from A x (the inverse output still in the line) and the g rows
   const double* gA = gS + (2 * g) * LS;
   const double* gB = gA + LS;
+  const int wext = n2 + 2 * q2;
   double p0 = 0.0;
-  constexpr int CP = (L2 + T - 1) / T;
-  double2 rv[CP];
-#pragma unroll
-  for (int i = 0; i < CP; ++i) {
-    const int c = t + i * T;
-    rv[i] = make_double2(0.0, 0.0);
-    if (c < n2) {
-      const double2 ax = buf[pad<L2>(c)];
-      rv[i] = make_double2(has_a ? gA[c] - ax.x : 0.0, has_b ? gB[c] - ax.y : 0.0);
-      p0 += rv[i].x * rv[i].x + rv[i].y * rv[i].y;
-    }
-  }
-  fft::line_sync(bar, T);
-#pragma unroll
-  for (int i = 0; i < CP; ++i) {
-    const int c = t + i * T;
-    if (c < n2) buf[pad<L2>(q2 + c)] = rv[i];
-  }
-  fft::line_sync(bar, T);
-  // horizontal AR extension of r (boundary.hpp:56-62) and the zero tail
-  for (int p = t; p < L2; p += T) {
-    if (p >= q2 && p < q2 + n2) continue;
-    double2 v = make_double2(0.0, 0.0);
+  auto rr = [&](int c) {
+    const double2 ax = buf[pad<L2>(c)];
+    return make_double2(has_a ? gA[c] - ax.x : 0.0, has_b ? gB[c] - ax.y : 0.0);
+  };
+  fft::fft_in<L2, -1, T>(buf, twc, t, bar, [&](int p) {
     const int j = p - q2;
-    if (j < 0) {
-      const double2 r0 = buf[pad<L2>(q2)], ri = buf[pad<L2>(q2 - j)];
-      v = make_double2(2.0 * r0.x - ri.x, 2.0 * r0.y - ri.y);
-    } else if (j < n2 + q2) {
-      const double2 r0 = buf[pad<L2>(q2 + n2 - 1)], ri = buf[pad<L2>(q2 + 2 * (n2 - 1) - j)];
-      v = make_double2(2.0 * r0.x - ri.x, 2.0 * r0.y - ri.y);
+    int jc = j < 0 ? -j : j >= n2 ? 2 * (n2 - 1) - j : j;
+    jc = jc < 0 ? 0 : jc;
+    double2 v = rr(jc);
+    if (j < 0 || j >= n2) {
+      const double2 e = rr(j < 0 ? 0 : n2 - 1);
+      v = p < wext ? make_double2(2.0 * e.x - v.x, 2.0 * e.y - v.y) : make_double2(0.0, 0.0);
+    } else {
+      p0 += v.x * v.x + v.y * v.y;
     }
-    buf[pad<L2>(p)] = v;
-  }
-  fft::line_sync(bar, T);
-  fft::fft<L2, -1, T>(buf, twc, t, bar);
+    return v;
+  });
   double2* Z = a.zbuf + (size_t)b * n1 * Lh;
   const bool pair = has_b && ((ra | n1) & 1) == 0;
   for (int k = t; k < Lh; k += T) {

@@ -188,15 +188,16 @@ conv_col(SpecArgs a) {
     cp_async_wait_group<2>();  // twiddles landed (H may still be in flight)
     __syncthreads();
   }
-  fft::fft<L1, -1, T>(buf, tw, t, G > 1 ? 1 + g : 0);
-  cp_async_wait_all();  // each thread multiplies only the entries it staged
+  const int bar = G > 1 ? 1 + g : 0;
+  fft::fft<L1, -1, T>(buf, tw, t, bar);
+  // the kernel-spectrum product rides on the inverse FFT's first-stage loads
   if constexpr (SM::HS) {
-    for (int p = t; p < L1; p += T) buf[pad<L1>(p)] = cmul(buf[pad<L1>(p)], hst[p]);
+    cp_async_wait_all();
+    fft::line_sync(bar, T);  // the line's H entries (staged by all its threads) visible
+    fft::fft_in<L1, +1, T>(buf, tw, t, bar, [&](int p) { return cmul(buf[pad<L1>(p)], hst[p]); });
   } else {
-    for (int p = t; p < L1; p += T) buf[pad<L1>(p)] = cmul(buf[pad<L1>(p)], __ldg(Hcol + p));
+    fft::fft_in<L1, +1, T>(buf, tw, t, bar, [&](int p) { return cmul(buf[pad<L1>(p)], __ldg(Hcol + p)); });
   }
-  fft::line_sync(G > 1 ? 1 + g : 0, T);
-  fft::fft<L1, +1, T>(buf, tw, t, G > 1 ? 1 + g : 0);
   if (G > 1) __syncthreads();  // the stores interleave the CTA's lines
   const int YS = y_stride(Lh);
   double2* Y = a.ybuf + (size_t)b * n1 * YS;
