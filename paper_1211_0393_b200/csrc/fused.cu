@@ -233,12 +233,15 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   const double* fimg = a.f ? a.f + (size_t)b * N + (size_t)r0 * n2 : nullptr;
   PH_DECL
   if (fimg && threadIdx.x < nl) prefetch_l2(fimg + (size_t)threadIdx.x * n2, (unsigned)n2 * 8);
-  stage_lines(io, LSO, a.in + (size_t)b * N + (size_t)r0 * n2, nl, n2);  // v rows
+  __shared__ unsigned long long mb[2];
+  bulk_init(mb, 2);
+  const bool bv = stage_lines_bulk(io, LSO, a.in + (size_t)b * N + (size_t)r0 * n2, nl, n2, mb);  // v rows
   cp_async_commit();
-  stage_lines(stX, LS, xo, nl, n2);                                       // x_{k-1} rows
+  const bool bx = stage_lines_bulk(stX, LS, xo, nl, n2, mb + 1);  // x_{k-1} rows
   cp_async_commit();
   cp_async_wait_group<1>();
   __syncthreads();
+  stage_lines_wait(bv, mb, nl);
   PH(10)
   if (threadIdx.x < 4) {
     const int h = threadIdx.x;
@@ -267,6 +270,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   cp_async_commit();
   odd_scans2<LMAX>(io, LSO, 4, bt);
   cp_async_wait_all();
+  if (bx && nl > 0) mbar_wait(mb + 1, 0);
   __syncthreads();
   PH(13)
   // x_k = x_{k-1} + tau * T v (solver.hpp:106), rows r0..r0+nl-1 contiguous
@@ -345,14 +349,15 @@ __global__ void __launch_bounds__(RsCfg<L2>::NT, 2) rows_ainv_resid(SpecArgs a) 
   // g rows staged behind the inverse FFT (cp.async, rows r0..r0+3 contiguous)
   double* gS = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + C::gs);
   const int r0 = 4 * blockIdx.x, nl = n1 - r0 < 4 ? n1 - r0 : 4;
-  stage_lines(gS, LS, a.g + (size_t)b * N + (size_t)r0 * n2, nl, n2);
+  __shared__ unsigned long long mb[1];
+  bulk_init(mb, 1);
+  const bool bg = stage_lines_bulk(gS, LS, a.g + (size_t)b * N + (size_t)r0 * n2, nl, n2, mb);
   cp_async_commit();
   conv_inv_load<L2, T>(buf, a.ybuf + (size_t)b * n1 * y_stride(Lh), ra, rb, n1, Lh, t);
   cp_async_wait_group<1>();  // twiddles
   __syncthreads();
   fft::fft<L2, +1, T>(buf, twc, t, bar);
-  cp_async_wait_all();
-  __syncthreads();  // g rows (staged by the whole CTA) visible
+  stage_lines_wait(bg, mb, nl);  // g rows visible
   // r = g - A x (solver.hpp:105) and its horizontal AR extension
   // (boundary.hpp:56-62) produced inside the forward FFT's first-stage loads
   // straight from A x (the inverse output still in the line) and the g rows
@@ -434,12 +439,15 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   PH_DECL
   const int c0 = 4 * blockIdx.x;
   const int nl = n2 - c0 < 4 ? n2 - c0 : 4;
-  stage_lines(io, LSO, a.in + (size_t)b * N + (size_t)c0 * n, nl, n);  // u^T lines
+  __shared__ unsigned long long mb[2];
+  bulk_init(mb, 2);
+  const bool bi = stage_lines_bulk(io, LSO, a.in + (size_t)b * N + (size_t)c0 * n, nl, n, mb);  // u^T lines
   cp_async_commit();
-  stage_lines(dS, LS, a.dT + (size_t)b * a.dstride + (size_t)c0 * n, nl, n);  // d^T lines
+  const bool bd = stage_lines_bulk(dS, LS, a.dT + (size_t)b * a.dstride + (size_t)c0 * n, nl, n, mb + 1);  // d^T
   cp_async_commit();
   cp_async_wait_group<1>();
   __syncthreads();
+  stage_lines_wait(bi, mb, nl);
   PH(0)
   if (threadIdx.x < 4) {
     const int h = threadIdx.x;
@@ -469,6 +477,7 @@ __global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(
   PH(3)
   odd_scans2<LMAX>(io, LSO, 4, bt);
   cp_async_wait_all();
+  if (bd && nl > 0) mbar_wait(mb + 1, 0);
   __syncthreads();
   PH(4)
   // v = u o d (u_0 = alpha v_0, u_{n-1} = alpha v_{n-1}), then T (ar_forward)

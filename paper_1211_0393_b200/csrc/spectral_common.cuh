@@ -446,6 +446,76 @@ __device__ __forceinline__ void stage_lines(double* dst, int LS, const double* s
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA bulk staging (cp.async.bulk + mbarrier transaction counts): ONE thread
+// issues a whole contiguous line per instruction instead of every thread
+// issuing 16-byte cp.async copies.  Usage: bulk_init(mb) by the CTA at start
+// (thread 0), stage_lines_bulk(...) right after, and stage_lines_wait(...) by
+// every thread once the CTA has passed a barrier after the init.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void bulk_init(unsigned long long* mb, int n, bool lead = threadIdx.x == 0) {
+  if (lead) {
+    for (int i = 0; i < n; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mb + i)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(mb)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect(unsigned long long* mb, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
+
+// one contiguous global -> smem copy (16-byte aligned, bytes % 16 == 0)
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, unsigned long long* mb) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mb))
+               : "memory");
+}
+
+// Stage nl contiguous lines of n doubles into smem lines of stride LS: bulk
+// copies completing on mb when n, LS and both bases are 16-byte friendly
+// (returns true, CTA-uniform), else per-thread cp.async (caller commits).
+__device__ __forceinline__ bool stage_lines_bulk(double* dst, int LS, const double* src, int nl, int n,
+                                                 unsigned long long* mb) {
+  const bool v16 = ((n | LS) & 1) == 0 && (((unsigned long long)src | (unsigned long long)smem_u32(dst)) & 15) == 0;
+  if (!v16) {
+    stage_lines(dst, LS, src, nl, n);
+    return false;
+  }
+  if (threadIdx.x == 0 && nl > 0) {
+    const unsigned bytes = (unsigned)n * 8u;
+    mbar_expect(mb, bytes * nl);
+    for (int h = 0; h < nl; ++h) bulk_copy(dst + (size_t)h * LS, src + (size_t)h * n, bytes, mb);
+  }
+  return true;
+}
+
+// Every thread: the lines of stage_lines_bulk have landed and are visible
+// (bulk: the mbarrier phase; fallback: this thread's cp.async + a CTA barrier).
+__device__ __forceinline__ void stage_lines_wait(bool bulk, unsigned long long* mb, int nl) {
+  if (bulk) {
+    if (nl > 0) mbar_wait(mb, 0);
+  } else {
+    cp_async_wait_all();
+    __syncthreads();
+  }
+}
+
 template <typename K>
 bool set_smem(K kernel, size_t bytes) {
   if (bytes > 227 * 1024) return false;
