@@ -40,6 +40,7 @@ UNIT = "Mpixel-iterations/s"
 PEAKS_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
 HBM_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+E2E_CHUNKS = 4
 
 
 def parse():
@@ -52,6 +53,8 @@ def parse():
     ap.add_argument("--images", type=int, default=0, help="override images per rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the single-GPU graph-path lines of the other BASELINE configs (C1, C2, C4, C5)")
     ap.add_argument("--slab", action="store_true",
                     help="row-slab decomposition of one image (default for C5 at N > 1)")
     return ap.parse_args()
@@ -136,6 +139,60 @@ def cpu_sample(cfg, threads: int, iters: int):
     sample = (f"{threads} image(s) x {iters} D-Landweber iteration(s) of {cfg.name} ({cfg.n}^2, q={cfg.q}), "
               f"oracle port: reference algorithm (FFT correlation for q>7, FFT DST-I), {threads} thread(s)")
     return px_it / dt / 1e6, dt, sample
+
+
+def other_configs(L, dbx, cf, torch, dev, local, reps=3):
+    """Single-GPU graph-path throughput of the other BASELINE configs (the
+    parity cases), same timing rules as the headline (warm-up, CUDA events on
+    the plan's stream, device-resident inputs).  C2 also times plain Landweber
+    (configs[1] names both); C1/C2 are single small images (L2-resident,
+    launch/latency bound), C4/C5 single large images (separate-pass pipeline)."""
+    out = {}
+    for name in ("C1", "C2", "C4", "C5"):
+        cfg = cf.CONFIGS[name]
+        t0 = time.perf_counter()
+        F, G, taps = cf.make_batch(cfg, 1)
+        gen_s = time.perf_counter() - t0
+        n, q, H = cfg.n, cfg.q, cfg.iters
+        g = torch.from_numpy(G).to(dev)
+        f = torch.from_numpy(F).to(dev)
+        o = torch.empty_like(g)
+        del F, G
+        plan = C.c_void_p()
+        dbx._check(L.dbx_plan_create(n, n, 1, dbx._ptr(taps), q, q, 3, local, C.byref(plan)))
+        dbx._check(L.dbx_precond_build(plan, float(cfg.alpha)))
+        stream = torch.cuda.ExternalStream(L.dbx_plan_stream(plan), device=dev)
+        rre = np.zeros(H)
+        res = np.zeros(H)
+        best, done = (C.c_int * 1)(), (C.c_int * 1)()
+        entry = {"n": n, "q": q, "iters": H, "alpha": cfg.alpha, "host_generation_s": round(gen_s, 2)}
+        fz = C.c_int()
+        for prec in ((1, 0) if cfg.plain_too else (1,)):
+            def solve():
+                dbx._check(L.dbx_landweber_run(plan, dbx._ptr(g), dbx._ptr(f), 1.0, H, 1, 0, 0.0, prec,
+                                               dbx._ptr(o), dbx._ptr(rre), dbx._ptr(res), best, done, None))
+            for _ in range(3):
+                solve()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+            for _ in range(reps):
+                solve()
+            with torch.cuda.stream(stream):
+                e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            key = "value" if prec else "plain_value"
+            entry[key] = n * n * H / (ms * 1e-3) / 1e6
+            entry[("ms_per_run" if prec else "plain_ms_per_run")] = ms
+            if prec:
+                L.dbx_plan_pipeline(plan, C.byref(fz))
+                entry["pipeline"] = "fused" if fz.value == 1 else "separate passes"
+        L.dbx_plan_destroy(plan)
+        out[name] = entry
+        del g, f, o
+    return out
 
 
 def run_reference(args):
@@ -320,29 +377,48 @@ def main():
     px_it = world * B * N * H * args.steps
     value = px_it / (t_max * 1e-3) / 1e6
 
-    # ---- e2e: public C-ABI with pinned host buffers (H2D + D2H inside) ----
+    # ---- e2e: public C-ABI with pinned host buffers (H2D + D2H inside the
+    # timed region).  dbx_landweber_run_chunks splits the batch over E2E_CHUNKS
+    # plans so that every chunk's upload and its restored images' download
+    # overlap the other chunks' solves ----
     e2e = None
     if not args.no_e2e:
         gh = g_d.cpu().pin_memory()
         fh = f_d.cpu().pin_memory()
         oh = torch.empty_like(gh).pin_memory()
-        solve(gh, fh, oh)  # warm (host-staging buffers)
+        nch = E2E_CHUNKS if B % E2E_CHUNKS == 0 else 1
+        cplans = []
+        for _ in range(nch):
+            cp = C.c_void_p()
+            dbx._check(L.dbx_plan_create(n, n, B // nch, dbx._ptr(taps), q, q, 3, local, C.byref(cp)))
+            dbx._check(L.dbx_precond_build(cp, float(cfg.alpha)))
+            cplans.append(cp)
+        handles = (C.c_void_p * nch)(*cplans)
+
+        def solve_host():
+            dbx._check(L.dbx_landweber_run_chunks(handles, nch, dbx._ptr(gh), dbx._ptr(fh), 1.0, H, 1, 0, 0.0, 1,
+                                                  dbx._ptr(oh), dbx._ptr(rre_h), dbx._ptr(res_h), best, done))
+
+        solve_host()  # warm (graphs, staging buffers)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
+        e0.record()
         for _ in range(args.steps):
-            solve(gh, fh, oh)
-        with torch.cuda.stream(stream):
-            e1.record(stream)
+            solve_host()
+        e1.record()
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": px_it / (float(te.item()) * 1e-3) / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": int(2 * B * N * 8), "d2h_bytes_per_step": int(B * N * 8 + 2 * B * H * 8)}
+               "h2d_bytes_per_step": int(2 * B * N * 8), "d2h_bytes_per_step": int(B * N * 8 + 2 * B * H * 8),
+               "path": f"dbx_landweber_run_chunks: {nch} chunks of {B // nch} images, pinned host arrays, "
+                       "uploads/downloads overlapped with the other chunks' solves"}
+        for cp in cplans:
+            L.dbx_plan_destroy(cp)
+        del gh, fh, oh
 
     # ---- roofline of the dominant kernel class ----
     from paper_1211_0393_b200 import workmodel as wm
@@ -401,6 +477,10 @@ def main():
                      "peak_source": fsrc, "algorithmic_flops_per_launch": flops})
     roof["dense_stencil_sol"] = wm.canonical(q, float(world * B * N * H) / world, step_s, hbm_peak, p_fp64)
 
+    others = None
+    if rank == 0 and world == 1 and not args.no_other_configs and args.config == "C3" and not args.images:
+        others = other_configs(L, dbx, cf, torch, dev, local)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt, sample = cpu_sample(cfg, 1, 2)
@@ -417,6 +497,9 @@ def main():
                            "parallelism": f"batch-sharded x{world} (no data-path collective)",
                            "l2": "inputs larger than L2 (each 64x1024^2 FP64 array = 512 MiB)"},
                 "clocks": clk, "gpu_launches": launches, "roofline": roof, "e2e": e2e, "cpu_baseline": cpu}
+        if others:
+            line["other_configs"] = {"unit": UNIT, "note": "single-GPU graph path, D-Landweber unless plain_*; "
+                                                          "parity cases, not the headline", **others}
         print(json.dumps(line), flush=True)
     L.dbx_plan_destroy(plan)
     if world > 1:

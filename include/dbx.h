@@ -239,6 +239,24 @@ int dbx_landweber_run(dbx_plan* plan, const double* g, const double* f_true, dou
                       int* best_iter, int* iters_done, double* x_hist);
 
 /*
+ * dbx_landweber_run over a batch split into `nplans` chunks, one plan per
+ * chunk (plans[c] restores images [sum of earlier batches, + plans[c]->batch)
+ * of g / f_true / restored / the histories; same n1 x n2, mask and, for
+ * use_precond, a built preconditioner on every plan).  HOST arrays only
+ * (page-locked for overlap): the chunks' inputs are copied up on a copy stream
+ * ahead of time and each chunk's restored images are copied down while the
+ * next chunk computes, so the host<->device traffic hides behind the solves.
+ * Results equal dbx_landweber_run on the whole batch (images are
+ * independent).  Divergence: every chunk still runs; the first diverging image
+ * (global index) is reported with DBX_EDIVERGED.  No reference equivalent (the
+ * reference restores one image per call on the host).
+ */
+int dbx_landweber_run_chunks(dbx_plan* const* plans, int nplans, const double* g, const double* f_true,
+                             double tau, int max_iters, int stop_kind, int fixed_iters, double resid_eps,
+                             int use_precond, double* restored, double* rre_hist, double* res_hist,
+                             int* best_iter, int* iters_done);
+
+/*
  * Per-kernel-class device time (ms) and launch counts of the most recent
  * dbx_landweber_run made with timing enabled (dbx_plan_set_timing(plan, 1)):
  * classes 0 = blur A' (+fused epilogue), 1 = blur A (+residual), 2 = AR

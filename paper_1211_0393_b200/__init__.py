@@ -75,6 +75,7 @@ def lib():
         L.dbx_tensor_apply.argtypes = [vp, i, vp, vp]
         L.dbx_landweber_run.argtypes = [vp, vp, vp, d, i, i, i, d, i, vp, vp, vp, vp, vp, vp]
         L.dbx_cgls_run.argtypes = [vp, vp, vp, i, i, i, d, i, vp, vp, vp, vp, vp, vp]
+        L.dbx_landweber_run_chunks.argtypes = [vp, i, vp, vp, d, i, i, i, d, i, vp, vp, vp, vp, vp]
         L.dbx_plan_set_timing.argtypes = [vp, i]
         L.dbx_plan_kernel_times.argtypes = [vp, vp, vp, i]
         L.dbx_plan_launch_count.argtypes = [vp]
@@ -534,6 +535,51 @@ def cgls(op: BlurOperator, g, cfg: SolverConfig, d: Optional[FilteredOperator] =
     """Reblurred CGLS on min ||A x - g||, preconditioned by D when given
     (config 2's "CGLS-type" iteration; cfg.tau is unused)."""
     return _run(op, d, g, cfg, keep_iterates, method="cgls")
+
+
+def landweber_chunks(ops, g, cfg: SolverConfig, d: Optional[FilteredOperator] = None):
+    """(D-)Landweber of a HOST batch g [B, n1, n2] split over the plans of
+    ``ops`` (BlurOperators whose batches sum to B, same size and mask): the
+    chunks' uploads and downloads overlap the solves (dbx_landweber_run_chunks;
+    page-locked arrays, e.g. torch ``pin_memory()`` tensors, for the overlap).
+    Returns one RestorationRun per image, identical to d_landweber/landweber on
+    the whole batch."""
+    g = _f64(g)
+    if hasattr(g, "data_ptr") and g.is_cuda:
+        raise ValueError("landweber_chunks: host arrays only")
+    B = sum(op.batch for op in ops)
+    if g.ndim != 3 or g.shape[0] != B or any((op.n1, op.n2) != tuple(g.shape[1:]) for op in ops):
+        raise ValueError("landweber_chunks: g must be [sum of plan batches, n1, n2]")
+    f = cfg.track_rre_against
+    if f is not None:
+        f = _f64(f)
+        if tuple(f.shape) != tuple(g.shape):
+            raise ValueError("landweber: true image size mismatch")
+    if d is not None:
+        for op in ops:
+            if op._eigs_id is not id(d):
+                _check(lib().dbx_precond_set_eigs(op.handle, _ptr(d.eigs)))
+                op._eigs_id = id(d)
+    stop = cfg.stop
+    total = stop.fixed_iterations if stop.kind == StoppingRuleKind.FixedIterations else cfg.max_iters
+    H = max(total, 1)
+    if hasattr(g, "data_ptr"):
+        import torch
+        restored = torch.empty(tuple(g.shape), dtype=torch.float64, pin_memory=bool(g.is_pinned()))
+    else:
+        restored = np.empty(g.shape)
+    rre_h = np.zeros((B, H))
+    res_h = np.zeros((B, H))
+    best = (C.c_int * B)()
+    done = (C.c_int * B)()
+    handles = (C.c_void_p * len(ops))(*[op.handle for op in ops])
+    _check(lib().dbx_landweber_run_chunks(
+        handles, len(ops), _ptr(g), _ptr(f), float(cfg.tau), int(cfg.max_iters), int(stop.kind),
+        int(stop.fixed_iterations), float(stop.residual_threshold), 1 if d is not None else 0,
+        _ptr(restored), _ptr(rre_h), _ptr(res_h), best, done))
+    return [RestorationRun(restored=restored[b], iterations_executed=done[b], best_iteration=best[b],
+                           rre_history=list(rre_h[b, :done[b]]) if f is not None else [],
+                           residual_history=list(res_h[b, :done[b]]), iterates=None) for b in range(B)]
 
 
 def semiconvergence_report(run: RestorationRun) -> SemiconvergenceReport:  # solver.hpp:152-160

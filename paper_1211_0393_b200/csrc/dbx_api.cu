@@ -1191,7 +1191,8 @@ int dbx_tensor_apply(dbx_plan* P, int kind, const double* x, double* y) {
 
 static int run_impl(dbx_plan* P, const double* g, const double* f_true, double tau, int max_iters, int stop_kind,
                     int fixed_iters, double resid_eps, int use_precond, double* restored, double* rre_hist,
-                    double* res_hist, int* best_iter, int* iters_done, double* x_hist, int method);
+                    double* res_hist, int* best_iter, int* iters_done, double* x_hist, int method,
+                    int img_base = 0);
 
 int dbx_landweber_run(dbx_plan* P, const double* g, const double* f_true, double tau,
                       int max_iters, int stop_kind, int fixed_iters, double resid_eps,
@@ -1210,7 +1211,8 @@ int dbx_cgls_run(dbx_plan* P, const double* g, const double* f_true, int max_ite
 
 static int run_impl(dbx_plan* P, const double* g, const double* f_true, double tau, int max_iters, int stop_kind,
                     int fixed_iters, double resid_eps, int use_precond, double* restored, double* rre_hist,
-                    double* res_hist, int* best_iter, int* iters_done, double* x_hist, int method) {
+                    double* res_hist, int* best_iter, int* iters_done, double* x_hist, int method,
+                    int img_base) {
   return guarded([&] {
     require(P && g && restored, "landweber: null argument");
     // solver.hpp:66-72, 17-32
@@ -1502,10 +1504,101 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
     if (div_img >= 0) {
       char msg[160];
       snprintf(msg, sizeof msg, "landweber: iterate exceeded 1e8 * ||g|| (image %d, iteration %d)",
-               div_img, div_k);
+               img_base + div_img, div_k);
       throw Diverged(msg);
     }
   });
+}
+
+// Chunked batch run with host<->device copies overlapped with compute: chunk
+// c's inputs go up on a copy stream ahead of time, its solve waits only for its
+// own inputs, and its restored images come down while chunk c+1 computes.
+// Results are those of dbx_landweber_run on the concatenated batch (every
+// image is independent; each plan computes its chunk bit-identically).
+int dbx_landweber_run_chunks(dbx_plan* const* plans, int nplans, const double* g, const double* f_true,
+                             double tau, int max_iters, int stop_kind, int fixed_iters, double resid_eps,
+                             int use_precond, double* restored, double* rre_hist, double* res_hist,
+                             int* best_iter, int* iters_done) {
+  int first_div = DBX_OK;
+  std::string div_msg;
+  const int st = guarded([&] {
+    require(plans && nplans >= 1, "landweber_chunks: no plans");
+    require(g && restored, "landweber_chunks: null argument");
+    for (int c = 0; c < nplans; ++c) {
+      require(plans[c] != nullptr, "landweber_chunks: null plan");
+      require(plans[c]->n1 == plans[0]->n1 && plans[c]->n2 == plans[0]->n2 && plans[c]->device == plans[0]->device,
+              "landweber_chunks: plans must share the image size and device");
+    }
+    require(!is_device_ptr(g) && !is_device_ptr(restored) && (!f_true || !is_device_ptr(f_true)),
+            "landweber_chunks: g, f_true and restored are host arrays (use dbx_landweber_run for device data)");
+    plans[0]->set_dev();
+    const int total = stop_kind == DBX_STOP_FIXED ? fixed_iters : max_iters;
+    const size_t H = (size_t)std::max(total, 1);
+    const size_t N = plans[0]->N;
+    cudaStream_t cs = nullptr;
+    std::vector<cudaEvent_t> ready((size_t)nplans, nullptr);
+    auto cleanup = [&] {
+      for (cudaEvent_t e : ready)
+        if (e) cudaEventDestroy(e);
+      if (cs) cudaStreamDestroy(cs);
+    };
+    try {
+      ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
+      size_t off = 0;
+      for (int c = 0; c < nplans; ++c) {  // every chunk's inputs queued up front, in chunk order
+        dbx_plan* P = plans[c];
+        const size_t cnt = N * P->batch;
+        P->g.ensure(cnt);
+        ck(cudaMemcpyAsync(P->g.p, g + off, cnt * sizeof(double), cudaMemcpyHostToDevice, cs), "H2D");
+        if (f_true) {
+          P->f.ensure(cnt);
+          ck(cudaMemcpyAsync(P->f.p, f_true + off, cnt * sizeof(double), cudaMemcpyHostToDevice, cs), "H2D");
+        }
+        ck(cudaEventCreateWithFlags(&ready[(size_t)c], cudaEventDisableTiming), "event");
+        ck(cudaEventRecord(ready[(size_t)c], cs), "event");
+        off += cnt;
+      }
+      off = 0;
+      size_t img = 0;
+      for (int c = 0; c < nplans; ++c) {
+        dbx_plan* P = plans[c];
+        const size_t cnt = N * P->batch;
+        P->out.ensure(cnt);
+        ck(cudaStreamWaitEvent(P->stream, ready[(size_t)c], 0), "wait");
+        const int rc = run_impl(P, P->g.p, f_true ? P->f.p : nullptr, tau, max_iters, stop_kind, fixed_iters,
+                                resid_eps, use_precond, P->out.p, rre_hist ? rre_hist + img * H : nullptr,
+                                res_hist ? res_hist + img * H : nullptr, best_iter ? best_iter + img : nullptr,
+                                iters_done ? iters_done + img : nullptr, nullptr, 0, (int)img);
+        if (rc == DBX_EDIVERGED) {
+          if (first_div == DBX_OK) {
+            first_div = rc;
+            div_msg = g_err;
+          }
+        } else if (rc == DBX_EINVAL) {
+          throw InvalidArg(g_err);
+        } else if (rc != DBX_OK) {
+          throw CudaErr(g_err);
+        }
+        // run_impl returned after its stream synchronised: this chunk's result
+        // is final; bring it down while the next chunk computes
+        ck(cudaMemcpyAsync(restored + off, P->out.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, cs), "D2H");
+        off += cnt;
+        img += (size_t)P->batch;
+      }
+      ck(cudaStreamSynchronize(cs), "sync");
+    } catch (...) {
+      if (cs) cudaStreamSynchronize(cs);
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+  if (st != DBX_OK) return st;
+  if (first_div != DBX_OK) {
+    g_err = div_msg;
+    return first_div;
+  }
+  return DBX_OK;
 }
 
 }  // extern "C"

@@ -149,6 +149,35 @@ def test_batch_equals_single_and_deterministic(dev):
         assert np.array_equal(runs2[i].restored, runs[i].restored)
 
 
+@pytest.mark.parametrize("name,n,chunks", [("C3", 1024, (2, 1, 1)), ("C1", 96, (1, 3))])
+def test_chunked_host_run_equals_batch(dev, name, n, chunks):
+    """dbx_landweber_run_chunks (copy/compute-overlapped host batch) equals
+    the one-plan batch run bit for bit, fused (C3 full size) and separate-pass
+    (C1 direct stencil) pipelines, plain pinned and pageable host arrays."""
+    import torch
+    from paper_1211_0393_b200 import configs as cf
+    c = cf.CONFIGS[name]
+    B = sum(chunks)
+    F, G, taps = cf.make_batch(c, B, n=n)
+    spec = dev.PreconditionerSpec(dev.Algebra.AntiReflective, c.alpha)
+    d = dev.build_tikhonov(dev.Psf(taps), spec, n, n)
+    cfg = dev.SolverConfig(max_iters=4, track_rre_against=F)
+    opb = dev.BlurOperator(dev.Psf(taps), dev.BoundaryCondition.AntiReflective, n, n, batch=B)
+    ref = dev.d_landweber(opb, d, G, cfg)
+    ops = [dev.BlurOperator(dev.Psf(taps), dev.BoundaryCondition.AntiReflective, n, n, batch=k) for k in chunks]
+    for pinned in (True, False):
+        g = torch.from_numpy(G).pin_memory() if pinned else G
+        fcfg = dev.SolverConfig(max_iters=4, track_rre_against=torch.from_numpy(F).pin_memory() if pinned else F)
+        runs = dev.landweber_chunks(ops, g, fcfg, d=d)
+        for i in range(B):
+            assert np.array_equal(np.asarray(runs[i].restored), ref[i].restored)
+            assert runs[i].rre_history == ref[i].rre_history
+            assert runs[i].residual_history == ref[i].residual_history
+            assert runs[i].best_iteration == ref[i].best_iteration
+    with pytest.raises(ValueError):
+        dev.landweber_chunks(ops, torch.from_numpy(G).cuda(), cfg, d=d)
+
+
 def test_stopping_rules_and_errors(dev, oracle):
     rng = np.random.default_rng(383)
     n = 20

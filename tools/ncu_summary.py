@@ -18,7 +18,11 @@ KEYS = [
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem_conflicts"),
     ("launch__registers_per_thread", "regs"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy_%"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_active_%"),
 ]
+# warp stall reasons, cycles per issued instruction
+STALLS = ["wait", "short_scoreboard", "barrier", "no_instruction", "long_scoreboard", "not_selected",
+          "math_pipe_throttle", "mio_throttle", "branch_resolving", "dispatch_stall"]
 
 
 def full_report(path):
@@ -35,6 +39,15 @@ def full_report(path):
                 vals.append(f"{r[i]} {units[i]}".strip())
             else:
                 vals.append("-")
+        out.append(f"| {name} | " + " | ".join(vals) + " |")
+    out += ["", "Warp stalls per issued instruction (smsp__average_warps_issue_stalled_*_per_issue_active):", "",
+            "| kernel | " + " | ".join(STALLS) + " |", "|---" * (len(STALLS) + 1) + "|"]
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")].replace("(anonymous namespace)::", "")[:48]
+        vals = []
+        for st in STALLS:
+            k = f"smsp__average_warps_issue_stalled_{st}_per_issue_active.ratio"
+            vals.append(r[hdr.index(k)] if k in hdr else "-")
         out.append(f"| {name} | " + " | ".join(vals) + " |")
     return "\n".join(out)
 

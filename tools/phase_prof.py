@@ -42,13 +42,18 @@ def main():
     run()
     L.dbx_debug_phases(buf, 64)
     v = np.array(buf[:64], dtype=np.float64)
-    for lo, hi in ((0, 10), (10, 20), (20, 30), (40, 43)):
+    # CTAs per run: every fused kernel covers the image in 4-line blocks; the
+    # DST FFT stages (40-42) run in rows_ainv_tt, dst_tcols (x2), rows_t_axpy
+    ctas = (cfg.n // 4) * B * H
+    per = {(0, 10): ctas, (10, 20): ctas, (20, 30): ctas, (40, 43): 4 * ctas}
+    for (lo, hi), nc in per.items():
         tot = v[lo:hi].sum()
         if tot <= 0:
             continue
+        print("%-22s %8.0f cycles per CTA (thread 0 wall clock)" % ("[group %d-%d]" % (lo, hi - 1), tot / nc))
         for i in range(lo, hi):
             if v[i] > 0:
-                print("%-22s %6.1f%%" % (NAMES.get(i, "phase%d" % i), 100 * v[i] / tot))
+                print("%-22s %6.1f%%  %8.0f" % (NAMES.get(i, "phase%d" % i), 100 * v[i] / tot, v[i] / nc))
     L.dbx_plan_destroy(plan)
 
 
