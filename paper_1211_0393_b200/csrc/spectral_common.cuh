@@ -280,11 +280,20 @@ __device__ __forceinline__ void pk_fill(double2* buf, const BlueTables& bt, int 
     for (int p = N + t; p < M; p += T) buf[pad<M>(p)] = make_double2(0.0, 0.0);
   constexpr int HMAX = (BLUE ? M / 2 + 1 : M) / 2;
   constexpr int PF = (HMAX + T - 1) / T;
+  // the thread's sine weights first, all in flight at once (one L1/L2 round
+  // trip instead of one per element: the loop's shared-memory stores would
+  // otherwise keep the compiler from hoisting the global loads)
+  double sw[PF];
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int j = 1 + t + i * T;
+    sw[i] = j <= H ? __ldg(bt.sn + j) : 0.0;
+  }
 #pragma unroll
   for (int i = 0; i < PF; ++i) {
     const int j = 1 + t + i * T;
     if (j <= H) {
-      const double s = __ldg(bt.sn + j);
+      const double s = sw[i];
       const double2 A = sd(0, j), B = sd(1, j);
       const double2 zj = make_double2(fma(s, A.x, 0.5 * A.y), fma(s, B.x, 0.5 * B.y));
       const double2 zm = make_double2(fma(s, A.x, -0.5 * A.y), fma(s, B.x, -0.5 * B.y));
