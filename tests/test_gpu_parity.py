@@ -109,6 +109,10 @@ def test_config1_full_trajectory(dev, oracle, precond):
         run = dev.landweber(op, g, cfg, keep_iterates=True)
         ref = oracle.landweber(taps, g, f_true=f, max_iters=c.iters, keep_iterates=True)
     _trajectory_check(run, ref)
+    # below the reference's q > 7 cutover AUTO still picks the FFT engine here:
+    # it unlocks the fused preconditioned pipeline for this shape
+    assert op.engines()[0] == dev.ConvEngine.Fft
+    assert op.pipeline_fused() == precond
 
 
 @pytest.mark.parametrize("name,n,iters", [("C2", 128, 30), ("C3", 128, 20), ("C4", 160, 10), ("C5", 128, 10)])
