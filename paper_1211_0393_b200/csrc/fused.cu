@@ -25,9 +25,16 @@ namespace dbx {
 
 namespace {
 
+// Fused DST lines carry one radix-8 butterfly per thread also for the
+// power-of-two Bluestein lengths (twice the threads of the separate-pass
+// kernels): the fused shapes with Bluestein lines are single small images
+// (C2: 512^2 -> 128 CTAs for 148 SMs), where per-CTA latency, not issue
+// width, sets the kernel time.
+__host__ __device__ constexpr int fused_dst_per(int) { return 8; }
+
 template <int L2, int M, bool BLUE>
 struct Fused {
-  static constexpr int TD = line_threads(M, dst_per(M));   // threads per line
+  static constexpr int TD = line_threads(M, fused_dst_per(M));   // threads per line
   static constexpr int NT = 2 * TD;                         // CTA = two FFT lines
   static constexpr int LC = padded_len(L2);                 // conv line (double2)
   static constexpr int LD = padded_len(M);                  // DST line (double2)
@@ -409,7 +416,7 @@ __global__ void __launch_bounds__(RsCfg<L2>::NT, 2) rows_ainv_resid(SpecArgs a) 
 // (pk_fill / pk_split), so the row-major stores are full 32-byte sectors.
 template <int M, bool BLUE>
 struct TcolSmem {
-  static constexpr int TD = line_threads(M, dst_per(M));
+  static constexpr int TD = line_threads(M, fused_dst_per(M));
   static constexpr int LMAX = BLUE ? M / 2 + 1 : M + 1;         // max line length n
   static constexpr int LS = (LMAX + 1) / 2 * 2 + 4;             // line stride (doubles): 4 lines hit distinct banks
   static constexpr int LSO = ((LMAX > PkOut<LMAX>::OL ? LMAX : PkOut<LMAX>::OL) + 1) / 2 * 2 + 4;  // io lines
@@ -422,7 +429,7 @@ struct TcolSmem {
 };
 
 template <int M, bool BLUE>
-__global__ void __launch_bounds__(2 * line_threads(M, dst_per(M)), 2) dst_tcols(SpecArgs a) {
+__global__ void __launch_bounds__(2 * line_threads(M, fused_dst_per(M)), 2) dst_tcols(SpecArgs a) {
   using S = TcolSmem<M, BLUE>;
   constexpr int TD = S::TD, NT = 2 * TD, LS = S::LS, LSO = S::LSO, LMAX = S::LMAX;
   const int b = blockIdx.y;
