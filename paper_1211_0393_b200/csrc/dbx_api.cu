@@ -12,6 +12,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dbx.h"
@@ -1568,33 +1569,54 @@ int dbx_landweber_run_chunks(dbx_plan* const* plans, int nplans, const double* g
         ck(cudaEventRecord(ready[(size_t)c], cs), "event");
         off += cnt;
       }
-      off = 0;
-      size_t img = 0;
+      // the chunks' solves run concurrently (one host thread per plan: the
+      // call is host-synchronous), so one chunk's kernel tails overlap the
+      // others' work; each chunk's restored images go down on its own stream
+      std::vector<size_t> first((size_t)nplans + 1, 0);
       for (int c = 0; c < nplans; ++c) {
-        dbx_plan* P = plans[c];
-        const size_t cnt = N * P->batch;
-        P->out.ensure(cnt);
-        ck(cudaStreamWaitEvent(P->stream, ready[(size_t)c], 0), "wait");
-        const int rc = run_impl(P, P->g.p, f_true ? P->f.p : nullptr, tau, max_iters, stop_kind, fixed_iters,
-                                resid_eps, use_precond, P->out.p, rre_hist ? rre_hist + img * H : nullptr,
-                                res_hist ? res_hist + img * H : nullptr, best_iter ? best_iter + img : nullptr,
-                                iters_done ? iters_done + img : nullptr, nullptr, 0, (int)img);
-        if (rc == DBX_EDIVERGED) {
-          if (first_div == DBX_OK) {
-            first_div = rc;
-            div_msg = g_err;
-          }
-        } else if (rc == DBX_EINVAL) {
-          throw InvalidArg(g_err);
-        } else if (rc != DBX_OK) {
-          throw CudaErr(g_err);
-        }
-        // run_impl returned after its stream synchronised: this chunk's result
-        // is final; bring it down while the next chunk computes
-        ck(cudaMemcpyAsync(restored + off, P->out.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, cs), "D2H");
-        off += cnt;
-        img += (size_t)P->batch;
+        plans[c]->out.ensure(N * plans[c]->batch);
+        first[(size_t)c + 1] = first[(size_t)c] + (size_t)plans[c]->batch;
       }
+      std::vector<int> rcs((size_t)nplans, DBX_OK);
+      std::vector<std::string> msgs((size_t)nplans);
+      auto work = [&](int c) {
+        dbx_plan* P = plans[c];
+        const size_t img = first[(size_t)c], cnt = N * P->batch;
+        int rc = DBX_OK;
+        if (cudaSetDevice(P->device) != cudaSuccess || cudaStreamWaitEvent(P->stream, ready[(size_t)c], 0) != cudaSuccess) {
+          rc = DBX_ECUDA;
+          g_err = "landweber_chunks: stream setup failed";
+        } else {
+          rc = run_impl(P, P->g.p, f_true ? P->f.p : nullptr, tau, max_iters, stop_kind, fixed_iters, resid_eps,
+                        use_precond, P->out.p, rre_hist ? rre_hist + img * H : nullptr,
+                        res_hist ? res_hist + img * H : nullptr, best_iter ? best_iter + img : nullptr,
+                        iters_done ? iters_done + img : nullptr, nullptr, 0, (int)img);
+        }
+        if (rc == DBX_OK || rc == DBX_EDIVERGED) {  // restored images exist either way
+          if (cudaMemcpyAsync(restored + img * N, P->out.p, cnt * sizeof(double), cudaMemcpyDeviceToHost,
+                              P->stream) != cudaSuccess ||
+              cudaStreamSynchronize(P->stream) != cudaSuccess) {
+            rc = DBX_ECUDA;
+            g_err = "landweber_chunks: D2H failed";
+          }
+        }
+        rcs[(size_t)c] = rc;
+        msgs[(size_t)c] = g_err;  // g_err is per thread
+      };
+      std::vector<std::thread> pool;
+      for (int c = 1; c < nplans; ++c) pool.emplace_back(work, c);
+      work(0);
+      for (std::thread& t : pool) t.join();
+      for (int c = 0; c < nplans; ++c) {
+        const int rc = rcs[(size_t)c];
+        if (rc == DBX_EINVAL) throw InvalidArg(msgs[(size_t)c]);
+        if (rc != DBX_OK && rc != DBX_EDIVERGED) throw CudaErr(msgs[(size_t)c]);
+      }
+      for (int c = 0; c < nplans && first_div == DBX_OK; ++c)
+        if (rcs[(size_t)c] == DBX_EDIVERGED) {
+          first_div = DBX_EDIVERGED;
+          div_msg = msgs[(size_t)c];
+        }
       ck(cudaStreamSynchronize(cs), "sync");
     } catch (...) {
       if (cs) cudaStreamSynchronize(cs);
