@@ -507,8 +507,106 @@ __device__ __forceinline__ void odd_pairs_store_dispatch(int part, const double2
 // registers; (3) after a barrier the outputs go to the Stockham positions.
 // No thread holds the R inputs at once, so the stage needs ~4(H/P) + O(1)
 // live complex values instead of R + accumulators.
+// Twiddle-free (first) large-prime stage whose G*NB butterflies do not fill
+// whole warps (1023 = 31*33 on two lines: 66 = 2*32 + 2).  The padded form
+// above runs P replicas of ceil(66/32) = 3 warps, two of them with 2 of 32
+// lanes busy but still issuing every FMA of the sweep (a third of the stage's
+// FP64 issue).  Here the P replicas cover only the NBf = 64 butterflies that
+// fill warps; one extra warp takes the REM leftovers with one output pair per
+// lane (REM*H <= 32 lanes), its cos/sin weights read from a shared-memory copy
+// of the constant table (runtime k), so its sweep costs H FMA quadruples.
+template <int L, int R, int S, int G, int PL, int NTH>
+struct OddSplit {
+  static constexpr int NB = L / R, H = (R - 1) / 2;
+  static constexpr int NBt = G * NB, NBf = NBt / 32 * 32, REM = NBt - NBf;
+  static constexpr int P0 = NBf > 0 ? (NTH - 32) / NBf : 0;
+  static constexpr int P = P0 > H ? H : P0;
+  static constexpr bool ok = REM > 0 && NBf > 0 && P >= 1 && REM * H <= 32 && NTH % 32 == 0;
+};
+
+template <int L, int R, int S, int G, int PL, int NTH>
+__device__ __forceinline__ void stage_odd_cta_split(double2* sm, int tid) {
+  using Z = OddSplit<L, R, S, G, PL, NTH>;
+  using K = OddConst<R>;
+  constexpr int NB = Z::NB, H = Z::H, NBf = Z::NBf, P = Z::P;
+  constexpr int KPM = (H + P - 1) / P;
+  __shared__ double2 ocs[R];  // (cos, sin)(2 pi e / R)
+  if (tid < R) ocs[tid] = make_double2(K::c(tid), K::s(tid));
+  const int part = tid / NBf;  // warp-uniform (NBf % 32 == 0)
+  const bool mainp = part < P;
+  const int lane = tid - P * NBf;
+  const bool rem = lane >= 0 && lane < Z::REM * H;
+  // main butterflies: slots 0 .. NBf-1; leftover lane: butterfly NBf + lane/H, pair k
+  const int slot = mainp ? tid - part * NBf : (rem ? NBf + lane / H : 0);
+  const int line = slot / NB;
+  const int b = slot - line * NB;
+  double2* buf = sm + line * PL;
+  const int kr = rem ? 1 + lane % H : 0;
+  // fold the symmetric pairs in place (a_j at slot j, b_j at slot R-j)
+  if (mainp) {
+    const int j0 = 1 + (part * H) / P, j1 = ((part + 1) * H) / P;
+    for (int j = j0; j <= j1; ++j) {
+      double2& vj = buf[pad<L>(b + j * NB)];
+      double2& vm = buf[pad<L>(b + (R - j) * NB)];
+      const double2 x = vj, y = vm;
+      vj = cadd(x, y);
+      vm = csub(x, y);
+    }
+  } else if (rem) {
+    double2& vj = buf[pad<L>(b + kr * NB)];
+    double2& vm = buf[pad<L>(b + (R - kr) * NB)];
+    const double2 x = vj, y = vm;
+    vj = cadd(x, y);
+    vm = csub(x, y);
+  }
+  __syncthreads();
+  double2 out[2 * KPM];
+  double2 sum = make_double2(0.0, 0.0);
+  if (mainp) {
+    sum = buf[pad<L>(b)];
+    odd_pairs_smem_dispatch<R, S, L, H, P, 0, KPM>(part, buf, b, NB, sum, out, &sum);
+  } else if (rem) {
+    const double2 x0 = buf[pad<L>(b)];
+    double2 A = x0, B = make_double2(0.0, 0.0);
+    sum = x0;
+    int e = 0;
+#pragma unroll
+    for (int j = 1; j <= H; ++j) {
+      e += kr;
+      e = e >= R ? e - R : e;  // (j * kr) mod R
+      const double2 a = buf[pad<L>(b + j * NB)], c = buf[pad<L>(b + (R - j) * NB)];
+      const double2 w = ocs[e];
+      sum = cadd(sum, a);
+      A.x = fma(w.x, a.x, A.x);
+      A.y = fma(w.x, a.y, A.y);
+      B.x = fma(w.y, c.x, B.x);
+      B.y = fma(w.y, c.y, B.y);
+    }
+    const double2 sb = mul_si<S>(B);
+    out[0] = cadd(A, sb);
+    out[1] = csub(A, sb);
+  }
+  __syncthreads();
+  const int base = b * R;  // Ns = 1
+  if (mainp) {
+    if (part == 0) buf[pad<L>(base)] = sum;
+    odd_pairs_store_dispatch<R, S, L, H, P, 0>(part, out, buf, base, 1);
+  } else if (rem) {
+    if (kr == 1) buf[pad<L>(base)] = sum;
+    buf[pad<L>(base + kr)] = out[0];
+    buf[pad<L>(base + R - kr)] = out[1];
+  }
+  __syncthreads();
+}
+
 template <int L, int Ns, int R, int S, int G, int PL, int NTH>
 __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __restrict__ tw, int tid) {
+#ifndef DBX_NO_ODD_SPLIT
+  if constexpr (Ns == 1 && OddSplit<L, R, S, G, PL, NTH>::ok) {
+    stage_odd_cta_split<L, R, S, G, PL, NTH>(sm, tid);
+    return;
+  }
+#endif
   constexpr int NB = L / R;
   constexpr int H = (R - 1) / 2;
   constexpr int NBp = (G * NB + 31) / 32 * 32;
