@@ -31,10 +31,17 @@ namespace {
 // (C2: 512^2 -> 128 CTAs for 148 SMs), where per-CTA latency, not issue
 // width, sets the kernel time.
 __host__ __device__ constexpr int fused_dst_per(int) { return 8; }
+// Threads per fused DST line (FUSED_TD_ODD overrides long odd lines, A/B).
+#ifndef FUSED_TD_ODD
+#define FUSED_TD_ODD 128  // A/B r1s2m: 96 (line_threads) 14972, 128 15455, 160 15152, 192 15209
+#endif
+__host__ __device__ constexpr int fused_td(int M) {
+  return (FUSED_TD_ODD > 0 && (M & 1) && M > 512) ? FUSED_TD_ODD : line_threads(M, fused_dst_per(M));
+}
 
 template <int L2, int M, bool BLUE>
 struct Fused {
-  static constexpr int TD = line_threads(M, fused_dst_per(M));   // threads per line
+  static constexpr int TD = fused_td(M);   // threads per line
   static constexpr int NT = 2 * TD;                         // CTA = two FFT lines
   static constexpr int LC = padded_len(L2);                 // conv line (double2)
   static constexpr int LD = padded_len(M);                  // DST line (double2)
@@ -416,7 +423,7 @@ __global__ void __launch_bounds__(RsCfg<L2>::NT, 2) rows_ainv_resid(SpecArgs a) 
 // (pk_fill / pk_split), so the row-major stores are full 32-byte sectors.
 template <int M, bool BLUE>
 struct TcolSmem {
-  static constexpr int TD = line_threads(M, fused_dst_per(M));
+  static constexpr int TD = fused_td(M);
   static constexpr int LMAX = BLUE ? M / 2 + 1 : M + 1;         // max line length n
   static constexpr int LS = (LMAX + 1) / 2 * 2 + 4;             // line stride (doubles): 4 lines hit distinct banks
   static constexpr int LSO = ((LMAX > PkOut<LMAX>::OL ? LMAX : PkOut<LMAX>::OL) + 1) / 2 * 2 + 4;  // io lines
@@ -429,7 +436,7 @@ struct TcolSmem {
 };
 
 template <int M, bool BLUE>
-__global__ void __launch_bounds__(2 * line_threads(M, fused_dst_per(M)), 2) dst_tcols(SpecArgs a) {
+__global__ void __launch_bounds__(2 * fused_td(M), 2) dst_tcols(SpecArgs a) {
   using S = TcolSmem<M, BLUE>;
   constexpr int TD = S::TD, NT = 2 * TD, LS = S::LS, LSO = S::LSO, LMAX = S::LMAX;
   const int b = blockIdx.y;
