@@ -61,6 +61,7 @@ extern "C" {
 #define DBX_CONV_AUTO 0
 #define DBX_CONV_DIRECT 1
 #define DBX_CONV_FFT 2
+#define DBX_CONV_FFT_DENSE 3  /* FFT engine with the full 2D kernel spectrum even for a rank-1 mask */
 
 /* AR-transform engine selection (dbx_plan_set_dst).  FFT = packed real DST-I in
  * shared memory (two lines per complex N-point DFT) whose DFT core is direct
@@ -110,6 +111,17 @@ int dbx_plan_set_dst(dbx_plan* plan, int engine);
 /* Fused row pipelines for the preconditioned FFT-form iteration (default 1):
  * 6 launches + finalize per iteration instead of 9 + finalize. */
 int dbx_plan_set_fusion(dbx_plan* plan, int enable);
+
+/*
+ * Whether the FFT engine's column pass runs separable (*separable = 1): the
+ * mask factors as w = a b^T within 1e-14 of its largest tap (axis-aligned
+ * Gaussians, e.g. BASELINE C1, C3, C5), so FFT -> x H -> IFFT along each
+ * column is the direct 2 q1 + 1 tap correlation of the AR-extended column
+ * times one complex scale per column.  *resid = max |w - a b^T| / max |w|
+ * (of the mask and its 180-degree rotation).  Diagnostic; no reference
+ * equivalent (the reference correlates with the full mask, blur.hpp:39-68).
+ */
+int dbx_plan_separable(dbx_plan* plan, int* separable, double* resid);
 
 /* Engines the plan will use: *conv in {DBX_CONV_DIRECT, DBX_CONV_FFT},
  * *dst in {DBX_DST_DENSE, DBX_DST_FFT}. */

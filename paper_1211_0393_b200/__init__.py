@@ -66,6 +66,7 @@ def lib():
         L.dbx_plan_set_dst.argtypes = [vp, i]
         L.dbx_plan_engines.argtypes = [vp, C.POINTER(i), C.POINTER(i)]
         L.dbx_plan_pipeline.argtypes = [vp, C.POINTER(i)]
+        L.dbx_plan_separable.argtypes = [vp, C.POINTER(i), C.POINTER(d)]
         L.dbx_plan_set_fusion.argtypes = [vp, i]
         L.dbx_blur_apply.argtypes = [vp, vp, vp, i]
         L.dbx_precond_build.argtypes = [vp, d]
@@ -160,6 +161,7 @@ class ConvEngine(enum.IntEnum):
     Auto = 0
     Direct = 1
     Fft = 2
+    FftDense = 3  # FFT engine with the full 2D kernel spectrum even for a rank-1 mask
 
 
 class DstEngine(enum.IntEnum):
@@ -276,6 +278,13 @@ class BlurOperator:
         c, d = C.c_int(), C.c_int()
         _check(lib().dbx_plan_engines(self.handle, C.byref(c), C.byref(d)))
         return ConvEngine(c.value), DstEngine(d.value)
+
+    def separable(self):
+        """(True if the FFT column pass runs the rank-1 separable stencil,
+        max |w - a b^T| / max |w| of the mask's best rank-1 factorisation)."""
+        f, r = C.c_int(), C.c_double()
+        _check(lib().dbx_plan_separable(self.handle, C.byref(f), C.byref(r)))
+        return bool(f.value), float(r.value)
 
     def pipeline_fused(self) -> bool:
         """True when the last landweber run used the fused row pipelines."""

@@ -200,6 +200,8 @@ enum KClass { KC_BLUR_ADJ = 0, KC_BLUR = 1, KC_TRANSFORM = 2, KC_FINALIZE = 3, K
 
 }  // namespace
 
+constexpr double kSepTol = 1e-14;  // rank-1 test: max |w - a b^T| / max |w|
+
 struct dbx_plan {
   int n1 = 0, n2 = 0, batch = 0, q1 = 0, q2 = 0, device = 0;
   size_t N = 0;
@@ -237,6 +239,11 @@ struct dbx_plan {
   bool conv_ready = false;
   int L1 = 0, L2 = 0, Lh = 0;
   double *tw1 = nullptr, *tw2 = nullptr, *HA = nullptr, *HAt = nullptr;
+  // rank-1 mask: separable column pass (conv_col_sep) tables for A (rotated
+  // mask) and A' (mask); sep_ok when both factor within kSepTol
+  double *sepA_a = nullptr, *sepA_b = nullptr, *sepAt_a = nullptr, *sepAt_b = nullptr;
+  bool sep_ok = false;
+  double sep_resid = 1.0;
   DevBuf zb, yb, dT;  // dT: filter grid transposed (fused column pass)
   DevBuf cg_p, cg_q, cg_s, cg_z, cg_zero, cg_part, cg_sc;  // CGLS state (dbx_cgls_run)
   struct Blue {
@@ -287,7 +294,7 @@ struct dbx_plan {
   bool use_fft_conv() const {
     if (conv == DBX_CONV_DIRECT) return false;
     const bool fits = conv_len(n1, q1) > 0 && conv_len(n2, q2) > 0;
-    if (conv == DBX_CONV_FFT) return fits;
+    if (conv == DBX_CONV_FFT || conv == DBX_CONV_FFT_DENSE) return fits;
     return fits && (q1 > 7 || q2 > 7 || fused_shape());
   }
   bool fused_shape() const {
@@ -344,6 +351,15 @@ struct dbx_plan {
     return N1 >= 2 && N2 >= 2 && dst_core(N1, &M) >= 0 && dst_core(N2, &M) >= 0;
   }
 
+  // kernel spectrum of A (adjoint = false) or A' for the column pass, and the
+  // separable tables when the mask is rank 1 (unless DBX_CONV_FFT_DENSE)
+  void set_kernel(ConvTables& c, bool adjoint) const {
+    c.H = reinterpret_cast<const double2*>(adjoint ? HAt : HA);
+    const bool sep = sep_ok && conv != DBX_CONV_FFT_DENSE;
+    c.sepa = sep ? (adjoint ? sepAt_a : sepA_a) : nullptr;
+    c.sepb = sep ? reinterpret_cast<const double2*>(adjoint ? sepAt_b : sepA_b) : nullptr;
+  }
+
   void ensure_conv() {
     if (conv_ready) return;
     L1 = conv_len(n1, q1);
@@ -355,6 +371,21 @@ struct dbx_plan {
     std::vector<double> rot(taps.rbegin(), taps.rend());
     HA = upload_owned(conv_spectrum(rot.data(), q1, q2, L1, L2));
     HAt = upload_owned(conv_spectrum(taps.data(), q1, q2, L1, L2));
+    // separable column pass for a rank-1 mask (factorisation residual within
+    // kSepTol of the largest tap: rounding level, far below the 1e-10 parity)
+    if (q1 > 0 && conv_sep_supported(q1)) {
+      std::vector<double> aA, bA, aAt, bAt;
+      double rA = 1.0, rAt = 1.0;
+      if (rank1_factor(rot.data(), q1, q2, L2, kSepTol, aA, bA, &rA) &&
+          rank1_factor(taps.data(), q1, q2, L2, kSepTol, aAt, bAt, &rAt)) {
+        sepA_a = upload_owned(aA);
+        sepA_b = upload_owned(bA);
+        sepAt_a = upload_owned(aAt);
+        sepAt_b = upload_owned(bAt);
+        sep_ok = true;
+      }
+      sep_resid = std::max(rA, rAt);
+    }
     (void)nt;
     zb.ensure((size_t)batch * n1 * Lh * 2);
     yb.ensure((size_t)batch * n1 * y_stride(Lh) * 2);
@@ -501,7 +532,7 @@ struct dbx_plan {
       SpecArgs a = spec_base(stp, pt);
       a.conv.tw1 = reinterpret_cast<const double2*>(tw1);
       a.conv.tw2 = reinterpret_cast<const double2*>(tw2);
-      a.conv.H = reinterpret_cast<const double2*>(adjoint ? HAt : HA);
+      set_kernel(a.conv, adjoint);
       a.conv.L1 = L1; a.conv.L2 = L2; a.conv.Lh = Lh;
       a.zbuf = reinterpret_cast<double2*>(zb.p);
       a.ybuf = reinterpret_cast<double2*>(yb.p);
@@ -776,7 +807,8 @@ void* dbx_plan_stream(dbx_plan* plan) { return plan ? (void*)plan->stream : null
 int dbx_plan_set_conv(dbx_plan* plan, int conv) {
   return guarded([&] {
     require(plan != nullptr, "null plan");
-    require(conv == DBX_CONV_AUTO || conv == DBX_CONV_DIRECT || conv == DBX_CONV_FFT,
+    require(conv == DBX_CONV_AUTO || conv == DBX_CONV_DIRECT || conv == DBX_CONV_FFT ||
+                conv == DBX_CONV_FFT_DENSE,
             "dbx_plan_set_conv: unknown engine");
     plan->conv = conv;
   });
@@ -799,6 +831,16 @@ int dbx_plan_set_fusion(dbx_plan* plan, int enable) {
   return guarded([&] {
     require(plan != nullptr, "null plan");
     plan->fusion = enable != 0;
+  });
+}
+
+int dbx_plan_separable(dbx_plan* plan, int* separable, double* resid) {
+  return guarded([&] {
+    require(plan != nullptr, "null plan");
+    plan->set_dev();
+    if (plan->use_fft_conv()) plan->ensure_conv();
+    if (separable) *separable = plan->use_fft_conv() && plan->sep_ok && plan->conv != DBX_CONV_FFT_DENSE ? 1 : 0;
+    if (resid) *resid = plan->sep_resid;
   });
 }
 
@@ -922,7 +964,7 @@ int dbx_slab_blur(dbx_plan* P, const double* x_ext, double* y, int adjoint, cons
     SpecArgs a = P->spec_base(nullptr, pt);
     a.conv.tw1 = reinterpret_cast<const double2*>(P->tw1);
     a.conv.tw2 = reinterpret_cast<const double2*>(P->tw2);
-    a.conv.H = reinterpret_cast<const double2*>(adjoint ? P->HAt : P->HA);
+    P->set_kernel(a.conv, adjoint);
     a.conv.L1 = P->L1; a.conv.L2 = P->L2; a.conv.Lh = P->Lh;
     a.zbuf = reinterpret_cast<double2*>(P->zb.p);
     a.ybuf = reinterpret_cast<double2*>(P->yb.p);
@@ -1333,7 +1375,7 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
     auto enqueue_fused = [&](int k) {
       SpecArgs a = fa0;
       // K1: column pass of A' (spectral AR extension, kernel spectrum of the rotated mask)
-      a.conv.H = reinterpret_cast<const double2*>(P->HAt);
+      P->set_kernel(a.conv, true);
       P->ev_begin(KC_BLUR_ADJ); lc(launch_conv_col(a, s), "launch_conv_col"); P->ev_end();
       // K2: inverse row FFT -> A'r rows -> T~ along rows -> u
       a.out = P->u.p; a.outsel = SEL_EXPLICIT;
@@ -1348,7 +1390,7 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
       const int cnt_x = lc(launch_fused(FUSED_T_AXPY_AFWD, a, s), "rows_t_axpy_afwd");
       P->ev_end();
       // K5: column pass of A
-      a.conv.H = reinterpret_cast<const double2*>(P->HA);
+      P->set_kernel(a.conv, false);
       P->ev_begin(KC_BLUR); lc(launch_conv_col(a, s), "launch_conv_col"); P->ev_end();
       // K6: inverse row FFT -> r_k = g - A x_k + ||r||^2 -> forward row FFT for the next A'
       P->ev_begin(KC_BLUR);

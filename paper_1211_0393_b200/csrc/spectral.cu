@@ -278,6 +278,145 @@ conv_row_inv(SpecArgs a) {
   write_partials<NT>(a, e, red, b);
 }
 
+// ---------------------------------------------------------------------------
+// Column pass of a RANK-1 mask, w(t,u) = a_t b_u (the axis-aligned Gaussians of
+// C1, C3, C5).  The kernel spectrum factors, H[k2][k1] = conj(A(k1)) conj(B(k2))
+// / (L1 L2), so FFT_L1 -> x H -> IFFT_L1 of column k2 is the valid direct
+// correlation of the vertically AR-extended column with a, times
+// beta(k2) = conj(B(k2)) / L2:  Y[i][k2] = beta(k2) sum_t a_t Zext[i + t][k2]
+// (boundary.hpp:56-64 extension, blur.hpp:39-52 correlation along one axis).
+// 2q1+1 complex-by-real FMA pairs per output instead of two L1-point FFTs: no
+// barriers inside the arithmetic, every thread an independent register-blocked
+// stencil.  CK = 4 adjacent columns per CTA in a skewed smem layout (element p
+// of a column at p + p/8): lane (j, c) of a warp reads rows 8m + s of column c,
+// so each 8-lane phase hits 8 distinct 16-byte bank groups, and the stores of a
+// row's 4 columns are 64 contiguous bytes.
+constexpr int kSepCK = 4, kSepR = 8, kSepNT = 256, kSepBand = 1024;
+
+// Output rows are split into gridDim.z bands of sep_band rows (a multiple of
+// 8, at most kSepBand) so a CTA's staged columns stay within ~110 KB (two CTAs
+// per SM) at any image height; band z stages extended rows
+// [z RB, z RB + RB + 2 q1).
+__host__ __device__ constexpr int sep_bands(int n1) { return (n1 + kSepBand - 1) / kSepBand; }
+__host__ __device__ constexpr int sep_band(int n1, int nb) { return ((n1 + nb - 1) / nb + kSepR - 1) / kSepR * kSepR; }
+__host__ __device__ constexpr int sep_stride(int rb, int q1) {
+  const int e = rb + 2 * q1;
+  const int s = e + e / 8 + 1;
+  return s + ((2 - s % 8) + 8) % 8;  // = 2 mod 8: the 4 columns' bank groups interleave
+}
+__device__ __forceinline__ int skew(int p) { return p + (p >> 3); }
+
+template <int Q>
+__global__ void __launch_bounds__(kSepNT, 2) conv_col_sep(SpecArgs a) {
+  constexpr int NTAP = 2 * Q + 1, R = kSepR, CK = kSepCK;
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 sm[];
+  const int n1 = a.n1, Lh = a.conv.Lh;
+  const int k0 = blockIdx.x * CK;
+  const int RB = sep_band(n1, gridDim.z), S = sep_stride(RB, Q);
+  const int p0 = blockIdx.z * RB;                     // first extended row of the band
+  const int rows = min(RB, n1 - p0);                  // output rows of the band
+  const int NL = RB + 2 * Q;                          // staged rows (local l = p - p0)
+  const int E = n1 + 2 * Q;                           // extended column length
+  const double2* Z = a.zbuf + (size_t)b * n1 * Lh;
+  // ---- stage the band's staged-from-memory rows [lo, hi) (local index) with
+  // cp.async: the interior rows rho = l + p0 - q1 in [0, n1), or every row
+  // of the caller-extended slab (preext) ----
+  int lo, hi;
+  if (a.preext) {
+    lo = 0;
+    hi = min(NL, E - p0);
+    for (int idx = threadIdx.x; idx < (hi - lo) * CK; idx += kSepNT) {
+      const int l = idx / CK, c = idx % CK, k = k0 + c;
+      if (k < Lh) cp_async16(sm + c * S + skew(l), Z + (size_t)(p0 + l) * Lh + k);
+    }
+  } else {
+    const int rlo = max(0, p0 - Q), rhi = min(n1, p0 + NL - Q);
+    lo = rlo + Q - p0;
+    hi = rhi + Q - p0;
+    if (a.ztrans) {  // column k of Z^T is contiguous in rho
+      for (int c = 0; c < CK; ++c) {
+        const int k = k0 + c;
+        if (k >= Lh) break;
+        const double2* zc = Z + (size_t)k * n1;
+        for (int rho = rlo + threadIdx.x; rho < rhi; rho += kSepNT)
+          cp_async16(sm + c * S + skew(rho + Q - p0), zc + rho);
+      }
+    } else {  // row-major spectra: the CK columns of a row are contiguous
+      for (int idx = threadIdx.x; idx < (rhi - rlo) * CK; idx += kSepNT) {
+        const int rho = rlo + idx / CK, c = idx % CK, k = k0 + c;
+        if (k < Lh) cp_async16(sm + c * S + skew(rho + Q - p0), Z + (size_t)rho * Lh + k);
+      }
+    }
+  }
+  cp_async_commit();
+  double tap[NTAP];
+#pragma unroll
+  for (int t = 0; t < NTAP; ++t) tap[t] = __ldg(a.conv.sepa + t);
+  cp_async_wait_all();
+  __syncthreads();
+  // ---- the other local rows [0, lo) and [hi, NL): vertical extension (AR:
+  // Z[-i] = 2 Z[0] - Z[i]; reflective copies) from staged rows, zeros past
+  // the extended column ----
+  for (int idx = threadIdx.x; idx < (lo + NL - hi) * CK; idx += kSepNT) {
+    const int e = idx / CK, c = idx % CK, k = k0 + c;
+    const int l = e < lo ? e : hi + (e - lo), p = p0 + l, rho = p - Q;
+    double2 v = make_double2(0.0, 0.0);
+    if (k < Lh && p < E && !a.preext) {
+      const double2* col = sm + c * S;
+      if (a.bc == DBX_BC_REFLECTIVE) {
+        v = col[skew((rho < 0 ? -rho - 1 : 2 * n1 - 1 - rho) + Q - p0)];
+      } else {
+        const int r0 = rho < 0 ? 0 : n1 - 1, ri = rho < 0 ? -rho : 2 * (n1 - 1) - rho;
+        const double2 z0 = col[skew(r0 + Q - p0)], zi = col[skew(ri + Q - p0)];
+        v = make_double2(2.0 * z0.x - zi.x, 2.0 * z0.y - zi.y);
+      }
+    }
+    sm[c * S + skew(l)] = v;  // reads touch staged rows only
+  }
+  if (k0 + CK > Lh) {  // columns past Lh: read by the stencil, never stored
+    for (int idx = threadIdx.x; idx < (hi - lo) * CK; idx += kSepNT) {
+      const int l = lo + idx / CK, c = idx % CK;
+      if (k0 + c >= Lh) sm[c * S + skew(l)] = make_double2(0.0, 0.0);
+    }
+  }
+  __syncthreads();
+  // ---- register-blocked stencil: lane (j, c) computes rows 8m .. 8m+7 of
+  // column c (m = 8 w + j + 64 it); every staged value feeds all the
+  // accumulators it belongs to as soon as it is loaded ----
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = lane >> 2, c = lane & 3, k = k0 + c;
+  const double2 beta = k < Lh ? __ldg(a.conv.sepb + k) : make_double2(0.0, 0.0);
+  const int YS = y_stride(Lh);
+  double2* Y = a.ybuf + (size_t)b * n1 * YS + (size_t)p0 * YS;
+  const int nblk = (rows + R - 1) / R;
+  for (int m = w * 8 + j; m < nblk; m += (kSepNT / 32) * 8) {
+    const int i0 = m * R;
+    const double2* col = sm + c * S + 9 * (i0 >> 3);  // skew(i0 + s) = 9 i0/8 + s + s/8
+    double2 acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int s = 0; s < R + 2 * Q; ++s) {
+      const double2 z = col[s + (s >> 3)];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int t = s - r;
+        if (t >= 0 && t < NTAP) {
+          acc[r].x = fma(tap[t], z.x, acc[r].x);
+          acc[r].y = fma(tap[t], z.y, acc[r].y);
+        }
+      }
+    }
+    if (k < Lh) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (i0 + r < rows) Y[(size_t)(i0 + r) * YS + k] = cmul(acc[r], beta);
+    }
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -313,8 +452,31 @@ int launch_conv_row_fwd(const SpecArgs& a, cudaStream_t s) {
   return -1;
 }
 
+#define DBX_SEP_LIST(X) X(7) X(15)
+
+bool conv_sep_supported(int q1) {
+#define X(Q) if (q1 == (Q)) return true;
+  DBX_SEP_LIST(X)
+#undef X
+  return false;
+}
+
 int launch_conv_col(const SpecArgs& a, cudaStream_t s) {
   const int L1 = a.conv.L1;
+  if (a.conv.sepa) {
+    const int nb = sep_bands(a.n1);
+    const size_t sm = (size_t)kSepCK * sep_stride(sep_band(a.n1, nb), a.q1) * 16;
+#define X(Q)                                                                             \
+    if (a.q1 == (Q)) {                                                                   \
+      if (!set_smem(conv_col_sep<Q>, sm)) return -1;                                     \
+      dim3 grid((a.conv.Lh + kSepCK - 1) / kSepCK, a.batch, nb);                         \
+      conv_col_sep<Q><<<grid, kSepNT, sm, s>>>(a);                                       \
+      return (int)grid.x;                                                                \
+    }
+    DBX_SEP_LIST(X)
+#undef X
+    return -1;
+  }
 #define X(L)                                                                             \
   if (L1 == (L)) {                                                                       \
     constexpr int T = line_threads(L, 8), G = lines_for(L, kConvBudget, 8);                     \

@@ -22,6 +22,10 @@ struct ConvTables {
   const double2* tw2 = nullptr;
   const double2* H = nullptr;
   int L1 = 0, L2 = 0, Lh = 0;
+  // rank-1 mask w = a b^T (conv_col_sep): column taps a (2 q1 + 1) and the
+  // row factor's spectrum beta(k2) = conj(B(k2)) / L2 (Lh); null = full H
+  const double* sepa = nullptr;
+  const double2* sepb = nullptr;
 };
 
 // Bluestein DST-I tables for one line length n (device): M-point twiddles,
@@ -83,7 +87,8 @@ int rader_supported_len(int M);   // M (= N-1) if the Rader convolution length i
 // Each returns the number of CTAs per image (for the partial-sum count), -1 if
 // the size is not compiled.
 int launch_conv_row_fwd(const SpecArgs& a, cudaStream_t s);
-int launch_conv_col(const SpecArgs& a, cudaStream_t s);
+int launch_conv_col(const SpecArgs& a, cudaStream_t s);  // conv_col, or conv_col_sep when conv.sepa is set
+bool conv_sep_supported(int q1);                         // conv_col_sep compiled for this q1
 int launch_conv_row_inv(const SpecArgs& a, cudaStream_t s);
 int launch_dst_rows(const SpecArgs& a, cudaStream_t s);
 // CosineIII transforms along rows (dct.cu): kind1 = +1 forward R (DCT-II),

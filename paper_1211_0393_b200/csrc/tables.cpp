@@ -3,6 +3,7 @@
 // long double evaluation, so every table entry is the correctly rounded double
 // (naive sin(s t pi/(m+1)) arguments would burn ~1e-13 of the
 // parity budget at the config lengths).
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdint>
@@ -76,6 +77,37 @@ std::vector<double> conv_spectrum(const double* w, int q1, int q2, int L1, int L
       }
   });
   return H;
+}
+
+bool rank1_factor(const double* w, int q1, int q2, int L2, double tol, std::vector<double>& a,
+                  std::vector<double>& beta, double* resid) {
+  const int H1 = 2 * q1 + 1, W2 = 2 * q2 + 1, Lh = L2 / 2 + 1;
+  int i0 = 0, j0 = 0;
+  double mx = 0.0;
+  for (int t = 0; t < H1; ++t)
+    for (int u = 0; u < W2; ++u)
+      if (std::fabs(w[t * W2 + u]) > mx) mx = std::fabs(w[t * W2 + u]), i0 = t, j0 = u;
+  if (mx == 0.0) return false;
+  a.assign((size_t)H1, 0.0);
+  std::vector<double> bf((size_t)W2);
+  for (int t = 0; t < H1; ++t) a[(size_t)t] = w[t * W2 + j0];
+  for (int u = 0; u < W2; ++u) bf[(size_t)u] = w[i0 * W2 + u] / w[i0 * W2 + j0];
+  double r = 0.0;
+  for (int t = 0; t < H1; ++t)
+    for (int u = 0; u < W2; ++u) r = std::max(r, std::fabs(w[t * W2 + u] - a[(size_t)t] * bf[(size_t)u]));
+  if (resid) *resid = r / mx;
+  if (r > tol * mx) return false;
+  beta.assign(2 * (size_t)Lh, 0.0);
+  for (int k2 = 0; k2 < Lh; ++k2) {
+    std::complex<long double> acc = 0;
+    for (int u = 0; u < W2; ++u) {
+      const long double ang = 2.0L * kPiL * (long double)(((long)k2 * u) % L2) / (long double)L2;
+      acc += (long double)bf[(size_t)u] * std::complex<long double>(cosl(ang), -sinl(ang));
+    }
+    beta[2 * (size_t)k2] = (double)(acc.real() / (long double)L2);
+    beta[2 * (size_t)k2 + 1] = (double)(-acc.imag() / (long double)L2);
+  }
+  return true;
 }
 
 void blue_chirp(BlueHost& b, long N, int M);

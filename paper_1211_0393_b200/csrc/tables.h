@@ -11,6 +11,12 @@ std::vector<double> twiddles(int L);
 // Kernel spectrum of the correlation weights w ((2q1+1) x (2q2+1), row-major):
 // H[k2][k1] = conj(FFT2(w))[k1][k2] / (L1 L2), k1 < L1, k2 < L2/2 + 1 (k2-major).
 std::vector<double> conv_spectrum(const double* w, int q1, int q2, int L1, int L2);
+// Rank-1 factorisation w = a b^T of a (2 q1 + 1) x (2 q2 + 1) mask: true when
+// max |w - a b^T| <= tol * max |w|.  a: column factor (2 q1 + 1); beta: the
+// row factor's spectrum conj(B(k2)) / L2 for k2 < L2/2 + 1 (interleaved
+// re/im), the per-column scale of the separable column pass.
+bool rank1_factor(const double* w, int q1, int q2, int L2, double tol, std::vector<double>& a,
+                  std::vector<double>& beta, double* resid);
 
 struct BlueHost {
   int n = 0, N = 0, M = 0;

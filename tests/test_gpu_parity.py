@@ -47,6 +47,54 @@ def test_blur_matches_oracle(dev, oracle, n1, n2, q1, q2):
         assert rel(got, want) <= OP_TOL, (adj, rel(got, want))
 
 
+def sep_psf(rng, q1, q2):
+    """Rank-1 mask (outer product of two positive profiles), normalised."""
+    a = rng.uniform(0.05, 1.0, 2 * q1 + 1)
+    b = rng.uniform(0.05, 1.0, 2 * q2 + 1)
+    t = np.outer(a, b)
+    return t / t.sum()
+
+
+@pytest.mark.parametrize("n1,n2,q1,q2,bc", [(64, 64, 7, 7, "ar"), (96, 130, 15, 4, "ar"), (200, 77, 7, 12, "ar"),
+                                            (1024, 1024, 15, 15, "ar"), (61, 90, 15, 15, "reflective"),
+                                            (40, 33, 7, 0, "ar")])
+def test_separable_column_pass_matches_oracle(dev, oracle, n1, n2, q1, q2, bc):
+    """Rank-1 masks run the separable column pass (conv_col_sep: direct
+    2 q1 + 1 tap correlation of the extended column x one complex scale per
+    column) inside the FFT engine; A and A' match the oracle's full-mask
+    correlation like the dense kernel spectrum does."""
+    rng = np.random.default_rng(n1 * 7 + n2 * 3 + q1 + q2)
+    t = sep_psf(rng, q1, q2)
+    f = rng.uniform(0, 1, (n1, n2))
+    BC = dev.BoundaryCondition.AntiReflective if bc == "ar" else dev.BoundaryCondition.Reflective
+    obc = oracle.BC_ANTIREFLECTIVE if bc == "ar" else oracle.BC_REFLECTIVE
+    for eng in (dev.ConvEngine.Fft, dev.ConvEngine.FftDense):
+        op = dev.BlurOperator(dev.Psf(t), BC, n1, n2).set_conv(eng)
+        sep, resid = op.separable()
+        assert sep == (eng == dev.ConvEngine.Fft), (eng, sep, resid)
+        assert resid <= 1e-14
+        for adj in (False, True):
+            got = dev.apply_reblur_adjoint(op, f) if adj else dev.apply(op, f)
+            want = oracle.apply(t, f, adjoint=adj, path=1, bc=obc)
+            assert rel(got, want) <= OP_TOL, (eng, adj, rel(got, want))
+
+
+def test_separable_detection(dev):
+    """The BASELINE's axis-aligned Gaussians (C1, C3, C5) factor at rounding
+    level; the rotated (C4) and motion (C2) masks and a random mask do not."""
+    from paper_1211_0393_b200 import configs as cf
+    for name, want in (("C1", True), ("C3", True), ("C5", True), ("C2", False), ("C4", False)):
+        c = cf.CONFIGS[name]
+        taps = cf.make_psf(c)
+        n = 256 if name != "C4" else 200
+        op = dev.BlurOperator(dev.Psf(taps), dev.BoundaryCondition.AntiReflective, n, n)
+        sep, resid = op.separable()
+        assert sep == (want and c.q in (7, 15)), (name, sep, resid)
+    rng = np.random.default_rng(5)
+    op = dev.BlurOperator(dev.Psf(rand_psf(rng, 15, 15)), dev.BoundaryCondition.AntiReflective, 128, 128)
+    assert op.separable()[0] is False
+
+
 @pytest.mark.parametrize("name,n", [("C1", 256), ("C2", 512), ("C3", 160), ("C4", 200), ("C5", 96)])
 def test_config_blur_matches_oracle(dev, oracle, name, n):
     from paper_1211_0393_b200 import configs as cf
