@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -242,6 +243,7 @@ struct dbx_plan {
   // rank-1 mask: separable column pass (conv_col_sep) tables for A (rotated
   // mask) and A' (mask); sep_ok when both factor within kSepTol
   double *sepA_a = nullptr, *sepA_b = nullptr, *sepAt_a = nullptr, *sepAt_b = nullptr;
+  double *sepA_r = nullptr, *sepAt_r = nullptr;  // row factors (direct row passes, separable fused pipeline)
   bool sep_ok = false;
   double sep_resid = 1.0;
   DevBuf zb, yb, dT;  // dT: filter grid transposed (fused column pass)
@@ -358,6 +360,7 @@ struct dbx_plan {
     const bool sep = sep_ok && conv != DBX_CONV_FFT_DENSE;
     c.sepa = sep ? (adjoint ? sepAt_a : sepA_a) : nullptr;
     c.sepb = sep ? reinterpret_cast<const double2*>(adjoint ? sepAt_b : sepA_b) : nullptr;
+    c.sepr = sep ? (adjoint ? sepAt_r : sepA_r) : nullptr;
   }
 
   void ensure_conv() {
@@ -374,14 +377,16 @@ struct dbx_plan {
     // separable column pass for a rank-1 mask (factorisation residual within
     // kSepTol of the largest tap: rounding level, far below the 1e-10 parity)
     if (q1 > 0 && conv_sep_supported(q1)) {
-      std::vector<double> aA, bA, aAt, bAt;
+      std::vector<double> aA, bA, aAt, bAt, rwA, rwAt;
       double rA = 1.0, rAt = 1.0;
-      if (rank1_factor(rot.data(), q1, q2, L2, kSepTol, aA, bA, &rA) &&
-          rank1_factor(taps.data(), q1, q2, L2, kSepTol, aAt, bAt, &rAt)) {
+      if (rank1_factor(rot.data(), q1, q2, L2, kSepTol, aA, bA, &rA, &rwA) &&
+          rank1_factor(taps.data(), q1, q2, L2, kSepTol, aAt, bAt, &rAt, &rwAt)) {
         sepA_a = upload_owned(aA);
         sepA_b = upload_owned(bA);
         sepAt_a = upload_owned(aAt);
         sepAt_b = upload_owned(bAt);
+        sepA_r = upload_owned(rwA);
+        sepAt_r = upload_owned(rwAt);
         sep_ok = true;
       }
       sep_resid = std::max(rA, rAt);
@@ -1317,6 +1322,17 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
                        P->blue_tables(1, false).core != CORE_RADER &&
                        fused_supported(P->L2, P->blue_tables(1, false).M,
                                        P->blue_tables(1, false).core == CORE_BLUE);
+    // Separable fused pipeline (rank-1 mask): direct row passes in the row
+    // kernels and a real column pass instead of the row FFTs and the complex
+    // column pass (DBX_NO_SEP_ROWS=1 keeps the FFT rows, diagnostic A/B)
+    static const bool no_sep_rows = [] {
+      const char* e = std::getenv("DBX_NO_SEP_ROWS");
+      return e && e[0] == '1';
+    }();
+    const bool sepd = fused && !no_sep_rows && P->sep_ok && P->conv != DBX_CONV_FFT_DENSE &&
+                      conv_sep_supported(P->q1) &&
+                      fused_sep_supported(P->L2, P->blue_tables(1, false).M,
+                                          P->blue_tables(1, false).core == CORE_BLUE, P->n2, P->q2);
     P->last_fused = fused;
     SpecArgs fa0 = P->spec_base(P->st, pt);
     if (fused) {
@@ -1365,6 +1381,16 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
         return;
       }
       if (!fused) return;
+      if (sepd) {
+        // row pass of A' r_0 = A' g (r = g: no A x rows yet)
+        SpecArgs a = fa0;
+        P->set_kernel(a.conv, true);
+        a.in = nullptr; a.insel = SEL_EXPLICIT;
+        P->ev_begin(KC_BLUR_ADJ);
+        lc(launch_fused(FUSED_RESID_SEP, a, s), "rows_resid_sep");
+        P->ev_end();
+        return;
+      }
       // spectrum of the AR-extended r_0 = g for the first A' apply
       SpecArgs a = fa0;
       a.in = gd; a.insel = SEL_EXPLICIT;
@@ -1372,7 +1398,37 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
       lc(launch_conv_row_fwd(a, s), "launch_conv_row_fwd");
       P->ev_end();
     };
+    auto enqueue_fused_sep = [&]() {
+      SpecArgs a = fa0;
+      double* Yr = reinterpret_cast<double*>(P->yb.p);
+      // K1: column pass of A' (real): Z'^T -> Y' = A' r (row-major)
+      P->set_kernel(a.conv, true);
+      P->ev_begin(KC_BLUR_ADJ); lc(launch_cols_sep_real(a, s), "cols_sep_real"); P->ev_end();
+      // K2: s = A' r rows -> T~ along rows -> u
+      a.out = P->u.p; a.outsel = SEL_EXPLICIT;
+      P->ev_begin(KC_TRANSFORM); lc(launch_fused(FUSED_TT_SEP, a, s), "rows_tt_sep"); P->ev_end();
+      // K3: columns of u: T~ -> d -> T, into row-major s
+      a.in = P->u.p; a.insel = SEL_EXPLICIT; a.out = P->s.p; a.outsel = SEL_EXPLICIT;
+      a.kind1 = DBX_KIND_ARINV; a.kind2 = DBX_KIND_AR; a.epi = SPEC_STORE;
+      P->ev_begin(KC_TRANSFORM); lc(launch_fused(FUSED_DST_TCOLS, a, s), "dst_tcols"); P->ev_end();
+      // K4: T along rows -> x_k -> norms -> row pass of A x_k -> Z^T
+      P->set_kernel(a.conv, false);
+      a.in = P->s.p; a.out = P->X3.p; a.outsel = SEL_NXT; a.xold = P->X3.p; a.xoldsel = SEL_CUR;
+      P->ev_begin(KC_TRANSFORM);
+      const int cnt_x = lc(launch_fused(FUSED_T_AXPY_SEP, a, s), "rows_t_axpy_sep");
+      P->ev_end();
+      // K5: column pass of A (real): Z^T -> Y = A x_k
+      P->ev_begin(KC_BLUR); lc(launch_cols_sep_real(a, s), "cols_sep_real"); P->ev_end();
+      // K6: r = g - A x_k + ||r||^2 -> row pass of A' r -> Z'^T
+      P->set_kernel(a.conv, true);
+      a.in = Yr; a.insel = SEL_EXPLICIT;
+      P->ev_begin(KC_BLUR);
+      const int cnt_r = lc(launch_fused(FUSED_RESID_SEP, a, s), "rows_resid_sep");
+      P->ev_end();
+      return std::make_pair(cnt_x, cnt_r);
+    };
     auto enqueue_fused = [&](int k) {
+      if (sepd) return enqueue_fused_sep();
       SpecArgs a = fa0;
       // K1: column pass of A' (spectral AR extension, kernel spectrum of the rotated mask)
       P->set_kernel(a.conv, true);

@@ -141,7 +141,7 @@ __device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, 
 // rows_ainv_tt: FOUR rows per CTA.  Conv line g (TD threads) inverts the
 // spectra of rows 2g, 2g+1; DST line g then carries T~ of the same two rows
 // (packed real DST).  u is written transposed (u^T[k][row], 32-byte sectors).
-template <int L2, int M, bool BLUE>
+template <int L2, int M, bool BLUE, bool SEP = false>
 __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecArgs a) {
   using F = Fused<L2, M, BLUE>;
   constexpr int NT = F::NT, TD = F::TD, LS = F::LSO, LMAX = F::LMAX;
@@ -153,28 +153,44 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
   double* rowS = reinterpret_cast<double*>(base + F::off_rows);  // 4 rows: s, then T~ output
   const BlueTables& bt = a.blue2;
   const double2* twd = stage_twiddles<M, F::TT_TWD>(reinterpret_cast<double2*>(base + F::tt_twd), bt.tw);
-  const double2* twc = stage_twiddles<L2, F::TT_TWC>(reinterpret_cast<double2*>(base + F::tt_twc), a.conv.tw2);
+  const double2* twc =
+      stage_twiddles<L2, F::TT_TWC && !SEP>(reinterpret_cast<double2*>(base + F::tt_twc), a.conv.tw2);
   const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
   const size_t N = (size_t)n1 * n2;
   const int r0 = 4 * blockIdx.x;
   const int nl = n1 - r0 < 4 ? n1 - r0 : 4;
   const int g = threadIdx.x / TD, t = threadIdx.x - g * TD;
-  const int ra = r0 + 2 * g, rb = ra + 1;
   PH_DECL
-  // A' r rows: inverse packed row FFT (conv line g = rows 2g, 2g+1)
-  double2* cbuf = sm + g * F::LC;
-  conv_inv_load<L2, TD>(cbuf, a.ybuf + (size_t)b * n1 * y_stride(Lh), ra, rb, n1, Lh, t);
-  cp_async_wait_all();
-  __syncthreads();
-  PH(20)
-  fft::fft<L2, +1, TD>(cbuf, twc, t, 1 + g);
-  PH(21)
-  for (int c = t; c < n2; c += TD) {
-    const double2 v = cbuf[pad<L2>(c)];
-    rowS[(2 * g) * LS + c] = v.x;
-    rowS[(2 * g + 1) * LS + c] = v.y;
+  if constexpr (SEP) {
+    // separable pipeline: the column pass already produced s = A'r rows (real,
+    // row-major in ybuf): stage them straight into the DST input rows
+    __shared__ unsigned long long mbs[1];
+    bulk_init(mbs, 1);
+    const bool bs = stage_lines_bulk(rowS, LS, reinterpret_cast<const double*>(a.ybuf) + (size_t)b * N +
+                                                   (size_t)r0 * n2, nl, n2, mbs);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    stage_lines_wait(bs, mbs, nl);
+    (void)twc;
+    (void)Lh;
+  } else {
+    const int ra = r0 + 2 * g, rb = ra + 1;
+    // A' r rows: inverse packed row FFT (conv line g = rows 2g, 2g+1)
+    double2* cbuf = sm + g * F::LC;
+    conv_inv_load<L2, TD>(cbuf, a.ybuf + (size_t)b * n1 * y_stride(Lh), ra, rb, n1, Lh, t);
+    cp_async_wait_all();
+    __syncthreads();
+    PH(20)
+    fft::fft<L2, +1, TD>(cbuf, twc, t, 1 + g);
+    PH(21)
+    for (int c = t; c < n2; c += TD) {
+      const double2 v = cbuf[pad<L2>(c)];
+      rowS[(2 * g) * LS + c] = v.x;
+      rowS[(2 * g + 1) * LS + c] = v.y;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   PH(22)
   if (threadIdx.x < 4) {
     e0[threadIdx.x] = rowS[threadIdx.x * LS];
@@ -223,7 +239,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
 // rows_t_axpy_afwd: FOUR rows per CTA.  T (packed DST) of the rows of v ->
 // x_k = x_{k-1} + tau (.) with ||x||^2 / ||x - f||^2 partials -> forward
 // packed row FFTs of x_k (conv line g = rows 2g, 2g+1) -> Z^T.
-template <int L2, int M, bool BLUE>
+template <int L2, int M, bool BLUE, bool SEP = false>
 __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(SpecArgs a) {
   using F = Fused<L2, M, BLUE>;
   constexpr int NT = F::NT, TD = F::TD, LS = F::LS, LSO = F::LSO, LMAX = F::LMAX;
@@ -237,7 +253,8 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   double* stX = reinterpret_cast<double*>(base + F::off_x);    // x_{k-1} rows, then x_k
   const BlueTables& bt = a.blue2;
   const double2* twd = stage_twiddles<M, F::AX_TWD>(reinterpret_cast<double2*>(base + F::ax_twd), bt.tw);
-  const double2* twc = stage_twiddles<L2, F::AX_TWC>(reinterpret_cast<double2*>(base + F::ax_twc), a.conv.tw2);
+  const double2* twc =
+      stage_twiddles<L2, F::AX_TWC && !SEP>(reinterpret_cast<double2*>(base + F::ax_twc), a.conv.tw2);
   const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
   const size_t N = (size_t)n1 * n2;
   const int r0 = 4 * blockIdx.x;
@@ -314,9 +331,21 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   }
   __syncthreads();  // x rows complete; DST buffers free for the conv lines
   PH(14)
-  const int ra = r0 + 2 * g, rb = ra + 1;
-  conv_fwd_rows<L2, TD>(sm + g * F::LC, stX + (2 * g) * LS, stX + (2 * g + 1) * LS, n2, a.q2, twc,
-                        a.zbuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t, 1 + g);
+  if constexpr (SEP) {
+    // separable pipeline: row pass of A x_k as the direct row correlation of
+    // the AR-extended x_k rows (work region: the f rows are consumed)
+    double* ext = reinterpret_cast<double*>(sm);
+    const int LSX = sep_lsx(n2, a.q2);
+    sep_extend_rows(stX, LS, ext, LSX, n2, a.q2, nl);
+    __syncthreads();
+    sep_row_pass(ext, LSX, a.conv.sepr, a.q2, n2, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0, n1);
+    (void)twc;
+    (void)Lh;
+  } else {
+    const int ra = r0 + 2 * g, rb = ra + 1;
+    conv_fwd_rows<L2, TD>(sm + g * F::LC, stX + (2 * g) * LS, stX + (2 * g + 1) * LS, n2, a.q2, twc,
+                          a.zbuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t, 1 + g);
+  }
   PH(15)
   if (a.part.p) {
     double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
@@ -412,6 +441,60 @@ __global__ void __launch_bounds__(RsCfg<L2>::NT, 2) rows_ainv_resid(SpecArgs a) 
   if (a.part.p) {
     double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
     const double s0 = block_sum<NT>(p0, red);
+    if (threadIdx.x == 0) P[SLOT_R2 * a.part.cap + blockIdx.x] = s0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// rows_resid_sep (separable pipeline): FOUR rows per CTA.  r = g - A x_k
+// (A x_k rows from the column pass, row-major in ybuf; a.in == nullptr: r = g,
+// the first A' of a run) with ||r||^2 partials, then the row pass of A' r: the
+// AR-extended r rows correlated with the A' row taps -> Z'^T (solver.hpp:105,
+// blur.hpp:75-90 restricted to one axis).
+constexpr int kResidNT = 256;
+
+__host__ __device__ constexpr int resid_ls(int n2) { return (n2 + 1) / 2 * 2 + 4; }
+__host__ __device__ constexpr size_t resid_sep_bytes(int n2, int q2) {
+  return ((size_t)8 * resid_ls(n2) + (size_t)4 * sep_lsx(n2, q2)) * 8;
+}
+
+__global__ void __launch_bounds__(kResidNT, 2) rows_resid_sep(SpecArgs a) {
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 sm[];
+  __shared__ double red[32];
+  __shared__ unsigned long long mb[2];
+  const int n1 = a.n1, n2 = a.n2, q2 = a.q2, LS = resid_ls(n2), LSX = sep_lsx(n2, q2);
+  const size_t N = (size_t)n1 * n2;
+  const int r0 = 4 * blockIdx.x, nl = n1 - r0 < 4 ? n1 - r0 : 4;
+  double* yS = reinterpret_cast<double*>(sm);  // A x rows, then r
+  double* gS = yS + 4 * LS;
+  double* ext = gS + 4 * LS;
+  const bool have_y = a.in != nullptr;
+  bulk_init(mb, 2);
+  const bool bg = stage_lines_bulk(gS, LS, a.g + (size_t)b * N + (size_t)r0 * n2, nl, n2, mb);
+  cp_async_commit();
+  bool by = false;
+  if (have_y) by = stage_lines_bulk(yS, LS, a.in + (size_t)b * N + (size_t)r0 * n2, nl, n2, mb + 1);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  stage_lines_wait(bg, mb, nl);
+  if (have_y) stage_lines_wait(by, mb + 1, nl);
+  double p0 = 0.0;
+  for (int idx = threadIdx.x; idx < nl * n2; idx += kResidNT) {
+    const int h = idx / n2, c = idx - h * n2;
+    const double rv = have_y ? gS[h * LS + c] - yS[h * LS + c] : gS[h * LS + c];
+    yS[h * LS + c] = rv;
+    p0 += rv * rv;
+  }
+  __syncthreads();
+  sep_extend_rows(yS, LS, ext, LSX, n2, q2, nl);
+  __syncthreads();
+  sep_row_pass(ext, LSX, a.conv.sepr, q2, n2, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0, n1);
+  if (a.part.p) {
+    double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
+    const double s0 = block_sum<kResidNT>(p0, red);
     if (threadIdx.x == 0) P[SLOT_R2 * a.part.cap + blockIdx.x] = s0;
   }
 }
@@ -534,7 +617,9 @@ __global__ void __launch_bounds__(2 * fused_td(M), 2) dst_tcols(SpecArgs a) {
 template <int L2, int M, bool BLUE, int WHICH, typename K>
 int fused_launch(K kernel, const SpecArgs& a, cudaStream_t s) {
   using F = Fused<L2, M, BLUE>;
-  constexpr size_t bytes = WHICH == 0 ? F::tt_bytes : WHICH == 1 ? F::ax_bytes : RsCfg<L2>::bytes;
+  // WHICH: 0 tt, 1 t_axpy, 2 resid, 4 tt (separable), 5 t_axpy (separable)
+  constexpr size_t bytes = (WHICH == 0 || WHICH == 4) ? F::tt_bytes : (WHICH == 1 || WHICH == 5) ? F::ax_bytes
+                                                                                                   : RsCfg<L2>::bytes;
   constexpr int nt = WHICH == 2 ? RsCfg<L2>::NT : F::NT;
   constexpr int rows = 4;  // rows per CTA
   static bool init = false;
@@ -576,6 +661,15 @@ int fused_debug_phases(unsigned long long* out, int n) {
 // (conv L2, DST M, Bluestein?) combinations compiled for the fused pipeline.
 #define DBX_FUSED_LIST(X) X(1080, 1023, false) X(540, 1024, true) X(270, 255, false)
 
+bool fused_sep_supported(int L2, int M, bool blue, int n2, int q2) {
+  if (!conv_sep_supported(q2) || resid_sep_bytes(n2, q2) > 200 * 1024) return false;
+#define X(L, MM, BL) \
+  if (L2 == (L) && M == (MM) && blue == (BL)) return (size_t)4 * sep_lsx(n2, q2) * 8 <= (size_t)Fused<L, MM, BL>::W4 * 16;
+  DBX_FUSED_LIST(X)
+#undef X
+  return false;
+}
+
 bool fused_supported(int L2, int M, bool blue) {
 #define X(L, MM, BL) if (L2 == (L) && M == (MM) && blue == (BL)) return Fused<L, MM, BL>::ax_bytes <= 200 * 1024 && TcolSmem<MM, BL>::bytes <= 200 * 1024;
   DBX_FUSED_LIST(X)
@@ -584,6 +678,13 @@ bool fused_supported(int L2, int M, bool blue) {
 }
 
 int launch_fused(int which, const SpecArgs& a, cudaStream_t s) {
+  if (which == FUSED_RESID_SEP) {
+    const size_t bytes = resid_sep_bytes(a.n2, a.q2);
+    if (!set_smem(rows_resid_sep, bytes)) return -1;
+    dim3 grid((a.n1 + 3) / 4, a.batch);
+    rows_resid_sep<<<grid, kResidNT, bytes, s>>>(a);
+    return (int)grid.x;
+  }
   const int L2 = a.conv.L2, M = a.blue2.M;
   const bool blue = a.blue2.M != a.blue2.N;
 #define X(L, MM, BL)                                                                          \
@@ -592,6 +693,8 @@ int launch_fused(int which, const SpecArgs& a, cudaStream_t s) {
     if (which == FUSED_T_AXPY_AFWD) return fused_launch<L, MM, BL, 1>(rows_t_axpy_afwd<L, MM, BL>, a, s); \
     if (which == FUSED_AINV_RESID) return fused_launch<L, MM, BL, 2>(rows_ainv_resid<L>, a, s); \
     if (which == FUSED_DST_TCOLS) return tcols_launch<MM, BL>(a, s);                             \
+    if (which == FUSED_TT_SEP) return fused_launch<L, MM, BL, 4>(rows_ainv_tt<L, MM, BL, true>, a, s); \
+    if (which == FUSED_T_AXPY_SEP) return fused_launch<L, MM, BL, 5>(rows_t_axpy_afwd<L, MM, BL, true>, a, s); \
   }
   DBX_FUSED_LIST(X)
 #undef X

@@ -417,6 +417,88 @@ __global__ void __launch_bounds__(kSepNT, 2) conv_col_sep(SpecArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Column pass of the separable (rank-1 mask) fused pipeline on REAL data:
+// Y[i][c] = sum_t a_t Zext[i + t][c], Z^T = the row-correlated image stored
+// transposed ([c][row], real), Zext its vertical AR extension
+// (boundary.hpp:56-64), Y row-major.  CTA tile: 32 columns x a band of
+// kColBand rows; staged as [row][33] so a warp's lanes read 32 consecutive
+// doubles (one column each) and store 256 contiguous bytes of a Y row.
+// Each thread: 16 consecutive rows of its column, every staged value feeding
+// all its accumulators at once (31 FMAs per output for q1 = 15).
+constexpr int kColW = 32, kColLD = 33, kColBand = 256, kColRT = 16, kColNT = 256;
+
+template <int Q>
+__global__ void __launch_bounds__(kColNT, 2) cols_sep_real(SpecArgs a) {
+  constexpr int NTAP = 2 * Q + 1, NL = kColBand + 2 * Q, RT = kColRT;
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double smd[];
+  const int n1 = a.n1, n2 = a.n2;
+  const size_t N = (size_t)n1 * n2;
+  const int c0 = blockIdx.x * kColW, p0 = blockIdx.z * kColBand;
+  const int rows = min(kColBand, n1 - p0), E = n1 + 2 * Q;
+  const double* Z = reinterpret_cast<const double*>(a.zbuf) + (size_t)b * N;  // [c][row]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // stage interior rows rho in [rlo, rhi) at local l = rho + Q - p0 (cp.async, a column per warp pass)
+  const int rlo = max(0, p0 - Q), rhi = min(n1, p0 + NL - Q);
+  const int lo = rlo + Q - p0, hi = rhi + Q - p0;
+  for (int c = w; c < kColW; c += kColNT / 32) {
+    if (c0 + c >= n2) break;
+    const double* zc = Z + (size_t)(c0 + c) * n1;
+    for (int rho = rlo + lane; rho < rhi; rho += 32) cp_async8(smd + (rho + Q - p0) * kColLD + c, zc + rho);
+  }
+  cp_async_commit();
+  double tap[NTAP];
+#pragma unroll
+  for (int t = 0; t < NTAP; ++t) tap[t] = __ldg(a.conv.sepa + t);
+  cp_async_wait_all();
+  __syncthreads();
+  // extension rows (top band / bottom band) and zeros past the column or n2
+  for (int idx = threadIdx.x; idx < (lo + NL - hi) * kColW; idx += kColNT) {
+    const int e = idx / kColW, c = idx - e * kColW;
+    const int l = e < lo ? e : hi + (e - lo), p = p0 + l, rho = p - Q;
+    double v = 0.0;
+    if (c0 + c < n2 && p < E) {
+      if (a.bc == DBX_BC_REFLECTIVE) {
+        v = smd[((rho < 0 ? -rho - 1 : 2 * n1 - 1 - rho) + Q - p0) * kColLD + c];
+      } else {
+        const int r0 = rho < 0 ? 0 : n1 - 1, ri = rho < 0 ? -rho : 2 * (n1 - 1) - rho;
+        v = 2.0 * smd[(r0 + Q - p0) * kColLD + c] - smd[(ri + Q - p0) * kColLD + c];
+      }
+    }
+    smd[l * kColLD + c] = v;
+  }
+  if (c0 + kColW > n2)
+    for (int idx = threadIdx.x; idx < (hi - lo) * kColW; idx += kColNT) {
+      const int l = lo + idx / kColW, c = idx % kColW;
+      if (c0 + c >= n2) smd[l * kColLD + c] = 0.0;
+    }
+  __syncthreads();
+  double* Y = reinterpret_cast<double*>(a.ybuf) + (size_t)b * N + (size_t)p0 * n2 + c0 + lane;
+  const bool colok = c0 + lane < n2;
+  for (int i0 = w * RT; i0 < rows; i0 += (kColNT / 32) * RT) {
+    const double* col = smd + i0 * kColLD + lane;
+    double acc[RT];
+#pragma unroll
+    for (int r = 0; r < RT; ++r) acc[r] = 0.0;
+#pragma unroll
+    for (int s2 = 0; s2 < RT + 2 * Q; ++s2) {
+      const double z = col[s2 * kColLD];
+#pragma unroll
+      for (int r = 0; r < RT; ++r) {
+        const int t = s2 - r;
+        if (t >= 0 && t < NTAP) acc[r] = fma(tap[t], z, acc[r]);
+      }
+    }
+    if (colok) {
+#pragma unroll
+      for (int r = 0; r < RT; ++r)
+        if (i0 + r < rows) Y[(size_t)(i0 + r) * n2] = acc[r];
+    }
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -459,6 +541,20 @@ bool conv_sep_supported(int q1) {
   DBX_SEP_LIST(X)
 #undef X
   return false;
+}
+
+int launch_cols_sep_real(const SpecArgs& a, cudaStream_t s) {
+  const size_t sm = (size_t)(kColBand + 2 * a.q1) * kColLD * 8;
+#define X(Q)                                                                             \
+  if (a.q1 == (Q)) {                                                                     \
+    if (!set_smem(cols_sep_real<Q>, sm)) return -1;                                      \
+    dim3 grid((a.n2 + kColW - 1) / kColW, a.batch, (a.n1 + kColBand - 1) / kColBand);   \
+    cols_sep_real<Q><<<grid, kColNT, sm, s>>>(a);                                        \
+    return (int)grid.x;                                                                  \
+  }
+  DBX_SEP_LIST(X)
+#undef X
+  return -1;
 }
 
 int launch_conv_col(const SpecArgs& a, cudaStream_t s) {

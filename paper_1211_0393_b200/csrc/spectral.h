@@ -26,6 +26,7 @@ struct ConvTables {
   // row factor's spectrum beta(k2) = conj(B(k2)) / L2 (Lh); null = full H
   const double* sepa = nullptr;
   const double2* sepb = nullptr;
+  const double* sepr = nullptr;  // row taps b (2 q2 + 1): direct row pass of the separable fused pipeline
 };
 
 // Bluestein DST-I tables for one line length n (device): M-point twiddles,
@@ -98,8 +99,15 @@ int dct_supported_len(int m);
 int launch_dst_cols(const SpecArgs& a, cudaStream_t s);
 
 // Fused row pipelines of the preconditioned iteration (fused.cu).
-enum FusedKind { FUSED_AINV_TT = 0, FUSED_T_AXPY_AFWD = 1, FUSED_AINV_RESID = 2, FUSED_DST_TCOLS = 3 };
+// *_SEP: the separable (rank-1 mask) pipeline's row kernels — direct row
+// passes instead of the row FFTs (Z'^T / Y real, row-major Y).
+enum FusedKind {
+  FUSED_AINV_TT = 0, FUSED_T_AXPY_AFWD = 1, FUSED_AINV_RESID = 2, FUSED_DST_TCOLS = 3,
+  FUSED_TT_SEP = 4, FUSED_T_AXPY_SEP = 5, FUSED_RESID_SEP = 6
+};
 bool fused_supported(int L2, int M, bool bluestein);
+bool fused_sep_supported(int L2, int M, bool bluestein, int n2, int q2);
+int launch_cols_sep_real(const SpecArgs& a, cudaStream_t s);  // real column pass of the separable pipeline
 int launch_fused(int which, const SpecArgs& a, cudaStream_t s);
 #ifdef DBX_PHASES
 int fused_debug_phases(unsigned long long* out, int n);  // read + reset (instrumented builds)

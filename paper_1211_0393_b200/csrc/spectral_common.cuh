@@ -525,6 +525,75 @@ __device__ __forceinline__ void stage_lines_wait(bool bulk, unsigned long long* 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Direct row pass of a rank-1 mask (separable fused pipeline): the four rows
+// src[h] (smem, stride LS, length n2) are AR-extended horizontally
+// (boundary.hpp:56-62) into ext (stride LSX >= n2 + 2 q2 + 9, LSX = 4 mod
+// 16), then correlated with the row taps w (2 Q + 1), blur.hpp:39-52 along one
+// axis: outT[c * n1 + h] = sum_u w_u ext[h][c + u], c < n2, h < nl — stored
+// transposed (the column pass reads a column contiguously), 4 lanes = one
+// 32-byte sector.  Lane (cb, h) computes the 9 consecutive outputs of row h
+// starting at 9 cb (9 cb + 4 h hits 16 distinct 8-byte slots per half warp).
+__host__ __device__ constexpr int sep_lsx(int n2, int q2) {
+  const int e = n2 + 2 * q2 + 9;
+  return e + ((4 - e % 16) + 16) % 16;
+}
+
+__device__ __forceinline__ void sep_extend_rows(const double* src, int LS, double* ext, int LSX, int n2, int q2,
+                                                int nl) {
+  const int W = n2 + 2 * q2;
+  for (int idx = threadIdx.x; idx < 4 * W; idx += blockDim.x) {
+    const int h = idx / W, jp = idx - h * W, j = jp - q2;
+    const double* x = src + h * LS;
+    double v = 0.0;
+    if (h < nl) {
+      if (j < 0) v = 2.0 * x[0] - x[-j];
+      else if (j >= n2) v = 2.0 * x[n2 - 1] - x[2 * (n2 - 1) - j];
+      else v = x[j];
+    }
+    ext[h * LSX + jp] = v;
+  }
+}
+
+template <int Q>
+__device__ __forceinline__ void sep_row_stencil_T(const double* ext, int LSX, const double* __restrict__ w, int n2,
+                                                  int nl, double* outT, int n1) {
+  constexpr int R = 9, NTAP = 2 * Q + 1;
+  double tap[NTAP];
+#pragma unroll
+  for (int t = 0; t < NTAP; ++t) tap[t] = __ldg(w + t);
+  const int h = threadIdx.x & 3;
+  const int nblk = (n2 + R - 1) / R;
+  for (int cb = threadIdx.x >> 2; cb < nblk; cb += blockDim.x >> 2) {
+    const int c0 = cb * R;
+    const double* src = ext + h * LSX + c0;
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+#pragma unroll
+    for (int s = 0; s < R + 2 * Q; ++s) {
+      const double z = src[s];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int t = s - r;
+        if (t >= 0 && t < NTAP) acc[r] = fma(tap[t], z, acc[r]);
+      }
+    }
+    if (h < nl) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (c0 + r < n2) outT[(size_t)(c0 + r) * n1 + h] = acc[r];
+    }
+  }
+}
+
+// Q dispatch of the compiled separable row-tap counts (conv_sep_supported).
+__device__ __forceinline__ void sep_row_pass(const double* ext, int LSX, const double* w, int q2, int n2, int nl,
+                                             double* outT, int n1) {
+  if (q2 == 15) sep_row_stencil_T<15>(ext, LSX, w, n2, nl, outT, n1);
+  else if (q2 == 7) sep_row_stencil_T<7>(ext, LSX, w, n2, nl, outT, n1);
+}
+
 template <typename K>
 bool set_smem(K kernel, size_t bytes) {
   if (bytes > 227 * 1024) return false;

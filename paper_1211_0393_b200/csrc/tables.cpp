@@ -80,7 +80,7 @@ std::vector<double> conv_spectrum(const double* w, int q1, int q2, int L1, int L
 }
 
 bool rank1_factor(const double* w, int q1, int q2, int L2, double tol, std::vector<double>& a,
-                  std::vector<double>& beta, double* resid) {
+                  std::vector<double>& beta, double* resid, std::vector<double>* brow) {
   const int H1 = 2 * q1 + 1, W2 = 2 * q2 + 1, Lh = L2 / 2 + 1;
   int i0 = 0, j0 = 0;
   double mx = 0.0;
@@ -97,6 +97,7 @@ bool rank1_factor(const double* w, int q1, int q2, int L2, double tol, std::vect
     for (int u = 0; u < W2; ++u) r = std::max(r, std::fabs(w[t * W2 + u] - a[(size_t)t] * bf[(size_t)u]));
   if (resid) *resid = r / mx;
   if (r > tol * mx) return false;
+  if (brow) *brow = bf;
   beta.assign(2 * (size_t)Lh, 0.0);
   for (int k2 = 0; k2 < Lh; ++k2) {
     std::complex<long double> acc = 0;

@@ -14,9 +14,10 @@ std::vector<double> conv_spectrum(const double* w, int q1, int q2, int L1, int L
 // Rank-1 factorisation w = a b^T of a (2 q1 + 1) x (2 q2 + 1) mask: true when
 // max |w - a b^T| <= tol * max |w|.  a: column factor (2 q1 + 1); beta: the
 // row factor's spectrum conj(B(k2)) / L2 for k2 < L2/2 + 1 (interleaved
-// re/im), the per-column scale of the separable column pass.
+// re/im), the per-column scale of the separable column pass; brow: the row
+// factor b itself (2 q2 + 1) for a direct row pass.
 bool rank1_factor(const double* w, int q1, int q2, int L2, double tol, std::vector<double>& a,
-                  std::vector<double>& beta, double* resid);
+                  std::vector<double>& beta, double* resid, std::vector<double>* brow = nullptr);
 
 struct BlueHost {
   int n = 0, N = 0, M = 0;
