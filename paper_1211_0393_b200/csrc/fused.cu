@@ -482,11 +482,14 @@ __global__ void __launch_bounds__(kResidNT, 2) rows_resid_sep(SpecArgs a) {
   stage_lines_wait(bg, mb, nl);
   if (have_y) stage_lines_wait(by, mb + 1, nl);
   double p0 = 0.0;
-  for (int idx = threadIdx.x; idx < nl * n2; idx += kResidNT) {
-    const int h = idx / n2, c = idx - h * n2;
-    const double rv = have_y ? gS[h * LS + c] - yS[h * LS + c] : gS[h * LS + c];
-    yS[h * LS + c] = rv;
-    p0 += rv * rv;
+  for (int h = 0; h < nl; ++h) {
+    double* yr = yS + h * LS;
+    const double* gr = gS + h * LS;
+    for (int c = threadIdx.x; c < n2; c += kResidNT) {
+      const double rv = have_y ? gr[c] - yr[c] : gr[c];
+      yr[c] = rv;
+      p0 += rv * rv;
+    }
   }
   __syncthreads();
   sep_extend_rows(yS, LS, ext, LSX, n2, q2, nl);

@@ -541,15 +541,30 @@ __host__ __device__ constexpr int sep_lsx(int n2, int q2) {
 
 __device__ __forceinline__ void sep_extend_rows(const double* src, int LS, double* ext, int LSX, int n2, int q2,
                                                 int nl) {
-  const int W = n2 + 2 * q2;
-  for (int idx = threadIdx.x; idx < 4 * W; idx += blockDim.x) {
-    const int h = idx / W, jp = idx - h * W, j = jp - q2;
+  // interior copies (no per-element division or boundary test), then the
+  // 2 q2 mirrored samples per row
+  for (int h = 0; h < 4; ++h) {
+    const double* x = src + h * LS;
+    double* e = ext + h * LSX + q2;
+    if (h < nl) {
+      for (int j = threadIdx.x; j < n2; j += blockDim.x) e[j] = x[j];
+    } else {
+      for (int j = threadIdx.x; j < n2; j += blockDim.x) e[j] = 0.0;
+    }
+  }
+  for (int idx = threadIdx.x; idx < 8 * q2; idx += blockDim.x) {
+    const int h = idx / (2 * q2), m = idx - h * 2 * q2;  // m < q2: left sample q2 - m; else right
     const double* x = src + h * LS;
     double v = 0.0;
-    if (h < nl) {
-      if (j < 0) v = 2.0 * x[0] - x[-j];
-      else if (j >= n2) v = 2.0 * x[n2 - 1] - x[2 * (n2 - 1) - j];
-      else v = x[j];
+    int jp;
+    if (m < q2) {
+      const int k = q2 - m;  // f_{-k} = 2 f_0 - f_k
+      jp = q2 - k;
+      if (h < nl) v = 2.0 * x[0] - x[k];
+    } else {
+      const int k = m - q2 + 1;  // f_{n-1+k} = 2 f_{n-1} - f_{n-1-k}
+      jp = q2 + n2 - 1 + k;
+      if (h < nl) v = 2.0 * x[n2 - 1] - x[n2 - 1 - k];
     }
     ext[h * LSX + jp] = v;
   }
