@@ -454,8 +454,14 @@ __global__ void __launch_bounds__(RsCfg<L2>::NT, 2) rows_ainv_resid(SpecArgs a) 
 constexpr int kResidNT = 256;
 
 __host__ __device__ constexpr int resid_ls(int n2) { return (n2 + 1) / 2 * 2 + 4; }
+// g / r rows: data at offset 16 (128-byte aligned for the bulk copy), the 2 q2
+// AR extension samples written around them in place, stride = 4 mod 16
+__host__ __device__ constexpr int resid_lsr(int n2, int q2) {
+  const int e = 16 + n2 + q2 + 9;
+  return e + ((4 - e % 16) + 16) % 16;
+}
 __host__ __device__ constexpr size_t resid_sep_bytes(int n2, int q2) {
-  return ((size_t)8 * resid_ls(n2) + (size_t)4 * sep_lsx(n2, q2)) * 8;
+  return ((size_t)4 * resid_ls(n2) + (size_t)4 * resid_lsr(n2, q2)) * 8;
 }
 
 __global__ void __launch_bounds__(kResidNT, 2) rows_resid_sep(SpecArgs a) {
@@ -464,15 +470,14 @@ __global__ void __launch_bounds__(kResidNT, 2) rows_resid_sep(SpecArgs a) {
   extern __shared__ double2 sm[];
   __shared__ double red[32];
   __shared__ unsigned long long mb[2];
-  const int n1 = a.n1, n2 = a.n2, q2 = a.q2, LS = resid_ls(n2), LSX = sep_lsx(n2, q2);
+  const int n1 = a.n1, n2 = a.n2, q2 = a.q2, LS = resid_ls(n2), LSR = resid_lsr(n2, q2);
   const size_t N = (size_t)n1 * n2;
   const int r0 = 4 * blockIdx.x, nl = n1 - r0 < 4 ? n1 - r0 : 4;
-  double* yS = reinterpret_cast<double*>(sm);  // A x rows, then r
-  double* gS = yS + 4 * LS;
-  double* ext = gS + 4 * LS;
+  double* yS = reinterpret_cast<double*>(sm);  // A x rows
+  double* rS = yS + 4 * LS;                    // g rows at offset 16, then r in place + extension
   const bool have_y = a.in != nullptr;
   bulk_init(mb, 2);
-  const bool bg = stage_lines_bulk(gS, LS, a.g + (size_t)b * N + (size_t)r0 * n2, nl, n2, mb);
+  const bool bg = stage_lines_bulk(rS + 16, LSR, a.g + (size_t)b * N + (size_t)r0 * n2, nl, n2, mb);
   cp_async_commit();
   bool by = false;
   if (have_y) by = stage_lines_bulk(yS, LS, a.in + (size_t)b * N + (size_t)r0 * n2, nl, n2, mb + 1);
@@ -483,18 +488,31 @@ __global__ void __launch_bounds__(kResidNT, 2) rows_resid_sep(SpecArgs a) {
   if (have_y) stage_lines_wait(by, mb + 1, nl);
   double p0 = 0.0;
   for (int h = 0; h < nl; ++h) {
-    double* yr = yS + h * LS;
-    const double* gr = gS + h * LS;
+    const double* yr = yS + h * LS;
+    double* rr = rS + h * LSR + 16;
     for (int c = threadIdx.x; c < n2; c += kResidNT) {
-      const double rv = have_y ? gr[c] - yr[c] : gr[c];
-      yr[c] = rv;
+      const double rv = have_y ? rr[c] - yr[c] : rr[c];
+      rr[c] = rv;
       p0 += rv * rv;
     }
   }
   __syncthreads();
-  sep_extend_rows(yS, LS, ext, LSX, n2, q2, nl);
+  // horizontal AR extension of the r rows in place (boundary.hpp:56-62)
+  for (int idx = threadIdx.x; idx < 8 * q2; idx += kResidNT) {
+    const int h = idx / (2 * q2), m = idx - h * 2 * q2;
+    double* rr = rS + h * LSR + 16;
+    if (h < nl) {
+      if (m < q2) {
+        const int k = q2 - m;
+        rr[-k] = 2.0 * rr[0] - rr[k];
+      } else {
+        const int k = m - q2 + 1;
+        rr[n2 - 1 + k] = 2.0 * rr[n2 - 1] - rr[n2 - 1 - k];
+      }
+    }
+  }
   __syncthreads();
-  sep_row_pass(ext, LSX, a.conv.sepr, q2, n2, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0, n1);
+  sep_row_pass(rS + 16 - q2, LSR, a.conv.sepr, q2, n2, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0, n1);
   if (a.part.p) {
     double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
     const double s0 = block_sum<kResidNT>(p0, red);
