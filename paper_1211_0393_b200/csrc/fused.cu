@@ -63,7 +63,11 @@ struct Fused {
   static constexpr bool TT_TWC = tt_twc + TWC <= kBudget;
   static constexpr size_t tt_bytes = tt_twc + (TT_TWC ? TWC : 0);
   // rows_t_axpy_afwd: v rows (then T output), x rows, twiddles if they fit
-  static constexpr size_t ax_twd = off_x + (size_t)4 * LS * 8;
+  // x rows of rows_t_axpy: stride LS, or (separable variant) LSXR with the
+  // data at offset 16 and room for the in-place AR extension (q2 <= 15)
+  static constexpr int LSXR = (16 + LMAX + 15 + 9) + ((4 - (16 + LMAX + 15 + 9) % 16) + 16) % 16;
+  static constexpr int LSX_MAX = LSXR > LS ? LSXR : LS;
+  static constexpr size_t ax_twd = off_x + (size_t)4 * LSX_MAX * 8;
   static constexpr bool AX_TWD = ax_twd + TWD <= kBudget;
   static constexpr size_t ax_twc = ax_twd + (AX_TWD ? TWD : 0);
   static constexpr bool AX_TWC = ax_twc + TWC <= kBudget;
@@ -268,7 +272,8 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   bulk_init(mb, 2);
   const bool bv = stage_lines_bulk(io, LSO, a.in + (size_t)b * N + (size_t)r0 * n2, nl, n2, mb);  // v rows
   cp_async_commit();
-  const bool bx = stage_lines_bulk(stX, LS, xo, nl, n2, mb + 1);  // x_{k-1} rows
+  constexpr int XS = SEP ? F::LSXR : LS, XO = SEP ? 16 : 0;  // x row stride / offset
+  const bool bx = stage_lines_bulk(stX + XO, XS, xo, nl, n2, mb + 1);  // x_{k-1} rows
   cp_async_commit();
   cp_async_wait_group<1>();
   __syncthreads();
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   for (int h = 0; h < nl; ++h) {
     const double a0 = ia * e0[h], a1 = ia * e1[h];
     const double* o = io + h * LSO;
-    double* xs = stX + h * LS;
+    double* xs = stX + h * XS + XO;
     const double* fs = fS + h * LS;
     double* xr = xn + (size_t)h * n2;
 #pragma unroll 4
@@ -334,16 +339,29 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
   if constexpr (SEP) {
     // separable pipeline: row pass of A x_k as the direct row correlation of
     // the AR-extended x_k rows (work region: the f rows are consumed)
-    double* ext = reinterpret_cast<double*>(sm);
-    const int LSX = sep_lsx(n2, a.q2);
-    sep_extend_rows(stX, LS, ext, LSX, n2, a.q2, nl);
+    // (the x_k rows, extended in place around offset 16)
+    const int q2 = a.q2;
+    for (int idx = threadIdx.x; idx < 8 * q2; idx += NT) {
+      const int h = idx / (2 * q2), m = idx - h * 2 * q2;
+      double* xr = stX + h * XS + XO;
+      if (h < nl) {
+        if (m < q2) {
+          const int k = q2 - m;
+          xr[-k] = 2.0 * xr[0] - xr[k];
+        } else {
+          const int k = m - q2 + 1;
+          xr[n2 - 1 + k] = 2.0 * xr[n2 - 1] - xr[n2 - 1 - k];
+        }
+      }
+    }
     __syncthreads();
-    sep_row_pass(ext, LSX, a.conv.sepr, a.q2, n2, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0, n1);
+    sep_row_pass(stX + XO - q2, XS, a.conv.sepr, q2, n2, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0,
+                 n1);
     (void)twc;
     (void)Lh;
   } else {
     const int ra = r0 + 2 * g, rb = ra + 1;
-    conv_fwd_rows<L2, TD>(sm + g * F::LC, stX + (2 * g) * LS, stX + (2 * g + 1) * LS, n2, a.q2, twc,
+    conv_fwd_rows<L2, TD>(sm + g * F::LC, stX + (2 * g) * XS + XO, stX + (2 * g + 1) * XS + XO, n2, a.q2, twc,
                           a.zbuf + (size_t)b * n1 * Lh, ra, rb, n1, Lh, t, 1 + g);
   }
   PH(15)
@@ -685,7 +703,7 @@ int fused_debug_phases(unsigned long long* out, int n) {
 bool fused_sep_supported(int L2, int M, bool blue, int n2, int q2) {
   if (!conv_sep_supported(q2) || resid_sep_bytes(n2, q2) > 200 * 1024) return false;
 #define X(L, MM, BL) \
-  if (L2 == (L) && M == (MM) && blue == (BL)) return (size_t)4 * sep_lsx(n2, q2) * 8 <= (size_t)Fused<L, MM, BL>::W4 * 16;
+  if (L2 == (L) && M == (MM) && blue == (BL)) return n2 <= Fused<L, MM, BL>::LMAX && q2 <= 15;
   DBX_FUSED_LIST(X)
 #undef X
   return false;
