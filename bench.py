@@ -188,7 +188,7 @@ def other_configs(L, dbx, cf, torch, dev, local, reps=3):
             entry[("ms_per_run" if prec else "plain_ms_per_run")] = ms
             if prec:
                 L.dbx_plan_pipeline(plan, C.byref(fz))
-                entry["pipeline"] = "fused" if fz.value == 1 else "separate passes"
+                entry["pipeline"] = {0: "separate passes", 1: "fused", 2: "fused separable"}.get(fz.value, "?")
         L.dbx_plan_destroy(plan)
         out[name] = entry
         del g, f, o
@@ -434,7 +434,8 @@ def main():
     conv_e, dst_e, fz = C.c_int(), C.c_int(), C.c_int()
     L.dbx_plan_engines(plan, C.byref(conv_e), C.byref(dst_e))
     L.dbx_plan_pipeline(plan, C.byref(fz))
-    fft_conv, fft_dst, fused = conv_e.value == 2, dst_e.value == 2, fz.value == 1
+    fft_conv, fft_dst, fused = conv_e.value == 2, dst_e.value == 2, fz.value >= 1
+    separable = fz.value == 2
     p_fp64 = peaks.get("dfma_tflops_sustained", 34.0)
     fsrc = "measured DFMA FP64 sustained (profiles/r01_fp64_peak.json)"
     step_s = t_max * 1e-3 / args.steps
@@ -442,7 +443,7 @@ def main():
             "share_of_step": float(kms_tot[dom] / max(kms_tot.sum(), 1e-9)),
             "class_ms_per_step": {names[i]: float(kms_tot[i] / args.steps) for i in range(4)}}
     if fused and dom < 3:
-        cls = wm.fused_classes(n, q, B)[names[dom]]
+        cls = (wm.fused_sep_classes if separable else wm.fused_classes)(n, q, B)[names[dom]]
         flops, nbytes = cls["flops"] / cls["launches"], cls["bytes"] / cls["launches"]
         t_hbm, t_fp = nbytes / (hbm_peak * 1e9), flops / (p_fp64 * 1e12)
         gbs, tfs = nbytes / avg_s / 1e9, flops / avg_s / 1e12
@@ -458,10 +459,12 @@ def main():
         roof.update({"bound": "hbm" if t_hbm >= t_fp else "tensor", **main, "traffic": traffic,
                      "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per image, "
                                        "profiles/r01_ncu_traffic.json, x images per launch",
-                     "form": "fused FFT-form pipeline (packed real DST-I, FFT correlation)",
+                     "form": ("fused separable pipeline (rank-1 mask: direct row/column correlation passes; "
+                              "packed real FFT-form DST-I)") if separable else
+                             "fused FFT-form pipeline (packed real DST-I, FFT correlation)",
                      "secondary": other,
-                     "note": "nominal 5 N log2 N flops per FFT; arithmetic intensity below the FP64 ridge, "
-                             "so the HBM floor is the binding roofline"})
+                     "note": "nominal 5 N log2 N flops per FFT, 2(2q+1) per pixel per direct pass; arithmetic "
+                             "intensity below the FP64 ridge, so the HBM floor is the binding roofline"})
     else:
         per_launch_blur = (wm.conv_apply_flops(n, n, q, q) if fft_conv else wm.direct_apply_flops(n, n, q, q)) * B
         if dom == 2:

@@ -178,7 +178,9 @@ int dbx_slab_pack(dbx_plan* plan, const double* x, double* blocks, int parts, in
 /*
  * Pipeline used by the last dbx_landweber_run on this plan: *fused = 1 for the
  * fused row pipelines (6 launches + finalize per preconditioned iteration,
- * fused.cu), 0 for the separate passes.  Diagnostic; no reference equivalent.
+ * fused.cu), 2 for their separable form (rank-1 mask: direct row passes in
+ * the row kernels and a real column pass), 0 for the separate passes.
+ * Diagnostic; no reference equivalent.
  */
 int dbx_plan_pipeline(dbx_plan* plan, int* fused);
 

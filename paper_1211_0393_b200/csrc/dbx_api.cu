@@ -234,7 +234,7 @@ struct dbx_plan {
   int64_t glaunches = 0;
   bool fusion = true;  // fused row pipelines when compiled for the sizes
   int bc = DBX_BC_ANTIREFLECTIVE;  // BoundaryCondition of the blur (and the preconditioner algebra)
-  bool last_fused = false;  // pipeline of the last landweber run
+  int last_fused = 0;  // pipeline of the last landweber run: 0 separate passes, 1 fused, 2 fused separable
   // ---- FFT-form state ----
   int dst = DBX_DST_AUTO;
   bool conv_ready = false;
@@ -865,7 +865,7 @@ int dbx_debug_phases(unsigned long long* out, int n) { return dbx::fused_debug_p
 int dbx_plan_pipeline(dbx_plan* plan, int* fused) {
   return guarded([&] {
     require(plan != nullptr, "null plan");
-    if (fused) *fused = plan->last_fused ? 1 : 0;
+    if (fused) *fused = plan->last_fused;
   });
 }
 
@@ -1333,7 +1333,7 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
                       conv_sep_supported(P->q1) &&
                       fused_sep_supported(P->L2, P->blue_tables(1, false).M,
                                           P->blue_tables(1, false).core == CORE_BLUE, P->n2, P->q2);
-    P->last_fused = fused;
+    P->last_fused = fused ? (sepd ? 2 : 1) : 0;
     SpecArgs fa0 = P->spec_base(P->st, pt);
     if (fused) {
       fa0.conv.tw1 = reinterpret_cast<const double2*>(P->tw1);

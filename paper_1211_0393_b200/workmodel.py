@@ -86,6 +86,25 @@ def fused_classes(n: int, q: int, images: int) -> dict:
     }
 
 
+def fused_sep_classes(n: int, q: int, images: int) -> dict:
+    """Same for the separable pipeline of a rank-1 mask (fused.cu *_sep,
+    spectral.cu cols_sep_real): the blurs are direct row / column
+    correlations, 2(2q+1) flops per pixel per axis; every intermediate is a
+    real n x n array (8 n^2 bytes)."""
+    P = 8.0 * n * n
+    stencil = 2.0 * (2 * q + 1) * n * n
+    dst = n * dst_line_flops(n, packed=True)
+    return {
+        # rows_tt_sep (A'r rows -> T~ rows), dst_tcols (T~ cols, d, T cols),
+        # rows_t_axpy_sep (T rows + axpy + row pass of A x)
+        "ar_transform_pass": {"launches": 3, "flops": images * (4 * dst + stencil), "bytes": images * 9 * P + P},
+        # cols_sep_real(A) + rows_resid_sep (r = g - A x, row pass of A' r)
+        "blur(A)+residual": {"launches": 2, "flops": images * (2 * stencil + 2.0 * n * n), "bytes": images * 5 * P},
+        # cols_sep_real(A')
+        "blur_adjoint(A')": {"launches": 1, "flops": images * stencil, "bytes": images * 2 * P},
+    }
+
+
 def conv_apply_flops(n1: int, n2: int, q1: int, q2: int) -> float:
     L1, L2 = conv_len(n1, q1), conv_len(n2, q2)
     Lh = L2 // 2 + 1

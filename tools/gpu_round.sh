@@ -14,10 +14,10 @@ fi
 timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 echo "bench exit $?"; cat gpurun_out/${TAG}_bench.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
+  --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-other-configs \
   > gpurun_out/${TAG}_ncu_launch.log 2>&1
 echo "ncu launch list exit $?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'conv_col|rows_|dst_tcols' \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'conv_col|cols_sep|rows_|dst_tcols' \
   -s 7 -c 6 -o gpurun_out/${TAG}_full -f python bench.py --images 8 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
   > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "ncu full exit $?"

@@ -25,15 +25,17 @@ def main():
         ks.append({"kernel": r[hdr.index("Kernel Name")][:60], "bytes": rd + wr})
     assert len(ks) >= 6, "expected the six kernels of one fused iteration"
     ks = ks[:6]
-    # conv_col right after rows_t_axpy_afwd is A (blur class); the other is A'
+    # the column pass right after rows_t_axpy is A's (blur class); the other is A'
+    is_col = lambda k: "conv_col" in k["kernel"] or "cols_sep" in k["kernel"]
     ia = next(i for i, k in enumerate(ks) if "rows_t_axpy" in k["kernel"])
-    conv = [i for i, k in enumerate(ks) if "conv_col" in k["kernel"]]
+    conv = [i for i, k in enumerate(ks) if is_col(k)]
     ca = (ia + 1) % 6 if (ia + 1) % 6 in conv else conv[0]
     cadj = next(i for i in conv if i != ca)
     find = lambda s: next(i for i, k in enumerate(ks) if s in k["kernel"])
+    resid = next(i for i, k in enumerate(ks) if "resid" in k["kernel"])
     classes = {"blur_adjoint(A')": [cadj],
                "ar_transform_pass": [find("rows_ainv_tt"), find("dst_tcols"), ia],
-               "blur(A)+residual": [ca, find("rows_ainv_resid")]}
+               "blur(A)+residual": [ca, resid]}
     per = {c: sum(ks[i]["bytes"] for i in idx) / len(idx) / images for c, idx in classes.items()}
     json.dump({"report": rep.split("/")[-1], "images": images, "kernels": ks[:6],
                "per_image_launch_bytes": per}, open(out, "w"), indent=1)
