@@ -40,7 +40,7 @@ UNIT = "Mpixel-iterations/s"
 PEAKS_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
 HBM_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
-E2E_CHUNKS = int(os.environ.get("DBX_E2E_CHUNKS", "2"))  # measured best of 1/2/4/8 (r1s2j, r1s2k)
+E2E_CHUNKS = int(os.environ.get("DBX_E2E_CHUNKS", "4"))  # with 2 in flight: measured best (r1s2bb, r1s2cc)
 
 
 def parse():

@@ -259,9 +259,10 @@ int dbx_landweber_run(dbx_plan* plan, const double* g, const double* f_true, dou
  * use_precond, a built preconditioner on every plan).  HOST arrays only
  * (page-locked for overlap): the chunks' inputs are copied up on a copy stream
  * in chunk order, each chunk's solve starts as soon as its own inputs landed
- * (the chunks solve concurrently, one host thread per plan) and its restored
- * images are copied down on its own stream, so the host<->device traffic hides
- * behind the other chunks' solves.
+ * and the chunk two places earlier finished (two chunks solve concurrently,
+ * one host thread per plan; DBX_CHUNK_DEPTH overrides the two) and its
+ * restored images are copied down on its own stream, so the host<->device
+ * traffic hides behind the other chunks' solves.
  * Results equal dbx_landweber_run on the whole batch (images are
  * independent).  Divergence: every chunk still runs; the first diverging image
  * (global index) is reported with DBX_EDIVERGED.  No reference equivalent (the

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -1677,7 +1678,21 @@ int dbx_landweber_run_chunks(dbx_plan* const* plans, int nplans, const double* g
       }
       std::vector<int> rcs((size_t)nplans, DBX_OK);
       std::vector<std::string> msgs((size_t)nplans);
+      // at most `depth` chunks solve at once (chunk c starts when chunk
+      // c - depth has finished): concurrent chunks share the GPU and would all
+      // finish together, leaving every download for the end; a bounded
+      // pipeline finishes them in order, so all but the last downloads
+      // overlap the remaining solves
+      static const int depth = [] {
+        const char* e = std::getenv("DBX_CHUNK_DEPTH");
+        const int v = e ? std::atoi(e) : 2;
+        return v < 1 ? 1 : v;
+      }();
+      std::vector<std::promise<void>> fin((size_t)nplans);
+      std::vector<std::shared_future<void>> fin_f;
+      for (auto& pr : fin) fin_f.push_back(pr.get_future().share());
       auto work = [&](int c) {
+        if (c >= depth) fin_f[(size_t)(c - depth)].wait();
         dbx_plan* P = plans[c];
         const size_t img = first[(size_t)c], cnt = N * P->batch;
         int rc = DBX_OK;
@@ -1700,6 +1715,7 @@ int dbx_landweber_run_chunks(dbx_plan* const* plans, int nplans, const double* g
         }
         rcs[(size_t)c] = rc;
         msgs[(size_t)c] = g_err;  // g_err is per thread
+        fin[(size_t)c].set_value();
       };
       std::vector<std::thread> pool;
       for (int c = 1; c < nplans; ++c) pool.emplace_back(work, c);

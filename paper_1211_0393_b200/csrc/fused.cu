@@ -482,7 +482,7 @@ __host__ __device__ constexpr size_t resid_sep_bytes(int n2, int q2) {
   return ((size_t)4 * resid_ls(n2) + (size_t)4 * resid_lsr(n2, q2)) * 8;
 }
 
-__global__ void __launch_bounds__(kResidNT, 2) rows_resid_sep(SpecArgs a) {
+__global__ void __launch_bounds__(kResidNT, DBX_SEP_MINB) rows_resid_sep(SpecArgs a) {
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 sm[];

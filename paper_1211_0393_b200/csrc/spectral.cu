@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(kSepNT, 2) conv_col_sep(SpecArgs a) {
 constexpr int kColW = 32, kColLD = 33, kColBand = 256, kColRT = 16, kColNT = 256;
 
 template <int Q>
-__global__ void __launch_bounds__(kColNT, 2) cols_sep_real(SpecArgs a) {
+__global__ void __launch_bounds__(kColNT, DBX_SEP_MINB) cols_sep_real(SpecArgs a) {
   constexpr int NTAP = 2 * Q + 1, NL = kColBand + 2 * Q, RT = kColRT;
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;

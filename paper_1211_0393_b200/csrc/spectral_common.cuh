@@ -534,6 +534,11 @@ __device__ __forceinline__ void stage_lines_wait(bool bulk, unsigned long long* 
 // transposed (the column pass reads a column contiguously), 4 lanes = one
 // 32-byte sector.  Lane (cb, h) computes the 9 consecutive outputs of row h
 // starting at 9 cb (9 cb + 4 h hits 16 distinct 8-byte slots per half warp).
+// resident CTAs per SM the separable row/column kernels are compiled for
+#ifndef DBX_SEP_MINB
+#define DBX_SEP_MINB 2
+#endif
+
 __host__ __device__ constexpr int sep_lsx(int n2, int q2) {
   const int e = n2 + 2 * q2 + 9;
   return e + ((4 - e % 16) + 16) % 16;
