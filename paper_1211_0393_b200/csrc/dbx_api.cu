@@ -245,6 +245,7 @@ struct dbx_plan {
   // mask) and A' (mask); sep_ok when both factor within kSepTol
   double *sepA_a = nullptr, *sepA_b = nullptr, *sepAt_a = nullptr, *sepAt_b = nullptr;
   double *sepA_r = nullptr, *sepAt_r = nullptr;  // row factors (direct row passes, separable fused pipeline)
+  std::vector<double> sepA_a_h, sepAt_a_h;         // host copies of the column taps (kernel-parameter taps)
   bool sep_ok = false;
   double sep_resid = 1.0;
   DevBuf zb, yb, dT;  // dT: filter grid transposed (fused column pass)
@@ -362,6 +363,7 @@ struct dbx_plan {
     c.sepa = sep ? (adjoint ? sepAt_a : sepA_a) : nullptr;
     c.sepb = sep ? reinterpret_cast<const double2*>(adjoint ? sepAt_b : sepA_b) : nullptr;
     c.sepr = sep ? (adjoint ? sepAt_r : sepA_r) : nullptr;
+    c.sepa_host = sep ? (adjoint ? sepAt_a_h.data() : sepA_a_h.data()) : nullptr;
   }
 
   void ensure_conv() {
@@ -388,6 +390,8 @@ struct dbx_plan {
         sepAt_b = upload_owned(bAt);
         sepA_r = upload_owned(rwA);
         sepAt_r = upload_owned(rwAt);
+        sepA_a_h = aA;
+        sepAt_a_h = aAt;
         sep_ok = true;
       }
       sep_resid = std::max(rA, rAt);
@@ -1308,8 +1312,8 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
     Partials pt{P->part.p, P->part_cap};
 
     launch_state_init(P->st, B, s);
-    launch_norms_init(gd, fd, B, N, P->st, nullptr, s);
-    P->launches += 2;
+    launch_norms_init(gd, fd, B, N, P->st, pt, s);
+    P->launches += 3;
     // x_0 = 0 in buffer 0, r_0 = g
     ck(cudaMemsetAsync(P->X3.p, 0, cnt * sizeof(double), s), "memset");
     ck(cudaMemcpyAsync(P->r.p, gd, cnt * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");

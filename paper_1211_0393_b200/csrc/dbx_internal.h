@@ -95,8 +95,8 @@ void launch_build_filter(const double* sym_taps, int q1, int q2, int n1, int n2,
 void launch_build_filter_block(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha, int r0,
                                int nr, int c0, int nc, int tr, double* d, int* zero_flag, cudaStream_t s,
                                int grid = 0);
-void launch_norms_init(const double* g, const double* f, int batch, size_t N, ImgState* st,
-                       double* scratch, cudaStream_t s);
+void launch_norms_init(const double* g, const double* f, int batch, size_t N, ImgState* st, Partials pt,
+                       cudaStream_t s);
 struct FinalizeArgs {
   ImgState* st;
   Partials part;

@@ -85,14 +85,34 @@ __device__ double strided_sumsq(const double* p, size_t n) {
   return block_reduce(s);
 }
 
-__global__ void norms_init_kernel(const double* g, const double* f, size_t N, ImgState* st) {
+// ||g||, ||f|| (solver.hpp:73-74, image.hpp:85-91) as a two-level fixed-order
+// reduction: grid (K, batch) CTAs each reduce one contiguous chunk into the
+// partials buffer, then one CTA per image sums its K partials in index order
+// (deterministic; a single CTA per image left 148-SM HBM idle: 59 ms for one
+// 8192^2 image).
+__global__ void norms_partial_kernel(const double* g, const double* f, size_t N, size_t chunk, Partials pt) {
+  const int b = blockIdx.y, k = blockIdx.x;
+  const size_t lo = (size_t)k * chunk, n = lo < N ? (N - lo < chunk ? N - lo : chunk) : 0;
+  const double gs = strided_sumsq(g + (size_t)b * N + lo, n);
+  const double fs = f ? strided_sumsq(f + (size_t)b * N + lo, n) : 0.0;
+  if (threadIdx.x == 0) {
+    double* P = pt.p + (size_t)b * NUM_SLOTS * pt.cap;
+    P[SLOT_X2 * pt.cap + k] = gs;
+    P[SLOT_XF2 * pt.cap + k] = fs;
+  }
+}
+
+__global__ void norms_init_kernel(Partials pt, int cnt, int has_f, ImgState* st) {
   const int b = blockIdx.x;
-  const double gs = strided_sumsq(g + (size_t)b * N, N);
-  double fs = 0.0;
-  if (f) fs = strided_sumsq(f + (size_t)b * N, N);
+  const double* P = pt.p + (size_t)b * NUM_SLOTS * pt.cap;
+  double gs = 0.0, fs = 0.0;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) gs += P[SLOT_X2 * pt.cap + i];
+  gs = block_reduce(gs);
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) fs += P[SLOT_XF2 * pt.cap + i];
+  fs = block_reduce(fs);
   if (threadIdx.x == 0) {
     st[b].g_norm = sqrt(gs);
-    st[b].f_norm = f ? sqrt(fs) : 0.0;
+    st[b].f_norm = has_f ? sqrt(fs) : 0.0;
   }
 }
 
@@ -231,9 +251,17 @@ void launch_build_filter_block(const double* sym_taps, int q1, int q2, int n1, i
   cudaFreeAsync(c2, s);
 }
 
-void launch_norms_init(const double* g, const double* f, int batch, size_t N, ImgState* st,
-                       double* /*scratch*/, cudaStream_t s) {
-  norms_init_kernel<<<batch, 1024, 0, s>>>(g, f, N, st);
+void launch_norms_init(const double* g, const double* f, int batch, size_t N, ImgState* st, Partials pt,
+                       cudaStream_t s) {
+  // ~4 resident 512-thread CTAs per SM over the whole batch, chunks >= 16 K elements
+  size_t K = (size_t)(4 * 148 + batch - 1) / batch;
+  const size_t kmax = (N + 16383) / 16384;
+  if (K > kmax) K = kmax;
+  if (K > (size_t)pt.cap) K = pt.cap;
+  if (K < 1) K = 1;
+  const size_t chunk = (N + K - 1) / K;
+  norms_partial_kernel<<<dim3((unsigned)K, batch), 512, 0, s>>>(g, f, N, chunk, pt);
+  norms_init_kernel<<<batch, 256, 0, s>>>(pt, (int)K, f != nullptr, st);
 }
 
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s) {

@@ -24,6 +24,8 @@
 //                  half of D = T diag(d) T~ in one pass.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "spectral_common.cuh"
 
 namespace dbx {
@@ -421,23 +423,32 @@ __global__ void __launch_bounds__(kSepNT, 2) conv_col_sep(SpecArgs a) {
 // Column pass of the separable (rank-1 mask) fused pipeline on REAL data:
 // Y[i][c] = sum_t a_t Zext[i + t][c], Z^T = the row-correlated image stored
 // transposed ([c][row], real), Zext its vertical AR extension
-// (boundary.hpp:56-64), Y row-major.  CTA tile: 32 columns x a band of
-// kColBand rows; staged as [row][33] so a warp's lanes read 32 consecutive
-// doubles (one column each) and store 256 contiguous bytes of a Y row.
-// Each thread: 16 consecutive rows of its column, every staged value feeding
-// all its accumulators at once (31 FMAs per output for q1 = 15).
-constexpr int kColW = 32, kColLD = 33, kColBand = 256, kColRT = 16, kColNT = 256;
+// (boundary.hpp:56-64), Y row-major.  CTA tile: 32 columns x a band of BAND
+// rows; staged as [row][33] so a warp's lanes read 32 consecutive doubles (one
+// column each) and store 256 contiguous bytes of a Y row.  Each thread: 16
+// consecutive rows of its column, every staged value feeding all its
+// accumulators at once (31 FMAs per output for q1 = 15).  The taps travel as
+// kernel parameters: the DFMAs read them from the constant bank, so they cost
+// no registers (64 fewer than taps held in registers) and more CTAs fit per SM.
+constexpr int kColW = 32, kColLD = 33, kColRT = 16, kColNT = 256;
 
-template <int Q>
-__global__ void __launch_bounds__(kColNT, DBX_SEP_MINB) cols_sep_real(SpecArgs a) {
-  constexpr int NTAP = 2 * Q + 1, NL = kColBand + 2 * Q, RT = kColRT;
+template <int NTAP>
+struct ColTaps {
+  double t[NTAP];
+};
+
+__host__ __device__ constexpr int col_minb(int band) { return band <= 128 ? 4 : band <= 192 ? 3 : 2; }
+
+template <int Q, int BAND>
+__global__ void __launch_bounds__(kColNT, col_minb(BAND)) cols_sep_real(SpecArgs a, const ColTaps<2 * Q + 1> tp) {
+  constexpr int NTAP = 2 * Q + 1, NL = BAND + 2 * Q, RT = kColRT;
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double smd[];
   const int n1 = a.n1, n2 = a.n2;
   const size_t N = (size_t)n1 * n2;
-  const int c0 = blockIdx.x * kColW, p0 = blockIdx.z * kColBand;
-  const int rows = min(kColBand, n1 - p0), E = n1 + 2 * Q;
+  const int c0 = blockIdx.x * kColW, p0 = blockIdx.z * BAND;
+  const int rows = min(BAND, n1 - p0), E = n1 + 2 * Q;
   const double* Z = reinterpret_cast<const double*>(a.zbuf) + (size_t)b * N;  // [c][row]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // stage interior rows rho in [rlo, rhi) at local l = rho + Q - p0 (cp.async, a column per warp pass)
@@ -449,9 +460,6 @@ __global__ void __launch_bounds__(kColNT, DBX_SEP_MINB) cols_sep_real(SpecArgs a
     for (int rho = rlo + lane; rho < rhi; rho += 32) cp_async8(smd + (rho + Q - p0) * kColLD + c, zc + rho);
   }
   cp_async_commit();
-  double tap[NTAP];
-#pragma unroll
-  for (int t = 0; t < NTAP; ++t) tap[t] = __ldg(a.conv.sepa + t);
   cp_async_wait_all();
   __syncthreads();
   // extension rows (top band / bottom band) and zeros past the column or n2
@@ -488,7 +496,7 @@ __global__ void __launch_bounds__(kColNT, DBX_SEP_MINB) cols_sep_real(SpecArgs a
 #pragma unroll
       for (int r = 0; r < RT; ++r) {
         const int t = s2 - r;
-        if (t >= 0 && t < NTAP) acc[r] = fma(tap[t], z, acc[r]);
+        if (t >= 0 && t < NTAP) acc[r] = fma(tp.t[t], z, acc[r]);
       }
     }
     if (colok) {
@@ -543,15 +551,32 @@ bool conv_sep_supported(int q1) {
   return false;
 }
 
+template <int Q, int BAND>
+int launch_cols_sep_real_t(const SpecArgs& a, cudaStream_t s) {
+  ColTaps<2 * Q + 1> tp;
+  if (!a.conv.sepa_host) return -1;
+  for (int t = 0; t < 2 * Q + 1; ++t) tp.t[t] = a.conv.sepa_host[t];
+  const size_t sm = (size_t)(BAND + 2 * Q) * kColLD * 8;
+  if (!set_smem(cols_sep_real<Q, BAND>, sm)) return -1;
+  dim3 grid((a.n2 + kColW - 1) / kColW, a.batch, (a.n1 + BAND - 1) / BAND);
+  cols_sep_real<Q, BAND><<<grid, kColNT, sm, s>>>(a, tp);
+  return (int)grid.x;
+}
+
+// row band per CTA: 256 (2 CTAs / SM) or 128 (4 CTAs / SM); DBX_COL_BAND overrides
+static int col_band() {
+  static int band = [] {
+    const char* e = getenv("DBX_COL_BAND");
+    const int v = e ? atoi(e) : 128;
+    return v == 256 ? 256 : 128;
+  }();
+  return band;
+}
+
 int launch_cols_sep_real(const SpecArgs& a, cudaStream_t s) {
-  const size_t sm = (size_t)(kColBand + 2 * a.q1) * kColLD * 8;
 #define X(Q)                                                                             \
-  if (a.q1 == (Q)) {                                                                     \
-    if (!set_smem(cols_sep_real<Q>, sm)) return -1;                                      \
-    dim3 grid((a.n2 + kColW - 1) / kColW, a.batch, (a.n1 + kColBand - 1) / kColBand);   \
-    cols_sep_real<Q><<<grid, kColNT, sm, s>>>(a);                                        \
-    return (int)grid.x;                                                                  \
-  }
+  if (a.q1 == (Q))                                                                       \
+    return col_band() == 256 ? launch_cols_sep_real_t<Q, 256>(a, s) : launch_cols_sep_real_t<Q, 128>(a, s);
   DBX_SEP_LIST(X)
 #undef X
   return -1;

@@ -27,6 +27,7 @@ struct ConvTables {
   const double* sepa = nullptr;
   const double2* sepb = nullptr;
   const double* sepr = nullptr;  // row taps b (2 q2 + 1): direct row pass of the separable fused pipeline
+  const double* sepa_host = nullptr;  // host copy of sepa: cols_sep_real takes its taps as kernel parameters
 };
 
 // Bluestein DST-I tables for one line length n (device): M-point twiddles,
