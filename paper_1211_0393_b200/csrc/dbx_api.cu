@@ -246,6 +246,7 @@ struct dbx_plan {
   double *sepA_a = nullptr, *sepA_b = nullptr, *sepAt_a = nullptr, *sepAt_b = nullptr;
   double *sepA_r = nullptr, *sepAt_r = nullptr;  // row factors (direct row passes, separable fused pipeline)
   std::vector<double> sepA_a_h, sepAt_a_h;         // host copies of the column taps (kernel-parameter taps)
+  std::vector<double> sepA_r_h, sepAt_r_h;         // host copies of the row taps (ConvTables::sepr_v)
   bool sep_ok = false;
   double sep_resid = 1.0;
   DevBuf zb, yb, dT;  // dT: filter grid transposed (fused column pass)
@@ -364,6 +365,10 @@ struct dbx_plan {
     c.sepb = sep ? reinterpret_cast<const double2*>(adjoint ? sepAt_b : sepA_b) : nullptr;
     c.sepr = sep ? (adjoint ? sepAt_r : sepA_r) : nullptr;
     c.sepa_host = sep ? (adjoint ? sepAt_a_h.data() : sepA_a_h.data()) : nullptr;
+    if (sep) {
+      const std::vector<double>& r = adjoint ? sepAt_r_h : sepA_r_h;
+      for (size_t t = 0; t < r.size() && t < 31; ++t) c.sepr_v[t] = r[t];
+    }
   }
 
   void ensure_conv() {
@@ -392,6 +397,8 @@ struct dbx_plan {
         sepAt_r = upload_owned(rwAt);
         sepA_a_h = aA;
         sepAt_a_h = aAt;
+        sepA_r_h = rwA;
+        sepAt_r_h = rwAt;
         sep_ok = true;
       }
       sep_resid = std::max(rA, rAt);

@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
       }
     }
     __syncthreads();
-    sep_row_pass(stX + XO - q2, XS, a.conv.sepr, q2, n2, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0,
+    sep_row_pass(stX + XO - q2, XS, a.conv, q2, n2, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0,
                  n1);
     (void)twc;
     (void)Lh;
@@ -478,41 +478,58 @@ __host__ __device__ constexpr int resid_lsr(int n2, int q2) {
   const int e = 16 + n2 + q2 + 9;
   return e + ((4 - e % 16) + 16) % 16;
 }
+// only the g / r rows are staged: A x is read straight from global in the
+// residual loop (coalesced, once), halving the shared memory per CTA so four
+// CTAs fit per SM
 __host__ __device__ constexpr size_t resid_sep_bytes(int n2, int q2) {
-  return ((size_t)4 * resid_ls(n2) + (size_t)4 * resid_lsr(n2, q2)) * 8;
+  return (size_t)4 * resid_lsr(n2, q2) * 8;
 }
 
-__global__ void __launch_bounds__(kResidNT, DBX_SEP_MINB) rows_resid_sep(SpecArgs a) {
+__global__ void __launch_bounds__(kResidNT, 4) rows_resid_sep(SpecArgs a) {
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 sm[];
   __shared__ double red[32];
-  __shared__ unsigned long long mb[2];
-  const int n1 = a.n1, n2 = a.n2, q2 = a.q2, LS = resid_ls(n2), LSR = resid_lsr(n2, q2);
+  __shared__ unsigned long long mb[1];
+  const int n1 = a.n1, n2 = a.n2, q2 = a.q2, LSR = resid_lsr(n2, q2);
   const size_t N = (size_t)n1 * n2;
   const int r0 = 4 * blockIdx.x, nl = n1 - r0 < 4 ? n1 - r0 : 4;
-  double* yS = reinterpret_cast<double*>(sm);  // A x rows
-  double* rS = yS + 4 * LS;                    // g rows at offset 16, then r in place + extension
+  double* rS = reinterpret_cast<double*>(sm);  // g rows at offset 16, then r in place + extension
   const bool have_y = a.in != nullptr;
-  bulk_init(mb, 2);
+  bulk_init(mb, 1);
   const bool bg = stage_lines_bulk(rS + 16, LSR, a.g + (size_t)b * N + (size_t)r0 * n2, nl, n2, mb);
   cp_async_commit();
-  bool by = false;
-  if (have_y) by = stage_lines_bulk(yS, LS, a.in + (size_t)b * N + (size_t)r0 * n2, nl, n2, mb + 1);
-  cp_async_commit();
+  // A x rows into registers while g lands (8 per thread at n2 = 1024)
+  constexpr int YR = 8;
+  const double* yg = have_y ? a.in + (size_t)b * N + (size_t)r0 * n2 : nullptr;
+  const int tot = nl * n2;
+  double yv[YR];
+#pragma unroll
+  for (int k = 0; k < YR; ++k) {
+    const int e = threadIdx.x + k * kResidNT;
+    yv[k] = have_y && e < tot ? __ldcs(yg + e) : 0.0;
+  }
   cp_async_wait_all();
   __syncthreads();
   stage_lines_wait(bg, mb, nl);
-  if (have_y) stage_lines_wait(by, mb + 1, nl);
   double p0 = 0.0;
-  for (int h = 0; h < nl; ++h) {
-    const double* yr = yS + h * LS;
-    double* rr = rS + h * LSR + 16;
-    for (int c = threadIdx.x; c < n2; c += kResidNT) {
-      const double rv = have_y ? rr[c] - yr[c] : rr[c];
+#pragma unroll
+  for (int k = 0; k < YR; ++k) {
+    const int e = threadIdx.x + k * kResidNT;
+    if (e < tot) {
+      const int h = e / n2, c = e - h * n2;
+      double* rr = rS + h * LSR + 16;
+      const double rv = rr[c] - yv[k];
       rr[c] = rv;
       p0 += rv * rv;
     }
+  }
+  for (int e = threadIdx.x + YR * kResidNT; e < tot; e += kResidNT) {
+    const int h = e / n2, c = e - h * n2;
+    double* rr = rS + h * LSR + 16;
+    const double rv = have_y ? rr[c] - __ldcs(yg + e) : rr[c];
+    rr[c] = rv;
+    p0 += rv * rv;
   }
   __syncthreads();
   // horizontal AR extension of the r rows in place (boundary.hpp:56-62)
@@ -530,7 +547,7 @@ __global__ void __launch_bounds__(kResidNT, DBX_SEP_MINB) rows_resid_sep(SpecArg
     }
   }
   __syncthreads();
-  sep_row_pass(rS + 16 - q2, LSR, a.conv.sepr, q2, n2, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0, n1);
+  sep_row_pass(rS + 16 - q2, LSR, a.conv, q2, n2, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0, n1);
   if (a.part.p) {
     double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
     const double s0 = block_sum<kResidNT>(p0, red);

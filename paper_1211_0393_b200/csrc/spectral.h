@@ -28,6 +28,9 @@ struct ConvTables {
   const double2* sepb = nullptr;
   const double* sepr = nullptr;  // row taps b (2 q2 + 1): direct row pass of the separable fused pipeline
   const double* sepa_host = nullptr;  // host copy of sepa: cols_sep_real takes its taps as kernel parameters
+  // row taps b by value (q2 <= 15): part of the kernel parameter block, so the
+  // direct row passes' DFMAs read them from the constant bank, not registers
+  double sepr_v[31] = {};
 };
 
 // Bluestein DST-I tables for one line length n (device): M-point twiddles,

@@ -576,12 +576,9 @@ __device__ __forceinline__ void sep_extend_rows(const double* src, int LS, doubl
 }
 
 template <int Q>
-__device__ __forceinline__ void sep_row_stencil_T(const double* ext, int LSX, const double* __restrict__ w, int n2,
+__device__ __forceinline__ void sep_row_stencil_T(const double* ext, int LSX, const ConvTables& ct, int n2,
                                                   int nl, double* outT, int n1) {
   constexpr int R = 9, NTAP = 2 * Q + 1;
-  double tap[NTAP];
-#pragma unroll
-  for (int t = 0; t < NTAP; ++t) tap[t] = __ldg(w + t);
   const int h = threadIdx.x & 3;
   const int nblk = (n2 + R - 1) / R;
   for (int cb = threadIdx.x >> 2; cb < nblk; cb += blockDim.x >> 2) {
@@ -596,7 +593,7 @@ __device__ __forceinline__ void sep_row_stencil_T(const double* ext, int LSX, co
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int t = s - r;
-        if (t >= 0 && t < NTAP) acc[r] = fma(tap[t], z, acc[r]);
+        if (t >= 0 && t < NTAP) acc[r] = fma(ct.sepr_v[t], z, acc[r]);
       }
     }
     if (h < nl) {
@@ -608,10 +605,10 @@ __device__ __forceinline__ void sep_row_stencil_T(const double* ext, int LSX, co
 }
 
 // Q dispatch of the compiled separable row-tap counts (conv_sep_supported).
-__device__ __forceinline__ void sep_row_pass(const double* ext, int LSX, const double* w, int q2, int n2, int nl,
+__device__ __forceinline__ void sep_row_pass(const double* ext, int LSX, const ConvTables& ct, int q2, int n2, int nl,
                                              double* outT, int n1) {
-  if (q2 == 15) sep_row_stencil_T<15>(ext, LSX, w, n2, nl, outT, n1);
-  else if (q2 == 7) sep_row_stencil_T<7>(ext, LSX, w, n2, nl, outT, n1);
+  if (q2 == 15) sep_row_stencil_T<15>(ext, LSX, ct, n2, nl, outT, n1);
+  else if (q2 == 7) sep_row_stencil_T<7>(ext, LSX, ct, n2, nl, outT, n1);
 }
 
 template <typename K>
