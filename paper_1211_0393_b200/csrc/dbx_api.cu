@@ -356,6 +356,15 @@ struct dbx_plan {
     return N1 >= 2 && N2 >= 2 && dst_core(N1, &M) >= 0 && dst_core(N2, &M) >= 0;
   }
 
+  // direct separable blur in the separate passes (rank-1 mask, compiled tap
+  // counts; plain Landweber's AXPY epilogue keeps the FFT form).
+  // DBX_SEP_DIRECT=0 disables it (A/B and tests).
+  bool sep_direct(int mode) const {
+    static const bool off = [] { const char* e = getenv("DBX_SEP_DIRECT"); return e && e[0] == '0'; }();
+    return !off && sep_ok && conv != DBX_CONV_FFT_DENSE && mode != BLUR_AXPY && conv_sep_supported(q1) &&
+           rows_sep_supported(q2);
+  }
+
   // kernel spectrum of A (adjoint = false) or A' for the column pass, and the
   // separable tables when the mask is rank 1 (unless DBX_CONV_FFT_DENSE)
   void set_kernel(ConvTables& c, bool adjoint) const {
@@ -546,6 +555,23 @@ struct dbx_plan {
            const ImgState* stp, Partials pt, int cls) {
     if (use_fft_conv()) {
       ensure_conv();
+      if (sep_direct(mode)) {
+        // rank-1 mask: direct row pass + direct column pass (2 (2q+1) flops
+        // per pixel, no FFTs), residual / store fused into the column pass
+        SpecArgs a = spec_base(stp, pt);
+        set_kernel(a.conv, adjoint);
+        a.zbuf = reinterpret_cast<double2*>(zb.p);
+        a.in = x; a.insel = xsel;
+        a.out = y; a.outsel = ysel;
+        a.g = gg;
+        ev_begin(cls);
+        lc(launch_rows_sep_seg(a, stream), "rows_sep_seg");
+        const int ctas = lc(launch_cols_sep_epi(a, mode == BLUR_RESID ? 1 : 0, stream), "cols_sep_real");
+        ev_end();
+        launches += 2;
+        check_launch();
+        return ctas;
+      }
       SpecArgs a = spec_base(stp, pt);
       a.conv.tw1 = reinterpret_cast<const double2*>(tw1);
       a.conv.tw2 = reinterpret_cast<const double2*>(tw2);

@@ -439,7 +439,10 @@ struct ColTaps {
 
 __host__ __device__ constexpr int col_minb(int band) { return band <= 128 ? 4 : band <= 192 ? 3 : 2; }
 
-template <int Q, int BAND>
+// MODE 0: Y -> a.ybuf (separable fused pipeline); MODE 1: Y -> a.out
+// (BLUR_STORE); MODE 2: r = g - Y -> a.out with ||r||^2 partials (BLUR_RESID)
+// — the separate-pass path's direct separable blur (rows_sep_seg + this).
+template <int Q, int BAND, int MODE>
 __global__ void __launch_bounds__(kColNT, col_minb(BAND)) cols_sep_real(SpecArgs a, const ColTaps<2 * Q + 1> tp) {
   constexpr int NTAP = 2 * Q + 1, NL = BAND + 2 * Q, RT = kColRT;
   const int b = blockIdx.y;
@@ -483,7 +486,11 @@ __global__ void __launch_bounds__(kColNT, col_minb(BAND)) cols_sep_real(SpecArgs
       if (c0 + c >= n2) smd[l * kColLD + c] = 0.0;
     }
   __syncthreads();
-  double* Y = reinterpret_cast<double*>(a.ybuf) + (size_t)b * N + (size_t)p0 * n2 + c0 + lane;
+  double* Y = (MODE == 0 ? reinterpret_cast<double*>(a.ybuf) + (size_t)b * N
+                          : const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N))) +
+              (size_t)p0 * n2 + c0 + lane;
+  const double* G = MODE == 2 ? a.g + (size_t)b * N + (size_t)p0 * n2 + c0 + lane : nullptr;
+  double p2 = 0.0;
   const bool colok = c0 + lane < n2;
   for (int i0 = w * RT; i0 < rows; i0 += (kColNT / 32) * RT) {
     const double* col = smd + i0 * kColLD + lane;
@@ -502,9 +509,70 @@ __global__ void __launch_bounds__(kColNT, col_minb(BAND)) cols_sep_real(SpecArgs
     if (colok) {
 #pragma unroll
       for (int r = 0; r < RT; ++r)
-        if (i0 + r < rows) Y[(size_t)(i0 + r) * n2] = acc[r];
+        if (i0 + r < rows) {
+          if constexpr (MODE == 2) {
+            const double rv = __ldcs(G + (size_t)(i0 + r) * n2) - acc[r];
+            Y[(size_t)(i0 + r) * n2] = rv;
+            p2 += rv * rv;
+          } else {
+            Y[(size_t)(i0 + r) * n2] = acc[r];
+          }
+        }
     }
   }
+  if constexpr (MODE == 2) {
+    __shared__ double red[32];
+    const double s2 = block_sum<kColNT>(p2, red);
+    if (a.part.p && threadIdx.x == 0)
+      a.part.p[(size_t)b * NUM_SLOTS * a.part.cap + SLOT_R2 * a.part.cap + blockIdx.z * gridDim.x + blockIdx.x] = s2;
+  } else {
+    (void)p2;
+    (void)G;
+  }
+}
+
+// Row pass of the separate-pass direct separable blur (any n2): FOUR rows x a
+// segment of kRowSeg columns per CTA.  The segment and its 2 q2 halo columns
+// are staged (halo columns past the image from the AR / reflective extension,
+// boundary.hpp:56-64, read straight from global), then correlated with the
+// row taps (sep_row_stencil_T) into Z^T ([c][row]) for cols_sep_real.
+constexpr int kRowSeg = 1024, kRowNT = 256;
+__host__ __device__ constexpr int rowseg_ls(int q2) {
+  const int e = kRowSeg + 2 * q2 + 8;
+  return e + ((4 - e % 16) + 16) % 16;  // stride = 4 mod 16 (sep_row_stencil_T bank pattern)
+}
+
+template <int Q>
+__global__ void __launch_bounds__(kRowNT, 4) rows_sep_seg(SpecArgs a) {
+  const int b = blockIdx.z;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double smd[];
+  const int n1 = a.n1, n2 = a.n2, LSX = rowseg_ls(Q);
+  const size_t N = (size_t)n1 * n2;
+  const int c0 = blockIdx.x * kRowSeg, r0 = blockIdx.y * 4;
+  const int nl = min(4, n1 - r0), nc = min(kRowSeg, n2 - c0), W = nc + 2 * Q;
+  const double* X = resolve_ptr(a.in, a.st, a.insel, b, a.batch, N);
+  for (int h = 0; h < 4; ++h) {
+    const double* xr = X + (size_t)(r0 + h) * n2;
+    for (int j = threadIdx.x; j < W; j += kRowNT) {
+      const int c = c0 + j - Q;
+      double v = 0.0;
+      if (h < nl) {
+        if (c >= 0 && c < n2) {
+          v = __ldcs(xr + c);
+        } else if (a.bc == DBX_BC_REFLECTIVE) {
+          v = xr[c < 0 ? -c - 1 : 2 * n2 - 1 - c];
+        } else {
+          const int e = c < 0 ? 0 : n2 - 1, ri = c < 0 ? -c : 2 * (n2 - 1) - c;
+          v = 2.0 * xr[e] - xr[ri];
+        }
+      }
+      smd[h * LSX + j] = v;
+    }
+  }
+  __syncthreads();
+  sep_row_pass(smd, LSX, a.conv, Q, nc, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + (size_t)c0 * n1 + r0,
+               n1);
 }
 
 }  // namespace
@@ -551,16 +619,16 @@ bool conv_sep_supported(int q1) {
   return false;
 }
 
-template <int Q, int BAND>
+template <int Q, int BAND, int MODE>
 int launch_cols_sep_real_t(const SpecArgs& a, cudaStream_t s) {
   ColTaps<2 * Q + 1> tp;
   if (!a.conv.sepa_host) return -1;
   for (int t = 0; t < 2 * Q + 1; ++t) tp.t[t] = a.conv.sepa_host[t];
   const size_t sm = (size_t)(BAND + 2 * Q) * kColLD * 8;
-  if (!set_smem(cols_sep_real<Q, BAND>, sm)) return -1;
+  if (!set_smem(cols_sep_real<Q, BAND, MODE>, sm)) return -1;
   dim3 grid((a.n2 + kColW - 1) / kColW, a.batch, (a.n1 + BAND - 1) / BAND);
-  cols_sep_real<Q, BAND><<<grid, kColNT, sm, s>>>(a, tp);
-  return (int)grid.x;
+  cols_sep_real<Q, BAND, MODE><<<grid, kColNT, sm, s>>>(a, tp);
+  return MODE == 2 ? (int)(grid.x * grid.z) : (int)grid.x;
 }
 
 // row band per CTA: 256 (2 CTAs / SM) or 128 (4 CTAs / SM); DBX_COL_BAND overrides
@@ -576,10 +644,30 @@ static int col_band() {
 int launch_cols_sep_real(const SpecArgs& a, cudaStream_t s) {
 #define X(Q)                                                                             \
   if (a.q1 == (Q))                                                                       \
-    return col_band() == 256 ? launch_cols_sep_real_t<Q, 256>(a, s) : launch_cols_sep_real_t<Q, 128>(a, s);
+    return col_band() == 256 ? launch_cols_sep_real_t<Q, 256, 0>(a, s) : launch_cols_sep_real_t<Q, 128, 0>(a, s);
   DBX_SEP_LIST(X)
 #undef X
   return -1;
+}
+
+int launch_cols_sep_epi(const SpecArgs& a, int resid, cudaStream_t s) {
+#define X(Q)                                                                             \
+  if (a.q1 == (Q))                                                                       \
+    return resid ? launch_cols_sep_real_t<Q, 128, 2>(a, s) : launch_cols_sep_real_t<Q, 128, 1>(a, s);
+  DBX_SEP_LIST(X)
+#undef X
+  return -1;
+}
+
+bool rows_sep_supported(int q2) { return q2 == 7 || q2 == 15; }
+
+int launch_rows_sep_seg(const SpecArgs& a, cudaStream_t s) {
+  dim3 grid((a.n2 + kRowSeg - 1) / kRowSeg, (a.n1 + 3) / 4, a.batch);
+  const size_t sm = (size_t)4 * rowseg_ls(a.q2) * 8;
+  if (a.q2 == 15) rows_sep_seg<15><<<grid, kRowNT, sm, s>>>(a);
+  else if (a.q2 == 7) rows_sep_seg<7><<<grid, kRowNT, sm, s>>>(a);
+  else return -1;
+  return (int)(grid.x * grid.y);
 }
 
 int launch_conv_col(const SpecArgs& a, cudaStream_t s) {

@@ -112,6 +112,11 @@ enum FusedKind {
 bool fused_supported(int L2, int M, bool bluestein);
 bool fused_sep_supported(int L2, int M, bool bluestein, int n2, int q2);
 int launch_cols_sep_real(const SpecArgs& a, cudaStream_t s);  // real column pass of the separable pipeline
+// separate-pass direct separable blur: row pass (any n2) -> Z^T, then the
+// column pass with a store (resid = 0) or residual r = g - Y (resid = 1) epilogue
+bool rows_sep_supported(int q2);
+int launch_rows_sep_seg(const SpecArgs& a, cudaStream_t s);
+int launch_cols_sep_epi(const SpecArgs& a, int resid, cudaStream_t s);
 int launch_fused(int which, const SpecArgs& a, cudaStream_t s);
 #ifdef DBX_PHASES
 int fused_debug_phases(unsigned long long* out, int n);  // read + reset (instrumented builds)

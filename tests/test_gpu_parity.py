@@ -57,12 +57,17 @@ def sep_psf(rng, q1, q2):
 
 @pytest.mark.parametrize("n1,n2,q1,q2,bc", [(64, 64, 7, 7, "ar"), (96, 130, 15, 4, "ar"), (200, 77, 7, 12, "ar"),
                                             (1024, 1024, 15, 15, "ar"), (61, 90, 15, 15, "reflective"),
-                                            (40, 33, 7, 0, "ar")])
+                                            (40, 33, 7, 0, "ar"), (40, 2100, 7, 15, "ar"),
+                                            (33, 1030, 15, 7, "ar"), (35, 1031, 15, 15, "reflective")])
 def test_separable_column_pass_matches_oracle(dev, oracle, n1, n2, q1, q2, bc):
-    """Rank-1 masks run the separable column pass (conv_col_sep: direct
-    2 q1 + 1 tap correlation of the extended column x one complex scale per
-    column) inside the FFT engine; A and A' match the oracle's full-mask
-    correlation like the dense kernel spectrum does."""
+    """Rank-1 masks with q1, q2 in {7, 15} run the direct separable blur
+    (rows_sep_seg: 1024-column row segments with their extension halo, then
+    cols_sep_real); other rank-1 masks run the separable column pass inside
+    the FFT engine (conv_col_sep: direct 2 q1 + 1 tap correlation of the
+    extended column x one complex scale per column).  n2 = 2100 / 1030 / 1031
+    span several row segments, the last shorter than q2 (its extension reads
+    the previous segment).  A and A' match the oracle's full-mask correlation
+    like the dense kernel spectrum does."""
     rng = np.random.default_rng(n1 * 7 + n2 * 3 + q1 + q2)
     t = sep_psf(rng, q1, q2)
     f = rng.uniform(0, 1, (n1, n2))
