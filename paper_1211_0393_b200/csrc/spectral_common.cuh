@@ -22,6 +22,9 @@ namespace {
 // threads per FFT line: conv lines get one radix-8 butterfly per thread, DST
 // lines (power-of-two M) two; both capped at 256 so a CTA of <= 512 threads
 // keeps >= 128 registers per thread for the in-register radix stages.
+#ifndef DBX_BIG_LINE_T
+#define DBX_BIG_LINE_T 512
+#endif
 __host__ __device__ constexpr int line_threads(int L, int per) {
   if (L & 1) {
     // direct odd length: the first (largest-prime) stage runs packed across
@@ -33,7 +36,10 @@ __host__ __device__ constexpr int line_threads(int L, int per) {
     return t < 32 ? 32 : (t > 256 ? 256 : t);
   }
   int t = (L / per + 31) / 32 * 32;
-  return t < 32 ? 32 : (t > 256 ? 256 : t);
+  // one line per CTA at L >= 8000 (C5: 8190 / 8192 / 8640): a wider line keeps
+  // more warps resident on the SM
+  const int cap = L >= 8000 ? DBX_BIG_LINE_T : 256;
+  return t < 32 ? 32 : (t > cap ? cap : t);
 }
 // lines (rows / columns / row pairs) per CTA for a line length L
 __host__ __device__ constexpr int lines_for(int L, int budget_bytes, int per) {
