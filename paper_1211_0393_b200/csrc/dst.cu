@@ -72,11 +72,30 @@ __device__ __forceinline__ void pkc_fill(double2* buf, const BlueTables& bt, int
     if constexpr (CORE == CORE_BLUE)
       for (int p = N + t; p < M; p += T) buf[pad<M>(p)] = make_double2(0.0, 0.0);
   }
-  for (int j = 1 + t; j <= H; j += T) {
-    const double s = __ldg(bt.sn + j);
-    const double2 A = sd(0, j), B = sd(1, j);
-    put(j, make_double2(fma(s, A.x, 0.5 * A.y), fma(s, B.x, 0.5 * B.y)));
-    if (N - j != j) put(N - j, make_double2(fma(s, A.x, -0.5 * A.y), fma(s, B.x, -0.5 * B.y)));
+  // U positions per thread in flight: every global load of a group is issued
+  // before the first shared-memory store (the loads cannot move above the
+  // stores on their own: generic pointers may alias)
+  constexpr int U = 4;
+  for (int j0 = 1 + t; j0 <= H; j0 += U * T) {
+    double s[U];
+    double2 A[U], B[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * T;
+      if (j <= H) {
+        s[u] = __ldg(bt.sn + j);
+        A[u] = sd(0, j);
+        B[u] = sd(1, j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * T;
+      if (j <= H) {
+        put(j, make_double2(fma(s[u], A[u].x, 0.5 * A[u].y), fma(s[u], B[u].x, 0.5 * B[u].y)));
+        if (N - j != j) put(N - j, make_double2(fma(s[u], A[u].x, -0.5 * A[u].y), fma(s[u], B[u].x, -0.5 * B[u].y)));
+      }
+    }
   }
 }
 
@@ -95,7 +114,16 @@ __device__ __forceinline__ void pkc_core(double2* sm, double2* buf, const BlueTa
       if constexpr (CORE == CORE_RADER) {
         if (t == 0) A0s[g] = buf[pad<M>(0)];  // X_0 = sum of a (z_0 = 0)
       }
-      for (int p = t; p < M; p += T) buf[pad<M>(p)] = cmul(buf[pad<M>(p)], __ldg(bt.bhat + p));
+      constexpr int U = 4;  // kernel-spectrum loads in flight per thread
+      for (int p0 = t; p0 < M; p0 += U * T) {
+        double2 h[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (p0 + u * T < M) h[u] = __ldg(bt.bhat + p0 + u * T);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (p0 + u * T < M) buf[pad<M>(p0 + u * T)] = cmul(buf[pad<M>(p0 + u * T)], h[u]);
+      }
       fft::line_sync(bar, T);
       fft::fft<M, +1, T>(buf, tw, t, bar);
     }
@@ -143,12 +171,37 @@ __device__ __forceinline__ void pkc_split(double2* buf, const BlueTables& bt, in
 }
 
 // Odd-output scans of the CTA's 2G output lines (every thread calls it).
+// With at least two warps per output line (the one-line CTAs of the long
+// lengths: 16 warps, 2 lines) each line's scan is split into contiguous
+// warp chunks (odd_scan_range) plus a prefix of the chunk totals, instead of
+// one warp per line while the others wait at the barrier.
 template <int G, int LINE, int LO>
 __device__ __forceinline__ void pkc_scans(double2* sm, const BlueTables& bt) {
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int s = w; s < 2 * G; s += nw)
-    odd_scan(reinterpret_cast<double*>(sm + (s >> 1) * LINE) + (s & 1) * LO, bt.N / 2, bt.scale, lane);
+  constexpr int NLN = 2 * G;
+  if (nw >= 2 * NLN) {
+    __shared__ double tot[32];
+    const int wpl = nw / NLN < 32 / NLN ? nw / NLN : 32 / NLN;  // warps per line
+    const int s = w / wpl, wi = w - s * wpl, cnt = bt.N / 2;
+    const int chunk = ((cnt + wpl - 1) / wpl + 31) / 32 * 32;
+    const int lo = wi * chunk, hi = lo + chunk < cnt ? lo + chunk : cnt;
+    double* o = reinterpret_cast<double*>(sm + (s >> 1) * LINE) + (s & 1) * LO;
+    if (s < NLN) {
+      const double tt = odd_scan_range(o, lo, hi, lane);
+      if (lane == 0) tot[w] = tt;
+    }
+    __syncthreads();
+    if (s < NLN) {
+      double pre = 0.0;
+      for (int i = 0; i < wi; ++i) pre += tot[s * wpl + i];
+      const double sc = bt.scale;
+      for (int m = lo + lane; m < hi; m += 32) o[2 * m + 1] = (o[2 * m + 1] + pre) * sc;
+    }
+  } else {
+    for (int s = w; s < NLN; s += nw)
+      odd_scan(reinterpret_cast<double*>(sm + (s >> 1) * LINE) + (s & 1) * LO, bt.N / 2, bt.scale, lane);
+  }
   __syncthreads();
 }
 

@@ -362,6 +362,37 @@ __device__ __forceinline__ void odd_scan(double* o, int cnt, double sc, int lane
   }
 }
 
+// One warp: unscaled inclusive prefix sums of o[2m + 1], m in [lo, hi), in
+// place; returns the range total (every lane).
+__device__ __forceinline__ double odd_scan_range(double* o, int lo, int hi, int lane) {
+  double carry = 0.0;
+  constexpr int RW = 8;
+  for (int base = lo; base < hi; base += RW * 32) {
+    double v[RW];
+#pragma unroll
+    for (int i = 0; i < RW; ++i) {
+      const int m = base + i * 32 + lane;
+      v[i] = m < hi ? o[2 * m + 1] : 0.0;
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+      for (int i = 0; i < RW; ++i) {
+        const double y = __shfl_up_sync(0xffffffffu, v[i], d);
+        if (lane >= d) v[i] += y;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RW; ++i) {
+      const double tot = __shfl_sync(0xffffffffu, v[i], 31);
+      const int m = base + i * 32 + lane;
+      if (m < hi) o[2 * m + 1] = v[i] + carry;
+      carry += tot;
+    }
+  }
+  return carry;
+}
+
 // Scans of `nlines` output lines of stride LS (doubles), spread over the warps.
 __device__ __forceinline__ void odd_scans(double* o, int LS, int nlines, const BlueTables& bt) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
