@@ -39,6 +39,9 @@ __host__ __device__ constexpr int fused_td(int M) {
   return (FUSED_TD_ODD > 0 && (M & 1) && M > 512) ? FUSED_TD_ODD : line_threads(M, fused_dst_per(M));
 }
 
+#ifndef DBX_TT_MINB
+#define DBX_TT_MINB 3
+#endif
 template <int L2, int M, bool BLUE>
 struct Fused {
   static constexpr int TD = fused_td(M);   // threads per line
@@ -62,6 +65,10 @@ struct Fused {
   static constexpr size_t tt_twc = tt_twd + (TT_TWD ? TWD : 0);
   static constexpr bool TT_TWC = tt_twc + TWC <= kBudget;
   static constexpr size_t tt_bytes = tt_twc + (TT_TWC ? TWC : 0);
+  // separable rows_ainv_tt: no conv FFT, so no conv twiddles; DBX_TT_MINB = 3
+  // also leaves the DST twiddles in global memory (L1) so three CTAs fit
+  static constexpr bool TTS_TWD = DBX_TT_MINB < 3 && TT_TWD;
+  static constexpr size_t tts_bytes = tt_twd + (TTS_TWD ? TWD : 0);
   // rows_t_axpy_afwd: v rows (then T output), x rows, twiddles if they fit
   // x rows of rows_t_axpy: stride LS, or (separable variant) LSXR with the
   // data at offset 16 and room for the in-place AR extension (q2 <= 15)
@@ -146,7 +153,7 @@ __device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, 
 // spectra of rows 2g, 2g+1; DST line g then carries T~ of the same two rows
 // (packed real DST).  u is written transposed (u^T[k][row], 32-byte sectors).
 template <int L2, int M, bool BLUE, bool SEP = false>
-__global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecArgs a) {
+__global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, SEP ? DBX_TT_MINB : 2) rows_ainv_tt(SpecArgs a) {
   using F = Fused<L2, M, BLUE>;
   constexpr int NT = F::NT, TD = F::TD, LS = F::LSO, LMAX = F::LMAX;
   const int b = blockIdx.y;
@@ -156,7 +163,8 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_ainv_tt(SpecAr
   char* base = reinterpret_cast<char*>(sm);
   double* rowS = reinterpret_cast<double*>(base + F::off_rows);  // 4 rows: s, then T~ output
   const BlueTables& bt = a.blue2;
-  const double2* twd = stage_twiddles<M, F::TT_TWD>(reinterpret_cast<double2*>(base + F::tt_twd), bt.tw);
+  const double2* twd =
+      stage_twiddles<M, SEP ? F::TTS_TWD : F::TT_TWD>(reinterpret_cast<double2*>(base + F::tt_twd), bt.tw);
   const double2* twc =
       stage_twiddles<L2, F::TT_TWC && !SEP>(reinterpret_cast<double2*>(base + F::tt_twc), a.conv.tw2);
   const int n1 = a.n1, n2 = a.n2, Lh = a.conv.Lh;
@@ -674,8 +682,8 @@ template <int L2, int M, bool BLUE, int WHICH, typename K>
 int fused_launch(K kernel, const SpecArgs& a, cudaStream_t s) {
   using F = Fused<L2, M, BLUE>;
   // WHICH: 0 tt, 1 t_axpy, 2 resid, 4 tt (separable), 5 t_axpy (separable)
-  constexpr size_t bytes = (WHICH == 0 || WHICH == 4) ? F::tt_bytes : (WHICH == 1 || WHICH == 5) ? F::ax_bytes
-                                                                                                   : RsCfg<L2>::bytes;
+  constexpr size_t bytes = WHICH == 0 ? F::tt_bytes : WHICH == 4 ? F::tts_bytes
+                           : (WHICH == 1 || WHICH == 5) ? F::ax_bytes : RsCfg<L2>::bytes;
   constexpr int nt = WHICH == 2 ? RsCfg<L2>::NT : F::NT;
   constexpr int rows = 4;  // rows per CTA
   static bool init = false;
