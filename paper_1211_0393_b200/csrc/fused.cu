@@ -42,6 +42,9 @@ __host__ __device__ constexpr int fused_td(int M) {
 #ifndef DBX_TT_MINB
 #define DBX_TT_MINB 3
 #endif
+#ifndef DBX_TC_MINB
+#define DBX_TC_MINB 2
+#endif
 template <int L2, int M, bool BLUE>
 struct Fused {
   static constexpr int TD = fused_td(M);   // threads per line
@@ -576,14 +579,18 @@ struct TcolSmem {
   static constexpr int LSO = ((LMAX > PkOut<LMAX>::OL ? LMAX : PkOut<LMAX>::OL) + 1) / 2 * 2 + 4;  // io lines
   static constexpr size_t off_io = (size_t)2 * padded_len(M) * 16;
   static constexpr size_t off_d = off_io + (size_t)4 * LSO * 8;
-  static constexpr size_t off_tw = off_d + (size_t)4 * LS * 8;
+  // DL (DBX_TC_MINB >= 3): d^T is not staged — it multiplies the T~ outputs in
+  // place straight from global (L2-resident, shared by the batch) — and the
+  // twiddles are read through L1, so three CTAs fit per SM
+  static constexpr bool DL = DBX_TC_MINB >= 3;
+  static constexpr size_t off_tw = off_d + (DL ? 0 : (size_t)4 * LS * 8);
   static constexpr size_t TWB = (size_t)fft::twiddles_needed(M) * 16;
-  static constexpr bool TW = off_tw + TWB <= 115200;  // keep 2 CTAs / SM
+  static constexpr bool TW = !DL && off_tw + TWB <= 115200;  // keep 2 CTAs / SM
   static constexpr size_t bytes = TW ? off_tw + TWB : off_tw;
 };
 
 template <int M, bool BLUE>
-__global__ void __launch_bounds__(2 * fused_td(M), 2) dst_tcols(SpecArgs a) {
+__global__ void __launch_bounds__(2 * fused_td(M), DBX_TC_MINB) dst_tcols(SpecArgs a) {
   using S = TcolSmem<M, BLUE>;
   constexpr int TD = S::TD, NT = 2 * TD, LS = S::LS, LSO = S::LSO, LMAX = S::LMAX;
   const int b = blockIdx.y;
@@ -604,7 +611,8 @@ __global__ void __launch_bounds__(2 * fused_td(M), 2) dst_tcols(SpecArgs a) {
   bulk_init(mb, 2);
   const bool bi = stage_lines_bulk(io, LSO, a.in + (size_t)b * N + (size_t)c0 * n, nl, n, mb);  // u^T lines
   cp_async_commit();
-  const bool bd = stage_lines_bulk(dS, LS, a.dT + (size_t)b * a.dstride + (size_t)c0 * n, nl, n, mb + 1);  // d^T
+  const double* dg = a.dT + (size_t)b * a.dstride + (size_t)c0 * n;
+  const bool bd = S::DL ? false : stage_lines_bulk(dS, LS, dg, nl, n, mb + 1);  // d^T
   cp_async_commit();
   cp_async_wait_group<1>();
   __syncthreads();
@@ -640,14 +648,46 @@ __global__ void __launch_bounds__(2 * fused_td(M), 2) dst_tcols(SpecArgs a) {
   cp_async_wait_all();
   if (bd && nl > 0) mbar_wait(mb + 1, 0);
   __syncthreads();
+  __shared__ double dd0[4], dd1[4];
+  if constexpr (S::DL) {
+    // u o d in place on the T~ outputs (pk_at layout), d^T from global,
+    // four loads in flight per thread
+    using P = PkOut<LMAX>;
+    constexpr int U = 4;
+    for (int e0i = threadIdx.x; e0i < nl * n; e0i += U * NT) {
+      double dv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0i + u * NT;
+        dv[u] = e < nl * n ? __ldg(dg + (e / n) * n + (e - (e / n) * n)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0i + u * NT;
+        if (e < nl * n) {
+          const int h = e / n, k = e - h * n, m = k >> 1;
+          double* o = io + h * LSO + ((k & 1) ? P::EB + (m & 15) * P::STR1 + (m >> 4) : m);
+          *o *= dv[u];
+          if (k == 0) dd0[h] = dv[u];
+          if (k == n - 1) dd1[h] = dv[u];
+        }
+      }
+    }
+    __syncthreads();
+  }
   PH(4)
   // v = u o d (u_0 = alpha v_0, u_{n-1} = alpha v_{n-1}), then T (ar_forward)
   pk_fill<M, TD, BLUE>(buf, bt, t, [&](int hh, int j) {
     const int h = 2 * g + hh;
     if (h >= nl) return make_double2(0.0, 0.0);
     const double* o = io + h * LSO;
-    const double mj = pk_at<LMAX>(o, j) * dS[h * LS + j], mm = pk_at<LMAX>(o, NL - j) * dS[h * LS + NL - j];
-    return make_double2(mj + mm, mj - mm);
+    if constexpr (S::DL) {
+      const double mj = pk_at<LMAX>(o, j), mm = pk_at<LMAX>(o, NL - j);
+      return make_double2(mj + mm, mj - mm);
+    } else {
+      const double mj = pk_at<LMAX>(o, j) * dS[h * LS + j], mm = pk_at<LMAX>(o, NL - j) * dS[h * LS + NL - j];
+      return make_double2(mj + mm, mj - mm);
+    }
   });
   PH(5)
   blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
@@ -665,7 +705,7 @@ __global__ void __launch_bounds__(2 * fused_td(M), 2) dst_tcols(SpecArgs a) {
   if (h < nl) {
     double* s = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c0 + h;
     const double* o = io + h * LSO;
-    const double a0 = e0[h] * dS[h * LS], a1 = e1[h] * dS[h * LS + n - 1];
+    const double a0 = e0[h] * (S::DL ? dd0[h] : dS[h * LS]), a1 = e1[h] * (S::DL ? dd1[h] : dS[h * LS + n - 1]);
 #pragma unroll 4
     for (int k = threadIdx.x >> 2; k < n; k += NT / 4) {
       const double t1 = (double)k * ri;
