@@ -6,13 +6,15 @@ Workload (default): BASELINE config C3 — a batch of 64 FP64 1024x1024 images
 40 preconditioned (D-)Landweber iterations under anti-reflective BCs.  One
 "step" is one complete 40-iteration restoration of the rank's 64-image batch
 (histories, best-iterate tracking and all per-iteration norms included).
-Weak scaling: every rank restores its own 64-image batch (images
-rank*64 .. rank*64+63), no data-path collective.
+Multi-GPU: the fixed 64-image batch is sharded over the ranks
+(64/N contiguous images per GPU, 8 at N = 8; strong scaling, no data-path
+collective); --weak gives every rank its own 64 images instead.
 
   value  : device-resident inputs, CUDA events on the plan's stream, max over ranks
   e2e    : same solve through the public C-ABI with pinned HOST buffers, i.e.
            H2D of g and f_true + D2H of the restored images inside the timed region
-  roofline: dominant kernel class (per-launch CUDA events over the timed region)
+  roofline: the dominant kernel (per-launch CUDA events of one extra eager
+           step), with every kernel of the iteration listed in roofline.kernels
   cpu_baseline: the CPU oracle port (oracle/), rank 0 at N=1, bounded sample
 
 `--impl reference` times the reference algorithm's CPU restatement (the oracle
@@ -39,7 +41,7 @@ METRIC = "Mpixel-iterations/s of preconditioned AR-BC iteration"
 UNIT = "Mpixel-iterations/s"
 PEAKS_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
 HBM_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
 E2E_CHUNKS = int(os.environ.get("DBX_E2E_CHUNKS", "4"))  # with 2 in flight: measured best (r1s2bb, r1s2cc)
 
 
@@ -68,6 +70,8 @@ def parse():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--images", type=int, default=0, help="override images per rank")
+    ap.add_argument("--weak", action="store_true",
+                    help="every rank restores its own full batch (default: the batch is sharded over the ranks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true",
@@ -158,6 +162,34 @@ def cpu_sample(cfg, threads: int, iters: int):
     return px_it / dt / 1e6, dt, sample
 
 
+def cpu_per_config(cf):
+    """1-core CPU oracle line for every BASELINE config, each
+    a bounded sample of that config's D-Landweber run (iterations timed
+    linearly extrapolate: the loop does the same work every iteration).  C5
+    (8192^2) uses every host core (line-parallel oracle passes, results
+    bit-identical to one thread) so that the sample stays within seconds."""
+    from oracle import oracle as O
+    O.build()
+    out = {"unit": UNIT, "kind": "port", "note": "oracle port of the reference algorithm (FFT correlation for q>7, "
+                                                 "FFT DST-I); the reference's FFTW is unavailable"}
+    plan = {"C1": (10, 1), "C2": (5, 1), "C3": (2, 1), "C4": (1, 1), "C5": (1, os.cpu_count() or 1)}
+    for name, (iters, threads) in plan.items():
+        c = cf.CONFIGS[name]
+        f, g, taps = cf.make_problem(c)
+        d = O.build_tikhonov(taps, c.alpha, c.n, c.n)
+        O.set_threads(threads)
+        try:
+            t0 = time.perf_counter()
+            O.landweber(taps, g, d=d, f_true=f, max_iters=iters)
+            dt = time.perf_counter() - t0
+        finally:
+            O.set_threads(1)
+        out[name] = {"value": c.n * c.n * iters / dt / 1e6, "cores": threads,
+                     "sample": f"1 image x {iters} D-Landweber iteration(s) of {c.n}^2, q={c.q}", "seconds": round(dt, 2)}
+        del f, g, d
+    return out
+
+
 def other_configs(L, dbx, cf, torch, dev, local, reps=3):
     """Single-GPU graph-path throughput of the other BASELINE configs (the
     parity cases), same timing rules as the headline (warm-up, CUDA events on
@@ -212,12 +244,36 @@ def other_configs(L, dbx, cf, torch, dev, local, reps=3):
     return out
 
 
+def images_per_rank(cfg, args, world):
+    if args.images:
+        return args.images
+    if args.weak or cfg.batch % world:
+        return cfg.batch
+    return cfg.batch // world
+
+
+def workload_config(cfg, B, world, weak):
+    """The `config` object of both arms' JSON lines (identical by construction)."""
+    return {"workload": f"{cfg.name}: {B * world if not weak else cfg.batch} x {cfg.n}x{cfg.n} FP64 images"
+                        f"{' per GPU' if weak else ''}, q={cfg.q} mask, {cfg.iters} D-Landweber iterations, AR BCs, "
+                        f"alpha={cfg.alpha}",
+            "images_per_gpu": B, "global_images": B * world, "n": cfg.n, "q": cfg.q, "iters": cfg.iters,
+            "parallelism": f"batch-sharded x{world} (no data-path collective)",
+            "l2": f"inputs larger than L2 (each {B}x{cfg.n}^2 FP64 array = {B * cfg.n * cfg.n * 8 >> 20} MiB)"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    from oracle import oracle as O
     from paper_1211_0393_b200 import configs as cf
+    O.build()
+    # inputs through the oracle's own build of the generators: this CPU arm
+    # never maps the product library libdbx.so
+    cf.use_generator_library(O.gen_lib_path())
     cfg = cf.CONFIGS[args.config]
+    B = images_per_rank(cfg, args, world)
     threads = os.cpu_count() or 1
     vals = []
     for s in range(args.warmup + args.steps):
@@ -228,12 +284,13 @@ def run_reference(args):
     ms = float(np.median([x[1] for x in vals])) * 1e3
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, host-generated)",
-            "config": {"workload": f"{cfg.name} (bounded CPU sample)", "n": cfg.n, "q": cfg.q},
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, host-generated)",
+            "config": workload_config(cfg, B, world, args.weak),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": "reference (Eigen3/FFTW3 header library) is unbuildable here; timed its CPU restatement "
-                    "oracle/deblur_oracle.cpp (own FFT in place of FFTW), one image per host thread"}
+                    "oracle/deblur_oracle.cpp (own Stockham/Bluestein FFT in place of FFTW), one image per host "
+                    "thread, each step a bounded sample (1 iteration per image) of the same workload"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -324,7 +381,7 @@ def main():
     torch.cuda.set_device(local)
     L = dbx.lib()
     cfg = cf.CONFIGS[args.config]
-    B = args.images or cfg.batch
+    B = images_per_rank(cfg, args, world)
     n, q = cfg.n, cfg.q
     N = n * n
 
@@ -384,6 +441,12 @@ def main():
     L.dbx_plan_kernel_times(plan, ms, cnt, 8)
     kms_tot = np.array(ms[:4]) * args.steps
     kcnt_tot = np.array(cnt[:4]) * args.steps
+    kprof = {}
+    nm = C.create_string_buffer(128)
+    kms1, kc1 = C.c_double(), C.c_int()
+    for i in range(L.dbx_plan_kernel_profile(plan, -1, None, 0, None, None)):
+        L.dbx_plan_kernel_profile(plan, i, nm, 128, C.byref(kms1), C.byref(kc1))
+        kprof[nm.value.decode()] = (kms1.value, kc1.value)
     L.dbx_plan_set_timing(plan, 0)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     t_ms = float(np.sum(step_ms))
@@ -438,12 +501,10 @@ def main():
             L.dbx_plan_destroy(cp)
         del gh, fh, oh
 
-    # ---- roofline of the dominant kernel class ----
+    # ---- roofline of the dominant kernel (per-launch CUDA events of the
+    # eager step; every kernel of the iteration listed) ----
     from paper_1211_0393_b200 import workmodel as wm
     names = ["blur_adjoint(A')", "blur(A)+residual", "ar_transform_pass", "finalize"]
-    dom = int(np.argmax(kms_tot))
-    avg_ms = kms_tot[dom] / max(kcnt_tot[dom], 1)
-    avg_s = avg_ms * 1e-3
     peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
     if os.path.exists(HBM_FILE):
         hbm_peak, hsrc = float(json.load(open(HBM_FILE))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
@@ -452,50 +513,59 @@ def main():
     conv_e, dst_e, fz = C.c_int(), C.c_int(), C.c_int()
     L.dbx_plan_engines(plan, C.byref(conv_e), C.byref(dst_e))
     L.dbx_plan_pipeline(plan, C.byref(fz))
-    fft_conv, fft_dst, fused = conv_e.value == 2, dst_e.value == 2, fz.value >= 1
     separable = fz.value == 2
     p_fp64 = peaks.get("dfma_tflops_sustained", 34.0)
-    fsrc = "measured DFMA FP64 sustained (profiles/r01_fp64_peak.json)"
+    fsrc = "measured DFMA FP64 sustained (profiles/r01_fp64_peak.json, SM clock 1965 MHz)"
     step_s = t_max * 1e-3 / args.steps
-    roof = {"kernel": names[dom], "avg_launch_ms": avg_ms,
-            "share_of_step": float(kms_tot[dom] / max(kms_tot.sum(), 1e-9)),
-            "class_ms_per_step": {names[i]: float(kms_tot[i] / args.steps) for i in range(4)}}
-    if fused and dom < 3:
-        cls = (wm.fused_sep_classes if separable else wm.fused_classes)(n, q, B)[names[dom]]
-        flops, nbytes = cls["flops"] / cls["launches"], cls["bytes"] / cls["launches"]
-        t_hbm, t_fp = nbytes / (hbm_peak * 1e9), flops / (p_fp64 * 1e12)
-        gbs, tfs = nbytes / avg_s / 1e9, flops / avg_s / 1e12
-        traffic = None
-        if os.path.exists(TRAFFIC_FILE):
-            tr = json.load(open(TRAFFIC_FILE)).get("per_image_launch_bytes", {}).get(names[dom])
-            traffic = tr * B if tr else None
-        fp = {"achieved": tfs, "peak": p_fp64, "unit": "TFLOP/s", "frac": tfs / p_fp64, "peak_source": fsrc,
-              "algorithmic_flops_per_launch": flops}
-        hb = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak, "peak_source": hsrc,
-              "algorithmic_bytes_per_launch": nbytes}
-        main, other = (hb, fp) if t_hbm >= t_fp else (fp, hb)
-        roof.update({"bound": "hbm" if t_hbm >= t_fp else "tensor", **main, "traffic": traffic,
-                     "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per image, "
-                                       "profiles/r01_ncu_traffic.json, x images per launch",
-                     "form": ("fused separable pipeline (rank-1 mask: direct row/column correlation passes; "
-                              "packed real FFT-form DST-I)") if separable else
-                             "fused FFT-form pipeline (packed real DST-I, FFT correlation)",
-                     "secondary": other,
-                     "note": "nominal 5 N log2 N flops per FFT, 2(2q+1) per pixel per direct pass; arithmetic "
-                             "intensity below the FP64 ridge, so the HBM floor is the binding roofline"})
-    else:
-        per_launch_blur = (wm.conv_apply_flops(n, n, q, q) if fft_conv else wm.direct_apply_flops(n, n, q, q)) * B
-        if dom == 2:
-            launches_per_it = 3 if fft_dst else 4
-            flops = (wm.transform_iteration_flops(n, n, packed=False) if fft_dst else 8.0 * n * n * n) * B / launches_per_it
-            if not fft_dst:
-                p_fp64, fsrc = peaks.get("dmma_tflops_sustained", 37.0), "measured DMMA FP64 sustained (profiles/r01_fp64_peak.json)"
-        else:
-            flops = per_launch_blur
-        tfs = flops / avg_s / 1e12
-        roof.update({"bound": "tensor", "pipe": "FP64 (no tcgen05 FP64 kind on sm_100a; DFMA/DMMA)",
-                     "achieved": tfs, "peak": p_fp64, "unit": "TFLOP/s", "frac": tfs / p_fp64, "traffic": None,
-                     "peak_source": fsrc, "algorithmic_flops_per_launch": flops})
+    traffic_tab = {}
+    if os.path.exists(TRAFFIC_FILE):
+        tj = json.load(open(TRAFFIC_FILE))
+        if tj.get("images") == B:
+            traffic_tab = tj.get("per_launch_bytes", {})
+    kern = []
+    model = wm.fused_sep_kernels(n, q, B) if separable else {}
+    tot_ms = sum(v[0] for v in kprof.values()) or 1e-9
+    for name, (kms_, kc_) in sorted(kprof.items(), key=lambda kv: -kv[1][0]):
+        e = {"kernel": name, "ms_per_step": kms_, "launches_per_step": kc_, "share_of_step": kms_ / tot_ms,
+             "avg_launch_ms": kms_ / max(kc_, 1)}
+        if name in model:
+            avg_s = e["avg_launch_ms"] * 1e-3
+            e.update({"algorithmic_bytes_per_launch": model[name]["bytes"],
+                      "achieved_gbs": model[name]["bytes"] / avg_s / 1e9,
+                      "frac_hbm": model[name]["bytes"] / avg_s / 1e9 / hbm_peak,
+                      "algorithmic_flops_per_launch": model[name]["flops"],
+                      "achieved_tflops": model[name]["flops"] / avg_s / 1e12,
+                      "frac_fp64": model[name]["flops"] / avg_s / 1e12 / p_fp64,
+                      "traffic_per_launch": traffic_tab.get(name)})
+        kern.append(e)
+    dom = next((e for e in kern if "frac_hbm" in e), kern[0] if kern else None)
+    roof = {"kernel": dom["kernel"] if dom else None, "bound": "hbm", "peak": hbm_peak, "unit": "GB/s",
+            "peak_source": hsrc}
+    if dom and "frac_hbm" in dom:
+        t_hbm = dom["algorithmic_bytes_per_launch"] / (hbm_peak * 1e9)
+        t_fp = dom["algorithmic_flops_per_launch"] / (p_fp64 * 1e12)
+        roof.update({"avg_launch_ms": dom["avg_launch_ms"], "share_of_step": dom["share_of_step"],
+                     "achieved": dom["achieved_gbs"], "frac": dom["frac_hbm"],
+                     "algorithmic_bytes_per_launch": dom["algorithmic_bytes_per_launch"],
+                     "traffic": dom["traffic_per_launch"],
+                     "traffic_source": ("ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch at "
+                                        f"{B} images ({os.path.basename(TRAFFIC_FILE)})") if traffic_tab else None,
+                     "binding": "hbm" if t_hbm >= t_fp else "fp64 (below the FP64 ridge the HBM floor binds)",
+                     "secondary": {"achieved": dom["achieved_tflops"], "peak": p_fp64, "unit": "TFLOP/s",
+                                   "frac": dom["frac_fp64"], "peak_source": fsrc,
+                                   "algorithmic_flops_per_launch": dom["algorithmic_flops_per_launch"]},
+                     "form": "fused separable pipeline (rank-1 mask: direct row/column correlation passes; "
+                             "packed real FFT-form DST-I)",
+                     "note": "bytes: every array the kernel must read/write once (workmodel.fused_sep_kernels); "
+                             "flops: nominal 5 N log2 N per FFT, 2(2q+1) per pixel per direct pass"})
+    roof["kernels"] = kern
+    roof["class_ms_per_step"] = {names[i]: float(kms_tot[i] / args.steps) for i in range(4)}
+    if separable:
+        cls = wm.fused_sep_classes(n, q, B)["ar_transform_pass"]
+        avg_cls = kms_tot[2] / max(kcnt_tot[2], 1) * 1e-3
+        roof["class_aggregate"] = {"class": "ar_transform_pass (3 kernels)",
+                                   "achieved": cls["bytes"] / cls["launches"] / avg_cls / 1e9,
+                                   "frac": cls["bytes"] / cls["launches"] / avg_cls / 1e9 / hbm_peak}
     roof["dense_stencil_sol"] = wm.canonical(q, float(world * B * N * H) / world, step_s, hbm_peak, p_fp64)
 
     others = None
@@ -506,17 +576,15 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt, sample = cpu_sample(cfg, 1, 2)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
+        if args.config == "C3" and not args.images:
+            cpu["per_config"] = cpu_per_config(cf)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded scenes/masks/noise, host-generated; stands in for Cameraman/Bridge)",
-                "config": {"workload": f"{cfg.name}: {B} x {n}x{n} FP64 images per GPU, q={q} mask, "
-                                       f"{H} D-Landweber iterations, AR BCs, alpha={cfg.alpha}",
-                           "images_per_gpu": B, "global_images": B * world, "n": n, "q": q, "iters": H,
-                           "parallelism": f"batch-sharded x{world} (no data-path collective)",
-                           "l2": "inputs larger than L2 (each 64x1024^2 FP64 array = 512 MiB)"},
+                "config": workload_config(cfg, B, world, args.weak),
                 "clocks": clk, "gpu_launches": launches, "roofline": roof, "e2e": e2e, "cpu_baseline": cpu}
         if others:
             line["other_configs"] = {"unit": UNIT, "note": "single-GPU graph path, D-Landweber unless plain_*; "

@@ -282,6 +282,10 @@ int dbx_landweber_run_chunks(dbx_plan* const* plans, int nplans, const double* g
 int dbx_plan_set_timing(dbx_plan* plan, int enable);
 int dbx_plan_kernel_times(dbx_plan* plan, double* ms, int* launches, int max_classes);
 
+/* Per-kernel timing of the last timed run (dbx_plan_set_timing): entry idx's
+ * "kernel#class" name, total ms and launch count; returns the entry count. */
+int dbx_plan_kernel_profile(dbx_plan* plan, int idx, char* name, int name_cap, double* ms, int* launches);
+
 /* Total kernels launched by this plan since creation (launch accounting). */
 int64_t dbx_plan_launch_count(dbx_plan* plan);
 

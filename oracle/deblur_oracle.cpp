@@ -1,31 +1,46 @@
 // ============================================================================
 // oracle/deblur_oracle.cpp — CPU ORACLE (TEST INFRASTRUCTURE ONLY)
 //
-// This file is the parity checker for the B200 hot path.  It is a scalar,
-// single-threaded C++ restatement of the reference library `deblur`
+// This file is the parity checker for the B200 hot path.  It is a scalar C++
+// restatement of the reference library `deblur`
 // (/root/reference/proj/include/deblur/*.hpp) for the anti-reflective (AR)
-// preconditioned-Landweber path.  Only tests/, __graft_entry__.smoke() and the
-// cpu_baseline / --impl reference legs of bench.py may load it; the product
+// preconditioned-Landweber path (plus the Reflective/CosineIII comparison
+// branch).  Only tests/, __graft_entry__.smoke() and the cpu_baseline /
+// --impl reference legs of bench.py may load it; the product
 // (paper_1211_0393_b200/libdbx.so) never links or calls it.
 //
 // The reference itself cannot be compiled here or on the GPU box (Eigen3,
 // FFTW3 and GoogleTest are absent).  Its DST-I / DFT
 // arithmetic lives in FFTW3 (unpinned, un-vendored: transforms.hpp:3, 39-82);
 // this restatement computes the same unnormalised transforms with its own
-// FFT (mixed radix + Bluestein), so results agree with FFTW to rounding.
-// Parity pinning: the oracle is certified against the reference tests'
-// known-answer and dense-formula assertions (tests/test_oracle_*.py) and
-// against scipy.fft.dst(type=1) / committed golden fixtures at the BASELINE
-// DST lengths (tests/golden/).
+// FFT (iterative Stockham mixed radix 2/3/4/5 + generic odd primes <= 31,
+// Bluestein chirp-z over a power of two for any larger prime factor), so
+// results agree with FFTW to rounding.  Parity pinning: the oracle is
+// certified against the reference tests' known-answer and dense-formula
+// assertions (tests/test_oracle_pinning.py) and against scipy.fft.dst(type=1)
+// / committed golden fixtures at the BASELINE DST lengths (tests/golden/).
+//
+// Everything numeric is a template on the scalar type R:
+//   R = double       the oracle proper (what the GPU is compared with);
+//   R = long double  the same algorithm with a 64-bit mantissa, used only to
+//                    measure the FP64 rounding floor of BOTH the oracle and
+//                    the GPU path.
+//
+// Threads (orc_set_threads): the independent lines of every 2D pass (rows /
+// columns of the 2D DFTs, of tensor_map, of the direct correlation, the
+// spectrum grid) are split over worker threads.  Each line's arithmetic and
+// every reduction order are unchanged, so results are bit-identical for any
+// thread count (tests/test_oracle_pinning.py checks this).
 //
 // Every function cites the reference file:line it restates.  Matrices are
-// row-major double buffers (core.hpp:17-19: vec(X) is the buffer).
+// row-major buffers (core.hpp:17-19: vec(X) is the buffer).
 // ============================================================================
 #include <algorithm>
+#include <atomic>
 #include <cmath>
-#include <complex>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <map>
 #include <memory>
@@ -33,23 +48,57 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace orc {
 
-using cd = std::complex<double>;
 constexpr double kPi = 3.141592653589793238462643383279502884;  // core.hpp:15
 constexpr long double kPiL = 3.141592653589793238462643383279502884L;
 
+template <class R> constexpr R pi_v() { return R(kPiL); }
+template <> constexpr double pi_v<double>() { return kPi; }
+
 thread_local std::string g_err;
 
-struct Mat {
+// ---------------------------------------------------------------------------
+// Worker threads (deterministic line partition)
+// ---------------------------------------------------------------------------
+static std::atomic<int> g_threads{1};
+
+// f(lo, hi) over contiguous chunks of [0, n); serial when one thread.
+static void parallel_for(long n, const std::function<void(long, long)>& f) {
+  const int T = std::max(1, std::min<int>(g_threads.load(), (int)std::min<long>(n, 1L << 20)));
+  if (T <= 1 || n < 2) {
+    if (n > 0) f(0, n);
+    return;
+  }
+  std::vector<std::thread> ts;
+  std::vector<std::exception_ptr> errs((size_t)T);
+  const long chunk = (n + T - 1) / T;
+  for (int t = 0; t < T; ++t) {
+    const long lo = t * chunk, hi = std::min(n, lo + chunk);
+    if (lo >= hi) break;
+    ts.emplace_back([&, t, lo, hi] {
+      try {
+        f(lo, hi);
+      } catch (...) {
+        errs[(size_t)t] = std::current_exception();
+      }
+    });
+  }
+  for (auto& th : ts) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+template <class R> struct Mat {
   long n1 = 0, n2 = 0;
-  std::vector<double> a;
+  std::vector<R> a;
   Mat() = default;
-  Mat(long r, long c, double v = 0.0) : n1(r), n2(c), a(size_t(r * c), v) {}
-  double& operator()(long i, long j) { return a[size_t(i * n2 + j)]; }
-  double operator()(long i, long j) const { return a[size_t(i * n2 + j)]; }
+  Mat(long r, long c, R v = R(0)) : n1(r), n2(c), a(size_t(r * c), v) {}
+  R& operator()(long i, long j) { return a[size_t(i * n2 + j)]; }
+  R operator()(long i, long j) const { return a[size_t(i * n2 + j)]; }
 };
 
 // core.hpp:26-28
@@ -57,41 +106,48 @@ inline void require(bool c, const char* what) {
   if (!c) throw std::invalid_argument(what);
 }
 
-static double fro(const double* x, size_t n) {
-  double s = 0.0;
+// Frobenius norm, sequential summation (fixed order).
+template <class R> static R fro(const R* x, size_t n) {
+  R s = 0;
   for (size_t i = 0; i < n; ++i) s += x[i] * x[i];
   return std::sqrt(s);
 }
 
 // ---------------------------------------------------------------------------
-// Generic complex FFT (stands in for FFTW's fftw_plan_dft / r2r codelets,
+// Complex FFT (stands in for FFTW's fftw_plan_dft / r2r codelets,
 // transforms.hpp:39-82).  Unnormalised, sign = -1 forward.
 // ---------------------------------------------------------------------------
-struct FftPlan {
+template <class R> struct Cx {
+  R re, im;
+};
+template <class R> inline Cx<R> cmul(Cx<R> a, Cx<R> b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+template <class R> inline Cx<R> cadd(Cx<R> a, Cx<R> b) { return {a.re + b.re, a.im + b.im}; }
+template <class R> inline Cx<R> csub(Cx<R> a, Cx<R> b) { return {a.re - b.re, a.im - b.im}; }
+
+template <class R> struct FftPlan {
   int n = 0, sign = -1;
   bool blue = false;
-  std::vector<int> fac;
-  std::vector<cd> tw;  // tw[k] = exp(sign*2*pi*i*k/n), k in [0,n)
-  // Bluestein
+  std::vector<int> fac;       // Stockham radices, in stage order
+  std::vector<Cx<R>> tw;      // tw[k] = exp(sign*2*pi*i*k/n), k in [0,n)
+  // Bluestein (n has a prime factor > 31)
   int M = 0;
-  std::vector<cd> chirp;      // exp(sign*i*pi*k^2/n)
-  std::vector<cd> kern_hat;   // FFT_M of conj chirp, wrapped
-  std::shared_ptr<FftPlan> fM, iM;
+  std::vector<Cx<R>> chirp;     // exp(sign*i*pi*k^2/n), exact integer reduction of k^2 mod 2n
+  std::vector<Cx<R>> kern_hat;  // FFT_M of the wrapped conjugate chirp, pre-scaled by 1/M
+  std::shared_ptr<FftPlan<R>> fM, iM;
 };
 
-static cd twiddle(long k, long n, int sign) {
+template <class R> static Cx<R> unit_root(long k, long n, int sign) {
   k %= n;
   if (k < 0) k += n;
-  long double a = 2.0L * kPiL * (long double)k / (long double)n;
-  return cd((double)cosl(a), (double)(sign * sinl(a)));
+  const long double a = 2.0L * kPiL * (long double)k / (long double)n;
+  return {R(cosl(a)), R(sign * sinl(a))};
 }
 
-static std::shared_ptr<FftPlan> get_plan(int n, int sign);
+template <class R> static std::shared_ptr<FftPlan<R>> get_plan(int n, int sign);
+template <class R> static void fft_exec(const FftPlan<R>& P, Cx<R>* x, Cx<R>* work);
 
-static void fft_exec(const FftPlan& P, cd* x);
-
-static std::shared_ptr<FftPlan> make_plan(int n, int sign) {
-  auto P = std::make_shared<FftPlan>();
+template <class R> static std::shared_ptr<FftPlan<R>> make_plan(int n, int sign) {
+  auto P = std::make_shared<FftPlan<R>>();
   P->n = n;
   P->sign = sign;
   int m = n;
@@ -103,145 +159,229 @@ static std::shared_ptr<FftPlan> make_plan(int n, int sign) {
     }
   }
   if (m != 1) {
-    // remaining large prime factor(s): Bluestein chirp-z over a power of two
+    // a prime factor above 31: Bluestein chirp-z over a power of two
     P->blue = true;
     int M = 1;
     while (M < 2 * n - 1) M <<= 1;
     P->M = M;
-    P->chirp.resize(n);
+    P->chirp.resize((size_t)n);
     const long two_n = 2L * n;
     for (long k = 0; k < n; ++k) {
-      long e = (k * k) % two_n;  // exact integer argument reduction
-      long double a = kPiL * (long double)e / (long double)n;
-      P->chirp[k] = cd((double)cosl(a), (double)(sign * sinl(a)));
+      const long e = (k * k) % two_n;  // exact integer argument reduction
+      const long double a = kPiL * (long double)e / (long double)n;
+      P->chirp[(size_t)k] = {R(cosl(a)), R(sign * sinl(a))};
     }
-    P->fM = get_plan(M, -1);
-    P->iM = get_plan(M, +1);
-    P->kern_hat.assign(M, cd(0, 0));
+    P->fM = get_plan<R>(M, -1);
+    P->iM = get_plan<R>(M, +1);
+    P->kern_hat.assign((size_t)M, Cx<R>{0, 0});
     for (long k = 0; k < n; ++k) {
-      P->kern_hat[k] = std::conj(P->chirp[k]);
-      if (k) P->kern_hat[M - k] = std::conj(P->chirp[k]);
+      const Cx<R> c{P->chirp[(size_t)k].re, -P->chirp[(size_t)k].im};
+      P->kern_hat[(size_t)k] = c;
+      if (k) P->kern_hat[(size_t)(M - k)] = c;
     }
-    fft_exec(*P->fM, P->kern_hat.data());
+    std::vector<Cx<R>> w((size_t)M);
+    fft_exec(*P->fM, P->kern_hat.data(), w.data());
+    const R inv = R(1) / R(M);
+    for (auto& v : P->kern_hat) v = {v.re * inv, v.im * inv};
     return P;
   }
   P->fac = f;
-  P->tw.resize(n);
-  for (int k = 0; k < n; ++k) P->tw[k] = twiddle(k, n, sign);
+  P->tw.resize((size_t)n);
+  for (int k = 0; k < n; ++k) P->tw[(size_t)k] = unit_root<R>(k, n, sign);
   return P;
 }
 
-static std::mutex g_plan_mu;
-static std::map<std::pair<int, int>, std::shared_ptr<FftPlan>> g_plans;
+template <class R> struct PlanCache {
+  std::mutex mu;
+  std::map<std::pair<int, int>, std::shared_ptr<FftPlan<R>>> plans;
+};
+template <class R> static PlanCache<R>& plan_cache() {
+  static PlanCache<R> c;
+  return c;
+}
 
-static std::shared_ptr<FftPlan> get_plan(int n, int sign) {
+template <class R> static std::shared_ptr<FftPlan<R>> get_plan(int n, int sign) {
+  auto& c = plan_cache<R>();
   {
-    std::lock_guard<std::mutex> lk(g_plan_mu);
-    auto it = g_plans.find({n, sign});
-    if (it != g_plans.end()) return it->second;
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.plans.find({n, sign});
+    if (it != c.plans.end()) return it->second;
   }
-  auto p = make_plan(n, sign);
-  std::lock_guard<std::mutex> lk(g_plan_mu);
-  g_plans[{n, sign}] = p;
+  auto p = make_plan<R>(n, sign);
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.plans[{n, sign}] = p;
   return p;
 }
 
-// decimation in time, out-of-place recursion over the factor list
-static void fft_rec(const FftPlan& P, const cd* in, long s, cd* out, int n, int lvl,
-                    std::vector<cd>& tmp) {
-  if (n == 1) {
-    out[0] = in[0];
-    return;
-  }
-  const int p = P.fac[lvl];
-  const int m = n / p;
-  for (int r = 0; r < p; ++r) fft_rec(P, in + r * s, s * p, out + r * m, m, lvl + 1, tmp);
-  const long step = P.n / n;  // W_n^e = tw[e*step]
-  cd z[32];
-  for (int k = 0; k < m; ++k) {
-    for (int r = 0; r < p; ++r) z[r] = out[r * m + k] * P.tw[(size_t)((long)r * k * step % P.n)];
-    for (int t = 0; t < p; ++t) {
-      cd acc = z[0];
-      for (int r = 1; r < p; ++r) acc += z[r] * P.tw[(size_t)(((long)r * t % p) * (P.n / p))];
-      tmp[(size_t)(k + (long)m * t)] = acc;
+// In-register radix-p DFT of v[0..p) (p-th roots from the plan's table).
+template <class R> static inline void small_dft(Cx<R>* v, int p, const FftPlan<R>& P) {
+  const int sign = P.sign;
+  if (p == 2) {
+    const Cx<R> a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if (p == 4) {
+    const Cx<R> a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
+    const Cx<R> b0 = cadd(v[1], v[3]), b1 = csub(v[1], v[3]);
+    // (-i*sign) * b1  (forward sign = -1: multiply by -i)
+    const Cx<R> jb1 = sign < 0 ? Cx<R>{b1.im, -b1.re} : Cx<R>{-b1.im, b1.re};
+    v[0] = cadd(a0, b0);
+    v[2] = csub(a0, b0);
+    v[1] = cadd(a1, jb1);
+    v[3] = csub(a1, jb1);
+  } else if (p == 3) {
+    const Cx<R> w = P.tw[(size_t)(P.n / 3)];
+    const Cx<R> s = cadd(v[1], v[2]), d = csub(v[1], v[2]);
+    const Cx<R> m{v[0].re + w.re * s.re, v[0].im + w.re * s.im};
+    const Cx<R> jd{-w.im * d.im, w.im * d.re};
+    v[0] = cadd(v[0], s);
+    v[1] = cadd(m, jd);
+    v[2] = csub(m, jd);
+  } else {
+    // generic odd prime: symmetric pairs, out_t = v0 + sum_r (c(rt) s_r + i sgn s(rt) d_r)
+    const int H = p / 2;
+    Cx<R> s[16], d[16];
+    for (int r = 1; r <= H; ++r) {
+      s[r] = cadd(v[r], v[p - r]);
+      d[r] = csub(v[r], v[p - r]);
     }
+    Cx<R> out[32];
+    Cx<R> sum = v[0];
+    for (int r = 1; r <= H; ++r) sum = cadd(sum, s[r]);
+    out[0] = sum;
+    const long step = P.n / p;
+    for (int t = 1; t <= H; ++t) {
+      Cx<R> a = v[0], b{0, 0};
+      for (int r = 1; r <= H; ++r) {
+        const Cx<R> w = P.tw[(size_t)(((long)r * t % p) * step)];
+        a.re += w.re * s[r].re;
+        a.im += w.re * s[r].im;
+        b.re += w.im * d[r].re;
+        b.im += w.im * d[r].im;
+      }
+      // w.im already carries the sign: i*b = (-b.im, b.re)
+      out[t] = {a.re - b.im, a.im + b.re};
+      out[p - t] = {a.re + b.im, a.im - b.re};
+    }
+    for (int t = 0; t < p; ++t) v[t] = out[t];
   }
-  for (int i = 0; i < n; ++i) out[i] = tmp[i];
 }
 
-static void fft_exec(const FftPlan& P, cd* x) {
+// Stockham autosort (decimation in time): stage with radix R_s over
+// Ns = product of the previous radices; x_j' for j in [0, n/R_s).
+// work: n scratch elements.  Result lands in x.
+template <class R> static void stockham(const FftPlan<R>& P, Cx<R>* x, Cx<R>* work) {
+  const int n = P.n;
+  Cx<R>* src = x;
+  Cx<R>* dst = work;
+  long Ns = 1;
+  for (int p : P.fac) {
+    const long nr = n / p;
+    const long tstep = n / (Ns * p);  // exp(sign 2 pi i r (j%Ns)/(Ns p)) = tw[r (j%Ns) tstep]
+    Cx<R> v[32];
+    for (long j = 0; j < nr; ++j) {
+      const long jm = j % Ns;
+      for (int r = 0; r < p; ++r) {
+        Cx<R> a = src[j + r * nr];
+        if (r && jm) a = cmul(a, P.tw[(size_t)(r * jm * tstep)]);
+        v[r] = a;
+      }
+      small_dft(v, p, P);
+      const long o = (j / Ns) * Ns * p + jm;
+      for (int r = 0; r < p; ++r) dst[o + r * Ns] = v[r];
+    }
+    std::swap(src, dst);
+    Ns *= p;
+  }
+  if (src != x) std::memcpy((void*)x, (const void*)src, sizeof(Cx<R>) * (size_t)n);
+}
+
+template <class R> static void fft_exec(const FftPlan<R>& P, Cx<R>* x, Cx<R>* work) {
   const int n = P.n;
   if (n == 1) return;
-  if (P.blue) {
-    const int M = P.M;
-    std::vector<cd> a(M, cd(0, 0));
-    for (int k = 0; k < n; ++k) a[k] = x[k] * P.chirp[k];
-    fft_exec(*P.fM, a.data());
-    for (int k = 0; k < M; ++k) a[k] *= P.kern_hat[k];
-    fft_exec(*P.iM, a.data());
-    const double inv = 1.0 / M;
-    for (int k = 0; k < n; ++k) x[k] = a[k] * inv * P.chirp[k];
+  if (!P.blue) {
+    stockham(P, x, work);
     return;
   }
-  std::vector<cd> in(x, x + n), tmp(n);
-  fft_rec(P, in.data(), 1, x, n, 0, tmp);
+  const int M = P.M;
+  // work holds a[M] followed by scratch[M]
+  Cx<R>* a = work;
+  Cx<R>* w2 = work + M;
+  for (int k = 0; k < n; ++k) a[k] = cmul(x[k], P.chirp[(size_t)k]);
+  for (int k = n; k < M; ++k) a[k] = {0, 0};
+  stockham(*P.fM, a, w2);
+  for (int k = 0; k < M; ++k) a[k] = cmul(a[k], P.kern_hat[(size_t)k]);
+  stockham(*P.iM, a, w2);
+  for (int k = 0; k < n; ++k) x[k] = cmul(a[k], P.chirp[(size_t)k]);
 }
 
-static void fft(cd* x, int n, int sign) { fft_exec(*get_plan(n, sign), x); }
+template <class R> static size_t work_size(const FftPlan<R>& P) { return P.blue ? 2 * (size_t)P.M : (size_t)P.n; }
+
+template <class R> static void fft(Cx<R>* x, int n, int sign) {
+  auto P = get_plan<R>(n, sign);
+  thread_local std::vector<Cx<R>> work;
+  if (work.size() < work_size(*P)) work.resize(work_size(*P));
+  fft_exec(*P, x, work.data());
+}
 
 // 2D unnormalised DFT, rows then columns (transforms.hpp:66-82, 229-249)
-static void dft2(std::vector<cd>& a, long L1, long L2, int sign) {
-  for (long r = 0; r < L1; ++r) fft(&a[size_t(r * L2)], (int)L2, sign);
-  std::vector<cd> col(L1);
-  for (long c = 0; c < L2; ++c) {
-    for (long r = 0; r < L1; ++r) col[r] = a[size_t(r * L2 + c)];
-    fft(col.data(), (int)L1, sign);
-    for (long r = 0; r < L1; ++r) a[size_t(r * L2 + c)] = col[r];
-  }
+template <class R> static void dft2(std::vector<Cx<R>>& a, long L1, long L2, int sign) {
+  Cx<R>* A = a.data();
+  parallel_for(L1, [&](long lo, long hi) {
+    for (long r = lo; r < hi; ++r) fft(A + r * L2, (int)L2, sign);
+  });
+  parallel_for(L2, [&](long lo, long hi) {
+    std::vector<Cx<R>> col((size_t)L1);
+    for (long c = lo; c < hi; ++c) {
+      for (long r = 0; r < L1; ++r) col[(size_t)r] = A[r * L2 + c];
+      fft(col.data(), (int)L1, sign);
+      for (long r = 0; r < L1; ++r) A[r * L2 + c] = col[(size_t)r];
+    }
+  });
 }
 
 // ---------------------------------------------------------------------------
 // PSF (psf.hpp)
 // ---------------------------------------------------------------------------
-struct Psf {
+template <class R> struct Psf {
   long q1, q2;
-  Mat t;  // (2q1+1) x (2q2+1), centre (q1,q2)
-  double tap(long i1, long i2) const { return t(q1 + i1, q2 + i2); }  // psf.hpp:32
+  Mat<R> t;  // (2q1+1) x (2q2+1), centre (q1,q2)
+  R tap(long i1, long i2) const { return t(q1 + i1, q2 + i2); }  // psf.hpp:32
 };
 
-// psf.hpp:15-25 (validation) — kMassTol = 1e-12 (psf.hpp:34)
-static Psf make_psf(const double* taps, long q1, long q2) {
+// psf.hpp:15-25 (validation) — kMassTol = 1e-12 (psf.hpp:34).  Validation is
+// done on the FP64 taps for every scalar type (the caller's mask is FP64).
+template <class R> static Psf<R> make_psf(const double* taps, long q1, long q2) {
   require(q1 >= 0 && q2 >= 0, "Psf: taps must have odd dimensions");
-  Psf p{q1, q2, Mat(2 * q1 + 1, 2 * q2 + 1)};
+  Psf<R> p{q1, q2, Mat<R>(2 * q1 + 1, 2 * q2 + 1)};
   double s = 0.0;
   for (size_t i = 0; i < p.t.a.size(); ++i) {
-    p.t.a[i] = taps[i];
+    p.t.a[i] = R(taps[i]);
     require(std::isfinite(taps[i]), "Psf: taps must be finite");
     require(taps[i] >= 0.0, "Psf: taps must be nonnegative");
   }
   // Eigen's sum() is a pairwise/vectorised reduction; the 1e-12 tolerance
   // makes the summation order irrelevant for the accept/reject decision.
-  for (double v : p.t.a) s += v;
+  for (size_t i = 0; i < p.t.a.size(); ++i) s += taps[i];
   require(std::abs(s - 1.0) <= 1e-12, "Psf: taps must sum to 1 (within 1e-12)");
   return p;
 }
 
 // psf.hpp:55-66
-static double max_asymmetry(const Psf& p) {
+template <class R> static double max_asymmetry(const Psf<R>& p) {
   double worst = 0.0;
   for (long i1 = -p.q1; i1 <= p.q1; ++i1)
     for (long i2 = -p.q2; i2 <= p.q2; ++i2)
-      worst = std::max(worst, std::abs(p.tap(i1, i2) - p.tap(std::labs(i1), std::labs(i2))));
+      worst = std::max(worst, (double)std::abs(p.tap(i1, i2) - p.tap(std::labs(i1), std::labs(i2))));
   return worst;
 }
 
 // psf.hpp:71-85
-static Psf symmetrize(const Psf& p) {
-  Psf s{p.q1, p.q2, Mat(2 * p.q1 + 1, 2 * p.q2 + 1)};
+template <class R> static Psf<R> symmetrize(const Psf<R>& p) {
+  Psf<R> s{p.q1, p.q2, Mat<R>(2 * p.q1 + 1, 2 * p.q2 + 1)};
   for (long i1 = 0; i1 <= p.q1; ++i1)
     for (long i2 = 0; i2 <= p.q2; ++i2) {
-      const double avg =
-          (p.tap(-i1, -i2) + p.tap(-i1, i2) + p.tap(i1, -i2) + p.tap(i1, i2)) / 4.0;
+      const R avg = (p.tap(-i1, -i2) + p.tap(-i1, i2) + p.tap(i1, -i2) + p.tap(i1, i2)) / R(4);
       s.t(p.q1 + i1, p.q2 + i2) = avg;
       s.t(p.q1 - i1, p.q2 + i2) = avg;
       s.t(p.q1 + i1, p.q2 - i2) = avg;
@@ -251,25 +391,25 @@ static Psf symmetrize(const Psf& p) {
 }
 
 // psf.hpp:88-91 (taps().reverse())
-static Psf rotate180(const Psf& p) {
-  Psf r = p;
+template <class R> static Psf<R> rotate180(const Psf<R>& p) {
+  Psf<R> r = p;
   std::reverse(r.t.a.begin(), r.t.a.end());
   return r;
 }
 
 // psf.hpp:98-109 (accumulation order: h00, axis-1, axis-2, cross terms)
-static double symbol_real(const Psf& p, double x1, double x2) {
-  double acc = p.tap(0, 0);
-  for (long s1 = 1; s1 <= p.q1; ++s1) acc += 2.0 * p.tap(s1, 0) * std::cos(s1 * x1);
-  for (long s2 = 1; s2 <= p.q2; ++s2) acc += 2.0 * p.tap(0, s2) * std::cos(s2 * x2);
+template <class R> static R symbol_real(const Psf<R>& p, R x1, R x2) {
+  R acc = p.tap(0, 0);
+  for (long s1 = 1; s1 <= p.q1; ++s1) acc += R(2) * p.tap(s1, 0) * std::cos(R(s1) * x1);
+  for (long s2 = 1; s2 <= p.q2; ++s2) acc += R(2) * p.tap(0, s2) * std::cos(R(s2) * x2);
   for (long s1 = 1; s1 <= p.q1; ++s1)
     for (long s2 = 1; s2 <= p.q2; ++s2)
-      acc += 4.0 * p.tap(s1, s2) * std::cos(s1 * x1) * std::cos(s2 * x2);
+      acc += R(4) * p.tap(s1, s2) * std::cos(R(s1) * x1) * std::cos(R(s2) * x2);
   return acc;
 }
 
 // ---------------------------------------------------------------------------
-// Boundary (boundary.hpp) — AR branch only (the north star is AR-only)
+// Boundary (boundary.hpp)
 // ---------------------------------------------------------------------------
 // boundary.hpp:66-81 (AR branch)
 static void check_support_ar(long n1, long n2, long q1, long q2) {
@@ -288,14 +428,14 @@ static void check_support_refl(long n1, long n2, long q1, long q2) {
 
 // boundary.hpp:88-102 with extend_axis Reflective (49-55): f_{1-i} = f_i,
 // f_{n+i} = f_{n+1-i}; rows first, then columns of the widened image.
-static Mat pad_refl(const Mat& f, long q1, long q2) {
+template <class R> static Mat<R> pad_refl(const Mat<R>& f, long q1, long q2) {
   const long n1 = f.n1, n2 = f.n2;
   check_support_refl(n1, n2, q1, q2);
-  Mat out(n1 + 2 * q1, n2 + 2 * q2);
+  Mat<R> out(n1 + 2 * q1, n2 + 2 * q2);
   for (long r = 0; r < n1; ++r)
     for (long c = 0; c < n2; ++c) out(q1 + r, q2 + c) = f(r, c);
   for (long r = 0; r < n1; ++r) {
-    double* b = &out(q1 + r, 0);
+    R* b = &out(q1 + r, 0);
     for (long i = 1; i <= q2; ++i) {
       b[q2 - i] = b[q2 + i - 1];
       b[q2 + n2 - 1 + i] = b[q2 + n2 - i];
@@ -311,26 +451,26 @@ static Mat pad_refl(const Mat& f, long q1, long q2) {
 
 // boundary.hpp:88-102 with extend_axis AR (56-62): rows (axis 2) of the FOV
 // first, then every column (axis 1) of the widened image.
-static Mat pad_ar(const Mat& f, long q1, long q2) {
+template <class R> static Mat<R> pad_ar(const Mat<R>& f, long q1, long q2) {
   const long n1 = f.n1, n2 = f.n2;
   check_support_ar(n1, n2, q1, q2);
-  Mat out(n1 + 2 * q1, n2 + 2 * q2);
+  Mat<R> out(n1 + 2 * q1, n2 + 2 * q2);
   for (long r = 0; r < n1; ++r)
     for (long c = 0; c < n2; ++c) out(q1 + r, q2 + c) = f(r, c);
   if (q2 > 0)
     for (long r = 0; r < n1; ++r) {
-      double* b = &out(q1 + r, 0);
+      R* b = &out(q1 + r, 0);
       for (long i = 1; i <= q2; ++i) {
-        b[q2 - i] = 2.0 * b[q2] - b[q2 + i];
-        b[q2 + n2 - 1 + i] = 2.0 * b[q2 + n2 - 1] - b[q2 + n2 - 1 - i];
+        b[q2 - i] = R(2) * b[q2] - b[q2 + i];
+        b[q2 + n2 - 1 + i] = R(2) * b[q2 + n2 - 1] - b[q2 + n2 - 1 - i];
       }
     }
   if (q1 > 0)
     for (long c = 0; c < n2 + 2 * q2; ++c) {
-      auto b = [&](long i) -> double& { return out(i, c); };
+      auto b = [&](long i) -> R& { return out(i, c); };
       for (long i = 1; i <= q1; ++i) {
-        b(q1 - i) = 2.0 * b(q1) - b(q1 + i);
-        b(q1 + n1 - 1 + i) = 2.0 * b(q1 + n1 - 1) - b(q1 + n1 - 1 - i);
+        b(q1 - i) = R(2) * b(q1) - b(q1 + i);
+        b(q1 + n1 - 1 + i) = R(2) * b(q1 + n1 - 1) - b(q1 + n1 - 1 - i);
       }
     }
   return out;
@@ -340,44 +480,80 @@ static Mat pad_ar(const Mat& f, long q1, long q2) {
 // Blur (blur.hpp)
 // ---------------------------------------------------------------------------
 // blur.hpp:39-52
-static Mat correlate_valid_direct(const Mat& P, const Psf& p, long n1, long n2) {
+template <class R> static Mat<R> correlate_valid_direct(const Mat<R>& P, const Psf<R>& p, long n1, long n2) {
   const long q1 = p.q1, q2 = p.q2;
-  Mat g(n1, n2);
-  for (long r = 0; r < n1; ++r)
-    for (long c = 0; c < n2; ++c) {
-      double acc = 0.0;
-      for (long s1 = -q1; s1 <= q1; ++s1)
-        for (long s2 = -q2; s2 <= q2; ++s2) acc += p.tap(s1, s2) * P(r + q1 - s1, c + q2 - s2);
-      g(r, c) = acc;
-    }
+  Mat<R> g(n1, n2);
+  parallel_for(n1, [&](long lo, long hi) {
+    for (long r = lo; r < hi; ++r)
+      for (long c = 0; c < n2; ++c) {
+        R acc = 0;
+        for (long s1 = -q1; s1 <= q1; ++s1)
+          for (long s2 = -q2; s2 <= q2; ++s2) acc += p.tap(s1, s2) * P(r + q1 - s1, c + q2 - s2);
+        g(r, c) = acc;
+      }
+  });
   return g;
 }
 
+// The reference recomputes the mask spectrum on every call (blur.hpp:65-66);
+// orc_set_kernel_cache(1) keeps the bit-identical spectrum of the last mask
+// (tests only: it changes no number, only the oracle's run time).
+static std::atomic<int> g_kernel_cache{0};
+template <class R> struct KernelCache {
+  struct Entry {
+    long L1, L2, q1, q2;
+    std::vector<R> taps;
+    std::shared_ptr<std::vector<Cx<R>>> spec;
+  };
+  std::mutex mu;
+  std::vector<Entry> e;  // A and A' masks alternate; keep a few
+};
+template <class R> static KernelCache<R>& kernel_cache() {
+  static KernelCache<R> c;
+  return c;
+}
+
+template <class R> static std::shared_ptr<std::vector<Cx<R>>> mask_spectrum(const Psf<R>& p, long L1, long L2) {
+  auto build = [&] {
+    auto k = std::make_shared<std::vector<Cx<R>>>(size_t(L1 * L2), Cx<R>{0, 0});
+    for (long r = 0; r < 2 * p.q1 + 1; ++r)
+      for (long c = 0; c < 2 * p.q2 + 1; ++c) (*k)[size_t(r * L2 + c)] = {p.t(r, c), 0};
+    dft2(*k, L1, L2, -1);
+    return k;
+  };
+  if (!g_kernel_cache.load()) return build();
+  auto& C = kernel_cache<R>();
+  std::lock_guard<std::mutex> lk(C.mu);
+  for (auto& e : C.e)
+    if (e.L1 == L1 && e.L2 == L2 && e.q1 == p.q1 && e.q2 == p.q2 && e.taps == p.t.a) return e.spec;
+  if (C.e.size() >= 4) C.e.erase(C.e.begin());
+  C.e.push_back({L1, L2, p.q1, p.q2, p.t.a, build()});
+  return C.e.back().spec;
+}
+
 // blur.hpp:56-68: zero-embed in (rows+2q1) x (cols+2q2), DFT product, crop
-static Mat correlate_valid_fft(const Mat& P, const Psf& p, long n1, long n2) {
+template <class R> static Mat<R> correlate_valid_fft(const Mat<R>& P, const Psf<R>& p, long n1, long n2) {
   const long q1 = p.q1, q2 = p.q2;
   const long L1 = P.n1 + 2 * q1, L2 = P.n2 + 2 * q2;
-  std::vector<cd> a(size_t(L1 * L2), cd(0, 0)), k(size_t(L1 * L2), cd(0, 0));
+  std::vector<Cx<R>> a(size_t(L1 * L2), Cx<R>{0, 0});
   for (long r = 0; r < P.n1; ++r)
-    for (long c = 0; c < P.n2; ++c) a[size_t(r * L2 + c)] = P(r, c);
-  for (long r = 0; r < 2 * q1 + 1; ++r)
-    for (long c = 0; c < 2 * q2 + 1; ++c) k[size_t(r * L2 + c)] = p.t(r, c);
+    for (long c = 0; c < P.n2; ++c) a[size_t(r * L2 + c)] = {P(r, c), 0};
+  auto k = mask_spectrum(p, L1, L2);
   dft2(a, L1, L2, -1);
-  dft2(k, L1, L2, -1);
-  for (size_t i = 0; i < a.size(); ++i) a[i] *= k[i];
+  for (size_t i = 0; i < a.size(); ++i) a[i] = cmul(a[i], (*k)[i]);
   dft2(a, L1, L2, +1);
-  const double inv = 1.0 / double(L1 * L2);
-  Mat g(n1, n2);
+  const R inv = R(1) / R(L1 * L2);
+  Mat<R> g(n1, n2);
   for (long r = 0; r < n1; ++r)
-    for (long c = 0; c < n2; ++c) g(r, c) = (a[size_t((r + 2 * q1) * L2 + c + 2 * q2)] * inv).real();
+    for (long c = 0; c < n2; ++c) g(r, c) = a[size_t((r + 2 * q1) * L2 + c + 2 * q2)].re * inv;
   return g;
 }
 
 constexpr long kDirectConvMaxQ = 7;  // blur.hpp:70
 
 // blur.hpp:75-83 (path: 0 auto, 1 direct, 2 fft)
-static Mat apply(const Psf& p, const Mat& f, int path = 0, int bc = kAntiReflective) {
-  const Mat P = bc == kReflective ? pad_refl(f, p.q1, p.q2) : pad_ar(f, p.q1, p.q2);
+template <class R> static Mat<R> apply(const Psf<R>& p, const Mat<R>& f, int path = 0, int bc = kAntiReflective) {
+  const Mat<R> P = bc == kReflective ? pad_refl(f, p.q1, p.q2) : pad_ar(f, p.q1, p.q2);
   const bool direct = path == 1 || (path == 0 && p.q1 <= kDirectConvMaxQ && p.q2 <= kDirectConvMaxQ);
   return direct ? correlate_valid_direct(P, p, f.n1, f.n2) : correlate_valid_fft(P, p, f.n1, f.n2);
 }
@@ -387,52 +563,54 @@ static Mat apply(const Psf& p, const Mat& f, int path = 0, int bc = kAntiReflect
 // ---------------------------------------------------------------------------
 // FFTW RODFT00 semantics: y_k = 2 sum_j x_j sin(pi (j+1)(k+1)/(m+1)),
 // computed through the 2(m+1)-point DFT of the odd extension.
-static void rodft00(const double* x, double* y, long m) {
+template <class R> static void rodft00(const R* x, R* y, long m) {
   const long N = m + 1, L = 2 * N;
-  std::vector<cd> v(size_t(L), cd(0, 0));
+  thread_local std::vector<Cx<R>> v;
+  v.assign(size_t(L), Cx<R>{0, 0});
   for (long j = 0; j < m; ++j) {
-    v[size_t(j + 1)] = x[j];
-    v[size_t(L - 1 - j)] = -x[j];
+    v[size_t(j + 1)] = {x[j], 0};
+    v[size_t(L - 1 - j)] = {-x[j], 0};
   }
   fft(v.data(), (int)L, -1);
-  for (long k = 0; k < m; ++k) y[k] = -v[size_t(k + 1)].imag();
+  for (long k = 0; k < m; ++k) y[k] = -v[size_t(k + 1)].im;
 }
 
 // transforms.hpp:114-121
-static void sine1_forward(const double* v, double* y, long m) {
+template <class R> static void sine1_forward(const R* v, R* y, long m) {
   require(m >= 1, "sine1_forward: empty input");
   rodft00(v, y, m);
-  const double s = 0.5 * std::sqrt(2.0 / double(m + 1));
+  const R s = R(0.5) * std::sqrt(R(2) / R(m + 1));
   for (long i = 0; i < m; ++i) y[i] *= s;
 }
 
 // transforms.hpp:129-144
-struct ArT {
+template <class R> struct ArT {
   long m = 0;
-  double alpha = 1.0;
-  std::vector<double> p;
+  R alpha = 1;
+  std::vector<R> p;
 };
-static ArT make_ar_transform(long m) {
+template <class R> static ArT<R> make_ar_transform(long m) {
   require(m >= 3, "ArTransform1D: size must be at least 3");
-  ArT t;
+  ArT<R> t;
   t.m = m;
   t.p.resize(size_t(m - 2));
-  double sq = 0.0;
-  for (long j = 1; j <= m - 2; ++j) t.p[size_t(j - 1)] = 1.0 - double(j) / double(m - 1);
-  for (double v : t.p) sq += v * v;  // Eigen squaredNorm: order differs only by rounding
-  t.alpha = std::sqrt(1.0 + sq);
+  R sq = 0;
+  for (long j = 1; j <= m - 2; ++j) t.p[size_t(j - 1)] = R(1) - R(j) / R(m - 1);
+  for (R v : t.p) sq += v * v;  // Eigen squaredNorm: order differs only by rounding
+  t.alpha = std::sqrt(R(1) + sq);
   return t;
 }
 
 // transforms.hpp:148-160
-static void ar_forward(const ArT& t, const double* v, double* w) {
+template <class R> static void ar_forward(const ArT<R>& t, const R* v, R* w) {
   const long m = t.m;
-  const double inv_a = 1.0 / t.alpha;
-  std::vector<double> in(v + 1, v + m - 1), out(size_t(m - 2));
-  sine1_forward(in.data(), out.data(), m - 2);
-  const double a0 = inv_a * v[0], a1 = inv_a * v[m - 1];
+  const R inv_a = R(1) / t.alpha;
+  thread_local std::vector<R> out;
+  out.resize(size_t(m - 2));
+  sine1_forward(v + 1, out.data(), m - 2);
+  const R a0 = inv_a * v[0], a1 = inv_a * v[m - 1];
   for (long j = 0; j < m - 2; ++j) {
-    double s = out[size_t(j)];
+    R s = out[size_t(j)];
     s += a0 * t.p[size_t(j)];
     s += a1 * t.p[size_t(m - 3 - j)];
     out[size_t(j)] = s;
@@ -443,11 +621,13 @@ static void ar_forward(const ArT& t, const double* v, double* w) {
 }
 
 // transforms.hpp:163-173
-static void ar_inverse(const ArT& t, const double* v, double* u) {
+template <class R> static void ar_inverse(const ArT<R>& t, const R* v, R* u) {
   const long m = t.m;
-  std::vector<double> in(size_t(m - 2)), out(size_t(m - 2));
+  thread_local std::vector<R> in, out;
+  in.resize(size_t(m - 2));
+  out.resize(size_t(m - 2));
   for (long j = 0; j < m - 2; ++j) {
-    double s = v[j + 1] - v[0] * t.p[size_t(j)];
+    R s = v[j + 1] - v[0] * t.p[size_t(j)];
     s -= v[m - 1] * t.p[size_t(m - 3 - j)];
     in[size_t(j)] = s;
   }
@@ -462,63 +642,71 @@ enum Kind { kCosineIII = 1, kSineI = 2, kAR = 3, kARInv = 4 };  // TransformKind
 // transforms.hpp:88-110: R_m(s,t) = sqrt((2 - delta_{s,0})/m) cos(s (2t+1) pi / (2m))
 // (0-based), FFTW REDFT10 / REDFT01 with the orthonormal scaling; restated
 // as the dense definition with exact integer argument reduction (angle index
-// s (2t+1) mod 4m) and long-double cosines.
-static const std::vector<double>& cos4m(long m) {
-  static thread_local std::map<long, std::vector<double>> cache;
+// s (2t+1) mod 4m) and long-double cosines / accumulation.
+static const std::vector<long double>& cos4m(long m) {
+  static std::mutex mu;
+  static std::map<long, std::vector<long double>> cache;
+  std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(m);
   if (it != cache.end()) return it->second;
-  std::vector<double> c(size_t(4 * m));
-  for (long e = 0; e < 4 * m; ++e) c[size_t(e)] = double(cosl(kPiL * (long double)e / (long double)(2 * m)));
+  std::vector<long double> c(size_t(4 * m));
+  for (long e = 0; e < 4 * m; ++e) c[size_t(e)] = cosl(kPiL * (long double)e / (long double)(2 * m));
   return cache.emplace(m, std::move(c)).first->second;
 }
-static void cosine3_forward(const double* v, double* y, long m) {
+template <class R> static void cosine3_forward(const R* v, R* y, long m) {
   require(m >= 1, "cosine3_forward: empty input");
   const auto& c = cos4m(m);
   const long double w0 = sqrtl(1.0L / (long double)m), w = sqrtl(2.0L / (long double)m);
   for (long s = 0; s < m; ++s) {
     long double acc = 0;
-    for (long t = 0; t < m; ++t) acc += (long double)v[t] * c[size_t((s * (2 * t + 1)) % (4 * m))];
-    y[s] = double(acc * (s == 0 ? w0 : w));
+    for (long t = 0; t < m; ++t) acc += (long double)v[t] * (long double)R(c[size_t((s * (2 * t + 1)) % (4 * m))]);
+    y[s] = R(acc * (s == 0 ? w0 : w));
   }
 }
-static void cosine3_inverse(const double* v, double* y, long m) {
+template <class R> static void cosine3_inverse(const R* v, R* y, long m) {
   require(m >= 1, "cosine3_inverse: empty input");
   const auto& c = cos4m(m);
   const long double w0 = sqrtl(1.0L / (long double)m), w = sqrtl(2.0L / (long double)m);
   for (long t = 0; t < m; ++t) {
     long double acc = (long double)v[0] * w0;
-    for (long s = 1; s < m; ++s) acc += (long double)v[s] * w * c[size_t((s * (2 * t + 1)) % (4 * m))];
-    y[t] = double(acc);
+    for (long s = 1; s < m; ++s)
+      acc += (long double)v[s] * w * (long double)R(c[size_t((s * (2 * t + 1)) % (4 * m))]);
+    y[t] = R(acc);
   }
 }
 
 // transforms.hpp:179-192 (columns first, then rows) + 198-226
-static Mat tensor_apply(int kind, const Mat& x) {
+template <class R> static Mat<R> tensor_apply(int kind, const Mat<R>& x) {
   const long n1 = x.n1, n2 = x.n2;
-  ArT t1, t2;
+  ArT<R> t1, t2;
   if (kind == kAR || kind == kARInv) {
     require(n1 >= 3 && n2 >= 3, "tensor_apply: anti-reflective transform needs sizes >= 3");
-    t1 = make_ar_transform(n1);
-    t2 = make_ar_transform(n2);
+    t1 = make_ar_transform<R>(n1);
+    t2 = make_ar_transform<R>(n2);
   }
-  auto kern = [&](const ArT& t, const double* in, double* out, long m) {
+  auto kern = [&](const ArT<R>& t, const R* in, R* out, long m) {
     if (kind == kCosineIII) cosine3_forward(in, out, m);
     else if (kind == -kCosineIII) cosine3_inverse(in, out, m);
     else if (kind == kSineI) sine1_forward(in, out, m);
     else if (kind == kAR) ar_forward(t, in, out);
     else ar_inverse(t, in, out);
   };
-  Mat y(n1, n2);
-  std::vector<double> buf(size_t(std::max(n1, n2))), o(size_t(std::max(n1, n2)));
-  for (long c = 0; c < n2; ++c) {
-    for (long r = 0; r < n1; ++r) buf[size_t(r)] = x(r, c);
-    kern(t1, buf.data(), o.data(), n1);
-    for (long r = 0; r < n1; ++r) y(r, c) = o[size_t(r)];
-  }
-  for (long r = 0; r < n1; ++r) {
-    kern(t2, &y(r, 0), o.data(), n2);
-    for (long c = 0; c < n2; ++c) y(r, c) = o[size_t(c)];
-  }
+  Mat<R> y(n1, n2);
+  parallel_for(n2, [&](long lo, long hi) {
+    std::vector<R> buf((size_t)n1), o((size_t)n1);
+    for (long c = lo; c < hi; ++c) {
+      for (long r = 0; r < n1; ++r) buf[size_t(r)] = x(r, c);
+      kern(t1, buf.data(), o.data(), n1);
+      for (long r = 0; r < n1; ++r) y(r, c) = o[size_t(r)];
+    }
+  });
+  parallel_for(n1, [&](long lo, long hi) {
+    std::vector<R> o((size_t)n2);
+    for (long r = lo; r < hi; ++r) {
+      kern(t2, &y(r, 0), o.data(), n2);
+      for (long c = 0; c < n2; ++c) y(r, c) = o[size_t(c)];
+    }
+  });
   return y;
 }
 
@@ -526,70 +714,74 @@ static Mat tensor_apply(int kind, const Mat& x) {
 // Spectral / preconditioner (spectral.hpp, preconditioner.hpp)
 // ---------------------------------------------------------------------------
 // spectral.hpp:63-69
-static std::vector<double> antireflective_grid(long m) {
-  std::vector<double> x(size_t(m), 0.0);
-  for (long r = 1; r <= m - 2; ++r) x[size_t(r)] = double(r) * kPi / double(m - 1);
-  x[size_t(m - 1)] = 0.0;
+template <class R> static std::vector<R> antireflective_grid(long m) {
+  std::vector<R> x(size_t(m), R(0));
+  for (long r = 1; r <= m - 2; ++r) x[size_t(r)] = R(r) * pi_v<R>() / R(m - 1);
+  x[size_t(m - 1)] = R(0);
   return x;
 }
 
 // spectral.hpp:120-133 + 43-48
-static Mat eig_antireflective(const Psf& p, long n1, long n2) {
+template <class R> static Mat<R> eig_antireflective(const Psf<R>& p, long n1, long n2) {
   require(max_asymmetry(p) <= 1e-12, "eig_antireflective: mask is not strongly symmetric");
   require(n1 >= 3 && n2 >= 3, "eig_antireflective: sizes must be >= 3");
   require(p.q1 <= n1 - 2 && p.q2 <= n2 - 2, "eig_antireflective: support condition violated");
-  const auto x1 = antireflective_grid(n1), x2 = antireflective_grid(n2);
-  Mat e(n1, n2);
-  for (long a = 0; a < n1; ++a)
-    for (long b = 0; b < n2; ++b) e(a, b) = symbol_real(p, x1[size_t(a)], x2[size_t(b)]);
+  const auto x1 = antireflective_grid<R>(n1), x2 = antireflective_grid<R>(n2);
+  Mat<R> e(n1, n2);
+  parallel_for(n1, [&](long lo, long hi) {
+    for (long a = lo; a < hi; ++a)
+      for (long b = 0; b < n2; ++b) e(a, b) = symbol_real(p, x1[size_t(a)], x2[size_t(b)]);
+  });
   return e;
 }
 
 // spectral.hpp:50-54, 73-84: x_r = r pi / m, r = 0..m-1
-static Mat eig_reflective(const Psf& p, long n1, long n2) {
+template <class R> static Mat<R> eig_reflective(const Psf<R>& p, long n1, long n2) {
   require(max_asymmetry(p) <= 1e-12, "eig_reflective: mask is not strongly symmetric");
-  Mat e(n1, n2);
-  for (long a = 0; a < n1; ++a)
-    for (long b = 0; b < n2; ++b)
-      e(a, b) = symbol_real(p, double(a) * kPi / double(n1), double(b) * kPi / double(n2));
+  Mat<R> e(n1, n2);
+  parallel_for(n1, [&](long lo, long hi) {
+    for (long a = lo; a < hi; ++a)
+      for (long b = 0; b < n2; ++b)
+        e(a, b) = symbol_real(p, R(a) * pi_v<R>() / R(n1), R(b) * pi_v<R>() / R(n2));
+  });
   return e;
 }
 
 // preconditioner.hpp:37-57 (real algebra branch)
-static Mat tikhonov_filter(const Mat& base, double alpha) {
-  require(alpha >= 0.0, "tikhonov_filter: alpha must be nonnegative");
+template <class R> static Mat<R> tikhonov_filter(const Mat<R>& base, R alpha) {
+  require(alpha >= 0, "tikhonov_filter: alpha must be nonnegative");
   bool allpos = true;
-  for (double l : base.a) allpos = allpos && (l * l > 0.0);
-  require(alpha > 0.0 || allpos, "tikhonov_filter: alpha = 0 with a zero eigenvalue");
-  Mat d(base.n1, base.n2);
-  for (size_t i = 0; i < d.a.size(); ++i) d.a[i] = 1.0 / (base.a[i] * base.a[i] + alpha);
+  for (R l : base.a) allpos = allpos && (l * l > 0);
+  require(alpha > 0 || allpos, "tikhonov_filter: alpha = 0 with a zero eigenvalue");
+  Mat<R> d(base.n1, base.n2);
+  for (size_t i = 0; i < d.a.size(); ++i) d.a[i] = R(1) / (base.a[i] * base.a[i] + alpha);
   return d;
 }
 
 // preconditioner.hpp:62-85 (AntiReflective branch)
-static Mat build_tikhonov(const Psf& p, double alpha, long n1, long n2) {
-  const Psf s = symmetrize(p);
+template <class R> static Mat<R> build_tikhonov(const Psf<R>& p, R alpha, long n1, long n2) {
+  const Psf<R> s = symmetrize(p);
   return tikhonov_filter(eig_antireflective(s, n1, n2), alpha);
 }
 
 // preconditioner.hpp:62-85 (CosineIII branch)
-static Mat build_tikhonov_cos(const Psf& p, double alpha, long n1, long n2) {
-  const Psf s = symmetrize(p);
+template <class R> static Mat<R> build_tikhonov_cos(const Psf<R>& p, R alpha, long n1, long n2) {
+  const Psf<R> s = symmetrize(p);
   return tikhonov_filter(eig_reflective(s, n1, n2), alpha);
 }
 
 // spectral.hpp:147-154: R^T diag(d) R (forward tensor, Hadamard, inverse tensor)
-static Mat filter_apply_cos(const Mat& d, const Mat& x) {
+template <class R> static Mat<R> filter_apply_cos(const Mat<R>& d, const Mat<R>& x) {
   require(x.n1 == d.n1 && x.n2 == d.n2, "filter_apply: size mismatch");
-  Mat xhat = tensor_apply(kCosineIII, x);
+  Mat<R> xhat = tensor_apply(kCosineIII, x);
   for (size_t i = 0; i < xhat.a.size(); ++i) xhat.a[i] *= d.a[i];
   return tensor_apply(-kCosineIII, xhat);
 }
 
 // spectral.hpp:161-165 / preconditioner.hpp:88-90
-static Mat filter_apply_ar(const Mat& d, const Mat& x) {
+template <class R> static Mat<R> filter_apply_ar(const Mat<R>& d, const Mat<R>& x) {
   require(x.n1 == d.n1 && x.n2 == d.n2, "filter_apply: size mismatch");
-  Mat xhat = tensor_apply(kARInv, x);
+  Mat<R> xhat = tensor_apply(kARInv, x);
   for (size_t i = 0; i < xhat.a.size(); ++i) xhat.a[i] *= d.a[i];
   return tensor_apply(kAR, xhat);
 }
@@ -636,12 +828,82 @@ static void add_noise(const double* g, long n1, long n2, double level, uint64_t 
 }
 
 // image.hpp:85-91
-static double rre(const double* x, const double* f, size_t n) {
-  const double den = fro(f, n);
-  require(den > 0.0, "rre: zero true image");
-  double s = 0.0;
+template <class R> static R rre(const R* x, const R* f, size_t n) {
+  const R den = fro(f, n);
+  require(den > 0, "rre: zero true image");
+  R s = 0;
   for (size_t i = 0; i < n; ++i) s += (x[i] - f[i]) * (x[i] - f[i]);
   return std::sqrt(s) / den;
+}
+
+// solver.hpp:17-32 StoppingRule kinds
+enum { STOP_FIXED = 0, STOP_MINRRE = 1, STOP_RESID = 2 };
+
+// solver.hpp:63-132 landweber_loop (+ 139-148) in scalar type R.  d == NULL
+// -> plain Landweber (for R = long double the filter is rebuilt from the taps
+// in R when `alpha_ld` >= 0, so the preconditioner carries no FP64 rounding).
+// x_hist (nullable) receives every iterate x_k (rounded to FP64), k = 1..executed.
+template <class R>
+static void landweber_loop(const double* taps, long q1, long q2, long n1, long n2, const double* d, double alpha_ld,
+                           const double* g, const double* f_true, double tau_d, int max_iters, int stop_kind,
+                           int fixed_iters, double resid_eps, int conv_path, int bc, double* restored,
+                           double* rre_hist, double* res_hist, int* best_iter, int* iters_done, double* x_hist) {
+  Psf<R> p = make_psf<R>(taps, q1, q2);
+  require(n1 >= 1 && n2 >= 1, "BlurOperator: empty field of view");
+  require(bc == kReflective || bc == kAntiReflective, "landweber: unsupported boundary condition");
+  if (bc == kReflective) check_support_refl(n1, n2, q1, q2);
+  else check_support_ar(n1, n2, q1, q2);
+  require(tau_d > 0.0, "landweber: tau must be positive");
+  require(max_iters >= 1, "landweber: max_iters must be at least 1");
+  require(stop_kind != STOP_FIXED || fixed_iters >= 0, "StoppingRule: negative iteration count");
+  require(stop_kind != STOP_RESID || resid_eps > 0.0, "StoppingRule: threshold must be positive");
+  const size_t N = size_t(n1) * size_t(n2);
+  const int total = stop_kind == STOP_FIXED ? fixed_iters : max_iters;
+  const R tau = R(tau_d);
+  Mat<R> G(n1, n2), F;
+  for (size_t i = 0; i < N; ++i) G.a[i] = R(g[i]);
+  if (f_true) {
+    F = Mat<R>(n1, n2);
+    for (size_t i = 0; i < N; ++i) F.a[i] = R(f_true[i]);
+  }
+  const R g_norm = fro(G.a.data(), N);
+  const R guard = R(1e8) * g_norm;
+  const Psf<R> rot = rotate180(p);
+  Mat<R> D;
+  const bool precond = d != nullptr || alpha_ld >= 0.0;
+  if (d) {
+    D = Mat<R>(n1, n2);
+    for (size_t i = 0; i < N; ++i) D.a[i] = R(d[i]);
+  } else if (alpha_ld >= 0.0) {
+    D = bc == kReflective ? build_tikhonov_cos(p, R(alpha_ld), n1, n2) : build_tikhonov(p, R(alpha_ld), n1, n2);
+  }
+  Mat<R> x(n1, n2), best(n1, n2), r = G;
+  R best_rre = std::numeric_limits<R>::infinity();
+  for (int k = 1; k <= total; ++k) {
+    Mat<R> step = apply(rot, r, conv_path, bc);
+    if (precond) step = bc == kReflective ? filter_apply_cos(D, step) : filter_apply_ar(D, step);
+    for (size_t i = 0; i < N; ++i) x.a[i] += tau * step.a[i];
+    const Mat<R> ax = apply(p, x, conv_path, bc);
+    for (size_t i = 0; i < N; ++i) r.a[i] = G.a[i] - ax.a[i];
+    if (fro(x.a.data(), N) > guard && g_norm > 0) throw std::runtime_error("landweber: iterate exceeded 1e8 * ||g||");
+    const R rn = fro(r.a.data(), N);
+    res_hist[k - 1] = double(rn);
+    if (f_true) {
+      const R e = rre(x.a.data(), F.a.data(), N);
+      rre_hist[k - 1] = double(e);
+      if (e < best_rre) {
+        best_rre = e;
+        *best_iter = k;
+        if (stop_kind == STOP_MINRRE) best = x;
+      }
+    }
+    if (x_hist)
+      for (size_t i = 0; i < N; ++i) x_hist[size_t(k - 1) * N + i] = double(x.a[i]);
+    *iters_done = k;
+    if (stop_kind == STOP_RESID && g_norm > 0 && double(rn / g_norm) < resid_eps) break;
+  }
+  const Mat<R>& out = (stop_kind == STOP_MINRRE && f_true && *best_iter > 0) ? best : x;
+  for (size_t i = 0; i < N; ++i) restored[i] = double(out.a[i]);
 }
 
 }  // namespace orc
@@ -651,6 +913,8 @@ static double rre(const double* x, const double* f, size_t n) {
 // Status: 0 ok, 1 invalid argument, 2 divergence.
 // ============================================================================
 using namespace orc;
+using MatD = Mat<double>;
+using PsfD = Psf<double>;
 
 #define ORC_TRY(...)                  \
   try {                               \
@@ -664,48 +928,86 @@ using namespace orc;
     return 2;                         \
   }
 
-static Mat to_mat(const double* x, long n1, long n2) {
-  Mat m(n1, n2);
-  std::memcpy(m.a.data(), x, sizeof(double) * size_t(n1 * n2));
+template <class R = double> static Mat<R> to_mat(const double* x, long n1, long n2) {
+  Mat<R> m(n1, n2);
+  for (size_t i = 0; i < m.a.size(); ++i) m.a[i] = R(x[i]);
   return m;
 }
-static void from_mat(const Mat& m, double* y) { std::memcpy(y, m.a.data(), sizeof(double) * m.a.size()); }
+template <class R> static void from_mat(const Mat<R>& m, double* y) {
+  for (size_t i = 0; i < m.a.size(); ++i) y[i] = double(m.a[i]);
+}
 
 extern "C" {
 
 const char* orc_last_error(void) { return g_err.c_str(); }
 
-int orc_fft(double* re_im, int n, int sign) {
-  ORC_TRY(fft(reinterpret_cast<cd*>(re_im), n, sign));
+// Worker threads for the line-parallel 2D passes (results do not depend on it).
+int orc_set_threads(int n) {
+  g_threads.store(std::max(1, n));
+  return 0;
+}
+int orc_get_threads(void) { return g_threads.load(); }
+int orc_set_kernel_cache(int on) {
+  g_kernel_cache.store(on ? 1 : 0);
+  return 0;
 }
 
-int orc_psf_check(const double* taps, int q1, int q2) { ORC_TRY(make_psf(taps, q1, q2)); }
+int orc_fft(double* re_im, int n, int sign) {
+  ORC_TRY(fft(reinterpret_cast<Cx<double>*>(re_im), n, sign));
+}
+
+// long-double FFT of FP64 input (rounded back): the FFT floor check
+int orc_fft_ld(double* re_im, int n, int sign) {
+  ORC_TRY({
+    std::vector<Cx<long double>> z((size_t)n);
+    for (int i = 0; i < n; ++i) z[(size_t)i] = {re_im[2 * i], re_im[2 * i + 1]};
+    fft(z.data(), n, sign);
+    for (int i = 0; i < n; ++i) {
+      re_im[2 * i] = double(z[(size_t)i].re);
+      re_im[2 * i + 1] = double(z[(size_t)i].im);
+    }
+  });
+}
+
+int orc_psf_check(const double* taps, int q1, int q2) { ORC_TRY(make_psf<double>(taps, q1, q2)); }
 
 int orc_symmetrize(const double* taps, int q1, int q2, double* out) {
-  ORC_TRY(from_mat(symmetrize(make_psf(taps, q1, q2)).t, out));
+  ORC_TRY(from_mat(symmetrize(make_psf<double>(taps, q1, q2)).t, out));
 }
 
 int orc_pad_ar(const double* f, int n1, int n2, int q1, int q2, double* out) {
   ORC_TRY(from_mat(pad_ar(to_mat(f, n1, n2), q1, q2), out));
 }
 
-// path: 0 auto (reference cutover q<=7 direct), 1 direct, 2 fft
-int orc_apply(const double* taps, int q1, int q2, const double* f, int n1, int n2, int adjoint,
-              int path, double* out) {
+// path: 0 auto (reference cutover q<=7 direct), 1 direct, 2 fft; prec: 0 FP64, 1 long double
+int orc_apply_p(const double* taps, int q1, int q2, const double* f, int n1, int n2, int adjoint, int path, int bc,
+                int prec, double* out) {
   ORC_TRY({
-    Psf p = make_psf(taps, q1, q2);
+    require(bc == kReflective || bc == kAntiReflective, "apply: unsupported boundary condition");
     require(n1 >= 1 && n2 >= 1, "BlurOperator: empty field of view");
-    check_support_ar(n1, n2, q1, q2);
-    if (adjoint) p = rotate180(p);
-    from_mat(apply(p, to_mat(f, n1, n2), path), out);
+    if (bc == kAntiReflective) check_support_ar(n1, n2, q1, q2);
+    if (prec) {
+      Psf<long double> p = make_psf<long double>(taps, q1, q2);
+      if (adjoint) p = rotate180(p);
+      from_mat(apply(p, to_mat<long double>(f, n1, n2), path, bc), out);
+    } else {
+      PsfD p = make_psf<double>(taps, q1, q2);
+      if (adjoint) p = rotate180(p);
+      from_mat(apply(p, to_mat(f, n1, n2), path, bc), out);
+    }
   });
+}
+
+int orc_apply(const double* taps, int q1, int q2, const double* f, int n1, int n2, int adjoint, int path,
+              double* out) {
+  return orc_apply_p(taps, q1, q2, f, n1, n2, adjoint, path, kAntiReflective, 0, out);
 }
 
 int orc_sine1(const double* v, int m, double* y) { ORC_TRY(sine1_forward(v, y, m)); }
 
 int orc_ar_1d(int inverse, const double* v, int m, double* y) {
   ORC_TRY({
-    ArT t = make_ar_transform(m);
+    ArT<double> t = make_ar_transform<double>(m);
     if (inverse) ar_inverse(t, v, y);
     else ar_forward(t, v, y);
   });
@@ -713,22 +1015,27 @@ int orc_ar_1d(int inverse, const double* v, int m, double* y) {
 
 int orc_ar_alpha(int m, double* alpha, double* p) {
   ORC_TRY({
-    ArT t = make_ar_transform(m);
+    ArT<double> t = make_ar_transform<double>(m);
     *alpha = t.alpha;
     if (p) std::memcpy(p, t.p.data(), sizeof(double) * t.p.size());
   });
 }
 
-int orc_tensor_apply(int kind, const double* x, int n1, int n2, double* y) {
+int orc_tensor_apply_p(int kind, const double* x, int n1, int n2, int prec, double* y) {
   ORC_TRY({
     require(kind == kSineI || kind == kAR || kind == kARInv || kind == kCosineIII || kind == -kCosineIII,
             "tensor_apply: unsupported kind");
-    from_mat(tensor_apply(kind, to_mat(x, n1, n2)), y);
+    if (prec) from_mat(tensor_apply(kind, to_mat<long double>(x, n1, n2)), y);
+    else from_mat(tensor_apply(kind, to_mat(x, n1, n2)), y);
   });
 }
 
+int orc_tensor_apply(int kind, const double* x, int n1, int n2, double* y) {
+  return orc_tensor_apply_p(kind, x, n1, n2, 0, y);
+}
+
 int orc_eig_antireflective(const double* taps, int q1, int q2, int n1, int n2, double* eigs) {
-  ORC_TRY(from_mat(eig_antireflective(make_psf(taps, q1, q2), n1, n2), eigs));
+  ORC_TRY(from_mat(eig_antireflective(make_psf<double>(taps, q1, q2), n1, n2), eigs));
 }
 
 int orc_tikhonov_filter(const double* eigs, int n1, int n2, double alpha, double* d) {
@@ -736,11 +1043,20 @@ int orc_tikhonov_filter(const double* eigs, int n1, int n2, double alpha, double
 }
 
 int orc_build_tikhonov(const double* taps, int q1, int q2, int n1, int n2, double alpha, double* d) {
-  ORC_TRY(from_mat(build_tikhonov(make_psf(taps, q1, q2), alpha, n1, n2), d));
+  ORC_TRY(from_mat(build_tikhonov(make_psf<double>(taps, q1, q2), alpha, n1, n2), d));
 }
 
 int orc_precondition_apply(const double* d, const double* r, int n1, int n2, double* y) {
   ORC_TRY(from_mat(filter_apply_ar(to_mat(d, n1, n2), to_mat(r, n1, n2)), y));
+}
+
+// long-double D applied with the long-double filter rebuilt from the taps
+int orc_precondition_apply_ld(const double* taps, int q1, int q2, double alpha, const double* r, int n1, int n2,
+                              double* y) {
+  ORC_TRY({
+    const Mat<long double> D = build_tikhonov(make_psf<long double>(taps, q1, q2), (long double)alpha, n1, n2);
+    from_mat(filter_apply_ar(D, to_mat<long double>(r, n1, n2)), y);
+  });
 }
 
 int orc_add_noise(const double* g, int n1, int n2, double level, uint64_t seed, double* out) {
@@ -748,9 +1064,6 @@ int orc_add_noise(const double* g, int n1, int n2, double level, uint64_t seed, 
 }
 
 double orc_rre(const double* x, const double* f, long n) { return rre(x, f, size_t(n)); }
-
-// solver.hpp:17-32 StoppingRule kinds
-enum { STOP_FIXED = 0, STOP_MINRRE = 1, STOP_RESID = 2 };
 
 // solver.hpp:63-132 landweber_loop (+ 139-148).  d == NULL -> plain
 // Landweber.  x_hist (nullable) receives every iterate x_k, k = 1..executed.
@@ -762,52 +1075,22 @@ int orc_landweber_bc(const double* taps, int q1, int q2, int n1, int n2, const d
                      double* x_hist) {
   *iters_done = 0;
   *best_iter = 0;
-  ORC_TRY({
-    Psf p = make_psf(taps, q1, q2);
-    require(n1 >= 1 && n2 >= 1, "BlurOperator: empty field of view");
-    require(bc == kReflective || bc == kAntiReflective, "landweber: unsupported boundary condition");
-    if (bc == kReflective) check_support_refl(n1, n2, q1, q2);
-    else check_support_ar(n1, n2, q1, q2);
-    require(tau > 0.0, "landweber: tau must be positive");
-    require(max_iters >= 1, "landweber: max_iters must be at least 1");
-    require(stop_kind != STOP_FIXED || fixed_iters >= 0, "StoppingRule: negative iteration count");
-    require(stop_kind != STOP_RESID || resid_eps > 0.0, "StoppingRule: threshold must be positive");
-    const size_t N = size_t(n1) * size_t(n2);
-    const int total = stop_kind == STOP_FIXED ? fixed_iters : max_iters;
-    const Mat G = to_mat(g, n1, n2);
-    const double g_norm = fro(g, N);
-    const double guard = 1e8 * g_norm;
-    const Psf rot = rotate180(p);
-    Mat D;
-    if (d) D = to_mat(d, n1, n2);
-    Mat x(n1, n2), best(n1, n2), r = G;
-    double best_rre = std::numeric_limits<double>::infinity();
-    for (int k = 1; k <= total; ++k) {
-      Mat step = apply(rot, r, conv_path, bc);
-      if (d) step = bc == kReflective ? filter_apply_cos(D, step) : filter_apply_ar(D, step);
-      for (size_t i = 0; i < N; ++i) x.a[i] += tau * step.a[i];
-      const Mat ax = apply(p, x, conv_path, bc);
-      for (size_t i = 0; i < N; ++i) r.a[i] = G.a[i] - ax.a[i];
-      if (fro(x.a.data(), N) > guard && g_norm > 0.0)
-        throw std::runtime_error("landweber: iterate exceeded 1e8 * ||g||");
-      const double rn = fro(r.a.data(), N);
-      res_hist[k - 1] = rn;
-      if (f_true) {
-        const double e = rre(x.a.data(), f_true, N);
-        rre_hist[k - 1] = e;
-        if (e < best_rre) {
-          best_rre = e;
-          *best_iter = k;
-          if (stop_kind == STOP_MINRRE) best = x;
-        }
-      }
-      if (x_hist) std::memcpy(x_hist + size_t(k - 1) * N, x.a.data(), N * sizeof(double));
-      *iters_done = k;
-      if (stop_kind == STOP_RESID && g_norm > 0.0 && rn / g_norm < resid_eps) break;
-    }
-    const Mat& out = (stop_kind == STOP_MINRRE && f_true && *best_iter > 0) ? best : x;
-    from_mat(out, restored);
-  });
+  ORC_TRY(landweber_loop<double>(taps, q1, q2, n1, n2, d, -1.0, g, f_true, tau, max_iters, stop_kind, fixed_iters,
+                                 resid_eps, conv_path, bc, restored, rre_hist, res_hist, best_iter, iters_done,
+                                 x_hist));
+}
+
+// The same loop in long double (64-bit mantissa).  alpha >= 0: D-Landweber
+// with the filter rebuilt in long double from the taps; alpha < 0: plain.
+int orc_landweber_ld(const double* taps, int q1, int q2, int n1, int n2, double alpha, const double* g,
+                     const double* f_true, double tau, int max_iters, int stop_kind, int fixed_iters,
+                     double resid_eps, int conv_path, int bc, double* restored, double* rre_hist, double* res_hist,
+                     int* best_iter, int* iters_done, double* x_hist) {
+  *iters_done = 0;
+  *best_iter = 0;
+  ORC_TRY(landweber_loop<long double>(taps, q1, q2, n1, n2, nullptr, alpha, g, f_true, tau, max_iters, stop_kind,
+                                      fixed_iters, resid_eps, conv_path, bc, restored, rre_hist, res_hist, best_iter,
+                                      iters_done, x_hist));
 }
 
 int orc_landweber(const double* taps, int q1, int q2, int n1, int n2, const double* d,
@@ -824,7 +1107,7 @@ int orc_apply_bc(const double* taps, int q1, int q2, const double* f, int n1, in
                  int bc, double* out) {
   ORC_TRY({
     require(bc == kReflective || bc == kAntiReflective, "apply: unsupported boundary condition");
-    Psf p = make_psf(taps, q1, q2);
+    PsfD p = make_psf<double>(taps, q1, q2);
     if (adjoint) p = rotate180(p);
     from_mat(apply(p, to_mat(f, n1, n2), path, bc), out);
   });
@@ -833,14 +1116,14 @@ int orc_apply_bc(const double* taps, int q1, int q2, const double* f, int n1, in
 int orc_build_tikhonov_bc(const double* taps, int q1, int q2, int n1, int n2, double alpha, int bc, double* d) {
   ORC_TRY({
     require(bc == kReflective || bc == kAntiReflective, "build_tikhonov: unsupported boundary condition");
-    const Psf p = make_psf(taps, q1, q2);
+    const PsfD p = make_psf<double>(taps, q1, q2);
     from_mat(bc == kReflective ? build_tikhonov_cos(p, alpha, n1, n2) : build_tikhonov(p, alpha, n1, n2), d);
   });
 }
 
 int orc_precondition_apply_bc(const double* d, const double* r, int n1, int n2, int bc, double* y) {
   ORC_TRY({
-    const Mat D = to_mat(d, n1, n2), R = to_mat(r, n1, n2);
+    const MatD D = to_mat(d, n1, n2), R = to_mat(r, n1, n2);
     from_mat(bc == kReflective ? filter_apply_cos(D, R) : filter_apply_ar(D, R), y);
   });
 }

@@ -37,6 +37,14 @@ def build() -> str:
     return _LIB_PATH
 
 
+def gen_lib_path() -> str:
+    """Host-only build of the input generators (csrc/gen.cpp), see Makefile."""
+    path = os.path.join(_HERE, "build", "liborcgen.so")
+    if not os.path.exists(path):
+        build()
+    return path
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -48,6 +56,23 @@ def lib():
         _lib.orc_rre.argtypes = [C.c_void_p, C.c_void_p, C.c_long]
         _lib.orc_add_noise.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_void_p]
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """Worker threads for the line-parallel 2D passes; results are
+    bit-identical for any count (each line's arithmetic is unchanged)."""
+    lib().orc_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().orc_get_threads())
+
+
+def set_kernel_cache(on: bool) -> None:
+    """Keep the (bit-identical) mask spectrum between correlation calls
+    instead of recomputing it as the reference does (blur.hpp:65-66); tests
+    use it to shorten long trajectories, timing legs leave it off."""
+    lib().orc_set_kernel_cache(int(bool(on)))
 
 
 def _p(a: np.ndarray):
@@ -102,12 +127,16 @@ BC_REFLECTIVE, BC_ANTIREFLECTIVE = 2, 3  # BoundaryCondition order, boundary.hpp
 KIND_COSINE3 = 1  # TransformKind::CosineIII (forward R); -1 in tensor_apply = R^T
 
 
-def apply(taps, f, adjoint=False, path=0, bc=BC_ANTIREFLECTIVE):
-    """blur.hpp:75-83 (adjoint=True: apply_reblur_adjoint, blur.hpp:87-90)."""
+def apply(taps, f, adjoint=False, path=0, bc=BC_ANTIREFLECTIVE, long_double=False):
+    """blur.hpp:75-83 (adjoint=True: apply_reblur_adjoint, blur.hpp:87-90).
+    long_double=True computes in long double (the FP64 rounding floor)."""
     taps, q1, q2 = _q(taps)
     f = _f64(f)
     out = np.empty_like(f)
-    if bc == BC_ANTIREFLECTIVE:
+    if long_double:
+        _check(lib().orc_apply_p(_p(taps), q1, q2, _p(f), f.shape[0], f.shape[1], int(adjoint), int(path), bc, 1,
+                                 _p(out)))
+    elif bc == BC_ANTIREFLECTIVE:
         _check(lib().orc_apply(_p(taps), q1, q2, _p(f), f.shape[0], f.shape[1], int(adjoint), int(path), _p(out)))
     else:
         _check(lib().orc_apply_bc(_p(taps), q1, q2, _p(f), f.shape[0], f.shape[1], int(adjoint), int(path), bc,
@@ -151,10 +180,20 @@ def make_ar_transform(m):
     return alpha.value, p
 
 
-def tensor_apply(kind, x):
+def tensor_apply(kind, x, long_double=False):
     x = _f64(x)
     y = np.empty_like(x)
-    _check(lib().orc_tensor_apply(kind, _p(x), x.shape[0], x.shape[1], _p(y)))
+    _check(lib().orc_tensor_apply_p(kind, _p(x), x.shape[0], x.shape[1], int(bool(long_double)), _p(y)))
+    return y
+
+
+def precondition_apply_ld(taps, alpha, r):
+    """D r in long double with the filter rebuilt in long double from the taps."""
+    taps, q1, q2 = _q(taps)
+    r = _f64(r)
+    y = np.empty_like(r)
+    _check(lib().orc_precondition_apply_ld(_p(taps), q1, q2, C.c_double(alpha), _p(r), r.shape[0], r.shape[1],
+                                           _p(y)))
     return y
 
 
@@ -262,8 +301,14 @@ def cgls(taps, g, d=None, f_true=None, max_iters=100, stop=STOP_MINRRE, fixed_it
 
 
 def landweber(taps, g, d=None, f_true=None, tau=1.0, max_iters=100, stop=STOP_MINRRE,
-              fixed_iters=0, resid_eps=0.0, conv_path=0, keep_iterates=False, bc=BC_ANTIREFLECTIVE):
-    """solver.hpp:63-148.  Returns a dict shaped like RestorationRun."""
+              fixed_iters=0, resid_eps=0.0, conv_path=0, keep_iterates=False, bc=BC_ANTIREFLECTIVE,
+              long_double_alpha=None):
+    """solver.hpp:63-148.  Returns a dict shaped like RestorationRun.
+
+    long_double_alpha: run the same loop in long double instead (the FP64
+    rounding-floor reference); None -> FP64 oracle,
+    a value >= 0 -> D-Landweber with the filter rebuilt in long double for
+    that alpha, a negative value -> plain Landweber.  ``d`` must be None then."""
     taps, q1, q2 = _q(taps)
     g = _f64(g)
     n1, n2 = g.shape
@@ -277,11 +322,19 @@ def landweber(taps, g, d=None, f_true=None, tau=1.0, max_iters=100, stop=STOP_MI
     xh = np.empty((hist, n1, n2)) if keep_iterates else None
     dd = _f64(d) if d is not None else None
     ft = _f64(f_true) if f_true is not None else None
-    st = lib().orc_landweber_bc(
-        _p(taps), q1, q2, n1, n2, _p(dd) if dd is not None else None, _p(g),
-        _p(ft) if ft is not None else None, C.c_double(tau), max_iters, stop, fixed_iters,
-        C.c_double(resid_eps), conv_path, bc, _p(restored), _p(rre_h), _p(res_h), C.byref(best),
-        C.byref(done), _p(xh) if xh is not None else None)
+    if long_double_alpha is not None:
+        if dd is not None:
+            raise ValueError("landweber: pass either d or long_double_alpha")
+        st = lib().orc_landweber_ld(
+            _p(taps), q1, q2, n1, n2, C.c_double(long_double_alpha), _p(g), _p(ft) if ft is not None else None,
+            C.c_double(tau), max_iters, stop, fixed_iters, C.c_double(resid_eps), conv_path, bc, _p(restored),
+            _p(rre_h), _p(res_h), C.byref(best), C.byref(done), _p(xh) if xh is not None else None)
+    else:
+        st = lib().orc_landweber_bc(
+            _p(taps), q1, q2, n1, n2, _p(dd) if dd is not None else None, _p(g),
+            _p(ft) if ft is not None else None, C.c_double(tau), max_iters, stop, fixed_iters,
+            C.c_double(resid_eps), conv_path, bc, _p(restored), _p(rre_h), _p(res_h), C.byref(best),
+            C.byref(done), _p(xh) if xh is not None else None)
     _check(st)
     k = done.value
     return {

@@ -79,6 +79,7 @@ def lib():
         L.dbx_landweber_run_chunks.argtypes = [vp, i, vp, vp, d, i, i, i, d, i, vp, vp, vp, vp, vp]
         L.dbx_plan_set_timing.argtypes = [vp, i]
         L.dbx_plan_kernel_times.argtypes = [vp, vp, vp, i]
+        L.dbx_plan_kernel_profile.argtypes = [vp, i, C.c_char_p, i, C.POINTER(d), C.POINTER(i)]
         L.dbx_plan_launch_count.argtypes = [vp]
         L.dbx_plan_launch_count.restype = C.c_int64
         L.dbx_gen_scene.argtypes = [i, i, i, d, C.c_uint64, vp]
@@ -250,7 +251,6 @@ class BlurOperator:
             raise ValueError("anti-reflective support condition violated (q > n-2)")
         self._psf, self._bc, self.n1, self.n2, self.batch = psf, bc, n1, n2, batch
         self._plan = _Plan(n1, n2, batch, psf.taps(), psf.q1, psf.q2, device, bc)
-        self._eigs_id = None
 
     def psf(self):
         return self._psf
@@ -493,9 +493,10 @@ def _run(op: BlurOperator, d: Optional[FilteredOperator], g, cfg: SolverConfig, 
             raise ValueError("d_landweber: preconditioner size mismatch")
         if _ALGEBRA_BC.get(d.algebra) != op.bc():
             raise ValueError("d_landweber: preconditioner algebra does not match the BC")
-        if op._eigs_id is not id(d):
-            _check(lib().dbx_precond_set_eigs(op.handle, _ptr(d.eigs)))
-            op._eigs_id = id(d)
+        # the plan keeps one filter grid: always load this operator's (no
+        # identity cache: d.eigs may have been edited in place, and object
+        # ids are reused after garbage collection)
+        _check(lib().dbx_precond_set_eigs(op.handle, _ptr(d.eigs)))
     stop = cfg.stop
     total = stop.fixed_iterations if stop.kind == StoppingRuleKind.FixedIterations else cfg.max_iters
     H = max(total, 1)
@@ -566,9 +567,7 @@ def landweber_chunks(ops, g, cfg: SolverConfig, d: Optional[FilteredOperator] = 
             raise ValueError("landweber: true image size mismatch")
     if d is not None:
         for op in ops:
-            if op._eigs_id is not id(d):
-                _check(lib().dbx_precond_set_eigs(op.handle, _ptr(d.eigs)))
-                op._eigs_id = id(d)
+            _check(lib().dbx_precond_set_eigs(op.handle, _ptr(d.eigs)))
     stop = cfg.stop
     total = stop.fixed_iterations if stop.kind == StoppingRuleKind.FixedIterations else cfg.max_iters
     H = max(total, 1)

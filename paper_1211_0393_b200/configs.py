@@ -55,16 +55,49 @@ CONFIGS = {
 }
 
 
+_GEN_LIB = None
+
+
+def use_generator_library(path: Optional[str]) -> None:
+    """Generate inputs through another build of csrc/gen.cpp (same source,
+    same bytes out).  bench.py's reference arm points this at the oracle's own
+    copy (oracle/build/liborcgen.so) so that the CPU-only arm never maps the
+    product library libdbx.so; None restores the default."""
+    global _GEN_LIB
+    if path is None:
+        _GEN_LIB = None
+        return
+    import ctypes as C
+    L = C.CDLL(path)
+    vp, i, d = C.c_void_p, C.c_int, C.c_double
+    L.dbx_gen_scene.argtypes = [i, i, i, d, C.c_uint64, vp]
+    L.dbx_gen_psf_gaussian.argtypes = [i, i, d, d, d, d, d, vp]
+    L.dbx_gen_psf_motion.argtypes = [i, i, d, d, d, vp]
+    L.dbx_gen_honest.argtypes = [vp, i, i, vp, i, i, i, i, d, C.c_uint64, i, vp, vp]
+    _GEN_LIB = L
+
+
+def _gen():
+    from . import _ptr, lib
+    if _GEN_LIB is not None:
+        def check(st):
+            if st != 0:
+                raise ValueError(f"input generator: invalid argument (status {st})")
+        return _GEN_LIB, check, _ptr
+    from . import _check
+    return lib(), _check, _ptr
+
+
 def make_psf(cfg: Config, q: Optional[int] = None) -> np.ndarray:
-    from . import _check, _ptr, lib
+    L, _check, _ptr = _gen()
     q = cfg.q if q is None else q
     t = np.empty((2 * q + 1, 2 * q + 1))
     if cfg.psf_kind == "gauss":
-        _check(lib().dbx_gen_psf_gaussian(q, q, cfg.sigma[0], cfg.sigma[1], cfg.theta_deg,
-                                          cfg.offset[0], cfg.offset[1], _ptr(t)))
+        _check(L.dbx_gen_psf_gaussian(q, q, cfg.sigma[0], cfg.sigma[1], cfg.theta_deg,
+                                      cfg.offset[0], cfg.offset[1], _ptr(t)))
     else:
-        L, ang, tail = cfg.motion
-        _check(lib().dbx_gen_psf_motion(q, q, L, ang, tail, _ptr(t)))
+        length, ang, tail = cfg.motion
+        _check(L.dbx_gen_psf_motion(q, q, length, ang, tail, _ptr(t)))
     return t
 
 
@@ -75,17 +108,17 @@ def scene_seed(cfg: Config, image: int) -> int:
 def make_problem(cfg: Config, image: int = 0, n: Optional[int] = None, threads: int = 0):
     """Returns (f_true, g, taps) for one image of the config.  ``n`` overrides
     the FOV size (scaled-down parity cases keep the mask, shapes and noise)."""
-    from . import _check, _ptr, lib
+    L, _check, _ptr = _gen()
     n = cfg.n if n is None else n
     taps = make_psf(cfg)
     canvas = n + 2 * (2 * cfg.q + 1)
     scene = np.empty((canvas, canvas))
     s = scene_seed(cfg, image)
-    _check(lib().dbx_gen_scene(canvas, canvas, cfg.shapes, cfg.sinus_amp, s, _ptr(scene)))
+    _check(L.dbx_gen_scene(canvas, canvas, cfg.shapes, cfg.sinus_amp, s, _ptr(scene)))
     f = np.empty((n, n))
     g = np.empty((n, n))
-    _check(lib().dbx_gen_honest(_ptr(scene), canvas, canvas, _ptr(taps), cfg.q, cfg.q, n, n,
-                                cfg.noise, s ^ 0x5DEECE66D, threads, _ptr(f), _ptr(g)))
+    _check(L.dbx_gen_honest(_ptr(scene), canvas, canvas, _ptr(taps), cfg.q, cfg.q, n, n,
+                            cfg.noise, s ^ 0x5DEECE66D, threads, _ptr(f), _ptr(g)))
     return f, g, taps
 
 

@@ -168,11 +168,8 @@ void launch_blur(const BlurArgs& a, cudaStream_t s, int* ctas_per_image) {
   const size_t smem =
       sizeof(double) * ((size_t)(kTH + 2 * a.q1) * (kTW + 2 * a.q2) +
                         (size_t)(2 * a.q1 + 1) * (2 * a.q2 + 1) + kWarps);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(blur_ar_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
+  static AttrOnce attr;
+  attr.ensure(blur_ar_kernel, 227 * 1024);
   if (ctas_per_image) *ctas_per_image = grid.x * grid.y;
   blur_ar_kernel<<<grid, kThreads, smem, s>>>(a);
 }

@@ -71,6 +71,9 @@ int guarded(F&& f) {
   }
 }
 
+// Device (or managed) memory usable in place by kernels on the CURRENT device
+// (every entry point calls set_dev() first).  Device memory of another GPU
+// is refused instead of being read through peer mappings or faulting.
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes at;
@@ -78,7 +81,15 @@ bool is_device_ptr(const void* p) {
     cudaGetLastError();
     return false;
   }
-  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+  if (at.type == cudaMemoryTypeDevice) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (at.device != cur)
+      throw InvalidArg("device pointer on GPU " + std::to_string(at.device) + ", plan on GPU " +
+                       std::to_string(cur));
+    return true;
+  }
+  return at.type == cudaMemoryTypeManaged;
 }
 
 struct DevBuf {
@@ -193,8 +204,10 @@ std::vector<double> transpose(const std::vector<double>& a, long n) {
 
 // Launcher result check: a negative CTA count means the size is not compiled
 // or its shared-memory plan does not fit this device.
+thread_local const char* t_last_kernel = nullptr;  // name of the last lc() launch (per-kernel timing)
 inline int lc(int rc, const char* what) {
   if (rc < 0) throw CudaErr(std::string(what) + ": launch configuration unsupported on this device");
+  t_last_kernel = what;
   return rc;
 }
 
@@ -215,6 +228,7 @@ struct dbx_plan {
   double* d = nullptr;     // filter grid (one shared, or one per image for an alpha sweep)
   size_t d_cap = 0;        // doubles allocated at d
   size_t dstride = 0;      // 0: shared grid; N: per-image grids (dbx_precond_build_sweep)
+  uint64_t dgen = 0;       // filter generation (part of the graph-cache key)
   bool have_d = false;
   int conv = DBX_CONV_AUTO;
   // dense transform matrices [kind][0 col-matrix (n1), 1 row-matrix^T (n2)]
@@ -229,6 +243,8 @@ struct dbx_plan {
   std::vector<cudaEvent_t> evpool;
   size_t evused = 0;
   std::vector<std::pair<int, size_t>> evrecs;
+  std::vector<const char*> evnames;                       // kernel name per record (lc() name, else the class)
+  std::vector<std::pair<std::string, std::pair<double, int>>> kprof;  // per kernel name: ms, launches
   // graph cache
   cudaGraphExec_t gexec = nullptr;
   std::string gkey;
@@ -487,6 +503,7 @@ struct dbx_plan {
   void set_dev() const { ck(cudaSetDevice(device), "cudaSetDevice"); }
 
   void ensure_d(size_t count) {
+    ++dgen;  // every filter (re)build: captured graphs bake d, dT and dstride in
     if (d && d_cap >= count) return;
     if (d) cudaFree(d);
     d = nullptr;
@@ -529,22 +546,32 @@ struct dbx_plan {
     ck(cudaEventRecord(evpool[evused], stream), "cudaEventRecord");
     evrecs.push_back({cls, evused});
     evused += 2;
+    t_last_kernel = nullptr;
   }
   void ev_end() {
     if (!timing) return;
     ck(cudaEventRecord(evpool[evrecs.back().second + 1], stream), "cudaEventRecord");
+    static const char* cls_name[KC_NUM] = {"blur_adjoint", "blur", "ar_transform", "finalize"};
+    evnames.push_back(t_last_kernel ? t_last_kernel : cls_name[evrecs.back().first]);
   }
   void ev_collect() {
     if (!timing) return;
     ck(cudaStreamSynchronize(stream), "sync");
     for (int i = 0; i < KC_NUM; ++i) kms[i] = 0.0, kcount[i] = 0;
-    for (auto& rc : evrecs) {
+    kprof.clear();
+    for (size_t i = 0; i < evrecs.size(); ++i) {
+      const auto& rc = evrecs[i];
       float ms = 0.f;
       ck(cudaEventElapsedTime(&ms, evpool[rc.second], evpool[rc.second + 1]), "elapsed");
       kms[rc.first] += ms;
       kcount[rc.first] += 1;
+      const std::string nm = std::string(i < evnames.size() ? evnames[i] : "?") + "#" + std::to_string(rc.first);
+      auto it = std::find_if(kprof.begin(), kprof.end(), [&](const auto& e) { return e.first == nm; });
+      if (it == kprof.end()) kprof.push_back({nm, {(double)ms, 1}});
+      else it->second.first += ms, it->second.second += 1;
     }
     evrecs.clear();
+    evnames.clear();
     evused = 0;
   }
 
@@ -922,6 +949,21 @@ int dbx_plan_kernel_times(dbx_plan* plan, double* ms, int* launches, int max_cla
     if (launches) launches[i] = plan->kcount[i];
   }
   return KC_NUM;
+}
+
+int dbx_plan_kernel_profile(dbx_plan* plan, int idx, char* name, int name_cap, double* ms, int* launches) {
+  if (!plan) return 0;
+  const int n = (int)plan->kprof.size();
+  if (idx >= 0 && idx < n) {
+    const auto& e = plan->kprof[(size_t)idx];
+    if (name && name_cap > 0) {
+      std::strncpy(name, e.first.c_str(), (size_t)name_cap - 1);
+      name[name_cap - 1] = 0;
+    }
+    if (ms) *ms = e.second.first;
+    if (launches) *launches = e.second.second;
+  }
+  return n;
 }
 
 int64_t dbx_plan_launch_count(dbx_plan* plan) { return plan ? plan->launches : 0; }
@@ -1561,10 +1603,11 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
     if (total > 0) {
       // Graph path: one graph per run shape, replayed; kernels read the run's
       // buffers through stable plan-owned pointers.
-      char key[512];
-      snprintf(key, sizeof key, "%d|%d|%d|%.17g|%.17g|%d|%d|%p|%p|%d|%d|%d|%d", total, use_precond,
+      char key[640];
+      snprintf(key, sizeof key, "%d|%d|%d|%.17g|%.17g|%d|%d|%p|%p|%d|%d|%d|%d|%p|%p|%zu|%llu", total, use_precond,
                stop_kind, resid_eps, tau, (int)track, (int)want_xh, (const void*)gd,
-               (const void*)fd, P->conv, P->dst, (int)fused, method);
+               (const void*)fd, P->conv, P->dst, (int)fused, method, (const void*)P->d, (const void*)P->dT.p,
+               P->dstride, (unsigned long long)P->dgen);
       const bool use_graph = !P->timing;
       if (use_graph) {
         if (!P->gexec || P->gkey != key) {
@@ -1648,6 +1691,11 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
         div_k = h.diverged_at;
       }
     }
+    // rre() throws on a zero true image (image.hpp:89); the device loop ran
+    // with ||f|| = 0, so its histories are meaningless: report the reference's
+    // error instead of returning them
+    if (track && total > 0)
+      for (int b = 0; b < B; ++b) require(hs[(size_t)b].f_norm > 0.0, "rre: zero true image");
     if (div_img >= 0) {
       char msg[160];
       snprintf(msg, sizeof msg, "landweber: iterate exceeded 1e8 * ||g|| (image %d, iteration %d)",

@@ -5,10 +5,33 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
 namespace dbx {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: one bit per
+// device ordinal, set on the first launch on that device.  Thread-safe
+// (racing first launches both set the attribute, which is idempotent), so
+// plans on several GPUs in one process, and the chunk worker threads of
+// dbx_landweber_run_chunks, all see the attribute on their own device.
+struct AttrOnce {
+  std::atomic<unsigned long long> done{0};
+  template <typename K>
+  bool ensure(K kernel, size_t bytes) {
+    if (bytes > 227 * 1024) return false;
+    if (bytes <= 48 * 1024) return true;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return true;
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+      return false;
+    done.fetch_or(bit, std::memory_order_acq_rel);
+    return true;
+  }
+};
 
 // Per-image iteration state, resident in HBM for the whole run.  The three
 // iterate buffers X[0..2] are used round-robin so that tracking the best

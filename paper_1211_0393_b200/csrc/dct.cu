@@ -150,11 +150,8 @@ __global__ void __launch_bounds__(DctCfg<M>::NT) dct_rows(SpecArgs a) {
 template <int L>
 int dct_launch(const SpecArgs& a, cudaStream_t s) {
   using C = DctCfg<L>;
-  static bool init = false;
-  if (!init) {
-    if (!set_smem(dct_rows<L>, C::bytes)) return -1;
-    init = true;
-  }
+  static AttrOnce attr;
+  if (!attr.ensure(dct_rows<L>, C::bytes)) return -1;
   dim3 grid((a.n1 + 2 * C::G - 1) / (2 * C::G), a.batch);
   dct_rows<L><<<grid, C::NT, C::bytes, s>>>(a);
   return (int)grid.x;

@@ -343,11 +343,8 @@ __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_cols(SpecArgs a) {
 template <int L, int CORE>
 int rows_launch(const SpecArgs& a, cudaStream_t s) {
   using C = DstCfg<L, CORE>;
-  static bool init = false;
-  if (!init) {
-    if (!set_smem(dst_rows<L, CORE>, C::bytes)) return -1;
-    init = true;
-  }
+  static AttrOnce attr;
+  if (!attr.ensure(dst_rows<L, CORE>, C::bytes)) return -1;
   dim3 grid((a.n1 + 2 * C::G - 1) / (2 * C::G), a.batch);
   dst_rows<L, CORE><<<grid, C::NT, C::bytes, s>>>(a);
   return (int)grid.x;
@@ -356,11 +353,8 @@ int rows_launch(const SpecArgs& a, cudaStream_t s) {
 template <int L, int CORE>
 int cols_launch(const SpecArgs& a, cudaStream_t s) {
   using C = DstCfg<L, CORE>;
-  static bool init = false;
-  if (!init) {
-    if (!set_smem(dst_cols<L, CORE>, C::bytes)) return -1;
-    init = true;
-  }
+  static AttrOnce attr;
+  if (!attr.ensure(dst_cols<L, CORE>, C::bytes)) return -1;
   dim3 grid((a.n2 + 2 * C::G - 1) / (2 * C::G), a.batch);
   dst_cols<L, CORE><<<grid, C::NT, C::bytes, s>>>(a);
   return (int)grid.x;

@@ -726,11 +726,8 @@ int fused_launch(K kernel, const SpecArgs& a, cudaStream_t s) {
                            : (WHICH == 1 || WHICH == 5) ? F::ax_bytes : RsCfg<L2>::bytes;
   constexpr int nt = WHICH == 2 ? RsCfg<L2>::NT : F::NT;
   constexpr int rows = 4;  // rows per CTA
-  static bool init = false;
-  if (!init) {
-    if (!set_smem(kernel, bytes)) return -1;
-    init = true;
-  }
+  static AttrOnce attr;
+  if (!attr.ensure(kernel, bytes)) return -1;
   dim3 grid((a.n1 + rows - 1) / rows, a.batch);
   kernel<<<grid, nt, bytes, s>>>(a);
   return (int)grid.x;
@@ -739,11 +736,8 @@ int fused_launch(K kernel, const SpecArgs& a, cudaStream_t s) {
 template <int M, bool BLUE>
 int tcols_launch(const SpecArgs& a, cudaStream_t s) {
   using SMP = TcolSmem<M, BLUE>;
-  static bool init = false;
-  if (!init) {
-    if (!set_smem(dst_tcols<M, BLUE>, SMP::bytes)) return -1;
-    init = true;
-  }
+  static AttrOnce attr;
+  if (!attr.ensure(dst_tcols<M, BLUE>, SMP::bytes)) return -1;
   dim3 grid((a.n2 + 3) / 4, a.batch);
   dst_tcols<M, BLUE><<<grid, 2 * SMP::TD, SMP::bytes, s>>>(a);
   return (int)grid.x;

@@ -599,8 +599,8 @@ int launch_conv_row_fwd(const SpecArgs& a, cudaStream_t s) {
   if (L2 == (L)) {                                                                       \
     constexpr int T = line_threads(L, 8), G = lines_for(L, kConvBudget, 8);                     \
     const size_t sm = ConvSmem<L, G>::row_bytes;                                         \
-    static bool init = false;                                                            \
-    if (!init) { if (!set_smem(conv_row_fwd<L>, sm)) return -1; init = true; }                            \
+    static AttrOnce attr;                                                            \
+    if (!attr.ensure(conv_row_fwd<L>, sm)) return -1;                            \
     dim3 grid((a.n1 + 2 * G - 1) / (2 * G), a.batch);                                    \
     conv_row_fwd<L><<<grid, T * G, sm, s>>>(a);                                          \
     return (int)grid.x;                                                                  \
@@ -690,8 +690,8 @@ int launch_conv_col(const SpecArgs& a, cudaStream_t s) {
   if (L1 == (L)) {                                                                       \
     constexpr int T = line_threads(L, 8), G = lines_for(L, kConvBudget, 8);                     \
     const size_t sm = ConvSmem<L, G>::col_bytes;                                         \
-    static bool init = false;                                                            \
-    if (!init) { if (!set_smem(conv_col<L>, sm)) return -1; init = true; }                                \
+    static AttrOnce attr;                                                            \
+    if (!attr.ensure(conv_col<L>, sm)) return -1;                                \
     dim3 grid((a.conv.Lh + G - 1) / G, a.batch);                                         \
     conv_col<L><<<grid, T * G, sm, s>>>(a);                                              \
     return (int)grid.x;                                                                  \
@@ -707,8 +707,8 @@ int launch_conv_row_inv(const SpecArgs& a, cudaStream_t s) {
   if (L2 == (L)) {                                                                       \
     constexpr int T = line_threads(L, 8), G = lines_for(L, kConvBudget, 8);                     \
     const size_t sm = ConvSmem<L, G>::row_bytes;                                         \
-    static bool init = false;                                                            \
-    if (!init) { if (!set_smem(conv_row_inv<L>, sm)) return -1; init = true; }                            \
+    static AttrOnce attr;                                                            \
+    if (!attr.ensure(conv_row_inv<L>, sm)) return -1;                            \
     dim3 grid((a.n1 + 2 * G - 1) / (2 * G), a.batch);                                    \
     conv_row_inv<L><<<grid, T * G, sm, s>>>(a);                                          \
     return (int)grid.x;                                                                  \

@@ -193,7 +193,7 @@ class SlabLandweber:
 
     # ---- the loop ---------------------------------------------------------
     def run(self, g: Dict[int, "object"], f: Optional[Dict[int, "object"]], iters: int, tau: float = 1.0,
-            resid_eps: Optional[float] = None):
+            resid_eps: Optional[float] = None, on_iterate=None):
         """g, f: this process's slabs (device tensors rows x n).  Returns the
         restored slabs (best-RRE iterate when f is given, solver.hpp:127-131)
         and the global histories (identical on every rank)."""
@@ -203,6 +203,8 @@ class SlabLandweber:
         gn2 = self.world.allreduce({p: [float(torch.sum(g[p] * g[p]))] for p in S})[0]
         fn2 = self.world.allreduce({p: [float(torch.sum(f[p] * f[p]))] for p in S})[0] if f else 0.0
         gnorm, fnorm = math.sqrt(gn2), math.sqrt(fn2)
+        if f and not fnorm > 0.0:
+            raise ValueError("rre: zero true image")  # image.hpp:89
         for p, s in S.items():
             s.x.zero_()
             s.r.copy_(g[p])
@@ -250,6 +252,8 @@ class SlabLandweber:
                         s.best.copy_(s.x)
                     self._fence()
             done = k
+            if on_iterate is not None:  # tests: every iterate x_k, this process's slabs
+                on_iterate(k, {p: s.x for p, s in S.items()})
             if resid_eps is not None and gnorm > 0.0 and math.sqrt(rr) / gnorm < resid_eps:
                 break
         restored = {p: (s.best if (f and best_iter > 0) else s.x).clone() for p, s in S.items()}

@@ -105,6 +105,32 @@ def fused_sep_classes(n: int, q: int, images: int) -> dict:
     }
 
 
+def fused_sep_kernels(n: int, q: int, images: int) -> dict:
+    """Per-kernel, per-launch algorithmic work of the separable fused
+    pipeline (the C3 bench path), keyed by the launcher names dbx_api.cu
+    reports through dbx_plan_kernel_profile ("name#class").  Bytes per
+    pixel per image (8-byte reals, every array read / written once):
+
+      cols_sep_real (A')  Z'^T -> Y' = A'r                      16
+      rows_tt_sep         Y' -> T~ rows -> u^T                   16
+      dst_tcols           u^T -> T~ cols, x d, T cols -> s       16 (+ d once per launch)
+      rows_t_axpy_sep     s, x_{k-1}, f -> x_k, Z^T (row pass)   40
+      cols_sep_real (A)   Z^T -> Y = A x_k                       16
+      rows_resid_sep      Y, g -> r (norm), Z'^T (row pass)      24
+    """
+    P = 8.0 * n * n
+    stencil = 2.0 * (2 * q + 1) * n * n
+    dst = n * dst_line_flops(n, packed=True)
+    return {
+        "cols_sep_real#0": {"bytes": images * 2 * P, "flops": images * stencil},
+        "rows_tt_sep#2": {"bytes": images * 2 * P, "flops": images * dst},
+        "dst_tcols#2": {"bytes": images * 2 * P + P, "flops": images * 2 * dst},
+        "rows_t_axpy_sep#2": {"bytes": images * 5 * P, "flops": images * (dst + stencil + 4.0 * n * n)},
+        "cols_sep_real#1": {"bytes": images * 2 * P, "flops": images * stencil},
+        "rows_resid_sep#1": {"bytes": images * 3 * P, "flops": images * (stencil + 2.0 * n * n)},
+    }
+
+
 def conv_apply_flops(n1: int, n2: int, q1: int, q2: int) -> float:
     L1, L2 = conv_len(n1, q1), conv_len(n2, q2)
     Lh = L2 // 2 + 1

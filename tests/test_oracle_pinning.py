@@ -408,3 +408,54 @@ def test_acceleration_trend(oracle):  # solver_test.cpp:164-210 (AR branch)
             first = hit[0] + 1 if first == 0 else min(first, hit[0] + 1)
     assert first > 0
     assert plain["best_iteration"] >= 5 * first
+
+
+# ---------------------------------------------------------------------------
+# Oracle engineering: the Stockham/Bluestein FFT, line-parallel threads and
+# the kernel-spectrum cache must not change any number; the long-double
+# variant is the same algorithm with a 64-bit mantissa.
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 12, 31, 62, 97, 255, 271, 1023, 1084, 2172, 4096])
+def test_fft_against_numpy(oracle, n):
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    for sign in (-1, 1):
+        got = oracle.fft(x, sign)
+        want = np.fft.fft(x) if sign < 0 else np.fft.ifft(x) * n
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-14
+
+
+def test_oracle_threads_and_kernel_cache_bit_identical(oracle):
+    from paper_1211_0393_b200 import configs as cf
+    c = cf.CONFIGS["C3"]
+    f, g, taps = cf.make_problem(c, n=72)
+    d = oracle.build_tikhonov(taps, c.alpha, 72, 72)
+    runs = []
+    try:
+        for threads, cache in ((1, False), (5, False), (3, True)):
+            oracle.set_threads(threads)
+            oracle.set_kernel_cache(cache)
+            runs.append(oracle.landweber(taps, g, d=d, f_true=f, max_iters=6, keep_iterates=True))
+    finally:
+        oracle.set_threads(1)
+        oracle.set_kernel_cache(False)
+    for r in runs[1:]:
+        assert np.array_equal(r["iterates"], runs[0]["iterates"])
+        assert np.array_equal(r["rre_history"], runs[0]["rre_history"])
+
+
+def test_long_double_oracle_is_the_same_algorithm(oracle):
+    from paper_1211_0393_b200 import configs as cf
+    c = cf.CONFIGS["C2"]
+    n = 48
+    f, g, taps = cf.make_problem(c, n=n)
+    dbl = oracle.landweber(taps, g, d=oracle.build_tikhonov(taps, c.alpha, n, n), f_true=f, max_iters=8,
+                           keep_iterates=True)
+    ld = oracle.landweber(taps, g, f_true=f, max_iters=8, keep_iterates=True, long_double_alpha=c.alpha)
+    for k in range(8):
+        e = np.linalg.norm(dbl["iterates"][k] - ld["iterates"][k]) / np.linalg.norm(ld["iterates"][k])
+        assert 0 < e <= 1e-13
+    assert dbl["best_iteration"] == ld["best_iteration"]
+    x = np.random.default_rng(3).standard_normal((n, n))
+    for kind in (3, 4):
+        a, b = oracle.tensor_apply(kind, x), oracle.tensor_apply(kind, x, long_double=True)
+        assert 0 < np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-14
