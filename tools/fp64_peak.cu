@@ -40,6 +40,42 @@ __global__ void dmma_kernel(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// Mixed: even warps issue DMMA, odd warps DFMA, in the same CTA — does the
+// FP64 tensor path add throughput on top of the DFMA pipe, or share it?
+__global__ void mixed_kernel(double* out, int iters_mma, int iters_fma, double a0, double b0) {
+  const int w = threadIdx.x >> 5;
+  double s = 0;
+  if (w & 1) {
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters_fma; ++it) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a0, b0);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+  } else {
+    double a = threadIdx.x * 1e-3, b = 0.999;
+    double c[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = 0.0;
+    for (int it = 0; it < iters_mma; ++it) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s += c[i][0] + c[i][1];
+  }
+  if (s == 12345.678) out[0] = s;
+}
+
 int main() {
   double* out;
   cudaMalloc(&out, 8);
@@ -92,9 +128,22 @@ int main() {
     reps += 10;
   }
   double dmma_sust = flm * reps / (tot * 1e-3) / 1e12;
+  // mixed: half the warps each; per-warp work sized so that both halves take
+  // about the same time if the two paths were independent
+  const int im = 500, iff = 1000;
+  mixed_kernel<<<blocks, threads>>>(out, 10, 10, 1.0000001, 1e-9);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 10; ++r) mixed_kernel<<<blocks, threads>>>(out, im, iff, 1.0000001, 1e-9);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  double flmix = 10.0 * blocks * ((threads / 64) * (double)im * 8 * 4 * 512 +
+                                  (threads / 2) * (double)iff * 16 * 8 * 2);
+  double mixed = flmix / (ms * 1e-3) / 1e12;
   cudaError_t err = cudaGetLastError();
   printf("{\"sms\": %d, \"dfma_tflops_burst\": %.3f, \"dfma_tflops_sustained\": %.3f, "
-         "\"dmma_tflops_burst\": %.3f, \"dmma_tflops_sustained\": %.3f, \"err\": \"%s\"}\n",
-         sms, dfma_burst, dfma_sust, dmma_burst, dmma_sust, cudaGetErrorString(err));
+         "\"dmma_tflops_burst\": %.3f, \"dmma_tflops_sustained\": %.3f, \"mixed_half_warps_tflops\": %.3f, "
+         "\"err\": \"%s\"}\n",
+         sms, dfma_burst, dfma_sust, dmma_burst, dmma_sust, mixed, cudaGetErrorString(err));
   return err == cudaSuccess ? 0 : 1;
 }
