@@ -307,6 +307,26 @@ inline RestorationRun cgls(const BlurOperator& op, const Matrix& g, const Solver
   return detail::run(op, d, g, cfg, true);
 }
 
+struct SemiconvergenceReport {  // solver.hpp:150-151
+  int best_iter = 0;       // 1-based
+  double best_rre = 0.0;
+  bool diverged_after = false;
+};
+
+// First RRE minimum (std::min_element) and whether the last RRE degrades by
+// more than 5% past it (solver.hpp:152-160).  Host-side post-process.
+inline SemiconvergenceReport semiconvergence_report(const RestorationRun& run) {
+  detail::require(!run.rre_history.empty(), "semiconvergence_report: no RRE history");
+  std::size_t b = 0;
+  for (std::size_t i = 1; i < run.rre_history.size(); ++i)
+    if (run.rre_history[i] < run.rre_history[b]) b = i;
+  SemiconvergenceReport rep;
+  rep.best_iter = static_cast<int>(b) + 1;
+  rep.best_rre = run.rre_history[b];
+  rep.diverged_after = run.rre_history.back() > rep.best_rre * 1.05;
+  return rep;
+}
+
 struct NoiseSpec {  // image.hpp:31-34
   double relative_level = 0.0;
   std::uint64_t seed = 0;

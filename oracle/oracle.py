@@ -345,3 +345,17 @@ def landweber(taps, g, d=None, f_true=None, tau=1.0, max_iters=100, stop=STOP_MI
         "residual_history": res_h[:k].copy(),
         "iterates": xh[:k] if xh is not None else None,
     }
+
+
+def semiconvergence_report(rre_history):
+    """solver.hpp:152-160: (best_iter 1-based at the FIRST minimum — std::min_element
+    —, best_rre, diverged_after = last > 1.05 * best).  Raises ValueError on an
+    empty history (detail::require)."""
+    h = [float(v) for v in rre_history]
+    if not h:
+        raise ValueError("semiconvergence_report: no RRE history")
+    b = 0
+    for i in range(1, len(h)):
+        if h[i] < h[b]:
+            b = i
+    return b + 1, h[b], h[-1] > h[b] * 1.05

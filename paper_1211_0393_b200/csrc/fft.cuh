@@ -599,8 +599,132 @@ __device__ __forceinline__ void stage_odd_cta_split(double2* sm, int tid) {
   __syncthreads();
 }
 
+// FP64 tensor-core form of the twiddle-free (first) stage of a large odd
+// prime R (29, 31: H + 1 = (R+1)/2 <= 16, so nothing pads beyond 16): after
+// the in-place fold (a_j at slot j, b_j at slot R-j, x_0 at slot 0) the
+// stage's G*NB butterflies are two small real GEMMs on all of them at once,
+//   A[k][col] = sum_{j=0..H} Cw[k][j] * Aval[j][col],  Cw = [1 | cos(2 pi jk/R)]
+//   B[k][col] = sum_{j=1..H} Sw[k][j] * Bval[j][col],  Sw = sin(2 pi jk/R)
+// k = 0..H (row 0 of Cw is all ones: A[0] = X_0), col = 2 b + {re, im} of
+// butterfly b (the fold keeps a butterfly's complex value contiguous, so a
+// GEMM row j is the line's slot range [j NB, j NB + NB) read as doubles), and
+// X_k = A_k + S i B_k, X_{R-k} = A_k - S i B_k.  mma.sync.m8n8k4.f64: M = 16
+// (two m-tiles), K = 16 (four k-steps), N = 8 columns per tile; a warp task
+// is one (line, n-tile, m-tile) with 8 DMMA (cos + sin), the weight
+// fragments live in registers for the whole stage.  One DMMA is 256 FMAs, so
+// the stage's 900 FMAs per butterfly issue as ~4 warp instructions instead of
+// ~28 DFMA ones.  But the FP64 pipe is shared (DMMA + DFMA concurrently:
+// 35.4 TF/s, profiles/r02_fp64_peak.json) and the tiles pad 116% of the
+// useful FMAs, so the stage costs ~7% more pipe time than the DFMA sweep;
+// measured A/B on C3 (profiles/r02_dmma_ab.md): transform class 92.7 vs 89.4
+// ms/step, -2.7% overall.  Opt-in (-DDBX_DMMA_STAGE), not the default.
+template <int L, int R, int S, int G, int PL, int NTH>
+struct OddDmma {
+  static constexpr int NB = L / R, H = (R - 1) / 2;
+  static constexpr int NCOL = 2 * NB, NTILE = (NCOL + 7) / 8;
+  static constexpr int TASKS = G * NTILE * 2;           // (line, n-tile, m-tile)
+  static constexpr int NW = NTH / 32;
+  static constexpr int TPW = (TASKS + NW - 1) / NW;     // tasks per warp
+  static constexpr bool ok = H + 1 <= 16 && H >= 14 && NTH % 32 == 0 && (L & 1);
+};
+
+__device__ __forceinline__ void dmma_f64(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+template <int L, int R, int S, int G, int PL, int NTH>
+__device__ __forceinline__ void stage_odd_cta_dmma(double2* sm, int tid) {
+  using Z = OddDmma<L, R, S, G, PL, NTH>;
+  using K = OddConst<R>;
+  constexpr int NB = Z::NB, H = Z::H, NTILE = Z::NTILE, TPW = Z::TPW, NW = Z::NW;
+  __shared__ double2 ocs[R];  // (cos, sin)(2 pi e / R)
+  if (tid < R) ocs[tid] = make_double2(K::c(tid), K::s(tid));
+  // fold every butterfly's symmetric pairs in place
+  for (int e = tid; e < G * NB * H; e += NTH) {
+    const int line = e / (NB * H), r = e - line * (NB * H);
+    const int j = 1 + r / NB, b = r - (j - 1) * NB;
+    double2* buf = sm + line * PL;
+    double2& vj = buf[b + j * NB];
+    double2& vm = buf[b + (R - j) * NB];
+    const double2 x = vj, y = vm;
+    vj = cadd(x, y);
+    vm = csub(x, y);
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  // weight fragments (A operand: row k = 8 mt + gid, col j = 4 ks + tig)
+  double cw[2][4], sw[2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int k = 8 * mt + gid, j = 4 * ks + tig;
+      const bool in = k <= H && j <= H;
+      const double2 w = ocs[(j * k) % R];
+      cw[mt][ks] = in ? (j == 0 ? 1.0 : w.x) : 0.0;
+      sw[mt][ks] = in && j > 0 ? w.y : 0.0;
+    }
+  double res[TPW][4];
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) {
+    const int task = warp + u * NW;  // warp-uniform
+    res[u][0] = res[u][1] = res[u][2] = res[u][3] = 0.0;
+    if (task < Z::TASKS) {
+      const int mt = task & 1, tl = task >> 1;
+      const int line = tl / NTILE, nt = tl - line * NTILE;
+      const double* bd = reinterpret_cast<const double*>(sm + line * PL);
+      const int col = 8 * nt + gid;         // B operand column of this lane
+      const bool cv = col < 2 * NB;
+      double ac[2] = {0.0, 0.0}, bs[2] = {0.0, 0.0};
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int j = 4 * ks + tig;          // B operand row: j <= 15
+        const bool jv = cv && j <= H;
+        const double av = jv ? bd[2 * j * NB + col] : 0.0;                       // x_0 / a_j
+        const double bv = jv && j > 0 ? bd[2 * (R - j) * NB + col] : 0.0;        // b_j
+        dmma_f64(ac, mt ? cw[1][ks] : cw[0][ks], av);
+        dmma_f64(bs, mt ? sw[1][ks] : sw[0][ks], bv);
+      }
+      res[u][0] = ac[0]; res[u][1] = ac[1]; res[u][2] = bs[0]; res[u][3] = bs[1];
+    }
+  }
+  __syncthreads();  // every butterfly's inputs are consumed before the in-place outputs
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) {
+    const int task = warp + u * NW;
+    if (task < Z::TASKS) {
+      const int mt = task & 1, tl = task >> 1;
+      const int line = tl / NTILE, nt = tl - line * NTILE;
+      const int k = 8 * mt + gid;            // accumulator row
+      const int b = 4 * nt + tig;            // accumulator cols (2b, 2b+1) = butterfly b
+      if (k <= H && b < NB) {
+        double2* buf = sm + line * PL;
+        const double2 A = make_double2(res[u][0], res[u][1]);
+        const double2 sb = mul_si<S>(make_double2(res[u][2], res[u][3]));
+        const int base = b * R;                // Ns = 1
+        if (k == 0) {
+          buf[base] = A;
+        } else {
+          buf[base + k] = cadd(A, sb);
+          buf[base + R - k] = csub(A, sb);
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 template <int L, int Ns, int R, int S, int G, int PL, int NTH>
 __device__ __forceinline__ void stage_odd_cta(double2* sm, const double2* __restrict__ tw, int tid) {
+#ifdef DBX_DMMA_STAGE
+  if constexpr (Ns == 1 && OddDmma<L, R, S, G, PL, NTH>::ok) {
+    stage_odd_cta_dmma<L, R, S, G, PL, NTH>(sm, tid);
+    return;
+  }
+#endif
 #ifndef DBX_NO_ODD_SPLIT
   if constexpr (Ns == 1 && OddSplit<L, R, S, G, PL, NTH>::ok) {
     stage_odd_cta_split<L, R, S, G, PL, NTH>(sm, tid);

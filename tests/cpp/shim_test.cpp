@@ -46,6 +46,22 @@ int main() {
   auto run = d_landweber(dop, d, gg, cfg);
   for (Index i = 0; i < 8; ++i)
     for (Index j = 0; j < 8; ++j) CHECK(std::abs(run.restored(i, j) - gg(i, j) / 1.25) <= 1e-12);
+  // semiconvergence_report (solver.hpp:152-160): first minimum, 5% rule
+  {
+    RestorationRun h;
+    h.rre_history = {0.5, 0.3, 0.2, 0.2, 0.25};
+    auto rep = semiconvergence_report(h);
+    CHECK(rep.best_iter == 3 && rep.best_rre == 0.2 && rep.diverged_after);
+    h.rre_history = {0.5, 0.3, 0.2, 0.2, 0.205};
+    CHECK(!semiconvergence_report(h).diverged_after);
+    bool empty_threw = false;
+    try {
+      semiconvergence_report(RestorationRun{});
+    } catch (const std::invalid_argument&) {
+      empty_threw = true;
+    }
+    CHECK(empty_threw);
+  }
   // errors map to the reference exceptions
   bool threw = false;
   try {

@@ -1,6 +1,6 @@
 """Graph-path throughput of one BASELINE config under engine overrides, with
 per-class kernel times (diagnostic; bench.py is the contract).
-Usage: config_probe.py CONFIG [conv=0|1|2] [fusion=0|1] [reps]"""
+Usage: config_probe.py CONFIG [conv=0|1|2] [fusion=0|1] [reps] [dst=0 auto|1 dense|2 fft]"""
 import ctypes as C
 import json
 import os
@@ -13,7 +13,7 @@ import paper_1211_0393_b200 as dbx  # noqa: E402
 from paper_1211_0393_b200 import configs as cf  # noqa: E402
 
 
-def main(name, conv=0, fusion=1, reps=3):
+def main(name, conv=0, fusion=1, reps=3, dst=0):
     import torch
     L = dbx.lib()
     cfg = cf.CONFIGS[name]
@@ -26,6 +26,7 @@ def main(name, conv=0, fusion=1, reps=3):
     dbx._check(L.dbx_plan_create(n, n, 1, dbx._ptr(taps), q, q, 3, 0, C.byref(plan)))
     dbx._check(L.dbx_plan_set_conv(plan, conv))
     dbx._check(L.dbx_plan_set_fusion(plan, fusion))
+    dbx._check(L.dbx_plan_set_dst(plan, dst))
     dbx._check(L.dbx_precond_build(plan, float(cfg.alpha)))
     stream = torch.cuda.ExternalStream(L.dbx_plan_stream(plan))
     rre, res = np.zeros(H), np.zeros(H)
