@@ -199,14 +199,16 @@ def other_configs(L, dbx, cf, torch, dev, local, reps=3):
     out = {}
     for name in ("C1", "C2", "C4", "C5"):
         cfg = cf.CONFIGS[name]
-        t0 = time.perf_counter()
-        F, G, taps = cf.make_batch(cfg, 1)
-        gen_s = time.perf_counter() - t0
         n, q, H = cfg.n, cfg.q, cfg.iters
-        g = torch.from_numpy(G).to(dev)
-        f = torch.from_numpy(F).to(dev)
+        # inputs synthesised on the GPU straight into device buffers (§8f f4)
+        g = torch.empty((1, n, n), dtype=torch.float64, device=dev)
+        f = torch.empty_like(g)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, _, taps = cf.make_problem_device(cfg, device=local, out=(f, g))
+        torch.cuda.synchronize()
+        gen_s = time.perf_counter() - t0
         o = torch.empty_like(g)
-        del F, G
         plan = C.c_void_p()
         dbx._check(L.dbx_plan_create(n, n, 1, dbx._ptr(taps), q, q, 3, local, C.byref(plan)))
         dbx._check(L.dbx_precond_build(plan, float(cfg.alpha)))
@@ -214,7 +216,8 @@ def other_configs(L, dbx, cf, torch, dev, local, reps=3):
         rre = np.zeros(H)
         res = np.zeros(H)
         best, done = (C.c_int * 1)(), (C.c_int * 1)()
-        entry = {"n": n, "q": q, "iters": H, "alpha": cfg.alpha, "host_generation_s": round(gen_s, 2)}
+        entry = {"n": n, "q": q, "iters": H, "alpha": cfg.alpha, "generation_s": round(gen_s, 3),
+                 "generator": "device (dbx_gen_honest_device)"}
         fz = C.c_int()
         for prec in ((1, 0) if cfg.plain_too else (1,)):
             def solve():

@@ -318,6 +318,31 @@ int dbx_gen_honest(const double* scene, int rows, int cols, const double* taps, 
 /* add_noise alone (image.hpp:72-82). */
 int dbx_add_noise(const double* g, int n1, int n2, double level, uint64_t seed, double* out);
 
+/* Scene shape parameters in generation order (the mt19937_64 draws of
+ * dbx_gen_scene), DBX_SHAPE_PARAMS doubles per shape: ellipse flag, cy, cx,
+ * a, b, cos(theta), sin(theta), intensity, clipped bounding box r0, r1, c0, c1. */
+#define DBX_SHAPE_PARAMS 12
+int dbx_gen_scene_shapes(int rows, int cols, int nshapes, uint64_t seed, double* params);
+
+/* The first `count` outputs of std::mt19937_64(seed) (host; test reference). */
+int dbx_mt19937_64_host(uint64_t seed, uint64_t count, uint64_t* out);
+
+/* The same stream generated on the GPU (gen_dev.cu: one CTA twists the 312-word
+ * state two half-blocks at a time); `out` is host or device memory. */
+int dbx_mt19937_64_device(uint64_t seed, uint64_t count, uint64_t* out, int device);
+
+/* GPU-side Honest synthesis (experiment.hpp:71-99 + image.hpp:72-82):
+ * the scene of dbx_gen_scene painted on the device (per-tile shape lists,
+ * last covering shape wins — identical in/out decisions to the host painter),
+ * the direct correlation with the mask over the canvas, the centred FOV crop
+ * into f_true, and add_noise with the mt19937_64 stream twisted on the device
+ * and Box-Muller per sample pair.  f_true (nullable) and g may be host or
+ * device pointers (n1 x n2).  f_true equals the host generator's bit for bit;
+ * g agrees to rounding (device libm and reduction order, <= 1e-14 relative). */
+int dbx_gen_honest_device(int rows, int cols, int nshapes, double sinus_amp, uint64_t scene_seed,
+                          const double* taps, int q1, int q2, int n1, int n2, double noise_level,
+                          uint64_t noise_seed, double* f_true, double* g, int device);
+
 #ifdef __cplusplus
 }
 #endif

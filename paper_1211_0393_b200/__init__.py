@@ -86,6 +86,10 @@ def lib():
         L.dbx_gen_psf_gaussian.argtypes = [i, i, d, d, d, d, d, vp]
         L.dbx_gen_psf_motion.argtypes = [i, i, d, d, d, vp]
         L.dbx_gen_honest.argtypes = [vp, i, i, vp, i, i, i, i, d, C.c_uint64, i, vp, vp]
+        L.dbx_gen_scene_shapes.argtypes = [i, i, i, C.c_uint64, vp]
+        L.dbx_mt19937_64_host.argtypes = [C.c_uint64, C.c_uint64, vp]
+        L.dbx_mt19937_64_device.argtypes = [C.c_uint64, C.c_uint64, vp, i]
+        L.dbx_gen_honest_device.argtypes = [i, i, i, d, C.c_uint64, vp, i, i, i, i, d, C.c_uint64, vp, vp, i]
         L.dbx_add_noise.argtypes = [vp, i, i, d, C.c_uint64, vp]
         L.dbx_precond_build_sweep.argtypes = [vp, vp]
         L.dbx_slab_blur.argtypes = [vp, vp, vp, i, vp, C.POINTER(d)]

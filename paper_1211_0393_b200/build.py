@@ -40,7 +40,10 @@ def _compile(src: str, verbose: bool) -> str:
     if src.endswith(".cu"):
         cmd = [NVCC] + NVFLAGS + DEFS + ["-c", src, "-o", obj]
     else:
-        cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-march=x86-64-v3", "-I", INCLUDE] + DEFS + ["-c", src, "-o", obj]
+        # gen.cpp: no FMA contraction, so the host scene painter makes the same
+        # IEEE operations (and in/out decisions) as the device one (gen_dev.cu)
+        extra = ["-ffp-contract=off"] if src.endswith("gen.cpp") else []
+        cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-march=x86-64-v3", "-I", INCLUDE] + extra + DEFS + ["-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -122,6 +122,24 @@ def make_problem(cfg: Config, image: int = 0, n: Optional[int] = None, threads: 
     return f, g, taps
 
 
+def make_problem_device(cfg: Config, image: int = 0, n: Optional[int] = None, device: int = 0, out=None):
+    """make_problem's data generated on the GPU (dbx_gen_honest_device, SURVEY
+    §8f f4): same seeds, same scene (f_true bit for bit), g to rounding.
+    ``out``: optional (f, g) pair of float64 buffers (numpy arrays or
+    torch CUDA tensors) to fill in place; else numpy arrays are returned."""
+    from . import _check, _ptr, lib
+    n = cfg.n if n is None else n
+    taps = make_psf(cfg)
+    canvas = n + 2 * (2 * cfg.q + 1)
+    s = scene_seed(cfg, image)
+    if out is None:
+        out = (np.empty((n, n)), np.empty((n, n)))
+    f, g = out
+    _check(lib().dbx_gen_honest_device(canvas, canvas, cfg.shapes, cfg.sinus_amp, s, _ptr(taps), cfg.q, cfg.q,
+                                       n, n, cfg.noise, s ^ 0x5DEECE66D, _ptr(f), _ptr(g), int(device)))
+    return f, g, taps
+
+
 def make_batch(cfg: Config, images: int, first: int = 0, n: Optional[int] = None, threads: int = 0):
     n = cfg.n if n is None else n
     F = np.empty((images, n, n))

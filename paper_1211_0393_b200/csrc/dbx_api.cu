@@ -791,6 +791,23 @@ extern "C" {
 
 const char* dbx_last_error(void) { return g_err.c_str(); }
 
+int dbx_mt19937_64_device(uint64_t seed, uint64_t count, uint64_t* out, int device) {
+  std::string e;
+  const int st = dbx::mt19937_64_device(seed, count, out, device, e);
+  g_err = st ? e : std::string();
+  return st;
+}
+
+int dbx_gen_honest_device(int rows, int cols, int nshapes, double sinus_amp, uint64_t scene_seed,
+                          const double* taps, int q1, int q2, int n1, int n2, double noise_level,
+                          uint64_t noise_seed, double* f_true, double* g, int device) {
+  std::string e;
+  const int st = dbx::gen_honest_device(rows, cols, nshapes, sinus_amp, scene_seed, taps, q1, q2, n1, n2,
+                                        noise_level, noise_seed, f_true, g, device, e);
+  g_err = st ? e : std::string();
+  return st;
+}
+
 const char* dbx_version(void) { return "dbx 0.2 sm_100a (FP64 AR stencil / FFT correlation + Bluestein DST-I AR transform)"; }
 
 int dbx_device_count(void) {

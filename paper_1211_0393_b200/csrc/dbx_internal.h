@@ -111,6 +111,13 @@ struct GemmArgs {
 };
 void launch_gemm(const GemmArgs& a, cudaStream_t s, int* ctas_per_image);
 
+// ---- GPU-side input synthesis (gen_dev.cu) --------------------------------
+// Status DBX_* with the message in err (the C-ABI wrappers set dbx_last_error).
+int mt19937_64_device(uint64_t seed, uint64_t count, uint64_t* out, int device, std::string& err);
+int gen_honest_device(int rows, int cols, int nshapes, double sinus_amp, uint64_t scene_seed, const double* taps,
+                      int q1, int q2, int n1, int n2, double noise_level, uint64_t noise_seed, double* f_true,
+                      double* g, int device, std::string& err);
+
 // ---- spectrum, norms, finalize -----------------------------------------
 // grid 0: anti-reflective grid, 1: reflective (DCT-III) grid
 void launch_build_filter(const double* sym_taps, int q1, int q2, int n1, int n2, double alpha,

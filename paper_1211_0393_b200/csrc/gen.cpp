@@ -86,26 +86,44 @@ int dbx_add_noise(const double* g, int n1, int n2, double level, uint64_t seed, 
   return DBX_OK;
 }
 
-int dbx_gen_scene(int rows, int cols, int nshapes, double sinus_amp, uint64_t seed, double* out) {
-  if (rows < 1 || cols < 1 || nshapes < 0 || !out) return DBX_EINVAL;
+int dbx_gen_scene_shapes(int rows, int cols, int nshapes, uint64_t seed, double* params) {
+  if (rows < 1 || cols < 1 || nshapes < 0 || (nshapes > 0 && !params)) return DBX_EINVAL;
   std::mt19937_64 rng(seed);
-  std::fill(out, out + (size_t)rows * cols, 0.0);
   const double dim = std::min(rows, cols);
   for (int s = 0; s < nshapes; ++s) {
+    double* P = params + (size_t)s * DBX_SHAPE_PARAMS;
     const bool ellipse = u01(rng) < 0.5;
     const double cy = u01(rng) * rows, cx = u01(rng) * cols;
     const double a = (0.02 + 0.10 * u01(rng)) * dim;
     const double b = (0.02 + 0.10 * u01(rng)) * dim;
     const double th = u01(rng) * kPi;
     const double val = u01(rng);
-    const double ct = std::cos(th), st = std::sin(th);
     const double rad = std::max(a, b) * (ellipse ? 1.0 : std::sqrt(2.0));
-    const int r0 = std::max(0, (int)std::floor(cy - rad)), r1 = std::min(rows - 1, (int)std::ceil(cy + rad));
-    const int c0 = std::max(0, (int)std::floor(cx - rad)), c1 = std::min(cols - 1, (int)std::ceil(cx + rad));
+    P[0] = ellipse ? 1.0 : 0.0; P[1] = cy; P[2] = cx; P[3] = a; P[4] = b;
+    P[5] = std::cos(th); P[6] = std::sin(th); P[7] = val;
+    // clipped bounding box (rows r0..r1, cols c0..c1): the only pixels tested
+    P[8] = std::max(0, (int)std::floor(cy - rad)); P[9] = std::min(rows - 1, (int)std::ceil(cy + rad));
+    P[10] = std::max(0, (int)std::floor(cx - rad)); P[11] = std::min(cols - 1, (int)std::ceil(cx + rad));
+  }
+  return DBX_OK;
+}
+
+int dbx_gen_scene(int rows, int cols, int nshapes, double sinus_amp, uint64_t seed, double* out) {
+  if (rows < 1 || cols < 1 || nshapes < 0 || !out) return DBX_EINVAL;
+  std::vector<double> prm((size_t)nshapes * DBX_SHAPE_PARAMS);
+  if (dbx_gen_scene_shapes(rows, cols, nshapes, seed, prm.data()) != DBX_OK) return DBX_EINVAL;
+  std::fill(out, out + (size_t)rows * cols, 0.0);
+  for (int s = 0; s < nshapes; ++s) {
+    const double* P = prm.data() + (size_t)s * DBX_SHAPE_PARAMS;
+    const bool ellipse = P[0] != 0.0;
+    const double cy = P[1], cx = P[2], a = P[3], b = P[4], ct = P[5], st = P[6], val = P[7];
+    const int r0 = (int)P[8], r1 = (int)P[9], c0 = (int)P[10], c1 = (int)P[11];
     for (int r = r0; r <= r1; ++r) {
       const double dy = r + 0.5 - cy;
       double* row = out + (size_t)r * cols;
       for (int c = c0; c <= c1; ++c) {
+        // gen.cpp is compiled with -ffp-contract=off: the same IEEE operations
+        // as the device painter (gen_dev.cu), so both make identical in/out calls
         const double dx = c + 0.5 - cx;
         const double u = dx * ct + dy * st, v = -dx * st + dy * ct;
         const bool in = ellipse ? (u * u) / (a * a) + (v * v) / (b * b) <= 1.0
@@ -119,6 +137,13 @@ int dbx_gen_scene(int rows, int cols, int nshapes, double sinus_amp, uint64_t se
       for (int c = 0; c < cols; ++c)
         out[(size_t)r * cols + c] +=
             sinus_amp * std::sin(2.0 * kPi * (3.0 * (r + 0.5) / rows + 2.0 * (c + 0.5) / cols));
+  return DBX_OK;
+}
+
+int dbx_mt19937_64_host(uint64_t seed, uint64_t count, uint64_t* out) {
+  if (count > 0 && !out) return DBX_EINVAL;
+  std::mt19937_64 rng(seed);
+  for (uint64_t i = 0; i < count; ++i) out[i] = rng();
   return DBX_OK;
 }
 

@@ -70,3 +70,71 @@ def test_run_experiment_writes_reference_files(dbx, tmp_path):
     assert res.summary[1].alpha == best.alpha
     hist = open(tmp_path / (best.stem() + ".csv")).read().splitlines()
     assert hist[0] == "iter,rre,residual" and len(hist) == 11
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bc", ["AntiReflective", "Reflective"])
+def test_sweep_cells_match_oracle(dbx, oracle, bc):
+    """Every alpha cell of the batched GPU sweep against the CPU oracle's own
+    D-Landweber run for that alpha (experiment.hpp:209-232 run_cell): identical
+    divergence verdict, iteration count and best iteration; histories and the
+    restored image within the 1e-10 parity bar."""
+    from paper_1211_0393_b200 import configs as cf
+    c = cf.CONFIGS["C1"]
+    n, iters = 64, 15
+    f, g, taps = cf.make_problem(c, n=n)
+    alphas = ex.alpha_grid(1e-3, 0.3, 4)
+    bcv = int(getattr(dbx.BoundaryCondition, bc))
+    cells = ex.sweep_d_landweber(taps, g, f, alphas, iters, bc=bcv)
+    for a, cell in zip(alphas, cells):
+        assert cell.bc == bcv and cell.stem().startswith(ex.bc_name(bcv) + "_d-landweber_alpha")
+        try:
+            ref = oracle.landweber(taps, g, d=oracle.build_tikhonov(taps, a, n, n, bc=bcv), f_true=f,
+                                   max_iters=iters, bc=bcv)
+        except oracle.OracleDivergence:
+            assert cell.diverged, a
+            continue
+        assert not cell.diverged, a
+        assert cell.run.iterations_executed == ref["iterations_executed"]
+        assert cell.run.best_iteration == ref["best_iteration"]
+        np.testing.assert_allclose(cell.run.rre_history, ref["rre_history"], rtol=1e-10, atol=0)
+        np.testing.assert_allclose(cell.run.residual_history, ref["residual_history"], rtol=1e-10, atol=0)
+        r = ref["restored"]
+        assert np.linalg.norm(cell.run.restored - r) <= 1e-10 * np.linalg.norm(r)
+
+
+@pytest.mark.gpu
+def test_run_experiment_both_bcs_writes_pgms(dbx, tmp_path):
+    """Per-BC cell blocks and the restored PGMs of experiment.hpp:242-244, 266-268."""
+    from paper_1211_0393_b200 import configs as cf
+    from paper_1211_0393_b200 import io as dio
+    c = cf.CONFIGS["C1"]
+    f, g, taps = cf.make_problem(c, n=48)
+    f, g = 200.0 * f, 200.0 * g  # PGM range: the writer rounds and clamps to [0, 255]
+    bcs = (dbx.BoundaryCondition.AntiReflective, dbx.BoundaryCondition.Reflective)
+    res = ex.run_experiment(taps, g, f, ex.alpha_grid(1e-3, 1e-1, 3), max_iters=8, out_dir=str(tmp_path), bcs=bcs)
+    names = set(os.listdir(tmp_path))
+    for b in ("antireflective", "reflective"):
+        assert {b + "_landweber.csv", b + "_landweber.pgm", b + "_d-landweber.pgm"} <= names
+        assert sum(nm.startswith(b + "_d-landweber_alpha") for nm in names) == 3
+    rows = open(tmp_path / "summary.csv").read().splitlines()
+    assert [r.split(",")[0] for r in rows[1:]] == ["antireflective"] * 2 + ["reflective"] * 2
+    assert "bcs=antireflective,reflective" in open(tmp_path / "metadata.txt").read()
+    for b, bcv in zip(("antireflective", "reflective"), bcs):
+        plain = next(cc for cc in res.cells if cc.bc == bcv and cc.method == "landweber")
+        px, mx = dio.read_pgm(str(tmp_path / (b + "_landweber.pgm")))
+        assert mx == 255 and px.shape == (48, 48)
+        assert np.array_equal(px, np.clip(np.round(plain.run.restored), 0, 255))
+        row = next(r for r in res.summary if r.bc == bcv and r.method == "d-landweber")
+        best = next(cc for cc in res.cells if cc.bc == bcv and cc.method == "d-landweber" and cc.alpha == row.alpha)
+        px, _ = dio.read_pgm(str(tmp_path / (b + "_d-landweber.pgm")))
+        assert np.array_equal(px, np.clip(np.round(best.run.restored), 0, 255))
+
+
+def test_bc_names_and_refusal():
+    from paper_1211_0393_b200 import BoundaryCondition as BC
+    assert ex.bc_name(BC.AntiReflective) == "antireflective" and ex.bc_name(BC.Reflective) == "reflective"
+    with pytest.raises(ValueError):
+        ex.bc_name(BC.Zero)
+    run = ex.RestorationRun(rre_history=[0.5], residual_history=[1.0])
+    assert ex.CellResult("d-landweber", 0.1, run, 0.0, bc=BC.Reflective).stem() == "reflective_d-landweber_alpha0.1"
