@@ -19,6 +19,8 @@
 // with apply (blur.hpp:75-83), precondition_apply (preconditioner.hpp:88-90).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "spectral_common.cuh"
 
 namespace dbx {
@@ -782,6 +784,13 @@ int launch_fused(int which, const SpecArgs& a, cudaStream_t s) {
     dim3 grid((a.n1 + 3) / 4, a.batch);
     rows_resid_sep<<<grid, kResidNT, bytes, s>>>(a);
     return (int)grid.x;
+  }
+  // warp-owned column half (wdst.cu) for 1024-point columns; DBX_WDST=0
+  // keeps the CTA lock-step dst_tcols (A/B and tests)
+  static const bool wdst_off = [] { const char* e = getenv("DBX_WDST"); return e && e[0] == '0'; }();
+  if (which == FUSED_DST_TCOLS && !wdst_off) {
+    const int c = launch_dst_tcols_w(a, s);
+    if (c >= 0) return c;
   }
   const int L2 = a.conv.L2, M = a.blue2.M;
   const bool blue = a.blue2.M != a.blue2.N;

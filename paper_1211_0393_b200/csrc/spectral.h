@@ -118,6 +118,8 @@ bool rows_sep_supported(int q2);
 int launch_rows_sep_seg(const SpecArgs& a, cudaStream_t s);
 int launch_cols_sep_epi(const SpecArgs& a, int resid, cudaStream_t s);
 int launch_fused(int which, const SpecArgs& a, cudaStream_t s);
+// wdst.cu: warp-owned column half of D for 1024-point columns (-1: not this shape)
+int launch_dst_tcols_w(const SpecArgs& a, cudaStream_t s);
 #ifdef DBX_PHASES
 int fused_debug_phases(unsigned long long* out, int n);  // read + reset (instrumented builds)
 #endif

@@ -1,0 +1,341 @@
+// wdst.cu — warp-owned packed DST-I for n = 1024 lines (N = 1023 = 31 * 33):
+// the column half of D (T~ -> d -> T along columns of u) with no CTA barriers.
+//
+// Replaces (reference): sine1_forward / RODFT00 (transforms.hpp:114-121),
+// ar_inverse then ar_forward (transforms.hpp:148-173) along the columns of
+// tensor_map (transforms.hpp:179-192), and the Hadamard by d between them
+// (filter_apply, spectral.hpp:161-165).
+//
+// One warp owns one packed DFT (two adjacent columns c, c+1 of one image) the
+// whole way: global loads -> T~ fill -> DFT_1023 -> split + odd scan -> x d ->
+// T fill -> DFT_1023 -> split + scan -> ramp epilogue -> row-major stores.
+// Synchronisation is __syncwarp only, so the warps of an SM sit in different
+// phases (loads of one overlap the FP64 DFTs of others) instead of the CTA
+// lock-step of fused.cu's dst_tcols (a CTA barrier after every FFT stage).
+//
+// DFT_1023, Cooley-Tukey N = N2 * N1 with N1 = 33 (inner), N2 = 31, in-place
+// on one padded smem line (slot(p) = p + p/32: the fill's per-lane contiguous
+// runs hit distinct banks):
+//   level 1  lane n2 < 31: x[31 n1 + n2], n1 < 33 -> in-register DFT-33 (3 x 11
+//            Good-Thomas, no internal twiddles) -> * W_1023^{n2 k1} -> back to
+//            the same slots (31 k1 + n2);
+//   level 2  lane k1 < 32: the 31 contiguous slots 31 k1 + n2 -> in-register
+//            DFT-31 (symmetric pairs, compile-time constants) -> X[k1 + 33 k2]
+//            at slot 31 k1 + k2; the 33rd row (k1 = 32) is one output per lane.
+// Packed real DST (spectral_common.cuh pk_fill / pk_split2 / odd_scans2): lane
+// L owns output k in [32L, 32L+32), i.e. split pairs l in [16L, 16L+16): the
+// odd-output prefix sum is 16 sequential adds plus one warp scan of lane totals
+// (the same order as odd_scans2), and the mirrored fill operand N - k lives in
+// lane 31 - L at index 31 - i (one shuffle per element).
+#include <cuda_runtime.h>
+
+#include "spectral_common.cuh"
+
+namespace dbx {
+
+namespace {
+
+constexpr int kWN = 1023;     // DFT length
+constexpr int kWLine = 1024;  // double2 slots per warp line
+constexpr int kWWarps = 4;    // warps (column pairs) per CTA
+// CTAs per SM the register budget is sized for: 2 -> up to 255 registers (the
+// DFT-31 row keeps 30 folded values + 30 constants live), 3 -> 168 (spills)
+#ifndef DBX_WDST_MINB
+#define DBX_WDST_MINB 2
+#endif
+
+// Two layouts share a warp's line.  DFT data at slot p (level 1 reads lanes at
+// consecutive p, level 2 lanes at stride 31: both hit 8 distinct 16-byte bank
+// groups per quarter warp).  Split outputs k at oslot(k) = k ^ ((k >> 5) & 7):
+// the split writes lanes at stride 32 (k = 32 L + i), which the XOR spreads
+// over the bank groups, and the fills / epilogue read lanes at consecutive k,
+// which it keeps conflict-free.  Every change of layout is read-all, syncwarp,
+// write-all.
+__device__ __forceinline__ int wslot(int p) { return p; }
+__device__ __forceinline__ int oslot(int k) { return k ^ ((k >> 5) & 7); }
+
+// cos / sin(2 pi e / P) read through the half-period symmetry c(e) = c(P-e),
+// s(e) = -s(P-e): with e compile-time after unrolling, a DFT-P needs only the
+// (P-1)/2 + (P-1)/2 distinct constants in registers (negation folds into the
+// DFMA operand), not P-1 + P-1.
+template <int P>
+__device__ __forceinline__ double ccs(int e) {
+  return fft::OddConst<P>::c(e <= P / 2 ? e : P - e);
+}
+template <int P>
+__device__ __forceinline__ double scs(int e) {
+  return e <= P / 2 ? fft::OddConst<P>::s(e) : -fft::OddConst<P>::s(P - e);
+}
+// slot of DFT output frequency l after level 2 (k1 = l mod 33, k2 = l / 33)
+__device__ __forceinline__ int wpos(int l) {
+  const int k2 = l / 33;
+  return wslot(31 * (l - 33 * k2) + k2);
+}
+
+// Level-1 row of lane n2: in-register DFT-33 = 3 x 11 prime factor (input
+// n = (11 a + 3 b) mod 33, output k1 = (22 ka + 12 kb) mod 33), each output
+// twiddled by W_1023^{n2 k1} and stored to slot 31 k1 + n2 as soon as it is
+// formed (register-lean: the DFT-3s run in place, the DFT-11 of group ka
+// folds its inputs in place and emits its outputs pair by pair).
+__device__ __forceinline__ void level1_row(double2* buf, const double2* __restrict__ tw, int lane, double2* v) {
+  constexpr int S = -1;
+#pragma unroll
+  for (int b = 0; b < 11; ++b) {
+    double2 t[3] = {v[(3 * b) % 33], v[(11 + 3 * b) % 33], v[(22 + 3 * b) % 33]};
+    fft::dft3<S>(t);
+    v[(3 * b) % 33] = t[0];
+    v[(11 + 3 * b) % 33] = t[1];
+    v[(22 + 3 * b) % 33] = t[2];
+  }
+  auto put = [&](int k1, double2 x) {
+    if (k1 != 0) x = fft::cmul(x, __ldg(tw + lane * k1));  // n2 k1 <= 990
+    buf[wslot(31 * k1 + lane)] = x;
+  };
+#pragma unroll
+  for (int ka = 0; ka < 3; ++ka) {
+    double2* u[11];
+#pragma unroll
+    for (int b = 0; b < 11; ++b) u[b] = &v[(11 * ka + 3 * b) % 33];
+    const double2 x0 = *u[0];
+    double2 sum = x0;
+#pragma unroll
+    for (int j = 1; j <= 5; ++j) {
+      const double2 p = cadd(*u[j], *u[11 - j]), m = csub(*u[j], *u[11 - j]);
+      *u[j] = p;
+      *u[11 - j] = m;
+      sum = cadd(sum, p);
+    }
+    put((22 * ka) % 33, sum);
+#pragma unroll
+    for (int k = 1; k <= 5; ++k) {
+      double2 A = x0, B = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 1; j <= 5; ++j) {
+        const int e = (j * k) % 11;
+        A.x = fma(ccs<11>(e), u[j]->x, A.x);
+        A.y = fma(ccs<11>(e), u[j]->y, A.y);
+        B.x = fma(scs<11>(e), u[11 - j]->x, B.x);
+        B.y = fma(scs<11>(e), u[11 - j]->y, B.y);
+      }
+      const double2 sb = fft::mul_si<S>(B);
+      put((22 * ka + 12 * k) % 33, cadd(A, sb));
+      put((22 * ka + 12 * (11 - k)) % 33, csub(A, sb));
+    }
+  }
+}
+
+// Forward DFT_1023 of one warp's line (S = -1), in place; tw[e] = W_1023^e.
+__device__ __forceinline__ void wdft1023(double2* buf, const double2* __restrict__ tw, int lane) {
+  constexpr int S = -1;
+  if (lane < 31) {
+    double2 v[33];
+#pragma unroll
+    for (int n1 = 0; n1 < 33; ++n1) v[n1] = buf[wslot(31 * n1 + lane)];
+    level1_row(buf, tw, lane, v);
+  }
+  __syncwarp();
+  {
+    // own row k1 = lane: 31 contiguous slots, outputs back in place
+    const int base = 31 * lane;
+    double2 v[31];
+#pragma unroll
+    for (int j = 0; j < 31; ++j) v[j] = buf[wslot(base + j)];
+    const double2 x0 = v[0];
+    double2 sum = x0;
+#pragma unroll
+    for (int j = 1; j <= 15; ++j) {
+      const double2 a = cadd(v[j], v[31 - j]), b = csub(v[j], v[31 - j]);
+      v[j] = a;
+      v[31 - j] = b;
+      sum = cadd(sum, a);
+    }
+    buf[wslot(base)] = sum;
+#pragma unroll
+    for (int k = 1; k <= 15; ++k) {
+      double2 A = x0, B = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 1; j <= 15; ++j) {
+        const int e = (j * k) % 31;
+        A.x = fma(ccs<31>(e), v[j].x, A.x);
+        A.y = fma(ccs<31>(e), v[j].y, A.y);
+        B.x = fma(scs<31>(e), v[31 - j].x, B.x);
+        B.y = fma(scs<31>(e), v[31 - j].y, B.y);
+      }
+      const double2 sb = fft::mul_si<S>(B);
+      buf[wslot(base + k)] = cadd(A, sb);
+      buf[wslot(base + 31 - k)] = csub(A, sb);
+    }
+  }
+  // row k1 = 32 (slots 992..1022, untouched by the own rows): lane k2 < 31
+  // forms X[32 + 33 k2] = sum_n2 Y[32][n2] W_31^{n2 k2} from the pairs
+  double2 X = make_double2(0.0, 0.0);
+  {
+    const double2 y0 = buf[wslot(992)];
+    double2 A = y0, B = make_double2(0.0, 0.0);
+    int e = 0;
+#pragma unroll
+    for (int j = 1; j <= 15; ++j) {
+      e += lane;
+      e = e >= 31 ? e - 31 : e;  // (j * lane) mod 31
+      const double2 yj = buf[wslot(992 + j)], ym = buf[wslot(992 + 31 - j)];
+      const double2 w = __ldg(tw + 33 * e);  // (cos, -sin)(2 pi e / 31)
+      const double2 a = cadd(yj, ym), b = csub(yj, ym);
+      A.x = fma(w.x, a.x, A.x);
+      A.y = fma(w.x, a.y, A.y);
+      B.x = fma(-w.y, b.x, B.x);
+      B.y = fma(-w.y, b.y, B.y);
+    }
+    X = cadd(A, fft::mul_si<S>(B));
+  }
+  __syncwarp();
+  if (lane < 31) buf[wslot(992 + lane)] = X;
+  __syncwarp();
+}
+
+// Split + odd scan in place: the DFT outputs Y_l (slot wpos(l)) become the
+// two real output lines, out[k] = (X^a_k, X^b_k) at slot(k), k in [0, 1024),
+// in the scaled DST-I convention of pk_split2 + odd_scans2.  Lane L owns the
+// pairs l in [16L, 16L+16) (outputs k in [32L, 32L+32)): all its Y reads
+// precede a __syncwarp, then its outputs overwrite the line.
+__device__ __forceinline__ void wsplit(double2* buf, int lane, double hs, double sc) {
+  double2 zl[16], zm[16];
+  double ta = 0.0, tb = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int l = 16 * lane + i;
+    zl[i] = buf[wpos(l)];
+    zm[i] = buf[wpos(l == 0 ? 0 : kWN - l)];
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int l = 16 * lane + i;
+    if (2 * l + 1 <= kWN - 1) {
+      const double f = l == 0 ? 0.25 : 0.5;
+      ta += f * (zl[i].x + zm[i].x);
+      tb += f * (zl[i].y + zm[i].y);
+    }
+  }
+  double ia = ta, ib = tb;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double ya = __shfl_up_sync(0xffffffffu, ia, d), yb = __shfl_up_sync(0xffffffffu, ib, d);
+    if (lane >= d) {
+      ia += ya;
+      ib += yb;
+    }
+  }
+  double pa = ia - ta, pb = ib - tb;  // exclusive offsets; then the lane's own running sums
+  __syncwarp();  // every lane's Y reads precede the outputs (other layout, same slots)
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int l = 16 * lane + i;
+    const double ea = l >= 1 ? hs * (zm[i].y - zl[i].y) : 0.0;
+    const double eb = l >= 1 ? hs * (zl[i].x - zm[i].x) : 0.0;
+    if (2 * l + 1 <= kWN - 1) {
+      const double f = l == 0 ? 0.25 : 0.5;
+      pa += f * (zl[i].x + zm[i].x);
+      pb += f * (zl[i].y + zm[i].y);
+    }
+    buf[oslot(2 * l)] = make_double2(ea, eb);
+    buf[oslot(2 * l + 1)] = make_double2(pa * sc, pb * sc);
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecArgs a) {
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 wsm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double2* buf = wsm + (size_t)w * kWLine;
+  const BlueTables& bt = a.blue1;
+  const int n = a.n1, n2 = a.n2;
+  const size_t N = (size_t)n * n2;
+  const int c = 2 * (kWWarps * blockIdx.x + w);  // columns c, c+1
+  if (c >= n2) return;                           // warp-uniform; no CTA barriers below
+  const bool hb = c + 1 < n2;
+  const double ri = bt.rinv, hs = 0.5 * bt.scale, sc = bt.scale;
+  const double* __restrict__ sn = bt.sn;
+  // ---- T~ (ar_inverse, transforms.hpp:163-173) of columns c, c+1 (contiguous
+  // in u^T): lane L fills the mirror pairs p = L + 32 j <= N/2 and N - p
+  const double* ua = a.in + (size_t)b * N + (size_t)c * n;
+  const double* ub = hb ? ua + n : ua;
+  const double x0a = __ldg(ua), xea = __ldg(ua + n - 1), x0b = __ldg(ub), xeb = __ldg(ub + n - 1);
+  const double sa = x0a + xea, sb = x0b + xeb, da = x0a - xea, db = x0b - xeb;
+#pragma unroll 4
+  for (int j = 0; j < 16; ++j) {
+    const int p = lane + 32 * j, q = kWN - p;  // p in [0, 511], q in [512, 1023]
+    if (p == 0) {
+      buf[wslot(0)] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const double ap = __ldg(ua + p), aq = __ldg(ua + q), bp = __ldg(ub + p), bq = __ldg(ub + q);
+    const double s = __ldg(sn + p), r = fma(-2.0 * ri, (double)p, 1.0);
+    const double Aa = ap + aq - sa, Ba = (ap - aq) - da * r;  // sd(j) of pk_fill
+    const double Ab = bp + bq - sb, Bb = (bp - bq) - db * r;
+    buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), hb ? fma(s, Ab, 0.5 * Bb) : 0.0);
+    buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), hb ? fma(s, Ab, -0.5 * Bb) : 0.0);
+  }
+  __syncwarp();
+  wdft1023(buf, bt.tw, lane);
+  wsplit(buf, lane, hs, sc);
+  // ---- v = u o d (d^T rows c, c+1: L2-resident, shared by the batch), then
+  // the T fill from the same mirror pairs (reads and writes slots p, N - p only)
+  const double* dA = a.dT + (size_t)b * a.dstride + (size_t)c * n;
+  const double* dB = hb ? dA + n : dA;
+  const double a0a = x0a * __ldg(dA), a1a = xea * __ldg(dA + n - 1);
+  const double a0b = x0b * __ldg(dB), a1b = xeb * __ldg(dB + n - 1);
+  double2 zp[16], zq[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int p = lane + 32 * j, q = kWN - p;  // p = 0: z_0 = 0 (q = 1023 is no DFT slot)
+    const double2 op = buf[oslot(p)], oq = buf[oslot(q)];
+    const double mpa = op.x * __ldg(dA + p), mqa = oq.x * __ldg(dA + q);
+    const double mpb = op.y * __ldg(dB + p), mqb = oq.y * __ldg(dB + q);
+    const double s = __ldg(sn + p);
+    const double Aa = mpa + mqa, Ba = mpa - mqa, Ab = mpb + mqb, Bb = mpb - mqb;
+    zp[j] = p == 0 ? make_double2(0.0, 0.0) : make_double2(fma(s, Aa, 0.5 * Ba), fma(s, Ab, 0.5 * Bb));
+    zq[j] = make_double2(fma(s, Aa, -0.5 * Ba), fma(s, Ab, -0.5 * Bb));
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int p = lane + 32 * j;
+    buf[wslot(p)] = zp[j];
+    if (p != 0) buf[wslot(kWN - p)] = zq[j];
+  }
+  __syncwarp();
+  wdft1023(buf, bt.tw, lane);
+  wsplit(buf, lane, hs, sc);
+  // ---- T (ar_forward, transforms.hpp:148-160): w_0 = a0, w_{n-1} = a1,
+  // interior DST + ramp a0 (1 - k/(n-1)) + a1 k/(n-1); row-major stores
+  double* out = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c;
+#pragma unroll 4
+  for (int j = 0; j < 32; ++j) {
+    const int k = lane + 32 * j;
+    const double2 o = buf[oslot(k)];
+    const double t1 = (double)k * ri;
+    double wa = o.x + a0a * (1.0 - t1) + a1a * t1;
+    double wb = o.y + a0b * (1.0 - t1) + a1b * t1;
+    if (k == 0) { wa = a0a; wb = a0b; }
+    if (k == n - 1) { wa = a1a; wb = a1b; }
+    if (hb) *reinterpret_cast<double2*>(out + (size_t)k * n2) = make_double2(wa, wb);
+    else out[(size_t)k * n2] = wa;
+  }
+}
+
+}  // namespace
+
+// Warp-owned column half of D for n1 = 1024 (direct 1023-point core); returns
+// the CTA count, or -1 when the shape is not this kernel's.
+int launch_dst_tcols_w(const SpecArgs& a, cudaStream_t s) {
+  if (a.n1 != 1024 || a.blue1.N != kWN) return -1;
+  const size_t bytes = (size_t)kWWarps * kWLine * sizeof(double2);
+  static AttrOnce attr;
+  if (!attr.ensure(dst_tcols_w, bytes)) return -1;
+  dim3 grid((a.n2 + 2 * kWWarps - 1) / (2 * kWWarps), a.batch);
+  dst_tcols_w<<<grid, 32 * kWWarps, bytes, s>>>(a);
+  return (int)grid.x;
+}
+
+}  // namespace dbx
