@@ -43,6 +43,11 @@ constexpr int kWWarps = 4;    // warps (column pairs) per CTA
 #ifndef DBX_WDST_MINB
 #define DBX_WDST_MINB 2
 #endif
+// L2 prefetch (cp.async.bulk.prefetch.L2) of the input lines of the CTA this
+// many resident waves ahead (0 = off)
+#ifndef DBX_WDST_PREFETCH
+#define DBX_WDST_PREFETCH 0
+#endif
 
 // Two layouts share a warp's line.  DFT data at slot p (level 1 reads lanes at
 // consecutive p, level 2 lanes at stride 31: both hit 8 distinct 16-byte bank
@@ -258,23 +263,41 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
   const double* __restrict__ sn = bt.sn;
   // ---- T~ (ar_inverse, transforms.hpp:163-173) of columns c, c+1 (contiguous
   // in u^T): lane L fills the mirror pairs p = L + 32 j <= N/2 and N - p
+#if DBX_WDST_PREFETCH > 0
+  if (lane == 0) {
+    const long cta = (long)b * gridDim.x + blockIdx.x + (long)DBX_WDST_PREFETCH * 148 * DBX_WDST_MINB;
+    const long pb = cta / gridDim.x, pc = 2 * (kWWarps * (cta - pb * gridDim.x) + w);
+    if (pb < a.batch && pc + 1 < n2) prefetch_l2(a.in + (size_t)pb * N + (size_t)pc * n, (unsigned)(2 * n * 8));
+  }
+#endif
   const double* ua = a.in + (size_t)b * N + (size_t)c * n;
   const double* ub = hb ? ua + n : ua;
   const double x0a = __ldg(ua), xea = __ldg(ua + n - 1), x0b = __ldg(ub), xeb = __ldg(ub + n - 1);
   const double sa = x0a + xea, sb = x0b + xeb, da = x0a - xea, db = x0b - xeb;
-#pragma unroll 4
+  // every global load of the fill in flight at once (one HBM latency per
+  // item instead of one per unrolled group)
+  double ap[16], aq[16], bp[16], bq[16], sv[16];
+#pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int p = lane + 32 * j, q = kWN - p;  // p in [0, 511], q in [512, 1023]
+    ap[j] = __ldg(ua + p);
+    aq[j] = __ldg(ua + q);
+    bp[j] = __ldg(ub + p);
+    bq[j] = __ldg(ub + q);
+    sv[j] = __ldg(sn + p);
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int p = lane + 32 * j, q = kWN - p;
+    const double r = fma(-2.0 * ri, (double)p, 1.0), s = sv[j];
+    const double Aa = ap[j] + aq[j] - sa, Ba = (ap[j] - aq[j]) - da * r;  // sd(j) of pk_fill
+    const double Ab = bp[j] + bq[j] - sb, Bb = (bp[j] - bq[j]) - db * r;
     if (p == 0) {
       buf[wslot(0)] = make_double2(0.0, 0.0);
-      continue;
+    } else {
+      buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), hb ? fma(s, Ab, 0.5 * Bb) : 0.0);
+      buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), hb ? fma(s, Ab, -0.5 * Bb) : 0.0);
     }
-    const double ap = __ldg(ua + p), aq = __ldg(ua + q), bp = __ldg(ub + p), bq = __ldg(ub + q);
-    const double s = __ldg(sn + p), r = fma(-2.0 * ri, (double)p, 1.0);
-    const double Aa = ap + aq - sa, Ba = (ap - aq) - da * r;  // sd(j) of pk_fill
-    const double Ab = bp + bq - sb, Bb = (bp - bq) - db * r;
-    buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), hb ? fma(s, Ab, 0.5 * Bb) : 0.0);
-    buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), hb ? fma(s, Ab, -0.5 * Bb) : 0.0);
   }
   __syncwarp();
   wdft1023(buf, bt.tw, lane);
@@ -310,7 +333,7 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
   // ---- T (ar_forward, transforms.hpp:148-160): w_0 = a0, w_{n-1} = a1,
   // interior DST + ramp a0 (1 - k/(n-1)) + a1 k/(n-1); row-major stores
   double* out = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c;
-#pragma unroll 4
+#pragma unroll 8
   for (int j = 0; j < 32; ++j) {
     const int k = lane + 32 * j;
     const double2 o = buf[oslot(k)];
