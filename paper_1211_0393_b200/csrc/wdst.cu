@@ -40,8 +40,15 @@ constexpr int kWLine = 1024;  // double2 slots per warp line
 constexpr int kWWarps = 4;    // warps (column pairs) per CTA
 // CTAs per SM the register budget is sized for: 2 -> up to 255 registers (the
 // DFT-31 row keeps 30 folded values + 30 constants live), 3 -> 168 (spills)
+// Component-split DFT (-DDBX_WDST_RI=1, 168 registers, 12 warps/SM): measured
+// 0.819 ms per C3 launch vs 0.762 for the complex-per-lane form at 8 warps/SM
+// (and 0.794 for the split form at 8 warps) — the partner shuffles cost more
+// than the extra occupancy buys.  Off by default.
+#ifndef DBX_WDST_RI
+#define DBX_WDST_RI 0
+#endif
 #ifndef DBX_WDST_MINB
-#define DBX_WDST_MINB 2
+#define DBX_WDST_MINB (DBX_WDST_RI ? 3 : 2)
 #endif
 // L2 prefetch (cp.async.bulk.prefetch.L2) of the input lines of the CTA this
 // many resident waves ahead (0 = off)
@@ -197,6 +204,151 @@ __device__ __forceinline__ void wdft1023(double2* buf, const double2* __restrict
   __syncwarp();
 }
 
+// ---------------------------------------------------------------------------
+// Component-split DFT_1023 (opt-in DBX_WDST_RI): each row DFT runs on a LANE PAIR,
+// lane 2r holding the real and lane 2r+1 the imaginary component of every
+// value of row r.  Real linear maps act on each component alone; the only
+// re/im mixing — multiplication by S i (the sine half of a symmetric-pair DFT,
+// the DFT-3's u) and the twiddle product — takes one __shfl_xor with the
+// partner.  Both lanes run the same instructions on different data, so a
+// lane holds 31-33 doubles of a row instead of 62-66 complex halves: the
+// kernel fits 168 registers (3 CTAs = 12 warps per SM, the shared-memory cap)
+// without spills.  16 rows per warp pass: level 1 in two passes (31 rows),
+// level 2 in two passes (rows 0..31) + the cooperative row 32.
+struct Ri {
+  int h;            // 0: real lane, 1: imaginary lane
+  double sgn_si;    // S i v on this lane's component = sgn_si * partner (S = -1)
+  double sgn_mul;   // (v w).comp = own w.x + sgn_mul * partner w.y
+};
+__device__ __forceinline__ double partner(double v) { return __shfl_xor_sync(0xffffffffu, v, 1); }
+// comp of S i v (S = -1: -i v = (v.y, -v.x))
+__device__ __forceinline__ double si_comp(const Ri& R, double v) { return R.sgn_si * partner(v); }
+
+__device__ __forceinline__ void level1_row_ri(double* bd, const double2* __restrict__ tw, int n2, bool act,
+                                              const Ri& R, double* v) {
+  constexpr double c3 = 0.86602540378443864676372317075293618;  // sqrt(3)/2
+#pragma unroll
+  for (int b = 0; b < 11; ++b) {
+    const int i0 = (3 * b) % 33, i1 = (11 + 3 * b) % 33, i2 = (22 + 3 * b) % 33;
+    const double t = v[i1] + v[i2];
+    const double u = si_comp(R, c3 * (v[i1] - v[i2]));
+    const double m = v[i0] - 0.5 * t;
+    v[i0] = v[i0] + t;
+    v[i1] = m + u;
+    v[i2] = m - u;
+  }
+  auto put = [&](int k1, double x) {
+    if (k1 != 0) {
+      const double2 w = __ldg(tw + n2 * k1);  // n2 k1 <= 990
+      x = fma(x, w.x, R.sgn_mul * partner(x) * w.y);
+    }
+    if (act) bd[2 * (31 * k1 + n2) + R.h] = x;
+  };
+#pragma unroll
+  for (int ka = 0; ka < 3; ++ka) {
+    double* u[11];
+#pragma unroll
+    for (int b = 0; b < 11; ++b) u[b] = &v[(11 * ka + 3 * b) % 33];
+    const double x0 = *u[0];
+    double sum = x0;
+#pragma unroll
+    for (int j = 1; j <= 5; ++j) {
+      const double pp = *u[j] + *u[11 - j], mm = *u[j] - *u[11 - j];
+      *u[j] = pp;
+      *u[11 - j] = mm;
+      sum += pp;
+    }
+    put((22 * ka) % 33, sum);
+#pragma unroll
+    for (int k = 1; k <= 5; ++k) {
+      double A = x0, B = 0.0;
+#pragma unroll
+      for (int j = 1; j <= 5; ++j) {
+        const int e = (j * k) % 11;
+        A = fma(ccs<11>(e), *u[j], A);
+        B = fma(scs<11>(e), *u[11 - j], B);
+      }
+      const double sb = si_comp(R, B);
+      put((22 * ka + 12 * k) % 33, A + sb);
+      put((22 * ka + 12 * (11 - k)) % 33, A - sb);
+    }
+  }
+}
+
+__device__ __forceinline__ void wdft1023_ri(double2* buf, const double2* __restrict__ tw, int lane) {
+  Ri R;
+  R.h = lane & 1;
+  R.sgn_si = R.h ? -1.0 : 1.0;
+  R.sgn_mul = R.h ? 1.0 : -1.0;
+  double* bd = reinterpret_cast<double*>(buf);
+  const int r = lane >> 1;
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    const int n2 = 16 * pass + r;
+    const bool act = n2 < 31;
+    const int nr = act ? n2 : 30;  // lanes without a row shadow row 30 (shuffle partners, no stores)
+    double v[33];
+#pragma unroll
+    for (int n1 = 0; n1 < 33; ++n1) v[n1] = bd[2 * (31 * n1 + nr) + R.h];
+    level1_row_ri(bd, tw, nr, act, R, v);
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    const int base = 31 * (16 * pass + r);
+    double v[31];
+#pragma unroll
+    for (int j = 0; j < 31; ++j) v[j] = bd[2 * (base + j) + R.h];
+    const double x0 = v[0];
+    double sum = x0;
+#pragma unroll
+    for (int j = 1; j <= 15; ++j) {
+      const double a = v[j] + v[31 - j], b = v[j] - v[31 - j];
+      v[j] = a;
+      v[31 - j] = b;
+      sum += a;
+    }
+    bd[2 * base + R.h] = sum;
+#pragma unroll
+    for (int k = 1; k <= 15; ++k) {
+      double A = x0, B = 0.0;
+#pragma unroll
+      for (int j = 1; j <= 15; ++j) {
+        const int e = (j * k) % 31;
+        A = fma(ccs<31>(e), v[j], A);
+        B = fma(scs<31>(e), v[31 - j], B);
+      }
+      const double sb = si_comp(R, B);
+      bd[2 * (base + k) + R.h] = A + sb;
+      bd[2 * (base + 31 - k) + R.h] = A - sb;
+    }
+  }
+  // row k1 = 32: one complex output per lane (as in wdft1023)
+  double2 X = make_double2(0.0, 0.0);
+  {
+    constexpr int S = -1;
+    const double2 y0 = buf[992];
+    double2 A = y0, B = make_double2(0.0, 0.0);
+    int e = 0;
+#pragma unroll
+    for (int j = 1; j <= 15; ++j) {
+      e += lane;
+      e = e >= 31 ? e - 31 : e;
+      const double2 yj = buf[992 + j], ym = buf[992 + 31 - j];
+      const double2 w = __ldg(tw + 33 * e);
+      const double2 a = cadd(yj, ym), b = csub(yj, ym);
+      A.x = fma(w.x, a.x, A.x);
+      A.y = fma(w.x, a.y, A.y);
+      B.x = fma(-w.y, b.x, B.x);
+      B.y = fma(-w.y, b.y, B.y);
+    }
+    X = cadd(A, fft::mul_si<S>(B));
+  }
+  __syncwarp();
+  if (lane < 31) buf[992 + lane] = X;
+  __syncwarp();
+}
+
 // Split + odd scan in place: the DFT outputs Y_l (slot wpos(l)) become the
 // two real output lines, out[k] = (X^a_k, X^b_k) at slot(k), k in [0, 1024),
 // in the scaled DST-I convention of pk_split2 + odd_scans2.  Lane L owns the
@@ -247,6 +399,12 @@ __device__ __forceinline__ void wsplit(double2* buf, int lane, double hs, double
   __syncwarp();
 }
 
+#if DBX_WDST_RI
+#define WDFT wdft1023_ri
+#else
+#define WDFT wdft1023
+#endif
+
 __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecArgs a) {
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
@@ -276,7 +434,7 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
   const double sa = x0a + xea, sb = x0b + xeb, da = x0a - xea, db = x0b - xeb;
   // every global load of the fill in flight at once (one HBM latency per
   // item instead of one per unrolled group)
-  double ap[16], aq[16], bp[16], bq[16], sv[16];
+  double ap[16], aq[16], bp[16], bq[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int p = lane + 32 * j, q = kWN - p;  // p in [0, 511], q in [512, 1023]
@@ -284,12 +442,11 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
     aq[j] = __ldg(ua + q);
     bp[j] = __ldg(ub + p);
     bq[j] = __ldg(ub + q);
-    sv[j] = __ldg(sn + p);
   }
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int p = lane + 32 * j, q = kWN - p;
-    const double r = fma(-2.0 * ri, (double)p, 1.0), s = sv[j];
+    const double r = fma(-2.0 * ri, (double)p, 1.0), s = __ldg(sn + p);
     const double Aa = ap[j] + aq[j] - sa, Ba = (ap[j] - aq[j]) - da * r;  // sd(j) of pk_fill
     const double Ab = bp[j] + bq[j] - sb, Bb = (bp[j] - bq[j]) - db * r;
     if (p == 0) {
@@ -300,7 +457,7 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
     }
   }
   __syncwarp();
-  wdft1023(buf, bt.tw, lane);
+  WDFT(buf, bt.tw, lane);
   wsplit(buf, lane, hs, sc);
   // ---- v = u o d (d^T rows c, c+1: L2-resident, shared by the batch), then
   // the T fill from the same mirror pairs (reads and writes slots p, N - p only)
@@ -308,27 +465,37 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
   const double* dB = hb ? dA + n : dA;
   const double a0a = x0a * __ldg(dA), a1a = xea * __ldg(dA + n - 1);
   const double a0b = x0b * __ldg(dB), a1b = xeb * __ldg(dB + n - 1);
-  double2 zp[16], zq[16];
+  // d loads all in flight first; then per mirror row j: read out[p], out[q]
+  // (oslot), syncwarp, write z_p, z_q (slot p, q).  Every slot a lane writes
+  // in row j aliases only reads of the same row j (oslot permutes within
+  // 8-aligned groups keyed by k >> 5), so one __syncwarp per row orders them.
+  double dpa[16], dqa[16], dpb[16], dqb[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int p = lane + 32 * j, q = kWN - p;
+    dpa[j] = __ldg(dA + p);
+    dqa[j] = __ldg(dA + q);
+    dpb[j] = __ldg(dB + p);
+    dqb[j] = __ldg(dB + q);
+  }
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int p = lane + 32 * j, q = kWN - p;  // p = 0: z_0 = 0 (q = 1023 is no DFT slot)
     const double2 op = buf[oslot(p)], oq = buf[oslot(q)];
-    const double mpa = op.x * __ldg(dA + p), mqa = oq.x * __ldg(dA + q);
-    const double mpb = op.y * __ldg(dB + p), mqb = oq.y * __ldg(dB + q);
+    const double mpa = op.x * dpa[j], mqa = oq.x * dqa[j];
+    const double mpb = op.y * dpb[j], mqb = oq.y * dqb[j];
     const double s = __ldg(sn + p);
     const double Aa = mpa + mqa, Ba = mpa - mqa, Ab = mpb + mqb, Bb = mpb - mqb;
-    zp[j] = p == 0 ? make_double2(0.0, 0.0) : make_double2(fma(s, Aa, 0.5 * Ba), fma(s, Ab, 0.5 * Bb));
-    zq[j] = make_double2(fma(s, Aa, -0.5 * Ba), fma(s, Ab, -0.5 * Bb));
+    __syncwarp();
+    if (p == 0) {
+      buf[wslot(0)] = make_double2(0.0, 0.0);
+    } else {
+      buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), fma(s, Ab, 0.5 * Bb));
+      buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), fma(s, Ab, -0.5 * Bb));
+    }
   }
   __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int p = lane + 32 * j;
-    buf[wslot(p)] = zp[j];
-    if (p != 0) buf[wslot(kWN - p)] = zq[j];
-  }
-  __syncwarp();
-  wdft1023(buf, bt.tw, lane);
+  WDFT(buf, bt.tw, lane);
   wsplit(buf, lane, hs, sc);
   // ---- T (ar_forward, transforms.hpp:148-160): w_0 = a0, w_{n-1} = a1,
   // interior DST + ramp a0 (1 - k/(n-1)) + a1 k/(n-1); row-major stores
