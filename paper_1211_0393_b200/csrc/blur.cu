@@ -68,6 +68,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 }
 
 __global__ void __launch_bounds__(kThreads) blur_ar_kernel(BlurArgs a) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.z;
   if (a.st && a.st[b].done) return;
   extern __shared__ double smem[];
@@ -171,7 +172,7 @@ void launch_blur(const BlurArgs& a, cudaStream_t s, int* ctas_per_image) {
   static AttrOnce attr;
   attr.ensure(blur_ar_kernel, 227 * 1024);
   if (ctas_per_image) *ctas_per_image = grid.x * grid.y;
-  blur_ar_kernel<<<grid, kThreads, smem, s>>>(a);
+  launch_k(blur_ar_kernel, grid, kThreads, smem, s, a);
 }
 
 }  // namespace dbx

@@ -42,6 +42,7 @@ __device__ double partial_total(const double* p, int cnt) {
 
 // alpha = gamma / ||q||^2 from the q-blur's ||r||^2 slot (q' = -A p there)
 __global__ void cg_alpha_kernel(const ImgState* st, CgScalars* cs, Partials pt, int cnt) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.x;
   if (st[b].done) return;
   const double qq = partial_total(pt.p + ((size_t)b * NUM_SLOTS + SLOT_R2) * pt.cap, cnt);
@@ -53,6 +54,7 @@ __global__ void cg_alpha_kernel(const ImgState* st, CgScalars* cs, Partials pt, 
 __global__ void cg_update_kernel(const double* X3, const ImgState* st, const CgScalars* cs, const double* p,
                                  const double* qn, double* r, const double* f, int batch, size_t N, Partials pt,
                                  double* x_out) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.y;
   if (st[b].done) return;
   const double al = cs[b].alpha;
@@ -84,6 +86,7 @@ __global__ void cg_update_kernel(const double* X3, const ImgState* st, const CgS
 // per-block partials of <s, z>
 __global__ void cg_dot_kernel(const ImgState* st, const double* s, const double* z, size_t N, double* part,
                               int cap) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.y;
   if (st && st[b].done) return;
   const size_t o = (size_t)b * N;
@@ -96,6 +99,7 @@ __global__ void cg_dot_kernel(const ImgState* st, const double* s, const double*
 
 // gamma' = sum; beta = gamma' / gamma; gamma = gamma' (init: beta = 0)
 __global__ void cg_beta_kernel(const ImgState* st, CgScalars* cs, const double* part, int cap, int cnt, int init) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.x;
   if (st[b].done) return;
   const double gn = partial_total(part + (size_t)b * cap, cnt);
@@ -107,6 +111,7 @@ __global__ void cg_beta_kernel(const ImgState* st, CgScalars* cs, const double* 
 
 // p = z + beta p
 __global__ void cg_xpay_kernel(const ImgState* st, const CgScalars* cs, const double* z, double* p, size_t N) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.y;
   if (st[b].done) return;
   const double be = cs[b].beta;
@@ -125,31 +130,31 @@ int grid_x(size_t N, int cap) {
 }  // namespace
 
 void launch_cg_alpha(const ImgState* st, CgScalars* cs, Partials pt, int cnt, int batch, cudaStream_t s) {
-  cg_alpha_kernel<<<batch, kT, 0, s>>>(st, cs, pt, cnt);
+  launch_k(cg_alpha_kernel, batch, kT, 0, s, st, cs, pt, cnt);
 }
 
 int launch_cg_update(const double* X3, const ImgState* st, const CgScalars* cs, const double* p, const double* qn,
                      double* r, const double* f, int batch, size_t N, Partials pt, cudaStream_t s) {
   const int gx = grid_x(N, pt.cap);
-  cg_update_kernel<<<dim3(gx, batch), kT, 0, s>>>(X3, st, cs, p, qn, r, f, batch, N, pt, const_cast<double*>(X3));
+  launch_k(cg_update_kernel, dim3(gx, batch), kT, 0, s, X3, st, cs, p, qn, r, f, batch, N, pt, const_cast<double*>(X3));
   return gx;
 }
 
 int launch_cg_dot(const ImgState* st, const double* a, const double* b, int batch, size_t N, double* part, int cap,
                   cudaStream_t s) {
   const int gx = grid_x(N, cap);
-  cg_dot_kernel<<<dim3(gx, batch), kT, 0, s>>>(st, a, b, N, part, cap);
+  launch_k(cg_dot_kernel, dim3(gx, batch), kT, 0, s, st, a, b, N, part, cap);
   return gx;
 }
 
 void launch_cg_beta(const ImgState* st, CgScalars* cs, const double* part, int cap, int cnt, int init, int batch,
                     cudaStream_t s) {
-  cg_beta_kernel<<<batch, kT, 0, s>>>(st, cs, part, cap, cnt, init);
+  launch_k(cg_beta_kernel, batch, kT, 0, s, st, cs, part, cap, cnt, init);
 }
 
 void launch_cg_xpay(const ImgState* st, const CgScalars* cs, const double* z, double* p, int batch, size_t N,
                     cudaStream_t s) {
-  cg_xpay_kernel<<<dim3(grid_x(N, 1 << 30), batch), kT, 0, s>>>(st, cs, z, p, N);
+  launch_k(cg_xpay_kernel, dim3(grid_x(N, 1 << 30), batch), kT, 0, s, st, cs, z, p, N);
 }
 
 }  // namespace dbx

@@ -24,6 +24,15 @@
 
 using namespace dbx;
 
+// Off by default: measured A/B (profiles/r02_pdl_ab.txt) put every config
+// behind plain stream order with it on (C1 1468 vs 1564, C2 2972 vs 3695, C3
+// 22562 vs 23196 Mpx-it/s): the dependents' early-resident CTAs cost more than
+// the launch gaps they hide.  DBX_PDL=1 turns it on.
+bool dbx::pdl_enabled() {
+  static const bool on = [] { const char* e = getenv("DBX_PDL"); return e && e[0] == '1'; }();
+  return on;
+}
+
 namespace {
 
 thread_local std::string g_err;

@@ -33,6 +33,40 @@ struct AttrOnce {
   }
 };
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Every kernel of the solver loop starts with DBX_PDL_WAIT(): wait until the
+// previous grid of the stream has completed and its memory is visible, then
+// let the next grid begin launching.  Launched through launch_k (attribute
+// cudaLaunchAttributeProgrammaticStreamSerialization; captured into the CUDA
+// graph as programmatic edges), a kernel's CTAs are scheduled onto the SMs
+// the previous kernel's tail leaves idle and sit at the wait, so the launch
+// latency and prologue of every node overlap the previous node's drain —
+// the per-node gap that dominates small images (C1: 7 nodes per iteration).
+// A plainly launched kernel passes the wait immediately.
+#define DBX_PDL_WAIT()                                      \
+  do {                                                      \
+    asm volatile("griddepcontrol.wait;" ::: "memory");      \
+    asm volatile("griddepcontrol.launch_dependents;" ::);   \
+  } while (0)
+
+bool pdl_enabled();  // DBX_PDL=1 turns the attribute on (off by default: measured slower)
+
+template <typename... KP, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // Per-image iteration state, resident in HBM for the whole run.  The three
 // iterate buffers X[0..2] are used round-robin so that tracking the best
 // iterate (solver.hpp:111-119) never copies x: `best` pins a buffer, `cur`

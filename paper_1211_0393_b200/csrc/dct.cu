@@ -42,6 +42,7 @@ __device__ __forceinline__ int dct_perm(int n, int m) {  // position n of v hold
 
 template <int M>
 __global__ void __launch_bounds__(DctCfg<M>::NT) dct_rows(SpecArgs a) {
+  DBX_PDL_WAIT();
   using C = DctCfg<M>;
   constexpr int T = C::T, G = C::G, NT = C::NT;
   const int b = blockIdx.y;
@@ -153,7 +154,7 @@ int dct_launch(const SpecArgs& a, cudaStream_t s) {
   static AttrOnce attr;
   if (!attr.ensure(dct_rows<L>, C::bytes)) return -1;
   dim3 grid((a.n1 + 2 * C::G - 1) / (2 * C::G), a.batch);
-  dct_rows<L><<<grid, C::NT, C::bytes, s>>>(a);
+  launch_k(dct_rows<L>, grid, C::NT, C::bytes, s, a);
   return (int)grid.x;
 }
 

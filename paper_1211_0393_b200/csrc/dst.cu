@@ -231,6 +231,7 @@ __device__ __forceinline__ double kind_out(int kind, const double* o, int k, int
 // (store / Hadamard / r = g - v with ||r||^2 / x += tau v with norms).
 template <int M, int CORE>
 __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_rows(SpecArgs a) {
+  DBX_PDL_WAIT();
   using C = DstCfg<M, CORE>;
   constexpr int T = C::T, G = C::G, NT = C::NT;
   const int b = blockIdx.y;
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_rows(SpecArgs a) {
 // T in place on it.
 template <int M, int CORE>
 __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_cols(SpecArgs a) {
+  DBX_PDL_WAIT();
   using C = DstCfg<M, CORE>;
   constexpr int T = C::T, G = C::G, NT = C::NT;
   const int b = blockIdx.y;
@@ -346,7 +348,7 @@ int rows_launch(const SpecArgs& a, cudaStream_t s) {
   static AttrOnce attr;
   if (!attr.ensure(dst_rows<L, CORE>, C::bytes)) return -1;
   dim3 grid((a.n1 + 2 * C::G - 1) / (2 * C::G), a.batch);
-  dst_rows<L, CORE><<<grid, C::NT, C::bytes, s>>>(a);
+  launch_k(dst_rows<L, CORE>, grid, C::NT, C::bytes, s, a);
   return (int)grid.x;
 }
 
@@ -356,7 +358,7 @@ int cols_launch(const SpecArgs& a, cudaStream_t s) {
   static AttrOnce attr;
   if (!attr.ensure(dst_cols<L, CORE>, C::bytes)) return -1;
   dim3 grid((a.n2 + 2 * C::G - 1) / (2 * C::G), a.batch);
-  dst_cols<L, CORE><<<grid, C::NT, C::bytes, s>>>(a);
+  launch_k(dst_cols<L, CORE>, grid, C::NT, C::bytes, s, a);
   return (int)grid.x;
 }
 

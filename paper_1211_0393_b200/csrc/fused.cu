@@ -159,6 +159,7 @@ __device__ __forceinline__ void conv_fwd_rows(double2* buf, const double* rowa, 
 // (packed real DST).  u is written transposed (u^T[k][row], 32-byte sectors).
 template <int L2, int M, bool BLUE, bool SEP = false>
 __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, SEP ? DBX_TT_MINB : 2) rows_ainv_tt(SpecArgs a) {
+  DBX_PDL_WAIT();
   using F = Fused<L2, M, BLUE>;
   constexpr int NT = F::NT, TD = F::TD, LS = F::LSO, LMAX = F::LMAX;
   const int b = blockIdx.y;
@@ -258,6 +259,7 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, SEP ? DBX_TT_MINB : 2)
 // packed row FFTs of x_k (conv line g = rows 2g, 2g+1) -> Z^T.
 template <int L2, int M, bool BLUE, bool SEP = false>
 __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(SpecArgs a) {
+  DBX_PDL_WAIT();
   using F = Fused<L2, M, BLUE>;
   constexpr int NT = F::NT, TD = F::TD, LS = F::LS, LSO = F::LSO, LMAX = F::LMAX;
   const int b = blockIdx.y;
@@ -405,6 +407,7 @@ struct RsCfg {
 
 template <int L2>
 __global__ void __launch_bounds__(RsCfg<L2>::NT, 2) rows_ainv_resid(SpecArgs a) {
+  DBX_PDL_WAIT();
   using C = RsCfg<L2>;
   constexpr int T = C::T, NT = C::NT, LS = C::LS;
   const int b = blockIdx.y;
@@ -499,6 +502,7 @@ __host__ __device__ constexpr size_t resid_sep_bytes(int n2, int q2) {
 }
 
 __global__ void __launch_bounds__(kResidNT, 4) rows_resid_sep(SpecArgs a) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 sm[];
@@ -593,6 +597,7 @@ struct TcolSmem {
 
 template <int M, bool BLUE>
 __global__ void __launch_bounds__(2 * fused_td(M), DBX_TC_MINB) dst_tcols(SpecArgs a) {
+  DBX_PDL_WAIT();
   using S = TcolSmem<M, BLUE>;
   constexpr int TD = S::TD, NT = 2 * TD, LS = S::LS, LSO = S::LSO, LMAX = S::LMAX;
   const int b = blockIdx.y;
@@ -731,7 +736,7 @@ int fused_launch(K kernel, const SpecArgs& a, cudaStream_t s) {
   static AttrOnce attr;
   if (!attr.ensure(kernel, bytes)) return -1;
   dim3 grid((a.n1 + rows - 1) / rows, a.batch);
-  kernel<<<grid, nt, bytes, s>>>(a);
+  launch_k(kernel, grid, nt, bytes, s, a);
   return (int)grid.x;
 }
 
@@ -741,7 +746,7 @@ int tcols_launch(const SpecArgs& a, cudaStream_t s) {
   static AttrOnce attr;
   if (!attr.ensure(dst_tcols<M, BLUE>, SMP::bytes)) return -1;
   dim3 grid((a.n2 + 3) / 4, a.batch);
-  dst_tcols<M, BLUE><<<grid, 2 * SMP::TD, SMP::bytes, s>>>(a);
+  launch_k(dst_tcols<M, BLUE>, grid, 2 * SMP::TD, SMP::bytes, s, a);
   return (int)grid.x;
 }
 
@@ -782,7 +787,7 @@ int launch_fused(int which, const SpecArgs& a, cudaStream_t s) {
     const size_t bytes = resid_sep_bytes(a.n2, a.q2);
     if (!set_smem(rows_resid_sep, bytes)) return -1;
     dim3 grid((a.n1 + 3) / 4, a.batch);
-    rows_resid_sep<<<grid, kResidNT, bytes, s>>>(a);
+    launch_k(rows_resid_sep, grid, kResidNT, bytes, s, a);
     return (int)grid.x;
   }
   // warp-owned column half (wdst.cu) for 1024-point columns; DBX_WDST=0

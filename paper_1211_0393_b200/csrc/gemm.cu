@@ -76,6 +76,7 @@ struct Smem {
 
 template <int BM, int BN>
 __global__ void __launch_bounds__(kThreads) gemm_dmma_kernel(GemmArgs a) {
+  DBX_PDL_WAIT();
   constexpr int WM = BM / 2, WN = BN / 2;     // warp tile
   constexpr int TMI = WM / 8, TNI = WN / 8;   // 8x8 accumulators per warp
   const int b = blockIdx.z;
@@ -219,7 +220,7 @@ void launch_tile(const GemmArgs& a, cudaStream_t s, int* ctas_per_image) {
   once.ensure(gemm_dmma_kernel<BM, BN>, smem);
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.batch);
   if (ctas_per_image) *ctas_per_image = grid.x * grid.y;
-  gemm_dmma_kernel<BM, BN><<<grid, kThreads, smem, s>>>(a);
+  launch_k(gemm_dmma_kernel<BM, BN>, grid, kThreads, smem, s, a);
 }
 
 }  // namespace

@@ -91,6 +91,7 @@ __device__ double strided_sumsq(const double* p, size_t n) {
 // (deterministic; a single CTA per image left 148-SM HBM idle: 59 ms for one
 // 8192^2 image).
 __global__ void norms_partial_kernel(const double* g, const double* f, size_t N, size_t chunk, Partials pt) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.y, k = blockIdx.x;
   const size_t lo = (size_t)k * chunk, n = lo < N ? (N - lo < chunk ? N - lo : chunk) : 0;
   const double gs = strided_sumsq(g + (size_t)b * N + lo, n);
@@ -103,6 +104,7 @@ __global__ void norms_partial_kernel(const double* g, const double* f, size_t N,
 }
 
 __global__ void norms_init_kernel(Partials pt, int cnt, int has_f, ImgState* st) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.x;
   const double* P = pt.p + (size_t)b * NUM_SLOTS * pt.cap;
   double gs = 0.0, fs = 0.0;
@@ -117,6 +119,7 @@ __global__ void norms_init_kernel(Partials pt, int cnt, int has_f, ImgState* st)
 }
 
 __global__ void state_init_kernel(ImgState* st, int batch) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= batch) return;
   ImgState s = st[b];
@@ -140,6 +143,7 @@ __device__ double partial_sum(const double* p, int cnt) {
 // One CTA per image: reduce the fused-epilogue partials of iteration k and
 // apply the reference loop bookkeeping (solver.hpp:107-124).
 __global__ void finalize_kernel(FinalizeArgs a) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.x;
   ImgState* st = a.st + b;
   if (st->done) return;
@@ -182,6 +186,7 @@ __global__ void finalize_kernel(FinalizeArgs a) {
 
 __global__ void select_copy_kernel(const double* X3, const ImgState* st, int which_best,
                                    int batch, size_t N, double* out) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.y;
   const int idx = (which_best && st[b].best_iter > 0) ? st[b].best : st[b].cur;
   const double* src = X3 + ((size_t)idx * batch + b) * N;
@@ -193,6 +198,7 @@ __global__ void select_copy_kernel(const double* X3, const ImgState* st, int whi
 
 // out[c][r] = in[r][c] through a 32 x 33 shared tile (coalesced both ways).
 __global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out, int rows, int cols) {
+  DBX_PDL_WAIT();
   __shared__ double tile[32][33];
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   const size_t img = (size_t)blockIdx.z * rows * cols;  // batch of matrices
@@ -214,6 +220,7 @@ __global__ void transpose_kernel(const double* __restrict__ in, double* __restri
 // 2 x[rows-1] - x[rows-1-k] (k = 1..q).
 __global__ void slab_ar_rows_kernel(const double* __restrict__ x, double* __restrict__ ext, int rows, int n2,
                                     int q, int top, int bot) {
+  DBX_PDL_WAIT();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int k = blockIdx.y + 1;  // 1..q
   if (c >= n2) return;
@@ -222,6 +229,7 @@ __global__ void slab_ar_rows_kernel(const double* __restrict__ x, double* __rest
 }
 
 __global__ void zero_kernel(double* p, size_t n) {
+  DBX_PDL_WAIT();
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     p[i] = 0.0;
@@ -260,37 +268,37 @@ void launch_norms_init(const double* g, const double* f, int batch, size_t N, Im
   if (K > (size_t)pt.cap) K = pt.cap;
   if (K < 1) K = 1;
   const size_t chunk = (N + K - 1) / K;
-  norms_partial_kernel<<<dim3((unsigned)K, batch), 512, 0, s>>>(g, f, N, chunk, pt);
-  norms_init_kernel<<<batch, 256, 0, s>>>(pt, (int)K, f != nullptr, st);
+  launch_k(norms_partial_kernel, dim3((unsigned)K, batch), 512, 0, s, g, f, N, chunk, pt);
+  launch_k(norms_init_kernel, batch, 256, 0, s, pt, (int)K, f != nullptr, st);
 }
 
 void launch_finalize(const FinalizeArgs& a, cudaStream_t s) {
-  finalize_kernel<<<a.batch, 256, 0, s>>>(a);
+  launch_k(finalize_kernel, a.batch, 256, 0, s, a);
 }
 
 void launch_state_init(ImgState* st, int batch, cudaStream_t s) {
-  state_init_kernel<<<(batch + 127) / 128, 128, 0, s>>>(st, batch);
+  launch_k(state_init_kernel, (batch + 127) / 128, 128, 0, s, st, batch);
 }
 
 void launch_select_copy(const double* X3, const ImgState* st, int which_best, int batch,
                         size_t N, double* out, cudaStream_t s) {
   dim3 grid((unsigned)((N + 255) / 256 < 1024 ? (N + 255) / 256 : 1024), batch);
-  select_copy_kernel<<<grid, 256, 0, s>>>(X3, st, which_best, batch, N, out);
+  launch_k(select_copy_kernel, grid, 256, 0, s, X3, st, which_best, batch, N, out);
 }
 
 void launch_transpose(const double* in, double* out, int rows, int cols, cudaStream_t s, int batch) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32, batch);
-  transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols);
+  launch_k(transpose_kernel, grid, dim3(32, 8), 0, s, in, out, rows, cols);
 }
 
 void launch_slab_ar_rows(const double* x, double* ext, int rows, int n2, int q, int top, int bot, cudaStream_t s) {
   if (q <= 0 || !(top || bot)) return;
   dim3 grid((n2 + 255) / 256, q);
-  slab_ar_rows_kernel<<<grid, 256, 0, s>>>(x, ext, rows, n2, q, top, bot);
+  launch_k(slab_ar_rows_kernel, grid, 256, 0, s, x, ext, rows, n2, q, top, bot);
 }
 
 void launch_zero(double* p, size_t n, cudaStream_t s) {
-  zero_kernel<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(p, n);
+  launch_k(zero_kernel, (unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s, p, n);
 }
 
 }  // namespace dbx

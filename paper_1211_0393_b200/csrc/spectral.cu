@@ -36,6 +36,7 @@ namespace {
 template <int L2>
 __global__ void __launch_bounds__(lines_for(L2, kConvBudget, 8) * line_threads(L2, 8))
 conv_row_fwd(SpecArgs a) {
+  DBX_PDL_WAIT();
   constexpr int T = line_threads(L2, 8), G = lines_for(L2, kConvBudget, 8);
   using SM = ConvSmem<L2, G>;
   const int b = blockIdx.y;
@@ -86,6 +87,7 @@ conv_row_fwd(SpecArgs a) {
 template <int L1>
 __global__ void __launch_bounds__(lines_for(L1, kConvBudget, 8) * line_threads(L1, 8))
 conv_col(SpecArgs a) {
+  DBX_PDL_WAIT();
   constexpr int T = line_threads(L1, 8), G = lines_for(L1, kConvBudget, 8);
   constexpr int NT = T * G;
   using SM = ConvSmem<L1, G>;
@@ -218,6 +220,7 @@ conv_col(SpecArgs a) {
 template <int L2>
 __global__ void __launch_bounds__(lines_for(L2, kConvBudget, 8) * line_threads(L2, 8))
 conv_row_inv(SpecArgs a) {
+  DBX_PDL_WAIT();
   constexpr int T = line_threads(L2, 8), G = lines_for(L2, kConvBudget, 8);
   constexpr int NT = T * G;
   using SM = ConvSmem<L2, G>;
@@ -310,6 +313,7 @@ __device__ __forceinline__ int skew(int p) { return p + (p >> 3); }
 
 template <int Q>
 __global__ void __launch_bounds__(kSepNT, 2) conv_col_sep(SpecArgs a) {
+  DBX_PDL_WAIT();
   constexpr int NTAP = 2 * Q + 1, R = kSepR, CK = kSepCK;
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
@@ -444,6 +448,7 @@ __host__ __device__ constexpr int col_minb(int band) { return band <= 128 ? 4 : 
 // — the separate-pass path's direct separable blur (rows_sep_seg + this).
 template <int Q, int BAND, int MODE>
 __global__ void __launch_bounds__(kColNT, col_minb(BAND)) cols_sep_real(SpecArgs a, const ColTaps<2 * Q + 1> tp) {
+  DBX_PDL_WAIT();
   constexpr int NTAP = 2 * Q + 1, NL = BAND + 2 * Q, RT = kColRT;
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
@@ -544,6 +549,7 @@ __host__ __device__ constexpr int rowseg_ls(int q2) {
 
 template <int Q>
 __global__ void __launch_bounds__(kRowNT, 4) rows_sep_seg(SpecArgs a) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.z;
   if (a.st && a.st[b].done) return;
   extern __shared__ double smd[];
@@ -602,7 +608,7 @@ int launch_conv_row_fwd(const SpecArgs& a, cudaStream_t s) {
     static AttrOnce attr;                                                            \
     if (!attr.ensure(conv_row_fwd<L>, sm)) return -1;                            \
     dim3 grid((a.n1 + 2 * G - 1) / (2 * G), a.batch);                                    \
-    conv_row_fwd<L><<<grid, T * G, sm, s>>>(a);                                          \
+    launch_k(conv_row_fwd<L>, grid, T * G, sm, s, a);                                          \
     return (int)grid.x;                                                                  \
   }
   DBX_CONV_LIST(X)
@@ -627,7 +633,7 @@ int launch_cols_sep_real_t(const SpecArgs& a, cudaStream_t s) {
   const size_t sm = (size_t)(BAND + 2 * Q) * kColLD * 8;
   if (!set_smem(cols_sep_real<Q, BAND, MODE>, sm)) return -1;
   dim3 grid((a.n2 + kColW - 1) / kColW, a.batch, (a.n1 + BAND - 1) / BAND);
-  cols_sep_real<Q, BAND, MODE><<<grid, kColNT, sm, s>>>(a, tp);
+  launch_k(cols_sep_real<Q, BAND, MODE>, grid, kColNT, sm, s, a, tp);
   return MODE == 2 ? (int)(grid.x * grid.z) : (int)grid.x;
 }
 
@@ -664,8 +670,8 @@ bool rows_sep_supported(int q2) { return q2 == 7 || q2 == 15; }
 int launch_rows_sep_seg(const SpecArgs& a, cudaStream_t s) {
   dim3 grid((a.n2 + kRowSeg - 1) / kRowSeg, (a.n1 + 3) / 4, a.batch);
   const size_t sm = (size_t)4 * rowseg_ls(a.q2) * 8;
-  if (a.q2 == 15) rows_sep_seg<15><<<grid, kRowNT, sm, s>>>(a);
-  else if (a.q2 == 7) rows_sep_seg<7><<<grid, kRowNT, sm, s>>>(a);
+  if (a.q2 == 15) launch_k(rows_sep_seg<15>, grid, kRowNT, sm, s, a);
+  else if (a.q2 == 7) launch_k(rows_sep_seg<7>, grid, kRowNT, sm, s, a);
   else return -1;
   return (int)(grid.x * grid.y);
 }
@@ -679,7 +685,7 @@ int launch_conv_col(const SpecArgs& a, cudaStream_t s) {
     if (a.q1 == (Q)) {                                                                   \
       if (!set_smem(conv_col_sep<Q>, sm)) return -1;                                     \
       dim3 grid((a.conv.Lh + kSepCK - 1) / kSepCK, a.batch, nb);                         \
-      conv_col_sep<Q><<<grid, kSepNT, sm, s>>>(a);                                       \
+      launch_k(conv_col_sep<Q>, grid, kSepNT, sm, s, a);                                       \
       return (int)grid.x;                                                                \
     }
     DBX_SEP_LIST(X)
@@ -693,7 +699,7 @@ int launch_conv_col(const SpecArgs& a, cudaStream_t s) {
     static AttrOnce attr;                                                            \
     if (!attr.ensure(conv_col<L>, sm)) return -1;                                \
     dim3 grid((a.conv.Lh + G - 1) / G, a.batch);                                         \
-    conv_col<L><<<grid, T * G, sm, s>>>(a);                                              \
+    launch_k(conv_col<L>, grid, T * G, sm, s, a);                                              \
     return (int)grid.x;                                                                  \
   }
   DBX_CONV_LIST(X)
@@ -710,7 +716,7 @@ int launch_conv_row_inv(const SpecArgs& a, cudaStream_t s) {
     static AttrOnce attr;                                                            \
     if (!attr.ensure(conv_row_inv<L>, sm)) return -1;                            \
     dim3 grid((a.n1 + 2 * G - 1) / (2 * G), a.batch);                                    \
-    conv_row_inv<L><<<grid, T * G, sm, s>>>(a);                                          \
+    launch_k(conv_row_inv<L>, grid, T * G, sm, s, a);                                          \
     return (int)grid.x;                                                                  \
   }
   DBX_CONV_LIST(X)

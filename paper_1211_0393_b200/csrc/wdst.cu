@@ -406,6 +406,7 @@ __device__ __forceinline__ void wsplit(double2* buf, int lane, double hs, double
 #endif
 
 __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecArgs a) {
+  DBX_PDL_WAIT();
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 wsm[];
@@ -524,7 +525,7 @@ int launch_dst_tcols_w(const SpecArgs& a, cudaStream_t s) {
   static AttrOnce attr;
   if (!attr.ensure(dst_tcols_w, bytes)) return -1;
   dim3 grid((a.n2 + 2 * kWWarps - 1) / (2 * kWWarps), a.batch);
-  dst_tcols_w<<<grid, 32 * kWWarps, bytes, s>>>(a);
+  launch_k(dst_tcols_w, grid, 32 * kWWarps, bytes, s, a);
   return (int)grid.x;
 }
 

@@ -4,7 +4,7 @@ CPU: the shape-parameter export reproduces dbx_gen_scene's draws, and the
 host mt19937_64 stream matches the C++-standard known answer.  GPU: the device
 mt19937_64 stream equals std::mt19937_64 word for word (lengths around the
 312-word block), and dbx_gen_honest_device matches the host generator — f_true
-bit for bit, g to rounding — on C1 at full size, on the sinusoid-background C4
+bit for bit, g to rounding (<= 1e-12 relative) — on C1 at full size, on the sinusoid-background C4
 scene and on the full 8192^2 C5 canvas (the size the device path exists for)."""
 import ctypes as C
 import time
@@ -68,8 +68,10 @@ def _compare(cfg, n):
     else:
         # shapes bit for bit; the smooth background through device sin (<= 1 ulp)
         assert np.abs(f_d - f_h).max() <= 4e-16 * (1.0 + np.abs(f_h).max())
+    # noise: device libm (<= 1 ulp) and the norm reductions' order (rescale
+    # factor level ||g|| / ||eta|| over up to 67M terms) — rounding level
     rel = np.linalg.norm(g_d - g_h) / np.linalg.norm(g_h)
-    assert rel <= 1e-14, rel
+    assert rel <= 1e-12, rel
     return secs
 
 
