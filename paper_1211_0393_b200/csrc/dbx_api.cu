@@ -374,6 +374,11 @@ struct dbx_plan {
     return D.t;
   }
 
+  // DBX_DST_TDT=0: the column half of D as two row passes (A/B switch)
+  static bool dst_tdt_fused() {
+    static const bool on = [] { const char* e = getenv("DBX_DST_TDT"); return !(e && e[0] == '0'); }();
+    return on;
+  }
   bool use_fft_dst(bool sine) const {
     if (dst == DBX_DST_DENSE) return false;
     const int N1 = sine ? n1 + 1 : n1 - 1, N2 = sine ? n2 + 1 : n2 - 1;
@@ -466,6 +471,7 @@ struct dbx_plan {
       B.t.tw = reinterpret_cast<const double2*>(B.tw);
       B.t.chirp = reinterpret_cast<const double2*>(B.chirp);
       B.t.bhat = reinterpret_cast<const double2*>(B.bhat);
+      if (!h.bct.empty()) B.t.bct = reinterpret_cast<const double2*>(upload_owned(h.bct));
       B.t.p = B.p;
       B.t.alpha = h.alpha;
       B.t.rinv = n > 1 ? 1.0 / (double)(n - 1) : 1.0;
@@ -735,13 +741,22 @@ struct dbx_plan {
         c.blue2 = blue_tables(0, false);
         c.in = s.p; c.out = u.p; c.kind1 = DBX_KIND_ARINV; c.epi = SPEC_HADAMARD; c.d = dT.p;
         c.st = stp; c.part = Partials{nullptr, 0};
-        lc(launch_dst_rows(c, stream), "launch_dst_rows");
-        c.in = u.p; c.out = s.p; c.kind1 = DBX_KIND_AR; c.epi = SPEC_STORE; c.d = nullptr;
-        lc(launch_dst_rows(c, stream), "launch_dst_rows");
-        launch_transpose(s.p, u.p, n2, n1, stream, batch);
+        if (dst_tdt_fused()) {
+          // T~, x d^T, T in one row pass (dst_rows kind2)
+          c.kind2 = DBX_KIND_AR; c.epi = SPEC_STORE;
+          lc(launch_dst_rows(c, stream), "launch_dst_rows");
+          launch_transpose(u.p, s.p, n2, n1, stream, batch);
+          launches += 3;
+          colout = s.p;
+        } else {
+          lc(launch_dst_rows(c, stream), "launch_dst_rows");
+          c.in = u.p; c.out = s.p; c.kind1 = DBX_KIND_AR; c.epi = SPEC_STORE; c.d = nullptr;
+          lc(launch_dst_rows(c, stream), "launch_dst_rows");
+          launch_transpose(s.p, u.p, n2, n1, stream, batch);
+          launches += 4;
+          colout = u.p;
+        }
         ev_end();
-        launches += 4;
-        colout = u.p;
       } else {
         a.in = u.p; a.insel = SEL_EXPLICIT; a.out = s.p; a.outsel = SEL_EXPLICIT;
         a.kind1 = DBX_KIND_ARINV; a.kind2 = DBX_KIND_AR;

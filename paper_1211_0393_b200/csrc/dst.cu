@@ -19,11 +19,24 @@
 // (spectral.hpp:161-165).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "spectral_common.cuh"
 
 namespace dbx {
 
 namespace {
+
+#ifdef DBX_DST_STOCKHAM
+constexpr bool kDstCt = false;
+#else
+constexpr bool kDstCt = true;
+#endif
+#ifdef DBX_DST_CT_BLUE
+constexpr bool kDstCtBlue = true;
+#else
+constexpr bool kDstCtBlue = false;
+#endif
 
 template <int M, int CORE>
 struct DstCfg {
@@ -32,7 +45,12 @@ struct DstCfg {
   static constexpr int NT = T * G;
   static constexpr int LINE = padded_len(M);                      // double2 per FFT line
   static constexpr int LO = LINE;                                 // output line stride (doubles)
-  static constexpr int TWN = fft::twiddles_needed(M);
+  // the Rader convolution core runs the in-place Cooley-Tukey ct_convolve
+  // (C5 8190: transform class 146 -> 131 ms per run); Bluestein keeps the two
+  // Stockham FFTs (C4 4096 = 8^4: 13.7 vs 15.4 ms with CT).  -DDBX_DST_STOCKHAM
+  // forces Stockham, -DDBX_DST_CT_BLUE forces CT for Bluestein too (A/B).
+  static constexpr bool CT = (CORE == CORE_RADER || (CORE == CORE_BLUE && kDstCtBlue)) && kDstCt;
+  static constexpr int TWN = CT ? fft::ct_twiddles_needed(M) : fft::twiddles_needed(M);
   static constexpr size_t base = (size_t)G * LINE * 16;
   static constexpr bool TW = base + (size_t)TWN * 16 <= kSmemCap;
   static constexpr size_t bytes = base + (TW ? (size_t)TWN * 16 : 0);
@@ -55,23 +73,31 @@ __device__ __forceinline__ double2 pkc_get(const double2* buf, const BlueTables&
 
 // Fill one FFT line with z_j = y^a_j + i y^b_j (pk_fill), placed per core;
 // sd(h, j) = (x^h_j + x^h_{N-j}, x^h_j - x^h_{N-j}), j in [1, N/2].
-template <int M, int T, int CORE, typename F>
-__device__ __forceinline__ void pkc_fill(double2* buf, const BlueTables& bt, int t, F sd) {
-  const int N = bt.N, H = N / 2;
-  auto put = [&](int j, double2 z) {
-    if constexpr (CORE == CORE_RADER) {
-      buf[pad<M>(__ldg(bt.dlog + j))] = z;  // a_p = z_{g^p}: dlog is a bijection onto [0, M)
-    } else if constexpr (CORE == CORE_BLUE) {
-      buf[pad<M>(j)] = cmul(z, __ldg(bt.chirp + j));
-    } else {
-      buf[pad<M>(j)] = z;
-    }
-  };
+template <int M, int CORE>
+__device__ __forceinline__ void pkc_put(double2* buf, const BlueTables& bt, int j, double2 z) {
+  if constexpr (CORE == CORE_RADER) {
+    buf[pad<M>(__ldg(bt.dlog + j))] = z;  // a_p = z_{g^p}: dlog is a bijection onto [0, M)
+  } else if constexpr (CORE == CORE_BLUE) {
+    buf[pad<M>(j)] = cmul(z, __ldg(bt.chirp + j));
+  } else {
+    buf[pad<M>(j)] = z;
+  }
+}
+// positions no pair covers: 0, and the Bluestein zero padding [N, M)
+template <int M, int T, int CORE>
+__device__ __forceinline__ void pkc_zero_fill(double2* buf, const BlueTables& bt, int t) {
   if constexpr (CORE != CORE_RADER) {
     if (t == 0) buf[pad<M>(0)] = make_double2(0.0, 0.0);
     if constexpr (CORE == CORE_BLUE)
-      for (int p = N + t; p < M; p += T) buf[pad<M>(p)] = make_double2(0.0, 0.0);
+      for (int p = bt.N + t; p < M; p += T) buf[pad<M>(p)] = make_double2(0.0, 0.0);
   }
+}
+
+template <int M, int T, int CORE, typename F>
+__device__ __forceinline__ void pkc_fill(double2* buf, const BlueTables& bt, int t, F sd) {
+  const int N = bt.N, H = N / 2;
+  auto put = [&](int j, double2 z) { pkc_put<M, CORE>(buf, bt, j, z); };
+  pkc_zero_fill<M, T, CORE>(buf, bt, t);
   // U positions per thread in flight: every global load of a group is issued
   // before the first shared-memory store (the loads cannot move above the
   // stores on their own: generic pointers may alias)
@@ -99,6 +125,37 @@ __device__ __forceinline__ void pkc_fill(double2* buf, const BlueTables& bt, int
   }
 }
 
+
+// Refill the FFT line from values that live in the line itself (the outputs
+// of a previous transform, val(h, k) = value k of new line h): every read
+// lands in registers (PF pairs per thread), then a barrier, then the scatter.
+template <int M, int T, int CORE, int PF, typename V>
+__device__ __forceinline__ void pkc_refill(double2* buf, const BlueTables& bt, int t, V val) {
+  const int N = bt.N, H = N / 2;
+  double2 zj[PF], zm[PF];
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int j = 1 + t + i * T;
+    if (j <= H) {
+      const double s = __ldg(bt.sn + j);
+      const double aj = val(0, j), am = val(0, N - j), bj = val(1, j), bm = val(1, N - j);
+      const double2 A = make_double2(aj + am, aj - am), B = make_double2(bj + bm, bj - bm);
+      zj[i] = make_double2(fma(s, A.x, 0.5 * A.y), fma(s, B.x, 0.5 * B.y));
+      zm[i] = make_double2(fma(s, A.x, -0.5 * A.y), fma(s, B.x, -0.5 * B.y));
+    }
+  }
+  __syncthreads();
+  pkc_zero_fill<M, T, CORE>(buf, bt, t);
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int j = 1 + t + i * T;
+    if (j <= H) {
+      pkc_put<M, CORE>(buf, bt, j, zj[i]);
+      if (N - j != j) pkc_put<M, CORE>(buf, bt, N - j, zm[i]);
+    }
+  }
+}
+
 // The N-point DFT of the G lines (every thread of the CTA calls it).
 template <int M, int T, int G, int CORE>
 __device__ __forceinline__ void pkc_core(double2* sm, double2* buf, const BlueTables& bt, const double2* tw, int t,
@@ -107,6 +164,9 @@ __device__ __forceinline__ void pkc_core(double2* sm, double2* buf, const BlueTa
   __syncthreads();
   if constexpr (CORE == CORE_DIRECT && (M & 1)) {
     fft::fft_cta<M, -1, T, G>(sm, tw, threadIdx.x);
+  } else if constexpr (DstCfg<M, CORE>::CT) {
+    const int bar = G > 1 ? 1 + g : 0;
+    fft::ct_convolve<M, T>(buf, tw, bt.bct, t, bar, CORE == CORE_RADER ? &A0s[g] : nullptr);
   } else {
     const int bar = G > 1 ? 1 + g : 0;
     fft::fft<M, -1, T>(buf, tw, t, bar);
@@ -239,19 +299,32 @@ __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_rows(SpecArgs a) {
   extern __shared__ double2 sm[];
   __shared__ double red[32];
   __shared__ double2 A0s[G];
+  __shared__ double ends[G][4];
   const int g = threadIdx.x / T, t = threadIdx.x - g * T;
   double2* buf = sm + g * C::LINE;
   const BlueTables& bt = a.blue2;
-  const double2* tw = stage_twiddles<M, C::TW>(sm + G * C::LINE, bt.tw);
-  const int n1 = a.n1, n = a.n2, kind = a.kind1;
+  const double2* tw = stage_twiddles<M, C::TW, C::TWN>(sm + G * C::LINE, bt.tw);
+  const int n1 = a.n1, n = a.n2;
+  int kind = a.kind1;
   const size_t N = (size_t)n1 * n;
   const int ra = blockIdx.x * 2 * G + 2 * g;
   const double* in = resolve_ptr(a.in, a.st, a.insel, b, a.batch, N);
+  // L2 prefetch of the rows the CTA one resident wave ahead will read (the
+  // one-line-per-CTA lengths: the fill's DRAM latency is not hidden by any
+  // other resident CTA)
+  if (a.pf > 0 && threadIdx.x == 0) {
+    const size_t r0 = (size_t)(blockIdx.x + a.pf) * 2 * G;
+    if (r0 < (size_t)n1) {
+      const size_t nr = r0 + 2 * G <= (size_t)n1 ? 2 * G : n1 - r0;
+      const unsigned bytes = (unsigned)(nr * n * sizeof(double)) & ~15u;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(in + r0 * n), "r"(bytes) : "memory");
+    }
+  }
   const double* xa = ra < n1 ? in + (size_t)ra * n : nullptr;
   const double* xb = ra + 1 < n1 ? in + (size_t)(ra + 1) * n : nullptr;
   const bool sine = kind == DBX_KIND_SINEI;
-  const double a0 = (xa && !sine) ? xa[0] : 0.0, ae = (xa && !sine) ? xa[n - 1] : 0.0;
-  const double b0 = (xb && !sine) ? xb[0] : 0.0, be = (xb && !sine) ? xb[n - 1] : 0.0;
+  double a0 = (xa && !sine) ? xa[0] : 0.0, ae = (xa && !sine) ? xa[n - 1] : 0.0;
+  double b0 = (xb && !sine) ? xb[0] : 0.0, be = (xb && !sine) ? xb[n - 1] : 0.0;
   const double ri = bt.rinv;
   const int NL = bt.N;
   pkc_fill<M, T, CORE>(buf, bt, t, [&](int hh, int j) {
@@ -263,9 +336,31 @@ __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_rows(SpecArgs a) {
   pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g);
   pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0));
   pkc_scans<G, C::LINE, C::LO>(sm, bt);
-  Epi e = make_epi(a, b, N);
   const double* o = reinterpret_cast<const double*>(buf);
   const double al = bt.alpha;
+  if (a.kind2 >= 0) {
+    // kind1, x d (the CTA's rows of the filter grid), kind2 on the same rows:
+    // the column half of D = T diag(d) T~ on transposed images in one pass
+    // (AR kinds only; the intermediate never leaves shared memory)
+    const double* dd = a.d + (size_t)b * a.dstride;
+    const double* da = xa ? dd + (size_t)ra * n : nullptr;
+    const double* db = xb ? dd + (size_t)(ra + 1) * n : nullptr;
+    auto val = [&](int hh, int k) {
+      const double* dr = hh ? db : da;
+      if (!dr) return 0.0;
+      return kind_out(kind, o + hh * C::LO, k, n, hh ? b0 : a0, hh ? be : ae, al, ri) * __ldg(dr + k);
+    };
+    if (t < 4) ends[g][t] = val(t >> 1, (t & 1) ? n - 1 : 0);
+    constexpr int PF = (C::NMAX / 2 + T - 1) / T;
+    pkc_refill<M, T, CORE, PF>(buf, bt, t, val);
+    a0 = ends[g][0]; ae = ends[g][1]; b0 = ends[g][2]; be = ends[g][3];
+    kind = a.kind2;
+    pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g);
+    pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0));
+    pkc_scans<G, C::LINE, C::LO>(sm, bt);
+  }
+  Epi e = make_epi(a, b, N);
+  if (a.kind2 >= 0) e.d = nullptr;
   for (int hh = 0; hh < 2; ++hh) {
     const int r = ra + hh;
     if (r >= n1) continue;
@@ -300,7 +395,7 @@ __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_cols(SpecArgs a) {
   const int g = threadIdx.x / T, t = threadIdx.x - g * T;
   double2* buf = sm + g * C::LINE;
   const BlueTables& bt = a.blue1;
-  const double2* tw = stage_twiddles<M, C::TW>(sm + G * C::LINE, bt.tw);
+  const double2* tw = stage_twiddles<M, C::TW, C::TWN>(sm + G * C::LINE, bt.tw);
   const int n = a.n1, n2 = a.n2;
   const size_t N = (size_t)n * n2;
   const int c0 = blockIdx.x * 2 * G;
@@ -342,13 +437,32 @@ __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_cols(SpecArgs a) {
   }
 }
 
+// L2 prefetch of the next resident wave's rows in the one-line-per-CTA row
+// passes (C5: 125.8 -> 124.6 ms transform class per run); DBX_DST_PF=0 disables
+static bool dst_pf_enabled() {
+  static const bool on = [] { const char* e = getenv("DBX_DST_PF"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
 template <int L, int CORE>
 int rows_launch(const SpecArgs& a, cudaStream_t s) {
   using C = DstCfg<L, CORE>;
   static AttrOnce attr;
   if (!attr.ensure(dst_rows<L, CORE>, C::bytes)) return -1;
   dim3 grid((a.n1 + 2 * C::G - 1) / (2 * C::G), a.batch);
-  launch_k(dst_rows<L, CORE>, grid, C::NT, C::bytes, s, a);
+  SpecArgs b = a;
+  b.pf = 0;
+  if (C::G == 1 && dst_pf_enabled()) {
+    static const int resident = [] {
+      int dev = 0, sms = 0, occ = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dst_rows<L, CORE>, C::NT, C::bytes);
+      return sms * (occ > 0 ? occ : 1);
+    }();
+    b.pf = resident;
+  }
+  launch_k(dst_rows<L, CORE>, grid, C::NT, C::bytes, s, b);
   return (int)grid.x;
 }
 

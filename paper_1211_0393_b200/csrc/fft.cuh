@@ -20,6 +20,7 @@
 #include <type_traits>
 
 #include "dft_consts.h"
+#include "radix.h"
 
 namespace dbx {
 
@@ -56,24 +57,6 @@ __host__ __device__ constexpr int padded_len(int L) { return (L & 1) ? L + 1 : L
 __host__ __device__ constexpr int threads_for(int L) {
   int t = (L / 8 + 31) / 32 * 32;
   return t < 32 ? 32 : (t > 512 ? 512 : t);
-}
-
-// Power-of-two factors first (8, 4, 2), then the LARGEST odd prime <= 31: the
-// first stage (Ns = 1) needs no twiddles, so it takes the most expensive radix.
-__host__ __device__ constexpr int next_radix(int rem) {
-  if (rem % 8 == 0) return 8;
-  if (rem % 4 == 0) return 4;
-  if (rem % 2 == 0) return 2;
-  constexpr int primes[8] = {31, 29, 23, 19, 17, 13, 11, 7};
-  for (int i = 0; i < 8; ++i)
-    if (rem % primes[i] == 0) return primes[i];
-  // 3^a 5^b: composite in-register radices 15 (3x5 prime factor) and 9 (3x3)
-  // halve the number of shared-memory passes against 5, 3, 3, ...
-  if (rem % 15 == 0) return 15;
-  if (rem % 9 == 0) return 9;
-  if (rem % 5 == 0) return 5;
-  if (rem % 3 == 0) return 3;
-  return 0;
 }
 
 // Twiddle entries an FFT of length L reads: stage (Ns, R) reads W_L^{k L/(Ns R)},
@@ -860,6 +843,134 @@ __device__ __forceinline__ void fft_in(double2* buf, const double2* __restrict__
   constexpr int R = next_radix(L);
   stage<L, 1, R, S, T>(buf, tw, t, bar, fin);
   run_stages<L, R, S, T>(buf, tw, t, bar);
+}
+
+
+// ---------------------------------------------------------------------------
+// In-place Cooley-Tukey (no autosort) for convolution cores (Rader, Bluestein):
+// forward = decimation in frequency from natural order to digit-reversed order
+// (radix.h ct_freq_of_pos), the pointwise kernel product in that order (the
+// host permutes the kernel spectrum), inverse = decimation in time from
+// digit-reversed back to natural order.  Each butterfly reads and writes the
+// same R slots, so a thread finishes one butterfly (load, DFT, twiddles,
+// store) before it loads the next: one barrier per stage and R live complex
+// values per thread, against the Stockham stage's two barriers and PER x R
+// registers.  The last forward level, the kernel product and the first
+// inverse level act on the same contiguous R-blocks and run as one pass.
+
+// Butterflies a thread keeps in flight per pass (all loads of the group are
+// issued before the first DFT): about 16 complex values, so short radices get
+// load-level parallelism and long ones stay within the register budget.
+#ifndef DBX_CT_VALS
+#define DBX_CT_VALS 16
+#endif
+template <int R, int NB, int T>
+__host__ __device__ constexpr int ct_unroll() {
+  constexpr int u = DBX_CT_VALS / R < 1 ? 1 : DBX_CT_VALS / R;
+  constexpr int per = (NB + T - 1) / T;
+  return u < per ? u : per;
+}
+
+// Forward level with block size Ls (m = Ls/R): y_k = DFT_R(x_{j + r m}),
+// y_k *= W_Ls^{j k}.  DIR = -1; the inverse level (DIR = +1, transpose of the
+// forward one, conjugated) multiplies by conj W_Ls^{j k} first, then runs the
+// unnormalised inverse DFT_R.
+template <int L, int Ls, int T, int DIR>
+__device__ __forceinline__ void ct_level(double2* buf, const double2* __restrict__ tw, int t, int bar) {
+  constexpr int R = ct_radix(Ls), m = Ls / R, NB = L / R;
+  static_assert(R != 0, "unsupported FFT length");
+  constexpr int U = ct_unroll<R, NB, T>();
+#pragma unroll 1
+  for (int b0 = t; b0 < NB; b0 += U * T) {
+    double2 v[U][R], w1[U];
+    int base[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int beta = b0 + u * T;
+      const int blk = beta / m, j = beta - blk * m;
+      base[u] = blk * Ls + j;
+      if (U == 1 || beta < NB) {
+        w1[u] = tw[j * (L / Ls)];  // smem-staged or global table
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[u][r] = buf[pad<L>(base[u] + r * m)];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (U == 1 || b0 + u * T < NB) {
+        if constexpr (DIR < 0) {
+          dft<R, -1>(v[u]);
+          apply_twiddles<R, -1>(v[u], w1[u]);
+        } else {
+          apply_twiddles<R, +1>(v[u], w1[u]);
+          dft<R, +1>(v[u]);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[pad<L>(base[u] + r * m)] = v[u][r];
+      }
+    }
+  }
+  line_sync(bar, T);
+}
+
+template <int L, int Ls, int T>
+__device__ __forceinline__ void ct_dif_levels(double2* buf, const double2* __restrict__ tw, int t, int bar) {
+  if constexpr (Ls / ct_radix(Ls) > 1) {  // every level but the last (R-blocks)
+    ct_level<L, Ls, T, -1>(buf, tw, t, bar);
+    ct_dif_levels<L, Ls / ct_radix(Ls), T>(buf, tw, t, bar);
+  }
+}
+template <int L, int Ls, int T>
+__device__ __forceinline__ void ct_dit_levels(double2* buf, const double2* __restrict__ tw, int t, int bar) {
+  if constexpr (Ls / ct_radix(Ls) > 1) {
+    ct_dit_levels<L, Ls / ct_radix(Ls), T>(buf, tw, t, bar);
+    ct_level<L, Ls, T, +1>(buf, tw, t, bar);
+  }
+}
+// size of the innermost level's blocks (the last forward radix)
+template <int L>
+__host__ __device__ constexpr int ct_last_radix() {
+  int Ls = L;
+  while (Ls / ct_radix(Ls) > 1) Ls /= ct_radix(Ls);
+  return Ls;
+}
+
+// Cyclic convolution core: buf <- IDFT(K .* DFT(buf)) with K the kernel
+// spectrum in digit-reversed position order (kdr[p] = K_{ct_freq_of_pos(p)}),
+// unnormalised inverse (the host folds 1/L into K).  x0 (may be null)
+// receives DFT(buf)_0 (position 0, before the product).  bar as for fft().
+template <int L, int T>
+__device__ __forceinline__ void ct_convolve(double2* buf, const double2* __restrict__ tw,
+                                            const double2* __restrict__ kdr, int t, int bar, double2* x0) {
+  static_assert(supported(L), "unsupported FFT length");
+  ct_dif_levels<L, L, T>(buf, tw, t, bar);
+  constexpr int R = ct_last_radix<L>(), NB = L / R;
+  constexpr int U = ct_unroll<R, NB, T>();
+#pragma unroll 1
+  for (int b0 = t; b0 < NB; b0 += U * T) {
+    double2 v[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (U == 1 || b0 + u * T < NB) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[u][r] = buf[pad<L>((b0 + u * T) * R + r)];
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int base = (b0 + u * T) * R;
+      if (U == 1 || b0 + u * T < NB) {
+        dft<R, -1>(v[u]);
+        if (x0 && base == 0) *x0 = v[u][0];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[u][r] = cmul(v[u][r], __ldg(kdr + base + r));
+        dft<R, +1>(v[u]);
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[pad<L>(base + r)] = v[u][r];
+      }
+    }
+  }
+  line_sync(bar, T);
+  ct_dit_levels<L, L, T>(buf, tw, t, bar);
 }
 
 }  // namespace fft

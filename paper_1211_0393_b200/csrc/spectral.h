@@ -40,6 +40,7 @@ struct BlueTables {
   const double2* tw = nullptr;
   const double2* chirp = nullptr;
   const double2* bhat = nullptr;
+  const double2* bct = nullptr;  // bhat at the in-place Cooley-Tukey core's digit-reversed positions
   const double* p = nullptr;
   const double* sn = nullptr;  // sin(pi j / N), j < N (packed real DST)
   const int* dlog = nullptr;   // Rader: position of z_j (discrete log base g), j in [1, N)
@@ -75,6 +76,7 @@ struct SpecArgs {
   size_t dstride = 0;                            // filter grid per image (alpha sweep) or shared (0)
   // DST
   int kind1 = DBX_KIND_ARINV, kind2 = -1;
+  int pf = 0;                                    // dst_rows: prefetch the rows of CTA blockIdx.x + pf into L2 (0: off)
   BlueTables blue1;                              // columns (length n1)
   BlueTables blue2;                              // rows (length n2)
 };

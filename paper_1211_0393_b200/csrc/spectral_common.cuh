@@ -98,10 +98,10 @@ __device__ __forceinline__ int nsm() {
 
 // Twiddle table of an FFT length L staged into shared memory (cp.async group
 // committed here) when `smem_ok`, else read from global (L1/L2).
-template <int L, bool SMEM>
+template <int L, bool SMEM, int NEED_ = 0>
 __device__ __forceinline__ const double2* stage_twiddles(double2* dst, const double2* src) {
   if constexpr (SMEM) {
-    constexpr int NEED = fft::twiddles_needed(L);
+    constexpr int NEED = NEED_ > 0 ? NEED_ : fft::twiddles_needed(L);
     for (int i = threadIdx.x; i < NEED; i += blockDim.x) cp_async16(dst + i, src + i);
     cp_async_commit();
     return dst;

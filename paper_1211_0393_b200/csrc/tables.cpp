@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "tables.h"
+#include "radix.h"
 
 namespace dbx {
 namespace {
@@ -114,6 +115,18 @@ bool rank1_factor(const double* w, int q1, int q2, int L2, double tol, std::vect
 void blue_chirp(BlueHost& b, long N, int M);
 void ar_ramp(BlueHost& b, int n, bool sine_i);
 
+// The kernel spectrum in the in-place Cooley-Tukey core's digit-reversed
+// position order (radix.h ct_freq_of_pos; fft.cuh ct_convolve).
+void ct_permute(BlueHost& b) {
+  const int M = b.M;
+  b.bct.assign(2 * (size_t)M, 0.0);
+  for (int p = 0; p < M; ++p) {
+    const int k = fft::ct_freq_of_pos(M, p);
+    b.bct[2 * (size_t)p] = b.bhat[2 * (size_t)k];
+    b.bct[2 * (size_t)p + 1] = b.bhat[2 * (size_t)k + 1];
+  }
+}
+
 BlueHost bluestein(int n, bool sine_i, int M) {
   BlueHost b;
   b.n = n;
@@ -128,6 +141,7 @@ BlueHost bluestein(int n, bool sine_i, int M) {
     b.bhat.assign(2, 0.0);
   } else {
     blue_chirp(b, N, M);
+    ct_permute(b);
   }
   ar_ramp(b, n, sine_i);
   // sine pre-twiddle of the packed real DST (spectral_common.cuh, pk_fill)
@@ -206,6 +220,7 @@ BlueHost rader(int n, bool sine_i) {
       put(b.bhat.data(), k, acc.real(), acc.imag());
     }
   });
+  ct_permute(b);
   b.chirp.assign(2, 0.0);
   ar_ramp(b, n, sine_i);
   b.sn.assign((size_t)N, 0.0);

@@ -23,6 +23,7 @@ struct BlueHost {
   int n = 0, N = 0, M = 0;
   double alpha = 1.0, scale = 1.0;
   std::vector<double> tw, chirp, bhat, p, sn;  // sn[j] = sin(pi j / N), j < N
+  std::vector<double> bct;  // bhat in digit-reversed order (fft.cuh ct_convolve)
   std::vector<int> dlog, ridx;                 // Rader permutations (prime N)
   int core = 0;                                // DstCore (spectral.h)
 };
