@@ -176,6 +176,51 @@ int dbx_slab_extend(dbx_plan* plan, const double* x, const double* top, const do
 int dbx_slab_pack(dbx_plan* plan, const double* x, double* blocks, int parts, int unpack);
 
 /*
+ * C++ row-slab D-Landweber (the C5 config).  The loop that
+ * paper_1211_0393_b200/slab.py orchestrated from Python, driven in C++ with
+ * no host synchronisation inside the loop: per iteration the q-row halos go
+ * through grouped ncclSend/ncclRecv with the slab neighbours (the first / last
+ * slab synthesise the global AR rows on the device), the blur is the
+ * separable direct pass on the halo-extended slab (FFT correlation for masks
+ * that are not rank 1), the column half of D runs on column blocks obtained by
+ * an all-to-all from grouped send/recv (two per iteration), and the three norms
+ * are all-reduced on the device (ncclAllReduce of 3 doubles) and fed to a
+ * device-side copy of the loop bookkeeping (solver.hpp:101-131).
+ *
+ * dbx_comm: an NCCL communicator, built here (dbx_comm_unique_id on one rank,
+ *   broadcast the DBX_COMM_ID_BYTES bytes, dbx_comm_init on every rank) or
+ *   wrapping the caller's ncclComm_t (dbx_comm_wrap; not owned).  libnccl.so.2
+ *   is resolved at run time (the copy already loaded in the process first).
+ * dbx_slab_create: slab plan of an n x n image in `parts` row slabs.  rank >= 0:
+ *   this process holds slab `rank` (comm required when parts > 1); rank = -1:
+ *   this process holds all `parts` slabs and the exchanges are device copies
+ *   (in-process ranks, single-GPU parity tests).  alpha: the Tikhonov filter of
+ *   the symmetrised mask (each process builds its own d^T column blocks).
+ * dbx_slab_run: g, f (nullable), x_out are DEVICE arrays of the rows held here
+ *   (slab-major, local_slabs x (n/parts) x n); histories are host arrays of
+ *   max_iters; best_iter / iters_done as dbx_landweber_run.  Status as
+ *   dbx_landweber_run (DBX_EDIVERGED on the divergence guard).
+ */
+#define DBX_COMM_ID_BYTES 128
+typedef struct dbx_comm dbx_comm;
+typedef struct dbx_slab dbx_slab;
+int dbx_comm_unique_id(unsigned char* id);
+int dbx_comm_init(int nranks, const unsigned char* id, int rank, int device, dbx_comm** comm);
+int dbx_comm_wrap(void* nccl_comm, int nranks, int rank, dbx_comm** comm);
+void dbx_comm_destroy(dbx_comm* comm);
+int dbx_slab_create(int n, int parts, int rank, const double* taps, int q1, int q2, double alpha, dbx_comm* comm,
+                    int device, dbx_slab** slab);
+int dbx_slab_run(dbx_slab* slab, const double* g, const double* f, double tau, int max_iters, int stop_kind,
+                 double resid_eps, double* x_out, double* rre_hist, double* res_hist, int* best_iter,
+                 int* iters_done);
+int dbx_slab_info(dbx_slab* slab, int* rows, int* local_slabs, int* separable, int64_t* launches);
+void* dbx_slab_stream(dbx_slab* slab);
+/* Tests: copy x_k (the rows held here) to buf + (k-1) * local_rows * n after
+ * iteration k <= count (device buffer); buf = NULL disables. */
+int dbx_slab_set_iterates(dbx_slab* slab, double* buf, int count);
+void dbx_slab_destroy(dbx_slab* slab);
+
+/*
  * Pipeline used by the last dbx_landweber_run on this plan: *fused = 1 for the
  * fused row pipelines (6 launches + finalize per preconditioned iteration,
  * fused.cu), 2 for their separable form (rank-1 mask: direct row passes in

@@ -98,6 +98,20 @@ def lib():
         L.dbx_transpose.argtypes = [vp, vp, vp, i, i]
         L.dbx_slab_extend.argtypes = [vp, vp, vp, vp, vp]
         L.dbx_slab_pack.argtypes = [vp, vp, vp, i, i]
+        # C++ row-slab loop (NCCL communicators, dbx_slab_*)
+        L.dbx_comm_unique_id.argtypes = [vp]
+        L.dbx_comm_init.argtypes = [i, vp, i, i, C.POINTER(vp)]
+        L.dbx_comm_wrap.argtypes = [vp, i, i, C.POINTER(vp)]
+        L.dbx_comm_destroy.argtypes = [vp]
+        L.dbx_comm_destroy.restype = None
+        L.dbx_slab_create.argtypes = [i, i, i, vp, i, i, d, vp, i, C.POINTER(vp)]
+        L.dbx_slab_run.argtypes = [vp, vp, vp, d, i, i, d, vp, vp, vp, vp, vp]
+        L.dbx_slab_info.argtypes = [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(C.c_int64)]
+        L.dbx_slab_stream.argtypes = [vp]
+        L.dbx_slab_stream.restype = vp
+        L.dbx_slab_set_iterates.argtypes = [vp, vp, i]
+        L.dbx_slab_destroy.argtypes = [vp]
+        L.dbx_slab_destroy.restype = None
         _lib = L
     return _lib
 

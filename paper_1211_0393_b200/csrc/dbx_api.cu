@@ -811,6 +811,96 @@ void stage_out(dbx_plan* P, double* dst, const double* src, size_t count) {
 }  // namespace
 
 // ============================================================================
+// C++ row-slab D-Landweber (the C5 config): one n x n image split
+// into P row slabs of R = n/P rows.  Exchanges are NCCL calls on the plan's
+// stream (libnccl.so.2 resolved at run time, so processes that never build a
+// communicator do not need it) or, for P in-process ranks on one device, device
+// copies / halo views into the neighbour's rows (the parity tests' analogue of
+// slab.py's LocalWorld).  Nothing synchronises the host inside the loop: the
+// norms are reduced and all-reduced on the device and the bookkeeping runs in
+// a one-thread kernel, so every rank takes the same decisions.
+// ============================================================================
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*ErrStr)(ncclResult_t) = nullptr;
+};
+
+// The NCCL already mapped into the process (torch's) if any, else the system one.
+NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+      return a;
+    }
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
+    a.ErrStr = reinterpret_cast<decltype(a.ErrStr)>(sym("ncclGetErrorString"));
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GroupStart && a.GroupEnd &&
+           a.AllReduce && a.ErrStr;
+    if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+void nck(ncclResult_t r, const char* where) {
+  if (r != ncclSuccess) throw CudaErr(std::string(where) + ": " + nccl_api().ErrStr(r));
+}
+
+}  // namespace
+
+struct dbx_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  bool owned = false;
+};
+
+struct dbx_slab {
+  int n = 0, P = 1, q = 0, R = 0, C = 0;
+  int nloc = 1, rank0 = 0;  // slabs held here: all P (in-process ranks) or this rank's one
+  int device = 0;
+  bool sep = false;         // separable direct blur (rank-1 mask), else the FFT slab blur
+  dbx_comm* comm = nullptr;
+  dbx_plan* plan = nullptr; // R x n slab plan: tables, stream, Z^T scratch
+  DevBuf x, best, r, s, u, tA, tB, send, recv, top, bot, ext, dTb, part, tot, hist;
+  ImgState* st = nullptr;
+  double* keep = nullptr;   // dbx_slab_set_iterates: x_k copied here after iteration k (tests)
+  int keep_n = 0;
+  ~dbx_slab() {
+    for (DevBuf* b : {&x, &best, &r, &s, &u, &tA, &tB, &send, &recv, &top, &bot, &ext, &dTb, &part, &tot, &hist})
+      b->release();
+    if (st) cudaFree(st);
+    if (plan) dbx_plan_destroy(plan);
+  }
+};
+
+// ============================================================================
 extern "C" {
 
 const char* dbx_last_error(void) { return g_err.c_str(); }
@@ -1871,6 +1961,366 @@ int dbx_landweber_run_chunks(dbx_plan* const* plans, int nplans, const double* g
     return first_div;
   }
   return DBX_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// NCCL communicators and the C++ row-slab loop (see the section header above
+// `struct dbx_slab`).
+// ---------------------------------------------------------------------------
+int dbx_comm_unique_id(unsigned char* id) {
+  return guarded([&] {
+    require(id != nullptr, "comm_unique_id: null argument");
+    NcclApi& n = nccl_api();
+    if (!n.ok) throw CudaErr(n.why);
+    ncclUniqueId u;
+    nck(n.GetUniqueId(&u), "ncclGetUniqueId");
+    static_assert(sizeof(u.internal) == DBX_COMM_ID_BYTES, "ncclUniqueId size");
+    std::memcpy(id, u.internal, DBX_COMM_ID_BYTES);
+  });
+}
+
+int dbx_comm_init(int nranks, const unsigned char* id, int rank, int device, dbx_comm** out) {
+  return guarded([&] {
+    require(out && id && nranks >= 1 && rank >= 0 && rank < nranks, "comm_init: bad argument");
+    *out = nullptr;
+    NcclApi& n = nccl_api();
+    if (!n.ok) throw CudaErr(n.why);
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, DBX_COMM_ID_BYTES);
+    auto c = std::make_unique<dbx_comm>();
+    nck(n.CommInitRank(&c->comm, nranks, u, rank), "ncclCommInitRank");
+    c->nranks = nranks;
+    c->rank = rank;
+    c->owned = true;
+    *out = c.release();
+  });
+}
+
+int dbx_comm_wrap(void* nccl_comm, int nranks, int rank, dbx_comm** out) {
+  return guarded([&] {
+    require(out && nccl_comm && nranks >= 1 && rank >= 0 && rank < nranks, "comm_wrap: bad argument");
+    auto c = std::make_unique<dbx_comm>();
+    c->comm = static_cast<ncclComm_t>(nccl_comm);
+    c->nranks = nranks;
+    c->rank = rank;
+    *out = c.release();
+  });
+}
+
+void dbx_comm_destroy(dbx_comm* c) {
+  if (!c) return;
+  if (c->owned && c->comm && nccl_api().ok) nccl_api().CommDestroy(c->comm);
+  delete c;
+}
+
+int dbx_slab_create(int n, int parts, int rank, const double* taps, int q1, int q2, double alpha, dbx_comm* comm,
+                    int device, dbx_slab** out) {
+  return guarded([&] {
+    require(out != nullptr, "slab_create: null out");
+    *out = nullptr;
+    require(n >= 3 && parts >= 1 && n % parts == 0, "row slabs: image rows must divide evenly across ranks");
+    require(alpha >= 0.0, "tikhonov_filter: alpha must be nonnegative");
+    require(rank < parts, "slab_create: rank out of range");
+    if (rank >= 0 && parts > 1) {
+      require(comm != nullptr, "slab_create: a rank of a multi-rank decomposition needs a communicator");
+      require(comm->nranks == parts && comm->rank == rank, "slab_create: communicator does not match (parts, rank)");
+    }
+    const int R = n / parts;
+    require(R >= q1 + 1, "row slabs: every slab needs at least q + 1 rows (the global AR extension is local)");
+    auto S = std::make_unique<dbx_slab>();
+    S->n = n; S->P = parts; S->q = q1; S->R = R; S->C = R; S->device = device;
+    S->nloc = rank < 0 ? parts : 1;
+    S->rank0 = rank < 0 ? 0 : rank;
+    S->comm = (rank >= 0 && parts > 1) ? comm : nullptr;
+    dbx_plan* h = nullptr;
+    const int rc = dbx_plan_create(R, n, 1, taps, q1, q2, DBX_BC_ANTIREFLECTIVE, device, &h);
+    if (rc != DBX_OK) {
+      if (rc == DBX_EINVAL) throw InvalidArg(g_err);
+      throw CudaErr(g_err);
+    }
+    S->plan = h;
+    dbx_plan* P = h;
+    P->set_dev();
+    if (P->conv == DBX_CONV_DIRECT || !P->use_fft_conv()) P->conv = DBX_CONV_FFT;
+    require(P->use_fft_conv(), "slab_create: no compiled FFT correlation length for this slab");
+    P->ensure_conv();
+    S->sep = P->sep_direct(BLUR_RESID);
+    P->blue_tables(1, false);  // throws when no DST core exists for the row length
+    const size_t slab = (size_t)R * n, nl = (size_t)S->nloc;
+    for (DevBuf* b : {&S->x, &S->best, &S->r, &S->s, &S->u, &S->tA, &S->tB}) b->ensure(nl * slab);
+    if (parts > 1)
+      for (DevBuf* b : {&S->send, &S->recv}) b->ensure(nl * slab);
+    S->top.ensure(nl * q1 * n);
+    S->bot.ensure(nl * q1 * n);
+    if (!S->sep) S->ext.ensure((size_t)(R + 2 * q1) * n);
+    P->zb.ensure(std::max((size_t)(R + 2 * q1) * n, (size_t)(R + 2 * q1) * P->Lh * 2));
+    S->part.ensure(nl * NUM_SLOTS * (size_t)P->part_cap);
+    S->tot.ensure(nl * 4);
+    ck(cudaMalloc(&S->st, sizeof(ImgState)), "cudaMalloc");
+    // this process's blocks of d^T: rows c in [p C, (p+1) C) of d^T (columns of d)
+    S->dTb.ensure(nl * slab);
+    int* flag = nullptr;
+    ck(cudaMalloc(&flag, sizeof(int)), "cudaMalloc");
+    ck(cudaMemsetAsync(flag, 0, sizeof(int), P->stream), "memset");
+    for (int i = 0; i < S->nloc; ++i)
+      launch_build_filter_block(P->sym, q1, q2, n, n, alpha, 0, n, (S->rank0 + i) * S->C, S->C, 1,
+                                S->dTb.p + (size_t)i * slab, flag, P->stream, 0);
+    int hflag = 0;
+    ck(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, P->stream), "D2H");
+    ck(cudaStreamSynchronize(P->stream), "sync");
+    cudaFree(flag);
+    require(alpha > 0.0 || hflag == 0, "tikhonov_filter: alpha = 0 with a zero eigenvalue");
+    *out = S.release();
+  });
+}
+
+void dbx_slab_destroy(dbx_slab* S) { delete S; }
+
+int dbx_slab_set_iterates(dbx_slab* S, double* buf, int count) {
+  return guarded([&] {
+    require(S != nullptr && count >= 0, "slab_set_iterates: bad argument");
+    require(!buf || is_device_ptr(buf), "slab_set_iterates: device pointer");
+    S->keep = count > 0 ? buf : nullptr;
+    S->keep_n = buf ? count : 0;
+  });
+}
+
+void* dbx_slab_stream(dbx_slab* S) { return S ? (void*)S->plan->stream : nullptr; }
+
+int dbx_slab_info(dbx_slab* S, int* rows, int* local_slabs, int* separable, int64_t* launches) {
+  return guarded([&] {
+    require(S != nullptr, "slab_info: null slab");
+    if (rows) *rows = S->R;
+    if (local_slabs) *local_slabs = S->nloc;
+    if (separable) *separable = S->sep ? 1 : 0;
+    if (launches) *launches = S->plan->launches;
+  });
+}
+
+int dbx_slab_run(dbx_slab* S, const double* g, const double* f, double tau, int max_iters, int stop_kind,
+                 double resid_eps, double* x_out, double* rre_hist, double* res_hist, int* best_iter,
+                 int* iters_done) {
+  return guarded([&] {
+    require(S && g && x_out && best_iter && iters_done, "slab_run: null argument");
+    require(max_iters >= 1, "SolverConfig: max_iters must be >= 1");
+    require(stop_kind >= DBX_STOP_FIXED && stop_kind <= DBX_STOP_RESIDUAL, "slab_run: unknown stopping rule");
+    require(stop_kind != DBX_STOP_MINRRE || f, "StoppingRule::MinRre needs the true image");
+    require(is_device_ptr(g) && is_device_ptr(x_out) && (!f || is_device_ptr(f)), "slab_run: device pointers");
+    dbx_plan* P = S->plan;
+    P->set_dev();
+    const cudaStream_t st = P->stream;
+    const int n = S->n, R = S->R, C = S->C, q = S->q, PP = S->P, nl = S->nloc;
+    const size_t slab = (size_t)R * n, cap = (size_t)P->part_cap;
+    const bool track = f != nullptr;
+    NcclApi* nc = S->comm ? &nccl_api() : nullptr;
+    if (S->comm && !nc->ok) throw CudaErr(nc->why);
+    auto part_of = [&](int i) { return Partials{S->part.p + (size_t)i * NUM_SLOTS * cap, (int)cap}; };
+    auto tot_of = [&](int i) { return S->tot.p + (size_t)i * 4; };
+    auto allreduce = [&] {
+      if (nc) nck(nc->AllReduce(S->tot.p, S->tot.p, 3, ncclDouble, ncclSum, S->comm->comm, st), "ncclAllReduce");
+      else if (nl > 1) launch_slab_local_allreduce(S->tot.p, nl, 4, st);
+    };
+    int64_t& L = P->launches;
+    // ---- exchanges ----------------------------------------------------------
+    // halo views for slab i of buffer b: the neighbours' edge rows (in-process:
+    // their memory; NCCL: received into top/bot) or the global AR rows
+    std::vector<const double*> htop(nl), hbot(nl);
+    auto halos = [&](double* b) {
+      for (int i = 0; i < nl; ++i) {
+        const int p = S->rank0 + i;
+        double* bi = b + (size_t)i * slab;
+        double* ti = S->top.p + (size_t)i * q * n;
+        double* oi = S->bot.p + (size_t)i * q * n;
+        if (nc) {
+          nck(nc->GroupStart(), "ncclGroupStart");
+          if (p > 0) {
+            nck(nc->Send(bi, (size_t)q * n, ncclDouble, p - 1, S->comm->comm, st), "ncclSend");
+            nck(nc->Recv(ti, (size_t)q * n, ncclDouble, p - 1, S->comm->comm, st), "ncclRecv");
+          }
+          if (p + 1 < PP) {
+            nck(nc->Send(bi + (size_t)(R - q) * n, (size_t)q * n, ncclDouble, p + 1, S->comm->comm, st), "ncclSend");
+            nck(nc->Recv(oi, (size_t)q * n, ncclDouble, p + 1, S->comm->comm, st), "ncclRecv");
+          }
+          nck(nc->GroupEnd(), "ncclGroupEnd");
+          htop[i] = ti;
+          hbot[i] = oi;
+        } else {
+          htop[i] = p > 0 ? bi - (size_t)q * n : ti;
+          hbot[i] = p + 1 < PP ? bi + slab : oi;
+        }
+        if (p == 0 || p + 1 == PP) {
+          launch_slab_ar_halo(bi, R, n, q, p == 0 ? ti : nullptr, p + 1 == PP ? oi : nullptr, st);
+          ++L;
+        }
+      }
+    };
+    // all-to-all of nl x P chunks of R x C doubles (send -> recv)
+    auto all2all = [&] {
+      const size_t chunk = (size_t)R * C;
+      if (nc) {
+        nck(nc->GroupStart(), "ncclGroupStart");
+        for (int s = 0; s < PP; ++s) {
+          nck(nc->Send(S->send.p + s * chunk, chunk, ncclDouble, s, S->comm->comm, st), "ncclSend");
+          nck(nc->Recv(S->recv.p + s * chunk, chunk, ncclDouble, s, S->comm->comm, st), "ncclRecv");
+        }
+        nck(nc->GroupEnd(), "ncclGroupEnd");
+      } else {
+        for (int p = 0; p < nl; ++p)
+          for (int s = 0; s < PP; ++s)
+            ck(cudaMemcpyAsync(S->recv.p + (size_t)s * slab + p * chunk, S->send.p + (size_t)p * slab + s * chunk,
+                               chunk * sizeof(double), cudaMemcpyDeviceToDevice, st), "all-to-all copy");
+      }
+    };
+    auto pack = [&](const double* src, double* blocks, bool unpack) {  // slab (R x n) <-> P blocks of R x C
+      const size_t w = (size_t)C * sizeof(double), pitch = (size_t)n * sizeof(double);
+      for (int s = 0; s < PP; ++s) {
+        double* blk = blocks + (size_t)s * R * C;
+        double* col = const_cast<double*>(src) + (size_t)s * C;
+        if (unpack) ck(cudaMemcpy2DAsync(col, pitch, blk, w, w, R, cudaMemcpyDeviceToDevice, st), "unpack");
+        else ck(cudaMemcpy2DAsync(blk, w, col, pitch, w, R, cudaMemcpyDeviceToDevice, st), "pack");
+      }
+    };
+    // ---- blur of every local slab: y = A b (adjoint = 0, residual with g) or A' b
+    auto blur = [&](double* b, double* y, bool adjoint, bool resid) {
+      halos(b);
+      int cnt = 0;
+      for (int i = 0; i < nl; ++i) {
+        SpecArgs a = P->spec_base(S->st, part_of(i));
+        P->set_kernel(a.conv, adjoint);
+        a.conv.tw1 = reinterpret_cast<const double2*>(P->tw1);
+        a.conv.tw2 = reinterpret_cast<const double2*>(P->tw2);
+        a.conv.L1 = P->L1; a.conv.L2 = P->L2; a.conv.Lh = P->Lh;
+        a.zbuf = reinterpret_cast<double2*>(P->zb.p);
+        a.ybuf = reinterpret_cast<double2*>(P->yb.p);
+        a.out = y + (size_t)i * slab;
+        a.g = resid ? g + (size_t)i * slab : nullptr;
+        if (S->sep) {
+          a.in = b + (size_t)i * slab;
+          a.halo = q; a.htop = htop[i]; a.hbot = hbot[i];
+          lc(launch_rows_sep_seg(a, st), "rows_sep_seg");
+          cnt = lc(launch_cols_sep_epi(a, resid ? 1 : 0, st), "cols_sep_real");
+          L += 2;
+        } else {
+          double* e = S->ext.p;
+          ck(cudaMemcpyAsync(e, htop[i], (size_t)q * n * sizeof(double), cudaMemcpyDeviceToDevice, st), "ext");
+          ck(cudaMemcpyAsync(e + (size_t)q * n, b + (size_t)i * slab, slab * sizeof(double), cudaMemcpyDeviceToDevice,
+                             st), "ext");
+          ck(cudaMemcpyAsync(e + (size_t)(q + R) * n, hbot[i], (size_t)q * n * sizeof(double),
+                             cudaMemcpyDeviceToDevice, st), "ext");
+          a.in = e;
+          a.n1 = R + 2 * q;
+          lc(launch_conv_row_fwd(a, st), "launch_conv_row_fwd");
+          a.n1 = R;
+          a.preext = 1;
+          lc(launch_conv_col(a, st), "launch_conv_col");
+          a.preext = 0;
+          a.epi = resid ? SPEC_RESID : SPEC_STORE;
+          cnt = lc(launch_conv_row_inv(a, st), "launch_conv_row_inv");
+          L += 3;
+        }
+      }
+      P->check_launch();
+      return cnt;
+    };
+    auto rows = [&](int kind, const double* in, double* out, int rows_n, int i, int epi, const double* aux,
+                    const double* ff, int kind2) {
+      SpecArgs a = P->spec_base(S->st, part_of(i));
+      a.blue2 = P->blue_tables(1, false);
+      a.n1 = rows_n;
+      a.in = in; a.out = out; a.kind1 = kind; a.kind2 = kind2;
+      a.epi = epi;
+      a.d = epi == SPEC_HADAMARD || kind2 >= 0 ? aux : nullptr;
+      a.dstride = 0;
+      a.xold = epi == SPEC_AXPY ? aux : nullptr;
+      a.f = ff;
+      a.tau = tau;
+      ++L;
+      return lc(launch_dst_rows(a, st), "launch_dst_rows");
+    };
+    // ---- ||g||, ||f||, state -------------------------------------------------
+    for (int i = 0; i < nl; ++i) {
+      const int k = launch_slab_sumsq(g + (size_t)i * slab, f ? f + (size_t)i * slab : nullptr, slab, part_of(i), st);
+      launch_slab_tot(part_of(i), k, 0, 1, tot_of(i), nullptr, st);
+      L += 2;
+    }
+    allreduce();
+    launch_slab_state_init(S->st, S->tot.p, st);
+    ++L;
+    if (track) {  // rre() throws on a zero true image (image.hpp:89)
+      ImgState h;
+      ck(cudaMemcpyAsync(&h, S->st, sizeof h, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+      require(h.f_norm > 0.0, "rre: zero true image");
+    }
+    S->hist.ensure(2 * (size_t)max_iters);
+    ck(cudaMemsetAsync(S->x.p, 0, nl * slab * sizeof(double), st), "memset");
+    ck(cudaMemcpyAsync(S->r.p, g, nl * slab * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy");
+    for (int k = 1; k <= max_iters; ++k) {
+      // s = A' r, then T~ along the rows into u
+      blur(S->r.p, S->s.p, true, false);
+      for (int i = 0; i < nl; ++i)
+        rows(DBX_KIND_ARINV, S->s.p + i * slab, S->u.p + i * slab, R, i, SPEC_STORE, nullptr, nullptr, -1);
+      // column half of D on the transposed column blocks: T~, x d^T, T in one pass
+      if (PP == 1) {
+        launch_transpose(S->u.p, S->tA.p, R, n, st);
+        rows(DBX_KIND_ARINV, S->tA.p, S->tB.p, C, 0, SPEC_STORE, S->dTb.p, nullptr, DBX_KIND_AR);
+        launch_transpose(S->tB.p, S->s.p, C, n, st);
+        L += 2;
+      } else {
+        for (int i = 0; i < nl; ++i) pack(S->u.p + i * slab, S->send.p + i * slab, false);
+        all2all();
+        for (int i = 0; i < nl; ++i) {  // recv: n x C (rows stacked by source slab) -> C x n
+          launch_transpose(S->recv.p + i * slab, S->tA.p + i * slab, n, C, st);
+          rows(DBX_KIND_ARINV, S->tA.p + i * slab, S->tB.p + i * slab, C, i, SPEC_STORE, S->dTb.p + i * slab, nullptr,
+               DBX_KIND_AR);
+          launch_transpose(S->tB.p + i * slab, S->send.p + i * slab, C, n, st);
+          L += 2;
+        }
+        all2all();
+        for (int i = 0; i < nl; ++i) pack(S->s.p + i * slab, S->recv.p + i * slab, true);
+      }
+      // T along the rows, x_k = x_{k-1} + tau (.) in place, ||x||^2 and ||x - f||^2 partials
+      int cnt_x = 0;
+      for (int i = 0; i < nl; ++i)
+        cnt_x = rows(DBX_KIND_AR, S->s.p + i * slab, S->x.p + i * slab, R, i, SPEC_AXPY, S->x.p + i * slab,
+                     f ? f + i * slab : nullptr, -1);
+      // r = g - A x_k with ||r||^2 partials
+      const int cnt_r = blur(S->x.p, S->r.p, false, true);
+      for (int i = 0; i < nl; ++i) launch_slab_tot(part_of(i), cnt_x, cnt_r, track ? 1 : 0, tot_of(i), S->st, st);
+      allreduce();
+      launch_slab_finalize(S->st, S->tot.p, k, track ? S->hist.p : nullptr, S->hist.p + max_iters, track ? 1 : 0,
+                           stop_kind, resid_eps, st);
+      L += nl + 1;
+      if (track) {
+        launch_slab_best_copy(S->st, S->x.p, S->best.p, nl * slab, st);
+        ++L;
+      }
+      if (S->keep && k <= S->keep_n)
+        ck(cudaMemcpyAsync(S->keep + (size_t)(k - 1) * nl * slab, S->x.p, nl * slab * sizeof(double),
+                           cudaMemcpyDeviceToDevice, st), "keep iterate");
+      P->check_launch();
+    }
+    ImgState h;
+    ck(cudaMemcpyAsync(&h, S->st, sizeof h, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    const int done = h.done == 2 ? h.diverged_at - 1 : h.iters;
+    const double* src = (track && h.best_iter > 0) ? S->best.p : S->x.p;
+    ck(cudaMemcpyAsync(x_out, src, nl * slab * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy");
+    std::vector<double> hh(2 * (size_t)max_iters);
+    ck(cudaMemcpyAsync(hh.data(), S->hist.p, hh.size() * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    if (rre_hist && track) std::memcpy(rre_hist, hh.data(), sizeof(double) * (size_t)std::max(done, 0));
+    if (res_hist) std::memcpy(res_hist, hh.data() + max_iters, sizeof(double) * (size_t)std::max(done, 0));
+    *best_iter = h.best_iter;
+    *iters_done = done;
+    if (h.done == 2) {
+      char msg[160];
+      snprintf(msg, sizeof msg, "landweber: iterate exceeded 1e8 * ||g|| (row slabs, iteration %d)", h.diverged_at);
+      throw Diverged(msg);
+    }
+  });
 }
 
 }  // extern "C"

@@ -194,5 +194,14 @@ void launch_cg_xpay(const ImgState* st, const CgScalars* cs, const double* z, do
                     cudaStream_t s);
 void launch_slab_ar_rows(const double* x, double* ext, int rows, int n2, int q, int top, int bot, cudaStream_t s);
 void launch_transpose(const double* in, double* out, int rows, int cols, cudaStream_t s, int batch = 1);
+// C++ row-slab loop (dbx_slab_run)
+void launch_slab_ar_halo(const double* x, int rows, int n2, int q, double* top, double* bot, cudaStream_t s);
+int launch_slab_sumsq(const double* g, const double* f, size_t n, Partials pt, cudaStream_t s);
+void launch_slab_tot(Partials pt, int cnt_x, int cnt_r, int track, double* tot, const ImgState* st, cudaStream_t s);
+void launch_slab_local_allreduce(double* tots, int parts, int stride, cudaStream_t s);
+void launch_slab_state_init(ImgState* st, const double* tot2, cudaStream_t s);
+void launch_slab_finalize(ImgState* st, const double* tot, int k, double* rre_hist, double* res_hist, int track,
+                          int stop_kind, double eps, cudaStream_t s);
+void launch_slab_best_copy(const ImgState* st, const double* x, double* best, size_t n, cudaStream_t s);
 
 }  // namespace dbx

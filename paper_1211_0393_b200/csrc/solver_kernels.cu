@@ -228,6 +228,114 @@ __global__ void slab_ar_rows_kernel(const double* __restrict__ x, double* __rest
   if (bot) ext[(size_t)(q + rows + k - 1) * n2 + c] = 2.0 * x[(size_t)(rows - 1) * n2 + c] - x[(size_t)(rows - 1 - k) * n2 + c];
 }
 
+
+// ---- C++ row-slab loop (dbx_slab_run) -----------------------------------
+// Global AR rows of the first / last slab into separate halo buffers (the
+// separable slab blur reads halos in place): top[q - k] = 2 x[0] - x[k],
+// bot[k - 1] = 2 x[rows-1] - x[rows-1-k], k = 1..q (boundary.hpp:56-64).
+__global__ void slab_ar_halo_kernel(const double* __restrict__ x, int rows, int n2, int q, double* top, double* bot) {
+  DBX_PDL_WAIT();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.y + 1;
+  if (c >= n2) return;
+  if (top) top[(size_t)(q - k) * n2 + c] = 2.0 * x[c] - x[(size_t)k * n2 + c];
+  if (bot) bot[(size_t)(k - 1) * n2 + c] = 2.0 * x[(size_t)(rows - 1) * n2 + c] - x[(size_t)(rows - 1 - k) * n2 + c];
+}
+
+// sum of squares of the slab's g and f: per-CTA partials (slots X2 / XF2)
+__global__ void slab_sumsq_kernel(const double* g, const double* f, size_t n, size_t chunk, Partials pt) {
+  DBX_PDL_WAIT();
+  const size_t lo = (size_t)blockIdx.x * chunk, m = lo < n ? (n - lo < chunk ? n - lo : chunk) : 0;
+  const double gs = strided_sumsq(g + lo, m);
+  const double fs = f ? strided_sumsq(f + lo, m) : 0.0;
+  if (threadIdx.x == 0) {
+    pt.p[SLOT_X2 * pt.cap + blockIdx.x] = gs;
+    pt.p[SLOT_XF2 * pt.cap + blockIdx.x] = fs;
+  }
+}
+
+// fixed-order sums of the slab's partial slots into tot[0..2]
+__global__ void slab_tot_kernel(Partials pt, int cnt_x, int cnt_r, int track, double* tot, const ImgState* st) {
+  DBX_PDL_WAIT();
+  if (st && st->done) return;
+  const double x2 = partial_sum(pt.p + SLOT_X2 * pt.cap, cnt_x);
+  const double xf2 = track ? partial_sum(pt.p + SLOT_XF2 * pt.cap, cnt_x) : 0.0;
+  const double r2 = cnt_r > 0 ? partial_sum(pt.p + SLOT_R2 * pt.cap, cnt_r) : 0.0;
+  if (threadIdx.x == 0) {
+    tot[0] = x2;
+    tot[1] = xf2;
+    tot[2] = r2;
+  }
+}
+
+// in-process ranks (LocalWorld analogue): tot_p <- sum over p in rank order
+__global__ void slab_local_allreduce_kernel(double* tots, int parts, int stride) {
+  DBX_PDL_WAIT();
+  const int i = threadIdx.x;
+  if (i >= 3) return;
+  double s = 0.0;
+  for (int p = 0; p < parts; ++p) s += tots[(size_t)p * stride + i];
+  for (int p = 0; p < parts; ++p) tots[(size_t)p * stride + i] = s;
+}
+
+__global__ void slab_state_init_kernel(ImgState* st, const double* tot2) {
+  DBX_PDL_WAIT();
+  ImgState s;
+  s.cur = s.best = s.nxt = 0;
+  s.done = 0;
+  s.iters = 0;
+  s.best_iter = 0;
+  s.diverged_at = 0;
+  s.pad_ = 0;
+  s.best_rre = INFINITY;
+  s.g_norm = sqrt(tot2[0]);
+  s.f_norm = sqrt(tot2[1]);
+  *st = s;
+}
+
+// The loop bookkeeping of finalize_kernel on the all-reduced norms (every
+// rank holds the same totals, so every rank takes the same decisions).
+// s.best = 1 marks "x_k is the new best" for slab_best_copy_kernel.
+__global__ void slab_finalize_kernel(ImgState* st, const double* tot, int k, double* rre_hist, double* res_hist,
+                                     int track, int stop_kind, double eps) {
+  DBX_PDL_WAIT();
+  ImgState s = *st;
+  s.best = 0;
+  if (s.done) { *st = s; return; }
+  const double xn = sqrt(tot[0]);
+  if (xn > 1e8 * s.g_norm && s.g_norm > 0.0) {  // solver.hpp:107-108
+    s.done = 2;
+    s.diverged_at = k;
+    *st = s;
+    return;
+  }
+  const double rn = sqrt(tot[2]);
+  if (res_hist) res_hist[k - 1] = rn;
+  if (track) {
+    const double e = sqrt(tot[1]) / s.f_norm;
+    if (rre_hist) rre_hist[k - 1] = e;
+    if (e < s.best_rre) {  // strict '<' (solver.hpp:114)
+      s.best_rre = e;
+      s.best_iter = k;
+      s.best = 1;
+    }
+  }
+  s.iters = k;
+  if (stop_kind == 2 && s.g_norm > 0.0 && rn / s.g_norm < eps) s.done = 1;
+  *st = s;
+}
+
+__global__ void slab_best_copy_kernel(const ImgState* st, const double* __restrict__ x, double* __restrict__ best,
+                                      size_t n) {
+  DBX_PDL_WAIT();
+  if (!st->best) return;
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  double2* b2 = reinterpret_cast<double2*>(best);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 2; i += (size_t)gridDim.x * blockDim.x)
+    b2[i] = x2[i];
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) best[n - 1] = x[n - 1];
+}
+
 __global__ void zero_kernel(double* p, size_t n) {
   DBX_PDL_WAIT();
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -295,6 +403,36 @@ void launch_slab_ar_rows(const double* x, double* ext, int rows, int n2, int q, 
   if (q <= 0 || !(top || bot)) return;
   dim3 grid((n2 + 255) / 256, q);
   launch_k(slab_ar_rows_kernel, grid, 256, 0, s, x, ext, rows, n2, q, top, bot);
+}
+
+
+void launch_slab_ar_halo(const double* x, int rows, int n2, int q, double* top, double* bot, cudaStream_t s) {
+  if (q <= 0 || !(top || bot)) return;
+  dim3 grid((n2 + 255) / 256, q);
+  launch_k(slab_ar_halo_kernel, grid, 256, 0, s, x, rows, n2, q, top, bot);
+}
+int launch_slab_sumsq(const double* g, const double* f, size_t n, Partials pt, cudaStream_t s) {
+  int k = (int)((n + (1 << 20) - 1) >> 20);
+  k = k < 1 ? 1 : (k > pt.cap ? pt.cap : k);
+  const size_t chunk = (n + k - 1) / k;
+  launch_k(slab_sumsq_kernel, k, 256, 0, s, g, f, n, chunk, pt);
+  return k;
+}
+void launch_slab_tot(Partials pt, int cnt_x, int cnt_r, int track, double* tot, const ImgState* st, cudaStream_t s) {
+  launch_k(slab_tot_kernel, 1, 256, 0, s, pt, cnt_x, cnt_r, track, tot, st);
+}
+void launch_slab_local_allreduce(double* tots, int parts, int stride, cudaStream_t s) {
+  launch_k(slab_local_allreduce_kernel, 1, 32, 0, s, tots, parts, stride);
+}
+void launch_slab_state_init(ImgState* st, const double* tot2, cudaStream_t s) {
+  launch_k(slab_state_init_kernel, 1, 1, 0, s, st, tot2);
+}
+void launch_slab_finalize(ImgState* st, const double* tot, int k, double* rre_hist, double* res_hist, int track,
+                          int stop_kind, double eps, cudaStream_t s) {
+  launch_k(slab_finalize_kernel, 1, 1, 0, s, st, tot, k, rre_hist, res_hist, track, stop_kind, eps);
+}
+void launch_slab_best_copy(const ImgState* st, const double* x, double* best, size_t n, cudaStream_t s) {
+  launch_k(slab_best_copy_kernel, 1184, 256, 0, s, st, x, best, n);
 }
 
 void launch_zero(double* p, size_t n, cudaStream_t s) {

@@ -457,14 +457,18 @@ __global__ void __launch_bounds__(kColNT, col_minb(BAND)) cols_sep_real(SpecArgs
   const size_t N = (size_t)n1 * n2;
   const int c0 = blockIdx.x * kColW, p0 = blockIdx.z * BAND;
   const int rows = min(BAND, n1 - p0), E = n1 + 2 * Q;
-  const double* Z = reinterpret_cast<const double*>(a.zbuf) + (size_t)b * N;  // [c][row]
+  // halo mode (row slabs): Z^T holds the n1 + 2 Q extended rows (halo rows
+  // from the neighbours / the global AR rows), column stride E
+  const bool halo = a.halo != 0;
+  const int zs = halo ? E : n1;
+  const double* Z = reinterpret_cast<const double*>(a.zbuf) + (size_t)b * zs * n2;  // [c][row]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // stage interior rows rho in [rlo, rhi) at local l = rho + Q - p0 (cp.async, a column per warp pass)
-  const int rlo = max(0, p0 - Q), rhi = min(n1, p0 + NL - Q);
+  const int rlo = halo ? p0 - Q : max(0, p0 - Q), rhi = halo ? min(n1 + Q, p0 + NL - Q) : min(n1, p0 + NL - Q);
   const int lo = rlo + Q - p0, hi = rhi + Q - p0;
   for (int c = w; c < kColW; c += kColNT / 32) {
     if (c0 + c >= n2) break;
-    const double* zc = Z + (size_t)(c0 + c) * n1;
+    const double* zc = Z + (size_t)(c0 + c) * zs + (halo ? Q : 0);
     for (int rho = rlo + lane; rho < rhi; rho += 32) cp_async8(smd + (rho + Q - p0) * kColLD + c, zc + rho);
   }
   cp_async_commit();
@@ -475,7 +479,7 @@ __global__ void __launch_bounds__(kColNT, col_minb(BAND)) cols_sep_real(SpecArgs
     const int e = idx / kColW, c = idx - e * kColW;
     const int l = e < lo ? e : hi + (e - lo), p = p0 + l, rho = p - Q;
     double v = 0.0;
-    if (c0 + c < n2 && p < E) {
+    if (c0 + c < n2 && p < E && !halo) {
       if (a.bc == DBX_BC_REFLECTIVE) {
         v = smd[((rho < 0 ? -rho - 1 : 2 * n1 - 1 - rho) + Q - p0) * kColLD + c];
       } else {
@@ -554,12 +558,16 @@ __global__ void __launch_bounds__(kRowNT, 4) rows_sep_seg(SpecArgs a) {
   if (a.st && a.st[b].done) return;
   extern __shared__ double smd[];
   const int n1 = a.n1, n2 = a.n2, LSX = rowseg_ls(Q);
+  const int H = a.halo, ne = n1 + 2 * H;  // rows correlated (halo rows included)
   const size_t N = (size_t)n1 * n2;
   const int c0 = blockIdx.x * kRowSeg, r0 = blockIdx.y * 4;
-  const int nl = min(4, n1 - r0), nc = min(kRowSeg, n2 - c0), W = nc + 2 * Q;
+  const int nl = min(4, ne - r0), nc = min(kRowSeg, n2 - c0), W = nc + 2 * Q;
   const double* X = resolve_ptr(a.in, a.st, a.insel, b, a.batch, N);
   for (int h = 0; h < 4; ++h) {
-    const double* xr = X + (size_t)(r0 + h) * n2;
+    const int re = r0 + h;  // extended row index: [0, H) top halo, [H, H + n1) slab, then bottom halo
+    const double* xr = H == 0 ? X + (size_t)re * n2
+                     : re < H ? a.htop + (size_t)re * n2
+                     : re < H + n1 ? X + (size_t)(re - H) * n2 : a.hbot + (size_t)(re - H - n1) * n2;
     for (int j = threadIdx.x; j < W; j += kRowNT) {
       const int c = c0 + j - Q;
       double v = 0.0;
@@ -577,8 +585,8 @@ __global__ void __launch_bounds__(kRowNT, 4) rows_sep_seg(SpecArgs a) {
     }
   }
   __syncthreads();
-  sep_row_pass(smd, LSX, a.conv, Q, nc, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + (size_t)c0 * n1 + r0,
-               n1);
+  sep_row_pass(smd, LSX, a.conv, Q, nc, nl, reinterpret_cast<double*>(a.zbuf) + (size_t)b * ne * n2 + (size_t)c0 * ne + r0,
+               ne);
 }
 
 }  // namespace
@@ -668,7 +676,7 @@ int launch_cols_sep_epi(const SpecArgs& a, int resid, cudaStream_t s) {
 bool rows_sep_supported(int q2) { return q2 == 7 || q2 == 15; }
 
 int launch_rows_sep_seg(const SpecArgs& a, cudaStream_t s) {
-  dim3 grid((a.n2 + kRowSeg - 1) / kRowSeg, (a.n1 + 3) / 4, a.batch);
+  dim3 grid((a.n2 + kRowSeg - 1) / kRowSeg, (a.n1 + 2 * a.halo + 3) / 4, a.batch);
   const size_t sm = (size_t)4 * rowseg_ls(a.q2) * 8;
   if (a.q2 == 15) launch_k(rows_sep_seg<15>, grid, kRowNT, sm, s, a);
   else if (a.q2 == 7) launch_k(rows_sep_seg<7>, grid, kRowNT, sm, s, a);

@@ -72,6 +72,13 @@ struct SpecArgs {
   double2* ybuf = nullptr;                       // [batch][n1][Lh]
   int ztrans = 0;                                // fused pipeline: row-FFT spectra stored transposed
   int preext = 0;                                // conv_col: n1 + 2 q1 input rows already extended (row slabs)
+  // row slabs, separable direct blur: halo = q1 rows above (htop) and below
+  // (hbot) the slab's n1 rows; rows_sep_seg then correlates n1 + 2 halo rows
+  // into Z^T (column stride n1 + 2 halo) and cols_sep_real reads them as the
+  // vertical extension instead of synthesising it
+  int halo = 0;
+  const double* htop = nullptr;
+  const double* hbot = nullptr;
   const double* dT = nullptr;                    // d transposed [n2][n1] (fused column pass)
   size_t dstride = 0;                            // filter grid per image (alpha sweep) or shared (0)
   // DST

@@ -19,6 +19,18 @@ preconditioned iteration (solver.hpp:101-125) is
                guard, histories, strict-'<' best iterate, residual rule) is
                then identical on every rank.
 
+Two drivers of the same decomposition:
+
+* `SlabRun` (the product path): the whole loop in C++ behind the C-ABI
+  (`dbx_slab_create` / `dbx_slab_run`): grouped ncclSend/ncclRecv halos and
+  all-to-alls, the separable direct blur on halo-extended slabs, a device-side
+  ncclAllReduce of the three norms and device bookkeeping — no host
+  synchronisation inside the loop.  The NCCL communicator is built by the
+  library (`NcclComm`: the unique id travels over torch.distributed once).
+* `SlabLandweber`: the original Python orchestration of the C-ABI building
+  blocks (kept as an independent second implementation of the exchange
+  schedule; its exchange layer is what the gloo world-size-2 tests drive).
+
 Every compute step is a CUDA kernel of the C-ABI; torch is used for device
 buffers and torch.distributed for the exchanges only.  `LocalWorld` runs the
 P ranks of the decomposition inside one process (single-GPU parity tests:
@@ -260,3 +272,87 @@ class SlabLandweber:
         self._fence()
         return {"restored": restored, "iterations_executed": done, "best_iteration": best_iter,
                 "rre_history": rre, "residual_history": res}
+
+
+class NcclComm:
+    """An NCCL communicator owned by libdbx (ncclCommInitRank); the unique id
+    is broadcast from rank 0 over the default torch.distributed group."""
+
+    def __init__(self, device: int):
+        import torch
+        import torch.distributed as dist
+        L = lib()
+        self.rank, self.size = dist.get_rank(), dist.get_world_size()
+        buf = (C.c_ubyte * 128)()
+        if self.rank == 0:
+            _check(L.dbx_comm_unique_id(buf))
+        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8,
+                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.broadcast(t, 0)
+        raw = (C.c_ubyte * 128)(*t.cpu().tolist())
+        h = C.c_void_p()
+        _check(L.dbx_comm_init(self.size, raw, self.rank, device, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib().dbx_comm_destroy(self.handle)
+            self.handle = None
+
+
+class SlabRun:
+    """D-Landweber on an n x n image in `parts` row slabs, driven in C++.
+
+    rank = -1: this process holds all slabs (in-process ranks: exchanges are
+    device copies); else it holds slab `rank` and `comm` (NcclComm) carries
+    the exchanges (required for parts > 1)."""
+
+    def __init__(self, n: int, parts: int, taps, q: int, alpha: float, rank: int = -1, comm=None,
+                 device: int = 0):
+        L = lib()
+        h = C.c_void_p()
+        _check(L.dbx_slab_create(n, parts, rank, _ptr(taps), q, q, float(alpha),
+                                 comm.handle if comm is not None else None, device, C.byref(h)))
+        self.handle, self.n, self.parts, self.rank = h, n, parts, rank
+        rows, loc, sep = C.c_int(), C.c_int(), C.c_int()
+        _check(L.dbx_slab_info(h, C.byref(rows), C.byref(loc), C.byref(sep), None))
+        self.rows, self.local_slabs, self.separable = rows.value, loc.value, bool(sep.value)
+
+    def stream(self):
+        return lib().dbx_slab_stream(self.handle)
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _check(lib().dbx_slab_info(self.handle, None, None, None, C.byref(n)))
+        return n.value
+
+    def run(self, g, f=None, iters: int = 20, tau: float = 1.0, resid_eps: Optional[float] = None, out=None,
+            keep_iterates: bool = False):
+        """g, f, out: device tensors of the rows held here (local_slabs * rows x n).
+        Returns (restored, history dict); keep_iterates adds "iterates" (a
+        device tensor iters x rows x n of every x_k, for the parity tests)."""
+        import numpy as np
+        import torch
+        out = torch.empty_like(g) if out is None else out
+        keep = None
+        if keep_iterates:
+            keep = torch.empty((iters,) + tuple(g.shape), dtype=g.dtype, device=g.device)
+            _check(lib().dbx_slab_set_iterates(self.handle, _ptr(keep), iters))
+        rre, res = np.zeros(iters), np.zeros(iters)
+        best, done = C.c_int(), C.c_int()
+        stop = 2 if resid_eps is not None else (1 if f is not None else 0)
+        try:
+            _check(lib().dbx_slab_run(self.handle, _ptr(g), _ptr(f) if f is not None else None, float(tau), iters,
+                                      stop, float(resid_eps or 0.0), _ptr(out), _ptr(rre), _ptr(res), C.byref(best),
+                                      C.byref(done)))
+        finally:
+            if keep is not None:
+                _check(lib().dbx_slab_set_iterates(self.handle, None, 0))
+        k = done.value
+        return out, {"iterates": keep, "iterations_executed": k, "best_iteration": best.value,
+                     "rre_history": list(rre[:k]) if f is not None else [], "residual_history": list(res[:k])}
+
+    def close(self):
+        if self.handle:
+            lib().dbx_slab_destroy(self.handle)
+            self.handle = None

@@ -183,3 +183,31 @@ def test_c5_row_slabs_p2_every_iteration(dev, orc, c5):
         solver.close()
     check_run(lambda k: xs[k], run["rre_history"], run["residual_history"], run["best_iteration"],
               run["iterations_executed"], ref, "C5 slabs P=2")
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_c5_cpp_slab_loop_every_iteration(dev, orc, c5, P):
+    """C5 8192^2 through the C++ row-slab loop (dbx_slab_run: separable direct
+    blur on halo-extended slabs, fused T~ d^T T column blocks, device-side
+    norms and bookkeeping) with P in-process ranks, against the oracle at every
+    iteration."""
+    import torch
+
+    from paper_1211_0393_b200 import configs as cf
+    from paper_1211_0393_b200.slab import SlabRun
+    c = cf.CONFIGS["C5"]
+    n, iters = c.n, C5_ITERS
+    (f, g, taps), ref = c5
+    d0 = torch.device("cuda", 0)
+    gt, ft = torch.from_numpy(g).to(d0), torch.from_numpy(f).to(d0)
+    run = SlabRun(n, P, taps, c.q, c.alpha, rank=-1, device=0)
+    try:
+        assert run.separable and run.local_slabs == P
+        out, h = run.run(gt, ft, iters, keep_iterates=True)
+        xs = h["iterates"]
+        check_run(lambda k: xs[k - 1].cpu().numpy(), h["rre_history"], h["residual_history"], h["best_iteration"],
+                  h["iterations_executed"], ref, f"C5 C++ slabs P={P}")
+        best = h["best_iteration"]
+        assert rel(out.cpu().numpy(), ref["iterates"][best - 1]) <= ITER_TOL
+    finally:
+        run.close()

@@ -117,3 +117,126 @@ def test_slab_landweber_matches_single_image(dbx, P, n, iters):
     np.testing.assert_allclose(run["rre_history"], ref.rre_history, rtol=1e-10, atol=0)
     restored = np.concatenate([run["restored"][p].cpu().numpy() for p in range(P)])
     assert np.linalg.norm(restored - ref.restored) / np.linalg.norm(ref.restored) <= 1e-10
+
+
+# ---------------------------------------------------------------------------
+# The C++ row-slab loop (dbx_slab_run) against the oracle
+@pytest.fixture(scope="module")
+def _orc_threads(oracle):
+    oracle.set_threads(os.cpu_count() or 1)
+    yield oracle
+    oracle.set_threads(1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,P,n,iters", [("C5", 1, 256, 8), ("C5", 2, 256, 8), ("C5", 4, 256, 8),
+                                           ("C2", 2, 128, 6), ("C4", 4, 256, 4)])
+def test_cpp_slab_loop_matches_oracle(dbx, _orc_threads, cfg, P, n, iters):
+    """Every iterate of the C++ slab loop (P in-process ranks) vs the oracle's
+    single-image run; C2 (motion mask, q = 10) and C4 (rotated Gaussian,
+    q = 31) are not rank 1 and take the FFT slab blur."""
+    from paper_1211_0393_b200 import configs as cf
+    from paper_1211_0393_b200.slab import SlabRun
+    O = _orc_threads
+    c = cf.CONFIGS[cfg]
+    f, g, taps = cf.make_problem(c, n=n)
+    ref = O.landweber(taps, g, d=O.build_tikhonov(taps, c.alpha, n, n), f_true=f, max_iters=iters,
+                      keep_iterates=True)
+    dev = torch.device("cuda", 0)
+    run = SlabRun(n, P, taps, c.q, c.alpha, rank=-1, device=0)
+    try:
+        assert run.separable == (cfg == "C5")
+        out, h = run.run(torch.from_numpy(g).to(dev), torch.from_numpy(f).to(dev), iters, keep_iterates=True)
+        assert h["iterations_executed"] == ref["iterations_executed"]
+        assert h["best_iteration"] == ref["best_iteration"]
+        np.testing.assert_allclose(h["residual_history"], ref["residual_history"], rtol=1e-10, atol=0)
+        np.testing.assert_allclose(h["rre_history"], ref["rre_history"], rtol=1e-10, atol=0)
+        for k in range(1, iters + 1):
+            x = h["iterates"][k - 1].cpu().numpy()
+            e = np.linalg.norm(x - ref["iterates"][k - 1]) / np.linalg.norm(ref["iterates"][k - 1])
+            assert e <= 1e-10, (k, e)
+        best = ref["iterates"][ref["best_iteration"] - 1]
+        assert np.linalg.norm(out.cpu().numpy() - best) / np.linalg.norm(best) <= 1e-10
+    finally:
+        run.close()
+
+
+@pytest.mark.gpu
+def test_cpp_slab_loop_stopping_rules(dbx, _orc_threads):
+    """Fixed iterations without a true image, and the residual rule (the loop
+    keeps launching after the stop; every kernel then sees the done flag)."""
+    from paper_1211_0393_b200 import configs as cf
+    from paper_1211_0393_b200.slab import SlabRun
+    O = _orc_threads
+    c = cf.CONFIGS["C5"]
+    n = 128
+    f, g, taps = cf.make_problem(c, n=n)
+    dev = torch.device("cuda", 0)
+    gt = torch.from_numpy(g).to(dev)
+    run = SlabRun(n, 2, taps, c.q, c.alpha, rank=-1, device=0)
+    try:
+        ref = O.landweber(taps, g, d=O.build_tikhonov(taps, c.alpha, n, n), stop=O.STOP_FIXED, fixed_iters=5)
+        out, h = run.run(gt, None, 5)
+        assert h["iterations_executed"] == 5 and h["best_iteration"] == 0
+        np.testing.assert_allclose(h["residual_history"], ref["residual_history"], rtol=1e-10, atol=0)
+        x = out.cpu().numpy()
+        assert np.linalg.norm(x - ref["restored"]) / np.linalg.norm(ref["restored"]) <= 1e-10
+        eps = ref["residual_history"][2] / np.linalg.norm(g) * 1.0000001
+        ref2 = O.landweber(taps, g, d=O.build_tikhonov(taps, c.alpha, n, n), stop=O.STOP_RESID, max_iters=10,
+                           resid_eps=eps)
+        out2, h2 = run.run(gt, None, 10, resid_eps=eps)
+        assert h2["iterations_executed"] == ref2["iterations_executed"] == 3
+        x2 = out2.cpu().numpy()
+        assert np.linalg.norm(x2 - ref2["restored"]) / np.linalg.norm(ref2["restored"]) <= 1e-10
+        with pytest.raises(ValueError, match="zero true image"):
+            run.run(gt, torch.zeros_like(gt), 2)
+    finally:
+        run.close()
+
+
+@pytest.mark.gpu
+def test_nccl_comm_single_rank(dbx):
+    """libnccl resolves at run time and a one-rank communicator drives a
+    one-slab run (rank 0 of 1: no exchange is issued, the path is the
+    NCCL-rank code path)."""
+    import ctypes as C
+
+    from paper_1211_0393_b200 import configs as cf
+    from paper_1211_0393_b200.slab import SlabRun
+    L = dbx.lib()
+    uid = (C.c_ubyte * 128)()
+    assert L.dbx_comm_unique_id(uid) == 0, L.dbx_last_error()
+    h = C.c_void_p()
+    assert L.dbx_comm_init(1, uid, 0, 0, C.byref(h)) == 0, L.dbx_last_error()
+
+    class _Comm:
+        handle = h
+    try:
+        c = cf.CONFIGS["C5"]
+        f, g, taps = cf.make_problem(c, n=128)
+        dev = torch.device("cuda", 0)
+        a = SlabRun(128, 1, taps, c.q, c.alpha, rank=0, comm=_Comm(), device=0)
+        b = SlabRun(128, 1, taps, c.q, c.alpha, rank=-1, device=0)
+        try:
+            ga, fa = torch.from_numpy(g).to(dev), torch.from_numpy(f).to(dev)
+            xa, ha = a.run(ga, fa, 4)
+            xb, hb = b.run(ga, fa, 4)
+            assert torch.equal(xa, xb) and ha["rre_history"] == hb["rre_history"]
+        finally:
+            a.close()
+            b.close()
+    finally:
+        L.dbx_comm_destroy(h)
+
+
+def test_slab_create_without_device_fails_loudly(dbx):
+    """No sm_100 device (this CPU box): the C++ slab loop refuses with a device
+    error, there is no CPU fallback."""
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    from paper_1211_0393_b200 import configs as cf
+    from paper_1211_0393_b200.slab import SlabRun
+    c = cf.CONFIGS["C5"]
+    _, _, taps = cf.make_problem(c, n=64)
+    with pytest.raises(dbx.DeviceError):
+        SlabRun(64, 2, taps, c.q, c.alpha, rank=-1, device=0)
