@@ -299,14 +299,16 @@ def run_reference(args):
 
 
 def run_slab(args):
-    """One image split into row slabs across the ranks (C5):
-    NCCL halo exchange for the blur and all-to-all transposes for the column
-    DST; strong scaling (the image is fixed)."""
+    """One image split into row slabs across the ranks (C5),
+    through the C++ slab loop (dbx_slab_run): NCCL halo send/recv for the blur,
+    all-to-all from grouped send/recv for the column blocks of D, device-side
+    all-reduce of the norms and device bookkeeping; strong scaling (the image
+    is fixed)."""
     import torch
     import torch.distributed as dist
 
     from paper_1211_0393_b200 import configs as cf
-    from paper_1211_0393_b200.slab import DistWorld, LocalWorld, SlabLandweber
+    from paper_1211_0393_b200.slab import NcclComm, SlabRun
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
@@ -316,49 +318,78 @@ def run_slab(args):
     F, G, taps = cf.make_batch(cfg, 1)
     R = n // world
     dev = torch.device("cuda", local)
-    g = {rank: torch.from_numpy(np.ascontiguousarray(G[0, rank * R:(rank + 1) * R])).to(dev)}
-    f = {rank: torch.from_numpy(np.ascontiguousarray(F[0, rank * R:(rank + 1) * R])).to(dev)}
+    gh = torch.from_numpy(np.ascontiguousarray(G[0, rank * R:(rank + 1) * R])).pin_memory()
+    fh = torch.from_numpy(np.ascontiguousarray(F[0, rank * R:(rank + 1) * R])).pin_memory()
     del F, G
-    solver = SlabLandweber(DistWorld() if world > 1 else LocalWorld(1), n, taps, q, cfg.alpha, device=local)
+    g, f = gh.to(dev), fh.to(dev)
+    comm = NcclComm(local) if world > 1 else None
+    solver = SlabRun(n, world, taps, q, cfg.alpha, rank=rank if world > 1 else -1, comm=comm, device=local)
+    out = torch.empty_like(g)
     for _ in range(args.warmup):
-        solver.run(g, f, H)
+        solver.run(g, f, H, out=out)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    stream = torch.cuda.ExternalStream(solver.stream())
     clocks = Clocks(local)
     clocks.start()
+    l0 = solver.launch_count()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    t0.record()
+    t0.record(stream)
     for _ in range(args.steps):
-        solver.run(g, f, H)
-    t1.record()
+        solver.run(g, f, H, out=out)
+    t1.record(stream)
     torch.cuda.synchronize()
+    launches = (solver.launch_count() - l0) // max(args.steps, 1)
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    t = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+    # e2e: the same call with the rank's slab uploaded from pinned host memory
+    # and the restored slab read back inside the timed region
+    oh = torch.empty_like(gh).pin_memory()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        g.copy_(gh, non_blocking=True)
+        f.copy_(fh, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        solver.run(g, f, H, out=out)
+        oh.copy_(out, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([t0.elapsed_time(t1), e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_max = float(t.item())
+    t_max, t_e2e = float(t[0].item()), float(t[1].item())
     px_it = n * n * H * args.steps
     value = px_it / (t_max * 1e-3) / 1e6
+    separable = solver.separable
     solver.close()
+    if comm is not None:
+        comm.close()
     if rank == 0:
         hbm = float(json.load(open(HBM_FILE))["hbm_gbs"]) if os.path.exists(HBM_FILE) else 7700.0
         gbs = 72.0 * px_it / (t_max * 1e-3) / 1e9 / world
+        slab_bytes = R * n * 8
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded scene/mask/noise, host-generated)",
                 "config": {"workload": f"{cfg.name}: one {n}x{n} FP64 image in {world} row slabs of {R} rows, "
                                        f"q={q}, {H} D-Landweber iterations",
-                           "parallelism": f"row slabs x{world} (NCCL halo send/recv + all-to-all transposes)",
+                           "parallelism": f"row slabs x{world} (C++ loop: NCCL halo send/recv, all-to-all from "
+                                          "grouped send/recv, device all-reduce)",
+                           "blur": "separable direct on halo-extended slabs" if separable else "FFT slab blur",
                            "l2": "slab arrays exceed L2"},
-                "clocks": clk, "gpu_launches": None,
+                "clocks": clk, "gpu_launches": int(launches),
                 "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                              "traffic": None, "note": "SURVEY canonical 72 B per pixel-iteration, per GPU"},
-                "e2e": None, "cpu_baseline": None}
+                "e2e": {"value": px_it / (t_e2e * 1e-3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": 2 * slab_bytes,
+                        "d2h_bytes_per_step": slab_bytes,
+                        "path": "SlabRun.run (dbx_slab_run) with the slab uploaded from pinned host memory"},
+                "cpu_baseline": None}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
