@@ -797,6 +797,13 @@ int launch_fused(int which, const SpecArgs& a, cudaStream_t s) {
     const int c = launch_dst_tcols_w(a, s);
     if (c >= 0) return c;
   }
+  // warp-owned separable row kernels (wdst.cu) for 1024-point rows;
+  // DBX_WROWS=0 keeps the CTA lock-step ones (A/B and tests)
+  static const bool wrows_off = [] { const char* e = getenv("DBX_WROWS"); return e && e[0] == '0'; }();
+  if ((which == FUSED_TT_SEP || which == FUSED_T_AXPY_SEP) && !wrows_off) {
+    const int c = launch_rows_w(which == FUSED_TT_SEP ? 0 : 1, a, s);
+    if (c >= 0) return c;
+  }
   const int L2 = a.conv.L2, M = a.blue2.M;
   const bool blue = a.blue2.M != a.blue2.N;
 #define X(L, MM, BL)                                                                          \

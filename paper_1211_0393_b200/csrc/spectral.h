@@ -129,6 +129,9 @@ int launch_cols_sep_epi(const SpecArgs& a, int resid, cudaStream_t s);
 int launch_fused(int which, const SpecArgs& a, cudaStream_t s);
 // wdst.cu: warp-owned column half of D for 1024-point columns (-1: not this shape)
 int launch_dst_tcols_w(const SpecArgs& a, cudaStream_t s);
+// wdst.cu: warp-owned separable-pipeline row kernels for 1024-point rows
+// (which 0: rows_tt_w = K2, 1: rows_t_axpy_w = K4; -1: not this shape)
+int launch_rows_w(int which, const SpecArgs& a, cudaStream_t s);
 #ifdef DBX_PHASES
 int fused_debug_phases(unsigned long long* out, int n);  // read + reset (instrumented builds)
 #endif

@@ -515,6 +515,216 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-owned ROW kernels of the separable fused pipeline for n2 = 1024 (the
+// rows of C3): the same DFT_1023 / split as dst_tcols_w, one warp per packed
+// row pair, and ONE CTA barrier before the cooperative transposed stores.
+// CTA = kWWarps warps = 8 rows r0 .. r0+7.
+//
+// rows_tt_w (K2, replaces rows_ainv_tt<SEP>): s = A'r rows (row-major, ybuf)
+// -> T~ along the rows (ar_inverse, transforms.hpp:163-173) -> u^T[k][row]
+// (64-byte row segments: 8 rows per column k).
+constexpr int kRowLS = 1076;  // rows_t_axpy_w: double stride of the 8 x rows (= 4 mod 16, sep_row_stencil_T)
+
+__global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_tt_w(SpecArgs a) {
+  DBX_PDL_WAIT();
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 wsm[];
+  __shared__ double ends[2 * kWWarps][2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double2* buf = wsm + (size_t)w * kWLine;
+  const BlueTables& bt = a.blue2;
+  const int n1 = a.n1, n2 = a.n2;
+  const size_t N = (size_t)n1 * n2;
+  const int r0 = 2 * kWWarps * blockIdx.x, r = r0 + 2 * w;  // rows r, r+1
+  const bool act = r < n1, hb = r + 1 < n1;
+  if (act) {
+    const double ri = bt.rinv, hs = 0.5 * bt.scale, sc = bt.scale;
+    const double* __restrict__ sn = bt.sn;
+    const double* ua = reinterpret_cast<const double*>(a.ybuf) + (size_t)b * N + (size_t)r * n2;
+    const double* ub = hb ? ua + n2 : ua;
+    const double x0a = __ldg(ua), xea = __ldg(ua + n2 - 1), x0b = __ldg(ub), xeb = __ldg(ub + n2 - 1);
+    if (lane == 0) {
+      ends[2 * w][0] = x0a; ends[2 * w][1] = xea;
+      ends[2 * w + 1][0] = x0b; ends[2 * w + 1][1] = xeb;
+    }
+    const double sa = x0a + xea, sb = x0b + xeb, da = x0a - xea, db = x0b - xeb;
+    double ap[16], aq[16], bp[16], bq[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int p = lane + 32 * j, q = kWN - p;
+      ap[j] = __ldg(ua + p);
+      aq[j] = __ldg(ua + q);
+      bp[j] = __ldg(ub + p);
+      bq[j] = __ldg(ub + q);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int p = lane + 32 * j, q = kWN - p;
+      const double rr = fma(-2.0 * ri, (double)p, 1.0), s = __ldg(sn + p);
+      const double Aa = ap[j] + aq[j] - sa, Ba = (ap[j] - aq[j]) - da * rr;
+      const double Ab = bp[j] + bq[j] - sb, Bb = (bp[j] - bq[j]) - db * rr;
+      if (p == 0) {
+        buf[wslot(0)] = make_double2(0.0, 0.0);
+      } else {
+        buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), hb ? fma(s, Ab, 0.5 * Bb) : 0.0);
+        buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), hb ? fma(s, Ab, -0.5 * Bb) : 0.0);
+      }
+    }
+    __syncwarp();
+    WDFT(buf, bt.tw, lane);
+    wsplit(buf, lane, hs, sc);
+  }
+  __syncthreads();
+  // u^T[k][r0 + 2 ww .. + 1] from warp ww's line: 4 x 16 bytes per column k
+  double* uT = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N));
+  const double al = bt.alpha;
+#pragma unroll 4
+  for (int idx = threadIdx.x; idx < kWWarps * n2; idx += 32 * kWWarps) {
+    const int ww = idx & (kWWarps - 1), k = idx / kWWarps;
+    const int rr = r0 + 2 * ww;
+    if (rr >= n1) continue;
+    double2 o = wsm[(size_t)ww * kWLine + oslot(k)];
+    if (k == 0) o = make_double2(al * ends[2 * ww][0], al * ends[2 * ww + 1][0]);
+    if (k == n2 - 1) o = make_double2(al * ends[2 * ww][1], al * ends[2 * ww + 1][1]);
+    double* dst = uT + (size_t)k * n1 + rr;
+    if (rr + 1 < n1) *reinterpret_cast<double2*>(dst) = o;
+    else *dst = o.x;
+  }
+}
+
+// rows_t_axpy_w (K4, replaces rows_t_axpy_afwd<SEP>): T along the rows of v
+// (ar_forward, transforms.hpp:148-160) -> x_k = x_{k-1} + tau T v
+// (solver.hpp:106) with ||x||^2, ||x - f||^2 partials -> the x_k rows,
+// AR-extended in place (boundary.hpp:56-62), correlated with A's row taps into
+// Z^T (sep_row_stencil_T, 4 rows at a time).  Warp w's region (kRowLS
+// double2) holds its DFT line, then its two x rows at double offsets 16 and
+// kRowLS + 16 of the CTA's 8-row stencil block.
+__global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_t_axpy_w(SpecArgs a) {
+  DBX_PDL_WAIT();
+  const int b = blockIdx.y;
+  if (a.st && a.st[b].done) return;
+  extern __shared__ double2 wsm[];
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double2* buf = wsm + (size_t)w * kRowLS;
+  double* xs = reinterpret_cast<double*>(wsm);  // 8 rows at stride kRowLS, data at offset 16
+  const BlueTables& bt = a.blue2;
+  const int n1 = a.n1, n2 = a.n2, q2 = a.q2;
+  const size_t N = (size_t)n1 * n2;
+  const int r0 = 2 * kWWarps * blockIdx.x, r = r0 + 2 * w;
+  const bool act = r < n1, hb = r + 1 < n1;
+  const double* xo = resolve_ptr(a.xold, a.st, a.xoldsel, b, a.batch, N) + (size_t)r * n2;
+  const double* fimg = a.f ? a.f + (size_t)b * N + (size_t)r * n2 : nullptr;
+  // x_{k-1} and f rows are read after the two DFTs: start them towards L2 now
+  if (act && lane == 0) {
+    prefetch_l2(xo, (unsigned)((hb ? 2 : 1) * n2 * 8));
+    if (fimg) prefetch_l2(fimg, (unsigned)((hb ? 2 : 1) * n2 * 8));
+  }
+  double p0 = 0.0, p1 = 0.0;
+  if (act) {
+    const double ri = bt.rinv, hs = 0.5 * bt.scale, sc = bt.scale, tau = a.tau, ia = 1.0 / bt.alpha;
+    const double* __restrict__ sn = bt.sn;
+    const double* va = a.in + (size_t)b * N + (size_t)r * n2;
+    const double* vb = hb ? va + n2 : va;
+    const double a0a = ia * __ldg(va), a1a = ia * __ldg(va + n2 - 1);
+    const double a0b = ia * __ldg(vb), a1b = ia * __ldg(vb + n2 - 1);
+    double ap[16], aq[16], bp[16], bq[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int p = lane + 32 * j, q = kWN - p;
+      ap[j] = __ldg(va + p);
+      aq[j] = __ldg(va + q);
+      bp[j] = __ldg(vb + p);
+      bq[j] = __ldg(vb + q);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int p = lane + 32 * j, q = kWN - p;
+      const double s = __ldg(sn + p);
+      const double Aa = ap[j] + aq[j], Ba = ap[j] - aq[j];
+      const double Ab = bp[j] + bq[j], Bb = bp[j] - bq[j];
+      if (p == 0) {
+        buf[wslot(0)] = make_double2(0.0, 0.0);
+      } else {
+        buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), hb ? fma(s, Ab, 0.5 * Bb) : 0.0);
+        buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), hb ? fma(s, Ab, -0.5 * Bb) : 0.0);
+      }
+    }
+    __syncwarp();
+    WDFT(buf, bt.tw, lane);
+    wsplit(buf, lane, hs, sc);
+    // x_k = x_{k-1} + tau w, w = the T output with the ramp; all line reads
+    // precede the x row writes into the same region
+    double* xn = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + (size_t)r * n2;
+    double xa[32], xb[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int k = lane + 32 * j;
+      const double2 o = buf[oslot(k)];
+      const double t1 = (double)k * ri;
+      double wa = o.x + a0a * (1.0 - t1) + a1a * t1;
+      double wb = o.y + a0b * (1.0 - t1) + a1b * t1;
+      if (k == 0) { wa = a0a; wb = a0b; }
+      if (k == n2 - 1) { wa = a1a; wb = a1b; }
+      xa[j] = __ldcs(xo + k) + tau * wa;
+      xn[k] = xa[j];
+      p0 += xa[j] * xa[j];
+      if (fimg) {
+        const double e = xa[j] - __ldcs(fimg + k);
+        p1 += e * e;
+      }
+      if (hb) {
+        xb[j] = __ldcs(xo + n2 + k) + tau * wb;
+        xn[n2 + k] = xb[j];
+        p0 += xb[j] * xb[j];
+        if (fimg) {
+          const double e = xb[j] - __ldcs(fimg + n2 + k);
+          p1 += e * e;
+        }
+      } else {
+        xb[j] = 0.0;
+      }
+    }
+    __syncwarp();
+    double* ra = xs + (size_t)(2 * w) * kRowLS + 16;
+    double* rb = ra + kRowLS;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      ra[lane + 32 * j] = xa[j];
+      rb[lane + 32 * j] = xb[j];
+    }
+    __syncwarp();
+    // AR extension of both rows (f_{-k} = 2 f_0 - f_k, f_{n-1+k} = 2 f_{n-1} - f_{n-1-k})
+    for (int m = lane; m < 2 * q2; m += 32) {
+      if (m < q2) {
+        const int k = q2 - m;
+        ra[-k] = 2.0 * ra[0] - ra[k];
+        rb[-k] = 2.0 * rb[0] - rb[k];
+      } else {
+        const int k = m - q2 + 1;
+        ra[n2 - 1 + k] = 2.0 * ra[n2 - 1] - ra[n2 - 1 - k];
+        rb[n2 - 1 + k] = 2.0 * rb[n2 - 1] - rb[n2 - 1 - k];
+      }
+    }
+  }
+  __syncthreads();
+  double* zT = reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0;
+  for (int h0 = 0; h0 < 2 * kWWarps; h0 += 4) {
+    const int nl = n1 - r0 - h0 < 4 ? n1 - r0 - h0 : 4;
+    if (nl > 0) sep_row_pass(xs + (size_t)h0 * kRowLS + 16 - q2, kRowLS, a.conv, q2, n2, nl, zT + h0, n1);
+  }
+  if (a.part.p) {
+    double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
+    const double s0 = block_sum<32 * kWWarps>(p0, red);
+    if (threadIdx.x == 0) P[SLOT_X2 * a.part.cap + blockIdx.x] = s0;
+    const double s1 = block_sum<32 * kWWarps>(p1, red);
+    if (threadIdx.x == 0) P[SLOT_XF2 * a.part.cap + blockIdx.x] = s1;
+  }
+}
+
 }  // namespace
 
 // Warp-owned column half of D for n1 = 1024 (direct 1023-point core); returns
@@ -529,4 +739,25 @@ int launch_dst_tcols_w(const SpecArgs& a, cudaStream_t s) {
   return (int)grid.x;
 }
 
+}  // namespace dbx
+
+namespace dbx {
+// Warp-owned row kernels of the separable pipeline for n2 = 1024 (direct
+// 1023-point core, q2 <= 15); -1 when the shape is not theirs.
+int launch_rows_w(int which, const SpecArgs& a, cudaStream_t s) {
+  if (a.n2 != 1024 || a.blue2.N != kWN || a.q2 > 15 || !conv_sep_supported(a.q2)) return -1;
+  dim3 grid((a.n1 + 2 * kWWarps - 1) / (2 * kWWarps), a.batch);
+  if (which == 0) {
+    const size_t bytes = (size_t)kWWarps * kWLine * sizeof(double2);
+    static AttrOnce attr;
+    if (!attr.ensure(rows_tt_w, bytes)) return -1;
+    launch_k(rows_tt_w, grid, 32 * kWWarps, bytes, s, a);
+  } else {
+    const size_t bytes = (size_t)kWWarps * kRowLS * sizeof(double2);
+    static AttrOnce attr;
+    if (!attr.ensure(rows_t_axpy_w, bytes)) return -1;
+    launch_k(rows_t_axpy_w, grid, 32 * kWWarps, bytes, s, a);
+  }
+  return (int)grid.x;
+}
 }  // namespace dbx
