@@ -799,8 +799,9 @@ int launch_fused(int which, const SpecArgs& a, cudaStream_t s) {
   }
   // warp-owned separable row kernels (wdst.cu) for 1024-point rows;
   // DBX_WROWS=0 keeps the CTA lock-step ones (A/B and tests)
-  static const bool wrows_off = [] { const char* e = getenv("DBX_WROWS"); return e && e[0] == '0'; }();
-  if ((which == FUSED_TT_SEP || which == FUSED_T_AXPY_SEP) && !wrows_off) {
+  // (DBX_WROWS=2: rows_tt_w only, 3: rows_t_axpy_w only)
+  static const int wrows = [] { const char* e = getenv("DBX_WROWS"); return e ? atoi(e) : 1; }();
+  if ((which == FUSED_TT_SEP && (wrows == 1 || wrows == 2)) || (which == FUSED_T_AXPY_SEP && (wrows == 1 || wrows == 3))) {
     const int c = launch_rows_w(which == FUSED_TT_SEP ? 0 : 1, a, s);
     if (c >= 0) return c;
   }

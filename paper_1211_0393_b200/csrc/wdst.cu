@@ -659,42 +659,55 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_t_axpy_w(Spe
     // x_k = x_{k-1} + tau w, w = the T output with the ramp; all line reads
     // precede the x row writes into the same region
     double* xn = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + (size_t)r * n2;
-    double xa[32], xb[32];
+    double2 ov[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int k = lane + 32 * j;
-      const double2 o = buf[oslot(k)];
-      const double t1 = (double)k * ri;
-      double wa = o.x + a0a * (1.0 - t1) + a1a * t1;
-      double wb = o.y + a0b * (1.0 - t1) + a1b * t1;
-      if (k == 0) { wa = a0a; wb = a0b; }
-      if (k == n2 - 1) { wa = a1a; wb = a1b; }
-      xa[j] = __ldcs(xo + k) + tau * wa;
-      xn[k] = xa[j];
-      p0 += xa[j] * xa[j];
-      if (fimg) {
-        const double e = xa[j] - __ldcs(fimg + k);
-        p1 += e * e;
-      }
-      if (hb) {
-        xb[j] = __ldcs(xo + n2 + k) + tau * wb;
-        xn[n2 + k] = xb[j];
-        p0 += xb[j] * xb[j];
-        if (fimg) {
-          const double e = xb[j] - __ldcs(fimg + n2 + k);
-          p1 += e * e;
-        }
-      } else {
-        xb[j] = 0.0;
-      }
-    }
-    __syncwarp();
+    for (int j = 0; j < 32; ++j) ov[j] = buf[oslot(lane + 32 * j)];
+    __syncwarp();  // the x rows overwrite the line below
     double* ra = xs + (size_t)(2 * w) * kRowLS + 16;
     double* rb = ra + kRowLS;
+    // x_{k-1} / f loads eight columns deep per lane (the x_k stores would
+    // otherwise keep the compiler from hoisting them: one L2 round trip per
+    // group instead of per element)
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      ra[lane + 32 * j] = xa[j];
-      rb[lane + 32 * j] = xb[j];
+    for (int jc = 0; jc < 32; jc += 8) {
+      double oa[8], ob[8], fa[8], fb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = lane + 32 * (jc + u);
+        oa[u] = __ldcs(xo + k);
+        ob[u] = hb ? __ldcs(xo + n2 + k) : 0.0;
+        fa[u] = fimg ? __ldcs(fimg + k) : 0.0;
+        fb[u] = (fimg && hb) ? __ldcs(fimg + n2 + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = lane + 32 * (jc + u);
+        const double2 o = ov[jc + u];
+        const double t1 = (double)k * ri;
+        double wa = o.x + a0a * (1.0 - t1) + a1a * t1;
+        double wb = o.y + a0b * (1.0 - t1) + a1b * t1;
+        if (k == 0) { wa = a0a; wb = a0b; }
+        if (k == n2 - 1) { wa = a1a; wb = a1b; }
+        const double xa = oa[u] + tau * wa;
+        xn[k] = xa;
+        ra[k] = xa;
+        p0 += xa * xa;
+        if (fimg) {
+          const double e = xa - fa[u];
+          p1 += e * e;
+        }
+        double xb = 0.0;
+        if (hb) {
+          xb = ob[u] + tau * wb;
+          xn[n2 + k] = xb;
+          p0 += xb * xb;
+          if (fimg) {
+            const double e = xb - fb[u];
+            p1 += e * e;
+          }
+        }
+        rb[k] = xb;
+      }
     }
     __syncwarp();
     // AR extension of both rows (f_{-k} = 2 f_0 - f_k, f_{n-1+k} = 2 f_{n-1} - f_{n-1-k})
