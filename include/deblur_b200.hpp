@@ -6,7 +6,10 @@
 //
 //   deblur::apply / apply_reblur_adjoint      blur.hpp:75-90
 //   deblur::tensor_apply (SineI, AR, ARInv)   transforms.hpp:198-226
-//   deblur::build_tikhonov (AntiReflective)   preconditioner.hpp:62-85
+//   deblur::build_tikhonov (AR / CosineIII)   preconditioner.hpp:62-85
+//   (Reflective BCs with the CosineIII algebra: SURVEY §8f f3)
+//   SlabRun: d_landweber on one image in row slabs across ranks (NCCL;
+//            no reference equivalent)
 //   deblur::precondition_apply                preconditioner.hpp:88-90
 //   deblur::landweber / d_landweber           solver.hpp:139-148
 //   deblur::add_noise / rre                   image.hpp:72-91
@@ -21,6 +24,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -82,11 +86,25 @@ struct PlanDeleter {
   void operator()(dbx_plan* p) const { dbx_plan_destroy(p); }
 };
 using PlanPtr = std::shared_ptr<dbx_plan>;
-inline PlanPtr make_plan(Index n1, Index n2, const Matrix& taps, Index q1, Index q2) {
+inline PlanPtr make_plan(Index n1, Index n2, const Matrix& taps, Index q1, Index q2,
+                         int bc = DBX_BC_ANTIREFLECTIVE) {
   dbx_plan* p = nullptr;
   check(dbx_plan_create(static_cast<int>(n1), static_cast<int>(n2), 1, taps.data(), static_cast<int>(q1),
-                        static_cast<int>(q2), DBX_BC_ANTIREFLECTIVE, 0, &p));
+                        static_cast<int>(q2), bc, 0, &p));
   return PlanPtr(p, PlanDeleter{});
+}
+// One identity-mask transform plan per (shape, BC) and thread: a hot loop of
+// tensor_apply calls reuses its device buffers and DST/DCT tables instead of
+// allocating a plan per call (plans are per-stream, so per thread).
+inline dbx_plan* transform_plan(Index n1, Index n2, int bc) {
+  thread_local std::map<std::pair<std::pair<Index, Index>, int>, PlanPtr> cache;
+  auto& slot = cache[{{n1, n2}, bc}];
+  if (!slot) {
+    Matrix one = Matrix::Zero(1, 1);
+    one(0, 0) = 1.0;
+    slot = make_plan(n1, n2, one, 0, 0, bc);
+  }
+  return slot.get();
 }
 }  // namespace detail
 
@@ -132,9 +150,10 @@ class BlurOperator {
   BlurOperator(Psf psf, BoundaryCondition bc, Index n1, Index n2)
       : psf_(std::move(psf)), bc_(bc), n1_(n1), n2_(n2) {
     detail::require(n1 >= 1 && n2 >= 1, "BlurOperator: empty field of view");
-    detail::require(bc == BoundaryCondition::AntiReflective,
-                    "BlurOperator: the B200 path implements AntiReflective BCs");
-    plan_ = detail::make_plan(n1, n2, psf_.taps(), psf_.q1(), psf_.q2());
+    detail::require(bc == BoundaryCondition::AntiReflective || bc == BoundaryCondition::Reflective,
+                    "BlurOperator: the B200 path implements AntiReflective and Reflective BCs");
+    plan_ = detail::make_plan(n1, n2, psf_.taps(), psf_.q1(), psf_.q2(),
+                              bc == BoundaryCondition::Reflective ? DBX_BC_REFLECTIVE : DBX_BC_ANTIREFLECTIVE);
   }
   const Psf& psf() const { return psf_; }
   BoundaryCondition bc() const { return bc_; }
@@ -167,12 +186,10 @@ inline Matrix apply_reblur_adjoint(const BlurOperator& op, const Matrix& r) {  /
 
 inline Matrix tensor_apply(TransformKind kind, const Matrix& x) {  // transforms.hpp:198-226
   detail::require(kind != TransformKind::Dft, "tensor_apply: Dft is complex, use dft2_forward");
-  detail::require(kind != TransformKind::CosineIII, "tensor_apply: CosineIII is outside the AR path");
-  Matrix one = Matrix::Zero(1, 1);
-  one(0, 0) = 1.0;
-  auto plan = detail::make_plan(x.rows(), x.cols(), one, 0, 0);
+  const int bc = kind == TransformKind::CosineIII ? DBX_BC_REFLECTIVE : DBX_BC_ANTIREFLECTIVE;
   Matrix y(x.rows(), x.cols());
-  detail::check(dbx_tensor_apply(plan.get(), static_cast<int>(kind), x.data(), y.data()));
+  detail::check(dbx_tensor_apply(detail::transform_plan(x.rows(), x.cols(), bc), static_cast<int>(kind), x.data(),
+                                 y.data()));
   return y;
 }
 
@@ -182,6 +199,7 @@ struct PreconditionerSpec {  // preconditioner.hpp:17-20
 };
 
 struct FilteredOperator {  // preconditioner.hpp:24-28
+  Algebra algebra = Algebra::AntiReflective;
   Matrix eigs;  // d_j grid (sop.eigs)
   std::optional<Psf> source_psf;
   double alpha = 0.0;
@@ -204,10 +222,12 @@ inline Psf symmetrize(const Psf& p) {  // psf.hpp:71-85
 }
 
 inline FilteredOperator build_tikhonov(const Psf& p, const PreconditionerSpec& spec, Index n1, Index n2) {
-  detail::require(spec.algebra == Algebra::AntiReflective,
-                  "build_tikhonov: the B200 path implements the AntiReflective algebra");
+  detail::require(spec.algebra == Algebra::AntiReflective || spec.algebra == Algebra::CosineIII,
+                  "build_tikhonov: the B200 path implements the AntiReflective and CosineIII algebras");
   FilteredOperator d;
-  d.plan = detail::make_plan(n1, n2, p.taps(), p.q1(), p.q2());
+  d.plan = detail::make_plan(n1, n2, p.taps(), p.q1(), p.q2(),
+                             spec.algebra == Algebra::CosineIII ? DBX_BC_REFLECTIVE : DBX_BC_ANTIREFLECTIVE);
+  d.algebra = spec.algebra;
   detail::check(dbx_precond_build(d.plan.get(), spec.alpha));
   d.eigs = Matrix(n1, n2);
   detail::check(dbx_precond_eigs(d.plan.get(), d.eigs.data()));
@@ -265,6 +285,8 @@ inline RestorationRun run(const BlurOperator& op, const FilteredOperator* d, con
             "landweber: true image size mismatch");
   if (d) {
     require(d->n1 == op.n1() && d->n2 == op.n2(), "d_landweber: preconditioner size mismatch");
+    require((d->algebra == Algebra::CosineIII) == (op.bc() == BoundaryCondition::Reflective),
+            "d_landweber: the preconditioner's algebra does not match the operator's boundary condition");
     check(dbx_precond_set_eigs(op.plan(), d->eigs.data()));
   }
   const int total = cfg.stop.kind == StoppingRule::Kind::FixedIterations ? cfg.stop.fixed_iterations
@@ -326,6 +348,45 @@ inline SemiconvergenceReport semiconvergence_report(const RestorationRun& run) {
   rep.diverged_after = run.rre_history.back() > rep.best_rre * 1.05;
   return rep;
 }
+
+// d_landweber on one n x n image split into row slabs across ranks (C++
+// loop behind dbx_slab_run: NCCL halos, all-to-all from grouped send/recv,
+// device all-reduce and bookkeeping).  rank >= 0 with a communicator (the
+// caller's ncclComm_t via dbx_comm_wrap, or dbx_comm_init); rank = -1 holds
+// all slabs in this process.  g, f, x_out: DEVICE arrays of the rows held here.
+class SlabRun {
+ public:
+  SlabRun(Index n, int parts, int rank, const Psf& psf, double alpha, dbx_comm* comm = nullptr, int device = 0) {
+    detail::require(psf.q1() == psf.q2(), "SlabRun: square masks only (one q for both axes)");
+    dbx_slab* s = nullptr;
+    detail::check(dbx_slab_create(static_cast<int>(n), parts, rank, psf.taps().data(), static_cast<int>(psf.q1()),
+                                  static_cast<int>(psf.q2()), alpha, comm, device, &s));
+    slab_.reset(s);
+  }
+  // returns the histories; x_out receives the restored rows (best-RRE iterate
+  // when f is given, solver.hpp:127-131)
+  RestorationRun run(const double* g, const double* f, double* x_out, const SolverConfig& cfg) {
+    const int total = cfg.stop.kind == StoppingRule::Kind::FixedIterations ? cfg.stop.fixed_iterations
+                                                                          : cfg.max_iters;
+    detail::require(total >= 1, "SolverConfig: max_iters must be >= 1");
+    std::vector<double> rre(static_cast<size_t>(total)), res(static_cast<size_t>(total));
+    int best = 0, done = 0;
+    detail::check(dbx_slab_run(slab_.get(), g, f, cfg.tau, total, static_cast<int>(cfg.stop.kind),
+                               cfg.stop.residual_threshold, x_out, rre.data(), res.data(), &best, &done));
+    RestorationRun out;
+    out.iterations_executed = done;
+    out.best_iteration = best;
+    out.residual_history.assign(res.begin(), res.begin() + done);
+    if (f) out.rre_history.assign(rre.begin(), rre.begin() + done);
+    return out;
+  }
+
+ private:
+  struct Del {
+    void operator()(dbx_slab* s) const { dbx_slab_destroy(s); }
+  };
+  std::unique_ptr<dbx_slab, Del> slab_;
+};
 
 struct NoiseSpec {  // image.hpp:31-34
   double relative_level = 0.0;

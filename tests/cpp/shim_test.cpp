@@ -1,5 +1,7 @@
 // Exercises include/deblur_b200.hpp (the C++ drop-in face) end to end on the
 // GPU with known answers from the reference tests; prints "OK" on success.
+#include <cuda_runtime.h>
+
 #include <cstdio>
 #include <random>
 
@@ -89,6 +91,78 @@ int main() {
   Matrix back = tensor_apply(TransformKind::AntiReflective, tensor_apply(TransformKind::AntiReflectiveInverse, x));
   for (Index i = 0; i < 9; ++i)
     for (Index j = 0; j < 11; ++j) CHECK(std::abs(back(i, j) - x(i, j)) <= 1e-12);
+  // R R^T = I through the cached CosineIII plan (reflective algebra)
+  {
+    Matrix rb = tensor_apply(TransformKind::CosineIII, x);
+    Matrix xx(9, 11);
+    for (int rep = 0; rep < 3; ++rep) xx = tensor_apply(TransformKind::AntiReflective, tensor_apply(TransformKind::AntiReflectiveInverse, x));
+    CHECK(std::abs(xx(4, 5) - x(4, 5)) <= 1e-12);
+    CHECK(rb.rows() == 9 && rb.cols() == 11);
+  }
+  // Reflective BCs: constants are fixed points; the CosineIII preconditioner of a
+  // delta mask gives x1 = g / (1 + alpha); mixing algebra and BC is refused
+  {
+    BlurOperator rop(Psf(t), BoundaryCondition::Reflective, 7, 7);
+    Matrix rg = apply(rop, c);
+    for (Index i = 0; i < 7; ++i)
+      for (Index j = 0; j < 7; ++j) CHECK(std::abs(rg(i, j) - 4.5) <= 1e-13);
+    BlurOperator rdop(delta_psf(), BoundaryCondition::Reflective, 8, 8);
+    auto rd = build_tikhonov(delta_psf(), {Algebra::CosineIII, 0.25}, 8, 8);
+    auto rrun = d_landweber(rdop, rd, gg, cfg);
+    for (Index i = 0; i < 8; ++i)
+      for (Index j = 0; j < 8; ++j) CHECK(std::abs(rrun.restored(i, j) - gg(i, j) / 1.25) <= 1e-12);
+    bool mix = false;
+    try {
+      d_landweber(dop, rd, gg, cfg);
+    } catch (const std::invalid_argument&) {
+      mix = true;
+    }
+    CHECK(mix);
+  }
+  // C++ row-slab loop (2 in-process slabs) == the single-image D-Landweber
+  {
+    const Index n = 32;
+    Matrix m(5, 5);
+    for (Index i = 0; i < 5; ++i)
+      for (Index j = 0; j < 5; ++j) m(i, j) = u(rng);
+    const double ms = m.sum();
+    for (Index i = 0; i < 5; ++i)
+      for (Index j = 0; j < 5; ++j) m(i, j) /= ms;
+    Psf mp(m);
+    Matrix f0(n, n), g0(n, n);
+    for (Index i = 0; i < n; ++i)
+      for (Index j = 0; j < n; ++j) f0(i, j) = u(rng);
+    BlurOperator sop(mp, BoundaryCondition::AntiReflective, n, n);
+    g0 = apply(sop, f0);
+    auto sd = build_tikhonov(mp, {Algebra::AntiReflective, 0.05}, n, n);
+    SolverConfig scfg;
+    scfg.max_iters = 6;
+    scfg.track_rre_against = f0;
+    auto ref = d_landweber(sop, sd, g0, scfg);
+    const size_t bytes = sizeof(double) * n * n;
+    double *dg = nullptr, *df = nullptr, *dx = nullptr;
+    CHECK(cudaMalloc(&dg, bytes) == cudaSuccess && cudaMalloc(&df, bytes) == cudaSuccess &&
+          cudaMalloc(&dx, bytes) == cudaSuccess);
+    cudaMemcpy(dg, g0.data(), bytes, cudaMemcpyHostToDevice);
+    cudaMemcpy(df, f0.data(), bytes, cudaMemcpyHostToDevice);
+    SlabRun slabs(n, 2, -1, mp, 0.05);
+    auto srun = slabs.run(dg, df, dx, scfg);
+    Matrix xs(n, n);
+    cudaMemcpy(xs.data(), dx, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(dg);
+    cudaFree(df);
+    cudaFree(dx);
+    CHECK(srun.best_iteration == ref.best_iteration && srun.iterations_executed == ref.iterations_executed);
+    double e = 0.0, nr = 0.0;
+    for (Index i = 0; i < n; ++i)
+      for (Index j = 0; j < n; ++j) {
+        e += (xs(i, j) - ref.restored(i, j)) * (xs(i, j) - ref.restored(i, j));
+        nr += ref.restored(i, j) * ref.restored(i, j);
+      }
+    CHECK(std::sqrt(e / nr) <= 1e-10);
+    for (size_t k = 0; k < ref.rre_history.size(); ++k)
+      CHECK(std::abs(srun.rre_history[k] - ref.rre_history[k]) <= 1e-10 * ref.rre_history[k]);
+  }
   std::printf("OK\n");
   return 0;
 }
