@@ -52,6 +52,10 @@ constexpr int kWWarps = 4;    // warps (column pairs) per CTA
 #endif
 // L2 prefetch (cp.async.bulk.prefetch.L2) of the input lines of the CTA this
 // many resident waves ahead (0 = off)
+#ifndef DBX_WDST_CTA_STORE
+#define DBX_WDST_CTA_STORE 1
+#endif
+constexpr bool kWdstCtaStore = DBX_WDST_CTA_STORE != 0;
 #ifndef DBX_WDST_PREFETCH
 #define DBX_WDST_PREFETCH 0
 #endif
@@ -405,6 +409,10 @@ __device__ __forceinline__ void wsplit(double2* buf, int lane, double hs, double
 #define WDFT wdft1023
 #endif
 
+// CTA_STORE (n2 a multiple of 2 kWWarps): after one CTA barrier the 4 warps'
+// outputs leave as 64-byte row segments (8 columns) instead of each warp's
+// 16-byte pieces at 32 different rows per store instruction.
+template <bool CTA_STORE>
 __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecArgs a) {
   DBX_PDL_WAIT();
   const int b = blockIdx.y;
@@ -500,6 +508,29 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
   wsplit(buf, lane, hs, sc);
   // ---- T (ar_forward, transforms.hpp:148-160): w_0 = a0, w_{n-1} = a1,
   // interior DST + ramp a0 (1 - k/(n-1)) + a1 k/(n-1); row-major stores
+  if constexpr (CTA_STORE) {
+    __shared__ double2 ramp[kWWarps][2];
+    if (lane == 0) {
+      ramp[w][0] = make_double2(a0a, a0b);
+      ramp[w][1] = make_double2(a1a, a1b);
+    }
+    __syncthreads();
+    double* outb = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) +
+                   2 * kWWarps * blockIdx.x;
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < kWWarps * n; idx += 32 * kWWarps) {
+      const int ww = idx & (kWWarps - 1), k = idx / kWWarps;
+      const double2 o = wsm[(size_t)ww * kWLine + oslot(k)];
+      const double2 r0v = ramp[ww][0], r1v = ramp[ww][1];
+      const double t1 = (double)k * ri;
+      double wa = o.x + r0v.x * (1.0 - t1) + r1v.x * t1;
+      double wb = o.y + r0v.y * (1.0 - t1) + r1v.y * t1;
+      if (k == 0) { wa = r0v.x; wb = r0v.y; }
+      if (k == n - 1) { wa = r1v.x; wb = r1v.y; }
+      *reinterpret_cast<double2*>(outb + (size_t)k * n2 + 2 * ww) = make_double2(wa, wb);
+    }
+    return;
+  }
   double* out = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c;
 #pragma unroll 8
   for (int j = 0; j < 32; ++j) {
@@ -745,10 +776,16 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_t_axpy_w(Spe
 int launch_dst_tcols_w(const SpecArgs& a, cudaStream_t s) {
   if (a.n1 != 1024 || a.blue1.N != kWN) return -1;
   const size_t bytes = (size_t)kWWarps * kWLine * sizeof(double2);
-  static AttrOnce attr;
-  if (!attr.ensure(dst_tcols_w, bytes)) return -1;
   dim3 grid((a.n2 + 2 * kWWarps - 1) / (2 * kWWarps), a.batch);
-  launch_k(dst_tcols_w, grid, 32 * kWWarps, bytes, s, a);
+  if (a.n2 % (2 * kWWarps) == 0 && kWdstCtaStore) {
+    static AttrOnce attr;
+    if (!attr.ensure(dst_tcols_w<true>, bytes)) return -1;
+    launch_k(dst_tcols_w<true>, grid, 32 * kWWarps, bytes, s, a);
+  } else {
+    static AttrOnce attr;
+    if (!attr.ensure(dst_tcols_w<false>, bytes)) return -1;
+    launch_k(dst_tcols_w<false>, grid, 32 * kWWarps, bytes, s, a);
+  }
   return (int)grid.x;
 }
 
