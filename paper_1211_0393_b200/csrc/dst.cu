@@ -56,7 +56,20 @@ struct DstCfg {
   static constexpr size_t bytes = base + (TW ? (size_t)TWN * 16 : 0);
   static constexpr int NMAX = CORE == CORE_BLUE ? M / 2 + 1 : M + 1;  // N <= NMAX
   static constexpr int PS = ((NMAX - 1) / 2 + 1 + T - 1) / T;         // split items per thread
+  // resident CTAs per SM the register budget is sized for, only when asked
+  // (-DDBX_DST_MINB4096=3: the Bluestein 4096 lines of C4 at 80 registers —
+  // 1.2 KB of spills, not kept).  An explicit minimum of 1 is NOT neutral: it
+  // lets ptxas take 156 registers for dst_rows<4096> (one CTA per SM, C4
+  // 21.8 -> 27.3 ms per run), so the default is the one-argument form.
+#ifdef DBX_DST_MINB4096
+  static constexpr int MINB = (M == 4096 && CORE == CORE_BLUE) ? DBX_DST_MINB4096 : 1;
+#endif
 };
+#ifdef DBX_DST_MINB4096
+#define DBX_DST_BOUNDS __launch_bounds__(DstCfg<M, CORE>::NT, DstCfg<M, CORE>::MINB)
+#else
+#define DBX_DST_BOUNDS __launch_bounds__(DstCfg<M, CORE>::NT)
+#endif
 
 // buffer position of z_j and the DFT output Z_l for each core
 template <int M, int CORE>
@@ -290,7 +303,7 @@ __device__ __forceinline__ double kind_out(int kind, const double* o, int k, int
 // Row pass: 2G rows per CTA (line g carries rows 2g, 2g+1), fused epilogue
 // (store / Hadamard / r = g - v with ||r||^2 / x += tau v with norms).
 template <int M, int CORE>
-__global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_rows(SpecArgs a) {
+__global__ void DBX_DST_BOUNDS dst_rows(SpecArgs a) {
   DBX_PDL_WAIT();
   using C = DstCfg<M, CORE>;
   constexpr int T = C::T, G = C::G, NT = C::NT;
@@ -383,7 +396,7 @@ __global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_rows(SpecArgs a) {
 // side, launch_dst_cols): T~ with the Hadamard by d into the output array, then
 // T in place on it.
 template <int M, int CORE>
-__global__ void __launch_bounds__(DstCfg<M, CORE>::NT) dst_cols(SpecArgs a) {
+__global__ void DBX_DST_BOUNDS dst_cols(SpecArgs a) {
   DBX_PDL_WAIT();
   using C = DstCfg<M, CORE>;
   constexpr int T = C::T, G = C::G, NT = C::NT;

@@ -257,12 +257,21 @@ __device__ __forceinline__ void blue_core(double2* sm, double2* buf, const BlueT
     return;
   }
   const int bar = G > 1 ? 1 + (int)threadIdx.x / T : 0;  // per-line named barrier
+#ifndef DBX_FUSED_STOCKHAM_BLUE
+  // in-place Cooley-Tukey convolution core (fft.cuh ct_convolve, the Rader
+  // core of dst.cu): C2's 1024-point Bluestein lines 3763 -> 4052 Mpx-it/s
+  // (profiles/r02_fused_ct_ab.txt); -DDBX_FUSED_STOCKHAM_BLUE restores the two
+  // Stockham FFTs.  Needs the CT twiddle prefix inside the staged Stockham one.
+  static_assert(fft::ct_twiddles_needed(M) <= fft::twiddles_needed(M), "CT twiddle prefix");
+  fft::ct_convolve<M, T>(buf, tw, bt.bct, t, bar, nullptr);
+#else
   fft::fft<M, -1, T>(buf, tw, t, bar);
   if constexpr (BLUE) {
     for (int j = t; j < M; j += T) buf[pad<M>(j)] = cmul(buf[pad<M>(j)], __ldg(bt.bhat + j));
     fft::line_sync(bar, T);
     fft::fft<M, +1, T>(buf, tw, t, bar);
   }
+#endif
   __syncthreads();  // the split reads other lines' data only after every line finished
 }
 
