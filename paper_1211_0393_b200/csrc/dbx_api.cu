@@ -275,6 +275,7 @@ struct dbx_plan {
   bool sep_ok = false;
   double sep_resid = 1.0;
   DevBuf zb, yb, dT;  // dT: filter grid transposed (fused column pass)
+  DevBuf fincnt;      // per-image arrival counters of the last-block finalize (fused pipelines)
   DevBuf cg_p, cg_q, cg_s, cg_z, cg_zero, cg_part, cg_sc;  // CGLS state (dbx_cgls_run)
   struct Blue {
     bool ready = false;
@@ -293,7 +294,7 @@ struct dbx_plan {
       if (p) cudaFree(p);
     for (double* p : owned) cudaFree(p);
     if (st) cudaFree(st);
-    for (DevBuf* b : {&g, &f, &r, &s, &u, &X3, &in, &out, &part, &rre, &res, &xh, &zb, &yb, &dT, &cg_p, &cg_q,
+    for (DevBuf* b : {&g, &f, &r, &s, &u, &X3, &in, &out, &part, &rre, &res, &xh, &zb, &yb, &dT, &fincnt, &cg_p, &cg_q,
                       &cg_s, &cg_z, &cg_zero, &cg_part, &cg_sc})
       b->release();
     if (stream) cudaStreamDestroy(stream);
@@ -1518,6 +1519,8 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
     Partials pt{P->part.p, P->part_cap};
 
     launch_state_init(P->st, B, s);
+    P->fincnt.ensure((size_t)B);
+    ck(cudaMemsetAsync(P->fincnt.p, 0, (size_t)B * sizeof(unsigned), s), "memset");
     launch_norms_init(gd, fd, B, N, P->st, pt, s);
     P->launches += 3;
     // x_0 = 0 in buffer 0, r_0 = g
@@ -1609,7 +1612,26 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
       lc(launch_conv_row_fwd(a, s), "launch_conv_row_fwd");
       P->ev_end();
     };
-    auto enqueue_fused_sep = [&]() {
+    // DBX_FIN_FUSED=1: the fused pipelines run the iteration's finalize as the
+    // last-block tail of their residual kernel (finalize.cuh; one launch fewer
+    // per iteration).  Measured slower on every config (C1 1595 vs 1623, C2
+    // 3982 vs 4018, C3 25430 vs 25545 Mpx-it/s, profiles/r02_fin_fused_ab.txt):
+    // the fence + atomic + one CTA's serial tail cost more than a graph
+    // kernel boundary.  Off by default; parity-tested on.
+    static const bool fin_fused = [] { const char* e = getenv("DBX_FIN_FUSED"); return e && e[0] == '1'; }();
+    auto make_fa = [&](int k, int cnt_x, int cnt_r) {
+      FinalizeArgs fa{};
+      fa.st = P->st; fa.part = pt; fa.cnt_x = cnt_x; fa.cnt_r = cnt_r; fa.k = k;
+      fa.hist_len = H; fa.rre_hist = P->rre.p; fa.res_hist = P->res.p;
+      fa.track = track ? 1 : 0; fa.stop_kind = stop_kind; fa.resid_eps = resid_eps; fa.batch = B;
+      return fa;
+    };
+    auto set_fin = [&](SpecArgs& a, int k, int cnt_x) {
+      if (!fin_fused) return;
+      a.fin = make_fa(k, cnt_x, -1);
+      a.fin_cnt = reinterpret_cast<unsigned*>(P->fincnt.p);
+    };
+    auto enqueue_fused_sep = [&](int k) {
       SpecArgs a = fa0;
       double* Yr = reinterpret_cast<double*>(P->yb.p);
       // K1: column pass of A' (real): Z'^T -> Y' = A' r (row-major)
@@ -1633,13 +1655,14 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
       // K6: r = g - A x_k + ||r||^2 -> row pass of A' r -> Z'^T
       P->set_kernel(a.conv, true);
       a.in = Yr; a.insel = SEL_EXPLICIT;
+      set_fin(a, k, cnt_x);
       P->ev_begin(KC_BLUR);
       const int cnt_r = lc(launch_fused(FUSED_RESID_SEP, a, s), "rows_resid_sep");
       P->ev_end();
       return std::make_pair(cnt_x, cnt_r);
     };
     auto enqueue_fused = [&](int k) {
-      if (sepd) return enqueue_fused_sep();
+      if (sepd) return enqueue_fused_sep(k);
       SpecArgs a = fa0;
       // K1: column pass of A' (spectral AR extension, kernel spectrum of the rotated mask)
       P->set_kernel(a.conv, true);
@@ -1660,6 +1683,7 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
       P->set_kernel(a.conv, false);
       P->ev_begin(KC_BLUR); lc(launch_conv_col(a, s), "launch_conv_col"); P->ev_end();
       // K6: inverse row FFT -> r_k = g - A x_k + ||r||^2 -> forward row FFT for the next A'
+      set_fin(a, k, cnt_x);
       P->ev_begin(KC_BLUR);
       const int cnt_r = lc(launch_fused(FUSED_AINV_RESID, a, s), "rows_ainv_resid");
       P->ev_end();
@@ -1670,13 +1694,12 @@ static int run_impl(dbx_plan* P, const double* g, const double* f_true, double t
       int cnt_x = 0;
       if (fused) {
         const auto cr = enqueue_fused(k);
-        FinalizeArgs fa{};
-        fa.st = P->st; fa.part = pt; fa.cnt_x = cr.first; fa.cnt_r = cr.second; fa.k = k;
-        fa.hist_len = H; fa.rre_hist = P->rre.p; fa.res_hist = P->res.p;
-        fa.track = track ? 1 : 0; fa.stop_kind = stop_kind; fa.resid_eps = resid_eps; fa.batch = B;
-        P->ev_begin(KC_FINALIZE);
-        launch_finalize(fa, s);
-        P->ev_end();
+        if (!fin_fused) {
+          const FinalizeArgs fa = make_fa(k, cr.first, cr.second);
+          P->ev_begin(KC_FINALIZE);
+          launch_finalize(fa, s);
+          P->ev_end();
+        }
         P->check_launch();
         if (want_xh) {
           launch_select_copy(P->X3.p, P->st, 0, B, N, P->xh.p + (size_t)(k - 1) * cnt, s);

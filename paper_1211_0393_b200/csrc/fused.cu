@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include "spectral_common.cuh"
+#include "finalize.cuh"
 
 namespace dbx {
 
@@ -477,6 +478,7 @@ __global__ void __launch_bounds__(RsCfg<L2>::NT, 2) rows_ainv_resid(SpecArgs a) 
     const double s0 = block_sum<NT>(p0, red);
     if (threadIdx.x == 0) P[SLOT_R2 * a.part.cap + blockIdx.x] = s0;
   }
+  if (a.fin_cnt) finalize_last_block(a.fin, a.fin_cnt, b);
 }
 
 // ---------------------------------------------------------------------------
@@ -570,6 +572,7 @@ __global__ void __launch_bounds__(kResidNT, 4) rows_resid_sep(SpecArgs a) {
     const double s0 = block_sum<kResidNT>(p0, red);
     if (threadIdx.x == 0) P[SLOT_R2 * a.part.cap + blockIdx.x] = s0;
   }
+  if (a.fin_cnt) finalize_last_block(a.fin, a.fin_cnt, b);
 }
 
 // ---------------------------------------------------------------------------

@@ -11,6 +11,7 @@
 #include <math.h>
 
 #include "dbx_internal.h"
+#include "finalize.cuh"
 
 namespace dbx {
 
@@ -140,83 +141,10 @@ __device__ double partial_sum(const double* p, int cnt) {
   return block_reduce(s);
 }
 
-// The three fixed-order block sums of finalize in one pass: the same per-thread
-// strided order and the same shuffle tree as partial_sum / block_reduce (the
-// results are bit-identical), with all three slots' loads in flight together
-// and one barrier pair instead of three.
-__device__ void block_reduce3(double& a, double& b, double& c) {
-  __shared__ double red3[3][32];
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-    c += __shfl_xor_sync(0xffffffffu, c, o);
-  }
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) {
-    red3[0][w] = a;
-    red3[1][w] = b;
-    red3[2][w] = c;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double sa = 0.0, sb = 0.0, sc = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
-      sa += red3[0][i];
-      sb += red3[1][i];
-      sc += red3[2][i];
-    }
-    a = sa;
-    b = sb;
-    c = sc;
-  }
-}
-
-// One CTA per image: reduce the fused-epilogue partials of iteration k and
-// apply the reference loop bookkeeping (solver.hpp:107-124).
+// One CTA per image: finalize.cuh finalize_image.
 __global__ void finalize_kernel(FinalizeArgs a) {
   DBX_PDL_WAIT();
-  const int b = blockIdx.x;
-  ImgState* st = a.st + b;
-  const ImgState s0 = *st;  // in flight with the partial loads
-  if (s0.done) return;
-  const double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
-  double x2 = 0.0, xf2 = 0.0, r2 = 0.0;
-  for (int i = threadIdx.x; i < a.cnt_x; i += blockDim.x) x2 += P[SLOT_X2 * a.part.cap + i];
-  if (a.track)
-    for (int i = threadIdx.x; i < a.cnt_x; i += blockDim.x) xf2 += P[SLOT_XF2 * a.part.cap + i];
-  for (int i = threadIdx.x; i < a.cnt_r; i += blockDim.x) r2 += P[SLOT_R2 * a.part.cap + i];
-  block_reduce3(x2, xf2, r2);
-  if (threadIdx.x != 0) return;
-  ImgState s = s0;
-  const int k = a.k;
-  const double xn = sqrt(x2);
-  // divergence guard before recording (solver.hpp:107-108)
-  if (xn > 1e8 * s.g_norm && s.g_norm > 0.0) {
-    s.done = 2;
-    s.diverged_at = k;
-    s.cur = s.nxt;
-    *st = s;
-    return;
-  }
-  const double rn = sqrt(r2);
-  if (a.res_hist) a.res_hist[(size_t)b * a.hist_len + (k - 1)] = rn;
-  if (a.track) {
-    const double e = sqrt(xf2) / s.f_norm;
-    if (a.rre_hist) a.rre_hist[(size_t)b * a.hist_len + (k - 1)] = e;
-    if (e < s.best_rre) {  // strict '<': first minimum wins (solver.hpp:114)
-      s.best_rre = e;
-      s.best_iter = k;
-      s.best = s.nxt;
-    }
-  }
-  s.iters = k;
-  // rotate buffers: x_k becomes current; next target avoids cur and best
-  s.cur = s.nxt;
-  int n = 0;
-  while (n == s.cur || n == s.best) ++n;
-  s.nxt = n;
-  if (a.stop_kind == 2 && s.g_norm > 0.0 && rn / s.g_norm < a.resid_eps) s.done = 1;
-  *st = s;
+  finalize_image(a, blockIdx.x);
 }
 
 __global__ void select_copy_kernel(const double* X3, const ImgState* st, int which_best,

@@ -84,6 +84,11 @@ struct SpecArgs {
   // DST
   int kind1 = DBX_KIND_ARINV, kind2 = -1;
   int pf = 0;                                    // dst_rows: prefetch the rows of CTA blockIdx.x + pf into L2 (0: off)
+  // residual kernels of the fused pipelines: when fin_cnt is set, the last
+  // CTA of each image runs the iteration's finalize (finalize.cuh) — one
+  // launch fewer per iteration
+  FinalizeArgs fin{};
+  unsigned* fin_cnt = nullptr;
   BlueTables blue1;                              // columns (length n1)
   BlueTables blue2;                              // rows (length n2)
 };
