@@ -338,8 +338,11 @@ struct dbx_plan {
   // factors <= 31), Bluestein (compiled power of two M >= 2N-1), Rader (N
   // prime, N-1 compiled; e.g. 8191 for C5).  DBX_DST_RADER forces Rader.
   int dst_core(int N, int* M) const {
+    // DBX_DST_PFA=0: Bluestein instead of the prime-factor core (A/B, tests)
+    static const bool pfa_off = [] { const char* e = getenv("DBX_DST_PFA"); return e && e[0] == '0'; }();
     if (dst != DBX_DST_RADER) {
       if (direct_supported_len(N)) { *M = N; return CORE_DIRECT; }
+      if (!pfa_off && pfa_supported_len(N)) { *M = N; return CORE_PFA; }
       const int Mb = blue_supported_len(2 * N - 1 < 16 ? 16 : 2 * N - 1);
       if (Mb) { *M = Mb; return CORE_BLUE; }
     }
@@ -457,14 +460,17 @@ struct dbx_plan {
       int M = 0;
       const int core = dst_core(N, &M);
       require(core >= 0, "no FFT-form DST for this line length");
-      const BlueHost h = core == CORE_RADER ? rader(n, sine) : bluestein(n, sine, M);
+      int pn1 = 0, pn2 = 0;
+      if (core == CORE_PFA) pfa_factors(N, &pn1, &pn2);
+      const BlueHost h = core == CORE_RADER ? rader(n, sine)
+                         : core == CORE_PFA ? pfa(n, sine, pn1, pn2) : bluestein(n, sine, M);
       B.tw = upload_owned(h.tw);
       B.chirp = upload_owned(h.chirp);
       B.bhat = upload_owned(h.bhat);
       B.p = upload_owned(h.p);
       B.sn = upload_owned(h.sn);
       B.t.sn = B.sn;
-      if (core == CORE_RADER) {
+      if (core == CORE_RADER || core == CORE_PFA) {
         B.t.dlog = upload_owned_int(h.dlog);
         B.t.ridx = upload_owned_int(h.ridx);
       }

@@ -38,10 +38,21 @@ constexpr bool kDstCtBlue = true;
 constexpr bool kDstCtBlue = false;
 #endif
 
+// Prime-factor geometry (CORE_PFA): N1 = the largest compiled odd radix of
+// M, N2 = M / N1 prime, R = N2 - 1 the Rader convolution length.
+template <int M>
+struct Pfa {
+  static constexpr int N1 = fft::next_radix(M);
+  static constexpr int N2 = N1 ? M / N1 : 1;
+  static constexpr int R = N2 - 1;
+};
+
 template <int M, int CORE>
 struct DstCfg {
-  static constexpr int T = line_threads(M, dst_per(M));
-  static constexpr int G = lines_for(M, kDstBudget, dst_per(M));  // FFT lines per CTA
+  // PFA lines: one line per CTA, 256 threads (23 x 11 = 253 butterflies of
+  // the widest column level)
+  static constexpr int T = CORE == CORE_PFA ? 256 : line_threads(M, dst_per(M));
+  static constexpr int G = CORE == CORE_PFA ? 1 : lines_for(M, kDstBudget, dst_per(M));  // FFT lines per CTA
   static constexpr int NT = T * G;
   static constexpr int LINE = padded_len(M);                      // double2 per FFT line
   static constexpr int LO = LINE;                                 // output line stride (doubles)
@@ -50,7 +61,8 @@ struct DstCfg {
   // Stockham FFTs (C4 4096 = 8^4: 13.7 vs 15.4 ms with CT).  -DDBX_DST_STOCKHAM
   // forces Stockham, -DDBX_DST_CT_BLUE forces CT for Bluestein too (A/B).
   static constexpr bool CT = (CORE == CORE_RADER || (CORE == CORE_BLUE && kDstCtBlue)) && kDstCt;
-  static constexpr int TWN = CT ? fft::ct_twiddles_needed(M) : fft::twiddles_needed(M);
+  static constexpr int TWN = CORE == CORE_PFA ? fft::ct_twiddles_needed(Pfa<M>::R)
+                             : CT ? fft::ct_twiddles_needed(M) : fft::twiddles_needed(M);
   static constexpr size_t base = (size_t)G * LINE * 16;
   static constexpr bool TW = base + (size_t)TWN * 16 <= kSmemCap;
   static constexpr size_t bytes = base + (TW ? (size_t)TWN * 16 : 0);
@@ -73,8 +85,16 @@ struct DstCfg {
 
 // buffer position of z_j and the DFT output Z_l for each core
 template <int M, int CORE>
-__device__ __forceinline__ double2 pkc_get(const double2* buf, const BlueTables& bt, int l, double2 A0) {
-  if constexpr (CORE == CORE_RADER) {
+__device__ __forceinline__ double2 pkc_get(const double2* buf, const BlueTables& bt, int l, double2 A0,
+                                           const double2* u0 = nullptr) {
+  if constexpr (CORE == CORE_PFA) {
+    // X_l = U_{k1}[k2], k1 = l mod N1, k2 = l mod N2: row 0 holds k2 = 0, row
+    // 1 + q holds k2 = g^-q without the column's u0 (added here)
+    using P = Pfa<M>;
+    const int k1 = l % P::N1, k2 = l % P::N2;
+    if (k2 == 0) return buf[k1];
+    return cadd(buf[(1 + __ldg(bt.ridx + k2)) * P::N1 + k1], u0[k1]);
+  } else if constexpr (CORE == CORE_RADER) {
     if (l == 0) return A0;
     return buf[pad<M>(__ldg(bt.ridx + l))];
   } else if constexpr (CORE == CORE_BLUE) {
@@ -88,8 +108,10 @@ __device__ __forceinline__ double2 pkc_get(const double2* buf, const BlueTables&
 // sd(h, j) = (x^h_j + x^h_{N-j}, x^h_j - x^h_{N-j}), j in [1, N/2].
 template <int M, int CORE>
 __device__ __forceinline__ void pkc_put(double2* buf, const BlueTables& bt, int j, double2 z) {
-  if constexpr (CORE == CORE_RADER) {
-    buf[pad<M>(__ldg(bt.dlog + j))] = z;  // a_p = z_{g^p}: dlog is a bijection onto [0, M)
+  if constexpr (CORE == CORE_RADER || CORE == CORE_PFA) {
+    // Rader: a_p = z_{g^p}; PFA: the Good-Thomas input map into the row
+    // layout (dlog is a bijection onto the line's slots)
+    buf[pad<M>(__ldg(bt.dlog + j))] = z;
   } else if constexpr (CORE == CORE_BLUE) {
     buf[pad<M>(j)] = cmul(z, __ldg(bt.chirp + j));
   } else {
@@ -169,13 +191,103 @@ __device__ __forceinline__ void pkc_refill(double2* buf, const BlueTables& bt, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Prime-factor core: P = N1 independent length-R cyclic convolutions (the
+// Rader sequences of the N1 columns, rows 1..R at stride N1) on the in-place
+// Cooley-Tukey core of fft.cuh, threads mapped column-fastest (consecutive
+// lanes hit consecutive slots).
+template <int L, int Ls, int P, int T, int DIR>
+__device__ __forceinline__ void ctm_level(double2* buf, const double2* __restrict__ tw, int t) {
+  constexpr int R = fft::ct_radix(Ls), m = Ls / R, NB = L / R;
+#pragma unroll 1
+  for (int beta = t; beta < P * NB; beta += T) {
+    const int bb = beta / P, prob = beta - bb * P;
+    const int blk = bb / m, j = bb - blk * m;
+    const int base = blk * Ls + j;
+    const double2 w1 = tw[j * (L / Ls)];
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = buf[(1 + base + r * m) * P + prob];
+    if constexpr (DIR < 0) {
+      fft::dft<R, -1>(v);
+      fft::apply_twiddles<R, -1>(v, w1);
+    } else {
+      fft::apply_twiddles<R, +1>(v, w1);
+      fft::dft<R, +1>(v);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[(1 + base + r * m) * P + prob] = v[r];
+  }
+  __syncthreads();
+}
+template <int L, int Ls, int P, int T>
+__device__ __forceinline__ void ctm_dif(double2* buf, const double2* __restrict__ tw, int t) {
+  if constexpr (Ls / fft::ct_radix(Ls) > 1) {
+    ctm_level<L, Ls, P, T, -1>(buf, tw, t);
+    ctm_dif<L, Ls / fft::ct_radix(Ls), P, T>(buf, tw, t);
+  }
+}
+template <int L, int Ls, int P, int T>
+__device__ __forceinline__ void ctm_dit(double2* buf, const double2* __restrict__ tw, int t) {
+  if constexpr (Ls / fft::ct_radix(Ls) > 1) {
+    ctm_dit<L, Ls / fft::ct_radix(Ls), P, T>(buf, tw, t);
+    ctm_level<L, Ls, P, T, +1>(buf, tw, t);
+  }
+}
+
+// The N-point DFT of one PFA line: row DFTs (N2 rows of N1, in registers,
+// outputs stored as formed), then the N1 column DFTs of length N2: U[0] =
+// u0 + sum(a) into row 0, U[g^-q] - u0 at row 1 + q (u0 kept in u0s for the
+// split).  Every thread of the CTA calls it.
+template <int M, int T>
+__device__ __forceinline__ void pfa_core(double2* buf, const BlueTables& bt, const double2* tw, int t, double2* u0s,
+                                         double2* dcs) {
+  using P = Pfa<M>;
+  constexpr int N1 = P::N1, N2 = P::N2, R = P::R;
+#pragma unroll 1
+  for (int r = t; r < N2; r += T) {
+    double2 v[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = buf[r * N1 + n1];
+    fft::dft_odd_store<N1, -1, M>(v, buf, r * N1, 1);
+  }
+  __syncthreads();
+  if (t < N1) u0s[t] = buf[t];
+  ctm_dif<R, R, N1, T>(buf, tw, t);
+  {
+    constexpr int RL = fft::ct_last_radix<R>(), NB = R / RL;
+#pragma unroll 1
+    for (int beta = t; beta < N1 * NB; beta += T) {
+      const int bb = beta / N1, prob = beta - bb * N1;
+      const int base = bb * RL;
+      double2 v[RL];
+#pragma unroll
+      for (int r = 0; r < RL; ++r) v[r] = buf[(1 + base + r) * N1 + prob];
+      fft::dft<RL, -1>(v);
+      if (base == 0) dcs[prob] = v[0];  // sum of the column's Rader sequence
+#pragma unroll
+      for (int r = 0; r < RL; ++r) v[r] = cmul(v[r], __ldg(bt.bct + base + r));
+      fft::dft<RL, +1>(v);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) buf[(1 + base + r) * N1 + prob] = v[r];
+    }
+    __syncthreads();
+  }
+  ctm_dit<R, R, N1, T>(buf, tw, t);
+  if (t < N1) buf[t] = cadd(u0s[t], dcs[t]);
+  __syncthreads();
+}
+
 // The N-point DFT of the G lines (every thread of the CTA calls it).
 template <int M, int T, int G, int CORE>
 __device__ __forceinline__ void pkc_core(double2* sm, double2* buf, const BlueTables& bt, const double2* tw, int t,
-                                         double2* A0s, int g) {
+                                         double2* A0s, int g, double2* pfa_sm = nullptr) {
   cp_async_wait_all();
   __syncthreads();
-  if constexpr (CORE == CORE_DIRECT && (M & 1)) {
+  if constexpr (CORE == CORE_PFA) {
+    static_assert(G == 1, "one PFA line per CTA");
+    pfa_core<M, T>(buf, bt, tw, t, pfa_sm, pfa_sm + Pfa<M>::N1);
+  } else if constexpr (CORE == CORE_DIRECT && (M & 1)) {
     fft::fft_cta<M, -1, T, G>(sm, tw, threadIdx.x);
   } else if constexpr (DstCfg<M, CORE>::CT) {
     const int bar = G > 1 ? 1 + g : 0;
@@ -207,7 +319,8 @@ __device__ __forceinline__ void pkc_core(double2* sm, double2* buf, const BlueTa
 // doubles oa = [0, LO), ob = [LO, 2 LO).  Reads land in registers, then a
 // CTA barrier, then the writes.
 template <int M, int T, int CORE, int PS, int LO>
-__device__ __forceinline__ void pkc_split(double2* buf, const BlueTables& bt, int t, double2 A0) {
+__device__ __forceinline__ void pkc_split(double2* buf, const BlueTables& bt, int t, double2 A0,
+                                          const double2* u0 = nullptr) {
   const int N = bt.N;
   const double hs = 0.5 * bt.scale;
   double r[PS][4];
@@ -215,8 +328,8 @@ __device__ __forceinline__ void pkc_split(double2* buf, const BlueTables& bt, in
   for (int i = 0; i < PS; ++i) {
     const int l = t + i * T;
     if (2 * l <= N - 1) {
-      const double2 zl = pkc_get<M, CORE>(buf, bt, l, A0);
-      const double2 zm = pkc_get<M, CORE>(buf, bt, l == 0 ? 0 : N - l, A0);
+      const double2 zl = pkc_get<M, CORE>(buf, bt, l, A0, u0);
+      const double2 zm = pkc_get<M, CORE>(buf, bt, l == 0 ? 0 : N - l, A0, u0);
       const double f = l == 0 ? 0.25 : 0.5;
       r[i][0] = hs * (zm.y - zl.y);   // X^a_{2l}
       r[i][1] = hs * (zl.x - zm.x);   // X^b_{2l}
@@ -313,6 +426,7 @@ __global__ void DBX_DST_BOUNDS dst_rows(SpecArgs a) {
   __shared__ double red[32];
   __shared__ double2 A0s[G];
   __shared__ double ends[G][4];
+  __shared__ double2 pfa_sm[2 * (CORE == CORE_PFA ? Pfa<M>::N1 : 1)];  // PFA: column u0 and Rader sums
   const int g = threadIdx.x / T, t = threadIdx.x - g * T;
   double2* buf = sm + g * C::LINE;
   const BlueTables& bt = a.blue2;
@@ -346,8 +460,8 @@ __global__ void DBX_DST_BOUNDS dst_rows(SpecArgs a) {
     if (sine) return kind_sd(kind, x[j - 1], x[NL - j - 1], 0.0, 0.0, j, ri);
     return kind_sd(kind, x[j], x[NL - j], hh ? b0 : a0, hh ? be : ae, j, ri);
   });
-  pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g);
-  pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0));
+  pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g, pfa_sm);
+  pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0), pfa_sm);
   pkc_scans<G, C::LINE, C::LO>(sm, bt);
   const double* o = reinterpret_cast<const double*>(buf);
   const double al = bt.alpha;
@@ -368,8 +482,8 @@ __global__ void DBX_DST_BOUNDS dst_rows(SpecArgs a) {
     pkc_refill<M, T, CORE, PF>(buf, bt, t, val);
     a0 = ends[g][0]; ae = ends[g][1]; b0 = ends[g][2]; be = ends[g][3];
     kind = a.kind2;
-    pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g);
-    pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0));
+    pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g, pfa_sm);
+    pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0), pfa_sm);
     pkc_scans<G, C::LINE, C::LO>(sm, bt);
   }
   Epi e = make_epi(a, b, N);
@@ -405,6 +519,7 @@ __global__ void DBX_DST_BOUNDS dst_cols(SpecArgs a) {
   extern __shared__ double2 sm[];
   __shared__ double2 A0s[G];
   __shared__ double e0[2 * G], e1[2 * G];
+  __shared__ double2 pfa_sm[2 * (CORE == CORE_PFA ? Pfa<M>::N1 : 1)];  // PFA: column u0 and Rader sums
   const int g = threadIdx.x / T, t = threadIdx.x - g * T;
   double2* buf = sm + g * C::LINE;
   const BlueTables& bt = a.blue1;
@@ -434,8 +549,8 @@ __global__ void DBX_DST_BOUNDS dst_cols(SpecArgs a) {
     if (sine) return kind_sd(kind, x[(size_t)(j - 1) * n2], x[(size_t)(NL - j - 1) * n2], 0.0, 0.0, j, ri);
     return kind_sd(kind, x[(size_t)j * n2], x[(size_t)(NL - j) * n2], hh ? xb0 : xa0, hh ? xbe : xae, j, ri);
   });
-  pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g);
-  pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0));
+  pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g, pfa_sm);
+  pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0), pfa_sm);
   pkc_scans<G, C::LINE, C::LO>(sm, bt);
   // outputs: 2G adjacent columns per row (index s fastest)
   const bool had = a.epi == SPEC_HADAMARD && a.d;
@@ -494,6 +609,9 @@ int cols_launch(const SpecArgs& a, cudaStream_t s) {
 #define DBX_DIRECT_LIST(X) X(15) X(31) X(63) X(255) X(1023) X(4095)
 #define DBX_BLUE_LIST(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
 #define DBX_RADER_LIST(X) X(22) X(126) X(8190)
+// prime-factor lengths N = N1 N2 (N1 <= 31 compiled radix, N2 prime, N2 - 1 a
+// compiled CT length): 2047 = 23 x 89 (C4), 115 = 23 x 5 (tests: small lines)
+#define DBX_PFA_LIST(X) X(2047) X(115)
 
 int direct_supported_len(int N) {
 #define X(L) if (N == (L)) return (L);
@@ -508,6 +626,21 @@ int blue_supported_len(int need) {
   DBX_BLUE_LIST(X)
 #undef X
   return best;
+}
+
+int pfa_supported_len(int N) {
+#define X(L) if (N == (L)) return (L);
+  DBX_PFA_LIST(X)
+#undef X
+  return 0;
+}
+
+void pfa_factors(int N, int* N1, int* N2) {
+  *N1 = 0;
+  *N2 = 0;
+#define X(L) if (N == (L)) { *N1 = Pfa<L>::N1; *N2 = Pfa<L>::N2; }
+  DBX_PFA_LIST(X)
+#undef X
 }
 
 int rader_supported_len(int M) {
@@ -525,6 +658,10 @@ static int dispatch(int core, int M, const SpecArgs& a, cudaStream_t s, bool row
   } else if (core == CORE_BLUE) {
 #define X(L) if (M == (L)) return rows ? rows_launch<L, CORE_BLUE>(a, s) : cols_launch<L, CORE_BLUE>(a, s);
     DBX_BLUE_LIST(X)
+#undef X
+  } else if (core == CORE_PFA) {
+#define X(L) if (M == (L)) return rows ? rows_launch<L, CORE_PFA>(a, s) : cols_launch<L, CORE_PFA>(a, s);
+    DBX_PFA_LIST(X)
 #undef X
   } else {
 #define X(L) if (M == (L)) return rows ? rows_launch<L, CORE_RADER>(a, s) : cols_launch<L, CORE_RADER>(a, s);

@@ -11,7 +11,9 @@ namespace dbx {
 
 // N-point DFT core of the packed DST (dst.cu): direct (M = N smooth),
 // Bluestein (M = 2^k >= 2N-1), Rader (M = N-1, N prime).
-enum DstCore { CORE_DIRECT = 0, CORE_BLUE = 1, CORE_RADER = 2 };
+// CORE_PFA: prime factor N = N1 N2 (Good-Thomas), row DFTs of N1 in
+// registers, column DFTs of the prime N2 by Rader (C4: 2047 = 23 x 89).
+enum DstCore { CORE_DIRECT = 0, CORE_BLUE = 1, CORE_RADER = 2, CORE_PFA = 3 };
 
 enum SpecEpi { SPEC_STORE = 0, SPEC_HADAMARD = 1, SPEC_RESID = 2, SPEC_AXPY = 3 };
 
@@ -102,6 +104,8 @@ int blue_supported_len(int need);   // smallest compiled power of two M >= need,
 int conv_rows_per_cta(int L2);
 int direct_supported_len(int N);  // N if the direct odd-length DFT is compiled, else 0
 int rader_supported_len(int M);   // M (= N-1) if the Rader convolution length is compiled, else 0
+int pfa_supported_len(int N);     // N if the prime-factor core is compiled for N, else 0 (pfa_factors gives N1, N2)
+void pfa_factors(int N, int* N1, int* N2);
 
 // Each returns the number of CTAs per image (for the partial-sum count), -1 if
 // the size is not compiled.

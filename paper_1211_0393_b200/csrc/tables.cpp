@@ -274,4 +274,85 @@ void ar_ramp(BlueHost& b, int n, bool sine_i) {
   }
 }
 
+
+// Prime-factor (Good-Thomas) tables of the N-point DFT, N = N1 N2 coprime,
+// N1 a compiled odd radix (row DFTs in registers), N2 prime with N2 - 1 a
+// compiled in-place Cooley-Tukey length (column DFTs by Rader).  Line layout:
+// N2 rows of N1 complex; row 0 holds n2 = 0, row 1 + p holds n2 = g^p (the
+// Rader order), so the column convolutions read rows 1..N2-1 in place.
+//   dlog[j] = row(n2) N1 + n1 with j = (N2 n1 + N1 n2) mod N (input map)
+//   ridx[k2] = q with g^-q = k2 (mod N2), k2 in [1, N2): output U[k2] sits
+//              at row 1 + q of its column (after the convolution)
+//   tw      = W_{N2-1}^e, bct = FFT_{N2-1}(b) / (N2-1) in the CT core's
+//             digit-reversed order, b_m = exp(-2 pi i g^-m / N2)
+BlueHost pfa(int n, bool sine_i, int N1, int N2) {
+  BlueHost b;
+  b.n = n;
+  b.N = sine_i ? n + 1 : n - 1;
+  const long N = b.N, R = N2 - 1;
+  b.M = (int)N;
+  b.core = 3;
+  b.scale = (double)sqrtl(2.0L / (long double)N);
+  b.tw = twiddles((int)R);
+  std::vector<long> qs;
+  for (long m = R, d = 2; m > 1; ++d) {
+    if (d * d > m) d = m;
+    if (m % d == 0) {
+      qs.push_back(d);
+      while (m % d == 0) m /= d;
+    }
+  }
+  long g = 2;
+  for (;; ++g) {
+    bool ok = true;
+    for (long q : qs) ok = ok && powmod(g, R / q, N2) != 1;
+    if (ok) break;
+  }
+  std::vector<long> dl((size_t)N2, 0), gp((size_t)R);
+  long v = 1;
+  for (long p = 0; p < R; ++p) {
+    gp[(size_t)p] = v;
+    dl[(size_t)v] = p;
+    v = v * g % N2;
+  }
+  auto row = [&](long n2) { return n2 == 0 ? 0L : 1 + dl[(size_t)n2]; };
+  // modular inverses by search (small moduli)
+  long inv21 = 1, inv12 = 1;
+  while ((N2 * inv21) % N1 != 1) ++inv21;
+  while ((N1 * inv12) % N2 != 1) ++inv12;
+  b.dlog.assign((size_t)N, 0);
+  for (long j = 0; j < N; ++j) {
+    const long n1 = (j % N1) * inv21 % N1, n2 = (j % N2) * inv12 % N2;
+    b.dlog[(size_t)j] = (int)(row(n2) * N1 + n1);
+  }
+  b.ridx.assign((size_t)N2, 0);
+  for (long k2 = 1; k2 < N2; ++k2) b.ridx[(size_t)k2] = (int)((R - dl[(size_t)k2]) % R);
+  std::vector<std::complex<long double>> bb((size_t)R), eR((size_t)R);
+  for (long m = 0; m < R; ++m) {
+    const long e = gp[(size_t)((R - m) % R)];
+    const long double a = 2.0L * kPiL * (long double)e / (long double)N2;
+    bb[(size_t)m] = {cosl(a), -sinl(a)};
+    const long double c = 2.0L * kPiL * (long double)m / (long double)R;
+    eR[(size_t)m] = {cosl(c), -sinl(c)};
+  }
+  b.bhat.assign(2 * (size_t)R, 0.0);
+  for (long k = 0; k < R; ++k) {
+    std::complex<long double> acc = 0;
+    for (long t = 0; t < R; ++t) acc += bb[(size_t)t] * eR[(size_t)((k * t) % R)];
+    acc /= (long double)R;
+    put(b.bhat.data(), k, acc.real(), acc.imag());
+  }
+  b.bct.assign(2 * (size_t)R, 0.0);
+  for (int p = 0; p < (int)R; ++p) {
+    const int k = fft::ct_freq_of_pos((int)R, p);
+    b.bct[2 * (size_t)p] = b.bhat[2 * (size_t)k];
+    b.bct[2 * (size_t)p + 1] = b.bhat[2 * (size_t)k + 1];
+  }
+  b.chirp.assign(2, 0.0);
+  ar_ramp(b, n, sine_i);
+  b.sn.assign((size_t)N, 0.0);
+  for (long j = 1; j < N; ++j) b.sn[(size_t)j] = (double)sinl(kPiL * (long double)j / (long double)N);
+  return b;
+}
+
 }  // namespace dbx

@@ -36,6 +36,9 @@ BlueHost bluestein(int n, bool sine_i, int M);
 // (Z/N)^*, dlog[j] = p with g^p = j, ridx[l] = q with g^-q = l, and the kernel
 // spectrum bhat = FFT_M(b) / M, b_m = exp(-2 pi i g^-m / N).
 BlueHost rader(int n, bool sine_i);
+// Prime-factor tables (N = N1 N2, row DFTs of N1 in registers, column DFTs of
+// the prime N2 by Rader over the in-place CT core): see tables.cpp pfa().
+BlueHost pfa(int n, bool sine_i, int N1, int N2);
 bool is_prime(long N);
 
 }  // namespace dbx

@@ -352,6 +352,26 @@ def test_dst_engines_match_oracle(dev, oracle, n1, n2, engine):
         assert rel(dev.precondition_apply(d, r, engine=eng), ref) <= OP_TOL
 
 
+@pytest.mark.parametrize("n1,n2", [(116, 116), (116, 40), (2048, 64), (64, 2048), (114, 116)])
+def test_pfa_dst_matches_oracle(dev, oracle, n1, n2):
+    """Prime-factor core (N = 23 x 5 = 115, 23 x 89 = 2047 for C4: Good-Thomas
+    rows of 23 in registers, Rader columns over the in-place CT core) against
+    the oracle: tensor_apply along both axes (the column pass runs the
+    transposed images through the same row kernel), the preconditioner
+    (fused T~ d^T T pass) and SineI at N = n+1 = 115."""
+    rng = np.random.default_rng(n1 * 7 + n2)
+    x = rng.uniform(-1, 1, (n1, n2))
+    kinds = [dev.TransformKind.AntiReflective, dev.TransformKind.AntiReflectiveInverse, dev.TransformKind.SineI]
+    for kind in kinds:
+        got = dev.tensor_apply(kind, x)
+        assert rel(got, oracle.tensor_apply(int(kind), x)) <= OP_TOL, kind
+    t = rand_psf(rng, 2, 2)
+    d = dev.build_tikhonov(dev.Psf(t), dev.PreconditionerSpec(dev.Algebra.AntiReflective, 0.02), n1, n2)
+    r = rng.uniform(-1, 1, (n1, n2))
+    ref = oracle.precondition_apply(oracle.build_tikhonov(t, 0.02, n1, n2), r)
+    assert rel(dev.precondition_apply(d, r), ref) <= OP_TOL
+
+
 @pytest.mark.parametrize("n1,n2,kinds", [
     (24, 128, ("AntiReflective", "AntiReflectiveInverse")),  # N = n-1 = 23, 127 (prime; M = 22, 126)
     (22, 126, ("SineI",)),                                    # N = n+1 = 23, 127
