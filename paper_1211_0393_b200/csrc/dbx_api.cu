@@ -332,7 +332,8 @@ struct dbx_plan {
     if (bc != DBX_BC_ANTIREFLECTIVE || n1 != n2 || n1 < 3 || conv_len(n2, q2) <= 0) return false;
     int M = 0;
     const int core = dst_core(n1 - 1, &M);
-    return (core == CORE_DIRECT || core == CORE_BLUE) && fused_supported(conv_len(n2, q2), M, core == CORE_BLUE);
+    return (core == CORE_DIRECT || core == CORE_BLUE || core == CORE_PFA) &&
+           fused_supported(conv_len(n2, q2), M, core == CORE_BLUE);
   }
   // DST core and DFT length M for an N-point DFT: direct (N compiled: prime
   // factors <= 31), Bluestein (compiled power of two M >= 2N-1), Rader (N

@@ -38,15 +38,6 @@ constexpr bool kDstCtBlue = true;
 constexpr bool kDstCtBlue = false;
 #endif
 
-// Prime-factor geometry (CORE_PFA): N1 = the largest compiled odd radix of
-// M, N2 = M / N1 prime, R = N2 - 1 the Rader convolution length.
-template <int M>
-struct Pfa {
-  static constexpr int N1 = fft::next_radix(M);
-  static constexpr int N2 = N1 ? M / N1 : 1;
-  static constexpr int R = N2 - 1;
-};
-
 template <int M, int CORE>
 struct DstCfg {
   // PFA lines: one line per CTA, 256 threads (23 x 11 = 253 butterflies of
@@ -79,6 +70,9 @@ struct DstCfg {
 };
 #ifdef DBX_DST_MINB4096
 #define DBX_DST_BOUNDS __launch_bounds__(DstCfg<M, CORE>::NT, DstCfg<M, CORE>::MINB)
+#elif defined(DBX_PFA_MINB)
+// PFA lines (32 KB each) at DBX_PFA_MINB CTAs per SM (A/B of the register cap)
+#define DBX_DST_BOUNDS __launch_bounds__(DstCfg<M, CORE>::NT, CORE == CORE_PFA ? DBX_PFA_MINB : 1)
 #else
 #define DBX_DST_BOUNDS __launch_bounds__(DstCfg<M, CORE>::NT)
 #endif
@@ -88,12 +82,7 @@ template <int M, int CORE>
 __device__ __forceinline__ double2 pkc_get(const double2* buf, const BlueTables& bt, int l, double2 A0,
                                            const double2* u0 = nullptr) {
   if constexpr (CORE == CORE_PFA) {
-    // X_l = U_{k1}[k2], k1 = l mod N1, k2 = l mod N2: row 0 holds k2 = 0, row
-    // 1 + q holds k2 = g^-q without the column's u0 (added here)
-    using P = Pfa<M>;
-    const int k1 = l % P::N1, k2 = l % P::N2;
-    if (k2 == 0) return buf[k1];
-    return cadd(buf[(1 + __ldg(bt.ridx + k2)) * P::N1 + k1], u0[k1]);
+    return pfa_get<M>(buf, bt, l, u0);
   } else if constexpr (CORE == CORE_RADER) {
     if (l == 0) return A0;
     return buf[pad<M>(__ldg(bt.ridx + l))];
@@ -191,93 +180,6 @@ __device__ __forceinline__ void pkc_refill(double2* buf, const BlueTables& bt, i
   }
 }
 
-// ---------------------------------------------------------------------------
-// Prime-factor core: P = N1 independent length-R cyclic convolutions (the
-// Rader sequences of the N1 columns, rows 1..R at stride N1) on the in-place
-// Cooley-Tukey core of fft.cuh, threads mapped column-fastest (consecutive
-// lanes hit consecutive slots).
-template <int L, int Ls, int P, int T, int DIR>
-__device__ __forceinline__ void ctm_level(double2* buf, const double2* __restrict__ tw, int t) {
-  constexpr int R = fft::ct_radix(Ls), m = Ls / R, NB = L / R;
-#pragma unroll 1
-  for (int beta = t; beta < P * NB; beta += T) {
-    const int bb = beta / P, prob = beta - bb * P;
-    const int blk = bb / m, j = bb - blk * m;
-    const int base = blk * Ls + j;
-    const double2 w1 = tw[j * (L / Ls)];
-    double2 v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = buf[(1 + base + r * m) * P + prob];
-    if constexpr (DIR < 0) {
-      fft::dft<R, -1>(v);
-      fft::apply_twiddles<R, -1>(v, w1);
-    } else {
-      fft::apply_twiddles<R, +1>(v, w1);
-      fft::dft<R, +1>(v);
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) buf[(1 + base + r * m) * P + prob] = v[r];
-  }
-  __syncthreads();
-}
-template <int L, int Ls, int P, int T>
-__device__ __forceinline__ void ctm_dif(double2* buf, const double2* __restrict__ tw, int t) {
-  if constexpr (Ls / fft::ct_radix(Ls) > 1) {
-    ctm_level<L, Ls, P, T, -1>(buf, tw, t);
-    ctm_dif<L, Ls / fft::ct_radix(Ls), P, T>(buf, tw, t);
-  }
-}
-template <int L, int Ls, int P, int T>
-__device__ __forceinline__ void ctm_dit(double2* buf, const double2* __restrict__ tw, int t) {
-  if constexpr (Ls / fft::ct_radix(Ls) > 1) {
-    ctm_dit<L, Ls / fft::ct_radix(Ls), P, T>(buf, tw, t);
-    ctm_level<L, Ls, P, T, +1>(buf, tw, t);
-  }
-}
-
-// The N-point DFT of one PFA line: row DFTs (N2 rows of N1, in registers,
-// outputs stored as formed), then the N1 column DFTs of length N2: U[0] =
-// u0 + sum(a) into row 0, U[g^-q] - u0 at row 1 + q (u0 kept in u0s for the
-// split).  Every thread of the CTA calls it.
-template <int M, int T>
-__device__ __forceinline__ void pfa_core(double2* buf, const BlueTables& bt, const double2* tw, int t, double2* u0s,
-                                         double2* dcs) {
-  using P = Pfa<M>;
-  constexpr int N1 = P::N1, N2 = P::N2, R = P::R;
-#pragma unroll 1
-  for (int r = t; r < N2; r += T) {
-    double2 v[N1];
-#pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) v[n1] = buf[r * N1 + n1];
-    fft::dft_odd_store<N1, -1, M>(v, buf, r * N1, 1);
-  }
-  __syncthreads();
-  if (t < N1) u0s[t] = buf[t];
-  ctm_dif<R, R, N1, T>(buf, tw, t);
-  {
-    constexpr int RL = fft::ct_last_radix<R>(), NB = R / RL;
-#pragma unroll 1
-    for (int beta = t; beta < N1 * NB; beta += T) {
-      const int bb = beta / N1, prob = beta - bb * N1;
-      const int base = bb * RL;
-      double2 v[RL];
-#pragma unroll
-      for (int r = 0; r < RL; ++r) v[r] = buf[(1 + base + r) * N1 + prob];
-      fft::dft<RL, -1>(v);
-      if (base == 0) dcs[prob] = v[0];  // sum of the column's Rader sequence
-#pragma unroll
-      for (int r = 0; r < RL; ++r) v[r] = cmul(v[r], __ldg(bt.bct + base + r));
-      fft::dft<RL, +1>(v);
-#pragma unroll
-      for (int r = 0; r < RL; ++r) buf[(1 + base + r) * N1 + prob] = v[r];
-    }
-    __syncthreads();
-  }
-  ctm_dit<R, R, N1, T>(buf, tw, t);
-  if (t < N1) buf[t] = cadd(u0s[t], dcs[t]);
-  __syncthreads();
-}
-
 // The N-point DFT of the G lines (every thread of the CTA calls it).
 template <int M, int T, int G, int CORE>
 __device__ __forceinline__ void pkc_core(double2* sm, double2* buf, const BlueTables& bt, const double2* tw, int t,
@@ -286,7 +188,7 @@ __device__ __forceinline__ void pkc_core(double2* sm, double2* buf, const BlueTa
   __syncthreads();
   if constexpr (CORE == CORE_PFA) {
     static_assert(G == 1, "one PFA line per CTA");
-    pfa_core<M, T>(buf, bt, tw, t, pfa_sm, pfa_sm + Pfa<M>::N1);
+    pfa_core<M, T>(buf, bt, tw, t, 0, pfa_sm);
   } else if constexpr (CORE == CORE_DIRECT && (M & 1)) {
     fft::fft_cta<M, -1, T, G>(sm, tw, threadIdx.x);
   } else if constexpr (DstCfg<M, CORE>::CT) {
@@ -610,8 +512,9 @@ int cols_launch(const SpecArgs& a, cudaStream_t s) {
 #define DBX_BLUE_LIST(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
 #define DBX_RADER_LIST(X) X(22) X(126) X(8190)
 // prime-factor lengths N = N1 N2 (N1 <= 31 compiled radix, N2 prime, N2 - 1 a
-// compiled CT length): 2047 = 23 x 89 (C4), 115 = 23 x 5 (tests: small lines)
-#define DBX_PFA_LIST(X) X(2047) X(115)
+// compiled CT length; pfa.cuh pfa_len): 2047 = 23 x 89 (C4), 511 = 7 x 73 (C2),
+// 115 = 23 x 5 (tests: small lines)
+#define DBX_PFA_LIST(X) X(2047) X(511) X(115)
 
 int direct_supported_len(int N) {
 #define X(L) if (N == (L)) return (L);

@@ -39,7 +39,10 @@ __host__ __device__ constexpr int fused_dst_per(int) { return 8; }
 #define FUSED_TD_ODD 128  // A/B r1s2m: 96 (line_threads) 14972, 128 15455, 160 15152, 192 15209
 #endif
 __host__ __device__ constexpr int fused_td(int M) {
-  return (FUSED_TD_ODD > 0 && (M & 1) && M > 512) ? FUSED_TD_ODD : line_threads(M, fused_dst_per(M));
+  // prime-factor lines (pfa.cuh, C2's 511 = 7 x 73): 128 threads (73 row
+  // DFTs, 63 butterflies of the widest column level)
+  return pfa_len(M) ? 128
+         : (FUSED_TD_ODD > 0 && (M & 1) && M > 512) ? FUSED_TD_ODD : line_threads(M, fused_dst_per(M));
 }
 
 #ifndef DBX_TT_MINB
@@ -55,7 +58,7 @@ struct Fused {
   static constexpr int LC = padded_len(L2);                 // conv line (double2)
   static constexpr int LD = padded_len(M);                  // DST line (double2)
   static constexpr size_t kBudget = 115200;                 // two CTAs per SM (228 KB - reserved)
-  static constexpr size_t TWD = (size_t)fft::twiddles_needed(M) * 16;   // staged twiddle prefixes
+  static constexpr size_t TWD = (size_t)dst_twiddles_needed(M) * 16;     // staged twiddle prefixes
   static constexpr size_t TWC = (size_t)fft::twiddles_needed(L2) * 16;
   // ---- 4-row kernels (rows_ainv_tt, rows_t_axpy_afwd): two conv lines of
   // two packed rows each, then two packed DST lines of two rows each
@@ -232,9 +235,10 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, SEP ? DBX_TT_MINB : 2)
     return make_double2(lj + lm - (x0 + xe), (lj - lm) - (x0 - xe) * fma(-2.0 * ri, (double)j, 1.0));
   });
   PH(23)
-  blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
+  __shared__ double2 pfa_aux[2][2 * Pfa<M>::N1];  // prime-factor lines: u0 + Rader sums per line
+  blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t, pfa_aux[g]);
   PH(24)
-  pk_split2<M, BLUE, LMAX>(dbuf, bt, rowS + (2 * g) * LS, rowS + (2 * g + 1) * LS, t, TD);
+  pk_split2<M, BLUE, LMAX>(dbuf, bt, rowS + (2 * g) * LS, rowS + (2 * g + 1) * LS, t, TD, pfa_aux[g]);
   __syncthreads();
   odd_scans2<LMAX>(rowS, LS, 4, bt);
   __syncthreads();
@@ -311,9 +315,10 @@ __global__ void __launch_bounds__(Fused<L2, M, BLUE>::NT, 2) rows_t_axpy_afwd(Sp
     return make_double2(vj + vm, vj - vm);
   });
   PH(11)
-  blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t);
+  __shared__ double2 pfa_aux[2][2 * Pfa<M>::N1];  // prime-factor lines: u0 + Rader sums per line
+  blue_core<M, TD, 2, BLUE>(sm, dbuf, bt, twd, t, pfa_aux[g]);
   PH(12)
-  pk_split2<M, BLUE, LMAX>(dbuf, bt, io + (2 * g) * LSO, io + (2 * g + 1) * LSO, t, TD);
+  pk_split2<M, BLUE, LMAX>(dbuf, bt, io + (2 * g) * LSO, io + (2 * g + 1) * LSO, t, TD, pfa_aux[g]);
   __syncthreads();
   // the DST lines are free now: stage the f rows there (L2-prefetched at
   // kernel start) behind the scans
@@ -593,7 +598,7 @@ struct TcolSmem {
   // twiddles are read through L1, so three CTAs fit per SM
   static constexpr bool DL = DBX_TC_MINB >= 3;
   static constexpr size_t off_tw = off_d + (DL ? 0 : (size_t)4 * LS * 8);
-  static constexpr size_t TWB = (size_t)fft::twiddles_needed(M) * 16;
+  static constexpr size_t TWB = (size_t)dst_twiddles_needed(M) * 16;
   static constexpr bool TW = !DL && off_tw + TWB <= 115200;  // keep 2 CTAs / SM
   static constexpr size_t bytes = TW ? off_tw + TWB : off_tw;
 };
@@ -649,9 +654,10 @@ __global__ void __launch_bounds__(2 * fused_td(M), DBX_TC_MINB) dst_tcols(SpecAr
     return make_double2(lj + lm - (x0 + xe), (lj - lm) - (x0 - xe) * fma(-2.0 * ri, (double)j, 1.0));
   });
   PH(1)
-  blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
+  __shared__ double2 pfa_aux[2][2 * Pfa<M>::N1];  // prime-factor lines: u0 + Rader sums per line
+  blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t, pfa_aux[g]);
   PH(2)
-  pk_split2<M, BLUE, LMAX>(buf, bt, io + (2 * g) * LSO, io + (2 * g + 1) * LSO, t, TD);
+  pk_split2<M, BLUE, LMAX>(buf, bt, io + (2 * g) * LSO, io + (2 * g + 1) * LSO, t, TD, pfa_aux[g]);
   __syncthreads();
   PH(3)
   odd_scans2<LMAX>(io, LSO, 4, bt);
@@ -700,9 +706,9 @@ __global__ void __launch_bounds__(2 * fused_td(M), DBX_TC_MINB) dst_tcols(SpecAr
     }
   });
   PH(5)
-  blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t);
+  blue_core<M, TD, 2, BLUE>(sm, buf, bt, tw, t, pfa_aux[g]);
   PH(6)
-  pk_split2<M, BLUE, LMAX>(buf, bt, io + (2 * g) * LSO, io + (2 * g + 1) * LSO, t, TD);
+  pk_split2<M, BLUE, LMAX>(buf, bt, io + (2 * g) * LSO, io + (2 * g + 1) * LSO, t, TD, pfa_aux[g]);
   __syncthreads();
   PH(7)
   odd_scans2<LMAX>(io, LSO, 4, bt);
@@ -767,7 +773,7 @@ int fused_debug_phases(unsigned long long* out, int n) {
 #endif
 
 // (conv L2, DST M, Bluestein?) combinations compiled for the fused pipeline.
-#define DBX_FUSED_LIST(X) X(1080, 1023, false) X(540, 1024, true) X(270, 255, false)
+#define DBX_FUSED_LIST(X) X(1080, 1023, false) X(540, 1024, true) X(540, 511, false) X(270, 255, false)
 
 bool fused_sep_supported(int L2, int M, bool blue, int n2, int q2) {
   if (!conv_sep_supported(q2) || resid_sep_bytes(n2, q2) > 200 * 1024) return false;

@@ -7,6 +7,7 @@
 #include "dbx_internal.h"
 #include "fft.cuh"
 #include "spectral.h"
+#include "pfa.cuh"
 
 namespace dbx {
 
@@ -101,7 +102,7 @@ __device__ __forceinline__ int nsm() {
 template <int L, bool SMEM, int NEED_ = 0>
 __device__ __forceinline__ const double2* stage_twiddles(double2* dst, const double2* src) {
   if constexpr (SMEM) {
-    constexpr int NEED = NEED_ > 0 ? NEED_ : fft::twiddles_needed(L);
+    constexpr int NEED = NEED_ > 0 ? NEED_ : dst_twiddles_needed(L);
     for (int i = threadIdx.x; i < NEED; i += blockDim.x) cp_async16(dst + i, src + i);
     cp_async_commit();
     return dst;
@@ -248,31 +249,36 @@ __device__ __forceinline__ double2 pre(double2 z, const BlueTables& bt, int j) {
 // BLUE: FFT, multiply by the kernel spectrum, inverse FFT.  Direct: one FFT.
 template <int M, int T, int G, bool BLUE>
 __device__ __forceinline__ void blue_core(double2* sm, double2* buf, const BlueTables& bt, const double2* tw,
-                                          int t) {
+                                          int t, double2* pfa_aux = nullptr) {
   cp_async_wait_group<1>();  // the twiddle group (committed first) has landed
   __syncthreads();
-  if constexpr (!BLUE) {
+  if constexpr (pfa_len(M)) {
+    // prime-factor line (pfa.cuh), per-line named barriers
+    const int bar = G > 1 ? 1 + (int)threadIdx.x / T : 0;
+    pfa_core<M, T>(buf, bt, tw, t, bar, pfa_aux);
+    __syncthreads();
+    return;
+  } else if constexpr (!BLUE) {
     // direct odd length: large-prime stages packed across the CTA's G lines
     fft::fft_cta<M, -1, T, G>(sm, tw, threadIdx.x);
     return;
-  }
-  const int bar = G > 1 ? 1 + (int)threadIdx.x / T : 0;  // per-line named barrier
+  } else {
+    const int bar = G > 1 ? 1 + (int)threadIdx.x / T : 0;  // per-line named barrier
 #ifndef DBX_FUSED_STOCKHAM_BLUE
-  // in-place Cooley-Tukey convolution core (fft.cuh ct_convolve, the Rader
-  // core of dst.cu): C2's 1024-point Bluestein lines 3763 -> 4052 Mpx-it/s
-  // (profiles/r02_fused_ct_ab.txt); -DDBX_FUSED_STOCKHAM_BLUE restores the two
-  // Stockham FFTs.  Needs the CT twiddle prefix inside the staged Stockham one.
-  static_assert(fft::ct_twiddles_needed(M) <= fft::twiddles_needed(M), "CT twiddle prefix");
-  fft::ct_convolve<M, T>(buf, tw, bt.bct, t, bar, nullptr);
+    // in-place Cooley-Tukey convolution core (fft.cuh ct_convolve, the Rader
+    // core of dst.cu): C2's 1024-point Bluestein lines 3763 -> 4052 Mpx-it/s
+    // (profiles/r02_fused_ct_ab.txt); -DDBX_FUSED_STOCKHAM_BLUE restores the two
+    // Stockham FFTs.  Needs the CT twiddle prefix inside the staged Stockham one.
+    static_assert(fft::ct_twiddles_needed(M) <= fft::twiddles_needed(M), "CT twiddle prefix");
+    fft::ct_convolve<M, T>(buf, tw, bt.bct, t, bar, nullptr);
 #else
-  fft::fft<M, -1, T>(buf, tw, t, bar);
-  if constexpr (BLUE) {
+    fft::fft<M, -1, T>(buf, tw, t, bar);
     for (int j = t; j < M; j += T) buf[pad<M>(j)] = cmul(buf[pad<M>(j)], __ldg(bt.bhat + j));
     fft::line_sync(bar, T);
     fft::fft<M, +1, T>(buf, tw, t, bar);
-  }
 #endif
-  __syncthreads();  // the split reads other lines' data only after every line finished
+    __syncthreads();  // the split reads other lines' data only after every line finished
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -312,8 +318,13 @@ __device__ __forceinline__ void pk_fill(double2* buf, const BlueTables& bt, int 
       const double2 A = sd(0, j), B = sd(1, j);
       const double2 zj = make_double2(fma(s, A.x, 0.5 * A.y), fma(s, B.x, 0.5 * B.y));
       const double2 zm = make_double2(fma(s, A.x, -0.5 * A.y), fma(s, B.x, -0.5 * B.y));
-      buf[pad<M>(j)] = pre<BLUE>(zj, bt, j);
-      if (N - j != j) buf[pad<M>(N - j)] = pre<BLUE>(zm, bt, N - j);
+      if constexpr (pfa_len(M)) {  // Good-Thomas input map (pfa.cuh)
+        buf[__ldg(bt.dlog + j)] = zj;
+        if (N - j != j) buf[__ldg(bt.dlog + N - j)] = zm;
+      } else {
+        buf[pad<M>(j)] = pre<BLUE>(zj, bt, j);
+        if (N - j != j) buf[pad<M>(N - j)] = pre<BLUE>(zm, bt, N - j);
+      }
     }
   }
 }
@@ -434,14 +445,20 @@ __device__ __forceinline__ double pk_at(const double* o, int k) {
 
 template <int M, bool BLUE, int LMAX>
 __device__ __forceinline__ void pk_split2(const double2* buf, const BlueTables& bt, double* oa, double* ob, int t,
-                                          int T) {
+                                          int T, const double2* pfa_u0 = nullptr) {
   using P = PkOut<LMAX>;
   const int N = bt.N;
   const double hs = 0.5 * bt.scale;
   for (int l = t; 2 * l <= N - 1; l += T) {
     const int m = l == 0 ? 0 : N - l;
-    const double2 zl = pre<BLUE>(buf[pad<M>(l)], bt, l);
-    const double2 zm = pre<BLUE>(buf[pad<M>(m)], bt, m);
+    double2 zl, zm;
+    if constexpr (pfa_len(M)) {
+      zl = pfa_get<M>(buf, bt, l, pfa_u0);
+      zm = pfa_get<M>(buf, bt, m, pfa_u0);
+    } else {
+      zl = pre<BLUE>(buf[pad<M>(l)], bt, l);
+      zm = pre<BLUE>(buf[pad<M>(m)], bt, m);
+    }
     if (l >= 1) {
       oa[l] = hs * (zm.y - zl.y);
       ob[l] = hs * (zl.x - zm.x);
