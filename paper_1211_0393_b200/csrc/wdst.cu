@@ -37,6 +37,13 @@ namespace {
 
 constexpr int kWN = 1023;     // DFT length
 constexpr int kWLine = 1024;  // double2 slots per warp line
+// per-warp line stride: one slot more than the line, so the CTA-cooperative
+// reads of the 4 warps' outputs at the same k (64-byte row segments) hit 4
+// different bank groups instead of one (1024 slots = 16 KB = 0 mod 128 B)
+#ifndef DBX_WSTRIDE_PAD
+#define DBX_WSTRIDE_PAD 1
+#endif
+constexpr int kWStride = kWLine + DBX_WSTRIDE_PAD;
 constexpr int kWWarps = 4;    // warps (column pairs) per CTA
 // CTAs per SM the register budget is sized for: 2 -> up to 255 registers (the
 // DFT-31 row keeps 30 folded values + 30 constants live), 3 -> 168 (spills)
@@ -419,7 +426,7 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 wsm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double2* buf = wsm + (size_t)w * kWLine;
+  double2* buf = wsm + (size_t)w * kWStride;
   const BlueTables& bt = a.blue1;
   const int n = a.n1, n2 = a.n2;
   const size_t N = (size_t)n * n2;
@@ -520,7 +527,7 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
 #pragma unroll 4
     for (int idx = threadIdx.x; idx < kWWarps * n; idx += 32 * kWWarps) {
       const int ww = idx & (kWWarps - 1), k = idx / kWWarps;
-      const double2 o = wsm[(size_t)ww * kWLine + oslot(k)];
+      const double2 o = wsm[(size_t)ww * kWStride + oslot(k)];
       const double2 r0v = ramp[ww][0], r1v = ramp[ww][1];
       const double t1 = (double)k * ri;
       double wa = o.x + r0v.x * (1.0 - t1) + r1v.x * t1;
@@ -565,7 +572,7 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_tt_w(SpecArg
   extern __shared__ double2 wsm[];
   __shared__ double ends[2 * kWWarps][2];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double2* buf = wsm + (size_t)w * kWLine;
+  double2* buf = wsm + (size_t)w * kWStride;
   const BlueTables& bt = a.blue2;
   const int n1 = a.n1, n2 = a.n2;
   const size_t N = (size_t)n1 * n2;
@@ -617,7 +624,7 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_tt_w(SpecArg
     const int ww = idx & (kWWarps - 1), k = idx / kWWarps;
     const int rr = r0 + 2 * ww;
     if (rr >= n1) continue;
-    double2 o = wsm[(size_t)ww * kWLine + oslot(k)];
+    double2 o = wsm[(size_t)ww * kWStride + oslot(k)];
     if (k == 0) o = make_double2(al * ends[2 * ww][0], al * ends[2 * ww + 1][0]);
     if (k == n2 - 1) o = make_double2(al * ends[2 * ww][1], al * ends[2 * ww + 1][1]);
     double* dst = uT + (size_t)k * n1 + rr;
@@ -775,7 +782,7 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_t_axpy_w(Spe
 // the CTA count, or -1 when the shape is not this kernel's.
 int launch_dst_tcols_w(const SpecArgs& a, cudaStream_t s) {
   if (a.n1 != 1024 || a.blue1.N != kWN) return -1;
-  const size_t bytes = (size_t)kWWarps * kWLine * sizeof(double2);
+  const size_t bytes = (size_t)kWWarps * kWStride * sizeof(double2);
   dim3 grid((a.n2 + 2 * kWWarps - 1) / (2 * kWWarps), a.batch);
   if (a.n2 % (2 * kWWarps) == 0 && kWdstCtaStore) {
     static AttrOnce attr;
@@ -798,7 +805,7 @@ int launch_rows_w(int which, const SpecArgs& a, cudaStream_t s) {
   if (a.n2 != 1024 || a.blue2.N != kWN || a.q2 > 15 || !conv_sep_supported(a.q2)) return -1;
   dim3 grid((a.n1 + 2 * kWWarps - 1) / (2 * kWWarps), a.batch);
   if (which == 0) {
-    const size_t bytes = (size_t)kWWarps * kWLine * sizeof(double2);
+    const size_t bytes = (size_t)kWWarps * kWStride * sizeof(double2);
     static AttrOnce attr;
     if (!attr.ensure(rows_tt_w, bytes)) return -1;
     launch_k(rows_tt_w, grid, 32 * kWWarps, bytes, s, a);
