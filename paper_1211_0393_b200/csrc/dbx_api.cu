@@ -424,8 +424,22 @@ struct dbx_plan {
     tw2 = upload_owned(twiddles(L2));
     const size_t nt = taps.size();
     std::vector<double> rot(taps.rbegin(), taps.rend());
-    HA = upload_owned(conv_spectrum(rot.data(), q1, q2, L1, L2));
-    HAt = upload_owned(conv_spectrum(taps.data(), q1, q2, L1, L2));
+    // k2-major spectra; for the CT column core (kConvCt) each column k2 in
+    // the digit-reversed order of the in-place DIF output
+    auto ct_order = [&](std::vector<double> h) {
+      if (!kConvCt) return h;
+      std::vector<double> o(h.size());
+      const int Lh_ = L2 / 2 + 1;
+      for (int k2 = 0; k2 < Lh_; ++k2)
+        for (int p = 0; p < L1; ++p) {
+          const size_t src = 2 * ((size_t)k2 * L1 + fft::ct_freq_of_pos(L1, p)), dst = 2 * ((size_t)k2 * L1 + p);
+          o[dst] = h[src];
+          o[dst + 1] = h[src + 1];
+        }
+      return o;
+    };
+    HA = upload_owned(ct_order(conv_spectrum(rot.data(), q1, q2, L1, L2)));
+    HAt = upload_owned(ct_order(conv_spectrum(taps.data(), q1, q2, L1, L2)));
     // separable column pass for a rank-1 mask (factorisation residual within
     // kSepTol of the largest tap: rounding level, far below the 1e-10 parity)
     if (q1 > 0 && conv_sep_supported(q1)) {

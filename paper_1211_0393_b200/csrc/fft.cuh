@@ -941,7 +941,7 @@ __host__ __device__ constexpr int ct_last_radix() {
 // receives DFT(buf)_0 (position 0, before the product).  bar as for fft().
 template <int L, int T>
 __device__ __forceinline__ void ct_convolve(double2* buf, const double2* __restrict__ tw,
-                                            const double2* __restrict__ kdr, int t, int bar, double2* x0) {
+                                            const double2* kdr, int t, int bar, double2* x0) {
   static_assert(supported(L), "unsupported FFT length");
   ct_dif_levels<L, L, T>(buf, tw, t, bar);
   constexpr int R = ct_last_radix<L>(), NB = L / R;
@@ -962,7 +962,7 @@ __device__ __forceinline__ void ct_convolve(double2* buf, const double2* __restr
         dft<R, -1>(v[u]);
         if (x0 && base == 0) *x0 = v[u][0];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[u][r] = cmul(v[u][r], __ldg(kdr + base + r));
+        for (int r = 0; r < R; ++r) v[u][r] = cmul(v[u][r], kdr[base + r]);  // global or smem-staged
         dft<R, +1>(v[u]);
 #pragma unroll
         for (int r = 0; r < R; ++r) buf[pad<L>(base + r)] = v[u][r];

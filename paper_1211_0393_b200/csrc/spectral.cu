@@ -193,6 +193,15 @@ conv_col(SpecArgs a) {
     __syncthreads();
   }
   const int bar = G > 1 ? 1 + g : 0;
+  if constexpr (kConvCt) {
+    // cyclic convolution in place: DIF -> x digit-reversed spectrum -> DIT
+    static_assert(fft::ct_twiddles_needed(L1) <= fft::twiddles_needed(L1), "CT twiddle prefix");
+    if constexpr (SM::HS) {
+      cp_async_wait_all();
+      fft::line_sync(bar, T);  // the line's H entries (staged by all its threads) visible
+    }
+    fft::ct_convolve<L1, T>(buf, tw, SM::HS ? hst : Hcol, t, bar, nullptr);
+  } else {
   fft::fft<L1, -1, T>(buf, tw, t, bar);
   // the kernel-spectrum product rides on the inverse FFT's first-stage loads
   if constexpr (SM::HS) {
@@ -201,6 +210,7 @@ conv_col(SpecArgs a) {
     fft::fft_in<L1, +1, T>(buf, tw, t, bar, [&](int p) { return cmul(buf[pad<L1>(p)], hst[p]); });
   } else {
     fft::fft_in<L1, +1, T>(buf, tw, t, bar, [&](int p) { return cmul(buf[pad<L1>(p)], __ldg(Hcol + p)); });
+  }
   }
   if (G > 1) __syncthreads();  // the stores interleave the CTA's lines
   const int YS = y_stride(Lh);

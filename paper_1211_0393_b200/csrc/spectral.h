@@ -6,8 +6,20 @@
 
 #include "../../include/dbx.h"
 #include "dbx_internal.h"
+#include "radix.h"
 
 namespace dbx {
+
+// Column convolutions of the FFT-form blur (conv_col) run the in-place
+// Cooley-Tukey core with the kernel spectrum in digit-reversed order (the host
+// permutes each column, dbx_api.cu ensure_conv); -DDBX_CONV_STOCKHAM keeps
+// forward + inverse Stockham FFTs with the spectrum in natural order (A/B).
+#ifdef DBX_CONV_STOCKHAM
+constexpr bool kConvCt = false;
+#else
+constexpr bool kConvCt = true;
+#endif
+
 
 // N-point DFT core of the packed DST (dst.cu): direct (M = N smooth),
 // Bluestein (M = 2^k >= 2N-1), Rader (M = N-1, N prime).
