@@ -395,7 +395,7 @@ __global__ void DBX_DST_BOUNDS dst_rows(SpecArgs a) {
     if (r >= n1) continue;
     const double* oh = o + hh * C::LO;
     const double x0 = hh ? b0 : a0, xe = hh ? be : ae;
-    for (int k = t; k < n; k += T) e.put((size_t)r * n + k, kind_out(kind, oh, k, n, x0, xe, al, ri));
+    epi_row<4>(e, (size_t)r * n, n, t, T, [&](int k) { return kind_out(kind, oh, k, n, x0, xe, al, ri); });
   }
   write_partials<NT>(a, e, red, b);
 }

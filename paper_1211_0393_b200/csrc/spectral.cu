@@ -285,11 +285,9 @@ conv_row_inv(SpecArgs a) {
   cp_async_wait_all();
   __syncthreads();
   fft::fft<L2, +1, T>(buf, tw, t, G > 1 ? 1 + g : 0);
-  for (int c = t; c < n2; c += T) {
-    const double2 v = buf[pad<L2>(c)];
-    if (ra < n1) e.put((size_t)ra * n2 + c, v.x);
-    if (rb < n1) e.put((size_t)rb * n2 + c, v.y);
-  }
+  // operand loads (g / x_{k-1} / f / d) four deep per thread (epi_row)
+  if (ra < n1) epi_row<4>(e, (size_t)ra * n2, n2, t, T, [&](int c) { return buf[pad<L2>(c)].x; });
+  if (rb < n1) epi_row<4>(e, (size_t)rb * n2, n2, t, T, [&](int c) { return buf[pad<L2>(c)].y; });
   write_partials<NT>(a, e, red, b);
 }
 
