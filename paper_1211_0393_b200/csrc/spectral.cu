@@ -524,17 +524,27 @@ __global__ void __launch_bounds__(kColNT, col_minb(BAND)) cols_sep_real(SpecArgs
       }
     }
     if (colok) {
+      if constexpr (MODE == 2) {
+        // g loads four rows deep before their stores (the stores would keep
+        // the compiler from hoisting them; 16 deep spills at 64 registers)
 #pragma unroll
-      for (int r = 0; r < RT; ++r)
-        if (i0 + r < rows) {
-          if constexpr (MODE == 2) {
-            const double rv = __ldcs(G + (size_t)(i0 + r) * n2) - acc[r];
-            Y[(size_t)(i0 + r) * n2] = rv;
-            p2 += rv * rv;
-          } else {
-            Y[(size_t)(i0 + r) * n2] = acc[r];
-          }
+        for (int r0 = 0; r0 < RT; r0 += 4) {
+          double gv[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) gv[r] = i0 + r0 + r < rows ? __ldcs(G + (size_t)(i0 + r0 + r) * n2) : 0.0;
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (i0 + r0 + r < rows) {
+              const double rv = gv[r] - acc[r0 + r];
+              Y[(size_t)(i0 + r0 + r) * n2] = rv;
+              p2 += rv * rv;
+            }
         }
+      } else {
+#pragma unroll
+        for (int r = 0; r < RT; ++r)
+          if (i0 + r < rows) Y[(size_t)(i0 + r) * n2] = acc[r];
+      }
     }
   }
   if constexpr (MODE == 2) {
