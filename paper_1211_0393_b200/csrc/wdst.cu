@@ -63,6 +63,12 @@ constexpr int kWWarps = 4;    // warps (column pairs) per CTA
 #define DBX_WDST_CTA_STORE 1
 #endif
 constexpr bool kWdstCtaStore = DBX_WDST_CTA_STORE != 0;
+// warp-owned kernels for 256-point lines (C1); -DDBX_W255=0 keeps the CTA
+// lock-step fused kernels there (A/B)
+#ifndef DBX_W255
+#define DBX_W255 1
+#endif
+constexpr bool kW255 = DBX_W255 != 0;
 #ifndef DBX_WDST_PREFETCH
 #define DBX_WDST_PREFETCH 0
 #endif
@@ -416,21 +422,153 @@ __device__ __forceinline__ void wsplit(double2* buf, int lane, double hs, double
 #define WDFT wdft1023
 #endif
 
-// CTA_STORE (n2 a multiple of 2 kWWarps): after one CTA barrier the 4 warps'
+// ---------------------------------------------------------------------------
+// DFT_255 (C1's 256-point lines, N = 255 = 17 * 15) in the same warp-owned
+// form: level 1, lane n2 < 17: x[17 n1 + n2], n1 < 15 -> in-register DFT-15
+// (3 x 5 prime factor) -> * W_255^{n2 k1} -> slot 17 k1 + n2; level 2, lane
+// k1 < 15: the 17 contiguous slots 17 k1 + n2 -> DFT-17 (symmetric pairs) ->
+// X[k1 + 15 k2] at slot 17 k1 + k2.
+__device__ __forceinline__ int oslot255(int k) { return k ^ ((k >> 3) & 7); }
+__device__ __forceinline__ int wpos255(int l) {
+  const int k2 = l / 15;
+  return 17 * (l - 15 * k2) + k2;
+}
+
+__device__ __forceinline__ void wdft255(double2* buf, const double2* __restrict__ tw, int lane) {
+  constexpr int S = -1;
+  if (lane < 17) {
+    double2 v[15];
+#pragma unroll
+    for (int n1 = 0; n1 < 15; ++n1) v[n1] = buf[17 * n1 + lane];
+    fft::dft15<S>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < 15; ++k1) {
+      double2 x = v[k1];
+      if (k1 != 0) x = fft::cmul(x, __ldg(tw + lane * k1));  // n2 k1 <= 224
+      buf[17 * k1 + lane] = x;
+    }
+  }
+  __syncwarp();
+  if (lane < 15) {
+    const int base = 17 * lane;
+    double2 v[17];
+#pragma unroll
+    for (int j = 0; j < 17; ++j) v[j] = buf[base + j];
+    const double2 x0 = v[0];
+    double2 sum = x0;
+#pragma unroll
+    for (int j = 1; j <= 8; ++j) {
+      const double2 a = cadd(v[j], v[17 - j]), b = csub(v[j], v[17 - j]);
+      v[j] = a;
+      v[17 - j] = b;
+      sum = cadd(sum, a);
+    }
+    buf[base] = sum;
+#pragma unroll
+    for (int k = 1; k <= 8; ++k) {
+      double2 A = x0, B = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 1; j <= 8; ++j) {
+        const int e = (j * k) % 17;
+        A.x = fma(ccs<17>(e), v[j].x, A.x);
+        A.y = fma(ccs<17>(e), v[j].y, A.y);
+        B.x = fma(scs<17>(e), v[17 - j].x, B.x);
+        B.y = fma(scs<17>(e), v[17 - j].y, B.y);
+      }
+      const double2 sb = fft::mul_si<S>(B);
+      buf[base + k] = cadd(A, sb);
+      buf[base + 17 - k] = csub(A, sb);
+    }
+  }
+  __syncwarp();
+}
+
+// wsplit for N = 255: lane L owns the pairs l in [4L, 4L+4) (outputs
+// k in [8L, 8L+8)); same convention as wsplit.
+__device__ __forceinline__ void wsplit255(double2* buf, int lane, double hs, double sc) {
+  constexpr int NN = 255;
+  double2 zl[4], zm[4];
+  double ta = 0.0, tb = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int l = 4 * lane + i;
+    zl[i] = buf[wpos255(l)];
+    zm[i] = buf[wpos255(l == 0 ? 0 : NN - l)];
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int l = 4 * lane + i;
+    if (2 * l + 1 <= NN - 1) {
+      const double f = l == 0 ? 0.25 : 0.5;
+      ta += f * (zl[i].x + zm[i].x);
+      tb += f * (zl[i].y + zm[i].y);
+    }
+  }
+  double ia = ta, ib = tb;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double ya = __shfl_up_sync(0xffffffffu, ia, d), yb = __shfl_up_sync(0xffffffffu, ib, d);
+    if (lane >= d) {
+      ia += ya;
+      ib += yb;
+    }
+  }
+  double pa = ia - ta, pb = ib - tb;
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int l = 4 * lane + i;
+    const double ea = l >= 1 ? hs * (zm[i].y - zl[i].y) : 0.0;
+    const double eb = l >= 1 ? hs * (zl[i].x - zm[i].x) : 0.0;
+    if (2 * l + 1 <= NN - 1) {
+      const double f = l == 0 ? 0.25 : 0.5;
+      pa += f * (zl[i].x + zm[i].x);
+      pb += f * (zl[i].y + zm[i].y);
+    }
+    buf[oslot255(2 * l)] = make_double2(ea, eb);
+    buf[oslot255(2 * l + 1)] = make_double2(pa * sc, pb * sc);
+  }
+  __syncwarp();
+}
+
+// Geometry traits of the warp-owned kernels: DFT length N (line n = N + 1),
+// fill rows J = (N/2 + 1) / 32 and outputs K = n / 32 per lane, warps per CTA,
+// per-warp line stride (+1 slot: conflict-free cross-warp reads) and the x-row
+// stride RLS of rows_t_axpy_w (= 4 mod 16 for sep_row_stencil_T, room for the
+// 16-slot front offset and a q2 <= 15 extension).
+struct W1023 {
+  static constexpr int N = 1023, LINE = 1024, J = 16, K = 32, WARPS = kWWarps;
+  static constexpr int STRIDE = LINE + DBX_WSTRIDE_PAD, RLS = 1076;
+  __device__ static int oslot(int k) { return ::dbx::oslot(k); }
+  __device__ static void dft(double2* buf, const double2* tw, int lane) { WDFT(buf, tw, lane); }
+  __device__ static void split(double2* buf, int lane, double hs, double sc) { wsplit(buf, lane, hs, sc); }
+};
+#ifndef DBX_W255_WARPS
+#define DBX_W255_WARPS 4
+#endif
+struct W255 {
+  static constexpr int N = 255, LINE = 256, J = 4, K = 8, WARPS = DBX_W255_WARPS;
+  static constexpr int STRIDE = LINE + DBX_WSTRIDE_PAD, RLS = 308;
+  __device__ static int oslot(int k) { return oslot255(k); }
+  __device__ static void dft(double2* buf, const double2* tw, int lane) { wdft255(buf, tw, lane); }
+  __device__ static void split(double2* buf, int lane, double hs, double sc) { wsplit255(buf, lane, hs, sc); }
+};
+
+// CTA_STORE (n2 a multiple of 2 W::WARPS): after one CTA barrier the 4 warps'
 // outputs leave as 64-byte row segments (8 columns) instead of each warp's
 // 16-byte pieces at 32 different rows per store instruction.
-template <bool CTA_STORE>
-__global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecArgs a) {
+template <class W, bool CTA_STORE>
+__global__ void __launch_bounds__(32 * W::WARPS, DBX_WDST_MINB) dst_tcols_w(SpecArgs a) {
   DBX_PDL_WAIT();
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 wsm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double2* buf = wsm + (size_t)w * kWStride;
+  double2* buf = wsm + (size_t)w * W::STRIDE;
   const BlueTables& bt = a.blue1;
   const int n = a.n1, n2 = a.n2;
   const size_t N = (size_t)n * n2;
-  const int c = 2 * (kWWarps * blockIdx.x + w);  // columns c, c+1
+  const int c = 2 * (W::WARPS * blockIdx.x + w);  // columns c, c+1
   if (c >= n2) return;                           // warp-uniform; no CTA barriers below
   const bool hb = c + 1 < n2;
   const double ri = bt.rinv, hs = 0.5 * bt.scale, sc = bt.scale;
@@ -440,7 +578,7 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
 #if DBX_WDST_PREFETCH > 0
   if (lane == 0) {
     const long cta = (long)b * gridDim.x + blockIdx.x + (long)DBX_WDST_PREFETCH * 148 * DBX_WDST_MINB;
-    const long pb = cta / gridDim.x, pc = 2 * (kWWarps * (cta - pb * gridDim.x) + w);
+    const long pb = cta / gridDim.x, pc = 2 * (W::WARPS * (cta - pb * gridDim.x) + w);
     if (pb < a.batch && pc + 1 < n2) prefetch_l2(a.in + (size_t)pb * N + (size_t)pc * n, (unsigned)(2 * n * 8));
   }
 #endif
@@ -450,18 +588,18 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
   const double sa = x0a + xea, sb = x0b + xeb, da = x0a - xea, db = x0b - xeb;
   // every global load of the fill in flight at once (one HBM latency per
   // item instead of one per unrolled group)
-  double ap[16], aq[16], bp[16], bq[16];
+  double ap[W::J], aq[W::J], bp[W::J], bq[W::J];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int p = lane + 32 * j, q = kWN - p;  // p in [0, 511], q in [512, 1023]
+  for (int j = 0; j < W::J; ++j) {
+    const int p = lane + 32 * j, q = W::N - p;  // p in [0, 511], q in [512, 1023]
     ap[j] = __ldg(ua + p);
     aq[j] = __ldg(ua + q);
     bp[j] = __ldg(ub + p);
     bq[j] = __ldg(ub + q);
   }
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int p = lane + 32 * j, q = kWN - p;
+  for (int j = 0; j < W::J; ++j) {
+    const int p = lane + 32 * j, q = W::N - p;
     const double r = fma(-2.0 * ri, (double)p, 1.0), s = __ldg(sn + p);
     const double Aa = ap[j] + aq[j] - sa, Ba = (ap[j] - aq[j]) - da * r;  // sd(j) of pk_fill
     const double Ab = bp[j] + bq[j] - sb, Bb = (bp[j] - bq[j]) - db * r;
@@ -473,8 +611,8 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
     }
   }
   __syncwarp();
-  WDFT(buf, bt.tw, lane);
-  wsplit(buf, lane, hs, sc);
+  W::dft(buf, bt.tw, lane);
+  W::split(buf, lane, hs, sc);
   // ---- v = u o d (d^T rows c, c+1: L2-resident, shared by the batch), then
   // the T fill from the same mirror pairs (reads and writes slots p, N - p only)
   const double* dA = a.dT + (size_t)b * a.dstride + (size_t)c * n;
@@ -485,19 +623,19 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
   // (oslot), syncwarp, write z_p, z_q (slot p, q).  Every slot a lane writes
   // in row j aliases only reads of the same row j (oslot permutes within
   // 8-aligned groups keyed by k >> 5), so one __syncwarp per row orders them.
-  double dpa[16], dqa[16], dpb[16], dqb[16];
+  double dpa[W::J], dqa[W::J], dpb[W::J], dqb[W::J];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int p = lane + 32 * j, q = kWN - p;
+  for (int j = 0; j < W::J; ++j) {
+    const int p = lane + 32 * j, q = W::N - p;
     dpa[j] = __ldg(dA + p);
     dqa[j] = __ldg(dA + q);
     dpb[j] = __ldg(dB + p);
     dqb[j] = __ldg(dB + q);
   }
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int p = lane + 32 * j, q = kWN - p;  // p = 0: z_0 = 0 (q = 1023 is no DFT slot)
-    const double2 op = buf[oslot(p)], oq = buf[oslot(q)];
+  for (int j = 0; j < W::J; ++j) {
+    const int p = lane + 32 * j, q = W::N - p;  // p = 0: z_0 = 0 (q = 1023 is no DFT slot)
+    const double2 op = buf[W::oslot(p)], oq = buf[W::oslot(q)];
     const double mpa = op.x * dpa[j], mqa = oq.x * dqa[j];
     const double mpb = op.y * dpb[j], mqb = oq.y * dqb[j];
     const double s = __ldg(sn + p);
@@ -511,23 +649,23 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
     }
   }
   __syncwarp();
-  WDFT(buf, bt.tw, lane);
-  wsplit(buf, lane, hs, sc);
+  W::dft(buf, bt.tw, lane);
+  W::split(buf, lane, hs, sc);
   // ---- T (ar_forward, transforms.hpp:148-160): w_0 = a0, w_{n-1} = a1,
   // interior DST + ramp a0 (1 - k/(n-1)) + a1 k/(n-1); row-major stores
   if constexpr (CTA_STORE) {
-    __shared__ double2 ramp[kWWarps][2];
+    __shared__ double2 ramp[W::WARPS][2];
     if (lane == 0) {
       ramp[w][0] = make_double2(a0a, a0b);
       ramp[w][1] = make_double2(a1a, a1b);
     }
     __syncthreads();
     double* outb = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) +
-                   2 * kWWarps * blockIdx.x;
+                   2 * W::WARPS * blockIdx.x;
 #pragma unroll 4
-    for (int idx = threadIdx.x; idx < kWWarps * n; idx += 32 * kWWarps) {
-      const int ww = idx & (kWWarps - 1), k = idx / kWWarps;
-      const double2 o = wsm[(size_t)ww * kWStride + oslot(k)];
+    for (int idx = threadIdx.x; idx < W::WARPS * n; idx += 32 * W::WARPS) {
+      const int ww = idx & (W::WARPS - 1), k = idx / W::WARPS;
+      const double2 o = wsm[(size_t)ww * W::STRIDE + W::oslot(k)];
       const double2 r0v = ramp[ww][0], r1v = ramp[ww][1];
       const double t1 = (double)k * ri;
       double wa = o.x + r0v.x * (1.0 - t1) + r1v.x * t1;
@@ -540,9 +678,9 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
   }
   double* out = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + c;
 #pragma unroll 8
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < W::K; ++j) {
     const int k = lane + 32 * j;
-    const double2 o = buf[oslot(k)];
+    const double2 o = buf[W::oslot(k)];
     const double t1 = (double)k * ri;
     double wa = o.x + a0a * (1.0 - t1) + a1a * t1;
     double wb = o.y + a0b * (1.0 - t1) + a1b * t1;
@@ -558,25 +696,25 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) dst_tcols_w(SpecA
 // Warp-owned ROW kernels of the separable fused pipeline for n2 = 1024 (the
 // rows of C3): the same DFT_1023 / split as dst_tcols_w, one warp per packed
 // row pair, and ONE CTA barrier before the cooperative transposed stores.
-// CTA = kWWarps warps = 8 rows r0 .. r0+7.
+// CTA = W::WARPS warps = 8 rows r0 .. r0+7.
 //
 // rows_tt_w (K2, replaces rows_ainv_tt<SEP>): s = A'r rows (row-major, ybuf)
 // -> T~ along the rows (ar_inverse, transforms.hpp:163-173) -> u^T[k][row]
 // (64-byte row segments: 8 rows per column k).
-constexpr int kRowLS = 1076;  // rows_t_axpy_w: double stride of the 8 x rows (= 4 mod 16, sep_row_stencil_T)
 
-__global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_tt_w(SpecArgs a) {
+template <class W>
+__global__ void __launch_bounds__(32 * W::WARPS, DBX_WDST_MINB) rows_tt_w(SpecArgs a) {
   DBX_PDL_WAIT();
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 wsm[];
-  __shared__ double ends[2 * kWWarps][2];
+  __shared__ double ends[2 * W::WARPS][2];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double2* buf = wsm + (size_t)w * kWStride;
+  double2* buf = wsm + (size_t)w * W::STRIDE;
   const BlueTables& bt = a.blue2;
   const int n1 = a.n1, n2 = a.n2;
   const size_t N = (size_t)n1 * n2;
-  const int r0 = 2 * kWWarps * blockIdx.x, r = r0 + 2 * w;  // rows r, r+1
+  const int r0 = 2 * W::WARPS * blockIdx.x, r = r0 + 2 * w;  // rows r, r+1
   const bool act = r < n1, hb = r + 1 < n1;
   if (act) {
     const double ri = bt.rinv, hs = 0.5 * bt.scale, sc = bt.scale;
@@ -589,18 +727,18 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_tt_w(SpecArg
       ends[2 * w + 1][0] = x0b; ends[2 * w + 1][1] = xeb;
     }
     const double sa = x0a + xea, sb = x0b + xeb, da = x0a - xea, db = x0b - xeb;
-    double ap[16], aq[16], bp[16], bq[16];
+    double ap[W::J], aq[W::J], bp[W::J], bq[W::J];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int p = lane + 32 * j, q = kWN - p;
+    for (int j = 0; j < W::J; ++j) {
+      const int p = lane + 32 * j, q = W::N - p;
       ap[j] = __ldg(ua + p);
       aq[j] = __ldg(ua + q);
       bp[j] = __ldg(ub + p);
       bq[j] = __ldg(ub + q);
     }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int p = lane + 32 * j, q = kWN - p;
+    for (int j = 0; j < W::J; ++j) {
+      const int p = lane + 32 * j, q = W::N - p;
       const double rr = fma(-2.0 * ri, (double)p, 1.0), s = __ldg(sn + p);
       const double Aa = ap[j] + aq[j] - sa, Ba = (ap[j] - aq[j]) - da * rr;
       const double Ab = bp[j] + bq[j] - sb, Bb = (bp[j] - bq[j]) - db * rr;
@@ -612,19 +750,19 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_tt_w(SpecArg
       }
     }
     __syncwarp();
-    WDFT(buf, bt.tw, lane);
-    wsplit(buf, lane, hs, sc);
+    W::dft(buf, bt.tw, lane);
+    W::split(buf, lane, hs, sc);
   }
   __syncthreads();
   // u^T[k][r0 + 2 ww .. + 1] from warp ww's line: 4 x 16 bytes per column k
   double* uT = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N));
   const double al = bt.alpha;
 #pragma unroll 4
-  for (int idx = threadIdx.x; idx < kWWarps * n2; idx += 32 * kWWarps) {
-    const int ww = idx & (kWWarps - 1), k = idx / kWWarps;
+  for (int idx = threadIdx.x; idx < W::WARPS * n2; idx += 32 * W::WARPS) {
+    const int ww = idx & (W::WARPS - 1), k = idx / W::WARPS;
     const int rr = r0 + 2 * ww;
     if (rr >= n1) continue;
-    double2 o = wsm[(size_t)ww * kWStride + oslot(k)];
+    double2 o = wsm[(size_t)ww * W::STRIDE + W::oslot(k)];
     if (k == 0) o = make_double2(al * ends[2 * ww][0], al * ends[2 * ww + 1][0]);
     if (k == n2 - 1) o = make_double2(al * ends[2 * ww][1], al * ends[2 * ww + 1][1]);
     double* dst = uT + (size_t)k * n1 + rr;
@@ -637,22 +775,23 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_tt_w(SpecArg
 // (ar_forward, transforms.hpp:148-160) -> x_k = x_{k-1} + tau T v
 // (solver.hpp:106) with ||x||^2, ||x - f||^2 partials -> the x_k rows,
 // AR-extended in place (boundary.hpp:56-62), correlated with A's row taps into
-// Z^T (sep_row_stencil_T, 4 rows at a time).  Warp w's region (kRowLS
+// Z^T (sep_row_stencil_T, 4 rows at a time).  Warp w's region (W::RLS
 // double2) holds its DFT line, then its two x rows at double offsets 16 and
-// kRowLS + 16 of the CTA's 8-row stencil block.
-__global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_t_axpy_w(SpecArgs a) {
+// W::RLS + 16 of the CTA's 8-row stencil block.
+template <class W>
+__global__ void __launch_bounds__(32 * W::WARPS, DBX_WDST_MINB) rows_t_axpy_w(SpecArgs a) {
   DBX_PDL_WAIT();
   const int b = blockIdx.y;
   if (a.st && a.st[b].done) return;
   extern __shared__ double2 wsm[];
   __shared__ double red[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double2* buf = wsm + (size_t)w * kRowLS;
-  double* xs = reinterpret_cast<double*>(wsm);  // 8 rows at stride kRowLS, data at offset 16
+  double2* buf = wsm + (size_t)w * W::RLS;
+  double* xs = reinterpret_cast<double*>(wsm);  // 8 rows at stride W::RLS, data at offset 16
   const BlueTables& bt = a.blue2;
   const int n1 = a.n1, n2 = a.n2, q2 = a.q2;
   const size_t N = (size_t)n1 * n2;
-  const int r0 = 2 * kWWarps * blockIdx.x, r = r0 + 2 * w;
+  const int r0 = 2 * W::WARPS * blockIdx.x, r = r0 + 2 * w;
   const bool act = r < n1, hb = r + 1 < n1;
   const double* xo = resolve_ptr(a.xold, a.st, a.xoldsel, b, a.batch, N) + (size_t)r * n2;
   const double* fimg = a.f ? a.f + (size_t)b * N + (size_t)r * n2 : nullptr;
@@ -669,18 +808,18 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_t_axpy_w(Spe
     const double* vb = hb ? va + n2 : va;
     const double a0a = ia * __ldg(va), a1a = ia * __ldg(va + n2 - 1);
     const double a0b = ia * __ldg(vb), a1b = ia * __ldg(vb + n2 - 1);
-    double ap[16], aq[16], bp[16], bq[16];
+    double ap[W::J], aq[W::J], bp[W::J], bq[W::J];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int p = lane + 32 * j, q = kWN - p;
+    for (int j = 0; j < W::J; ++j) {
+      const int p = lane + 32 * j, q = W::N - p;
       ap[j] = __ldg(va + p);
       aq[j] = __ldg(va + q);
       bp[j] = __ldg(vb + p);
       bq[j] = __ldg(vb + q);
     }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int p = lane + 32 * j, q = kWN - p;
+    for (int j = 0; j < W::J; ++j) {
+      const int p = lane + 32 * j, q = W::N - p;
       const double s = __ldg(sn + p);
       const double Aa = ap[j] + aq[j], Ba = ap[j] - aq[j];
       const double Ab = bp[j] + bq[j], Bb = bp[j] - bq[j];
@@ -692,22 +831,22 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_t_axpy_w(Spe
       }
     }
     __syncwarp();
-    WDFT(buf, bt.tw, lane);
-    wsplit(buf, lane, hs, sc);
+    W::dft(buf, bt.tw, lane);
+    W::split(buf, lane, hs, sc);
     // x_k = x_{k-1} + tau w, w = the T output with the ramp; all line reads
     // precede the x row writes into the same region
     double* xn = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N)) + (size_t)r * n2;
-    double2 ov[32];
+    double2 ov[W::K];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) ov[j] = buf[oslot(lane + 32 * j)];
+    for (int j = 0; j < W::K; ++j) ov[j] = buf[W::oslot(lane + 32 * j)];
     __syncwarp();  // the x rows overwrite the line below
-    double* ra = xs + (size_t)(2 * w) * kRowLS + 16;
-    double* rb = ra + kRowLS;
+    double* ra = xs + (size_t)(2 * w) * W::RLS + 16;
+    double* rb = ra + W::RLS;
     // x_{k-1} / f loads eight columns deep per lane (the x_k stores would
     // otherwise keep the compiler from hoisting them: one L2 round trip per
     // group instead of per element)
 #pragma unroll
-    for (int jc = 0; jc < 32; jc += 8) {
+    for (int jc = 0; jc < W::K; jc += 8) {
       double oa[8], ob[8], fa[8], fb[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -763,58 +902,70 @@ __global__ void __launch_bounds__(32 * kWWarps, DBX_WDST_MINB) rows_t_axpy_w(Spe
   }
   __syncthreads();
   double* zT = reinterpret_cast<double*>(a.zbuf) + (size_t)b * N + r0;
-  for (int h0 = 0; h0 < 2 * kWWarps; h0 += 4) {
+  for (int h0 = 0; h0 < 2 * W::WARPS; h0 += 4) {
     const int nl = n1 - r0 - h0 < 4 ? n1 - r0 - h0 : 4;
-    if (nl > 0) sep_row_pass(xs + (size_t)h0 * kRowLS + 16 - q2, kRowLS, a.conv, q2, n2, nl, zT + h0, n1);
+    if (nl > 0) sep_row_pass(xs + (size_t)h0 * W::RLS + 16 - q2, W::RLS, a.conv, q2, n2, nl, zT + h0, n1);
   }
   if (a.part.p) {
     double* P = a.part.p + (size_t)b * NUM_SLOTS * a.part.cap;
-    const double s0 = block_sum<32 * kWWarps>(p0, red);
+    const double s0 = block_sum<32 * W::WARPS>(p0, red);
     if (threadIdx.x == 0) P[SLOT_X2 * a.part.cap + blockIdx.x] = s0;
-    const double s1 = block_sum<32 * kWWarps>(p1, red);
+    const double s1 = block_sum<32 * W::WARPS>(p1, red);
     if (threadIdx.x == 0) P[SLOT_XF2 * a.part.cap + blockIdx.x] = s1;
   }
 }
 
 }  // namespace
 
-// Warp-owned column half of D for n1 = 1024 (direct 1023-point core); returns
-// the CTA count, or -1 when the shape is not this kernel's.
+// Warp-owned column half of D for 1024- and 256-point columns (direct 1023-
+// and 255-point cores); returns the CTA count, or -1 when the shape is not
+// this kernel's.
+template <class W>
+int launch_tcols_w_t(const SpecArgs& a, cudaStream_t s) {
+  const size_t bytes = (size_t)W::WARPS * W::STRIDE * sizeof(double2);
+  dim3 grid((a.n2 + 2 * W::WARPS - 1) / (2 * W::WARPS), a.batch);
+  if (a.n2 % (2 * W::WARPS) == 0 && kWdstCtaStore) {
+    static AttrOnce attr;
+    if (!attr.ensure(dst_tcols_w<W, true>, bytes)) return -1;
+    launch_k(dst_tcols_w<W, true>, grid, 32 * W::WARPS, bytes, s, a);
+  } else {
+    static AttrOnce attr;
+    if (!attr.ensure(dst_tcols_w<W, false>, bytes)) return -1;
+    launch_k(dst_tcols_w<W, false>, grid, 32 * W::WARPS, bytes, s, a);
+  }
+  return (int)grid.x;
+}
+
 int launch_dst_tcols_w(const SpecArgs& a, cudaStream_t s) {
-  if (a.n1 != 1024 || a.blue1.N != kWN) return -1;
-  const size_t bytes = (size_t)kWWarps * kWStride * sizeof(double2);
-  dim3 grid((a.n2 + 2 * kWWarps - 1) / (2 * kWWarps), a.batch);
-  if (a.n2 % (2 * kWWarps) == 0 && kWdstCtaStore) {
-    static AttrOnce attr;
-    if (!attr.ensure(dst_tcols_w<true>, bytes)) return -1;
-    launch_k(dst_tcols_w<true>, grid, 32 * kWWarps, bytes, s, a);
-  } else {
-    static AttrOnce attr;
-    if (!attr.ensure(dst_tcols_w<false>, bytes)) return -1;
-    launch_k(dst_tcols_w<false>, grid, 32 * kWWarps, bytes, s, a);
-  }
-  return (int)grid.x;
+  if (a.n1 == 1024 && a.blue1.N == W1023::N) return launch_tcols_w_t<W1023>(a, s);
+  if (a.n1 == 256 && a.blue1.N == W255::N && kW255) return launch_tcols_w_t<W255>(a, s);
+  return -1;
 }
 
-}  // namespace dbx
-
-namespace dbx {
-// Warp-owned row kernels of the separable pipeline for n2 = 1024 (direct
-// 1023-point core, q2 <= 15); -1 when the shape is not theirs.
-int launch_rows_w(int which, const SpecArgs& a, cudaStream_t s) {
-  if (a.n2 != 1024 || a.blue2.N != kWN || a.q2 > 15 || !conv_sep_supported(a.q2)) return -1;
-  dim3 grid((a.n1 + 2 * kWWarps - 1) / (2 * kWWarps), a.batch);
+template <class W>
+int launch_rows_w_t(int which, const SpecArgs& a, cudaStream_t s) {
+  dim3 grid((a.n1 + 2 * W::WARPS - 1) / (2 * W::WARPS), a.batch);
   if (which == 0) {
-    const size_t bytes = (size_t)kWWarps * kWStride * sizeof(double2);
+    const size_t bytes = (size_t)W::WARPS * W::STRIDE * sizeof(double2);
     static AttrOnce attr;
-    if (!attr.ensure(rows_tt_w, bytes)) return -1;
-    launch_k(rows_tt_w, grid, 32 * kWWarps, bytes, s, a);
+    if (!attr.ensure(rows_tt_w<W>, bytes)) return -1;
+    launch_k(rows_tt_w<W>, grid, 32 * W::WARPS, bytes, s, a);
   } else {
-    const size_t bytes = (size_t)kWWarps * kRowLS * sizeof(double2);
+    const size_t bytes = (size_t)W::WARPS * W::RLS * sizeof(double2);
     static AttrOnce attr;
-    if (!attr.ensure(rows_t_axpy_w, bytes)) return -1;
-    launch_k(rows_t_axpy_w, grid, 32 * kWWarps, bytes, s, a);
+    if (!attr.ensure(rows_t_axpy_w<W>, bytes)) return -1;
+    launch_k(rows_t_axpy_w<W>, grid, 32 * W::WARPS, bytes, s, a);
   }
   return (int)grid.x;
 }
+
+// Warp-owned row kernels of the separable pipeline for 1024- and 256-point
+// rows (q2 <= 15); -1 when the shape is not theirs.
+int launch_rows_w(int which, const SpecArgs& a, cudaStream_t s) {
+  if (a.q2 > 15 || !conv_sep_supported(a.q2)) return -1;
+  if (a.n2 == 1024 && a.blue2.N == W1023::N) return launch_rows_w_t<W1023>(which, a, s);
+  if (a.n2 == 256 && a.blue2.N == W255::N && kW255) return launch_rows_w_t<W255>(which, a, s);
+  return -1;
+}
+
 }  // namespace dbx
