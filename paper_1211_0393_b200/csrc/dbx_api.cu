@@ -384,6 +384,12 @@ struct dbx_plan {
     static const bool on = [] { const char* e = getenv("DBX_DST_TDT"); return !(e && e[0] == '0'); }();
     return on;
   }
+  // DBX_DST_TOUT=1: transposed stores from dst_rows instead of explicit
+  // transposes between the row passes of D (A/B switch)
+  static bool dst_tout() {
+    static const bool on = [] { const char* e = getenv("DBX_DST_TOUT"); return e && e[0] == '1'; }();
+    return on;
+  }
   bool use_fft_dst(bool sine) const {
     if (dst == DBX_DST_DENSE) return false;
     const int N1 = sine ? n1 + 1 : n1 - 1, N2 = sine ? n2 + 1 : n2 - 1;
@@ -751,11 +757,32 @@ struct dbx_plan {
       // T~ along rows
       a.in = X; a.insel = xsel; a.out = u.p; a.outsel = SEL_EXPLICIT; a.kind1 = DBX_KIND_ARINV;
       a.epi = SPEC_STORE;
+      // transposed stores straight into the column pass's input (no transpose launches)
+      // (B1: transposed T~ rows, never the input; B2: the column pass's
+      // transposed output, may reuse the consumed input; neither is Y)
+      const bool tout = dT.p && dst_tdt_fused() && dst_tout() && Y != s.p && Y != u.p;
+      double* B1 = X == s.p ? u.p : s.p;
+      double* B2 = B1 == s.p ? u.p : s.p;
+      if (tout) {
+        a.out = B1;
+        a.tout = 1;
+      }
       ev_begin(KC_TRANSFORM); lc(launch_dst_rows(a, stream), "launch_dst_rows"); ev_end();
+      a.tout = 0;
       // T~ -> d -> T along columns, on the transposed images (columns become
       // contiguous rows: coalesced lines instead of 2-4 column row segments)
       const double* colout = s.p;
-      if (dT.p) {
+      if (tout) {
+        SpecArgs c = a;
+        c.n1 = n2; c.n2 = n1;
+        c.blue2 = blue_tables(0, false);
+        c.in = B1; c.out = B2; c.kind1 = DBX_KIND_ARINV; c.kind2 = DBX_KIND_AR; c.epi = SPEC_STORE; c.d = dT.p;
+        c.st = stp; c.part = Partials{nullptr, 0};
+        c.tout = 1;
+        ev_begin(KC_TRANSFORM); lc(launch_dst_rows(c, stream), "launch_dst_rows"); ev_end();
+        launches += 1;
+        colout = B2;
+      } else if (dT.p) {
         ev_begin(KC_TRANSFORM);
         launch_transpose(u.p, s.p, n1, n2, stream, batch);
         SpecArgs c = a;

@@ -38,6 +38,15 @@ constexpr bool kDstCtBlue = true;
 constexpr bool kDstCtBlue = false;
 #endif
 
+// One-line-per-CTA rows (Rader 8190 for C5, prime-factor 2047 for C4): the
+// two input rows land in the line buffer by two TMA bulk copies, then the
+// fill reads them from shared memory (pkc_fill_staged) instead of exposing
+// the global-load latency of every unrolled group (-DDBX_DST_STAGE=0: A/B).
+#ifndef DBX_DST_STAGE
+#define DBX_DST_STAGE 1
+#endif
+constexpr bool kDstStage = DBX_DST_STAGE != 0;
+
 template <int M, int CORE>
 struct DstCfg {
   // PFA lines: one line per CTA, 256 threads (23 x 11 = 253 butterflies of
@@ -45,7 +54,11 @@ struct DstCfg {
   static constexpr int T = CORE == CORE_PFA ? 256 : line_threads(M, dst_per(M));
   static constexpr int G = CORE == CORE_PFA ? 1 : lines_for(M, kDstBudget, dst_per(M));  // FFT lines per CTA
   static constexpr int NT = T * G;
-  static constexpr int LINE = padded_len(M);                      // double2 per FFT line
+  // double2 per FFT line (PFA: one spare slot, so the two staged raw rows of
+  // n = M + 1 doubles fit the line)
+  static constexpr int LINE = CORE == CORE_PFA ? M + 1 : padded_len(M);
+  // one-line CTAs stage their two input rows with TMA (pkc_fill_staged)
+  static constexpr bool STAGE = G == 1 && (CORE == CORE_RADER || CORE == CORE_PFA) && kDstStage;
   static constexpr int LO = LINE;                                 // output line stride (doubles)
   // the Rader convolution core runs the in-place Cooley-Tukey ct_convolve
   // (C5 8190: transform class 146 -> 131 ms per run); Bluestein keeps the two
@@ -72,7 +85,7 @@ struct DstCfg {
 #define DBX_DST_BOUNDS __launch_bounds__(DstCfg<M, CORE>::NT, DstCfg<M, CORE>::MINB)
 #elif defined(DBX_PFA_MINB)
 // PFA lines (32 KB each) at DBX_PFA_MINB CTAs per SM (A/B of the register cap)
-#define DBX_DST_BOUNDS __launch_bounds__(DstCfg<M, CORE>::NT, CORE == CORE_PFA ? DBX_PFA_MINB : 1)
+#define DBX_DST_BOUNDS __launch_bounds__(DstCfg<M, CORE>::NT, CORE == CORE_PFA ? DBX_PFA_MINB : 0)
 #else
 #define DBX_DST_BOUNDS __launch_bounds__(DstCfg<M, CORE>::NT)
 #endif
@@ -149,6 +162,53 @@ __device__ __forceinline__ void pkc_fill(double2* buf, const BlueTables& bt, int
   }
 }
 
+
+// pkc_fill from the two raw rows staged in the line itself (xs[0, n) = row a,
+// xs[n, 2n) = row b, TMA-landed on mb): the scatter indices and sine weights
+// are fetched while the copies fly, every read of the rows lands in
+// registers, one barrier, then the scatter over the same storage.  The
+// arithmetic is pkc_fill's (sd(h, j) on the same values), so the line is
+// bit-identical.
+template <int M, int T, int CORE, typename F>
+__device__ __forceinline__ void pkc_fill_staged(double2* buf, const BlueTables& bt, int t, unsigned long long* mb,
+                                                F sd) {
+  static_assert(CORE == CORE_RADER || CORE == CORE_PFA, "scatter cores only");
+  const int N = bt.N, H = N / 2;
+  constexpr int PF = ((M + 1) / 2 + T - 1) / T;
+  int pj[PF], pm[PF];
+  double s[PF];
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int j = 1 + t + i * T;
+    if (j <= H) {
+      pj[i] = __ldg(bt.dlog + j);
+      pm[i] = __ldg(bt.dlog + N - j);
+      s[i] = __ldg(bt.sn + j);
+    }
+  }
+  __syncthreads();  // the mbarrier init (thread 0) is visible
+  mbar_wait(mb, 0);
+  double2 zj[PF], zm[PF];
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int j = 1 + t + i * T;
+    if (j <= H) {
+      const double2 A = sd(0, j), B = sd(1, j);
+      zj[i] = make_double2(fma(s[i], A.x, 0.5 * A.y), fma(s[i], B.x, 0.5 * B.y));
+      zm[i] = make_double2(fma(s[i], A.x, -0.5 * A.y), fma(s[i], B.x, -0.5 * B.y));
+    }
+  }
+  __syncthreads();
+  pkc_zero_fill<M, T, CORE>(buf, bt, t);
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int j = 1 + t + i * T;
+    if (j <= H) {
+      buf[pad<M>(pj[i])] = zj[i];
+      if (N - j != j) buf[pad<M>(pm[i])] = zm[i];
+    }
+  }
+}
 
 // Refill the FFT line from values that live in the line itself (the outputs
 // of a previous transform, val(h, k) = value k of new line h): every read
@@ -352,16 +412,40 @@ __global__ void DBX_DST_BOUNDS dst_rows(SpecArgs a) {
   const double* xa = ra < n1 ? in + (size_t)ra * n : nullptr;
   const double* xb = ra + 1 < n1 ? in + (size_t)(ra + 1) * n : nullptr;
   const bool sine = kind == DBX_KIND_SINEI;
-  double a0 = (xa && !sine) ? xa[0] : 0.0, ae = (xa && !sine) ? xa[n - 1] : 0.0;
-  double b0 = (xb && !sine) ? xb[0] : 0.0, be = (xb && !sine) ? xb[n - 1] : 0.0;
   const double ri = bt.rinv;
   const int NL = bt.N;
-  pkc_fill<M, T, CORE>(buf, bt, t, [&](int hh, int j) {
-    const double* x = hh ? xb : xa;
-    if (!x) return make_double2(0.0, 0.0);
-    if (sine) return kind_sd(kind, x[j - 1], x[NL - j - 1], 0.0, 0.0, j, ri);
-    return kind_sd(kind, x[j], x[NL - j], hh ? b0 : a0, hh ? be : ae, j, ri);
-  });
+  double a0, ae, b0, be;
+  // TMA-staged fill (CTA-uniform condition): both rows present, AR kinds,
+  // 16-byte rows that fit the line
+  bool staged = false;
+  if constexpr (C::STAGE) {
+    __shared__ alignas(8) unsigned long long mb_fill;
+    staged = xb && !sine && (n & 1) == 0 && 2 * n <= 2 * C::LINE && ((reinterpret_cast<size_t>(xa) & 15) == 0);
+    if (staged) {
+      double* xs = reinterpret_cast<double*>(buf);
+      if (threadIdx.x == 0) {
+        bulk_init(&mb_fill, 1);
+        mbar_expect(&mb_fill, (unsigned)n * 16u);
+        bulk_copy(xs, xa, (unsigned)n * 8u, &mb_fill);
+        bulk_copy(xs + n, xb, (unsigned)n * 8u, &mb_fill);
+      }
+      a0 = __ldg(xa); ae = __ldg(xa + n - 1); b0 = __ldg(xb); be = __ldg(xb + n - 1);
+      pkc_fill_staged<M, T, CORE>(buf, bt, t, &mb_fill, [&](int hh, int j) {
+        const double* x = xs + hh * n;
+        return kind_sd(kind, x[j], x[NL - j], hh ? b0 : a0, hh ? be : ae, j, ri);
+      });
+    }
+  }
+  if (!staged) {
+    a0 = (xa && !sine) ? xa[0] : 0.0; ae = (xa && !sine) ? xa[n - 1] : 0.0;
+    b0 = (xb && !sine) ? xb[0] : 0.0; be = (xb && !sine) ? xb[n - 1] : 0.0;
+    pkc_fill<M, T, CORE>(buf, bt, t, [&](int hh, int j) {
+      const double* x = hh ? xb : xa;
+      if (!x) return make_double2(0.0, 0.0);
+      if (sine) return kind_sd(kind, x[j - 1], x[NL - j - 1], 0.0, 0.0, j, ri);
+      return kind_sd(kind, x[j], x[NL - j], hh ? b0 : a0, hh ? be : ae, j, ri);
+    });
+  }
   pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g, pfa_sm);
   pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0), pfa_sm);
   pkc_scans<G, C::LINE, C::LO>(sm, bt);
@@ -387,6 +471,25 @@ __global__ void DBX_DST_BOUNDS dst_rows(SpecArgs a) {
     pkc_core<M, T, G, CORE>(sm, buf, bt, tw, t, A0s, g, pfa_sm);
     pkc_split<M, T, CORE, C::PS, C::LO>(buf, bt, t, CORE == CORE_RADER ? A0s[g] : make_double2(0.0, 0.0), pfa_sm);
     pkc_scans<G, C::LINE, C::LO>(sm, bt);
+  }
+  if (a.tout && a.epi == SPEC_STORE) {
+    // transposed store (replaces a transpose launch between the row passes
+    // of D): the line's two rows leave as one 16-byte pair per column; the
+    // CTAs of adjacent row pairs run in the same wave, so L2 completes the
+    // sectors before they are written back
+    double* y = const_cast<double*>(resolve_ptr(a.out, a.st, a.outsel, b, a.batch, N));
+    const double x0a = a0, xea = ae, x0b = b0, xeb = be;
+    if (ra + 1 < n1 && (n1 & 1) == 0) {
+      for (int k = t; k < n; k += T)
+        *reinterpret_cast<double2*>(y + (size_t)k * n1 + ra) =
+            make_double2(kind_out(kind, o, k, n, x0a, xea, al, ri), kind_out(kind, o + C::LO, k, n, x0b, xeb, al, ri));
+    } else if (ra < n1) {
+      for (int k = t; k < n; k += T) {
+        y[(size_t)k * n1 + ra] = kind_out(kind, o, k, n, x0a, xea, al, ri);
+        if (ra + 1 < n1) y[(size_t)k * n1 + ra + 1] = kind_out(kind, o + C::LO, k, n, x0b, xeb, al, ri);
+      }
+    }
+    return;
   }
   Epi e = make_epi(a, b, N);
   if (a.kind2 >= 0) e.d = nullptr;

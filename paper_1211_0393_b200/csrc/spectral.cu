@@ -34,7 +34,7 @@ namespace dbx {
 namespace {
 
 template <int L2>
-__global__ void __launch_bounds__(lines_for(L2, kConvBudget, 8) * line_threads(L2, 8))
+__global__ void __launch_bounds__(lines_for(L2, kConvBudget, 8) * line_threads(L2, 8), conv_row_minb(L2))
 conv_row_fwd(SpecArgs a) {
   DBX_PDL_WAIT();
   constexpr int T = line_threads(L2, 8), G = lines_for(L2, kConvBudget, 8);
@@ -228,7 +228,7 @@ conv_col(SpecArgs a) {
 }
 
 template <int L2>
-__global__ void __launch_bounds__(lines_for(L2, kConvBudget, 8) * line_threads(L2, 8))
+__global__ void __launch_bounds__(lines_for(L2, kConvBudget, 8) * line_threads(L2, 8), conv_row_minb(L2))
 conv_row_inv(SpecArgs a) {
   DBX_PDL_WAIT();
   constexpr int T = line_threads(L2, 8), G = lines_for(L2, kConvBudget, 8);

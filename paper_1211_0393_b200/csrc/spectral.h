@@ -98,6 +98,7 @@ struct SpecArgs {
   // DST
   int kind1 = DBX_KIND_ARINV, kind2 = -1;
   int pf = 0;                                    // dst_rows: prefetch the rows of CTA blockIdx.x + pf into L2 (0: off)
+  int tout = 0;                                  // dst_rows, SPEC_STORE: write the output transposed, out[k * n1 + row]
   // residual kernels of the fused pipelines: when fin_cnt is set, the last
   // CTA of each image runs the iteration's finalize (finalize.cuh) — one
   // launch fewer per iteration

@@ -59,6 +59,14 @@ __host__ __device__ constexpr int lines_for(int L, int budget_bytes, int per) {
 // share per thread (L/8), power-of-two Bluestein lines two radix-8 butterflies.
 __host__ __device__ constexpr int dst_per(int L) { return (L & 1) ? 8 : 16; }
 constexpr int kConvBudget = 100 * 1024;
+// Resident CTAs per SM the FFT-form row kernels (conv_row_fwd / conv_row_inv)
+// are register-capped for at mid lengths (C4's 2160: 92-94 registers = 2 CTAs
+// of 256 threads per SM; at 3: C4 7143 -> 7270 Mpx-it/s, profiles/r03_conv_minb_ab.txt).  0 = no minimum (the one-argument launch bounds: an
+// explicit 1 is not neutral, see dst.cu).  A/B knob.
+#ifndef DBX_CONV_MINB_MID
+#define DBX_CONV_MINB_MID 3
+#endif
+__host__ __device__ constexpr int conv_row_minb(int L) { return (L >= 1500 && L < 4000) ? DBX_CONV_MINB_MID : 0; }
 constexpr int kDstBudget = 160 * 1024;
 
 // Asynchronous global -> shared copies (LDGSTS): operands needed only after a
