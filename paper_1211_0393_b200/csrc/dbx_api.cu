@@ -384,10 +384,11 @@ struct dbx_plan {
     static const bool on = [] { const char* e = getenv("DBX_DST_TDT"); return !(e && e[0] == '0'); }();
     return on;
   }
-  // DBX_DST_TOUT=1: transposed stores from dst_rows instead of explicit
-  // transposes between the row passes of D (A/B switch)
+  // Transposed stores from dst_rows instead of explicit transposes between the
+  // row passes of D (C4 7724 -> 8037, C5 9385 -> 9650 Mpx-it/s,
+  // profiles/r03_dst_tout_ab.txt); DBX_DST_TOUT=0 restores the transposes (A/B)
   static bool dst_tout() {
-    static const bool on = [] { const char* e = getenv("DBX_DST_TOUT"); return e && e[0] == '1'; }();
+    static const bool on = [] { const char* e = getenv("DBX_DST_TOUT"); return !(e && e[0] == '0'); }();
     return on;
   }
   bool use_fft_dst(bool sine) const {

@@ -47,11 +47,20 @@ constexpr bool kDstCtBlue = false;
 #endif
 constexpr bool kDstStage = DBX_DST_STAGE != 0;
 
+// Threads of the one-line CTAs at M >= 8000 (C5's Rader 8190): 640 = 20
+// warps puts the in-place CT levels (630 / 1170 / 546 / 2730 / 4095
+// butterflies of radix 13 / 7 / 15 / 3 / 2) at 1 / 2 / 1 / 5 / 7 per thread
+// instead of 2 / 3 / 2 / 6 / 8 at 512.
+#ifndef DBX_DST_BIG_T
+#define DBX_DST_BIG_T 512
+#endif
+constexpr int kDstBigT = DBX_DST_BIG_T;
+
 template <int M, int CORE>
 struct DstCfg {
   // PFA lines: one line per CTA, 256 threads (23 x 11 = 253 butterflies of
   // the widest column level)
-  static constexpr int T = CORE == CORE_PFA ? 256 : line_threads(M, dst_per(M));
+  static constexpr int T = CORE == CORE_PFA ? 256 : M >= 8000 ? kDstBigT : line_threads(M, dst_per(M));
   static constexpr int G = CORE == CORE_PFA ? 1 : lines_for(M, kDstBudget, dst_per(M));  // FFT lines per CTA
   static constexpr int NT = T * G;
   // double2 per FFT line (PFA: one spare slot, so the two staged raw rows of
