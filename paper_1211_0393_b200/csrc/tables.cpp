@@ -139,6 +139,25 @@ BlueHost bluestein(int n, bool sine_i, int M) {
   if (M == N) {  // direct odd-length DFT: no chirp / kernel spectrum
     b.chirp.assign(2, 0.0);
     b.bhat.assign(2, 0.0);
+    // level-1 twiddles of the warp-owned two-level DFTs, transposed (wdst.cu)
+    const int n1n = N == 1023 ? 33 : N == 255 ? 15 : 0, n2n = N == 1023 ? 31 : 17;
+    if (n1n) {
+      // N = 1023: 15 more rows [j - 1][lane k2] = W_31^{j k2} for the 33rd level-2 row
+      b.tw1t.assign(2 * 32 * (size_t)(n1n + (N == 1023 ? 15 : 0)), 0.0);
+      if (N == 1023)
+        for (int j = 1; j <= 15; ++j)
+          for (int k2 = 0; k2 < 31; ++k2) {
+            const size_t e = 33 * (size_t)((j * k2) % 31), o = (size_t)(33 + j - 1) * 32 + k2;
+            b.tw1t[2 * o] = b.tw[2 * e];
+            b.tw1t[2 * o + 1] = b.tw[2 * e + 1];
+          }
+      for (int k1 = 0; k1 < n1n; ++k1)
+        for (int n2 = 0; n2 < n2n; ++n2) {
+          const size_t e = (size_t)n2 * k1, o = (size_t)k1 * 32 + n2;
+          b.tw1t[2 * o] = b.tw[2 * e];
+          b.tw1t[2 * o + 1] = b.tw[2 * e + 1];
+        }
+    }
   } else {
     blue_chirp(b, N, M);
     ct_permute(b);

@@ -24,6 +24,9 @@ struct BlueHost {
   double alpha = 1.0, scale = 1.0;
   std::vector<double> tw, chirp, bhat, p, sn;  // sn[j] = sin(pi j / N), j < N
   std::vector<double> bct;  // bhat in digit-reversed order (fft.cuh ct_convolve)
+  // warp-owned DFT_1023 / DFT_255 (wdst.cu): level-1 twiddles W_N^{n2 k1} stored
+  // [k1][32 lanes n2], so a warp's load of one k1 is one contiguous 512-byte row
+  std::vector<double> tw1t;
   std::vector<int> dlog, ridx;                 // Rader permutations (prime N)
   int core = 0;                                // DstCore (spectral.h)
 };

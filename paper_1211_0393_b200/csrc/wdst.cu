@@ -72,6 +72,12 @@ constexpr bool kW255 = DBX_W255 != 0;
 #ifndef DBX_WDST_PREFETCH
 #define DBX_WDST_PREFETCH 0
 #endif
+// level-1 twiddles from the transposed table BlueTables::tw1t ([k1][lane]: one
+// contiguous 512-byte row per warp load) instead of the strided gather
+// tw[lane * k1] (up to 31 cache lines per load); -DDBX_TW1T=0 for the A/B
+#ifndef DBX_TW1T
+#define DBX_TW1T 1
+#endif
 
 // Two layouts share a warp's line.  DFT data at slot p (level 1 reads lanes at
 // consecutive p, level 2 lanes at stride 31: both hit 8 distinct 16-byte bank
@@ -117,7 +123,11 @@ __device__ __forceinline__ void level1_row(double2* buf, const double2* __restri
     v[(22 + 3 * b) % 33] = t[2];
   }
   auto put = [&](int k1, double2 x) {
+#if DBX_TW1T
+    if (k1 != 0) x = fft::cmul(x, __ldg(tw + 32 * k1 + lane));  // tw = tw1t: [k1][lane], one 512-byte row per load
+#else
     if (k1 != 0) x = fft::cmul(x, __ldg(tw + lane * k1));  // n2 k1 <= 990
+#endif
     buf[wslot(31 * k1 + lane)] = x;
   };
 #pragma unroll
@@ -207,7 +217,11 @@ __device__ __forceinline__ void wdft1023(double2* buf, const double2* __restrict
       e += lane;
       e = e >= 31 ? e - 31 : e;  // (j * lane) mod 31
       const double2 yj = buf[wslot(992 + j)], ym = buf[wslot(992 + 31 - j)];
+#if DBX_TW1T
+      const double2 w = __ldg(tw + 32 * (33 + j - 1) + lane);  // tw1t rows 33..47: W_31^{j lane}
+#else
       const double2 w = __ldg(tw + 33 * e);  // (cos, -sin)(2 pi e / 31)
+#endif
       const double2 a = cadd(yj, ym), b = csub(yj, ym);
       A.x = fma(w.x, a.x, A.x);
       A.y = fma(w.x, a.y, A.y);
@@ -444,7 +458,11 @@ __device__ __forceinline__ void wdft255(double2* buf, const double2* __restrict_
 #pragma unroll
     for (int k1 = 0; k1 < 15; ++k1) {
       double2 x = v[k1];
+#if DBX_TW1T
+      if (k1 != 0) x = fft::cmul(x, __ldg(tw + 32 * k1 + lane));  // tw1t [k1][lane]
+#else
       if (k1 != 0) x = fft::cmul(x, __ldg(tw + lane * k1));  // n2 k1 <= 224
+#endif
       buf[17 * k1 + lane] = x;
     }
   }
@@ -540,7 +558,9 @@ struct W1023 {
   static constexpr int N = 1023, LINE = 1024, J = 16, K = 32, WARPS = kWWarps;
   static constexpr int STRIDE = LINE + DBX_WSTRIDE_PAD, RLS = 1076;
   __device__ static int oslot(int k) { return ::dbx::oslot(k); }
-  __device__ static void dft(double2* buf, const double2* tw, int lane) { WDFT(buf, tw, lane); }
+  __device__ static void dft(double2* buf, const BlueTables& bt, int lane) {
+    WDFT(buf, (DBX_TW1T && !DBX_WDST_RI) ? bt.tw1t : bt.tw, lane);
+  }
   __device__ static void split(double2* buf, int lane, double hs, double sc) { wsplit(buf, lane, hs, sc); }
 };
 #ifndef DBX_W255_WARPS
@@ -550,7 +570,9 @@ struct W255 {
   static constexpr int N = 255, LINE = 256, J = 4, K = 8, WARPS = DBX_W255_WARPS;
   static constexpr int STRIDE = LINE + DBX_WSTRIDE_PAD, RLS = 308;
   __device__ static int oslot(int k) { return oslot255(k); }
-  __device__ static void dft(double2* buf, const double2* tw, int lane) { wdft255(buf, tw, lane); }
+  __device__ static void dft(double2* buf, const BlueTables& bt, int lane) {
+    wdft255(buf, DBX_TW1T ? bt.tw1t : bt.tw, lane);
+  }
   __device__ static void split(double2* buf, int lane, double hs, double sc) { wsplit255(buf, lane, hs, sc); }
 };
 
@@ -611,7 +633,7 @@ __global__ void __launch_bounds__(32 * W::WARPS, DBX_WDST_MINB) dst_tcols_w(Spec
     }
   }
   __syncwarp();
-  W::dft(buf, bt.tw, lane);
+  W::dft(buf, bt, lane);
   W::split(buf, lane, hs, sc);
   // ---- v = u o d (d^T rows c, c+1: L2-resident, shared by the batch), then
   // the T fill from the same mirror pairs (reads and writes slots p, N - p only)
@@ -649,7 +671,7 @@ __global__ void __launch_bounds__(32 * W::WARPS, DBX_WDST_MINB) dst_tcols_w(Spec
     }
   }
   __syncwarp();
-  W::dft(buf, bt.tw, lane);
+  W::dft(buf, bt, lane);
   W::split(buf, lane, hs, sc);
   // ---- T (ar_forward, transforms.hpp:148-160): w_0 = a0, w_{n-1} = a1,
   // interior DST + ramp a0 (1 - k/(n-1)) + a1 k/(n-1); row-major stores
@@ -750,7 +772,7 @@ __global__ void __launch_bounds__(32 * W::WARPS, DBX_WDST_MINB) rows_tt_w(SpecAr
       }
     }
     __syncwarp();
-    W::dft(buf, bt.tw, lane);
+    W::dft(buf, bt, lane);
     W::split(buf, lane, hs, sc);
   }
   __syncthreads();
@@ -831,7 +853,7 @@ __global__ void __launch_bounds__(32 * W::WARPS, DBX_WDST_MINB) rows_t_axpy_w(Sp
       }
     }
     __syncwarp();
-    W::dft(buf, bt.tw, lane);
+    W::dft(buf, bt, lane);
     W::split(buf, lane, hs, sc);
     // x_k = x_{k-1} + tau w, w = the T output with the ramp; all line reads
     // precede the x row writes into the same region
