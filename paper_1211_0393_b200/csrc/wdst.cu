@@ -41,7 +41,7 @@ constexpr int kWLine = 1024;  // double2 slots per warp line
 // reads of the 4 warps' outputs at the same k (64-byte row segments) hit 4
 // different bank groups instead of one (1024 slots = 16 KB = 0 mod 128 B)
 #ifndef DBX_WSTRIDE_PAD
-#define DBX_WSTRIDE_PAD 1
+#define DBX_WSTRIDE_PAD 2
 #endif
 constexpr int kWStride = kWLine + DBX_WSTRIDE_PAD;
 constexpr int kWWarps = 4;    // warps (column pairs) per CTA
