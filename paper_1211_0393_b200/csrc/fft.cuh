@@ -49,8 +49,17 @@ namespace fft {
 // Even lengths (power-of-two radices) pad one element per 8 so stride-8
 // accesses spread over the banks; odd lengths (odd strides) are conflict-free
 // unpadded, which keeps a butterfly's addresses base + immediate.
+// L = 8190 (C5's Rader convolution, in-place CT core 13.7.15.3.2) stays
+// unpadded: its two long levels walk unit-stride runs whose quarter-warp
+// alignment the padding breaks (2-way conflicts), and the short levels are made
+// conflict-free by the butterfly-to-lane maps in ct_level / ct_convolve instead
+// (-DDBX_CT_NOPAD=0 restores the padded layout for the A/B).
+#ifndef DBX_CT_NOPAD
+#define DBX_CT_NOPAD 1
+#endif
+__host__ __device__ constexpr bool ct_nopad(int L) { return DBX_CT_NOPAD && L == 8190; }
 template <int L>
-__host__ __device__ constexpr int pad(int i) { return (L & 1) ? i : i + (i >> 3); }
+__host__ __device__ constexpr int pad(int i) { return ((L & 1) || ct_nopad(L)) ? i : i + (i >> 3); }
 __host__ __device__ constexpr int padded_len(int L) { return (L & 1) ? L + 1 : L + (L >> 3) + 1; }
 
 // threads per line: one radix-8 butterfly per thread, rounded to a warp
@@ -887,7 +896,21 @@ __device__ __forceinline__ void ct_level(double2* buf, const double2* __restrict
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int beta = b0 + u * T;
-      const int blk = beta / m, j = beta - blk * m;
+      int blk = beta / m, j = beta - blk * m;
+      if constexpr (ct_nopad(L) && m < 8 && m % 2 == 0 && Ls % 8 == 2) {
+        // short blocks, unpadded line: a quarter warp takes 2 j's of 4 blocks
+        // (slots blk Ls + j = 2 blk + j mod 8: eight distinct 16-byte bank
+        // groups) instead of 8 consecutive butterflies (6 of one block + 2 of
+        // the next: two groups hit twice); the blocks past the last multiple
+        // of 4 keep the plain order
+        constexpr int MAIN = (L / Ls) / 4 * 4 * m;
+        if (beta < MAIN) {
+          const int lo = beta & 7, rest = beta >> 3;
+          const int bh = rest / (m / 2), jh = rest - bh * (m / 2);
+          j = 2 * jh + (lo & 1);
+          blk = 4 * bh + (lo >> 1);
+        }
+      }
       base[u] = blk * Ls + j;
       if (U == 1 || beta < NB) {
         w1[u] = tw[j * (L / Ls)];  // smem-staged or global table
@@ -946,6 +969,11 @@ __device__ __forceinline__ void ct_convolve(double2* buf, const double2* __restr
   ct_dif_levels<L, L, T>(buf, tw, t, bar);
   constexpr int R = ct_last_radix<L>(), NB = L / R;
   constexpr int U = ct_unroll<R, NB, T>();
+  // unpadded pairs (slots 2 b, 2 b + 1): lanes 0-3 of each group of 8 touch
+  // their even element first and lanes 4-7 their odd one, so a quarter warp
+  // covers all eight 16-byte bank groups (2 b + r alone reaches only four)
+  constexpr bool SWAP2 = ct_nopad(L) && R == 2 && T % 8 == 0;
+  const int sel = (t >> 2) & 1;
 #pragma unroll 1
   for (int b0 = t; b0 < NB; b0 += U * T) {
     double2 v[U][R];
@@ -953,7 +981,13 @@ __device__ __forceinline__ void ct_convolve(double2* buf, const double2* __restr
     for (int u = 0; u < U; ++u)
       if (U == 1 || b0 + u * T < NB) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[u][r] = buf[pad<L>((b0 + u * T) * R + r)];
+        if constexpr (SWAP2) {
+          const double2 a = buf[(b0 + u * T) * 2 + sel], c = buf[(b0 + u * T) * 2 + (sel ^ 1)];
+          v[u][0] = sel ? c : a;
+          v[u][1] = sel ? a : c;
+        } else {
+          for (int r = 0; r < R; ++r) v[u][r] = buf[pad<L>((b0 + u * T) * R + r)];
+        }
       }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -964,8 +998,13 @@ __device__ __forceinline__ void ct_convolve(double2* buf, const double2* __restr
 #pragma unroll
         for (int r = 0; r < R; ++r) v[u][r] = cmul(v[u][r], kdr[base + r]);  // global or smem-staged
         dft<R, +1>(v[u]);
+        if constexpr (SWAP2) {
+          buf[base + sel] = sel ? v[u][1] : v[u][0];
+          buf[base + (sel ^ 1)] = sel ? v[u][0] : v[u][1];
+        } else {
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[pad<L>(base + r)] = v[u][r];
+          for (int r = 0; r < R; ++r) buf[pad<L>(base + r)] = v[u][r];
+        }
       }
     }
   }
