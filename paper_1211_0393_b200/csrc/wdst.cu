@@ -101,10 +101,20 @@ template <int P>
 __device__ __forceinline__ double scs(int e) {
   return e <= P / 2 ? fft::OddConst<P>::s(e) : -fft::OddConst<P>::s(P - e);
 }
+// Level-2 row k1 lives at row position (k1 + kWRot) mod 33 (level 1 stores it
+// there; position 32 is the cooperative row): with kWRot = 17 the split's
+// loads (lanes 16 pairs apart) cost 156 instead of 280 wavefronts per DFT
+// (128 ideal; rotation 0 puts lanes L and L + 1 in the same 16-byte bank group)
+#ifndef DBX_WROT
+#define DBX_WROT 17
+#endif
+constexpr int kWRot = DBX_WROT;
+static_assert(!DBX_WDST_RI || DBX_WROT == 0, "the component-split DFT keeps the unrotated rows");
+__host__ __device__ constexpr int wrow(int k1) { return (k1 + kWRot) % 33; }
 // slot of DFT output frequency l after level 2 (k1 = l mod 33, k2 = l / 33)
 __device__ __forceinline__ int wpos(int l) {
-  const int k2 = l / 33;
-  return wslot(31 * (l - 33 * k2) + k2);
+  const int k2 = l / 33, k1 = l - 33 * k2;
+  return 31 * k1 + k2 + (k1 < 33 - kWRot ? 31 * kWRot : 31 * (kWRot - 33));
 }
 
 // Level-1 row of lane n2: in-register DFT-33 = 3 x 11 prime factor (input
@@ -128,7 +138,7 @@ __device__ __forceinline__ void level1_row(double2* buf, const double2* __restri
 #else
     if (k1 != 0) x = fft::cmul(x, __ldg(tw + lane * k1));  // n2 k1 <= 990
 #endif
-    buf[wslot(31 * k1 + lane)] = x;
+    buf[31 * wrow(k1) + lane] = x;
   };
 #pragma unroll
   for (int ka = 0; ka < 3; ++ka) {
