@@ -212,6 +212,22 @@ __device__ __forceinline__ void dft9(double2* v) {
   }
 }
 
+// Radix 6 = 2 x 3 prime-factor (no internal twiddles): input n = (3 n1 + 2 n2)
+// mod 6, output k = (3 k1 + 4 k2) mod 6.  The last level of the in-place CT
+// core when the chain ends in 6 (8190 = 13.7.15.6: one level, one barrier and
+// two line passes fewer than 13.7.15.3.2).
+template <int S>
+__device__ __forceinline__ void dft6(double2* v) {
+  double2 a[3] = {v[0], v[2], v[4]}, b[3] = {v[3], v[5], v[1]};
+  dft3<S>(a);
+  dft3<S>(b);
+#pragma unroll
+  for (int k2 = 0; k2 < 3; ++k2) {
+    v[(4 * k2) % 6] = cadd(a[k2], b[k2]);
+    v[(3 + 4 * k2) % 6] = csub(a[k2], b[k2]);
+  }
+}
+
 // Radix 15 = 3 x 5 prime-factor (Good-Thomas, no internal twiddles): input
 // n = (5 n1 + 3 n2) mod 15, output k = (10 k1 + 6 k2) mod 15.
 template <int S>
@@ -310,6 +326,7 @@ __device__ __forceinline__ void dft(double2* v) {
   else if constexpr (R == 4) dft4<S>(v[0], v[1], v[2], v[3]);
   else if constexpr (R == 8) dft8<S>(v);
   else if constexpr (R == 3) dft3<S>(v);
+  else if constexpr (R == 6) dft6<S>(v);
   else if constexpr (R == 5) dft5<S>(v);
   else if constexpr (R == 9) dft9<S>(v);
   else if constexpr (R == 15) dft15<S>(v);
@@ -969,10 +986,10 @@ __device__ __forceinline__ void ct_convolve(double2* buf, const double2* __restr
   ct_dif_levels<L, L, T>(buf, tw, t, bar);
   constexpr int R = ct_last_radix<L>(), NB = L / R;
   constexpr int U = ct_unroll<R, NB, T>();
-  // unpadded pairs (slots 2 b, 2 b + 1): lanes 0-3 of each group of 8 touch
-  // their even element first and lanes 4-7 their odd one, so a quarter warp
-  // covers all eight 16-byte bank groups (2 b + r alone reaches only four)
-  constexpr bool SWAP2 = ct_nopad(L) && R == 2 && T % 8 == 0;
+  // unpadded R-blocks with R = 2 mod 4 (slots R b + r): lanes 0-3 of each
+  // group of 8 touch element r and lanes 4-7 element r ^ 1, so a quarter warp
+  // covers all eight 16-byte bank groups (R b + r alone reaches only four)
+  constexpr bool SWAP2 = ct_nopad(L) && R % 4 == 2 && T % 8 == 0;
   const int sel = (t >> 2) & 1;
 #pragma unroll 1
   for (int b0 = t; b0 < NB; b0 += U * T) {
@@ -982,9 +999,12 @@ __device__ __forceinline__ void ct_convolve(double2* buf, const double2* __restr
       if (U == 1 || b0 + u * T < NB) {
 #pragma unroll
         if constexpr (SWAP2) {
-          const double2 a = buf[(b0 + u * T) * 2 + sel], c = buf[(b0 + u * T) * 2 + (sel ^ 1)];
-          v[u][0] = sel ? c : a;
-          v[u][1] = sel ? a : c;
+#pragma unroll
+          for (int r = 0; r < R; r += 2) {
+            const double2 a = buf[(b0 + u * T) * R + (r ^ sel)], c = buf[(b0 + u * T) * R + (r ^ sel ^ 1)];
+            v[u][r] = sel ? c : a;
+            v[u][r + 1] = sel ? a : c;
+          }
         } else {
           for (int r = 0; r < R; ++r) v[u][r] = buf[pad<L>((b0 + u * T) * R + r)];
         }
@@ -999,8 +1019,11 @@ __device__ __forceinline__ void ct_convolve(double2* buf, const double2* __restr
         for (int r = 0; r < R; ++r) v[u][r] = cmul(v[u][r], kdr[base + r]);  // global or smem-staged
         dft<R, +1>(v[u]);
         if constexpr (SWAP2) {
-          buf[base + sel] = sel ? v[u][1] : v[u][0];
-          buf[base + (sel ^ 1)] = sel ? v[u][0] : v[u][1];
+#pragma unroll
+          for (int r = 0; r < R; r += 2) {
+            buf[base + (r ^ sel)] = sel ? v[u][r + 1] : v[u][r];
+            buf[base + (r ^ sel ^ 1)] = sel ? v[u][r] : v[u][r + 1];
+          }
         } else {
 #pragma unroll
           for (int r = 0; r < R; ++r) buf[pad<L>(base + r)] = v[u][r];

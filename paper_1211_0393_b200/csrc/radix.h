@@ -34,7 +34,11 @@ DBX_HD constexpr int next_radix(int rem) {
 // largest odd prime first, then 15 / 9 / 5 / 3, powers of two last.  The
 // first level's twiddles W_L^{j}, j < L/R_1, dominate the table, so a large
 // R_1 keeps the staged prefix small (8190 = 13.7.15.3.2: 1366 entries).
+#ifndef DBX_CT_RADIX6
+#define DBX_CT_RADIX6 1
+#endif
 DBX_HD constexpr int ct_radix(int rem) {
+  if (DBX_CT_RADIX6 && rem == 6) return 6;  // 2 x 3 prime factor in registers (fft.cuh dft6)
   constexpr int primes[8] = {31, 29, 23, 19, 17, 13, 11, 7};
   for (int i = 0; i < 8; ++i)
     if (rem % primes[i] == 0) return primes[i];

@@ -1,0 +1,19 @@
+#!/bin/bash
+# e2e chunk-split sweep with the warp-owned kernels (128 CTAs per image, 296 resident: wave quantisation per chunk size)
+set -u
+mkdir -p gpurun_out
+run() {
+  v=$(DBX_E2E_SPLIT=$1 DBX_CHUNK_DEPTH=$2 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-other-configs 2>>gpurun_out/r04g.err \
+      | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"],1), round(d["e2e"]["value"],1))')
+  echo "split=$1 depth=$2 value/e2e $v" | tee -a gpurun_out/r04g_sweep.txt
+}
+run 8,24,24,8 2
+run 9,23,23,9 2
+run 16,16,16,16 2
+run 9,23,23,9 3
+run 9,46,9 2
+run 9,14,14,14,13 2
+run 16,32,16 2
+run 8,24,24,8 2
+run 9,23,23,9 2
+run 2,7,23,23,9 2
