@@ -132,6 +132,12 @@ def _ptr(a):
     if a is None:
         return None
     if hasattr(a, "data_ptr"):
+        if a.is_cuda:
+            # libdbx runs on its plans' own non-blocking streams: whatever torch
+            # still has queued for this tensor (fills, copies, clones) on its
+            # current stream must land before a C-ABI kernel touches the memory
+            import torch
+            torch.cuda.current_stream(a.device).synchronize()
         return C.c_void_p(a.data_ptr())
     return a.ctypes.data_as(C.c_void_p)
 

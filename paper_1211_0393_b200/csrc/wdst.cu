@@ -78,6 +78,13 @@ constexpr bool kW255 = DBX_W255 != 0;
 #ifndef DBX_TW1T
 #define DBX_TW1T 1
 #endif
+// packed-DST fills in level-1 geometry, mirrors by shuffle (wfill_pre): the
+// fill's store pass and level 1's load pass of every DFT_1023 are skipped at
+// the price of 132 shuffles per DFT.  Opt-in (-DDBX_WPRE=1): parity green but
+// measured slower (transform class 67.4 vs 64.1 ms/step, profiles/r02_wpre_ab.txt)
+#ifndef DBX_WPRE
+#define DBX_WPRE 0
+#endif
 
 // Two layouts share a warp's line.  DFT data at slot p (level 1 reads lanes at
 // consecutive p, level 2 lanes at stride 31: both hit 8 distinct 16-byte bank
@@ -173,6 +180,7 @@ __device__ __forceinline__ void level1_row(double2* buf, const double2* __restri
   }
 }
 
+__device__ __forceinline__ void wdft1023_tail(double2* buf, const double2* __restrict__ tw, int lane);
 // Forward DFT_1023 of one warp's line (S = -1), in place; tw[e] = W_1023^e.
 __device__ __forceinline__ void wdft1023(double2* buf, const double2* __restrict__ tw, int lane) {
   constexpr int S = -1;
@@ -183,6 +191,12 @@ __device__ __forceinline__ void wdft1023(double2* buf, const double2* __restrict
     level1_row(buf, tw, lane, v);
   }
   __syncwarp();
+  wdft1023_tail(buf, tw, lane);
+}
+
+// levels 2 and the cooperative 33rd row of DFT_1023 (after level 1's stores + __syncwarp)
+__device__ __forceinline__ void wdft1023_tail(double2* buf, const double2* __restrict__ tw, int lane) {
+  constexpr int S = -1;
   {
     // own row k1 = lane: 31 contiguous slots, outputs back in place
     const int base = 31 * lane;
@@ -243,6 +257,48 @@ __device__ __forceinline__ void wdft1023(double2* buf, const double2* __restrict
   __syncwarp();
   if (lane < 31) buf[wslot(992 + lane)] = X;
   __syncwarp();
+}
+
+// DFT_1023 whose level-1 inputs are already in registers (v[n1] = z at slot
+// 31 n1 + lane): skips the fill's store pass and level 1's load pass.
+__device__ __forceinline__ void wdft1023_pre(double2* buf, const double2* __restrict__ tw, int lane, double2* v) {
+  if (lane < 31) level1_row(buf, tw, lane, v);
+  __syncwarp();
+  wdft1023_tail(buf, tw, lane);
+}
+
+// Packed-DST fill in level-1 geometry (DBX_WPRE): lane L holds the raw pair
+// y_m = (line a, line b) at m = 31 n1 + L in v[n1], n1 < 33 (lane 31 shadows
+// lane 0's column one row down, m = 31 (n1 + 1)), so the mirror y_{N-m} of
+// every m sits in lane 31 - L at row 32 - n1: one shuffle per element instead
+// of a line pass through shared memory.  In place:
+//   z_m = s_m (y_m + y_{N-m} - S) + (y_m - y_{N-m} - D (1 - 2 m / N)) / 2
+// (pk_fill's sd(j) for both halves: s and the sum are even in m <-> N - m, the
+// difference and the ramp odd); S = D = 0 without the AR ramp.  z_0 = 0.
+__device__ __forceinline__ double2 wshfl2(double2 x, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, x.x, src), __shfl_sync(0xffffffffu, x.y, src));
+}
+__device__ __forceinline__ double2 wfill_z(double2 y, double2 ym, double s, double r, double2 S, double2 D) {
+  const double Aa = y.x + ym.x - S.x, Ba = (y.x - ym.x) - D.x * r;
+  const double Ab = y.y + ym.y - S.y, Bb = (y.y - ym.y) - D.y * r;
+  return make_double2(fma(s, Aa, 0.5 * Ba), fma(s, Ab, 0.5 * Bb));
+}
+__device__ __forceinline__ void wfill_pre(double2* v, const double* __restrict__ sn, int lane, double2 S, double2 D,
+                                          double ri) {
+  const int src = 31 - lane;
+  const int ml = lane < 31 ? lane : 30;  // lane 31's outputs are unused: keep its table reads in range
+#pragma unroll
+  for (int n1 = 0; n1 <= 16; ++n1) {
+    const int n1m = 32 - n1;
+    const int m0 = 31 * n1 + ml, m1 = 31 * n1m + ml;
+    const double s0 = __ldg(sn + m0), s1 = __ldg(sn + m1);
+    const double2 t0 = wshfl2(v[n1m], src);  // y_{N - m0}
+    const double2 t1 = n1 == n1m ? t0 : wshfl2(v[n1], src);  // y_{N - m1}
+    const double2 z0 = wfill_z(v[n1], t0, s0, fma(-2.0 * ri, (double)m0, 1.0), S, D);
+    const double2 z1 = wfill_z(v[n1m], t1, s1, fma(-2.0 * ri, (double)m1, 1.0), S, D);
+    v[n1] = (n1 == 0 && lane == 0) ? make_double2(0.0, 0.0) : z0;
+    if (n1 != n1m) v[n1m] = z1;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -568,8 +624,12 @@ struct W1023 {
   static constexpr int N = 1023, LINE = 1024, J = 16, K = 32, WARPS = kWWarps;
   static constexpr int STRIDE = LINE + DBX_WSTRIDE_PAD, RLS = 1076;
   __device__ static int oslot(int k) { return ::dbx::oslot(k); }
+  static constexpr bool PRE = DBX_WPRE && DBX_TW1T && !DBX_WDST_RI;
   __device__ static void dft(double2* buf, const BlueTables& bt, int lane) {
     WDFT(buf, (DBX_TW1T && !DBX_WDST_RI) ? bt.tw1t : bt.tw, lane);
+  }
+  __device__ static void dft_pre(double2* buf, const BlueTables& bt, int lane, double2* v) {
+    wdft1023_pre(buf, bt.tw1t, lane, v);
   }
   __device__ static void split(double2* buf, int lane, double hs, double sc) { wsplit(buf, lane, hs, sc); }
 };
@@ -580,9 +640,11 @@ struct W255 {
   static constexpr int N = 255, LINE = 256, J = 4, K = 8, WARPS = DBX_W255_WARPS;
   static constexpr int STRIDE = LINE + DBX_WSTRIDE_PAD, RLS = 308;
   __device__ static int oslot(int k) { return oslot255(k); }
+  static constexpr bool PRE = false;
   __device__ static void dft(double2* buf, const BlueTables& bt, int lane) {
     wdft255(buf, DBX_TW1T ? bt.tw1t : bt.tw, lane);
   }
+  __device__ static void dft_pre(double2*, const BlueTables&, int, double2*) {}
   __device__ static void split(double2* buf, int lane, double hs, double sc) { wsplit255(buf, lane, hs, sc); }
 };
 
@@ -618,32 +680,42 @@ __global__ void __launch_bounds__(32 * W::WARPS, DBX_WDST_MINB) dst_tcols_w(Spec
   const double* ub = hb ? ua + n : ua;
   const double x0a = __ldg(ua), xea = __ldg(ua + n - 1), x0b = __ldg(ub), xeb = __ldg(ub + n - 1);
   const double sa = x0a + xea, sb = x0b + xeb, da = x0a - xea, db = x0b - xeb;
-  // every global load of the fill in flight at once (one HBM latency per
-  // item instead of one per unrolled group)
-  double ap[W::J], aq[W::J], bp[W::J], bq[W::J];
+  if constexpr (W::PRE) {
+    // level-1 geometry: lane's column m = 31 n1 + lane of both lines (wfill_pre)
+    double2 v[33];
 #pragma unroll
-  for (int j = 0; j < W::J; ++j) {
-    const int p = lane + 32 * j, q = W::N - p;  // p in [0, 511], q in [512, 1023]
-    ap[j] = __ldg(ua + p);
-    aq[j] = __ldg(ua + q);
-    bp[j] = __ldg(ub + p);
-    bq[j] = __ldg(ub + q);
-  }
-#pragma unroll
-  for (int j = 0; j < W::J; ++j) {
-    const int p = lane + 32 * j, q = W::N - p;
-    const double r = fma(-2.0 * ri, (double)p, 1.0), s = __ldg(sn + p);
-    const double Aa = ap[j] + aq[j] - sa, Ba = (ap[j] - aq[j]) - da * r;  // sd(j) of pk_fill
-    const double Ab = bp[j] + bq[j] - sb, Bb = (bp[j] - bq[j]) - db * r;
-    if (p == 0) {
-      buf[wslot(0)] = make_double2(0.0, 0.0);
-    } else {
-      buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), hb ? fma(s, Ab, 0.5 * Bb) : 0.0);
-      buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), hb ? fma(s, Ab, -0.5 * Bb) : 0.0);
+    for (int n1 = 0; n1 < 33; ++n1)
+      v[n1] = make_double2(__ldg(ua + 31 * n1 + lane), hb ? __ldg(ub + 31 * n1 + lane) : 0.0);
+    wfill_pre(v, sn, lane, make_double2(sa, hb ? sb : 0.0), make_double2(da, hb ? db : 0.0), ri);
+    W::dft_pre(buf, bt, lane, v);
+  } else {
+    // every global load of the fill in flight at once (one HBM latency per
+    // item instead of one per unrolled group)
+    double ap[W::J], aq[W::J], bp[W::J], bq[W::J];
+  #pragma unroll
+    for (int j = 0; j < W::J; ++j) {
+      const int p = lane + 32 * j, q = W::N - p;  // p in [0, 511], q in [512, 1023]
+      ap[j] = __ldg(ua + p);
+      aq[j] = __ldg(ua + q);
+      bp[j] = __ldg(ub + p);
+      bq[j] = __ldg(ub + q);
     }
-  }
+  #pragma unroll
+    for (int j = 0; j < W::J; ++j) {
+      const int p = lane + 32 * j, q = W::N - p;
+      const double r = fma(-2.0 * ri, (double)p, 1.0), s = __ldg(sn + p);
+      const double Aa = ap[j] + aq[j] - sa, Ba = (ap[j] - aq[j]) - da * r;  // sd(j) of pk_fill
+      const double Ab = bp[j] + bq[j] - sb, Bb = (bp[j] - bq[j]) - db * r;
+      if (p == 0) {
+        buf[wslot(0)] = make_double2(0.0, 0.0);
+      } else {
+        buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), hb ? fma(s, Ab, 0.5 * Bb) : 0.0);
+        buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), hb ? fma(s, Ab, -0.5 * Bb) : 0.0);
+      }
+    }
   __syncwarp();
-  W::dft(buf, bt, lane);
+    W::dft(buf, bt, lane);
+  }
   W::split(buf, lane, hs, sc);
   // ---- v = u o d (d^T rows c, c+1: L2-resident, shared by the batch), then
   // the T fill from the same mirror pairs (reads and writes slots p, N - p only)
@@ -651,37 +723,51 @@ __global__ void __launch_bounds__(32 * W::WARPS, DBX_WDST_MINB) dst_tcols_w(Spec
   const double* dB = hb ? dA + n : dA;
   const double a0a = x0a * __ldg(dA), a1a = xea * __ldg(dA + n - 1);
   const double a0b = x0b * __ldg(dB), a1b = xeb * __ldg(dB + n - 1);
-  // d loads all in flight first; then per mirror row j: read out[p], out[q]
-  // (oslot), syncwarp, write z_p, z_q (slot p, q).  Every slot a lane writes
-  // in row j aliases only reads of the same row j (oslot permutes within
-  // 8-aligned groups keyed by k >> 5), so one __syncwarp per row orders them.
-  double dpa[W::J], dqa[W::J], dpb[W::J], dqb[W::J];
+  if constexpr (W::PRE) {
+    // y = out o d in level-1 geometry (column m = 31 n1 + lane), mirrors by shuffle
+    double2 v[33];
 #pragma unroll
-  for (int j = 0; j < W::J; ++j) {
-    const int p = lane + 32 * j, q = W::N - p;
-    dpa[j] = __ldg(dA + p);
-    dqa[j] = __ldg(dA + q);
-    dpb[j] = __ldg(dB + p);
-    dqb[j] = __ldg(dB + q);
-  }
-#pragma unroll
-  for (int j = 0; j < W::J; ++j) {
-    const int p = lane + 32 * j, q = W::N - p;  // p = 0: z_0 = 0 (q = 1023 is no DFT slot)
-    const double2 op = buf[W::oslot(p)], oq = buf[W::oslot(q)];
-    const double mpa = op.x * dpa[j], mqa = oq.x * dqa[j];
-    const double mpb = op.y * dpb[j], mqb = oq.y * dqb[j];
-    const double s = __ldg(sn + p);
-    const double Aa = mpa + mqa, Ba = mpa - mqa, Ab = mpb + mqb, Bb = mpb - mqb;
-    __syncwarp();
-    if (p == 0) {
-      buf[wslot(0)] = make_double2(0.0, 0.0);
-    } else {
-      buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), fma(s, Ab, 0.5 * Bb));
-      buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), fma(s, Ab, -0.5 * Bb));
+    for (int n1 = 0; n1 < 33; ++n1) {
+      const int m = 31 * n1 + lane;
+      const double2 o = buf[W::oslot(m)];
+      v[n1] = make_double2(o.x * __ldg(dA + m), o.y * __ldg(dB + m));
     }
-  }
+    __syncwarp();  // every read of the split outputs precedes level 1's stores
+    wfill_pre(v, sn, lane, make_double2(0.0, 0.0), make_double2(0.0, 0.0), ri);
+    W::dft_pre(buf, bt, lane, v);
+  } else {
+    // d loads all in flight first; then per mirror row j: read out[p], out[q]
+    // (oslot), syncwarp, write z_p, z_q (slot p, q).  Every slot a lane writes
+    // in row j aliases only reads of the same row j (oslot permutes within
+    // 8-aligned groups keyed by k >> 5), so one __syncwarp per row orders them.
+    double dpa[W::J], dqa[W::J], dpb[W::J], dqb[W::J];
+  #pragma unroll
+    for (int j = 0; j < W::J; ++j) {
+      const int p = lane + 32 * j, q = W::N - p;
+      dpa[j] = __ldg(dA + p);
+      dqa[j] = __ldg(dA + q);
+      dpb[j] = __ldg(dB + p);
+      dqb[j] = __ldg(dB + q);
+    }
+  #pragma unroll
+    for (int j = 0; j < W::J; ++j) {
+      const int p = lane + 32 * j, q = W::N - p;  // p = 0: z_0 = 0 (q = 1023 is no DFT slot)
+      const double2 op = buf[W::oslot(p)], oq = buf[W::oslot(q)];
+      const double mpa = op.x * dpa[j], mqa = oq.x * dqa[j];
+      const double mpb = op.y * dpb[j], mqb = oq.y * dqb[j];
+      const double s = __ldg(sn + p);
+      const double Aa = mpa + mqa, Ba = mpa - mqa, Ab = mpb + mqb, Bb = mpb - mqb;
+      __syncwarp();
+      if (p == 0) {
+        buf[wslot(0)] = make_double2(0.0, 0.0);
+      } else {
+        buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), fma(s, Ab, 0.5 * Bb));
+        buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), fma(s, Ab, -0.5 * Bb));
+      }
+    }
   __syncwarp();
-  W::dft(buf, bt, lane);
+    W::dft(buf, bt, lane);
+  }
   W::split(buf, lane, hs, sc);
   // ---- T (ar_forward, transforms.hpp:148-160): w_0 = a0, w_{n-1} = a1,
   // interior DST + ramp a0 (1 - k/(n-1)) + a1 k/(n-1); row-major stores
@@ -759,30 +845,39 @@ __global__ void __launch_bounds__(32 * W::WARPS, DBX_WDST_MINB) rows_tt_w(SpecAr
       ends[2 * w + 1][0] = x0b; ends[2 * w + 1][1] = xeb;
     }
     const double sa = x0a + xea, sb = x0b + xeb, da = x0a - xea, db = x0b - xeb;
-    double ap[W::J], aq[W::J], bp[W::J], bq[W::J];
+    if constexpr (W::PRE) {
+      double2 v[33];
 #pragma unroll
-    for (int j = 0; j < W::J; ++j) {
-      const int p = lane + 32 * j, q = W::N - p;
-      ap[j] = __ldg(ua + p);
-      aq[j] = __ldg(ua + q);
-      bp[j] = __ldg(ub + p);
-      bq[j] = __ldg(ub + q);
-    }
-#pragma unroll
-    for (int j = 0; j < W::J; ++j) {
-      const int p = lane + 32 * j, q = W::N - p;
-      const double rr = fma(-2.0 * ri, (double)p, 1.0), s = __ldg(sn + p);
-      const double Aa = ap[j] + aq[j] - sa, Ba = (ap[j] - aq[j]) - da * rr;
-      const double Ab = bp[j] + bq[j] - sb, Bb = (bp[j] - bq[j]) - db * rr;
-      if (p == 0) {
-        buf[wslot(0)] = make_double2(0.0, 0.0);
-      } else {
-        buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), hb ? fma(s, Ab, 0.5 * Bb) : 0.0);
-        buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), hb ? fma(s, Ab, -0.5 * Bb) : 0.0);
+      for (int n1 = 0; n1 < 33; ++n1)
+        v[n1] = make_double2(__ldg(ua + 31 * n1 + lane), hb ? __ldg(ub + 31 * n1 + lane) : 0.0);
+      wfill_pre(v, sn, lane, make_double2(sa, hb ? sb : 0.0), make_double2(da, hb ? db : 0.0), ri);
+      W::dft_pre(buf, bt, lane, v);
+    } else {
+      double ap[W::J], aq[W::J], bp[W::J], bq[W::J];
+  #pragma unroll
+      for (int j = 0; j < W::J; ++j) {
+        const int p = lane + 32 * j, q = W::N - p;
+        ap[j] = __ldg(ua + p);
+        aq[j] = __ldg(ua + q);
+        bp[j] = __ldg(ub + p);
+        bq[j] = __ldg(ub + q);
       }
-    }
+  #pragma unroll
+      for (int j = 0; j < W::J; ++j) {
+        const int p = lane + 32 * j, q = W::N - p;
+        const double rr = fma(-2.0 * ri, (double)p, 1.0), s = __ldg(sn + p);
+        const double Aa = ap[j] + aq[j] - sa, Ba = (ap[j] - aq[j]) - da * rr;
+        const double Ab = bp[j] + bq[j] - sb, Bb = (bp[j] - bq[j]) - db * rr;
+        if (p == 0) {
+          buf[wslot(0)] = make_double2(0.0, 0.0);
+        } else {
+          buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), hb ? fma(s, Ab, 0.5 * Bb) : 0.0);
+          buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), hb ? fma(s, Ab, -0.5 * Bb) : 0.0);
+        }
+      }
     __syncwarp();
-    W::dft(buf, bt, lane);
+      W::dft(buf, bt, lane);
+    }
     W::split(buf, lane, hs, sc);
   }
   __syncthreads();
@@ -840,30 +935,39 @@ __global__ void __launch_bounds__(32 * W::WARPS, DBX_WDST_MINB) rows_t_axpy_w(Sp
     const double* vb = hb ? va + n2 : va;
     const double a0a = ia * __ldg(va), a1a = ia * __ldg(va + n2 - 1);
     const double a0b = ia * __ldg(vb), a1b = ia * __ldg(vb + n2 - 1);
-    double ap[W::J], aq[W::J], bp[W::J], bq[W::J];
+    if constexpr (W::PRE) {
+      double2 v[33];
 #pragma unroll
-    for (int j = 0; j < W::J; ++j) {
-      const int p = lane + 32 * j, q = W::N - p;
-      ap[j] = __ldg(va + p);
-      aq[j] = __ldg(va + q);
-      bp[j] = __ldg(vb + p);
-      bq[j] = __ldg(vb + q);
-    }
-#pragma unroll
-    for (int j = 0; j < W::J; ++j) {
-      const int p = lane + 32 * j, q = W::N - p;
-      const double s = __ldg(sn + p);
-      const double Aa = ap[j] + aq[j], Ba = ap[j] - aq[j];
-      const double Ab = bp[j] + bq[j], Bb = bp[j] - bq[j];
-      if (p == 0) {
-        buf[wslot(0)] = make_double2(0.0, 0.0);
-      } else {
-        buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), hb ? fma(s, Ab, 0.5 * Bb) : 0.0);
-        buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), hb ? fma(s, Ab, -0.5 * Bb) : 0.0);
+      for (int n1 = 0; n1 < 33; ++n1)
+        v[n1] = make_double2(__ldg(va + 31 * n1 + lane), hb ? __ldg(vb + 31 * n1 + lane) : 0.0);
+      wfill_pre(v, sn, lane, make_double2(0.0, 0.0), make_double2(0.0, 0.0), ri);
+      W::dft_pre(buf, bt, lane, v);
+    } else {
+      double ap[W::J], aq[W::J], bp[W::J], bq[W::J];
+  #pragma unroll
+      for (int j = 0; j < W::J; ++j) {
+        const int p = lane + 32 * j, q = W::N - p;
+        ap[j] = __ldg(va + p);
+        aq[j] = __ldg(va + q);
+        bp[j] = __ldg(vb + p);
+        bq[j] = __ldg(vb + q);
       }
-    }
+  #pragma unroll
+      for (int j = 0; j < W::J; ++j) {
+        const int p = lane + 32 * j, q = W::N - p;
+        const double s = __ldg(sn + p);
+        const double Aa = ap[j] + aq[j], Ba = ap[j] - aq[j];
+        const double Ab = bp[j] + bq[j], Bb = bp[j] - bq[j];
+        if (p == 0) {
+          buf[wslot(0)] = make_double2(0.0, 0.0);
+        } else {
+          buf[wslot(p)] = make_double2(fma(s, Aa, 0.5 * Ba), hb ? fma(s, Ab, 0.5 * Bb) : 0.0);
+          buf[wslot(q)] = make_double2(fma(s, Aa, -0.5 * Ba), hb ? fma(s, Ab, -0.5 * Bb) : 0.0);
+        }
+      }
     __syncwarp();
-    W::dft(buf, bt, lane);
+      W::dft(buf, bt, lane);
+    }
     W::split(buf, lane, hs, sc);
     // x_k = x_{k-1} + tau w, w = the T output with the ramp; all line reads
     // precede the x row writes into the same region

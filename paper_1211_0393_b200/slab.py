@@ -139,6 +139,9 @@ class _Slab:
         self.recv = torch.zeros(rows * n, dtype=torch.float64, device=self.dev)
         self.tA, self.tB = z(self.cb, n), z(self.cb, n)
         self.dT = z(self.cb, n)  # d^T rows c in [p C, (p+1) C): d[:, c]
+        # the zero fills above are queued on torch's stream; dbx_precond_block
+        # writes dT on the plan's stream, so they must have landed first
+        torch.cuda.current_stream(self.dev).synchronize()
         _check(L.dbx_precond_block(h, n, n, float(alpha), 0, n, p * self.cb, self.cb, 1, _ptr(self.dT)))
 
     def close(self):
