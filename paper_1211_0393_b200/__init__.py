@@ -137,7 +137,9 @@ def _ptr(a):
             # still has queued for this tensor (fills, copies, clones) on its
             # current stream must land before a C-ABI kernel touches the memory
             import torch
-            torch.cuda.current_stream(a.device).synchronize()
+            st = torch.cuda.current_stream(a.device)
+            if not st.query():
+                st.synchronize()
         return C.c_void_p(a.data_ptr())
     return a.ctypes.data_as(C.c_void_p)
 
