@@ -1,14 +1,15 @@
-"""Per-class DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of
-the fused pipeline's kernels from one `ncu --set full` capture of
-`bench.py --images IMAGES` (six consecutive kernels of one iteration in launch order, any
-starting point: conv_col(A'), rows_ainv_tt, dst_tcols, rows_t_axpy_afwd,
-conv_col(A), rows_ainv_resid).  Writes the per-image, per-launch bytes bench.py reports as
-roofline.traffic.  Usage: ncu_traffic.py REPORT IMAGES OUT.json"""
+"""Per-kernel DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum per
+launch) of the separable fused pipeline's six kernels from one `ncu --set full`
+capture of `bench.py` at IMAGES images (six consecutive kernels of one
+iteration in launch order, any starting point).  Writes the JSON bench.py reads
+as roofline.traffic (profiles/r02_ncu_traffic.json: per_launch_bytes keyed by
+the bench's kernel tags).  Usage: ncu_traffic.py REPORT IMAGES OUT.json"""
 import csv
 import io
 import json
 import subprocess
 import sys
+
 
 def main():
     rep, images, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
@@ -22,24 +23,23 @@ def main():
     for r in rows[2:]:
         rd = float(r[hdr.index("dram__bytes_read.sum")]) * scale[units[hdr.index("dram__bytes_read.sum")]]
         wr = float(r[hdr.index("dram__bytes_write.sum")]) * scale[units[hdr.index("dram__bytes_write.sum")]]
-        ks.append({"kernel": r[hdr.index("Kernel Name")][:60], "bytes": rd + wr})
+        ks.append({"kernel": r[hdr.index("Kernel Name")][:70], "bytes": rd + wr})
     assert len(ks) >= 6, "expected the six kernels of one fused iteration"
     ks = ks[:6]
-    # the column pass right after rows_t_axpy is A's (blur class); the other is A'
-    is_col = lambda k: "conv_col" in k["kernel"] or "cols_sep" in k["kernel"]
-    ia = next(i for i, k in enumerate(ks) if "rows_t_axpy" in k["kernel"])
-    conv = [i for i, k in enumerate(ks) if is_col(k)]
-    ca = (ia + 1) % 6 if (ia + 1) % 6 in conv else conv[0]
-    cadj = next(i for i in conv if i != ca)
     find = lambda s: next(i for i, k in enumerate(ks) if s in k["kernel"])
-    resid = next(i for i, k in enumerate(ks) if "resid" in k["kernel"])
-    classes = {"blur_adjoint(A')": [cadj],
-               "ar_transform_pass": [find("rows_ainv_tt"), find("dst_tcols"), ia],
-               "blur(A)+residual": [ca, resid]}
-    per = {c: sum(ks[i]["bytes"] for i in idx) / len(idx) / images for c, idx in classes.items()}
-    json.dump({"report": rep.split("/")[-1], "images": images, "kernels": ks[:6],
-               "per_image_launch_bytes": per}, open(out, "w"), indent=1)
-    print(json.dumps(per, indent=1))
+    ia = find("rows_t_axpy")
+    cols = [i for i, k in enumerate(ks) if "cols_sep" in k["kernel"]]
+    ca = (ia + 1) % 6  # the column pass right after rows_t_axpy is A's; the other is A''s
+    assert ca in cols and len(cols) == 2
+    cadj = next(i for i in cols if i != ca)
+    tags = {"cols_sep_real#0": cadj, "rows_tt_sep#2": find("rows_tt"), "dst_tcols#2": find("dst_tcols"),
+            "rows_t_axpy_sep#2": ia, "cols_sep_real#1": ca, "rows_resid_sep#1": find("resid")}
+    doc = {"report": rep.split("/")[-1] + " (ncu --set full --clock-control none, bench.py C3, one iteration's six kernels)",
+           "images": images, "metric": "dram__bytes_read.sum + dram__bytes_write.sum per launch",
+           "per_launch_bytes": {t: ks[i]["bytes"] for t, i in tags.items()},
+           "ncu_kernel_names": {t: ks[i]["kernel"] for t, i in tags.items()}}
+    json.dump(doc, open(out, "w"), indent=1)
+    print(json.dumps(doc["per_launch_bytes"], indent=1))
 
 
 if __name__ == "__main__":
