@@ -143,14 +143,24 @@ BlueHost bluestein(int n, bool sine_i, int M) {
     const int n1n = N == 1023 ? 33 : N == 255 ? 15 : 0, n2n = N == 1023 ? 31 : 17;
     if (n1n) {
       // N = 1023: 15 more rows [j - 1][lane k2] = W_31^{j k2} for the 33rd level-2 row
-      b.tw1t.assign(2 * 32 * (size_t)(n1n + (N == 1023 ? 15 : 0)), 0.0);
+      // N = 1023 also: rows 33..47 hold real weights (doubles, [j - 1][lane],
+      // at double offset 2 * 32 * 48 + 32 (j - 1) + lane) of the split 33rd row:
+      // lanes k2 <= 15 the cosines cos(2 pi j k2 / 31), lanes 16..30 the sines
+      // sin(2 pi j (31 - lane) / 31) of their partner k2 = 31 - lane, lane 31 zero
+      b.tw1t.assign(2 * 32 * (size_t)(n1n + (N == 1023 ? 15 : 0)) + (N == 1023 ? 15 * 32 : 0), 0.0);
       if (N == 1023)
-        for (int j = 1; j <= 15; ++j)
+        for (int j = 1; j <= 15; ++j) {
           for (int k2 = 0; k2 < 31; ++k2) {
             const size_t e = 33 * (size_t)((j * k2) % 31), o = (size_t)(33 + j - 1) * 32 + k2;
             b.tw1t[2 * o] = b.tw[2 * e];
             b.tw1t[2 * o + 1] = b.tw[2 * e + 1];
           }
+          for (int lane = 0; lane < 31; ++lane) {
+            const int k2 = lane <= 15 ? lane : 31 - lane;
+            const size_t e = 33 * (size_t)((j * k2) % 31);  // tw[e] = (cos, -sin)(2 pi (j k2 mod 31) / 31)
+            b.tw1t[2 * 32 * 48 + (size_t)(j - 1) * 32 + lane] = lane <= 15 ? b.tw[2 * e] : -b.tw[2 * e + 1];
+          }
+        }
       for (int k1 = 0; k1 < n1n; ++k1)
         for (int n2 = 0; n2 < n2n; ++n2) {
           const size_t e = (size_t)n2 * k1, o = (size_t)k1 * 32 + n2;

@@ -85,6 +85,11 @@ constexpr bool kW255 = DBX_W255 != 0;
 #ifndef DBX_WPRE
 #define DBX_WPRE 0
 #endif
+// the cooperative 33rd level-2 row split between the lanes k2 (cosine sums)
+// and 31 - k2 (sine sums): half its FP64 work and twiddle bytes
+#ifndef DBX_WROW33_SPLIT
+#define DBX_WROW33_SPLIT 1
+#endif
 
 // Two layouts share a warp's line.  DFT data at slot p (level 1 reads lanes at
 // consecutive p, level 2 lanes at stride 31: both hit 8 distinct 16-byte bank
@@ -232,6 +237,28 @@ __device__ __forceinline__ void wdft1023_tail(double2* buf, const double2* __res
   // row k1 = 32 (slots 992..1022, untouched by the own rows): lane k2 < 31
   // forms X[32 + 33 k2] = sum_n2 Y[32][n2] W_31^{n2 k2} from the pairs
   double2 X = make_double2(0.0, 0.0);
+#if DBX_WROW33_SPLIT && DBX_TW1T
+  {
+    // X[k2] = A + (-i) B and X[31 - k2] = A - (-i) B share A (cosine sums of the
+    // folded sums) and B (sine sums of the folded differences): lane k2 <= 15
+    // forms A, lane 31 - k2 forms B (real weights, tables.cpp), one exchange
+    const bool isB = lane >= 16;
+    const double sgn = isB ? -1.0 : 1.0;
+    const double* __restrict__ wr = reinterpret_cast<const double*>(tw) + 2 * 32 * 48 + lane;
+    const double2 y0 = buf[wslot(992)];
+    double2 acc = isB ? make_double2(0.0, 0.0) : y0;
+#pragma unroll
+    for (int j = 1; j <= 15; ++j) {
+      const double2 yj = buf[wslot(992 + j)], ym = buf[wslot(992 + 31 - j)];
+      const double w = __ldg(wr + 32 * (j - 1));
+      acc.x = fma(w, fma(sgn, ym.x, yj.x), acc.x);
+      acc.y = fma(w, fma(sgn, ym.y, yj.y), acc.y);
+    }
+    const double2 P = make_double2(__shfl_sync(0xffffffffu, acc.x, 31 - lane), __shfl_sync(0xffffffffu, acc.y, 31 - lane));
+    // A-lane: A + (B.y, -B.x) with B = P;  B-lane: A - (B.y, -B.x) with A = P, B = acc
+    X = isB ? make_double2(P.x - acc.y, P.y + acc.x) : make_double2(acc.x + P.y, acc.y - P.x);
+  }
+#else
   {
     const double2 y0 = buf[wslot(992)];
     double2 A = y0, B = make_double2(0.0, 0.0);
@@ -254,6 +281,7 @@ __device__ __forceinline__ void wdft1023_tail(double2* buf, const double2* __res
     }
     X = cadd(A, fft::mul_si<S>(B));
   }
+#endif
   __syncwarp();
   if (lane < 31) buf[wslot(992 + lane)] = X;
   __syncwarp();
