@@ -501,6 +501,7 @@ struct dbx_plan {
       B.t.chirp = reinterpret_cast<const double2*>(B.chirp);
       B.t.bhat = reinterpret_cast<const double2*>(B.bhat);
       if (!h.bct.empty()) B.t.bct = reinterpret_cast<const double2*>(upload_owned(h.bct));
+      if (!h.bctT.empty()) B.t.bctT = reinterpret_cast<const double2*>(upload_owned(h.bctT));
       if (!h.tw1t.empty()) B.t.tw1t = reinterpret_cast<const double2*>(upload_owned(h.tw1t));
       B.t.p = B.p;
       B.t.alpha = h.alpha;

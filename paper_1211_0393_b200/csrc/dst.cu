@@ -262,7 +262,8 @@ __device__ __forceinline__ void pkc_core(double2* sm, double2* buf, const BlueTa
     fft::fft_cta<M, -1, T, G>(sm, tw, threadIdx.x);
   } else if constexpr (DstCfg<M, CORE>::CT) {
     const int bar = G > 1 ? 1 + g : 0;
-    fft::ct_convolve<M, T>(buf, tw, bt.bct, t, bar, CORE == CORE_RADER ? &A0s[g] : nullptr);
+    fft::ct_convolve<M, T, fft::ct_kt(M)>(buf, tw, fft::ct_kt(M) ? bt.bctT : bt.bct, t, bar,
+                                          CORE == CORE_RADER ? &A0s[g] : nullptr);
   } else {
     const int bar = G > 1 ? 1 + g : 0;
     fft::fft<M, -1, T>(buf, tw, t, bar);

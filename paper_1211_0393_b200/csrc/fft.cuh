@@ -54,10 +54,7 @@ namespace fft {
 // alignment the padding breaks (2-way conflicts), and the short levels are made
 // conflict-free by the butterfly-to-lane maps in ct_level / ct_convolve instead
 // (-DDBX_CT_NOPAD=0 restores the padded layout for the A/B).
-#ifndef DBX_CT_NOPAD
-#define DBX_CT_NOPAD 1
-#endif
-__host__ __device__ constexpr bool ct_nopad(int L) { return DBX_CT_NOPAD && L == 8190; }
+// (ct_nopad lives in radix.h: the host tables need it too)
 template <int L>
 __host__ __device__ constexpr int pad(int i) { return ((L & 1) || ct_nopad(L)) ? i : i + (i >> 3); }
 __host__ __device__ constexpr int padded_len(int L) { return (L & 1) ? L + 1 : L + (L >> 3) + 1; }
@@ -979,7 +976,14 @@ __host__ __device__ constexpr int ct_last_radix() {
 // spectrum in digit-reversed position order (kdr[p] = K_{ct_freq_of_pos(p)}),
 // unnormalised inverse (the host folds 1/L into K).  x0 (may be null)
 // receives DFT(buf)_0 (position 0, before the product).  bar as for fft().
-template <int L, int T>
+// KT: kdr is element-major, kdr[r NB + b] (tables.cpp bctT): consecutive
+// butterflies read consecutive addresses (one 512-byte row per warp load
+// instead of 32 lanes R * 16 bytes apart).
+#ifndef DBX_CT_KT
+#define DBX_CT_KT 1
+#endif
+__host__ __device__ constexpr bool ct_kt(int L) { return DBX_CT_KT && ct_nopad(L); }
+template <int L, int T, bool KT = false>
 __device__ __forceinline__ void ct_convolve(double2* buf, const double2* __restrict__ tw,
                                             const double2* kdr, int t, int bar, double2* x0) {
   static_assert(supported(L), "unsupported FFT length");
@@ -1016,7 +1020,7 @@ __device__ __forceinline__ void ct_convolve(double2* buf, const double2* __restr
         dft<R, -1>(v[u]);
         if (x0 && base == 0) *x0 = v[u][0];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[u][r] = cmul(v[u][r], kdr[base + r]);  // global or smem-staged
+        for (int r = 0; r < R; ++r) v[u][r] = cmul(v[u][r], KT ? kdr[r * NB + (b0 + u * T)] : kdr[base + r]);  // global or smem-staged
         dft<R, +1>(v[u]);
         if constexpr (SWAP2) {
 #pragma unroll

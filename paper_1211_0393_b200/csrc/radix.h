@@ -34,6 +34,12 @@ DBX_HD constexpr int next_radix(int rem) {
 // largest odd prime first, then 15 / 9 / 5 / 3, powers of two last.  The
 // first level's twiddles W_L^{j}, j < L/R_1, dominate the table, so a large
 // R_1 keeps the staged prefix small (8190 = 13.7.15.3.2: 1366 entries).
+// lines the in-place CT core keeps unpadded (fft.cuh pad / ct_level / ct_convolve)
+#ifndef DBX_CT_NOPAD
+#define DBX_CT_NOPAD 1
+#endif
+DBX_HD constexpr bool ct_nopad(int L) { return DBX_CT_NOPAD && L == 8190; }
+
 #ifndef DBX_CT_RADIX6
 #define DBX_CT_RADIX6 1
 #endif

@@ -55,6 +55,7 @@ struct BlueTables {
   const double2* chirp = nullptr;
   const double2* bhat = nullptr;
   const double2* bct = nullptr;  // bhat at the in-place Cooley-Tukey core's digit-reversed positions
+  const double2* bctT = nullptr; // bct element-major [r][block] (unpadded 8190-point CT line: coalesced product pass)
   const double2* tw1t = nullptr; // warp-owned DFT_1023 / DFT_255: level-1 twiddles [k1][32 lanes] (tables.h)
   const double* p = nullptr;
   const double* sn = nullptr;  // sin(pi j / N), j < N (packed real DST)

@@ -125,6 +125,21 @@ void ct_permute(BlueHost& b) {
     b.bct[2 * (size_t)p] = b.bhat[2 * (size_t)k];
     b.bct[2 * (size_t)p + 1] = b.bhat[2 * (size_t)k + 1];
   }
+  // unpadded long lines (fft.cuh ct_nopad): the same spectrum element-major,
+  // bctT[r][b] = bct[b R + r] with R the last level's radix, so the fused
+  // product pass reads consecutive butterflies b from consecutive addresses
+  if (fft::ct_nopad(M)) {
+    int R = M;
+    while (R / fft::ct_radix(R) > 1) R /= fft::ct_radix(R);
+    const int NB = M / R;
+    b.bctT.assign(2 * (size_t)M, 0.0);
+    for (int blk = 0; blk < NB; ++blk)
+      for (int r = 0; r < R; ++r) {
+        const size_t src = (size_t)blk * R + r, dst = (size_t)r * NB + blk;
+        b.bctT[2 * dst] = b.bct[2 * src];
+        b.bctT[2 * dst + 1] = b.bct[2 * src + 1];
+      }
+  }
 }
 
 BlueHost bluestein(int n, bool sine_i, int M) {

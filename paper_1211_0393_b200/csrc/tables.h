@@ -24,6 +24,7 @@ struct BlueHost {
   double alpha = 1.0, scale = 1.0;
   std::vector<double> tw, chirp, bhat, p, sn;  // sn[j] = sin(pi j / N), j < N
   std::vector<double> bct;  // bhat in digit-reversed order (fft.cuh ct_convolve)
+  std::vector<double> bctT; // bct element-major [r][block] for the unpadded long lines (tables.cpp ct_permute)
   // warp-owned DFT_1023 / DFT_255 (wdst.cu): level-1 twiddles W_N^{n2 k1} stored
   // [k1][32 lanes n2], so a warp's load of one k1 is one contiguous 512-byte row
   std::vector<double> tw1t;
